@@ -1,0 +1,391 @@
+"""Benchmark: decoded+augmented images/s at 224 through the GPU loader.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg4] [--batch B]
+
+Workload (BASELINE.json configs[1], "cfg2"): synthetic 256x256 q95 JPEGs,
+crop-decode + RandomResizedCrop(0.08,1)->224 + flip + normalize -> bf16
+NCHW, plus MAE-B/16 masking ratio 0.75 (mask ids, ids_keep, ids_restore),
+batch 256 per GPU.  A step = one batch through Loader.enqueue (the public
+API).  Inputs: an 8192-image pool (~235 MB of compressed bytes, > the 126 MB
+L2) resident in HBM, visited in permutation order, so consecutive steps never
+hit L2-resident inputs.
+
+`value`  : device-timed whole-job images/s (inputs resident in HBM).
+`e2e`    : same metric through Loader.epoch() with host-staged payloads
+           (pinned H2D of each batch's JPEG bytes + D2H of per-image status
+           inside the timed region).
+`roofline`: k_decode (dominant kernel) algorithmic bytes / measured launch
+           time (CUDA events around each launch, ESSL_OPT_PROFILE) vs the
+           measured HBM copy peak.
+`cpu_baseline`: the C oracle (oracle/essl_oracle.c, a port of the reference
+           algorithm) on all host cores over a bounded sample.
+--impl reference: that CPU implementation as the timed arm.
+
+N>1 (torchrun): one process per GPU, each rank decodes its own DDP shard
+(perm[r::world]) -- no collective on the data path; the timing is the max over
+ranks (one all_reduce after the timed region).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decoded+augmented images/s at 224 (1/2/4/8 B200) vs host-CPU ref; HBM roofline %"
+WORKLOADS = {
+    "cfg2": dict(side=256, quality=95, scale=(0.08, 1.0), batch=256, res=224, mask=0.75,
+                 desc="256 synthetic 256px q95 JPEGs per batch, crop-decode + RRC(0.08,1)->224 "
+                      "+ flip + normalize (bf16 NCHW) + MAE-B/16 mask 0.75 "
+                      "(mask/ids_keep/ids_restore)"),
+    "cfg1": dict(side=256, quality=95, scale=(0.08, 1.0), batch=256, res=224, mask=0.0,
+                 desc="256 synthetic 256px q95 JPEGs per batch, crop-decode + RRC(0.08,1)->224 "
+                      "+ flip + normalize (bf16 NCHW)"),
+    "cfg4": dict(side=512, quality=90, scale=(0.2, 1.0), batch=1024, res=224, mask=0.0,
+                 desc="1024 synthetic 512px q90 JPEGs per batch, RRC(0.2,1)->224 + flip + "
+                      "normalize (bf16 NCHW)"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+def make_dataset(wl: dict, pool: int, out_dir: Path, seed: int = 1) -> Path:
+    from paper_2404_00509_b200 import build_synthetic
+    path = out_dir / f"pool_{wl['side']}_{wl['quality']}_{pool}.essl"
+    if not path.exists():
+        t = time.perf_counter()
+        info = build_synthetic(path, pool, wl["side"], wl["quality"], classes=1000, seed=seed)
+        log(f"[bench] built {pool} images ({info['mean_payload']:.0f} B mean) in "
+            f"{time.perf_counter() - t:.1f}s")
+    return path
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in Path(self.path).read_text().splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path:
+                Path(self.path).unlink(missing_ok=True)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_oracle_rate(path: Path, wl: dict, seconds: float, seed_epoch=(0, 0)) -> dict:
+    """Bounded-sample throughput of the C oracle on all host threads."""
+    from oracle import oracle as O
+    from paper_2404_00509_b200.container import open_container
+    O.build()
+    nthreads = os.cpu_count() or 1
+    with open_container(path) as h:
+        perm = np.random.default_rng(0).permutation(len(h))
+        B = wl["batch"]
+        pix = np.empty((B, 3, wl["res"], wl["res"]), np.float32)
+        done, t0, i = 0, time.perf_counter(), 0
+        while True:
+            idx = perm[(i * B) % len(h):(i * B) % len(h) + B]
+            _, _, _, st = O.loader_batch(h.bytes, h.records, idx, seed_epoch[0], seed_epoch[1],
+                                         wl["res"], scale=wl["scale"], mask_ratio=wl["mask"],
+                                         nthreads=nthreads, pixels=pix[:len(idx)])
+            assert (st == 0).all()
+            done += len(idx)
+            i += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                break
+    return {"value": done / el, "unit": "images/s", "cores": nthreads, "kind": "port",
+            "sample": f"{done} images ({i} batches of {B}) of the same workload, "
+                      f"{el:.1f}s wall, C oracle with {nthreads} threads"}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, wl):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    data_dir = Path(tempfile.mkdtemp(prefix="essl_bench_"))
+    path = make_dataset(wl, args.pool, data_dir)
+    from oracle import oracle as O
+    from paper_2404_00509_b200.container import open_container
+    O.build()
+    nthreads = os.cpu_count() or 1
+    with open_container(path) as h:
+        perm = np.random.default_rng(0).permutation(len(h))
+        B = wl["batch"]
+        pix = np.empty((B, 3, wl["res"], wl["res"]), np.float32)
+
+        def step(i):
+            idx = perm[(i * B) % len(h):(i * B) % len(h) + B]
+            _, _, _, st = O.loader_batch(h.bytes, h.records, idx, 0, 0, wl["res"],
+                                         scale=wl["scale"], mask_ratio=wl["mask"],
+                                         nthreads=nthreads, pixels=pix[:len(idx)])
+            assert (st == 0).all()
+            return len(idx)
+
+        for i in range(args.warmup):
+            step(i)
+        t0 = time.perf_counter()
+        n = sum(step(args.warmup + i) for i in range(args.steps))
+        el = time.perf_counter() - t0
+    v = n / el
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": wl["batch"],
+                       "res": wl["res"], "mask_ratio": wl["mask"], "pool_images": args.pool},
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": nthreads, "kind": "port",
+                             "sample": f"{args.steps} timed batches of {wl['batch']} after "
+                                       f"{args.warmup} warm-up, C oracle (port of the reference "
+                                       f"algorithm) on {nthreads} threads"},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, wl):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_00509_b200 as E
+    from paper_2404_00509_b200 import _native as N
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    data_dir = Path(tempfile.mkdtemp(prefix=f"essl_bench_{rank}_"))
+    path = make_dataset(wl, args.pool, data_dir)
+    B, res = wl["batch"], wl["res"]
+    cfg = E.LoaderConfig(data=str(path), batch_size=B, res=res, scale=wl["scale"],
+                         mask_ratio=wl["mask"], out_dtype="bfloat16", device=str(dev),
+                         rank=rank, world_size=ws, resident=True, prefetch=2)
+    loader = E.Loader(cfg)
+    eng = loader.engine
+    handle = loader.handle
+    perm_epochs = {}
+
+    def batch_indices(i):
+        per_epoch = len(handle) // ws // B
+        e, j = divmod(i, max(per_epoch, 1))
+        if e not in perm_epochs:
+            perm_epochs[e] = E.shard(E.epoch_permutation(cfg.seed, e, len(handle)), rank, ws)
+        return e, perm_epochs[e][j * B:(j + 1) * B]
+
+    stream = torch.cuda.current_stream(dev)
+    # ---- warm-up ---------------------------------------------------------
+    for i in range(args.warmup):
+        e, idx = batch_indices(i)
+        loader.finish(loader.enqueue(e, idx))
+    torch.cuda.synchronize(dev)
+    # ---- timed region (device events, max over ranks) ----------------------
+    eng.set_option(N.ESSL_OPT_PROFILE, 1)
+    eng.profile_read()
+    launches0 = eng.launches
+    pend = []
+    with Clocks(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        n_img = 0
+        for i in range(args.steps):
+            e, idx = batch_indices(args.warmup + i)
+            pend.append(loader.enqueue(e, idx))
+            n_img += len(idx)
+            if len(pend) > 3:  # bounded run-ahead; statuses checked as we go
+                loader.finish(pend.pop(0))
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+    for p in pend:
+        loader.finish(p)
+    ms = t0.elapsed_time(t1)
+    launches = eng.launches - launches0
+    prof = eng.profile_read()
+    eng.set_option(N.ESSL_OPT_PROFILE, 0)
+    clocks = clk.summary()
+    # ---- e2e: public API, host-staged payloads ------------------------------
+    e2e_v = None
+    h2d = d2h = 0
+    if not args.no_e2e:
+        cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False})
+        l2 = E.Loader(cfg2, container=handle, engine=eng)
+        steps_e2e = min(args.steps, max(1, len(handle) // ws // B))
+        it = l2.epoch(1)
+        b = next(it)  # warm the staging path
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        n2 = 0
+        it = l2.epoch(2)
+        perm2 = E.shard(E.epoch_permutation(cfg.seed, 2, len(handle)), rank, ws)
+        for k, b in enumerate(it):
+            n2 += len(b)
+            if k + 1 >= steps_e2e:
+                break
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = s0.elapsed_time(s1)
+        lens = handle.records["payload_length"][perm2[:n2]].astype(np.int64)
+        h2d = int(((lens + 63) // 64 * 64).sum()) // max(steps_e2e, 1) + \
+            B * ctypes_sizeof_sample() + 8 * B * 2
+        d2h = B * 32
+        e2e_v = (n2, e2e_ms)
+    # ---- reduce over ranks ---------------------------------------------------
+    vals = torch.tensor([ms, float(n_img), e2e_v[1] if e2e_v else 0.0,
+                         float(e2e_v[0]) if e2e_v else 0.0], dtype=torch.float64, device=dev)
+    if ws > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, total, e2e_ms_max, e2e_total = float(mx[0]), float(sm[1]), float(mx[2]), float(sm[3])
+    else:
+        ms_max, total, e2e_ms_max, e2e_total = float(vals[0]), float(vals[1]), float(vals[2]), float(vals[3])
+    if rank == 0:
+        value = total / (ms_max / 1e3)
+        pk = peaks()
+        per_img = float(np.mean(handle.records["payload_length"])) + 3 * res * res * 2
+        if wl["mask"] > 0:
+            T = (res // 16) ** 2
+            k = int(np.floor(wl["mask"] * T + 0.5))
+            per_img += k * 4 + (T - k) * 8 + T * 8
+        dec_ms, dec_n = prof.get("decode", (0.0, 0))
+        imgs_per_launch = n_img / max(dec_n, 1)
+        achieved = per_img * imgs_per_launch / (dec_ms / max(dec_n, 1) / 1e3) / 1e9 if dec_n else None
+        roof = {"bound": "hbm", "kernel": "k_decode", "achieved": achieved, "peak": pk["hbm_gbs"],
+                "peak_src": pk["src"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"] if achieved else None,
+                "traffic": None, "bytes_per_image": per_img,
+                "kernel_ms": {k: v[0] / max(v[1], 1) for k, v in prof.items()},
+                "kernel_share": {k: v[0] / ms for k, v in prof.items()}}
+        cpu = None
+        if not args.no_cpu:
+            cpu = cpu_oracle_rate(path, wl, args.cpu_seconds)
+        line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "int32", "out_dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": B,
+                           "res": res, "mask_ratio": wl["mask"], "pool_images": args.pool,
+                           "mean_payload_bytes": float(np.mean(handle.records["payload_length"])),
+                           "l2": "inputs > L2: 8192-image pool (~235 MB) visited in permutation "
+                                 "order; outputs are fresh buffers each step",
+                           "parallelism": f"ddp{ws} (rank shards, no collective on path)"},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_total / (e2e_ms_max / 1e3) if e2e_v else None,
+                        "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    loader.close()
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def ctypes_sizeof_sample():
+    import ctypes
+
+    from paper_2404_00509_b200 import _native as N
+    return ctypes.sizeof(N.EsslSample)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--pool", type=int, default=8192)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        from paper_2404_00509_b200 import build as B
+        B.build()
+        run_gpu(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,237 @@
+/*
+ * essl.h -- C ABI of libessl, the B200-native (sm_100a) implementation of
+ * the ESSL / DailyMAE data-loading hot path:
+ *
+ *   read_sample -> sample_rrc -> decode_crop -> resize_bilinear -> hflip
+ *               -> normalize -> sample_mask            (+ ids_keep/restore)
+ *
+ * The reference (cropload, Python+numba) has no native ABI; its operator
+ * boundary is the Python API.  Each entry point below names the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/cropload).
+ * Plain pointers and sizes only; no torch types.  Every device call is
+ * stream-ordered on the caller's cudaStream_t (passed as void*), never
+ * synchronises implicitly, and returns 0 on success or a negative
+ * ESSL_E_* code (message via essl_last_error()).
+ *
+ * Threading: an essl_ctx is single-consumer (reference SPEC.md:555, "a
+ * session is single-consumer"); use one context per rank / consumer thread.
+ */
+#ifndef ESSL_H_
+#define ESSL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ---- API return codes ------------------------------------------------- */
+#define ESSL_OK 0
+#define ESSL_E_ARG -1      /* invalid argument */
+#define ESSL_E_CUDA -2     /* CUDA runtime error */
+#define ESSL_E_CAPACITY -3 /* batch / scratch capacity exceeded */
+#define ESSL_E_NOMEM -4
+
+/* ---- per-image status (int32 status[] arrays) ---------------------------
+ * Mirrors the reference scan status codes (jpeg/decode_kernels.py:14-15)
+ * plus the exception family of jpeg/codec.py and container.py. */
+#define ESSL_ST_OK 0
+#define ESSL_ST_CORRUPT_HUFFMAN 1 /* DecodeError "corrupt entropy-coded data" */
+#define ESSL_ST_MISSING_RST 3     /* DecodeError "missing restart marker" */
+#define ESSL_ST_TRUNCATED 4       /* DecodeError "truncated entropy-coded data" */
+#define ESSL_ST_CRC 5             /* CorruptionError "checksum mismatch" */
+#define ESSL_ST_UNSUPPORTED 6     /* progressive / multi-scan (no CPU fallback) */
+#define ESSL_ST_RECT 7            /* ValueError: crop rect out of bounds */
+#define ESSL_ST_MALFORMED 8       /* DecodeError from parse_stream */
+#define ESSL_ST_HUFFTABLE 9       /* DecodeError from _huff_lut */
+#define ESSL_ST_QUANT 10          /* DecodeError "missing quantization table" */
+#define ESSL_ST_CAPACITY 11       /* image exceeds the context's scratch */
+
+/* ---- output layouts (essl_decode_rrc out_kind) ------------------------- */
+#define ESSL_OUT_BF16_NCHW 0 /* bf16 [n,3,res,res], RNE of the f32 value */
+#define ESSL_OUT_F32_NCHW 1  /* float32 [n,3,res,res] == ImageBatch.pixels */
+#define ESSL_OUT_NONE 2      /* only the optional uint8 view */
+
+/* ---- decoder modes (essl_ctx_set_option ESSL_OPT_DECODE_MODE) ---------- */
+#define ESSL_DECODE_SPECULATIVE 0 /* self-synchronising parallel decode */
+#define ESSL_DECODE_SERIAL 1      /* one thread per image (validation) */
+
+#define ESSL_OPT_DECODE_MODE 1
+#define ESSL_OPT_SEQ_BITS 2     /* subsequence length target (bits) */
+#define ESSL_OPT_OVERLAP_BITS 3 /* speculative warm-up (bits) */
+#define ESSL_OPT_PROFILE 4      /* 1: bracket every launch with CUDA events */
+
+/* kernel ids for essl_ctx_profile_read */
+#define ESSL_K_DECODE 0
+#define ESSL_K_RESIZE 1
+#define ESSL_K_CROP 2
+#define ESSL_K_MASK 3
+#define ESSL_K_GATHER 4
+#define ESSL_K_DUMP 5
+#define ESSL_K_COUNT 6
+
+typedef struct essl_ctx essl_ctx;
+
+/* One sample of a batch.  `offset` indexes the byte blob passed to
+ * essl_decode_rrc (a device-resident container or the staging buffer).
+ * (x, y, w, h) is the RandomResizedCrop window (pipeline.py:51-75,
+ * codec.py:43-56); flip is the apply_aug draw (pipeline.py:86-87). */
+typedef struct {
+  uint64_t offset;
+  uint32_t length;
+  uint32_t crc32; /* expected zlib CRC32 (container.py:46-51 "checksum") */
+  int32_t x, y, w, h;
+  int32_t flip;
+  int32_t check_crc; /* 0 skips the CRC check (decode_crop has none) */
+} essl_sample;
+
+/* Per-image results: stats mirror DecodeStats (codec.py:59-71). */
+typedef struct {
+  int32_t status;
+  int32_t reason; /* sub-code for MALFORMED / UNSUPPORTED / HUFFTABLE */
+  int32_t offset; /* byte offset for DecodeError(offset) or -1 */
+  int32_t mcus_entropy_decoded;
+  int32_t mcus_reconstructed;
+  int32_t width, height, ncomp;
+} essl_result;
+
+/* ---- context ------------------------------------------------------------
+ * Replaces: Loader.__init__ (pipeline.py:181-195) resource setup.  The
+ * context owns device scratch sized for `max_batch` images of at most
+ * `max_side` pixels per side and `max_payload` bytes each, plus pinned
+ * staging for `max_batch * max_payload` bytes (double-buffered). */
+int essl_ctx_create(int device, int max_batch, int max_side, int max_payload,
+                    int flags, essl_ctx **out);
+int essl_ctx_destroy(essl_ctx *ctx);
+int essl_ctx_set_option(essl_ctx *ctx, int option, int64_t value);
+/* Number of kernels this context launched since creation (bench evidence). */
+int64_t essl_ctx_launch_count(const essl_ctx *ctx);
+/* With ESSL_OPT_PROFILE on: synchronise the recorded events, add each
+ * kernel's device time (ms) and launch count into ms[ESSL_K_COUNT] /
+ * count[ESSL_K_COUNT], and clear the record. */
+int essl_ctx_profile_read(essl_ctx *ctx, double *ms, int64_t *count);
+const char *essl_last_error(void);
+const char *essl_version(void);
+
+/* ---- staging (host bytes -> device) -------------------------------------
+ * Replaces: ContainerHandle.read_sample (container.py:249-265) bytes path.
+ * Gathers n payloads (host pointers, e.g. an mmap) into the context's
+ * pinned ring slot `slot` (0/1) with `nthreads` host threads, then issues
+ * one async H2D copy on `stream`.  Writes each sample's offset inside the
+ * staged blob into samples[i].offset and returns the device blob pointer
+ * in *dev_blob.  Payloads are 64-byte aligned in the blob. */
+int essl_stage(essl_ctx *ctx, int slot, const uint8_t *const *src,
+               const uint32_t *len, int n, essl_sample *samples,
+               int nthreads, void *stream, const uint8_t **dev_blob);
+
+/* ---- the hot path --------------------------------------------------------
+ * Replaces: Loader._fill_sample (pipeline.py:219-235) for a whole batch:
+ * CRC check (container.py:263) -> decode_crop (codec.py:448-511) ->
+ * resize_bilinear (imgops.py:63-72) -> hflip (imgops.py:256) ->
+ * normalize (imgops.py:243-248).
+ * `blob` is a DEVICE pointer; samples[] is HOST memory (copied async).
+ * out: [n,3,res,res] in out_kind layout with sample stride out_stride
+ * elements (0 = dense); out_u8: optional uint8 [n,res,res,3] view
+ * (ImageBatch.uint8, pipeline.py:114).  results: optional DEVICE array of
+ * n essl_result. */
+int essl_decode_rrc(essl_ctx *ctx, const uint8_t *blob,
+                    const essl_sample *samples, int n, int res, int out_kind,
+                    void *out, int64_t out_stride, uint8_t *out_u8,
+                    essl_result *results, void *stream);
+
+/* Replaces: decode_crop(bytes, CropRect) (codec.py:448-511) for a batch of
+ * crops: writes each uint8 [h,w,3] region at out + out_offsets[i]
+ * (device pointer + host offsets). */
+int essl_decode_crop_u8(essl_ctx *ctx, const uint8_t *blob,
+                        const essl_sample *samples, int n, uint8_t *out,
+                        const uint64_t *out_offsets, essl_result *results,
+                        void *stream);
+
+/* Debug/parity: the int16 coefficients of every block in the crop window
+ * (natural order, dequantisation not applied), per component c as
+ * [wbh_c][wbw_c][64], components back to back, at out + out_offsets[i]
+ * (element offsets, capacity out_cap elements).  geometry (HOST int32
+ * [12*n]) receives {wby0, wbx0, wbh, wbw} per component.  Synchronises.
+ * (decode_scan_baseline output, decode_kernels.py:111-179, rows <
+ * row_stop; the crop window of codec.py:502-508.) */
+int essl_dump_coefs(essl_ctx *ctx, const uint8_t *blob,
+                    const essl_sample *samples, int n, int16_t *out,
+                    const uint64_t *out_offsets, int64_t out_cap,
+                    int32_t *geometry, essl_result *results, void *stream);
+
+/* ---- MAE masking ----------------------------------------------------------
+ * Replaces: sample_mask (masking.py:48-56) with SampleRng(seed, epoch,
+ * index, DOMAIN_MASK) (pipeline.py:233-235), plus the MAE conventions
+ * ids_keep = sorted(complement(mask)), ids_restore = argsort(concat(
+ * ids_keep, mask)).  index: DEVICE int64[n].  Any of the outputs may be
+ * NULL.  tokens = grid*grid <= 4096. */
+int essl_mask(essl_ctx *ctx, uint64_t seed, uint64_t epoch,
+              const int64_t *index, int n, int tokens, int k,
+              int32_t *mask_sorted, int64_t *ids_keep, int64_t *ids_restore,
+              void *stream);
+
+/* Same, from explicit per-sample stream states (DEVICE uint64[n]): the
+ * state of SampleRng(seed, epoch, index, DOMAIN_MASK) before the shuffle
+ * (rng.py:39-44), for callers holding an arbitrary SampleRng. */
+int essl_mask_from_states(essl_ctx *ctx, const uint64_t *states, int n,
+                          int tokens, int k, int32_t *mask_sorted,
+                          int64_t *ids_keep, int64_t *ids_restore,
+                          void *stream);
+
+/* Visible-token gather of MAE patchify (nchpwq->nhwpqc): pixels bf16
+ * [n,3,res,res] -> tokens bf16 [n, n_keep, patch*patch*3]. */
+int essl_gather_visible(essl_ctx *ctx, const void *pixels_bf16, int n,
+                        int res, int patch, const int64_t *ids_keep,
+                        int n_keep, void *tokens_bf16, void *stream);
+
+/* ---- standalone pixel ops (device pointers) ------------------------------
+ * Replace imgops.resize_bilinear (imgops.py:63-72), hflip (:256) and
+ * normalize (:243-248) on caller-provided uint8 HWC images. */
+int essl_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh,
+                   int ow, int flip, void *stream);
+int essl_normalize_u8(const uint8_t *src, int h, int w, float *dst,
+                      void *stream);
+
+/* ---- host-side sampling (C++, glibc libm: bit-exact with CPython) ---------
+ * Replace rng.py:27-87 and pipeline.py:51-87. */
+uint64_t essl_rng_init(uint64_t seed, uint64_t epoch, uint64_t index,
+                       uint64_t domain);
+uint64_t essl_rng_next(uint64_t *state);
+double essl_rng_random(uint64_t *state);
+int64_t essl_rng_randint(uint64_t *state, int64_t n);
+int essl_epoch_permutation(uint64_t seed, uint64_t epoch, int64_t n,
+                           int64_t *out);
+/* One RRC rect (+ flip draw when flip_out != NULL) for (seed, epoch, index). */
+int essl_sample_rrc(uint64_t *state, int64_t src_w, int64_t src_h,
+                    double scale_lo, double scale_hi, double ratio_lo,
+                    double ratio_hi, int max_attempts, int32_t *xywh);
+/* Batch: rects + flips for dataset indices (record dims w/h indexed by
+ * dataset index), filling samples[i].{x,y,w,h,flip}. */
+int essl_rrc_batch(uint64_t seed, uint64_t epoch, const int64_t *indices,
+                   int n, const uint16_t *widths, const uint16_t *heights,
+                   double scale_lo, double scale_hi, double ratio_lo,
+                   double ratio_hi, essl_sample *samples);
+int essl_mask_count(int tokens, double ratio); /* masking.py:43-45 */
+
+/* ---- dataset builder (row f2; fixtures and benchmark inputs) --------------
+ * encode_jpeg (codec.py:574-632): baseline 4:2:0, Annex-K tables, float64
+ * FDCT with the pinned basis.  Returns the byte count written to out, or a
+ * negative code when out_cap is too small. */
+int64_t essl_encode_jpeg(const uint8_t *rgb, int h, int w, int quality,
+                         int restart_interval, uint8_t *out, int64_t out_cap);
+/* Deterministic synthetic natural-style image (own generator). */
+int essl_synth_image(uint64_t seed, int h, int w, uint8_t *rgb);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESSL_H_ */

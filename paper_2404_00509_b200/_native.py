@@ -1,0 +1,130 @@
+"""ctypes binding of libessl (include/essl.h).
+
+The library is built in-tree by ``paper_2404_00509_b200.build`` (nvcc,
+sm_100a).  There is no CPU fallback: if the library is missing, every GPU
+entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libessl.so"
+
+ESSL_OK = 0
+ESSL_OUT_BF16_NCHW, ESSL_OUT_F32_NCHW, ESSL_OUT_NONE = 0, 1, 2
+ESSL_DECODE_SPECULATIVE, ESSL_DECODE_SERIAL = 0, 1
+ESSL_OPT_DECODE_MODE, ESSL_OPT_SEQ_BITS, ESSL_OPT_OVERLAP_BITS, ESSL_OPT_PROFILE = 1, 2, 3, 4
+KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs")
+
+# Every symbol include/essl.h declares (checked by tests/test_native_abi.py).
+EXPORTS = (
+    "essl_ctx_create", "essl_ctx_destroy", "essl_ctx_set_option", "essl_ctx_launch_count",
+    "essl_ctx_profile_read",
+    "essl_last_error", "essl_version", "essl_stage", "essl_decode_rrc", "essl_decode_crop_u8",
+    "essl_dump_coefs", "essl_mask", "essl_mask_from_states", "essl_gather_visible", "essl_resize_u8",
+    "essl_normalize_u8", "essl_rng_init", "essl_rng_next", "essl_rng_random",
+    "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
+    "essl_mask_count", "essl_encode_jpeg", "essl_synth_image",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class EsslSample(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_uint64), ("length", ctypes.c_uint32),
+                ("crc32", ctypes.c_uint32), ("x", ctypes.c_int32), ("y", ctypes.c_int32),
+                ("w", ctypes.c_int32), ("h", ctypes.c_int32), ("flip", ctypes.c_int32),
+                ("check_crc", ctypes.c_int32)]
+
+
+class EsslResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("reason", ctypes.c_int32),
+                ("offset", ctypes.c_int32), ("mcus_entropy_decoded", ctypes.c_int32),
+                ("mcus_reconstructed", ctypes.c_int32), ("width", ctypes.c_int32),
+                ("height", ctypes.c_int32), ("ncomp", ctypes.c_int32)]
+
+
+SAMPLE_NP_DTYPE = None  # filled lazily (numpy view of EsslSample arrays)
+RESULT_NP_DTYPE = None
+
+_lib = None
+
+
+def _np_dtypes():
+    global SAMPLE_NP_DTYPE, RESULT_NP_DTYPE
+    import numpy as np
+    if SAMPLE_NP_DTYPE is None:
+        SAMPLE_NP_DTYPE = np.dtype([("offset", "<u8"), ("length", "<u4"), ("crc32", "<u4"),
+                                    ("x", "<i4"), ("y", "<i4"), ("w", "<i4"), ("h", "<i4"),
+                                    ("flip", "<i4"), ("check_crc", "<i4")])
+        assert SAMPLE_NP_DTYPE.itemsize == ctypes.sizeof(EsslSample)
+        RESULT_NP_DTYPE = np.dtype([(n, "<i4") for n, _ in EsslResult._fields_])
+        assert RESULT_NP_DTYPE.itemsize == ctypes.sizeof(EsslResult)
+    return SAMPLE_NP_DTYPE, RESULT_NP_DTYPE
+
+
+def lib():
+    """Load libessl.so (raises NativeUnavailable if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise NativeUnavailable(
+            f"{LIB_PATH} not built; run `python -m paper_2404_00509_b200.build` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    P = ctypes.c_void_p
+    i32, i64, u64, dbl = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
+    sig = {
+        "essl_ctx_create": (i32, [i32, i32, i32, i32, i32, P]),
+        "essl_ctx_destroy": (i32, [P]),
+        "essl_ctx_set_option": (i32, [P, i32, i64]),
+        "essl_ctx_launch_count": (i64, [P]),
+        "essl_ctx_profile_read": (i32, [P, P, P]),
+        "essl_last_error": (ctypes.c_char_p, []),
+        "essl_version": (ctypes.c_char_p, []),
+        "essl_stage": (i32, [P, i32, P, P, i32, P, i32, P, P]),
+        "essl_decode_rrc": (i32, [P, P, P, i32, i32, i32, P, i64, P, P, P]),
+        "essl_decode_crop_u8": (i32, [P, P, P, i32, P, P, P, P]),
+        "essl_dump_coefs": (i32, [P, P, P, i32, P, P, i64, P, P, P]),
+        "essl_mask": (i32, [P, u64, u64, P, i32, i32, i32, P, P, P, P]),
+        "essl_mask_from_states": (i32, [P, P, i32, i32, i32, P, P, P, P]),
+        "essl_gather_visible": (i32, [P, P, i32, i32, i32, P, i32, P, P]),
+        "essl_resize_u8": (i32, [P, i32, i32, P, i32, i32, i32, P]),
+        "essl_normalize_u8": (i32, [P, i32, i32, P, P]),
+        "essl_rng_init": (u64, [u64, u64, u64, u64]),
+        "essl_rng_next": (u64, [P]),
+        "essl_rng_random": (dbl, [P]),
+        "essl_rng_randint": (i64, [P, i64]),
+        "essl_epoch_permutation": (i32, [u64, u64, i64, P]),
+        "essl_sample_rrc": (i32, [P, i64, i64, dbl, dbl, dbl, dbl, i32, P]),
+        "essl_rrc_batch": (i32, [u64, u64, P, i32, P, P, dbl, dbl, dbl, dbl, P]),
+        "essl_mask_count": (i32, [i32, dbl]),
+        "essl_encode_jpeg": (i64, [P, i32, i32, i32, i32, P, i64]),
+        "essl_synth_image": (i32, [u64, i32, i32, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "libessl") -> None:
+    if rc != ESSL_OK:
+        msg = lib().essl_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+def ptr(a) -> ctypes.c_void_p | None:
+    """Raw pointer of a numpy array or torch tensor (None passes NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ctypes.c_void_p)

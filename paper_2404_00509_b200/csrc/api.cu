@@ -1,0 +1,444 @@
+// C ABI of libessl (include/essl.h): context, staging, launch plumbing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "essl.h"
+#include "essl_common.cuh"
+
+namespace essl {
+void init_crc_tables();
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ESSL_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kDescRing = 8;
+
+}  // namespace
+
+struct essl_ctx {
+  int device = 0;
+  int max_batch = 0, max_side = 0, max_payload = 0;
+  essl::Scratch s{};
+  // descriptor ring (pinned host -> device)
+  essl_sample *h_desc[kDescRing] = {};
+  essl_sample *d_desc[kDescRing] = {};
+  cudaEvent_t ev_desc[kDescRing] = {};
+  bool desc_used[kDescRing] = {};
+  int desc_next = 0;
+  // staging (pinned ring, two slots)
+  uint8_t *h_stage[2] = {};
+  uint8_t *d_stage[2] = {};
+  uint64_t stage_cap = 0;
+  cudaEvent_t ev_stage[2] = {};
+  bool stage_used[2] = {};
+  // misc device buffers
+  uint64_t *d_offsets = nullptr;  // crop / dump output offsets
+  int mode = ESSL_DECODE_SPECULATIVE;
+  int seq_bits = 1024;
+  int overlap_bits = 1024;
+  std::atomic<int64_t> launches{0};
+  // profiling: event pairs per launch
+  bool profile = false;
+  struct Rec { int kid; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+// Bracket a launch with events when profiling (ESSL_OPT_PROFILE).
+struct Prof {
+  essl_ctx *c; int kid; cudaStream_t st; cudaEvent_t a = nullptr;
+  Prof(essl_ctx *c_, int k, cudaStream_t s) : c(c_), kid(k), st(s) {
+    if (c && c->profile) { a = c->take(); cudaEventRecord(a, st); }
+  }
+  ~Prof() {
+    if (c) c->launches += 1;
+    if (c && c->profile) {
+      cudaEvent_t b = c->take();
+      cudaEventRecord(b, st);
+      c->recs.push_back({kid, a, b});
+    }
+  }
+};
+}  // namespace
+
+namespace {
+
+int pick_desc(essl_ctx *c, const essl_sample *samples, int n, cudaStream_t st,
+              essl_sample **d_out) {
+  const int r = c->desc_next;
+  c->desc_next = (c->desc_next + 1) % kDescRing;
+  if (c->desc_used[r]) CK(cudaEventSynchronize(c->ev_desc[r]));
+  std::memcpy(c->h_desc[r], samples, sizeof(essl_sample) * n);
+  CK(cudaMemcpyAsync(c->d_desc[r], c->h_desc[r], sizeof(essl_sample) * n,
+                     cudaMemcpyHostToDevice, st));
+  *d_out = c->d_desc[r];
+  c->desc_used[r] = true;
+  return r;
+}
+
+int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
+               essl_result *results, cudaStream_t st, int *ring) {
+  if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
+  for (int i = 0; i < n; i++)
+    if ((int)samples[i].length > c->max_payload)
+      return fail(ESSL_E_CAPACITY, "payload larger than context max_payload");
+  essl_sample *d_desc = nullptr;
+  int r = pick_desc(c, samples, n, st, &d_desc);
+  if (r < 0) return r;
+  *ring = r;
+  CK(cudaMemsetAsync(c->s.counters, 0, 4 * sizeof(unsigned long long), st));
+  essl::DecodeParams p;
+  p.blob = blob;
+  p.samples = d_desc;
+  p.n = n;
+  p.s = c->s;
+  p.mode = c->mode;
+  p.seq_bits = c->seq_bits;
+  p.overlap_bits = c->overlap_bits;
+  p.results = results;
+  {
+    Prof pr(c, ESSL_K_DECODE, st);
+    essl::launch_decode(p, st);
+  }
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *essl_last_error(void) { return g_err.c_str(); }
+const char *essl_version(void) { return "essl-b200 0.1 (sm_100a)"; }
+
+int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, int flags,
+                    essl_ctx **out) {
+  (void)flags;
+  if (!out || max_batch < 1 || max_side < 1 || max_payload < 4)
+    return fail(ESSL_E_ARG, "essl_ctx_create: bad arguments");
+  CK(cudaSetDevice(device));
+  essl_ctx *c = new essl_ctx();
+  c->device = device;
+  c->max_batch = max_batch;
+  c->max_side = max_side;
+  c->max_payload = max_payload;
+  // worst-case per-image scratch (4:4:4 / h,v<=4 padding included)
+  const uint64_t side_blocks = (uint64_t)(max_side + 7) / 8 + 4;
+  const uint64_t blocks = 3 * side_blocks * side_blocks;
+  const uint64_t mcus = ((uint64_t)max_side + 7) / 8 * (((uint64_t)max_side + 7) / 8);
+  c->s.clean_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 64 + 4 * (mcus + 2) + 64 + 15) / 16 * 16);
+  c->s.coef_cap = (uint64_t)max_batch * blocks * 64;
+  c->s.plane_cap = (uint64_t)max_batch * blocks * 64 + 16 * (uint64_t)max_batch;
+  auto cleanup = [&](int code) {
+    essl_ctx_destroy(c);
+    return code;
+  };
+#define CKC(call)                                                                   \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return cleanup(fail(ESSL_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_))); \
+  } while (0)
+  CKC(cudaMalloc(&c->s.clean, c->s.clean_cap));
+  CKC(cudaMalloc(&c->s.coef, c->s.coef_cap * sizeof(int16_t)));
+  CKC(cudaMalloc(&c->s.plane, c->s.plane_cap));
+  CKC(cudaMalloc(&c->s.counters, 4 * sizeof(unsigned long long)));
+  CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
+  CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
+  for (int r = 0; r < kDescRing; r++) {
+    CKC(cudaMallocHost(&c->h_desc[r], sizeof(essl_sample) * max_batch));
+    CKC(cudaMalloc(&c->d_desc[r], sizeof(essl_sample) * max_batch));
+    CKC(cudaEventCreateWithFlags(&c->ev_desc[r], cudaEventDisableTiming));
+  }
+  c->stage_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 63) / 64 * 64);
+  for (int r = 0; r < 2; r++) {
+    CKC(cudaMallocHost(&c->h_stage[r], c->stage_cap));
+    CKC(cudaMalloc(&c->d_stage[r], c->stage_cap));
+    CKC(cudaEventCreateWithFlags(&c->ev_stage[r], cudaEventDisableTiming));
+  }
+#undef CKC
+  static std::once_flag once;
+  std::call_once(once, [] { essl::init_crc_tables(); });
+  *out = c;
+  return ESSL_OK;
+}
+
+int essl_ctx_destroy(essl_ctx *c) {
+  if (!c) return ESSL_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  cudaFree(c->s.clean);
+  cudaFree(c->s.coef);
+  cudaFree(c->s.plane);
+  cudaFree(c->s.counters);
+  cudaFree(c->s.info);
+  cudaFree(c->d_offsets);
+  for (int r = 0; r < kDescRing; r++) {
+    if (c->h_desc[r]) cudaFreeHost(c->h_desc[r]);
+    if (c->d_desc[r]) cudaFree(c->d_desc[r]);
+    if (c->ev_desc[r]) cudaEventDestroy(c->ev_desc[r]);
+  }
+  for (int r = 0; r < 2; r++) {
+    if (c->h_stage[r]) cudaFreeHost(c->h_stage[r]);
+    if (c->d_stage[r]) cudaFree(c->d_stage[r]);
+    if (c->ev_stage[r]) cudaEventDestroy(c->ev_stage[r]);
+  }
+  for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  delete c;
+  return ESSL_OK;
+}
+
+int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
+  if (!c) return fail(ESSL_E_ARG, "null context");
+  switch (option) {
+    case ESSL_OPT_DECODE_MODE:
+      if (value != ESSL_DECODE_SPECULATIVE && value != ESSL_DECODE_SERIAL)
+        return fail(ESSL_E_ARG, "bad decode mode");
+      c->mode = (int)value;
+      return ESSL_OK;
+    case ESSL_OPT_SEQ_BITS:
+      if (value < 32 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad seq bits");
+      c->seq_bits = (int)value;
+      return ESSL_OK;
+    case ESSL_OPT_PROFILE:
+      c->profile = value != 0;
+      return ESSL_OK;
+    case ESSL_OPT_OVERLAP_BITS:
+      if (value < 0 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad overlap bits");
+      c->overlap_bits = (int)value;
+      return ESSL_OK;
+  }
+  return fail(ESSL_E_ARG, "unknown option");
+}
+
+int64_t essl_ctx_launch_count(const essl_ctx *c) { return c ? c->launches.load() : -1; }
+
+int essl_ctx_profile_read(essl_ctx *c, double *ms, int64_t *count) {
+  if (!c || !ms || !count) return fail(ESSL_E_ARG, "essl_ctx_profile_read: bad arguments");
+  for (auto &r : c->recs) {
+    CK(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    if (r.kid >= 0 && r.kid < ESSL_K_COUNT) {
+      ms[r.kid] += t;
+      count[r.kid] += 1;
+    }
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->recs.clear();
+  return ESSL_OK;
+}
+
+int essl_stage(essl_ctx *c, int slot, const uint8_t *const *src, const uint32_t *len, int n,
+               essl_sample *samples, int nthreads, void *stream, const uint8_t **dev_blob) {
+  if (!c || slot < 0 || slot > 1 || n < 0 || n > c->max_batch || !dev_blob)
+    return fail(ESSL_E_ARG, "essl_stage: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
+  std::vector<uint64_t> off(n + 1);
+  uint64_t pos = 0;
+  for (int i = 0; i < n; i++) {
+    if ((int)len[i] > c->max_payload) return fail(ESSL_E_CAPACITY, "payload larger than max_payload");
+    off[i] = pos;
+    pos += ((uint64_t)len[i] + 63) / 64 * 64;
+  }
+  off[n] = pos;
+  uint8_t *h = c->h_stage[slot];
+  nthreads = std::max(1, std::min(nthreads, n));
+  auto work = [&](int t) {
+    for (int i = t; i < n; i += nthreads) std::memcpy(h + off[i], src[i], len[i]);
+  };
+  if (nthreads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; t++) th.emplace_back(work, t);
+    for (auto &x : th) x.join();
+  }
+  for (int i = 0; i < n; i++) {
+    samples[i].offset = off[i];
+    samples[i].length = len[i];
+  }
+  if (pos) CK(cudaMemcpyAsync(c->d_stage[slot], h, pos, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(c->ev_stage[slot], st));
+  c->stage_used[slot] = true;
+  *dev_blob = c->d_stage[slot];
+  return ESSL_OK;
+}
+
+int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n, int res,
+                    int out_kind, void *out, int64_t out_stride, uint8_t *out_u8,
+                    essl_result *results, void *stream) {
+  if (!c || n < 0 || res < 1 || (n > 0 && (!blob || !samples)))
+    return fail(ESSL_E_ARG, "essl_decode_rrc: bad arguments");
+  if (out_kind != ESSL_OUT_BF16_NCHW && out_kind != ESSL_OUT_F32_NCHW && out_kind != ESSL_OUT_NONE)
+    return fail(ESSL_E_ARG, "bad out_kind");
+  if (out_kind != ESSL_OUT_NONE && !out) return fail(ESSL_E_ARG, "null output");
+  if (n == 0) return ESSL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int ring = -1;
+  int rc = run_decode(c, blob, samples, n, results, st, &ring);
+  if (rc) return rc;
+  essl::PixelParams pp;
+  pp.info = c->s.info;
+  pp.plane = c->s.plane;
+  pp.n = n;
+  pp.res = res;
+  pp.out_kind = out_kind;
+  pp.out = out;
+  pp.out_stride = out_stride;
+  pp.out_u8 = out_u8;
+  if (out_kind != ESSL_OUT_NONE || out_u8) {
+    Prof pr(c, ESSL_K_RESIZE, st);
+    essl::launch_resize(pp, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_desc[ring], st));
+  return ESSL_OK;
+}
+
+int essl_decode_crop_u8(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
+                        uint8_t *out, const uint64_t *out_offsets, essl_result *results,
+                        void *stream) {
+  if (!c || n < 0 || (n > 0 && (!blob || !samples || !out || !out_offsets)))
+    return fail(ESSL_E_ARG, "essl_decode_crop_u8: bad arguments");
+  if (n == 0) return ESSL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int ring = -1;
+  int rc = run_decode(c, blob, samples, n, results, st, &ring);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->d_offsets, out_offsets, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
+  {
+    Prof pr(c, ESSL_K_CROP, st);
+    essl::launch_crop_u8(c->s.info, c->s.plane, n, out, c->d_offsets, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_desc[ring], st));
+  CK(cudaStreamSynchronize(st));  // out_offsets is a host array
+  return ESSL_OK;
+}
+
+int essl_dump_coefs(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
+                    int16_t *out, const uint64_t *out_offsets, int64_t out_cap, int32_t *geometry,
+                    essl_result *results, void *stream) {
+  if (!c || n < 0 || (n > 0 && (!blob || !samples || !out || !out_offsets || !geometry)))
+    return fail(ESSL_E_ARG, "essl_dump_coefs: bad arguments");
+  if (n == 0) return ESSL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int ring = -1;
+  int rc = run_decode(c, blob, samples, n, results, st, &ring);
+  if (rc) return rc;
+  std::vector<essl::ImgInfo> info(n);
+  CK(cudaMemcpyAsync(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; i++) {
+    int64_t need = 0;
+    for (int q = 0; q < 3; q++) {
+      const bool ok = info[i].status == 0 && q < info[i].ncomp;
+      geometry[i * 12 + 4 * q + 0] = ok ? info[i].wby0[q] : 0;
+      geometry[i * 12 + 4 * q + 1] = ok ? info[i].wbx0[q] : 0;
+      geometry[i * 12 + 4 * q + 2] = ok ? info[i].wbh[q] : 0;
+      geometry[i * 12 + 4 * q + 3] = ok ? info[i].wbw[q] : 0;
+      if (ok) need += (int64_t)info[i].wbh[q] * info[i].wbw[q] * 64;
+    }
+    if ((int64_t)out_offsets[i] + need > out_cap) return fail(ESSL_E_CAPACITY, "dump buffer too small");
+  }
+  CK(cudaMemcpyAsync(c->d_offsets, out_offsets, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
+  {
+    Prof pr(c, ESSL_K_DUMP, st);
+    essl::launch_dump_coefs(c->s.info, c->s.coef, n, out, c->d_offsets, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_desc[ring], st));
+  CK(cudaStreamSynchronize(st));
+  return ESSL_OK;
+}
+
+int essl_mask(essl_ctx *c, uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens,
+              int k, int32_t *mask_sorted, int64_t *ids_keep, int64_t *ids_restore, void *stream) {
+  if (n < 0 || tokens < 1 || tokens > 4096 || k < 0 || k > tokens || (n > 0 && !index))
+    return fail(ESSL_E_ARG, "essl_mask: bad arguments");
+  {
+    Prof pr(c, ESSL_K_MASK, (cudaStream_t)stream);
+    essl::launch_mask(seed, epoch, index, n, tokens, k, mask_sorted, ids_keep, ids_restore,
+                      (cudaStream_t)stream);
+  }
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+int essl_mask_from_states(essl_ctx *c, const uint64_t *states, int n, int tokens, int k,
+                          int32_t *mask_sorted, int64_t *ids_keep, int64_t *ids_restore,
+                          void *stream) {
+  if (n < 0 || tokens < 1 || tokens > 4096 || k < 0 || k > tokens || (n > 0 && !states))
+    return fail(ESSL_E_ARG, "essl_mask_from_states: bad arguments");
+  {
+    Prof pr(c, ESSL_K_MASK, (cudaStream_t)stream);
+    essl::launch_mask_states(states, n, tokens, k, mask_sorted, ids_keep, ids_restore,
+                             (cudaStream_t)stream);
+  }
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+int essl_gather_visible(essl_ctx *c, const void *pixels_bf16, int n, int res, int patch,
+                        const int64_t *ids_keep, int n_keep, void *tokens_bf16, void *stream) {
+  if (n < 0 || patch < 1 || res % patch || n_keep < 0 || (n > 0 && (!pixels_bf16 || !tokens_bf16)))
+    return fail(ESSL_E_ARG, "essl_gather_visible: bad arguments");
+  {
+    Prof pr(c, ESSL_K_GATHER, (cudaStream_t)stream);
+    essl::launch_gather(pixels_bf16, n, res, patch, ids_keep, n_keep, tokens_bf16,
+                        (cudaStream_t)stream);
+  }
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+int essl_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, int ow, int flip,
+                   void *stream) {
+  if (!src || !dst || ih < 1 || iw < 1 || oh < 1 || ow < 1)
+    return fail(ESSL_E_ARG, "essl_resize_u8: bad arguments");
+  essl::launch_resize_u8(src, ih, iw, dst, oh, ow, flip, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+int essl_normalize_u8(const uint8_t *src, int h, int w, float *dst, void *stream) {
+  if (!src || !dst || h < 1 || w < 1) return fail(ESSL_E_ARG, "essl_normalize_u8: bad arguments");
+  essl::launch_normalize_u8(src, h, w, dst, (cudaStream_t)stream);
+  CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+}  // extern "C"

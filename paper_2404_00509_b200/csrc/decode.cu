@@ -1,0 +1,1205 @@
+// k_decode: one CTA per image.  Replaces, for a whole batch on the GPU,
+//   container.py:249-265   read_sample CRC check
+//   jpeg/codec.py:124-265  parse_stream + _finish_geometry
+//   jpeg/codec.py:272-320  _huff_lut / _destuff
+//   jpeg/decode_kernels.py:27-179  destuff_scan / bit reader / decode_scan_baseline
+//   jpeg/codec.py:323-330  _check_consumed
+//   jpeg/decode_kernels.py:388-534 reconstruct_blocks (crop window only)
+//
+// Entropy decoding of a restart-free baseline scan is inherently serial; it
+// is parallelised inside the CTA by self-synchronising speculative decode:
+// the clean bitstream is cut into <=256 subsequences, thread t decodes
+// subsequence t from a guessed state (warm-up of `overlap_bits` before the
+// boundary), then a fixpoint pass re-decodes every subsequence whose entry
+// state disagrees with its predecessor's exit state.  Entry states are
+// proven correct by induction from the exact start, after
+// which a prefix scan over per-subsequence block counts / DC sums gives each
+// thread its absolute block index and DC predictors, and a final pass writes
+// coefficients of crop-window blocks only, stopping at the last MCU row the
+// crop needs (codec.py:483-500 row_stop).  Streams with restart intervals
+// (DRI) are decoded one interval per thread (exact entry states).
+#include <cstdint>
+
+#include "essl_common.cuh"
+
+namespace essl {
+
+__constant__ uint8_t c_zz[64] = {
+    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+    12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+    35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+    58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+
+// x^(2^k) mod P (reflected CRC-32), k = 0..31; filled by init_crc_tables().
+__constant__ uint32_t c_x2n[32];
+
+constexpr uint32_t kErrP = 0xFFFFFFFFu;  // "error / dead" exit state marker
+constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
+
+struct HuffTab {
+  uint16_t fast[1 << kFastBits];  // (sym << 4) | len, len in 1..kFastBits; 0 = slow path
+  int32_t lim[17];                // first[L] + count[L]
+  int32_t first[17];
+  int16_t vptr[17];
+  uint8_t vals[256];
+};
+
+struct SeqRec {
+  uint32_t gp, gkb;  // entry state: bit position, k | b << 8
+  uint32_t ep, ekb;  // exit state (ep == kErrP: error or dead)
+  uint32_t nblk;     // blocks completed inside the subsequence
+  int32_t dc[3];     // sum of DC differences per scan slot
+  uint32_t errblk, errp;
+  int32_t err;       // own decode error (1) / dead entry (2)
+};
+
+struct ParseState {
+  int pos, n, ri, have_sof, progressive, width, height, ncomp, nscans;
+  int comp_id[3], comp_h[3], comp_v[3], comp_tq[3];
+  int quant_pos[16], quant_pq[16];
+  int huff_pos[2][16], huff_tot[2][16];
+  int ns, slot_comp[4], slot_dpos[4], slot_dtot[4], slot_apos[4], slot_atot[4];
+  int scan_ri, scan_start, scan_end;
+  int status, reason, offset;
+  int cmd, dstart;
+};
+
+struct __align__(16) Smem {
+  uint32_t crc_tab[256];
+  uint32_t crc_part[kDecodeThreads];
+  uint8_t hdr[kHdrCache];
+  HuffTab tab[kMaxTables];
+  SeqRec seq[kDecodeThreads];
+  ParseState ps;
+  int32_t q[3][64];            // dequantisation tables, natural order
+  uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
+  int slot_dc[4], slot_ac[4];  // table index per slot
+  int slot_comp[4], slot_h[4], slot_v[4];
+  int ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1;
+  int wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
+  uint64_t coef_off[3];
+  uint64_t coef_base;
+  uint32_t K[8];
+  uint32_t limit_blocks, clean_bits;
+  uint32_t clean_words;
+  uint64_t clean_off;
+  uint32_t rst_off;  // word offset of the restart table inside the clean region
+  int n_restarts, max_restarts;
+  int status, reason, offset;
+  uint32_t p_final;
+  int coef_range;
+  int stop, red_i[2];
+  uint32_t scan_a[kDecodeThreads], scan_b[kDecodeThreads];
+  int changed;
+  int32_t idct_tr[kDecodeThreads / 32][4][64];
+};
+
+// ---------------------------------------------------------------------------
+// small helpers
+
+__device__ __forceinline__ int extend_bits(uint32_t v, int size) {  // decode_kernels.py:101-108
+  return (size && v < (1u << (size - 1))) ? (int)v - (1 << size) + 1 : (int)v;
+}
+
+__device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+  // a(x) * b(x) modulo the reflected CRC-32 polynomial (zlib multmodp).
+  uint32_t p = 0;
+#pragma unroll 1
+  for (int i = 0; i < 32; i++) {
+    if (a & (0x80000000u >> i)) p ^= b;
+    b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+  }
+  return p;
+}
+
+__device__ uint32_t x2nmodp(uint64_t n, int k) {  // x^(n * 2^k) mod P
+  uint32_t p = 0x80000000u;
+  while (n) {
+    if (n & 1) p = multmodp(c_x2n[k & 31], p);
+    n >>= 1;
+    k++;
+  }
+  return p;
+}
+
+__device__ __forceinline__ bool is_rst(uint32_t m) { return m >= 0xD0 && m <= 0xD7; }
+
+// Block-wide exclusive scan of two u32 values (256 threads).
+__device__ void block_scan2(Smem &S, uint32_t &a, uint32_t &b, uint32_t &ta, uint32_t &tb) {
+  const int tid = threadIdx.x;
+  S.scan_a[tid] = a;
+  S.scan_b[tid] = b;
+  __syncthreads();
+#pragma unroll 1
+  for (int off = 1; off < kDecodeThreads; off <<= 1) {
+    uint32_t va = tid >= off ? S.scan_a[tid - off] : 0;
+    uint32_t vb = tid >= off ? S.scan_b[tid - off] : 0;
+    __syncthreads();
+    S.scan_a[tid] += va;
+    S.scan_b[tid] += vb;
+    __syncthreads();
+  }
+  ta = S.scan_a[kDecodeThreads - 1];
+  tb = S.scan_b[kDecodeThreads - 1];
+  a = S.scan_a[tid] - a;  // exclusive
+  b = S.scan_b[tid] - b;
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// header parse (thread 0), codec.py:124-251
+
+struct PayloadView {
+  const uint8_t *g;
+  int n;
+  const uint8_t *hdr;
+  int hdr_n;
+  __device__ __forceinline__ int operator[](int i) const { return i < hdr_n ? hdr[i] : g[i]; }
+};
+
+__device__ void parse_fail(ParseState &P, int reason, int off) {
+  P.status = ESSL_ST_MALFORMED;
+  P.reason = reason;
+  P.offset = off;
+  P.cmd = 2;
+}
+
+// Runs until the next SOS (cmd=1, dstart set), EOI/end (cmd=0) or error (cmd=2).
+__device__ void parse_until_sos(ParseState &P, const PayloadView &d) {
+  const int n = d.n;
+  while (P.pos < n) {
+    int pos = P.pos;
+    if (d[pos] != 0xFF) return parse_fail(P, R_EXPECTED_MARKER, pos);
+    while (pos < n && d[pos] == 0xFF) pos++;
+    if (pos >= n) break;
+    const int marker = d[pos++];
+    if (marker == 0xD9) { P.pos = n; break; }
+    if (marker == 0x01 || is_rst(marker)) { P.pos = pos; continue; }
+    if (pos + 2 > n) return parse_fail(P, R_UNEXPECTED_END, pos);
+    const int seglen = (d[pos] << 8) | d[pos + 1];
+    if (seglen < 2 || pos + seglen > n) return parse_fail(P, R_TRUNC_SEGMENT, pos);
+    const int body = pos + 2, end = pos + seglen;
+    if (marker == 0xDB) {  // DQT
+      int p = body;
+      while (p < end) {
+        int pq = d[p] >> 4, tq = d[p] & 15;
+        p++;
+        int count = 64 * (pq == 1 ? 2 : 1);
+        if (p + count > end) return parse_fail(P, R_TRUNC_DQT, p);
+        P.quant_pos[tq] = p;
+        P.quant_pq[tq] = pq;
+        p += count;
+      }
+    } else if (marker == 0xC4) {  // DHT
+      int p = body;
+      while (p < end) {
+        int tc = d[p] >> 4, th = d[p] & 15;
+        p++;
+        if (p + 16 > end) return parse_fail(P, R_TRUNC_DHT, p);
+        int total = 0;
+        for (int i = 0; i < 16; i++) total += d[p + i];
+        int bits_pos = p;
+        p += 16;
+        if (p + total > end) return parse_fail(P, R_TRUNC_DHT, p);
+        if (tc < 2) {
+          P.huff_pos[tc][th] = bits_pos;
+          P.huff_tot[tc][th] = total;
+        }
+        p += total;
+      }
+    } else if (marker == 0xC0 || marker == 0xC1 || marker == 0xC2) {  // SOF0/1/2
+      if (P.have_sof) return parse_fail(P, R_MULTI_SOF, pos);
+      if (body + 6 > n) return parse_fail(P, R_SEGMENT, body);
+      P.progressive = marker == 0xC2;
+      if (d[body] != 8) return parse_fail(P, R_PRECISION, body);
+      P.height = (d[body + 1] << 8) | d[body + 2];
+      P.width = (d[body + 3] << 8) | d[body + 4];
+      int nc = d[body + 5];
+      if (P.height == 0 || P.width == 0) return parse_fail(P, R_ZERO_DIM, body + 1);
+      if (nc != 1 && nc != 3) return parse_fail(P, R_NCOMP, body + 5);
+      int p = body + 6;
+      if (p + 3 * nc > n) return parse_fail(P, R_SEGMENT, p);
+      for (int i = 0; i < nc; i++) {
+        P.comp_id[i] = d[p];
+        P.comp_h[i] = d[p + 1] >> 4;
+        P.comp_v[i] = d[p + 1] & 15;
+        P.comp_tq[i] = d[p + 2];
+        p += 3;
+      }
+      for (int i = 0; i < nc; i++) {
+        int h = P.comp_h[i], v = P.comp_v[i];
+        if (!(h == 1 || h == 2 || h == 4) || !(v == 1 || v == 2 || v == 4))
+          return parse_fail(P, R_SAMPLING, pos);
+      }
+      P.ncomp = nc;
+      P.have_sof = 1;
+    } else if (marker == 0xC3 || marker == 0xC5 || marker == 0xC6 || marker == 0xC7 ||
+               marker == 0xC9 || marker == 0xCA || marker == 0xCB || marker == 0xCD ||
+               marker == 0xCE || marker == 0xCF) {
+      return parse_fail(P, R_SOF_TYPE, pos);
+    } else if (marker == 0xDD) {  // DRI
+      if (body + 2 > n) return parse_fail(P, R_UNEXPECTED_END, body);
+      P.ri = (d[body] << 8) | d[body + 1];
+    } else if (marker == 0xDA) {  // SOS
+      if (!P.have_sof) return parse_fail(P, R_SOS_BEFORE_SOF, pos);
+      if (body >= n) return parse_fail(P, R_SEGMENT, body);
+      int ns = d[body], p = body + 1;
+      if (p + 2 * ns + 3 > n) return parse_fail(P, R_SEGMENT, p);
+      for (int s = 0; s < ns; s++) {
+        int cs = d[p], td = d[p + 1] >> 4, ta = d[p + 1] & 15;
+        int idx = -1;
+        for (int i = 0; i < P.ncomp; i++)
+          if (P.comp_id[i] == cs) { idx = i; break; }
+        if (idx < 0) return parse_fail(P, R_UNKNOWN_COMP, p);
+        if (P.nscans == 0 && s < 4) {
+          P.slot_comp[s] = idx;
+          P.slot_dpos[s] = P.huff_pos[0][td];
+          P.slot_dtot[s] = P.huff_tot[0][td];
+          P.slot_apos[s] = P.huff_pos[1][ta];
+          P.slot_atot[s] = P.huff_tot[1][ta];
+        }
+        p += 2;
+      }
+      if (P.nscans == 0) {
+        P.ns = ns;
+        P.scan_ri = P.ri;
+        P.scan_start = end;
+      }
+      P.dstart = end;
+      P.cmd = 1;
+      return;
+    }
+    P.pos = end;
+  }
+  if (!P.have_sof || P.nscans == 0) return parse_fail(P, R_NO_IMAGE, P.pos < n ? P.pos : n);
+  P.cmd = 0;
+}
+
+// ---------------------------------------------------------------------------
+// entropy decoding
+
+struct BitReader {
+  const uint32_t *w;
+  uint32_t nw;
+  uint64_t buf;
+  int n;
+  uint32_t wi;
+  uint32_t p;
+  __device__ __forceinline__ uint32_t load(uint32_t i) const {
+    return i < nw ? __byte_perm(__ldg(w + i), 0, 0x0123) : 0xFFFFFFFFu;
+  }
+  __device__ __forceinline__ void init(uint32_t pos) {
+    wi = pos >> 5;
+    const int off = pos & 31;
+    uint64_t a = load(wi), b = load(wi + 1);
+    buf = ((a << 32) | b) << off;
+    n = 64 - off;
+    wi += 2;
+    p = pos;
+  }
+  __device__ __forceinline__ void refill() {
+    if (n <= 32) {
+      buf |= (uint64_t)load(wi) << (32 - n);
+      wi++;
+      n += 32;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek(int bits) const { return (uint32_t)(buf >> (64 - bits)); }
+  __device__ __forceinline__ void skip(int bits) {
+    buf <<= bits;
+    n -= bits;
+    p += bits;
+  }
+};
+
+__device__ __forceinline__ int decode_sym(const HuffTab &T, BitReader &br) {
+  const uint32_t e = T.fast[br.peek(kFastBits)];
+  if (e & 15) {
+    br.skip(e & 15);
+    return (int)(e >> 4);
+  }
+  const int code = (int)br.peek(16);
+#pragma unroll 1
+  for (int L = kFastBits + 1; L <= 16; L++) {
+    const int c = code >> (16 - L);
+    if (c < T.lim[L]) {
+      br.skip(L);
+      return T.vals[T.vptr[L] + c - T.first[L]];
+    }
+  }
+  return -1;
+}
+
+struct RunState {
+  uint32_t p;
+  int k, b;
+  uint32_t nblk;
+  int32_t dc[3];
+  int err;
+  uint32_t errblk, errp;
+  int coef_range;
+};
+
+// Decode units from (p0, k0, b0) while p < end_bit.  WRITE additionally tracks
+// the absolute block index (stopping at `limit`), DC predictors and stores the
+// crop-window coefficients (natural order) to `coef`.
+template <bool WRITE>
+__device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, int k0, int b0,
+                           uint32_t end_bit, RunState &o, uint32_t blk, uint32_t limit,
+                           int32_t *pred, int16_t *coef, uint32_t *p_final) {
+  BitReader br;
+  br.w = words;
+  br.nw = S.clean_words;
+  br.init(p0);
+  int k = k0, b = b0;
+  uint32_t nblk = 0;
+  int32_t dc0 = 0, dc1 = 0, dc2 = 0;
+  o.err = 0;
+  o.coef_range = 0;
+  // WRITE-mode block cursor
+  int mx = 0, my = 0;
+  int16_t *cur = nullptr;
+  auto locate = [&]() {
+    cur = nullptr;
+    if (coef && my >= S.my0 && my <= S.my1 && mx >= S.mx0 && mx <= S.mx1) {
+      const int s = S.blk_slot[b];
+      const int c = S.slot_comp[s];
+      const int byr = (my - S.my0) * S.slot_v[s] + S.blk_dy[b];
+      const int bxr = (mx - S.mx0) * S.slot_h[s] + S.blk_dx[b];
+      cur = coef + S.coef_off[c] + ((uint64_t)byr * S.wbw[c] + bxr) * 64;
+    }
+  };
+  if (WRITE) {
+    const uint32_t mcu = blk / S.bpm;
+    my = mcu / S.gx;
+    mx = mcu % S.gx;
+    locate();
+  }
+#pragma unroll 1
+  while (br.p < end_bit) {
+    if (WRITE && blk >= limit) break;
+    br.refill();
+    const uint32_t ustart = br.p;
+    const int s = S.blk_slot[b];
+    if (k == 0) {
+      const int sym = decode_sym(S.tab[S.slot_dc[s]], br);
+      if (sym < 0 || sym > 15) {
+        o.err = 1; o.errblk = nblk; o.errp = ustart;
+        break;
+      }
+      int diff = 0;
+      if (sym) {
+        diff = extend_bits(br.peek(sym), sym);
+        br.skip(sym);
+      }
+      if (s == 0) dc0 += diff; else if (s == 1) dc1 += diff; else dc2 += diff;
+      if (WRITE) {
+        const int32_t v = pred[s] + diff;
+        pred[s] = v;
+        if (cur) {
+          if (v < -32768 || v > 32767) o.coef_range = 1;
+          cur[0] = (int16_t)v;
+        }
+      }
+      k = 1;
+    } else {
+      const int rs = decode_sym(S.tab[S.slot_ac[s]], br);
+      if (rs < 0) {
+        o.err = 1; o.errblk = nblk; o.errp = ustart;
+        break;
+      }
+      const int r = rs >> 4, sz = rs & 15;
+      if (sz == 0) {
+        k = (r == 15) ? k + 16 : 64;
+      } else {
+        k += r;
+        if (k > 63) {
+          o.err = 1; o.errblk = nblk; o.errp = ustart;
+          break;
+        }
+        const int v = extend_bits(br.peek(sz), sz);
+        br.skip(sz);
+        if (WRITE && cur) cur[c_zz[k]] = (int16_t)v;
+        k++;
+      }
+    }
+    if (k >= 64) {
+      k = 0;
+      nblk++;
+      b = (b + 1 == S.bpm) ? 0 : b + 1;
+      if (WRITE) {
+        blk++;
+        if (b == 0) {
+          if (++mx == S.gx) { mx = 0; my++; }
+        }
+        if (blk == S.limit_blocks && p_final) *p_final = br.p;
+        locate();
+      }
+    }
+  }
+  o.p = o.err ? kErrP : br.p;
+  o.k = k;
+  o.b = b;
+  o.nblk = nblk;
+  o.dc[0] = dc0; o.dc[1] = dc1; o.dc[2] = dc2;
+}
+
+// ---------------------------------------------------------------------------
+// IDCT, decode_kernels.py:388-534 (int64 islow, exact)
+
+#define F_0_298631336 2446
+#define F_0_390180644 3196
+#define F_0_541196100 4433
+#define F_0_765366865 6270
+#define F_0_899976223 7373
+#define F_1_175875602 9633
+#define F_1_501321110 12299
+#define F_1_847759065 15137
+#define F_1_961570560 16069
+#define F_2_053119869 16819
+#define F_2_562915447 20995
+#define F_3_072711026 25172
+
+template <typename T>
+__device__ __forceinline__ void idct_1d(T d0, T d1, T d2, T d3, T d4, T d5, T d6, T d7,
+                                        T out[8], T bias, int shift) {
+  T z1 = (d2 + d6) * (T)F_0_541196100;
+  T t2 = z1 - d6 * (T)F_1_847759065;
+  T t3 = z1 + d2 * (T)F_0_765366865;
+  T t0 = (d0 + d4) * (T)8192;
+  T t1 = (d0 - d4) * (T)8192;
+  T t10 = t0 + t3, t13 = t0 - t3, t11 = t1 + t2, t12 = t1 - t2;
+  T o0 = d7, o1 = d5, o2 = d3, o3 = d1;
+  z1 = o0 + o3;
+  T z2 = o1 + o2, z3 = o0 + o2, z4 = o1 + o3;
+  T z5 = (z3 + z4) * (T)F_1_175875602;
+  o0 *= (T)F_0_298631336; o1 *= (T)F_2_053119869;
+  o2 *= (T)F_3_072711026; o3 *= (T)F_1_501321110;
+  z1 = -z1 * (T)F_0_899976223; z2 = -z2 * (T)F_2_562915447;
+  z3 = -z3 * (T)F_1_961570560 + z5; z4 = -z4 * (T)F_0_390180644 + z5;
+  o0 += z1 + z3; o1 += z2 + z4; o2 += z2 + z3; o3 += z1 + z4;
+  out[0] = (t10 + o3 + bias) >> shift;
+  out[7] = (t10 - o3 + bias) >> shift;
+  out[1] = (t11 + o2 + bias) >> shift;
+  out[6] = (t11 - o2 + bias) >> shift;
+  out[2] = (t12 + o1 + bias) >> shift;
+  out[5] = (t12 - o1 + bias) >> shift;
+  out[3] = (t13 + o0 + bias) >> shift;
+  out[4] = (t13 - o0 + bias) >> shift;
+}
+
+// Eight lanes per 8x8 block: lane j owns column j in pass 1 and row j in pass
+// 2 (transpose through shared memory).  int32 arithmetic is used when it is
+// provably exact: every intermediate of one 1-D pass is a linear form with
+// sum|c| <= 61214 (tools/idct_bound.py), so |input| <= 35079 keeps pass 1 and
+// |ws| <= 35078 keeps pass 2 below 2^31; otherwise the lane group falls back
+// to int64, matching the reference's unbounded ints.
+constexpr int kIdctMax1 = 35079;
+constexpr int kIdctMax2 = 35078;
+
+__device__ __forceinline__ int grp_max8(int v) {
+  v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 1));
+  v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 2));
+  v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, 4));
+  return v;
+}
+
+// Must be called by all 32 lanes of a warp (lanes with valid=false idle).
+__device__ void idct_block_8lanes(bool valid, const int16_t *coef, const int32_t *q, uint8_t *dst,
+                                  int pitch, int32_t *tr /* 64 ints per 8-lane group */) {
+  const int j = threadIdx.x & 7;
+  int32_t d[8];
+  int mabs = 0;
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    d[r] = valid ? (int32_t)coef[8 * r + j] * q[8 * r + j] : 0;
+    mabs = max(mabs, abs(d[r]));
+  }
+  const bool wide1 = grp_max8(mabs) > kIdctMax1;
+  int64_t w64[8];
+  int32_t w[8];
+  if (!(d[1] | d[2] | d[3] | d[4] | d[5] | d[6] | d[7])) {  // DC-only column (exact shortcut)
+#pragma unroll
+    for (int r = 0; r < 8; r++) { w64[r] = (int64_t)d[0] * 4; }
+  } else if (!wide1) {
+    int32_t o[8];
+    idct_1d<int32_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], o, 1024, 11);
+#pragma unroll
+    for (int r = 0; r < 8; r++) w64[r] = o[r];
+  } else {
+    idct_1d<int64_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], w64, 1024, 11);
+  }
+  int64_t m2 = 0;
+#pragma unroll
+  for (int r = 0; r < 8; r++) m2 = max(m2, w64[r] < 0 ? -w64[r] : w64[r]);
+  const bool wide2 = grp_max8(m2 > kIdctMax2 ? kIdctMax2 + 1 : (int)m2) > kIdctMax2;
+  uint32_t lo = 0, hi = 0;
+  if (!wide2) {
+    // transpose: column j -> tr[r*8 + j]
+#pragma unroll
+    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)w64[r];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; i++) w[i] = tr[j * 8 + i];
+    __syncwarp();
+    if (!(w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7])) {
+      int v = ((w[0] + 16) >> 5) + 128;
+      uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+      lo = hi = u * 0x01010101u;
+    } else {
+      int32_t o[8];
+      idct_1d<int32_t>(w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], o, 131072, 18);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        int v = o[i] + 128;
+        uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+        if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
+      }
+    }
+  } else {
+    // int64 transpose through two 32-bit halves
+    int64_t x[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(uint32_t)(w64[r] & 0xFFFFFFFF);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = (uint32_t)tr[j * 8 + i];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(w64[r] >> 32);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] |= (int64_t)tr[j * 8 + i] << 32;
+    __syncwarp();
+    if (!(x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7])) {
+      int64_t v = ((x[0] + 16) >> 5) + 128;
+      uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+      lo = hi = u * 0x01010101u;
+    } else {
+      int64_t o[8];
+      idct_1d<int64_t>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], o, 131072, 18);
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        int64_t v = o[i] + 128;
+        uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+        if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
+      }
+    }
+  }
+  if (valid) *reinterpret_cast<uint2 *>(dst + (int64_t)j * pitch) = make_uint2(lo, hi);
+}
+
+// ---------------------------------------------------------------------------
+
+__device__ void set_status(Smem &S, int st, int reason, int off) {
+  if (S.status == 0) {
+    S.status = st;
+    S.reason = reason;
+    S.offset = off;
+  }
+}
+
+__global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
+  __shared__ Smem S;
+  const int img = blockIdx.x;
+  const int tid = threadIdx.x;
+  const essl_sample smp = P.samples[img];
+  const uint8_t *g = P.blob + smp.offset;
+  const int n = (int)smp.length;
+  ImgInfo *info = P.s.info + img;
+
+  if (tid == 0) {
+    S.status = 0; S.reason = 0; S.offset = -1;
+    S.coef_range = 0;
+    S.p_final = kNoEnd;
+  }
+  // ---- stage header prefix, CRC table -------------------------------------
+  const int hdr_n = n < kHdrCache ? n : kHdrCache;
+  for (int i = tid; i < hdr_n; i += kDecodeThreads) S.hdr[i] = g[i];
+  {
+    uint32_t c = tid;
+#pragma unroll
+    for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+    S.crc_tab[tid] = c;
+  }
+  __syncthreads();
+
+  // ---- CRC32 (container.py:263) -------------------------------------------
+  // End-aligned chunks of L bytes (zero-padded at the front: leading zeros do
+  // not change a zero-init CRC); the 0xFFFFFFFF init is applied by
+  // complementing the first 4 message bytes; chunks combine in a tree with
+  // multiplication by x^(8 L 2^j).
+  if (smp.check_crc) {
+    uint32_t crc;
+    if (n < 4) {
+      crc = 0;
+      if (tid == 0) {
+        uint32_t c = 0xFFFFFFFFu;
+        for (int i = 0; i < n; i++) c = S.crc_tab[(c ^ g[i]) & 0xFF] ^ (c >> 8);
+        crc = c ^ 0xFFFFFFFFu;
+      }
+    } else {
+      const int L = (n + kDecodeThreads - 1) / kDecodeThreads;
+      const int start = n - (kDecodeThreads - tid) * L;
+      uint32_t c = 0;
+      for (int i = start < 0 ? 0 : start; i < start + L; i++) {
+        uint32_t byte = i < hdr_n ? S.hdr[i] : g[i];
+        if (i < 4) byte ^= 0xFF;
+        c = S.crc_tab[(c ^ byte) & 0xFF] ^ (c >> 8);
+      }
+      S.crc_part[tid] = c;
+      if (tid < 8) S.K[tid] = x2nmodp((uint64_t)L << tid, 3);
+      __syncthreads();
+#pragma unroll 1
+      for (int j = 0; (1 << j) < kDecodeThreads; j++) {
+        const int stride = 1 << j;
+        uint32_t v = 0;
+        const bool act = (tid % (2 * stride)) == 0;
+        if (act) {
+          v = multmodp(S.K[j], S.crc_part[tid]) ^ S.crc_part[tid + stride];
+        }
+        __syncthreads();
+        if (act) S.crc_part[tid] = v;
+        __syncthreads();
+      }
+      crc = S.crc_part[0] ^ 0xFFFFFFFFu;
+    }
+    if (tid == 0 && crc != smp.crc32) set_status(S, ESSL_ST_CRC, 0, -1);
+  }
+  __syncthreads();
+
+  // ---- parse (thread 0) + parallel entropy-segment end search --------------
+  ParseState &PS = S.ps;
+  if (tid == 0) {
+    PS.pos = 2; PS.n = n; PS.ri = 0; PS.have_sof = 0; PS.progressive = 0;
+    PS.ncomp = 0; PS.nscans = 0; PS.status = 0; PS.cmd = 0; PS.ns = 0;
+    for (int i = 0; i < 16; i++) { PS.quant_pos[i] = -1; PS.huff_pos[0][i] = -1; PS.huff_pos[1][i] = -1; }
+    if (n < 4 || S.hdr[0] != 0xFF || S.hdr[1] != 0xD8) parse_fail(PS, R_NO_SOI, 0);
+    else PS.cmd = 3;  // "continue"
+  }
+  __syncthreads();
+  PayloadView pv{g, n, S.hdr, hdr_n};
+  if (S.status == 0) {
+#pragma unroll 1
+    while (true) {
+      if (tid == 0 && PS.cmd != 2) parse_until_sos(PS, pv);
+      __syncthreads();
+      if (PS.cmd != 1) break;
+      // entropy_end (codec.py:109-121): first FF followed by a byte that is
+      // not 00, RSTn or FF.
+      if (tid == 0) S.stop = n;
+      __syncthreads();
+      const int d0 = PS.dstart;
+      const int span = n - d0;
+      const int per = (span + kDecodeThreads - 1) / kDecodeThreads;
+      const int a = d0 + tid * per, e = min(a + per, n - 1);
+      for (int i = a; i < e; i++) {
+        if (pv[i] == 0xFF) {
+          const int m = pv[i + 1];
+          if (!(m == 0x00 || is_rst(m) || m == 0xFF)) { atomicMin(&S.stop, i); break; }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        if (PS.nscans == 0) PS.scan_end = S.stop;
+        PS.nscans++;
+        PS.pos = S.stop;
+        PS.cmd = 3;
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && PS.cmd == 2) set_status(S, PS.status, PS.reason, PS.offset);
+  }
+  __syncthreads();
+
+  // ---- geometry, validation (codec.py:254-265, 448-482) --------------------
+  if (tid == 0 && S.status == 0) {
+    int hmax = 1, vmax = 1;
+    for (int i = 0; i < PS.ncomp; i++) {
+      hmax = max(hmax, PS.comp_h[i]);
+      vmax = max(vmax, PS.comp_v[i]);
+    }
+    const int W = PS.width, H = PS.height;
+    const int mcus_x = (W + 8 * hmax - 1) / (8 * hmax), mcus_y = (H + 8 * vmax - 1) / (8 * vmax);
+    for (int i = 0; i < PS.ncomp; i++) {
+      const int cw = (W * PS.comp_h[i] + hmax - 1) / hmax, ch = (H * PS.comp_v[i] + vmax - 1) / vmax;
+      S.bw[i] = (cw + 7) / 8;
+      S.bh[i] = (ch + 7) / 8;
+    }
+    info->width = W; info->height = H; info->ncomp = PS.ncomp;
+    info->hmax = hmax; info->vmax = vmax;
+    for (int i = 0; i < 3; i++) {
+      info->comp_h[i] = i < PS.ncomp ? PS.comp_h[i] : 1;
+      info->comp_v[i] = i < PS.ncomp ? PS.comp_v[i] : 1;
+    }
+    int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
+    if (w < 1 || h < 1 || x < 0 || y < 0 || x + w > W || y + h > H) {
+      set_status(S, ESSL_ST_RECT, 0, -1);
+    } else if (PS.progressive) {
+      set_status(S, ESSL_ST_UNSUPPORTED, R_PROGRESSIVE, -1);
+    } else if (PS.nscans != 1 || PS.ns != PS.ncomp) {
+      set_status(S, ESSL_ST_UNSUPPORTED, R_MULTI_SCAN, -1);
+    } else {
+      const int ns = PS.ns;
+      S.ns = ns;
+      int mcu_w, mcu_h;
+      if (ns == 1) {
+        S.gx = S.bw[PS.slot_comp[0]];
+        S.gy = S.bh[PS.slot_comp[0]];
+        mcu_w = mcu_h = 8;
+      } else {
+        S.gx = mcus_x;
+        S.gy = mcus_y;
+        mcu_w = 8 * hmax;
+        mcu_h = 8 * vmax;
+      }
+      int bpm = 0;
+      for (int s = 0; s < ns; s++) {
+        const int c = PS.slot_comp[s];
+        const int hh = ns > 1 ? PS.comp_h[c] : 1, vv = ns > 1 ? PS.comp_v[c] : 1;
+        S.slot_comp[s] = c; S.slot_h[s] = hh; S.slot_v[s] = vv;
+        for (int dy = 0; dy < vv; dy++)
+          for (int dx = 0; dx < hh; dx++) {
+            S.blk_slot[bpm] = s; S.blk_dy[bpm] = dy; S.blk_dx[bpm] = dx;
+            bpm++;
+          }
+      }
+      S.bpm = bpm;
+      S.mx0 = x / mcu_w; S.mx1 = (x + w - 1) / mcu_w;
+      S.my0 = y / mcu_h; S.my1 = (y + h - 1) / mcu_h;
+      S.row_stop = S.my1 + 1;
+      S.limit_blocks = (uint32_t)S.row_stop * S.gx * bpm;
+      info->mcus_entropy = S.row_stop * S.gx;
+      info->mcus_recon = (S.my1 - S.my0 + 1) * (S.mx1 - S.mx0 + 1);
+      // per-component window (full MCU extents), codec.py:502-508
+      uint64_t total = 0;
+      for (int c = 0; c < 3; c++) { S.wbh[c] = 0; S.wbw[c] = 0; S.wby0[c] = 0; S.wbx0[c] = 0; }
+      for (int s = 0; s < ns; s++) {
+        const int c = S.slot_comp[s];
+        S.wby0[c] = S.my0 * S.slot_v[s];
+        S.wbx0[c] = S.mx0 * S.slot_h[s];
+        S.wbh[c] = (S.my1 - S.my0 + 1) * S.slot_v[s];
+        S.wbw[c] = (S.mx1 - S.mx0 + 1) * S.slot_h[s];
+        S.coef_off[c] = total;
+        total += (uint64_t)S.wbh[c] * S.wbw[c] * 64;
+      }
+      const unsigned long long cbase = atomicAdd(&P.s.counters[1], (unsigned long long)total);
+      if (cbase + total > P.s.coef_cap) {
+        set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+      } else {
+        for (int c = 0; c < 3; c++) S.coef_off[c] += cbase;
+        S.coef_base = cbase;
+      }
+      // clean-bytes region: segment + padding + restart table
+      const int seglen = PS.scan_end - PS.scan_start;
+      S.max_restarts = PS.scan_ri ? (S.gx * S.gy) / PS.scan_ri : 0;
+      const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
+      const uint64_t clean_bytes = ((uint64_t)seglen + 16 + 15) / 16 * 16;
+      const uint64_t alloc = clean_bytes + 4ull * max_r + 16;
+      const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)((alloc + 15) / 16 * 16));
+      if (base + alloc > P.s.clean_cap) set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+      S.clean_off = base;
+      S.rst_off = (uint32_t)(clean_bytes / 4);
+    }
+  }
+  __syncthreads();
+
+  // ---- destuff (decode_kernels.py:27-61) into the clean region --------------
+  uint8_t *clean = P.s.clean + S.clean_off;
+  if (S.status == 0) {
+    const int seg0 = PS.scan_start, seg1 = PS.scan_end;
+    const int segn = seg1 - seg0;
+    const int per = (segn + kDecodeThreads - 1) / kDecodeThreads;
+    const int a = seg0 + tid * per, e = min(a + per, seg1);
+    if (tid == 0) S.stop = seg1;
+    __syncthreads();
+    for (int i = a; i < e; i++) {
+      if (pv[i] == 0xFF) {
+        if (i + 1 >= seg1) { atomicMin(&S.stop, i); break; }
+        const int m = pv[i + 1];
+        if (!(m == 0x00 || is_rst(m))) { atomicMin(&S.stop, i); break; }
+      }
+    }
+    __syncthreads();
+    const int stop = S.stop;
+    const int e2 = min(e, stop);
+    uint32_t kept = 0, nrst = 0;
+    for (int i = a; i < e2; i++) {
+      const int v = pv[i];
+      const bool second = i > seg0 && pv[i - 1] == 0xFF;
+      const bool rst = v == 0xFF && is_rst(pv[i + 1]);
+      kept += (!second && !rst);
+      nrst += rst;
+    }
+    uint32_t tk, tr;
+    block_scan2(S, kept, nrst, tk, tr);
+    const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
+    uint32_t *rst_tab = reinterpret_cast<uint32_t *>(clean) + S.rst_off;
+    for (int i = a; i < e2; i++) {
+      const int v = pv[i];
+      const bool second = i > seg0 && pv[i - 1] == 0xFF;
+      const bool rst = v == 0xFF && is_rst(pv[i + 1]);
+      if (rst) {
+        if ((int)nrst < max_r) rst_tab[nrst] = kept;
+        nrst++;
+      } else if (!second) {
+        clean[kept++] = (uint8_t)v;
+      }
+    }
+    __syncthreads();
+    if (tid < 16) clean[tk + tid] = 0xFF;  // 0xFF padding past the end (_br_fill)
+    if (tid == 0) {
+      S.clean_bits = tk * 8;
+      S.clean_words = (tk + 3) / 4;
+      S.n_restarts = (int)tr;
+      if (PS.scan_ri == 0 && tr > 0) set_status(S, ESSL_ST_MALFORMED, R_RST_NO_DRI, seg0);
+      else if ((int)tr > S.max_restarts + 2) set_status(S, ESSL_ST_MALFORMED, R_TOO_MANY_RST, seg0);
+    }
+  }
+  __syncthreads();
+
+  // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
+  if (tid == 0 && S.status == 0) {
+    int ntab = 0;
+    int tab_pos[kMaxTables];
+    for (int pass = 0; pass < 2 && S.status == 0; pass++) {
+      for (int s = 0; s < S.ns && S.status == 0; s++) {
+        const int pos = pass == 0 ? PS.slot_dpos[s] : PS.slot_apos[s];
+        const int tot = pass == 0 ? PS.slot_dtot[s] : PS.slot_atot[s];
+        if (pos < 0) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_UNDEFINED, -1); break; }
+        if (tot > 256) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_TOO_MANY, -1); break; }
+        int ti = -1;
+        for (int t = 0; t < ntab; t++) if (tab_pos[t] == pos) ti = t;
+        if (ti < 0) {
+          ti = ntab++;
+          tab_pos[ti] = pos;
+          HuffTab &T = S.tab[ti];
+          int code = 0, vi = 0;
+          T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
+          for (int L = 1; L <= 16; L++) {
+            const int cnt = pv[pos + L - 1];
+            T.first[L] = code;
+            T.vptr[L] = (int16_t)vi;
+            if (cnt && code + cnt > (1 << L)) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
+            code += cnt;
+            vi += cnt;
+            T.lim[L] = code;
+            code <<= 1;
+          }
+          for (int v = 0; v < tot; v++) T.vals[v] = (uint8_t)pv[pos + 16 + v];
+        }
+        if (pass == 0) S.slot_dc[s] = ti; else S.slot_ac[s] = ti;
+      }
+    }
+    S.red_i[0] = ntab;
+  }
+  __syncthreads();
+  if (S.status == 0) {
+    const int ntab = S.red_i[0];
+    for (int t = 0; t < ntab; t++) {
+      HuffTab &T = S.tab[t];
+      for (int e = tid; e < (1 << kFastBits); e += kDecodeThreads) {
+        uint16_t ent = 0;
+        for (int L = 1; L <= kFastBits; L++) {
+          const int c = e >> (kFastBits - L);
+          if (c < T.lim[L]) {
+            ent = (uint16_t)((T.vals[T.vptr[L] + c - T.first[L]] << 4) | L);
+            break;
+          }
+        }
+        T.fast[e] = ent;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- zero the coefficient window ------------------------------------------
+  if (S.status == 0) {
+    uint64_t total = 0;
+    for (int c = 0; c < 3; c++) total += (uint64_t)S.wbh[c] * S.wbw[c] * 64;
+    int4 *z = reinterpret_cast<int4 *>(P.s.coef + S.coef_base);
+    const uint64_t n16 = total / 8;
+    for (uint64_t i = tid; i < n16; i += kDecodeThreads) z[i] = make_int4(0, 0, 0, 0);
+  }
+  __syncthreads();
+
+  // ---- entropy decode ---------------------------------------------------------
+  const uint32_t *words = reinterpret_cast<const uint32_t *>(clean);
+  int16_t *coef = P.s.coef;
+  if (S.status == 0 && PS.scan_ri > 0) {
+    // DRI: one restart interval per thread, exact entry states
+    // (decode_kernels.py:130-138).
+    const uint32_t ri = PS.scan_ri;
+    const uint32_t lim_mcu = (uint32_t)S.row_stop * S.gx;
+    const uint32_t nint = (lim_mcu + ri - 1) / ri;
+    const uint32_t *rst_tab = words + S.rst_off;
+    if (tid == 0) { S.red_i[0] = 0x7FFFFFFF; S.red_i[1] = 0; }
+    __syncthreads();
+    for (uint32_t j = tid; j < nint; j += kDecodeThreads) {
+      if (j >= 1 && (int)(j - 1) >= S.n_restarts) {  // status 3
+        atomicMin(&S.red_i[0], (int)(2 * j + 1));
+        continue;
+      }
+      const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
+      int32_t pred[3] = {0, 0, 0};
+      RunState o;
+      const uint32_t blk0 = j * ri * S.bpm;
+      const uint32_t lim = min((j + 1) * ri, lim_mcu) * S.bpm;
+      decode_run<true>(S, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
+      if (o.err) atomicMin(&S.red_i[0], (int)(2 * j));
+      if (o.coef_range) S.coef_range = 1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int code = S.red_i[0];
+      if (code != 0x7FFFFFFF) {
+        const uint32_t j = code >> 1;
+        if (code & 1) {
+          set_status(S, ESSL_ST_MISSING_RST, 0, PS.scan_start);
+        } else {
+          // recompute the erroring interval's error position on one thread
+          const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
+          int32_t pred[3] = {0, 0, 0};
+          RunState o;
+          decode_run<false>(S, words, p0, 0, 0, kNoEnd, o, j * ri * S.bpm,
+                            min((j + 1) * ri, lim_mcu) * S.bpm, pred, coef, nullptr);
+          // decode_run<false> has no block limit; the WRITE pass already proved
+          // an error inside the interval, so this run reaches it.
+          const int seglen = PS.scan_end - PS.scan_start;
+          const uint32_t vpos = (o.errp + 25 + 7) / 8;
+          set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
+        }
+      } else if (S.p_final != kNoEnd && S.p_final > S.clean_bits) {
+        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      }
+    }
+  } else if (S.status == 0 && P.mode == ESSL_DECODE_SERIAL) {
+    if (tid == 0) {
+      int32_t pred[3] = {0, 0, 0};
+      RunState o;
+      decode_run<true>(S, words, 0, 0, 0, kNoEnd, o, 0, S.limit_blocks, pred, coef, &S.p_final);
+      if (o.err) {
+        const int seglen = PS.scan_end - PS.scan_start;
+        const uint32_t vpos = (o.errp + 25 + 7) / 8;
+        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
+      } else if (S.p_final > S.clean_bits) {
+        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      }
+      if (o.coef_range) S.coef_range = 1;
+    }
+  } else if (S.status == 0) {
+    // ---- speculative parallel decode --------------------------------------
+    const uint32_t cbits = S.clean_bits;
+    int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
+    nseq = max(1, min(nseq, kDecodeThreads));
+    const uint32_t slen = (cbits + nseq - 1) / nseq;
+    const uint32_t sbeg = tid * slen;
+    const uint32_t send = tid == nseq - 1 ? cbits : min(cbits, (tid + 1) * slen);
+    SeqRec &R = S.seq[tid];
+    if (tid < nseq) {
+      RunState o;
+      uint32_t gp = 0;
+      int gk = 0, gb = 0;
+      if (tid > 0) {
+        // warm-up from a guessed state (k=0, first block of an MCU)
+        uint32_t wp = sbeg > (uint32_t)P.overlap_bits ? sbeg - P.overlap_bits : 0;
+        int wk = 0, wb = 0;
+        while (true) {
+          decode_run<false>(S, words, wp, wk, wb, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
+          if (!o.err) break;
+          wp = o.errp + 1;  // re-guess after an impossible code
+          wk = 0; wb = 0;
+          if (wp >= sbeg) { o.p = sbeg; o.k = 0; o.b = 0; break; }
+        }
+        gp = o.p; gk = o.k; gb = o.b;
+      }
+      decode_run<false>(S, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
+      R.gp = gp; R.gkb = gk | (gb << 8);
+      R.ep = o.p; R.ekb = o.k | (o.b << 8);
+      R.nblk = o.nblk;
+      R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
+      R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
+    }
+    __syncthreads();
+    // fixpoint: re-decode subsequences whose entry != predecessor's exit
+#pragma unroll 1
+    for (int it = 0; it < nseq; it++) {
+      uint32_t pp = 0, pkb = 0;
+      bool redo = false;
+      if (tid > 0 && tid < nseq) {
+        pp = S.seq[tid - 1].ep;
+        pkb = S.seq[tid - 1].ekb;
+        redo = !(pp == R.gp && (pp == kErrP || pkb == R.gkb));
+      }
+      if (tid == 0) S.changed = 0;
+      __syncthreads();
+      if (redo) {
+        S.changed = 1;
+        R.gp = pp; R.gkb = pkb;
+        if (pp == kErrP) {
+          R.ep = kErrP; R.err = 2; R.nblk = 0;
+        } else {
+          RunState o;
+          decode_run<false>(S, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr, nullptr);
+          R.ep = o.p; R.ekb = o.k | (o.b << 8);
+          R.nblk = o.nblk;
+          R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
+          R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
+        }
+      }
+      __syncthreads();
+      if (!S.changed) break;
+    }
+    // prefix sums: block index and DC predictors at each subsequence entry
+    uint32_t my_entry = tid < nseq ? R.nblk : 0, zero = 0, tnb, tz;
+    block_scan2(S, my_entry, zero, tnb, tz);
+    uint32_t d0 = tid < nseq ? (uint32_t)R.dc[0] : 0, d1 = tid < nseq ? (uint32_t)R.dc[1] : 0;
+    uint32_t d2 = tid < nseq ? (uint32_t)R.dc[2] : 0, zero2 = 0;
+    block_scan2(S, d0, d1, tz, tz);
+    block_scan2(S, d2, zero2, tz, tz);
+    if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
+    __syncthreads();
+    if (tid < nseq && R.err == 1) atomicMin(&S.red_i[0], tid);
+    __syncthreads();
+    const int tstar = S.red_i[0];  // first subsequence whose true path errors
+    if (tid == tstar) {
+      if (my_entry + R.errblk < S.limit_blocks) {  // the reference reaches it
+        const int seglen = PS.scan_end - PS.scan_start;
+        const uint32_t vpos = (R.errp + 25 + 7) / 8;  // _br_fill keeps >= 25 bits
+        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && S.status == 0 && tstar == 0x7FFFFFFF && tnb < S.limit_blocks) {
+      // the data ends before the crop's last MCU row: continue serially into
+      // the 0xFF padding to classify corrupt (1) vs truncated (4)
+      const SeqRec &Lr = S.seq[nseq - 1];
+      RunState o;
+      int32_t pred[3] = {0, 0, 0};
+      decode_run<true>(S, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
+                       S.limit_blocks, pred, nullptr, nullptr);
+      if (o.err) {
+        const int seglen = PS.scan_end - PS.scan_start;
+        const uint32_t vpos = (o.errp + 25 + 7) / 8;
+        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
+      } else {
+        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      }
+    }
+    __syncthreads();
+    // write pass: crop-window coefficients, stopping at row_stop
+    if (S.status == 0 && tid < nseq && my_entry < S.limit_blocks && tid <= tstar) {
+      RunState o;
+      int32_t pred[3] = {(int32_t)d0, (int32_t)d1, (int32_t)d2};
+      decode_run<true>(S, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
+                       S.limit_blocks, pred, coef, &S.p_final);
+      if (o.coef_range) S.coef_range = 1;
+    }
+    __syncthreads();
+    if (tid == 0 && S.status == 0) {
+      if (S.p_final != kNoEnd && S.p_final > S.clean_bits)
+        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && S.status == 0 && S.coef_range) set_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
+
+  // ---- quantisation tables (codec.py:405-409) -------------------------------
+  if (tid == 0 && S.status == 0) {
+    for (int i = 0; i < PS.ncomp; i++) {
+      const int tq = PS.comp_tq[i];
+      if (tq > 15 || PS.quant_pos[tq] < 0) { set_status(S, ESSL_ST_QUANT, 0, tq); break; }
+    }
+  }
+  __syncthreads();
+  if (S.status == 0) {
+    for (int e = tid; e < PS.ncomp * 64; e += kDecodeThreads) {
+      const int c = e >> 6, k = e & 63;
+      const int tq = PS.comp_tq[c], pos = PS.quant_pos[tq];
+      const int v = PS.quant_pq[tq] == 1 ? ((pv[pos + 2 * k] << 8) | pv[pos + 2 * k + 1]) : pv[pos + k];
+      S.q[c][c_zz[k]] = v;
+    }
+  }
+  __syncthreads();
+
+  // ---- reconstruct crop-window blocks -> planes -------------------------------
+  if (tid == 0) {
+    if (S.status == 0) {
+      uint64_t total = 0;
+      uint64_t off[3];
+      for (int c = 0; c < 3; c++) {
+        off[c] = total;
+        total += (uint64_t)S.wbh[c] * 8 * S.wbw[c] * 8;
+      }
+      const unsigned long long base = atomicAdd(&P.s.counters[2], (unsigned long long)((total + 15) / 16 * 16));
+      if (base + total > P.s.plane_cap) {
+        set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+      } else {
+        for (int c = 0; c < 3; c++) {
+          info->plane_off[c] = base + off[c];
+          info->plane_pitch[c] = S.wbw[c] * 8;
+          info->wby0[c] = S.wby0[c]; info->wbx0[c] = S.wbx0[c];
+          info->wbh[c] = S.wbh[c]; info->wbw[c] = S.wbw[c];
+          info->coef_off[c] = S.coef_off[c];
+        }
+      }
+    }
+    info->status = S.status;
+    info->reason = S.reason;
+    info->offset = S.offset;
+    info->rx = smp.x; info->ry = smp.y; info->rw = smp.w; info->rh = smp.h;
+    info->flip = smp.flip;
+    if (P.results) {
+      essl_result r;
+      r.status = S.status; r.reason = S.reason; r.offset = S.offset;
+      r.mcus_entropy_decoded = S.status == 0 ? info->mcus_entropy : 0;
+      r.mcus_reconstructed = S.status == 0 ? info->mcus_recon : 0;
+      r.width = PS.width; r.height = PS.height; r.ncomp = PS.ncomp;
+      P.results[img] = r;
+    }
+  }
+  __syncthreads();
+  if (S.status != 0) return;
+  // 4 blocks per warp, 8 lanes per block
+  int32_t *tr = S.idct_tr[tid >> 5][(tid >> 3) & 3];
+  for (int c = 0; c < PS.ncomp; c++) {
+    const int hb = min(S.wby0[c] + S.wbh[c], S.bh[c]) - S.wby0[c];
+    const int wb = min(S.wbx0[c] + S.wbw[c], S.bw[c]) - S.wbx0[c];
+    if (hb <= 0 || wb <= 0) continue;
+    const int pitch = S.wbw[c] * 8;
+    uint8_t *plane = P.s.plane + info->plane_off[c];
+    const int nblk = hb * wb;
+    const int rounds = (nblk + kDecodeThreads / 8 - 1) / (kDecodeThreads / 8);
+    for (int rd = 0; rd < rounds; rd++) {
+      const int jb = rd * (kDecodeThreads / 8) + (tid >> 3);
+      const bool valid = jb < nblk;
+      const int byr = valid ? jb / wb : 0, bxr = valid ? jb % wb : 0;
+      const int16_t *cf = coef + S.coef_off[c] + ((uint64_t)byr * S.wbw[c] + bxr) * 64;
+      idct_block_8lanes(valid, cf, S.q[c], plane + (uint64_t)byr * 8 * pitch + bxr * 8, pitch, tr);
+    }
+  }
+}
+
+void launch_decode(const DecodeParams &p, cudaStream_t st) {
+  if (p.n <= 0) return;
+  k_decode<<<p.n, kDecodeThreads, 0, st>>>(p);
+}
+
+void init_crc_tables() {
+  uint32_t x2n[32];
+  // x^1 in reflected form, then repeated squaring (zlib crc32.c x2n_table)
+  uint32_t p = 1u << 30;
+  auto mul = [](uint32_t a, uint32_t b) {
+    uint32_t r = 0;
+    for (int i = 0; i < 32; i++) {
+      if (a & (0x80000000u >> i)) r ^= b;
+      b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return r;
+  };
+  x2n[0] = p;
+  for (int k = 1; k < 32; k++) x2n[k] = p = mul(p, p);
+  cudaMemcpyToSymbol(c_x2n, x2n, sizeof(x2n));
+}
+
+}  // namespace essl

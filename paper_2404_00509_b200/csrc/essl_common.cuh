@@ -1,0 +1,114 @@
+// Shared device-side definitions for libessl (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "essl.h"
+
+namespace essl {
+
+constexpr int kDecodeThreads = 256;  // one CTA per image, one subsequence per thread
+constexpr int kFastBits = 10;        // first-level Huffman lookahead
+constexpr int kMaxTables = 6;        // distinct (class,id) tables a 3-slot scan can use
+constexpr int kMaxBpm = 48;          // blocks per MCU (h,v <= 4, 3 components)
+constexpr int kHdrCache = 2048;      // payload prefix staged in shared memory
+
+// Reason sub-codes (must match oracle/essl_oracle.c and errors.py).
+enum Reason : int32_t {
+  R_NONE = 0, R_NO_SOI = 1, R_EXPECTED_MARKER = 2, R_UNEXPECTED_END = 3,
+  R_TRUNC_SEGMENT = 4, R_TRUNC_DQT = 5, R_TRUNC_DHT = 6, R_MULTI_SOF = 7,
+  R_PRECISION = 8, R_ZERO_DIM = 9, R_NCOMP = 10, R_SAMPLING = 11,
+  R_SOF_TYPE = 12, R_SOS_BEFORE_SOF = 13, R_UNKNOWN_COMP = 14,
+  R_NO_IMAGE = 15, R_RST_NO_DRI = 16, R_TOO_MANY_RST = 17,
+  R_PROGRESSIVE = 18, R_MULTI_SCAN = 19, R_HUFF_UNDEFINED = 20,
+  R_HUFF_OVERFLOW = 21, R_HUFF_TOO_MANY = 22, R_SEGMENT = 23,
+  R_COEF_RANGE = 24, R_SCRATCH = 25,
+};
+
+// Per-image decode products consumed by the pixel kernels.  Written by
+// k_decode (one CTA per image), read by k_resize / k_crop_u8.
+struct ImgInfo {
+  int32_t status, reason, offset;
+  int32_t width, height, ncomp;
+  int32_t hmax, vmax;
+  int32_t comp_h[3], comp_v[3];
+  // crop window per component in blocks (full MCU extents, codec.py:502-508)
+  int32_t wby0[3], wbx0[3], wbh[3], wbw[3];
+  int32_t plane_pitch[3];
+  uint64_t plane_off[3];  // bytes into Scratch::plane
+  uint64_t coef_off[3];   // int16 elements into Scratch::coef
+  int32_t mcus_entropy, mcus_recon;
+  int32_t rx, ry, rw, rh, flip;
+};
+
+// Device scratch owned by the context; per-image regions are carved with
+// atomics on `counters` (reset per batch), so placement is order-free and
+// results never depend on it.
+struct Scratch {
+  uint8_t *clean;
+  uint64_t clean_cap;
+  int16_t *coef;
+  uint64_t coef_cap;  // elements
+  uint8_t *plane;
+  uint64_t plane_cap;
+  unsigned long long *counters;  // [0] clean bytes, [1] coef elems, [2] plane bytes
+  ImgInfo *info;
+};
+
+struct DecodeParams {
+  const uint8_t *blob;
+  const essl_sample *samples;  // device copy of the batch descriptors
+  int n;
+  Scratch s;
+  int mode;          // ESSL_DECODE_*
+  int seq_bits;      // speculative subsequence target length
+  int overlap_bits;  // speculative warm-up before each subsequence
+  essl_result *results;  // optional
+};
+
+struct PixelParams {
+  const ImgInfo *info;
+  const uint8_t *plane;
+  int n, res;
+  int out_kind;
+  void *out;
+  int64_t out_stride;  // elements per sample
+  uint8_t *out_u8;
+};
+
+// splitmix64 (rng.py:27-31)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+
+__host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t epoch,
+                                                      uint64_t index, uint64_t domain) {
+  uint64_t h = mix64(seed);
+  h = mix64(h ^ (epoch * kGamma));
+  h = mix64(h ^ (index * kGamma));
+  h = mix64(h ^ (domain * kGamma));
+  return h;
+}
+
+// launch wrappers (defined in the .cu files)
+void launch_decode(const DecodeParams &p, cudaStream_t st);
+void launch_resize(const PixelParams &p, cudaStream_t st);
+void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
+                    const uint64_t *offsets, cudaStream_t st);
+void launch_mask(uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens,
+                 int k, int32_t *mask, int64_t *keep, int64_t *restore, cudaStream_t st);
+void launch_mask_states(const uint64_t *states, int n, int tokens, int k, int32_t *mask,
+                        int64_t *keep, int64_t *restore, cudaStream_t st);
+void launch_gather(const void *pix, int n, int res, int patch, const int64_t *keep,
+                   int n_keep, void *tokens, cudaStream_t st);
+void launch_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, int ow,
+                      int flip, cudaStream_t st);
+void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStream_t st);
+void launch_results(const ImgInfo *info, int n, essl_result *res, cudaStream_t st);
+void launch_dump_coefs(const ImgInfo *info, const int16_t *coef, int n, int16_t *out,
+                       const uint64_t *offsets, cudaStream_t st);
+
+}  // namespace essl

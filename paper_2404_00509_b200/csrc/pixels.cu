@@ -1,0 +1,398 @@
+// Pixel-side kernels:
+//   k_resize   : YCbCr planes -> colour convert (decode_kernels.py:537-589) ->
+//                bilinear (imgops.py:24-60) -> hflip (imgops.py:256) ->
+//                normalize (imgops.py:231-240) -> bf16/f32 NCHW (+ u8 NHWC)
+//   k_crop_u8  : YCbCr planes -> RGB uint8 crop region (codec.py:422-431)
+//   k_mask     : sample_mask (masking.py:48-56) + ids_keep / ids_restore
+//   k_gather   : MAE patchify + visible-token gather
+//   k_resize_u8 / k_normalize_u8 : standalone imgops
+//
+// Exactness: the resize is float64 without contraction (__dmul_rn/__dadd_rn),
+// normalize is float32 IEEE (__fmul_rn/__fsub_rn/__fdiv_rn), so uint8 and
+// float32 outputs are bit-identical to the reference; bf16 is the RNE of the
+// exact float32.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "essl_common.cuh"
+
+namespace essl {
+
+constexpr int kPixThreads = 256;
+
+__device__ __forceinline__ int clamp255(int v) { return v < 0 ? 0 : (v > 255 ? 255 : v); }
+
+// Per-image source accessor over the decoded crop-window planes.
+struct PlaneSrc {
+  const uint8_t *p[3];
+  int pitch[3];
+  int oy[3], ox[3];  // window origin in component samples
+  int h[3], v[3];
+  int hmax, vmax, ncomp;
+  __device__ __forceinline__ void load(const ImgInfo &I, const uint8_t *plane) {
+    ncomp = I.ncomp;
+    hmax = I.hmax;
+    vmax = I.vmax;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      p[c] = plane + I.plane_off[c];
+      pitch[c] = I.plane_pitch[c];
+      oy[c] = I.wby0[c] * 8;
+      ox[c] = I.wbx0[c] * 8;
+      h[c] = I.comp_h[c];
+      v[c] = I.comp_v[c];
+    }
+  }
+  // RGB of image pixel (sy, sx): replication upsampling + fixed-point
+  // YCbCr->RGB (decode_kernels.py:551-576), gray replicated (579-589).
+  __device__ __forceinline__ void rgb(int sy, int sx, int &r, int &g, int &b) const {
+    if (ncomp == 1) {
+      r = g = b = p[0][(sy - oy[0]) * pitch[0] + (sx - ox[0])];
+      return;
+    }
+    const int yv = p[0][(sy * v[0] / vmax - oy[0]) * pitch[0] + (sx * h[0] / hmax - ox[0])];
+    const int cb = (int)p[1][(sy * v[1] / vmax - oy[1]) * pitch[1] + (sx * h[1] / hmax - ox[1])] - 128;
+    const int cr = (int)p[2][(sy * v[2] / vmax - oy[2]) * pitch[2] + (sx * h[2] / hmax - ox[2])] - 128;
+    r = clamp255(yv + ((91881 * cr + 32768) >> 16));
+    g = clamp255(yv + ((-22554 * cb - 46802 * cr + 32768) >> 16));
+    b = clamp255(yv + ((116130 * cb + 32768) >> 16));
+  }
+};
+
+// Bilinear tap geometry for one output coordinate (imgops.py:33-53).
+__device__ __forceinline__ void tap(int o, double scale, int in, int &i0, int &i1, double &w) {
+  double f = __dsub_rn(__dmul_rn((double)o + 0.5, scale), 0.5);
+  if (f < 0.0) f = 0.0;
+  i0 = __double2int_rz(f);
+  if (i0 > in - 1) i0 = in - 1;
+  i1 = i0 + 1;
+  if (i1 > in - 1) i1 = in - 1;
+  w = __dsub_rn(f, (double)i0);
+}
+
+__device__ __forceinline__ int bilerp(double wx, double wy, int s00, int s01, int s10, int s11) {
+  const double ax = __dsub_rn(1.0, wx), ay = __dsub_rn(1.0, wy);
+  const double top = __dadd_rn(__dmul_rn(ax, (double)s00), __dmul_rn(wx, (double)s01));
+  const double bot = __dadd_rn(__dmul_rn(ax, (double)s10), __dmul_rn(wx, (double)s11));
+  const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, top), __dmul_rn(wy, bot)), 0.5);
+  const int iv = __double2int_rz(v);
+  return iv > 255 ? 255 : iv;
+}
+
+// imgops.py:231-240: (f32(v) * f32(1/255) - mean) / std, IEEE float32.
+__device__ __forceinline__ float norm_value(int c, int v) {
+  const float inv255 = __fdiv_rn(1.0f, 255.0f);
+  const float mean = c == 0 ? 0.485f : (c == 1 ? 0.456f : 0.406f);
+  const float sd = c == 0 ? 0.229f : (c == 1 ? 0.224f : 0.225f);
+  return __fdiv_rn(__fsub_rn(__fmul_rn((float)v, inv255), mean), sd);
+}
+
+// grid: (ceil(res * ceil(res/8) / kPixThreads), n).  Thread = 8 consecutive
+// output pixels of one row, all three channels.
+__global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
+  __shared__ float lut[3][256];
+  __shared__ __nv_bfloat16 lutb[3][256];
+  for (int i = threadIdx.x; i < 768; i += kPixThreads) {
+    const float f = norm_value(i >> 8, i & 255);
+    lut[i >> 8][i & 255] = f;
+    lutb[i >> 8][i & 255] = __float2bfloat16_rn(f);
+  }
+  __syncthreads();
+  const int img = blockIdx.y;
+  const ImgInfo &I = P.info[img];
+  if (I.status != 0) return;
+  const int res = P.res;
+  const int groups = (res + 7) >> 3;
+  const int t = blockIdx.x * kPixThreads + threadIdx.x;
+  if (t >= res * groups) return;
+  const int oy = t / groups, ox0 = (t % groups) * 8;
+  PlaneSrc S;
+  S.load(I, P.plane);
+  const int ih = I.rh, iw = I.rw;
+  const double sy = __ddiv_rn((double)ih, (double)res), sx = __ddiv_rn((double)iw, (double)res);
+  int y0, y1;
+  double wy;
+  tap(oy, sy, ih, y0, y1, wy);
+  y0 += I.ry;
+  y1 += I.ry;
+  uint8_t px[8][3];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int ox = ox0 + i;
+    if (ox >= res) { px[i][0] = px[i][1] = px[i][2] = 0; continue; }
+    const int xs = I.flip ? res - 1 - ox : ox;  // hflip after resize
+    int x0, x1;
+    double wx;
+    tap(xs, sx, iw, x0, x1, wx);
+    x0 += I.rx;
+    x1 += I.rx;
+    int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
+    S.rgb(y0, x0, r00, g00, b00);
+    S.rgb(y0, x1, r01, g01, b01);
+    S.rgb(y1, x0, r10, g10, b10);
+    S.rgb(y1, x1, r11, g11, b11);
+    px[i][0] = (uint8_t)bilerp(wx, wy, r00, r01, r10, r11);
+    px[i][1] = (uint8_t)bilerp(wx, wy, g00, g01, g10, g11);
+    px[i][2] = (uint8_t)bilerp(wx, wy, b00, b01, b10, b11);
+  }
+  const int64_t plane_sz = (int64_t)res * res;
+  const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
+  const bool full = ox0 + 8 <= res && (res & 7) == 0;
+  if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      if (full) {
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = lutb[c][px[i][c]];
+        *reinterpret_cast<int4 *>(o + c * plane_sz) = *reinterpret_cast<int4 *>(v);
+      } else {
+        for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lutb[c][px[i][c]];
+      }
+    }
+  } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+    float *o = reinterpret_cast<float *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      if (full) {
+        float4 a = make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]);
+        float4 b = make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]);
+        reinterpret_cast<float4 *>(o + c * plane_sz)[0] = a;
+        reinterpret_cast<float4 *>(o + c * plane_sz)[1] = b;
+      } else {
+        for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lut[c][px[i][c]];
+      }
+    }
+  }
+  if (P.out_u8) {
+    uint8_t *o = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox0) * 3;
+    if (full) {
+      uint32_t w[6];
+#pragma unroll
+      for (int q = 0; q < 6; q++) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int e = q * 4 + b;
+          acc |= (uint32_t)px[e / 3][e % 3] << (8 * b);
+        }
+        w[q] = acc;
+      }
+      // 24 bytes at an 8-byte aligned address (res % 8 == 0)
+      reinterpret_cast<uint2 *>(o)[0] = make_uint2(w[0], w[1]);
+      reinterpret_cast<uint2 *>(o)[1] = make_uint2(w[2], w[3]);
+      reinterpret_cast<uint2 *>(o)[2] = make_uint2(w[4], w[5]);
+    } else {
+      for (int i = 0; i < 8 && ox0 + i < res; i++)
+        for (int c = 0; c < 3; c++) o[i * 3 + c] = px[i][c];
+    }
+  }
+}
+
+void launch_resize(const PixelParams &p, cudaStream_t st) {
+  if (p.n <= 0) return;
+  const int groups = (p.res + 7) / 8;
+  dim3 grid((p.res * groups + kPixThreads - 1) / kPixThreads, p.n);
+  k_resize<<<grid, kPixThreads, 0, st>>>(p);
+}
+
+// decode_crop output: uint8 [h, w, 3] at out + offsets[img].
+__global__ void k_crop_u8(const ImgInfo *info, const uint8_t *plane, uint8_t *out,
+                          const uint64_t *offsets) {
+  const int img = blockIdx.y;
+  const ImgInfo &I = info[img];
+  if (I.status != 0) return;
+  PlaneSrc S;
+  S.load(I, plane);
+  uint8_t *o = out + offsets[img];
+  const int64_t npx = (int64_t)I.rw * I.rh;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int yy = (int)(i / I.rw), xx = (int)(i % I.rw);
+    int r, g, b;
+    S.rgb(I.ry + yy, I.rx + xx, r, g, b);
+    o[i * 3 + 0] = (uint8_t)r;
+    o[i * 3 + 1] = (uint8_t)g;
+    o[i * 3 + 2] = (uint8_t)b;
+  }
+}
+
+void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
+                    const uint64_t *offsets, cudaStream_t st) {
+  if (n <= 0) return;
+  k_crop_u8<<<dim3(64, n), 256, 0, st>>>(info, plane, out, offsets);
+}
+
+// ---------------------------------------------------------------------------
+// MAE masking: one warp per sample.  Fisher-Yates draws are independent of
+// the permutation state (counter-based stream), so lanes compute them in
+// parallel; lane 0 applies the swaps; ballot/popc ranks give the sorted mask,
+// ids_keep and ids_restore.
+
+__global__ void k_mask(uint64_t seed, uint64_t epoch, const int64_t *index, const uint64_t *states,
+                       int tokens, int k, int32_t *mask, int64_t *keep, int64_t *restore) {
+  extern __shared__ int16_t sm[];
+  int16_t *perm = sm;             // [tokens]
+  int16_t *jd = sm + tokens;      // [tokens] draw for step d
+  const int s = blockIdx.x;
+  const int lane = threadIdx.x;
+  const uint64_t st0 = states ? states[s] : rng_init(seed, epoch, (uint64_t)index[s], 1);  // DOMAIN_MASK
+  for (int t = lane; t < tokens; t += 32) perm[t] = (int16_t)t;
+  for (int d = lane; d < tokens - 1; d += 32) {
+    const int i = tokens - 1 - d;
+    const uint64_t u = mix64(st0 + (uint64_t)(d + 1) * kGamma);
+    const double r = __dmul_rn((double)(u >> 11), 0x1p-53);  // rng.py:50-52
+    int j = (int)__double2ll_rz(__dmul_rn(r, (double)(i + 1)));  // rng.py:57-60
+    if (j >= i + 1) j = i;
+    jd[d] = (int16_t)j;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int d = 0; d < tokens - 1; d++) {
+      const int i = tokens - 1 - d, j = jd[d];
+      const int16_t a = perm[i];
+      perm[i] = perm[j];
+      perm[j] = a;
+    }
+  }
+  __syncwarp();
+  // membership: jd reused as flags
+  for (int t = lane; t < tokens; t += 32) jd[t] = 0;
+  __syncwarp();
+  for (int q = lane; q < k; q += 32) jd[perm[q]] = 1;
+  __syncwarp();
+  int base_m = 0, base_k = 0;
+  const int nkeep = tokens - k;
+  for (int t0 = 0; t0 < tokens; t0 += 32) {
+    const int t = t0 + lane;
+    const bool in = t < tokens;
+    const bool m = in && jd[t];
+    const unsigned bm = __ballot_sync(0xFFFFFFFFu, m);
+    const unsigned bk = __ballot_sync(0xFFFFFFFFu, in && !m);
+    const unsigned lower = (1u << lane) - 1;
+    if (in) {
+      if (m) {
+        const int rm = base_m + __popc(bm & lower);
+        if (mask) mask[(int64_t)s * k + rm] = t;
+        if (restore) restore[(int64_t)s * tokens + t] = nkeep + rm;
+      } else {
+        const int rk = base_k + __popc(bk & lower);
+        if (keep) keep[(int64_t)s * nkeep + rk] = t;
+        if (restore) restore[(int64_t)s * tokens + t] = rk;
+      }
+    }
+    base_m += __popc(bm);
+    base_k += __popc(bk);
+  }
+}
+
+void launch_mask(uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens, int k,
+                 int32_t *mask, int64_t *keep, int64_t *restore, cudaStream_t st) {
+  if (n <= 0 || tokens <= 0) return;
+  k_mask<<<n, 32, 2 * tokens * sizeof(int16_t), st>>>(seed, epoch, index, nullptr, tokens, k, mask,
+                                                       keep, restore);
+}
+
+void launch_mask_states(const uint64_t *states, int n, int tokens, int k, int32_t *mask,
+                        int64_t *keep, int64_t *restore, cudaStream_t st) {
+  if (n <= 0 || tokens <= 0) return;
+  k_mask<<<n, 32, 2 * tokens * sizeof(int16_t), st>>>(0, 0, nullptr, states, tokens, k, mask, keep,
+                                                       restore);
+}
+
+// MAE patchify ('nchpwq->nhwpqc') of the visible tokens: thread = 8 bf16 of
+// one token row (patch row pr, 8 consecutive (q, c) elements).
+__global__ void k_gather(const __nv_bfloat16 *pix, int res, int patch, const int64_t *keep,
+                         int n_keep, __nv_bfloat16 *tok) {
+  const int s = blockIdx.y;
+  const int dim = patch * patch * 3;
+  const int g = res / patch;
+  const int64_t total = (int64_t)n_keep * dim;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int ti = (int)(e / dim), w = (int)(e % dim);
+    const int id = (int)keep[(int64_t)s * n_keep + ti];
+    const int ph = id / g, pw = id % g;
+    const int pr = w / (patch * 3), rem = w % (patch * 3);
+    const int pc = rem / 3, c = rem % 3;
+    tok[(int64_t)s * total + e] =
+        pix[(((int64_t)s * 3 + c) * res + ph * patch + pr) * res + pw * patch + pc];
+  }
+}
+
+void launch_gather(const void *pix, int n, int res, int patch, const int64_t *keep, int n_keep,
+                   void *tokens, cudaStream_t st) {
+  if (n <= 0 || n_keep <= 0) return;
+  k_gather<<<dim3(48, n), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(pix), res, patch,
+                                         keep, n_keep, reinterpret_cast<__nv_bfloat16 *>(tokens));
+}
+
+// ---------------------------------------------------------------------------
+// standalone imgops on a single HWC uint8 image
+
+__global__ void k_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, int ow,
+                            int flip) {
+  const int64_t npx = (int64_t)oh * ow;
+  const double sy = __ddiv_rn((double)ih, (double)oh), sx = __ddiv_rn((double)iw, (double)ow);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int oy = (int)(i / ow), ox = (int)(i % ow);
+    const int xs = flip ? ow - 1 - ox : ox;
+    int y0, y1, x0, x1;
+    double wy, wx;
+    tap(oy, sy, ih, y0, y1, wy);
+    tap(xs, sx, iw, x0, x1, wx);
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+      dst[i * 3 + c] = (uint8_t)bilerp(wx, wy, src[((int64_t)y0 * iw + x0) * 3 + c],
+                                       src[((int64_t)y0 * iw + x1) * 3 + c],
+                                       src[((int64_t)y1 * iw + x0) * 3 + c],
+                                       src[((int64_t)y1 * iw + x1) * 3 + c]);
+    }
+  }
+}
+
+void launch_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, int ow, int flip,
+                      cudaStream_t st) {
+  k_resize_u8<<<148, 256, 0, st>>>(src, ih, iw, dst, oh, ow, flip);
+}
+
+__global__ void k_normalize_u8(const uint8_t *src, int h, int w, float *dst) {
+  const int64_t npx = (int64_t)h * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npx;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 3; c++) dst[c * npx + i] = norm_value(c, src[i * 3 + c]);
+  }
+}
+
+void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStream_t st) {
+  k_normalize_u8<<<148, 256, 0, st>>>(src, h, w, dst);
+}
+
+// Debug copy of the crop-window coefficients (components back to back).
+__global__ void k_dump_coefs(const ImgInfo *info, const int16_t *coef, int16_t *out,
+                             const uint64_t *offsets) {
+  const int img = blockIdx.y;
+  const ImgInfo &I = info[img];
+  if (I.status != 0) return;
+  int16_t *o = out + offsets[img];
+  uint64_t pos = 0;
+  for (int c = 0; c < I.ncomp; c++) {
+    const uint64_t cnt = (uint64_t)I.wbh[c] * I.wbw[c] * 64;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < cnt;
+         e += (uint64_t)gridDim.x * blockDim.x)
+      o[pos + e] = coef[I.coef_off[c] + e];
+    pos += cnt;
+  }
+}
+
+void launch_dump_coefs(const ImgInfo *info, const int16_t *coef, int n, int16_t *out,
+                       const uint64_t *offsets, cudaStream_t st) {
+  if (n <= 0) return;
+  k_dump_coefs<<<dim3(32, n), 256, 0, st>>>(info, coef, out, offsets);
+}
+
+}  // namespace essl

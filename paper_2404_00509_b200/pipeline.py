@@ -1,0 +1,338 @@
+"""GPU drop-in for the reference sample pipeline (cropload/pipeline.py).
+
+Same API surface -- ``RrcConfig``, ``sample_rrc``, ``apply_aug``,
+``ImageBatch``, ``LoaderConfig`` (same JSON keys), ``Loader`` with
+``epoch(e)`` / ``batches_per_epoch`` / context manager -- and the same
+determinism contract: every sample is a pure function of (bytes, config,
+seed, epoch, index), so batch content matches the reference bit for bit
+(float32 mode) no matter how work is scheduled.
+
+Per batch (pipeline.py:219-267):
+  host C++   : epoch permutation, DDP shard, RRC rect + flip per sample
+               (glibc libm, bit-exact with CPython), descriptor table
+  GPU        : CRC32 -> parse -> destuff -> speculative Huffman decode of the
+               crop's MCU rows -> IDCT of crop MCUs -> colour + bilinear +
+               flip + normalize -> bf16/f32 NCHW (+ uint8 NHWC) ;
+               MAE mask + ids_keep/ids_restore
+Compressed bytes are either HBM-resident (the container uploaded once) or
+staged per batch through a pinned double buffer.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+from collections import deque
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .container import ContainerHandle, open_container
+from .errors import ConfigError, CorruptionError
+from .jpeg import CropRect
+from .masking import MaskSpec
+from .rng import SampleRng, epoch_permutation, shard
+from .schedule import AugLevel
+
+
+@dataclass(frozen=True)
+class RrcConfig:
+    """RandomResizedCrop distribution (pipeline.py:31-48)."""
+
+    scale: tuple = (0.08, 1.0)
+    ratio: tuple = (3.0 / 4.0, 4.0 / 3.0)
+    out_size: int = 224
+    max_attempts: int = 10
+
+    def __post_init__(self):
+        if not 0.0 < self.scale[0] <= self.scale[1] <= 1.0:
+            raise ConfigError(f"scale bounds must satisfy 0 < lo <= hi <= 1: {self.scale}")
+        if not 0.0 < self.ratio[0] <= self.ratio[1]:
+            raise ConfigError(f"ratio bounds must be positive and ordered: {self.ratio}")
+        if self.out_size < 16:
+            raise ConfigError(f"output size must be >= 16: {self.out_size}")
+        if self.max_attempts < 1:
+            raise ConfigError("max_attempts must be >= 1")
+
+
+def sample_rrc(rng: SampleRng, src_w: int, src_h: int, cfg: RrcConfig) -> CropRect:
+    """Crop window draw (pipeline.py:51-75), native host C++ (glibc libm)."""
+    import ctypes
+    out = np.zeros(4, np.int32)
+    N.check(N.lib().essl_sample_rrc(ctypes.byref(rng._state), src_w, src_h, cfg.scale[0],
+                                    cfg.scale[1], cfg.ratio[0], cfg.ratio[1], cfg.max_attempts,
+                                    N.ptr(out)), "essl_sample_rrc")
+    return CropRect(int(out[0]), int(out[1]), int(out[2]), int(out[3]))
+
+
+def apply_aug(rng: SampleRng, img, level: AugLevel):
+    """Simple augmentation: horizontal flip at p=0.5 (pipeline.py:78-87).
+    The 3-Aug levels (pipeline.py:88-101) are SURVEY 8(f) row f1 (next)."""
+    from .imgops import hflip
+    if level is not AugLevel.SIMPLE:
+        raise ConfigError(f"aug level {level.value!r} is not implemented on the GPU path yet")
+    if rng.random() < 0.5:
+        img = hflip(img)
+    return img
+
+
+@dataclass
+class ImageBatch:
+    """One assembled batch (pipeline.py:105-117); tensors live on the GPU.
+
+    pixels: [b,3,h,h] float32 (reference dtype) or bfloat16; labels/indices
+    int64 [b]; mask int32 [b,k] sorted masked ids; uint8 [b,h,h,3] view;
+    ids_keep int64 [b,N-k]; ids_restore int64 [b,N]."""
+
+    pixels: object
+    labels: object
+    indices: object
+    epoch: int
+    mask: object = None
+    uint8: object = None
+    ids_keep: object = None
+    ids_restore: object = None
+
+    def __len__(self) -> int:
+        return int(self.pixels.shape[0])
+
+
+_GPU_KEYS = ("device", "out_dtype", "rank", "world_size", "resident", "prefetch")
+
+
+@dataclass
+class LoaderConfig:
+    """pipeline.py:120-170 plus GPU-only keys (device, out_dtype, rank,
+    world_size, resident, prefetch)."""
+
+    data: str
+    batch_size: int = 256
+    workers: int = 0
+    seed: int = 0
+    res: int = 224
+    scale: tuple = (0.08, 1.0)
+    ratio: tuple = (3.0 / 4.0, 4.0 / 3.0)
+    aug: str = "simple"
+    mask_ratio: float = 0.0
+    patch: int = 16
+    keep_uint8: bool = False
+    # GPU extensions
+    device: str | None = None
+    out_dtype: str = "float32"
+    rank: int = 0
+    world_size: int = 1
+    resident: bool = True
+    prefetch: int = 2
+
+    _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
+             "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
+
+    @classmethod
+    def from_document(cls, doc) -> "LoaderConfig":
+        if isinstance(doc, Path) or (isinstance(doc, str) and not doc.lstrip().startswith("{")):
+            doc = Path(doc).read_text()
+        if isinstance(doc, str):
+            doc = json.loads(doc)
+        if not isinstance(doc, dict):
+            raise ConfigError("loader config must be a JSON object")
+        unknown = set(doc) - set(cls._KEYS)
+        if unknown:
+            raise ConfigError(f"unknown loader config keys: {sorted(unknown)}")
+        if "data" not in doc:
+            raise ConfigError("loader config missing required key: data")
+        kw = dict(doc)
+        for key in ("scale", "ratio"):
+            if key in kw:
+                v = kw[key]
+                if not (isinstance(v, (list, tuple)) and len(v) == 2):
+                    raise ConfigError(f"{key} must be a [lo, hi] pair")
+                kw[key] = (float(v[0]), float(v[1]))
+        return cls(**kw)
+
+    def validate(self) -> None:
+        if self.batch_size < 1:
+            raise ConfigError("batch_size must be >= 1")
+        if self.aug not in tuple(a.value for a in AugLevel):
+            raise ConfigError(f"aug must be one of {[a.value for a in AugLevel]}, got {self.aug!r}")
+        if not 0.0 <= self.mask_ratio <= 1.0:
+            raise ConfigError(f"mask_ratio out of [0, 1]: {self.mask_ratio}")
+        if self.mask_ratio > 0.0 and self.res % self.patch != 0:
+            raise ConfigError(f"mask_ratio set but patch {self.patch} does not divide res {self.res}")
+        if self.out_dtype not in ("float32", "bfloat16"):
+            raise ConfigError(f"out_dtype must be float32 or bfloat16, got {self.out_dtype!r}")
+        if self.world_size < 1 or not 0 <= self.rank < self.world_size:
+            raise ConfigError(f"bad rank/world_size {self.rank}/{self.world_size}")
+
+
+@dataclass
+class _Pending:
+    batch: ImageBatch
+    samples: np.ndarray
+    indices: np.ndarray
+    results_host: object
+    event: object
+    keep: list = field(default_factory=list)
+
+
+class Loader:
+    """Epoch iterator over a container with the GPU sample pipeline
+    (pipeline.py:173-267).  Rank r of a DDP job iterates perm[r::world]."""
+
+    def __init__(self, config: LoaderConfig, container: ContainerHandle | None = None,
+                 engine=None):
+        import torch
+        config.validate()
+        self.config = config
+        self.handle = container if container is not None else open_container(config.data)
+        self._own_handle = container is None
+        self.handle.validate_all()
+        self.rrc = RrcConfig(tuple(config.scale), tuple(config.ratio), config.res)
+        self.aug_level = AugLevel(config.aug)
+        if self.aug_level is not AugLevel.SIMPLE:
+            raise ConfigError(f"aug level {config.aug!r} is not implemented on the GPU path yet "
+                              "(SURVEY 8(f) row f1)")
+        self.mask_spec = (MaskSpec.from_resolution(config.res, config.patch, config.mask_ratio)
+                          if config.mask_ratio > 0.0 else None)
+        from .engine import Engine
+        dev = config.device
+        if dev is None:
+            dev = f"cuda:{torch.cuda.current_device()}"
+        w, h = self.handle.max_dims()
+        self.engine = engine if engine is not None else Engine(
+            dev, max_batch=config.batch_size, max_side=max(w, h, 16),
+            max_payload=self.handle.max_payload())
+        self.device = self.engine.device
+        self.workers = config.workers if config.workers > 0 else (os.cpu_count() or 1)
+        rec = self.handle.records
+        self._widths = np.ascontiguousarray(rec["width"], np.uint16)
+        self._heights = np.ascontiguousarray(rec["height"], np.uint16)
+        self._offsets = np.ascontiguousarray(rec["payload_offset"], np.uint64)
+        self._lengths = np.ascontiguousarray(rec["payload_length"], np.uint32)
+        self._crcs = np.ascontiguousarray(rec["checksum"], np.uint32)
+        self._labels = torch.from_numpy(rec["label"].astype(np.int64))
+        self._blob = self.handle.to_device(self.device) if config.resident else None
+        self._host_base = self.handle.bytes.ctypes.data if not config.resident else 0
+        self._slot = 0
+        self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
+
+    @classmethod
+    def from_document(cls, doc) -> "Loader":
+        return cls(LoaderConfig.from_document(doc))
+
+    def __len__(self) -> int:
+        return len(self.handle)
+
+    def _shard_len(self) -> int:
+        n, r, w = len(self.handle), self.config.rank, self.config.world_size
+        return max(0, (n - r + w - 1) // w)
+
+    @property
+    def batches_per_epoch(self) -> int:
+        return -(-self._shard_len() // self.config.batch_size)
+
+    def retarget(self, res: int | None = None, mask_ratio: float | None = None,
+                 scale=None) -> None:
+        """Switch progressive-training stage (schedule.py params_for_epoch)
+        without reallocating the context or the resident dataset."""
+        cfg = self.config
+        if res is not None:
+            cfg.res = int(res)
+        if mask_ratio is not None:
+            cfg.mask_ratio = float(mask_ratio)
+        if scale is not None:
+            cfg.scale = (float(scale[0]), float(scale[1]))
+        cfg.validate()
+        self.rrc = RrcConfig(tuple(cfg.scale), tuple(cfg.ratio), cfg.res)
+        self.mask_spec = (MaskSpec.from_resolution(cfg.res, cfg.patch, cfg.mask_ratio)
+                          if cfg.mask_ratio > 0.0 else None)
+
+    def close(self) -> None:
+        if self._own_handle:
+            self.handle.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ------------------------------------------------------------------
+    def _descriptors(self, epoch: int, idxs: np.ndarray) -> np.ndarray:
+        cfg = self.config
+        s = self.engine.samples(len(idxs))
+        s["offset"] = self._offsets[idxs]
+        s["length"] = self._lengths[idxs]
+        s["crc32"] = self._crcs[idxs]
+        s["check_crc"] = 1
+        N.check(N.lib().essl_rrc_batch(cfg.seed & (2**64 - 1), epoch & (2**64 - 1), N.ptr(idxs),
+                                       len(idxs), N.ptr(self._widths), N.ptr(self._heights),
+                                       self.rrc.scale[0], self.rrc.scale[1], self.rrc.ratio[0],
+                                       self.rrc.ratio[1], N.ptr(s)), "essl_rrc_batch")
+        return s
+
+    def enqueue(self, epoch: int, idxs: np.ndarray, stream=None) -> _Pending:
+        """Issue one batch on the device (asynchronous)."""
+        import torch
+        cfg = self.config
+        eng = self.engine
+        idxs = np.ascontiguousarray(idxs, np.int64)
+        b, res = len(idxs), cfg.res
+        samples = self._descriptors(epoch, idxs)
+        if self._blob is not None:
+            blob_ptr = self._blob.data_ptr()
+        else:
+            ptrs = np.uint64(self._host_base) + samples["offset"].astype(np.uint64)
+            blob_ptr = eng.stage(self._slot, ptrs, samples["length"].copy(), samples,
+                                 nthreads=min(self.workers, 16), stream=stream)
+            self._slot ^= 1
+        dev = self.device
+        pixels = torch.empty((b, 3, res, res), dtype=self._out_dtype, device=dev)
+        u8 = torch.empty((b, res, res, 3), dtype=torch.uint8, device=dev) if cfg.keep_uint8 else None
+        results = eng.new_results(b)
+        kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
+        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=stream)
+        indices = torch.from_numpy(idxs).to(dev, non_blocking=True)
+        labels = self._labels[torch.from_numpy(idxs)].to(dev, non_blocking=True)
+        mask = keep = restore = None
+        if self.mask_spec is not None:
+            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
+            mask = torch.empty((b, k), dtype=torch.int32, device=dev)
+            keep = torch.empty((b, T - k), dtype=torch.int64, device=dev)
+            restore = torch.empty((b, T), dtype=torch.int64, device=dev)
+            eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=stream)
+        res_host = torch.empty(results.shape, dtype=torch.int32, pin_memory=True)
+        res_host.copy_(results, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream if stream is not None else eng.stream())
+        batch = ImageBatch(pixels, labels, indices, epoch, mask, u8, keep, restore)
+        return _Pending(batch, samples, idxs, res_host, ev)
+
+    def finish(self, p: _Pending) -> ImageBatch:
+        """Wait for a batch and raise the reference exception on failure."""
+        p.event.synchronize()
+        self.engine.raise_for(p.results_host.numpy(), p.samples, p.indices)
+        return p.batch
+
+    def epoch(self, epoch: int):
+        """Yield the batches of one epoch (this rank's shard) in permutation order."""
+        cfg = self.config
+        perm = shard(epoch_permutation(cfg.seed, epoch, len(self.handle)), cfg.rank,
+                     cfg.world_size)
+        B = cfg.batch_size
+        starts = range(0, len(perm), B)
+        q: deque = deque()
+        it = iter(starts)
+        depth = max(1, cfg.prefetch)
+        for s in it:
+            q.append(self.enqueue(epoch, perm[s:s + B]))
+            if len(q) >= depth:
+                break
+        while q:
+            p = q.popleft()
+            nxt = next(it, None)
+            if nxt is not None:
+                q.append(self.enqueue(epoch, perm[nxt:nxt + B]))
+            yield self.finish(p)

@@ -1,0 +1,273 @@
+"""CUDA path parity: every GPU output against the reference's golden vectors
+and the pinned CPU oracle on identical inputs.  Bars (BASELINE.json
+north_star): DCT coefficients, crop boxes, masks, ids bit-exact; uint8 and
+float32 pixels bit-exact (stricter than +-1 LSB); bf16 within 1e-2 abs."""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, stream_bytes
+
+pytestmark = pytest.mark.gpu
+
+STREAMS = ["q85_rst7", "q85_rst1", "q92", "q100", "q50_odd", "white_1x1", "flat_64", "pil_444",
+           "pil_422", "pil_420_opt", "pil_gray"]
+BF16_TOL = 1e-2
+
+
+def sha(a) -> str:
+    if hasattr(a, "cpu"):
+        a = a.cpu().numpy()
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def E(cuda):
+    import paper_2404_00509_b200 as E
+    return E
+
+
+@pytest.fixture(params=["speculative", "serial"])
+def mode(request, E):
+    from paper_2404_00509_b200 import _native as N
+    from paper_2404_00509_b200.engine import default_engine
+    eng = default_engine()
+    eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if request.param == "serial"
+                   else N.ESSL_DECODE_SPECULATIVE)
+    yield request.param
+    eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SPECULATIVE)
+
+
+@pytest.mark.parametrize("name", STREAMS)
+def test_stream_crops_match_reference(E, golden, name, mode):
+    ent = golden["streams"][name]
+    data = stream_bytes(name)
+    full, st = E.decode_full(data)
+    assert sha(full) == ent["full"]["sha"]
+    assert [st.mcus_entropy_decoded, st.mcus_reconstructed] == ent["full"]["stats"][:2]
+    items = [(data, E.CropRect(*c["rect"])) for c in ent["crops"]]
+    for (crop, cs), c in zip(E.decode_crops(items), ent["crops"]):
+        assert sha(crop) == c["sha"], c["rect"]
+        assert [cs.mcus_entropy_decoded, cs.mcus_reconstructed] == c["stats"][:2]
+    for br in ent["bad_rects"]:
+        with pytest.raises(ValueError):
+            E.decode_crop(data, E.CropRect(*br))
+
+
+@pytest.mark.parametrize("name", STREAMS)
+def test_coefficients_bit_exact(E, oracle, golden, name, mode):
+    """int16 crop-window coefficients == the reference's int32 arrays."""
+    import torch
+    from paper_2404_00509_b200.engine import default_engine
+    eng = default_engine()
+    data = stream_bytes(name)
+    for c in golden["streams"][name]["crops"][:6]:
+        rect = c["rect"]
+        ref = oracle.dump_coefs(data, tuple(rect))
+        assert [hashlib.sha256(a.tobytes()).hexdigest() for a in ref] == c["coef_sha"]
+        blob = torch.from_numpy(np.frombuffer(data + bytes(64), np.uint8).copy()).to(eng.device)
+        s = eng.samples(1)
+        s["length"] = len(data)
+        s["x"], s["y"], s["w"], s["h"] = rect
+        cap = sum(a.size for a in ref)
+        out = torch.zeros(cap, dtype=torch.int16, device=eng.device)
+        res = eng.new_results(1)
+        geo = eng.dump_coefs(blob.data_ptr(), s, out, np.zeros(1, np.uint64), cap, res,
+                             max_side=4096)
+        assert res.cpu().numpy()[0, 0] == 0
+        o = out.cpu().numpy()
+        pos = 0
+        for comp, a in enumerate(ref):
+            by0, bx0, bh, bw = geo[0, comp]
+            win = o[pos:pos + bh * bw * 64].reshape(bh, bw, 64)
+            pos += bh * bw * 64
+            assert np.array_equal(win, a[by0:by0 + bh, bx0:bx0 + bw]), (name, rect, comp)
+
+
+@pytest.mark.parametrize("name", ["truncated_half", "truncated_hdr", "not_jpeg"])
+def test_stream_errors_match_reference(E, golden, name, mode):
+    ent = golden["streams"][name]["error"]
+    with pytest.raises(E.DecodeError) as e:
+        E.decode_full(stream_bytes(name))
+    assert str(e.value) == ent["msg"]
+
+
+def test_progressive_unsupported(E):
+    with pytest.raises(E.UnsupportedStreamError):
+        E.decode_full(stream_bytes("pil_progressive"))
+
+
+def test_truncation_every_cut(E, oracle):
+    """Cut a stream at many points: GPU status/offset == oracle (== ref)."""
+    from paper_2404_00509_b200.errors import status_error
+    data = stream_bytes("q92")
+    rect = E.CropRect(0, 0, 64, 40)
+    cuts = list(range(620, len(data), 997)) + [len(data) - 1, len(data) - 2]
+    for cut in cuts:
+        d = data[:cut]
+        try:
+            oracle.decode_crop(d, (rect.x, rect.y, rect.w, rect.h))
+            ref = None
+        except oracle.OracleError as e:
+            ref = str(status_error(e.status, e.reason, e.offset))
+        try:
+            E.decode_crop(d, rect)
+            got = None
+        except Exception as e:  # noqa: BLE001
+            got = str(e)
+        assert got == ref, cut
+
+
+def _golden_loader(E, golden, key, dtype="float32"):
+    spec = golden["loader"][key]
+    cfg = dict(spec["cfg"])
+    cfg.update(data=str(GOLDEN / spec["data"]), workers=2, out_dtype=dtype)
+    return spec, E.Loader(E.LoaderConfig(**{k: (tuple(v) if isinstance(v, list) else v)
+                                            for k, v in cfg.items()}))
+
+
+@pytest.mark.parametrize("key", ["cfg1_simple_224", "cfg1_mask_224", "cfg4_pt_224",
+                                 "mixed_96_u8", "cfg3_epoch0", "cfg3_epoch1", "cfg3_epoch2",
+                                 "cfg3_epoch3"])
+def test_loader_float32_bit_exact(E, golden, key):
+    spec, loader = _golden_loader(E, golden, key)
+    with loader:
+        got = []
+        for e in spec["epochs"]:
+            for b in loader.epoch(e):
+                for s in range(len(b)):
+                    got.append((e, int(b.indices[s]), int(b.labels[s]), sha(b.pixels[s]),
+                                sha(b.uint8[s]) if b.uint8 is not None else None,
+                                b.mask[s].cpu().tolist() if b.mask is not None else None))
+    exp = [(s["epoch"], s["index"], s["label"], s["pixels"], s["uint8"], s["mask"])
+           for s in spec["samples"]]
+    assert got == exp
+
+
+def test_loader_bf16_within_tolerance(E, golden, oracle):
+    import torch
+    spec, loader = _golden_loader(E, golden, "cfg1_mask_224", dtype="bfloat16")
+    _, loader32 = _golden_loader(E, golden, "cfg1_mask_224")
+    with loader, loader32:
+        for b16, b32 in zip(loader.epoch(0), loader32.epoch(0)):
+            d = (b16.pixels.float() - b32.pixels).abs().max().item()
+            assert d <= BF16_TOL
+            assert torch.equal(b16.pixels, b32.pixels.to(torch.bfloat16))  # exact RNE
+            # ids_keep / ids_restore are the MAE conventions over the mask
+            T = b16.ids_restore.shape[1]
+            for s in range(len(b16)):
+                m = b16.mask[s].cpu().numpy()
+                keep = np.setdiff1d(np.arange(T), m)
+                assert np.array_equal(b16.ids_keep[s].cpu().numpy(), keep)
+                shuffle = np.concatenate([keep, m])
+                assert np.array_equal(b16.ids_restore[s].cpu().numpy(), np.argsort(shuffle))
+
+
+def test_gather_visible(E, golden):
+    import torch
+    from paper_2404_00509_b200.engine import default_engine
+    spec, loader = _golden_loader(E, golden, "cfg1_mask_224", dtype="bfloat16")
+    with loader:
+        b = next(iter(loader.epoch(0)))
+    eng = default_engine()
+    n, p, res = len(b), 16, 224
+    keep = b.ids_keep.to(eng.device)
+    tok = torch.empty((n, keep.shape[1], p * p * 3), dtype=torch.bfloat16, device=eng.device)
+    eng.gather_visible(b.pixels.to(eng.device), res, p, keep, tok)
+    x = b.pixels.to(eng.device).reshape(n, 3, res // p, p, res // p, p)
+    patches = torch.einsum("nchpwq->nhwpqc", x).reshape(n, (res // p) ** 2, p * p * 3)
+    ref = torch.gather(patches, 1, keep[:, :, None].expand(-1, -1, p * p * 3))
+    assert torch.equal(tok, ref)
+
+
+def test_standalone_imgops(E, golden, arrays):
+    for i, r in enumerate(golden["resize"]):
+        assert sha(E.imgops.resize_bilinear(arrays[f"resize_src_{i}"], *r["out"])) == r["sha"]
+    src = np.zeros((2, 2, 3), np.uint8)
+    src[:, 1] = 255
+    assert E.imgops.resize_bilinear(src, 4)[0, :, 0].tolist() == golden["resize_2x2_row"]
+    assert sha(E.imgops.normalize(arrays["normalize_src"])) == golden["normalize_sha"]
+
+
+def test_sample_mask_matches_reference(E, golden):
+    for m in golden["masks"]:
+        spec = E.MaskSpec.from_resolution(m["res"], 16, m["m"])
+        rng = E.SampleRng(3, 1, m["i"], E.DOMAIN_MASK)
+        assert E.sample_mask(rng, spec).tolist() == m["mask"]
+
+
+def test_crc_corruption_raises(E, tmp_path):
+    good = bytearray((GOLDEN / "cfg1_small.essl").read_bytes())
+    with E.open_container(GOLDEN / "cfg1_small.essl") as h:
+        off = int(h.records["payload_offset"][5])
+    good[off + 1000] ^= 0x21
+    p = tmp_path / "c.essl"
+    p.write_bytes(bytes(good))
+    with E.Loader(E.LoaderConfig(data=str(p), batch_size=16, res=64)) as loader:
+        with pytest.raises(E.CorruptionError, match="sample 5: checksum mismatch"):
+            list(loader.epoch(0))
+
+
+@pytest.fixture(scope="module")
+def synth_sets(E, tmp_path_factory):
+    d = tmp_path_factory.mktemp("synth")
+    a = d / "s256.essl"
+    E.build_synthetic(a, 96, 256, 95, seed=5)
+    b = d / "s512.essl"
+    E.build_synthetic(b, 24, 512, 90, seed=6)
+    c = d / "mixed.essl"
+    E.build_synthetic(c, 40, (17, 333), 80, seed=7)
+    return a, b, c
+
+
+@pytest.mark.parametrize("seq_bits,overlap", [(1024, 1024), (64, 0), (4096, 256), (300, 5000)])
+def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, overlap):
+    """Synthetic datasets (random crops, all rows) through the speculative
+    decoder with adversarial subsequence settings == the oracle, bit for bit."""
+    from paper_2404_00509_b200 import _native as N
+    for path, scale in zip(synth_sets, ((0.08, 1.0), (0.2, 1.0), (0.08, 1.0))):
+        with E.open_container(path) as h:
+            cfg = E.LoaderConfig(data=str(path), batch_size=32, res=160, scale=scale,
+                                 mask_ratio=0.75, keep_uint8=True)
+            loader = E.Loader(cfg, container=h)
+            loader.engine.set_option(N.ESSL_OPT_SEQ_BITS, seq_bits)
+            loader.engine.set_option(N.ESSL_OPT_OVERLAP_BITS, overlap)
+            for b in loader.epoch(3):
+                idx = b.indices.cpu().numpy()
+                pix, u8, mask, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 3, 160,
+                                                        scale=scale, mask_ratio=0.75,
+                                                        keep_uint8=True, nthreads=8)
+                assert (st == 0).all()
+                assert np.array_equal(b.pixels.cpu().numpy(), pix)
+                assert np.array_equal(b.uint8.cpu().numpy(), u8)
+                assert np.array_equal(b.mask.cpu().numpy(), mask)
+
+
+def test_staged_equals_resident(E, synth_sets):
+    path = synth_sets[0]
+    outs = []
+    for resident in (True, False):
+        cfg = E.LoaderConfig(data=str(path), batch_size=40, res=224, out_dtype="bfloat16",
+                             resident=resident, prefetch=3)
+        with E.Loader(cfg) as loader:
+            outs.append([sha(b.pixels) for b in loader.epoch(1)])
+    assert outs[0] == outs[1]
+
+
+def test_ddp_shards_cover_epoch(E, synth_sets):
+    path = synth_sets[2]
+    seen = {}
+    for r in range(3):
+        cfg = E.LoaderConfig(data=str(path), batch_size=7, res=64, rank=r, world_size=3)
+        with E.Loader(cfg) as loader:
+            for b in loader.epoch(2):
+                for s in range(len(b)):
+                    seen[int(b.indices[s])] = sha(b.pixels[s])
+    cfg = E.LoaderConfig(data=str(path), batch_size=7, res=64)
+    with E.Loader(cfg) as loader:
+        full = {int(b.indices[s]): sha(b.pixels[s]) for b in loader.epoch(2) for s in range(len(b))}
+    assert seen == full
