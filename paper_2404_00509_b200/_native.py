@@ -21,7 +21,7 @@ KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs")
 # Every symbol include/essl.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "essl_ctx_create", "essl_ctx_destroy", "essl_ctx_set_option", "essl_ctx_launch_count",
-    "essl_ctx_profile_read",
+    "essl_ctx_profile_read", "essl_debug_stats",
     "essl_last_error", "essl_version", "essl_stage", "essl_decode_rrc", "essl_decode_crop_u8",
     "essl_dump_coefs", "essl_mask", "essl_mask_from_states", "essl_gather_visible", "essl_resize_u8",
     "essl_normalize_u8", "essl_rng_init", "essl_rng_next", "essl_rng_random",
@@ -85,6 +85,7 @@ def lib():
         "essl_ctx_set_option": (i32, [P, i32, i64]),
         "essl_ctx_launch_count": (i64, [P]),
         "essl_ctx_profile_read": (i32, [P, P, P]),
+        "essl_debug_stats": (i32, [P, P, i32]),
         "essl_last_error": (ctypes.c_char_p, []),
         "essl_version": (ctypes.c_char_p, []),
         "essl_stage": (i32, [P, i32, P, P, i32, P, i32, P, P]),

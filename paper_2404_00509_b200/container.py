@@ -155,8 +155,11 @@ class ContainerHandle:
         key = str(device)
         t = self._dev.get(key)
         if t is None:
-            host = torch.from_numpy(np.array(self.bytes, copy=False)) if self._size else \
-                torch.zeros(1, dtype=torch.uint8)
+            import warnings
+            with warnings.catch_warnings():  # read-only mmap: the copy never writes it
+                warnings.simplefilter("ignore", UserWarning)
+                host = torch.frombuffer(self._mmap, dtype=torch.uint8) if self._size else \
+                    torch.zeros(1, dtype=torch.uint8)
             t = torch.empty(max(self._size, 1), dtype=torch.uint8, device=device)
             chunk = 1 << 28
             for s in range(0, self._size, chunk):

@@ -108,9 +108,12 @@ int pick_desc(essl_ctx *c, const essl_sample *samples, int n, cudaStream_t st,
 int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
                essl_result *results, cudaStream_t st, int *ring) {
   if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
-  for (int i = 0; i < n; i++)
+  int max_len = 0;
+  for (int i = 0; i < n; i++) {
     if ((int)samples[i].length > c->max_payload)
       return fail(ESSL_E_CAPACITY, "payload larger than context max_payload");
+    max_len = std::max(max_len, (int)samples[i].length);
+  }
   essl_sample *d_desc = nullptr;
   int r = pick_desc(c, samples, n, st, &d_desc);
   if (r < 0) return r;
@@ -127,7 +130,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   p.results = results;
   {
     Prof pr(c, ESSL_K_DECODE, st);
-    essl::launch_decode(p, st);
+    essl::launch_decode(p, st, max_len);
   }
   CK(cudaGetLastError());
   return ESSL_OK;
@@ -242,6 +245,14 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
 }
 
 int64_t essl_ctx_launch_count(const essl_ctx *c) { return c ? c->launches.load() : -1; }
+
+int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
+  if (!c || !out || n < 0 || n > c->max_batch) return fail(ESSL_E_ARG, "essl_debug_stats: bad arguments");
+  std::vector<essl::ImgInfo> info(n);
+  CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; i++) std::memcpy(out + 12 * i, info[i].dbg, 12 * sizeof(int64_t));
+  return ESSL_OK;
+}
 
 int essl_ctx_profile_read(essl_ctx *c, double *ms, int64_t *count) {
   if (!c || !ms || !count) return fail(ESSL_E_ARG, "essl_ctx_profile_read: bad arguments");

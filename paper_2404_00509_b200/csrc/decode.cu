@@ -6,18 +6,26 @@
 //   jpeg/codec.py:323-330  _check_consumed
 //   jpeg/decode_kernels.py:388-534 reconstruct_blocks (crop window only)
 //
+// Layout: the compressed payload is staged into shared memory with 16-byte
+// loads and destuffed into a second shared buffer; every later phase (CRC,
+// marker parse, Huffman decode) reads shared memory only.  Payloads too
+// large for shared memory use the same code on global memory (SMEM=false).
+//
 // Entropy decoding of a restart-free baseline scan is inherently serial; it
 // is parallelised inside the CTA by self-synchronising speculative decode:
-// the clean bitstream is cut into <=256 subsequences, thread t decodes
-// subsequence t from a guessed state (warm-up of `overlap_bits` before the
-// boundary), then a fixpoint pass re-decodes every subsequence whose entry
-// state disagrees with its predecessor's exit state.  Entry states are
-// proven correct by induction from the exact start, after
-// which a prefix scan over per-subsequence block counts / DC sums gives each
-// thread its absolute block index and DC predictors, and a final pass writes
-// coefficients of crop-window blocks only, stopping at the last MCU row the
-// crop needs (codec.py:483-500 row_stop).  Streams with restart intervals
-// (DRI) are decoded one interval per thread (exact entry states).
+// the clean bitstream is cut into <=256 subsequences; thread t guesses its
+// entry state by decoding `overlap_bits` before its boundary from a guessed
+// state (k=0, first block of an MCU; impossible codes re-guess one bit
+// later), decodes its subsequence counting blocks and DC differences, then a
+// fixpoint pass re-decodes every subsequence whose entry state differs from
+// its predecessor's exit state.  At the fixpoint every entry state up to the
+// first true error equals the exit state of a verified predecessor, so by
+// induction from the exact start all entry states are the reference decoder's
+// states.  A prefix scan gives each subsequence its absolute
+// block index and DC predictors, and a final pass writes coefficients of
+// crop-window blocks only, stopping at the last MCU row the crop needs
+// (codec.py:483-500 row_stop).  Streams with restart intervals (DRI) are
+// decoded one interval per thread (exact entry states).
 #include <cstdint>
 
 #include "essl_common.cuh"
@@ -33,8 +41,9 @@ __constant__ uint8_t c_zz[64] = {
 // x^(2^k) mod P (reflected CRC-32), k = 0..31; filled by init_crc_tables().
 __constant__ uint32_t c_x2n[32];
 
-constexpr uint32_t kErrP = 0xFFFFFFFFu;  // "error / dead" exit state marker
+constexpr uint32_t kErrP = 0xFFFFFFFFu;  // error exit-state marker
 constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
+constexpr int kNT = kDecodeThreads;
 
 struct HuffTab {
   uint16_t fast[1 << kFastBits];  // (sym << 4) | len, len in 1..kFastBits; 0 = slow path
@@ -42,15 +51,16 @@ struct HuffTab {
   int32_t first[17];
   int16_t vptr[17];
   uint8_t vals[256];
+  int dht_pos, nvals;  // where the DHT symbols live in the payload
 };
 
 struct SeqRec {
   uint32_t gp, gkb;  // entry state: bit position, k | b << 8
-  uint32_t ep, ekb;  // exit state (ep == kErrP: error or dead)
+  uint32_t ep, ekb;  // exit state (ep == kErrP: decode error)
   uint32_t nblk;     // blocks completed inside the subsequence
   int32_t dc[3];     // sum of DC differences per scan slot
   uint32_t errblk, errp;
-  int32_t err;       // own decode error (1) / dead entry (2)
+  int32_t err;
 };
 
 struct ParseState {
@@ -65,33 +75,36 @@ struct ParseState {
 };
 
 struct __align__(16) Smem {
-  uint32_t crc_tab[256];
-  uint32_t crc_part[kDecodeThreads];
-  uint8_t hdr[kHdrCache];
+  union {
+    struct {
+      uint32_t T[4][256];  // slice-by-4 CRC tables
+      uint32_t part[kNT];
+    } crc;
+    int32_t idct_tr[kNT / 32][4][64];
+  } u;
   HuffTab tab[kMaxTables];
-  SeqRec seq[kDecodeThreads];
+  SeqRec seq[kNT];
   ParseState ps;
-  int32_t q[3][64];            // dequantisation tables, natural order
+  int32_t q[3][64];  // dequantisation tables, natural order
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
   int slot_dc[4], slot_ac[4];  // table index per slot
   int slot_comp[4], slot_h[4], slot_v[4];
-  int ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1;
+  int ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ntab;
   int wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
   uint64_t coef_off[3];
   uint64_t coef_base;
   uint32_t K[8];
-  uint32_t limit_blocks, clean_bits;
-  uint32_t clean_words;
+  uint32_t limit_blocks, clean_bits, clean_words;
   uint64_t clean_off;
-  uint32_t rst_off;  // word offset of the restart table inside the clean region
+  uint32_t rst_off;
   int n_restarts, max_restarts;
   int status, reason, offset;
   uint32_t p_final;
   int coef_range;
   int stop, red_i[2];
-  uint32_t scan_a[kDecodeThreads], scan_b[kDecodeThreads];
+  uint32_t warp_tot[kNT / 32][4];
   int changed;
-  int32_t idct_tr[kDecodeThreads / 32][4][64];
+  long long t_ph[12];
 };
 
 // ---------------------------------------------------------------------------
@@ -104,7 +117,7 @@ __device__ __forceinline__ int extend_bits(uint32_t v, int size) {  // decode_ke
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
   // a(x) * b(x) modulo the reflected CRC-32 polynomial (zlib multmodp).
   uint32_t p = 0;
-#pragma unroll 1
+#pragma unroll 4
   for (int i = 0; i < 32; i++) {
     if (a & (0x80000000u >> i)) p ^= b;
     b = (b & 1) ? (b >> 1) ^ 0xEDB88320u : b >> 1;
@@ -123,38 +136,49 @@ __device__ uint32_t x2nmodp(uint64_t n, int k) {  // x^(n * 2^k) mod P
 }
 
 __device__ __forceinline__ bool is_rst(uint32_t m) { return m >= 0xD0 && m <= 0xD7; }
+__device__ __forceinline__ bool has_ff(uint32_t w) { return __vcmpeq4(w, 0xFFFFFFFFu) != 0; }
 
-// Block-wide exclusive scan of two u32 values (256 threads).
-__device__ void block_scan2(Smem &S, uint32_t &a, uint32_t &b, uint32_t &ta, uint32_t &tb) {
-  const int tid = threadIdx.x;
-  S.scan_a[tid] = a;
-  S.scan_b[tid] = b;
-  __syncthreads();
-#pragma unroll 1
-  for (int off = 1; off < kDecodeThreads; off <<= 1) {
-    uint32_t va = tid >= off ? S.scan_a[tid - off] : 0;
-    uint32_t vb = tid >= off ? S.scan_b[tid - off] : 0;
-    __syncthreads();
-    S.scan_a[tid] += va;
-    S.scan_b[tid] += vb;
-    __syncthreads();
+// Block-wide exclusive scan of four u32 values (kNT threads, warp shuffles).
+// Returns the block totals in tot[].
+__device__ void block_scan4(Smem &S, uint32_t v[4], uint32_t tot[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t x = v[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    inc[q] = x;
   }
-  ta = S.scan_a[kDecodeThreads - 1];
-  tb = S.scan_b[kDecodeThreads - 1];
-  a = S.scan_a[tid] - a;  // exclusive
-  b = S.scan_b[tid] - b;
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) S.warp_tot[warp][q] = inc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    uint32_t before = 0, all = 0;
+    for (int w = 0; w < kNT / 32; w++) {
+      const uint32_t t = S.warp_tot[w][q];
+      if (w < warp) before += t;
+      all += t;
+    }
+    v[q] = inc[q] - v[q] + before;
+    tot[q] = all;
+  }
   __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
 // header parse (thread 0), codec.py:124-251
 
-struct PayloadView {
-  const uint8_t *g;
+struct PayloadView {  // the payload bytes (shared or global memory)
+  const uint8_t *d;
   int n;
-  const uint8_t *hdr;
-  int hdr_n;
-  __device__ __forceinline__ int operator[](int i) const { return i < hdr_n ? hdr[i] : g[i]; }
+  __device__ __forceinline__ int operator[](int i) const { return d[i]; }
 };
 
 __device__ void parse_fail(ParseState &P, int reason, int off) {
@@ -279,19 +303,19 @@ __device__ void parse_until_sos(ParseState &P, const PayloadView &d) {
 // entropy decoding
 
 struct BitReader {
-  const uint32_t *w;
-  uint32_t nw;
-  uint64_t buf;
-  int n;
-  uint32_t wi;
-  uint32_t p;
+  const uint32_t *w;  // big-endian byte stream as words (smem or global)
+  uint32_t nw;        // words holding data (+0xFF padding); beyond -> 0xFFFFFFFF
+  uint64_t buf;       // left-aligned bit buffer
+  int n;              // valid bits in buf
+  uint32_t wi;        // next word to load
+  uint32_t p;         // absolute bit position of buf's MSB
   __device__ __forceinline__ uint32_t load(uint32_t i) const {
-    return i < nw ? __byte_perm(__ldg(w + i), 0, 0x0123) : 0xFFFFFFFFu;
+    return i < nw ? __byte_perm(w[i], 0, 0x0123) : 0xFFFFFFFFu;
   }
   __device__ __forceinline__ void init(uint32_t pos) {
     wi = pos >> 5;
     const int off = pos & 31;
-    uint64_t a = load(wi), b = load(wi + 1);
+    const uint64_t a = load(wi), b = load(wi + 1);
     buf = ((a << 32) | b) << off;
     n = 64 - off;
     wi += 2;
@@ -340,13 +364,19 @@ struct RunState {
   int coef_range;
 };
 
-// Decode units from (p0, k0, b0) while p < end_bit.  WRITE additionally tracks
-// the absolute block index (stopping at `limit`), DC predictors and stores the
-// crop-window coefficients (natural order) to `coef`.
-template <bool WRITE>
+enum { RUN_COUNT = 0, RUN_WRITE = 1, RUN_GUESS = 2 };
+
+// Decode units from (p0, k0, b0) while p < end_bit (decode_kernels.py:139-177).
+//  RUN_COUNT: count completed blocks and DC differences; stop at an error.
+//  RUN_GUESS: speculative warm-up; an impossible code re-guesses (k=0, b=0)
+//             one bit after the failing unit's start.
+//  RUN_WRITE: also track the absolute block index (stop at `limit`), DC
+//             predictors, and store crop-window coefficients (natural order).
+template <int MODE>
 __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, int k0, int b0,
                            uint32_t end_bit, RunState &o, uint32_t blk, uint32_t limit,
                            int32_t *pred, int16_t *coef, uint32_t *p_final) {
+  constexpr bool WRITE = MODE == RUN_WRITE;
   BitReader br;
   br.w = words;
   br.nw = S.clean_words;
@@ -356,7 +386,6 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
   int32_t dc0 = 0, dc1 = 0, dc2 = 0;
   o.err = 0;
   o.coef_range = 0;
-  // WRITE-mode block cursor
   int mx = 0, my = 0;
   int16_t *cur = nullptr;
   auto locate = [&]() {
@@ -381,47 +410,52 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
     br.refill();
     const uint32_t ustart = br.p;
     const int s = S.blk_slot[b];
-    if (k == 0) {
-      const int sym = decode_sym(S.tab[S.slot_dc[s]], br);
-      if (sym < 0 || sym > 15) {
-        o.err = 1; o.errblk = nblk; o.errp = ustart;
-        break;
-      }
-      int diff = 0;
-      if (sym) {
-        diff = extend_bits(br.peek(sym), sym);
-        br.skip(sym);
-      }
-      if (s == 0) dc0 += diff; else if (s == 1) dc1 += diff; else dc2 += diff;
-      if (WRITE) {
-        const int32_t v = pred[s] + diff;
-        pred[s] = v;
-        if (cur) {
-          if (v < -32768 || v > 32767) o.coef_range = 1;
-          cur[0] = (int16_t)v;
+    const bool dc = k == 0;
+    const HuffTab &T = S.tab[dc ? S.slot_dc[s] : S.slot_ac[s]];
+    const int sym = decode_sym(T, br);
+    const int size = dc ? sym : (sym & 15);
+    const int run = dc ? 0 : (sym >> 4);
+    bool bad = sym < 0 || (dc && sym > 15);
+    int v = 0;
+    if (!bad && size) {
+      v = extend_bits(br.peek(size), size);
+      br.skip(size);
+    }
+    if (!bad) {
+      if (dc) {
+        if (s == 0) dc0 += v; else if (s == 1) dc1 += v; else dc2 += v;
+        if (WRITE) {
+          const int32_t pv = pred[s] + v;
+          pred[s] = pv;
+          if (cur) {
+            if (pv < -32768 || pv > 32767) o.coef_range = 1;
+            cur[0] = (int16_t)pv;
+          }
         }
-      }
-      k = 1;
-    } else {
-      const int rs = decode_sym(S.tab[S.slot_ac[s]], br);
-      if (rs < 0) {
-        o.err = 1; o.errblk = nblk; o.errp = ustart;
-        break;
-      }
-      const int r = rs >> 4, sz = rs & 15;
-      if (sz == 0) {
-        k = (r == 15) ? k + 16 : 64;
+        k = 1;
+      } else if (size == 0) {
+        k = (run == 15) ? k + 16 : 64;
       } else {
-        k += r;
+        k += run;
         if (k > 63) {
-          o.err = 1; o.errblk = nblk; o.errp = ustart;
-          break;
+          bad = true;
+        } else {
+          if (WRITE && cur) cur[c_zz[k]] = (int16_t)v;
+          k++;
         }
-        const int v = extend_bits(br.peek(sz), sz);
-        br.skip(sz);
-        if (WRITE && cur) cur[c_zz[k]] = (int16_t)v;
-        k++;
       }
+    }
+    if (bad) {
+      if (MODE == RUN_GUESS) {
+        k = 0;
+        b = 0;
+        br.init(ustart + 1);
+        continue;
+      }
+      o.err = 1;
+      o.errblk = nblk;
+      o.errp = ustart;
+      break;
     }
     if (k >= 64) {
       k = 0;
@@ -429,9 +463,7 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
       b = (b + 1 == S.bpm) ? 0 : b + 1;
       if (WRITE) {
         blk++;
-        if (b == 0) {
-          if (++mx == S.gx) { mx = 0; my++; }
-        }
+        if (b == 0 && ++mx == S.gx) { mx = 0; my++; }
         if (blk == S.limit_blocks && p_final) *p_final = br.p;
         locate();
       }
@@ -445,7 +477,7 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
 }
 
 // ---------------------------------------------------------------------------
-// IDCT, decode_kernels.py:388-534 (int64 islow, exact)
+// IDCT, decode_kernels.py:388-534 (islow, exact)
 
 #define F_0_298631336 2446
 #define F_0_390180644 3196
@@ -591,7 +623,7 @@ __device__ void idct_block_8lanes(bool valid, const int16_t *coef, const int32_t
 
 // ---------------------------------------------------------------------------
 
-__device__ void set_status(Smem &S, int st, int reason, int off) {
+__device__ __forceinline__ void set_status(Smem &S, int st, int reason, int off) {
   if (S.status == 0) {
     S.status = st;
     S.reason = reason;
@@ -599,86 +631,130 @@ __device__ void set_status(Smem &S, int st, int reason, int off) {
   }
 }
 
-__global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
+__device__ __forceinline__ int corrupt_offset(const ParseState &PS, uint32_t errp) {
+  // _check_consumed: scan.start + min(vpos, seglen); the reference's reader
+  // keeps >= 25 bits buffered, so vpos = ceil((p + 25) / 8) at the failing unit.
+  const uint32_t seglen = (uint32_t)(PS.scan_end - PS.scan_start);
+  const uint32_t vpos = (errp + 25 + 7) / 8;
+  return PS.scan_start + (int)min(vpos, seglen);
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
+  extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ Smem S;
+#define PHASE(i) do { if (threadIdx.x == 0) S.t_ph[i] = clock64(); } while (0)
   const int img = blockIdx.x;
   const int tid = threadIdx.x;
   const essl_sample smp = P.samples[img];
   const uint8_t *g = P.blob + smp.offset;
   const int n = (int)smp.length;
+  const int n_pad = (n + 15) / 16 * 16 + 16;
   ImgInfo *info = P.s.info + img;
+  const uint8_t *raw = SMEM ? dyn : g;
+  PayloadView pv{raw, n};
 
+  if (tid < 12) S.t_ph[tid] = 0;
   if (tid == 0) {
     S.status = 0; S.reason = 0; S.offset = -1;
     S.coef_range = 0;
     S.p_final = kNoEnd;
   }
-  // ---- stage header prefix, CRC table -------------------------------------
-  const int hdr_n = n < kHdrCache ? n : kHdrCache;
-  for (int i = tid; i < hdr_n; i += kDecodeThreads) S.hdr[i] = g[i];
+  PHASE(0);
+  // ---- stage the payload into shared memory (16-byte loads) ----------------
+  if (SMEM) {
+    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+      const int n16 = n / 16;
+      const int4 *src = reinterpret_cast<const int4 *>(g);
+      int4 *dst = reinterpret_cast<int4 *>(dyn);
+      for (int i = tid; i < n16; i += kNT) dst[i] = __ldg(src + i);
+      for (int i = n16 * 16 + tid; i < n; i += kNT) dyn[i] = g[i];
+    } else {
+      for (int i = tid; i < n; i += kNT) dyn[i] = g[i];
+    }
+    for (int i = n + tid; i < n_pad; i += kNT) dyn[i] = 0;
+  }
+  // CRC tables (slice-by-4)
   {
     uint32_t c = tid;
 #pragma unroll
     for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-    S.crc_tab[tid] = c;
+    S.u.crc.T[0][tid] = c;
+  }
+  __syncthreads();
+  {
+    uint32_t c = S.u.crc.T[0][tid];
+#pragma unroll
+    for (int t = 1; t < 4; t++) {
+      c = (c >> 8) ^ S.u.crc.T[0][c & 0xFF];
+      S.u.crc.T[t][tid] = c;
+    }
   }
   __syncthreads();
 
+  PHASE(1);
   // ---- CRC32 (container.py:263) -------------------------------------------
-  // End-aligned chunks of L bytes (zero-padded at the front: leading zeros do
-  // not change a zero-init CRC); the 0xFFFFFFFF init is applied by
-  // complementing the first 4 message bytes; chunks combine in a tree with
-  // multiplication by x^(8 L 2^j).
+  // The message is viewed as 256 chunks of L bytes (L % 4 == 0) with zeros
+  // prepended (leading zeros do not change a zero-init CRC); the 0xFFFFFFFF
+  // init is applied by complementing the first 4 message bytes; chunk CRCs
+  // combine in a tree with multiplication by x^(8 L 2^j) mod P.
   if (smp.check_crc) {
-    uint32_t crc;
+    uint32_t crc = 0;
     if (n < 4) {
-      crc = 0;
       if (tid == 0) {
         uint32_t c = 0xFFFFFFFFu;
-        for (int i = 0; i < n; i++) c = S.crc_tab[(c ^ g[i]) & 0xFF] ^ (c >> 8);
+        for (int i = 0; i < n; i++) c = S.u.crc.T[0][(c ^ raw[i]) & 0xFF] ^ (c >> 8);
         crc = c ^ 0xFFFFFFFFu;
       }
     } else {
-      const int L = (n + kDecodeThreads - 1) / kDecodeThreads;
-      const int start = n - (kDecodeThreads - tid) * L;
+      const int L = ((n + kNT - 1) / kNT + 3) & ~3;
+      const int pad = kNT * L - n;
       uint32_t c = 0;
-      for (int i = start < 0 ? 0 : start; i < start + L; i++) {
-        uint32_t byte = i < hdr_n ? S.hdr[i] : g[i];
-        if (i < 4) byte ^= 0xFF;
-        c = S.crc_tab[(c ^ byte) & 0xFF] ^ (c >> 8);
+      for (int j = 0; j < L; j += 4) {
+        const int rp = tid * L + j - pad;
+        uint32_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int r = rp + b;
+          uint32_t byte = (r >= 0 && r < n) ? raw[r] : 0u;
+          if (r >= 0 && r < 4) byte ^= 0xFF;
+          w |= byte << (8 * b);
+        }
+        c ^= w;
+        c = S.u.crc.T[3][c & 0xFF] ^ S.u.crc.T[2][(c >> 8) & 0xFF] ^
+            S.u.crc.T[1][(c >> 16) & 0xFF] ^ S.u.crc.T[0][c >> 24];
       }
-      S.crc_part[tid] = c;
+      S.u.crc.part[tid] = c;
       if (tid < 8) S.K[tid] = x2nmodp((uint64_t)L << tid, 3);
       __syncthreads();
 #pragma unroll 1
-      for (int j = 0; (1 << j) < kDecodeThreads; j++) {
+      for (int j = 0; (1 << j) < kNT; j++) {
         const int stride = 1 << j;
         uint32_t v = 0;
         const bool act = (tid % (2 * stride)) == 0;
-        if (act) {
-          v = multmodp(S.K[j], S.crc_part[tid]) ^ S.crc_part[tid + stride];
-        }
+        if (act) v = multmodp(S.K[j], S.u.crc.part[tid]) ^ S.u.crc.part[tid + stride];
         __syncthreads();
-        if (act) S.crc_part[tid] = v;
+        if (act) S.u.crc.part[tid] = v;
         __syncthreads();
       }
-      crc = S.crc_part[0] ^ 0xFFFFFFFFu;
+      crc = S.u.crc.part[0] ^ 0xFFFFFFFFu;
     }
     if (tid == 0 && crc != smp.crc32) set_status(S, ESSL_ST_CRC, 0, -1);
   }
   __syncthreads();
 
+  PHASE(2);
   // ---- parse (thread 0) + parallel entropy-segment end search --------------
   ParseState &PS = S.ps;
   if (tid == 0) {
     PS.pos = 2; PS.n = n; PS.ri = 0; PS.have_sof = 0; PS.progressive = 0;
     PS.ncomp = 0; PS.nscans = 0; PS.status = 0; PS.cmd = 0; PS.ns = 0;
+    PS.scan_start = 0; PS.scan_end = 0; PS.scan_ri = 0;
     for (int i = 0; i < 16; i++) { PS.quant_pos[i] = -1; PS.huff_pos[0][i] = -1; PS.huff_pos[1][i] = -1; }
-    if (n < 4 || S.hdr[0] != 0xFF || S.hdr[1] != 0xD8) parse_fail(PS, R_NO_SOI, 0);
-    else PS.cmd = 3;  // "continue"
+    if (n < 4 || raw[0] != 0xFF || raw[1] != 0xD8) parse_fail(PS, R_NO_SOI, 0);
+    else PS.cmd = 3;  // continue
   }
   __syncthreads();
-  PayloadView pv{g, n, S.hdr, hdr_n};
   if (S.status == 0) {
 #pragma unroll 1
     while (true) {
@@ -690,14 +766,19 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       if (tid == 0) S.stop = n;
       __syncthreads();
       const int d0 = PS.dstart;
-      const int span = n - d0;
-      const int per = (span + kDecodeThreads - 1) / kDecodeThreads;
+      const int per = ((n - d0 + kNT - 1) / kNT + 3) & ~3;
       const int a = d0 + tid * per, e = min(a + per, n - 1);
-      for (int i = a; i < e; i++) {
-        if (pv[i] == 0xFF) {
-          const int m = pv[i + 1];
+      for (int i = a; i < e;) {
+        if (SMEM && (i & 3) == 0 && i + 4 <= e &&
+            !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
+          i += 4;
+          continue;
+        }
+        if (raw[i] == 0xFF) {
+          const int m = raw[i + 1];
           if (!(m == 0x00 || is_rst(m) || m == 0xFF)) { atomicMin(&S.stop, i); break; }
         }
+        i++;
       }
       __syncthreads();
       if (tid == 0) {
@@ -732,7 +813,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       info->comp_h[i] = i < PS.ncomp ? PS.comp_h[i] : 1;
       info->comp_v[i] = i < PS.ncomp ? PS.comp_v[i] : 1;
     }
-    int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
+    const int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
     if (w < 1 || h < 1 || x < 0 || y < 0 || x + w > W || y + h > H) {
       set_status(S, ESSL_ST_RECT, 0, -1);
     } else if (PS.progressive) {
@@ -771,7 +852,6 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       S.limit_blocks = (uint32_t)S.row_stop * S.gx * bpm;
       info->mcus_entropy = S.row_stop * S.gx;
       info->mcus_recon = (S.my1 - S.my0 + 1) * (S.mx1 - S.mx0 + 1);
-      // per-component window (full MCU extents), codec.py:502-508
       uint64_t total = 0;
       for (int c = 0; c < 3; c++) { S.wbh[c] = 0; S.wbw[c] = 0; S.wby0[c] = 0; S.wbx0[c] = 0; }
       for (int s = 0; s < ns; s++) {
@@ -790,13 +870,13 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
         for (int c = 0; c < 3; c++) S.coef_off[c] += cbase;
         S.coef_base = cbase;
       }
-      // clean-bytes region: segment + padding + restart table
+      // global region: clean bytes (global variant) + restart table
       const int seglen = PS.scan_end - PS.scan_start;
       S.max_restarts = PS.scan_ri ? (S.gx * S.gy) / PS.scan_ri : 0;
       const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
-      const uint64_t clean_bytes = ((uint64_t)seglen + 16 + 15) / 16 * 16;
-      const uint64_t alloc = clean_bytes + 4ull * max_r + 16;
-      const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)((alloc + 15) / 16 * 16));
+      const uint64_t clean_bytes = SMEM ? 0 : ((uint64_t)seglen + 16 + 15) / 16 * 16;
+      const uint64_t alloc = (clean_bytes + 4ull * max_r + 16 + 15) / 16 * 16;
+      const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)alloc);
       if (base + alloc > P.s.clean_cap) set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
       S.clean_off = base;
       S.rst_off = (uint32_t)(clean_bytes / 4);
@@ -804,41 +884,70 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
   }
   __syncthreads();
 
-  // ---- destuff (decode_kernels.py:27-61) into the clean region --------------
-  uint8_t *clean = P.s.clean + S.clean_off;
+  // ---- dequantisation tables (values; the check happens after decoding) ----
+  if (S.status == 0) {
+    for (int e = tid; e < PS.ncomp * 64; e += kNT) {
+      const int c = e >> 6, k = e & 63;
+      const int tq = PS.comp_tq[c];
+      const int pos = tq <= 15 ? PS.quant_pos[tq] : -1;
+      int v = 0;
+      if (pos >= 0) v = PS.quant_pq[tq] == 1 ? ((raw[pos + 2 * k] << 8) | raw[pos + 2 * k + 1]) : raw[pos + k];
+      S.q[c][c_zz[k]] = v;
+    }
+  }
+
+  PHASE(3);
+  // ---- destuff (decode_kernels.py:27-61) ------------------------------------
+  uint8_t *gclean = P.s.clean + S.clean_off;
+  uint8_t *clean = SMEM ? dyn + n_pad : gclean;
+  uint32_t *rst_tab = reinterpret_cast<uint32_t *>(gclean) + S.rst_off;
   if (S.status == 0) {
     const int seg0 = PS.scan_start, seg1 = PS.scan_end;
     const int segn = seg1 - seg0;
-    const int per = (segn + kDecodeThreads - 1) / kDecodeThreads;
+    const int per = ((segn + kNT - 1) / kNT + 3) & ~3;
     const int a = seg0 + tid * per, e = min(a + per, seg1);
     if (tid == 0) S.stop = seg1;
     __syncthreads();
-    for (int i = a; i < e; i++) {
-      if (pv[i] == 0xFF) {
+    for (int i = a; i < e;) {
+      if (SMEM && (i & 3) == 0 && i + 4 <= e &&
+          !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
+        i += 4;
+        continue;
+      }
+      if (raw[i] == 0xFF) {
         if (i + 1 >= seg1) { atomicMin(&S.stop, i); break; }
-        const int m = pv[i + 1];
+        const int m = raw[i + 1];
         if (!(m == 0x00 || is_rst(m))) { atomicMin(&S.stop, i); break; }
       }
+      i++;
     }
     __syncthreads();
     const int stop = S.stop;
     const int e2 = min(e, stop);
-    uint32_t kept = 0, nrst = 0;
-    for (int i = a; i < e2; i++) {
-      const int v = pv[i];
-      const bool second = i > seg0 && pv[i - 1] == 0xFF;
-      const bool rst = v == 0xFF && is_rst(pv[i + 1]);
-      kept += (!second && !rst);
-      nrst += rst;
+    uint32_t cnt[4] = {0, 0, 0, 0}, tot[4];
+    for (int i = a; i < e2;) {
+      if (SMEM && (i & 3) == 0 && i + 4 <= e2) {
+        const uint32_t w = *reinterpret_cast<const uint32_t *>(raw + i);
+        if (!has_ff(w)) {
+          cnt[0] += 4 - (i > seg0 && raw[i - 1] == 0xFF);
+          i += 4;
+          continue;
+        }
+      }
+      const int v = raw[i];
+      const bool second = i > seg0 && raw[i - 1] == 0xFF;
+      const bool rst = v == 0xFF && is_rst(raw[i + 1]);
+      cnt[0] += (!second && !rst);
+      cnt[1] += rst;
+      i++;
     }
-    uint32_t tk, tr;
-    block_scan2(S, kept, nrst, tk, tr);
+    block_scan4(S, cnt, tot);
     const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
-    uint32_t *rst_tab = reinterpret_cast<uint32_t *>(clean) + S.rst_off;
+    uint32_t kept = cnt[0], nrst = cnt[1];
     for (int i = a; i < e2; i++) {
-      const int v = pv[i];
-      const bool second = i > seg0 && pv[i - 1] == 0xFF;
-      const bool rst = v == 0xFF && is_rst(pv[i + 1]);
+      const int v = raw[i];
+      const bool second = i > seg0 && raw[i - 1] == 0xFF;
+      const bool rst = v == 0xFF && is_rst(raw[i + 1]);
       if (rst) {
         if ((int)nrst < max_r) rst_tab[nrst] = kept;
         nrst++;
@@ -846,6 +955,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
         clean[kept++] = (uint8_t)v;
       }
     }
+    const uint32_t tk = tot[0], tr = tot[1];
     __syncthreads();
     if (tid < 16) clean[tk + tid] = 0xFF;  // 0xFF padding past the end (_br_fill)
     if (tid == 0) {
@@ -858,6 +968,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
   }
   __syncthreads();
 
+  PHASE(4);
   // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
   if (tid == 0 && S.status == 0) {
     int ntab = 0;
@@ -877,7 +988,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
           int code = 0, vi = 0;
           T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
           for (int L = 1; L <= 16; L++) {
-            const int cnt = pv[pos + L - 1];
+            const int cnt = raw[pos + L - 1];
             T.first[L] = code;
             T.vptr[L] = (int16_t)vi;
             if (cnt && code + cnt > (1 << L)) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
@@ -886,26 +997,39 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
             T.lim[L] = code;
             code <<= 1;
           }
-          for (int v = 0; v < tot; v++) T.vals[v] = (uint8_t)pv[pos + 16 + v];
+          T.dht_pos = pos;
+          T.nvals = tot;
         }
         if (pass == 0) S.slot_dc[s] = ti; else S.slot_ac[s] = ti;
       }
     }
-    S.red_i[0] = ntab;
+    S.ntab = ntab;
   }
   __syncthreads();
   if (S.status == 0) {
-    const int ntab = S.red_i[0];
+    const int ntab = S.ntab;
+    for (int e = tid; e < ntab * 256; e += kNT) {
+      HuffTab &T = S.tab[e >> 8];
+      const int v = e & 255;
+      T.vals[v] = v < T.nvals ? (uint8_t)raw[T.dht_pos + 16 + v] : 0;
+    }
+    __syncthreads();
     for (int t = 0; t < ntab; t++) {
       HuffTab &T = S.tab[t];
-      for (int e = tid; e < (1 << kFastBits); e += kDecodeThreads) {
+      int lim[kFastBits + 1], first[kFastBits + 1], vptr[kFastBits + 1];
+#pragma unroll
+      for (int L = 1; L <= kFastBits; L++) {
+        lim[L] = T.lim[L];
+        first[L] = T.first[L];
+        vptr[L] = T.vptr[L];
+      }
+      for (int e = tid; e < (1 << kFastBits); e += kNT) {
         uint16_t ent = 0;
-        for (int L = 1; L <= kFastBits; L++) {
+#pragma unroll
+        for (int L = kFastBits; L >= 1; L--) {  // shortest match wins (prefix-free)
           const int c = e >> (kFastBits - L);
-          if (c < T.lim[L]) {
-            ent = (uint16_t)((T.vals[T.vptr[L] + c - T.first[L]] << 4) | L);
-            break;
-          }
+          if (c < lim[L] && c >= first[L])
+            ent = (uint16_t)((T.vals[vptr[L] + c - first[L]] << 4) | L);
         }
         T.fast[e] = ent;
       }
@@ -919,10 +1043,11 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
     for (int c = 0; c < 3; c++) total += (uint64_t)S.wbh[c] * S.wbw[c] * 64;
     int4 *z = reinterpret_cast<int4 *>(P.s.coef + S.coef_base);
     const uint64_t n16 = total / 8;
-    for (uint64_t i = tid; i < n16; i += kDecodeThreads) z[i] = make_int4(0, 0, 0, 0);
+    for (uint64_t i = tid; i < n16; i += kNT) z[i] = make_int4(0, 0, 0, 0);
   }
   __syncthreads();
 
+  PHASE(5);
   // ---- entropy decode ---------------------------------------------------------
   const uint32_t *words = reinterpret_cast<const uint32_t *>(clean);
   int16_t *coef = P.s.coef;
@@ -932,10 +1057,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
     const uint32_t ri = PS.scan_ri;
     const uint32_t lim_mcu = (uint32_t)S.row_stop * S.gx;
     const uint32_t nint = (lim_mcu + ri - 1) / ri;
-    const uint32_t *rst_tab = words + S.rst_off;
-    if (tid == 0) { S.red_i[0] = 0x7FFFFFFF; S.red_i[1] = 0; }
+    if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
     __syncthreads();
-    for (uint32_t j = tid; j < nint; j += kDecodeThreads) {
+    for (uint32_t j = tid; j < nint; j += kNT) {
       if (j >= 1 && (int)(j - 1) >= S.n_restarts) {  // status 3
         atomicMin(&S.red_i[0], (int)(2 * j + 1));
         continue;
@@ -945,7 +1069,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       RunState o;
       const uint32_t blk0 = j * ri * S.bpm;
       const uint32_t lim = min((j + 1) * ri, lim_mcu) * S.bpm;
-      decode_run<true>(S, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
+      decode_run<RUN_WRITE>(S, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
       if (o.err) atomicMin(&S.red_i[0], (int)(2 * j));
       if (o.coef_range) S.coef_range = 1;
     }
@@ -957,17 +1081,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
         if (code & 1) {
           set_status(S, ESSL_ST_MISSING_RST, 0, PS.scan_start);
         } else {
-          // recompute the erroring interval's error position on one thread
           const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
-          int32_t pred[3] = {0, 0, 0};
           RunState o;
-          decode_run<false>(S, words, p0, 0, 0, kNoEnd, o, j * ri * S.bpm,
-                            min((j + 1) * ri, lim_mcu) * S.bpm, pred, coef, nullptr);
-          // decode_run<false> has no block limit; the WRITE pass already proved
-          // an error inside the interval, so this run reaches it.
-          const int seglen = PS.scan_end - PS.scan_start;
-          const uint32_t vpos = (o.errp + 25 + 7) / 8;
-          set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
+          decode_run<RUN_COUNT>(S, words, p0, 0, 0, kNoEnd, o, 0, 0, nullptr, nullptr, nullptr);
+          set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
         }
       } else if (S.p_final != kNoEnd && S.p_final > S.clean_bits) {
         set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
@@ -977,21 +1094,17 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
     if (tid == 0) {
       int32_t pred[3] = {0, 0, 0};
       RunState o;
-      decode_run<true>(S, words, 0, 0, 0, kNoEnd, o, 0, S.limit_blocks, pred, coef, &S.p_final);
-      if (o.err) {
-        const int seglen = PS.scan_end - PS.scan_start;
-        const uint32_t vpos = (o.errp + 25 + 7) / 8;
-        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
-      } else if (S.p_final > S.clean_bits) {
-        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
-      }
+      decode_run<RUN_WRITE>(S, words, 0, 0, 0, kNoEnd, o, 0, S.limit_blocks, pred, coef,
+                            &S.p_final);
+      if (o.err) set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
+      else if (S.p_final > S.clean_bits) set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
       if (o.coef_range) S.coef_range = 1;
     }
   } else if (S.status == 0) {
     // ---- speculative parallel decode --------------------------------------
     const uint32_t cbits = S.clean_bits;
     int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
-    nseq = max(1, min(nseq, kDecodeThreads));
+    nseq = max(1, min(nseq, kNT));
     const uint32_t slen = (cbits + nseq - 1) / nseq;
     const uint32_t sbeg = tid * slen;
     const uint32_t send = tid == nseq - 1 ? cbits : min(cbits, (tid + 1) * slen);
@@ -1000,28 +1113,25 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       RunState o;
       uint32_t gp = 0;
       int gk = 0, gb = 0;
-      if (tid > 0) {
-        // warm-up from a guessed state (k=0, first block of an MCU)
-        uint32_t wp = sbeg > (uint32_t)P.overlap_bits ? sbeg - P.overlap_bits : 0;
-        int wk = 0, wb = 0;
-        while (true) {
-          decode_run<false>(S, words, wp, wk, wb, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
-          if (!o.err) break;
-          wp = o.errp + 1;  // re-guess after an impossible code
-          wk = 0; wb = 0;
-          if (wp >= sbeg) { o.p = sbeg; o.k = 0; o.b = 0; break; }
-        }
+      if (tid > 0) {  // warm-up from a guessed state
+        const uint32_t wp = sbeg > (uint32_t)P.overlap_bits ? sbeg - P.overlap_bits : 0;
+        decode_run<RUN_GUESS>(S, words, wp, 0, 0, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
         gp = o.p; gk = o.k; gb = o.b;
       }
-      decode_run<false>(S, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
+      decode_run<RUN_COUNT>(S, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
       R.gp = gp; R.gkb = gk | (gb << 8);
       R.ep = o.p; R.ekb = o.k | (o.b << 8);
       R.nblk = o.nblk;
       R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
       R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
     }
+    if (tid == 0) S.red_i[1] = 0;
     __syncthreads();
-    // fixpoint: re-decode subsequences whose entry != predecessor's exit
+    PHASE(6);
+    int n_iter = 0;
+    // fixpoint: re-decode subsequences whose entry differs from a valid
+    // predecessor exit (an erroring predecessor is left alone: it is either
+    // fixed later or it is the true error, past which nothing is needed)
 #pragma unroll 1
     for (int it = 0; it < nseq; it++) {
       uint32_t pp = 0, pkb = 0;
@@ -1029,46 +1139,41 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       if (tid > 0 && tid < nseq) {
         pp = S.seq[tid - 1].ep;
         pkb = S.seq[tid - 1].ekb;
-        redo = !(pp == R.gp && (pp == kErrP || pkb == R.gkb));
+        redo = pp != kErrP && !(pp == R.gp && pkb == R.gkb);
       }
       if (tid == 0) S.changed = 0;
       __syncthreads();
       if (redo) {
         S.changed = 1;
+        atomicAdd(&S.red_i[1], 1);
         R.gp = pp; R.gkb = pkb;
-        if (pp == kErrP) {
-          R.ep = kErrP; R.err = 2; R.nblk = 0;
-        } else {
-          RunState o;
-          decode_run<false>(S, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr, nullptr);
-          R.ep = o.p; R.ekb = o.k | (o.b << 8);
-          R.nblk = o.nblk;
-          R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
-          R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
-        }
+        RunState o;
+        decode_run<RUN_COUNT>(S, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr,
+                              nullptr);
+        R.ep = o.p; R.ekb = o.k | (o.b << 8);
+        R.nblk = o.nblk;
+        R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
+        R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
       }
       __syncthreads();
+      n_iter++;
       if (!S.changed) break;
     }
+    PHASE(7);
+    if (tid == 0) { S.t_ph[10] = n_iter; S.t_ph[11] = nseq | ((long long)S.red_i[1] << 32); }
     // prefix sums: block index and DC predictors at each subsequence entry
-    uint32_t my_entry = tid < nseq ? R.nblk : 0, zero = 0, tnb, tz;
-    block_scan2(S, my_entry, zero, tnb, tz);
-    uint32_t d0 = tid < nseq ? (uint32_t)R.dc[0] : 0, d1 = tid < nseq ? (uint32_t)R.dc[1] : 0;
-    uint32_t d2 = tid < nseq ? (uint32_t)R.dc[2] : 0, zero2 = 0;
-    block_scan2(S, d0, d1, tz, tz);
-    block_scan2(S, d2, zero2, tz, tz);
+    uint32_t v4[4] = {tid < nseq ? R.nblk : 0u, tid < nseq ? (uint32_t)R.dc[0] : 0u,
+                      tid < nseq ? (uint32_t)R.dc[1] : 0u, tid < nseq ? (uint32_t)R.dc[2] : 0u};
+    uint32_t t4[4];
+    block_scan4(S, v4, t4);
+    const uint32_t my_entry = v4[0], tnb = t4[0];
     if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
     __syncthreads();
     if (tid < nseq && R.err == 1) atomicMin(&S.red_i[0], tid);
     __syncthreads();
     const int tstar = S.red_i[0];  // first subsequence whose true path errors
-    if (tid == tstar) {
-      if (my_entry + R.errblk < S.limit_blocks) {  // the reference reaches it
-        const int seglen = PS.scan_end - PS.scan_start;
-        const uint32_t vpos = (R.errp + 25 + 7) / 8;  // _br_fill keeps >= 25 bits
-        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
-      }
-    }
+    if (tid == tstar && my_entry + R.errblk < S.limit_blocks)
+      set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, R.errp));
     __syncthreads();
     if (tid == 0 && S.status == 0 && tstar == 0x7FFFFFFF && tnb < S.limit_blocks) {
       // the data ends before the crop's last MCU row: continue serially into
@@ -1076,48 +1181,34 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
       const SeqRec &Lr = S.seq[nseq - 1];
       RunState o;
       int32_t pred[3] = {0, 0, 0};
-      decode_run<true>(S, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
-                       S.limit_blocks, pred, nullptr, nullptr);
-      if (o.err) {
-        const int seglen = PS.scan_end - PS.scan_start;
-        const uint32_t vpos = (o.errp + 25 + 7) / 8;
-        set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, PS.scan_start + (int)min(vpos, (uint32_t)seglen));
-      } else {
-        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
-      }
+      decode_run<RUN_WRITE>(S, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
+                            S.limit_blocks, pred, nullptr, nullptr);
+      if (o.err) set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
+      else set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
     }
     __syncthreads();
+    PHASE(8);
     // write pass: crop-window coefficients, stopping at row_stop
     if (S.status == 0 && tid < nseq && my_entry < S.limit_blocks && tid <= tstar) {
       RunState o;
-      int32_t pred[3] = {(int32_t)d0, (int32_t)d1, (int32_t)d2};
-      decode_run<true>(S, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
-                       S.limit_blocks, pred, coef, &S.p_final);
+      int32_t pred[3] = {(int32_t)v4[1], (int32_t)v4[2], (int32_t)v4[3]};
+      decode_run<RUN_WRITE>(S, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
+                            S.limit_blocks, pred, coef, &S.p_final);
       if (o.coef_range) S.coef_range = 1;
     }
     __syncthreads();
-    if (tid == 0 && S.status == 0) {
-      if (S.p_final != kNoEnd && S.p_final > S.clean_bits)
-        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
-    }
+    if (tid == 0 && S.status == 0 && S.p_final != kNoEnd && S.p_final > S.clean_bits)
+      set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
   }
   __syncthreads();
+  PHASE(9);
   if (tid == 0 && S.status == 0 && S.coef_range) set_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
 
-  // ---- quantisation tables (codec.py:405-409) -------------------------------
+  // ---- quantisation table check (codec.py:405-409) ---------------------------
   if (tid == 0 && S.status == 0) {
     for (int i = 0; i < PS.ncomp; i++) {
       const int tq = PS.comp_tq[i];
       if (tq > 15 || PS.quant_pos[tq] < 0) { set_status(S, ESSL_ST_QUANT, 0, tq); break; }
-    }
-  }
-  __syncthreads();
-  if (S.status == 0) {
-    for (int e = tid; e < PS.ncomp * 64; e += kDecodeThreads) {
-      const int c = e >> 6, k = e & 63;
-      const int tq = PS.comp_tq[c], pos = PS.quant_pos[tq];
-      const int v = PS.quant_pq[tq] == 1 ? ((pv[pos + 2 * k] << 8) | pv[pos + 2 * k + 1]) : pv[pos + k];
-      S.q[c][c_zz[k]] = v;
     }
   }
   __syncthreads();
@@ -1149,6 +1240,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
     info->offset = S.offset;
     info->rx = smp.x; info->ry = smp.y; info->rw = smp.w; info->rh = smp.h;
     info->flip = smp.flip;
+    for (int i = 0; i < 12; i++) info->dbg[i] = S.t_ph[i];
     if (P.results) {
       essl_result r;
       r.status = S.status; r.reason = S.reason; r.offset = S.offset;
@@ -1161,7 +1253,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
   __syncthreads();
   if (S.status != 0) return;
   // 4 blocks per warp, 8 lanes per block
-  int32_t *tr = S.idct_tr[tid >> 5][(tid >> 3) & 3];
+  int32_t *tr = S.u.idct_tr[tid >> 5][(tid >> 3) & 3];
   for (int c = 0; c < PS.ncomp; c++) {
     const int hb = min(S.wby0[c] + S.wbh[c], S.bh[c]) - S.wby0[c];
     const int wb = min(S.wbx0[c] + S.wbw[c], S.bw[c]) - S.wbx0[c];
@@ -1169,26 +1261,44 @@ __global__ void __launch_bounds__(kDecodeThreads, 2) k_decode(DecodeParams P) {
     const int pitch = S.wbw[c] * 8;
     uint8_t *plane = P.s.plane + info->plane_off[c];
     const int nblk = hb * wb;
-    const int rounds = (nblk + kDecodeThreads / 8 - 1) / (kDecodeThreads / 8);
+    const int rounds = (nblk + kNT / 8 - 1) / (kNT / 8);
     for (int rd = 0; rd < rounds; rd++) {
-      const int jb = rd * (kDecodeThreads / 8) + (tid >> 3);
+      const int jb = rd * (kNT / 8) + (tid >> 3);
       const bool valid = jb < nblk;
       const int byr = valid ? jb / wb : 0, bxr = valid ? jb % wb : 0;
       const int16_t *cf = coef + S.coef_off[c] + ((uint64_t)byr * S.wbw[c] + bxr) * 64;
       idct_block_8lanes(valid, cf, S.q[c], plane + (uint64_t)byr * 8 * pitch + bxr * 8, pitch, tr);
     }
   }
+#undef PHASE
 }
 
-void launch_decode(const DecodeParams &p, cudaStream_t st) {
+// Shared-memory budget for the payload + clean stream of one image.
+constexpr int kMaxDynSmem = 160 * 1024;
+
+int decode_dyn_smem(int max_len) {
+  const int n_pad = (max_len + 15) / 16 * 16 + 16;
+  return 2 * n_pad + 64;
+}
+
+void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len) {
   if (p.n <= 0) return;
-  k_decode<<<p.n, kDecodeThreads, 0, st>>>(p);
+  const int dyn = decode_dyn_smem(max_len);
+  if (dyn <= kMaxDynSmem) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+      attr = true;
+    }
+    k_decode<true><<<p.n, kNT, dyn, st>>>(p);
+  } else {
+    k_decode<false><<<p.n, kNT, 0, st>>>(p);
+  }
 }
 
 void init_crc_tables() {
   uint32_t x2n[32];
-  // x^1 in reflected form, then repeated squaring (zlib crc32.c x2n_table)
-  uint32_t p = 1u << 30;
+  uint32_t p = 1u << 30;  // x^1 (reflected), then repeated squaring (zlib x2n_table)
   auto mul = [](uint32_t a, uint32_t b) {
     uint32_t r = 0;
     for (int i = 0; i < 32; i++) {

@@ -39,6 +39,7 @@ struct ImgInfo {
   uint64_t coef_off[3];   // int16 elements into Scratch::coef
   int32_t mcus_entropy, mcus_recon;
   int32_t rx, ry, rw, rh, flip;
+  int64_t dbg[12];  // phase clocks / counters (essl_debug_stats)
 };
 
 // Device scratch owned by the context; per-image regions are carved with
@@ -94,7 +95,7 @@ __host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t ep
 }
 
 // launch wrappers (defined in the .cu files)
-void launch_decode(const DecodeParams &p, cudaStream_t st);
+void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);

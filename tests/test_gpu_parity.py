@@ -21,7 +21,11 @@ BF16_TOL = 1e-2
 
 def sha(a) -> str:
     if hasattr(a, "cpu"):
-        a = a.cpu().numpy()
+        import torch
+        a = a.cpu()
+        if a.dtype == torch.bfloat16:
+            a = a.view(torch.int16)
+        a = a.numpy()
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 

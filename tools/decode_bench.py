@@ -1,0 +1,88 @@
+"""Decode-kernel microbenchmark + per-phase clock breakdown (GPU).
+
+    python tools/decode_bench.py [--n 256] [--side 256] [--q 95] [--sweep]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+PHASES = ["setup", "crc", "parse", "destuff", "tables", "pass1", "fixpoint", "scan+tail",
+          "write", "idct"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--pool", type=int, default=1024)
+    ap.add_argument("--side", type=int, default=256)
+    ap.add_argument("--q", type=int, default=95)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2404_00509_b200 as E
+    from paper_2404_00509_b200 import _native as N
+    d = Path(tempfile.mkdtemp())
+    path = d / "pool.essl"
+    E.build_synthetic(path, args.pool, args.side, args.q, seed=3)
+    cfg = E.LoaderConfig(data=str(path), batch_size=args.n, res=224, out_dtype="bfloat16",
+                         mask_ratio=0.75)
+    loader = E.Loader(cfg)
+    eng = loader.engine
+    perm = E.epoch_permutation(0, 0, len(loader.handle))
+    settings = [("spec", 1024, 1024)]
+    if args.sweep:
+        settings = [("serial", 0, 0)] + [("spec", s, o) for s in (512, 1024, 2048, 4096)
+                                         for o in (0, 512, 1024, 2048)]
+    results = []
+    for mode, sb, ov in settings:
+        eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if mode == "serial"
+                       else N.ESSL_DECODE_SPECULATIVE)
+        if mode == "spec":
+            eng.set_option(N.ESSL_OPT_SEQ_BITS, sb)
+            eng.set_option(N.ESSL_OPT_OVERLAP_BITS, ov)
+        idx = perm[:args.n]
+        loader.finish(loader.enqueue(0, idx))  # warm
+        eng.set_option(N.ESSL_OPT_PROFILE, 1)
+        eng.profile_read()
+        for r in range(args.reps):
+            loader.finish(loader.enqueue(0, perm[(r * args.n) % len(perm):][:args.n]))
+        prof = eng.profile_read()
+        eng.set_option(N.ESSL_OPT_PROFILE, 0)
+        dbg = np.zeros(12 * args.n, np.int64)
+        N.check(N.lib().essl_debug_stats(eng._ctx, N.ptr(dbg), args.n))
+        dbg = dbg.reshape(args.n, 12)
+        ph = np.diff(dbg[:, :10], axis=1)  # cycles per phase
+        ph = np.concatenate([ph, np.zeros((args.n, 1), np.int64)], axis=1)
+        iters = dbg[:, 10]
+        nseq = dbg[:, 11] & 0xFFFFFFFF
+        redo = dbg[:, 11] >> 32
+        row = {"mode": mode, "seq_bits": sb, "overlap": ov,
+               "decode_ms": prof["decode"][0] / prof["decode"][1],
+               "resize_ms": prof.get("resize", (0, 1))[0] / max(prof.get("resize", (0, 1))[1], 1),
+               "phase_kcycles_median": {PHASES[i + 1]: float(np.median(ph[:, i])) / 1e3
+                                        for i in range(8)},
+               "phase_kcycles_max": {PHASES[i + 1]: float(np.max(ph[:, i])) / 1e3 for i in range(8)},
+               "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
+               "nseq_mean": float(nseq.mean()), "redo_frac": float(redo.sum() / max(nseq.sum(), 1))}
+        results.append(row)
+        print(json.dumps(row), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(results, indent=1))
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
