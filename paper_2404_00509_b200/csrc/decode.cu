@@ -46,7 +46,7 @@ constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
 constexpr int kNT = kDecodeThreads;
 
 struct HuffTab {
-  uint16_t fast[1 << kFastBits];  // (sym << 4) | len, len in 1..kFastBits; 0 = slow path
+  uint16_t fast[1 << kFastBits];  // (sym << 5) | len, len in 1..kFastBits; 0 = slow path
   int32_t lim[17];                // first[L] + count[L]
   int32_t first[17];
   int16_t vptr[17];
@@ -88,7 +88,9 @@ struct __align__(16) Smem {
   int32_t q[3][64];  // dequantisation tables, natural order
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
   int slot_dc[4], slot_ac[4];  // table index per slot
-  int slot_comp[4], slot_h[4], slot_v[4];
+  int slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
+  uint32_t tab_index_word;
+  uint8_t zz[64];
   int ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ntab;
   int wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
   uint64_t coef_off[3];
@@ -307,25 +309,27 @@ struct BitReader {
   uint32_t nw;        // words holding data (+0xFF padding); beyond -> 0xFFFFFFFF
   uint64_t buf;       // left-aligned bit buffer
   int n;              // valid bits in buf
-  uint32_t wi;        // next word to load
+  uint32_t wi;        // index of `nextw`
+  uint32_t nextw;     // prefetched next word (hides the load latency)
   uint32_t p;         // absolute bit position of buf's MSB
   __device__ __forceinline__ uint32_t load(uint32_t i) const {
     return i < nw ? __byte_perm(w[i], 0, 0x0123) : 0xFFFFFFFFu;
   }
   __device__ __forceinline__ void init(uint32_t pos) {
-    wi = pos >> 5;
+    const uint32_t i = pos >> 5;
     const int off = pos & 31;
-    const uint64_t a = load(wi), b = load(wi + 1);
+    const uint64_t a = load(i), b = load(i + 1);
     buf = ((a << 32) | b) << off;
     n = 64 - off;
-    wi += 2;
+    wi = i + 2;
+    nextw = load(wi);
     p = pos;
   }
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      buf |= (uint64_t)load(wi) << (32 - n);
-      wi++;
+      buf |= (uint64_t)nextw << (32 - n);
       n += 32;
+      nextw = load(++wi);
     }
   }
   __device__ __forceinline__ uint32_t peek(int bits) const { return (uint32_t)(buf >> (64 - bits)); }
@@ -336,22 +340,16 @@ struct BitReader {
   }
 };
 
-__device__ __forceinline__ int decode_sym(const HuffTab &T, BitReader &br) {
-  const uint32_t e = T.fast[br.peek(kFastBits)];
-  if (e & 15) {
-    br.skip(e & 15);
-    return (int)(e >> 4);
-  }
-  const int code = (int)br.peek(16);
+// Slow path of the Huffman decode: codes longer than kFastBits
+// (canonical maxcode walk, same symbols as the 16-bit LUT of
+// codec.py:272-295).  Returns (sym << 5) | len, or 0 for an invalid code.
+__device__ __noinline__ uint32_t decode_slow(const HuffTab &T, uint32_t code16) {
 #pragma unroll 1
   for (int L = kFastBits + 1; L <= 16; L++) {
-    const int c = code >> (16 - L);
-    if (c < T.lim[L]) {
-      br.skip(L);
-      return T.vals[T.vptr[L] + c - T.first[L]];
-    }
+    const int c = (int)(code16 >> (16 - L));
+    if (c < T.lim[L]) return ((uint32_t)T.vals[T.vptr[L] + c - T.first[L]] << 5) | (uint32_t)L;
   }
-  return -1;
+  return 0;
 }
 
 struct RunState {
@@ -372,6 +370,9 @@ enum { RUN_COUNT = 0, RUN_WRITE = 1, RUN_GUESS = 2 };
 //             one bit after the failing unit's start.
 //  RUN_WRITE: also track the absolute block index (stop at `limit`), DC
 //             predictors, and store crop-window coefficients (natural order).
+// One unit (Huffman code + magnitude bits) per iteration as straight-line
+// predicated code: lanes of a warp sit at different states (DC/AC, EOB,
+// refill) of different subsequences, so every branch would diverge.
 template <int MODE>
 __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, int k0, int b0,
                            uint32_t end_bit, RunState &o, uint32_t blk, uint32_t limit,
@@ -381,6 +382,10 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
   br.w = words;
   br.nw = S.clean_words;
   br.init(p0);
+  // register-resident per-image constants
+  const int bpm = S.bpm;
+  const int c1 = S.slot_nb[0], c2 = S.slot_nb[0] + S.slot_nb[1];
+  const uint32_t tix = S.tab_index_word;  // 4 bits per (dc/ac, slot) table index
   int k = k0, b = b0;
   uint32_t nblk = 0;
   int32_t dc0 = 0, dc1 = 0, dc2 = 0;
@@ -399,7 +404,7 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
     }
   };
   if (WRITE) {
-    const uint32_t mcu = blk / S.bpm;
+    const uint32_t mcu = blk / bpm;
     my = mcu / S.gx;
     mx = mcu % S.gx;
     locate();
@@ -408,65 +413,65 @@ __device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, in
   while (br.p < end_bit) {
     if (WRITE && blk >= limit) break;
     br.refill();
-    const uint32_t ustart = br.p;
-    const int s = S.blk_slot[b];
-    const bool dc = k == 0;
-    const HuffTab &T = S.tab[dc ? S.slot_dc[s] : S.slot_ac[s]];
-    const int sym = decode_sym(T, br);
-    const int size = dc ? sym : (sym & 15);
-    const int run = dc ? 0 : (sym >> 4);
-    bool bad = sym < 0 || (dc && sym > 15);
-    int v = 0;
-    if (!bad && size) {
-      v = extend_bits(br.peek(size), size);
-      br.skip(size);
-    }
-    if (!bad) {
-      if (dc) {
-        if (s == 0) dc0 += v; else if (s == 1) dc1 += v; else dc2 += v;
-        if (WRITE) {
-          const int32_t pv = pred[s] + v;
-          pred[s] = pv;
-          if (cur) {
-            if (pv < -32768 || pv > 32767) o.coef_range = 1;
-            cur[0] = (int16_t)pv;
-          }
-        }
-        k = 1;
-      } else if (size == 0) {
-        k = (run == 15) ? k + 16 : 64;
-      } else {
-        k += run;
-        if (k > 63) {
-          bad = true;
-        } else {
-          if (WRITE && cur) cur[c_zz[k]] = (int16_t)v;
-          k++;
-        }
-      }
-    }
+    const uint32_t hi = (uint32_t)(br.buf >> 32);
+    const int s = (b >= c1) + (b >= c2);
+    const bool isdc = k == 0;
+    const int ti = (tix >> (4 * (isdc ? s : s + 3))) & 15;
+    uint32_t e = S.tab[ti].fast[hi >> (32 - kFastBits)];
+    if ((e & 31) == 0) e = decode_slow(S.tab[ti], hi >> 16);
+    const int len = e & 31;
+    const int sym = (int)(e >> 5);
+    const int size = isdc ? sym : (sym & 15);
+    const int run = sym >> 4;
+    const int kac = k + run;
+    const bool zsz = size == 0;
+    const bool bad = len == 0 || (isdc ? sym > 15 : (!zsz && kac > 63));
     if (bad) {
       if (MODE == RUN_GUESS) {
+        const uint32_t q = br.p + 1;
         k = 0;
         b = 0;
-        br.init(ustart + 1);
+        br.init(q);
         continue;
       }
       o.err = 1;
       o.errblk = nblk;
-      o.errp = ustart;
+      o.errp = br.p;
       break;
     }
-    if (k >= 64) {
-      k = 0;
-      nblk++;
-      b = (b + 1 == S.bpm) ? 0 : b + 1;
-      if (WRITE) {
-        blk++;
-        if (b == 0 && ++mx == S.gx) { mx = 0; my++; }
-        if (blk == S.limit_blocks && p_final) *p_final = br.p;
-        locate();
+    const int total = len + size;  // <= 31: code + magnitude bits, all in `hi`
+    const uint32_t mask = (1u << size) - 1u;
+    const uint32_t raw = (hi >> (32 - total)) & mask;
+    const uint32_t half = (1u << size) >> 1;
+    const int v = raw < half ? (int)raw - (int)mask : (int)raw;  // decode_kernels.py:101-108
+    const int dv = isdc ? v : 0;
+    dc0 += s == 0 ? dv : 0;
+    dc1 += s == 1 ? dv : 0;
+    dc2 += s == 2 ? dv : 0;
+    if (WRITE) {
+      if (isdc) {
+        const int32_t pv = pred[s] + v;
+        pred[s] = pv;
+        if (cur) {
+          if (pv < -32768 || pv > 32767) o.coef_range = 1;
+          cur[0] = (int16_t)pv;
+        }
+      } else if (!zsz && cur) {
+        cur[S.zz[kac]] = (int16_t)v;
       }
+    }
+    const int knew = isdc ? 1 : (zsz ? (run == 15 ? k + 16 : 64) : kac + 1);
+    br.skip(total);
+    const bool be = knew >= 64;
+    k = be ? 0 : knew;
+    nblk += be;
+    const int bn = b + 1 == bpm ? 0 : b + 1;
+    b = be ? bn : b;
+    if (WRITE && be) {
+      blk++;
+      if (b == 0 && ++mx == S.gx) { mx = 0; my++; }
+      if (blk == S.limit_blocks && p_final) *p_final = br.p;
+      locate();
     }
   }
   o.p = o.err ? kErrP : br.p;
@@ -655,6 +660,7 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
   PayloadView pv{raw, n};
 
   if (tid < 12) S.t_ph[tid] = 0;
+  if (tid < 64) S.zz[tid] = c_zz[tid];
   if (tid == 0) {
     S.status = 0; S.reason = 0; S.offset = -1;
     S.coef_range = 0;
@@ -838,13 +844,14 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       for (int s = 0; s < ns; s++) {
         const int c = PS.slot_comp[s];
         const int hh = ns > 1 ? PS.comp_h[c] : 1, vv = ns > 1 ? PS.comp_v[c] : 1;
-        S.slot_comp[s] = c; S.slot_h[s] = hh; S.slot_v[s] = vv;
+        S.slot_comp[s] = c; S.slot_h[s] = hh; S.slot_v[s] = vv; S.slot_nb[s] = hh * vv;
         for (int dy = 0; dy < vv; dy++)
           for (int dx = 0; dx < hh; dx++) {
             S.blk_slot[bpm] = s; S.blk_dy[bpm] = dy; S.blk_dx[bpm] = dx;
             bpm++;
           }
       }
+      for (int s = ns; s < 4; s++) { S.slot_nb[s] = 64; S.slot_dc[s] = 0; S.slot_ac[s] = 0; }
       S.bpm = bpm;
       S.mx0 = x / mcu_w; S.mx1 = (x + w - 1) / mcu_w;
       S.my0 = y / mcu_h; S.my1 = (y + h - 1) / mcu_h;
@@ -1004,6 +1011,10 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       }
     }
     S.ntab = ntab;
+    uint32_t w = 0;
+    for (int q = 0; q < 3; q++) w |= (uint32_t)(S.slot_dc[q] & 15) << (4 * q);
+    for (int q = 0; q < 3; q++) w |= (uint32_t)(S.slot_ac[q] & 15) << (4 * (q + 3));
+    S.tab_index_word = w;
   }
   __syncthreads();
   if (S.status == 0) {
@@ -1029,7 +1040,7 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
         for (int L = kFastBits; L >= 1; L--) {  // shortest match wins (prefix-free)
           const int c = e >> (kFastBits - L);
           if (c < lim[L] && c >= first[L])
-            ent = (uint16_t)((T.vals[vptr[L] + c - first[L]] << 4) | L);
+            ent = (uint16_t)((T.vals[vptr[L] + c - first[L]] << 5) | L);
         }
         T.fast[e] = ent;
       }

@@ -29,11 +29,11 @@ struct PlaneSrc {
   int pitch[3];
   int oy[3], ox[3];  // window origin in component samples
   int h[3], v[3];
-  int hmax, vmax, ncomp;
+  int lh, lv, ncomp;  // log2(hmax), log2(vmax): sampling factors are 1, 2 or 4
   __device__ __forceinline__ void load(const ImgInfo &I, const uint8_t *plane) {
     ncomp = I.ncomp;
-    hmax = I.hmax;
-    vmax = I.vmax;
+    lh = I.hmax == 4 ? 2 : I.hmax - 1;
+    lv = I.vmax == 4 ? 2 : I.vmax - 1;
 #pragma unroll
     for (int c = 0; c < 3; c++) {
       p[c] = plane + I.plane_off[c];
@@ -51,9 +51,10 @@ struct PlaneSrc {
       r = g = b = p[0][(sy - oy[0]) * pitch[0] + (sx - ox[0])];
       return;
     }
-    const int yv = p[0][(sy * v[0] / vmax - oy[0]) * pitch[0] + (sx * h[0] / hmax - ox[0])];
-    const int cb = (int)p[1][(sy * v[1] / vmax - oy[1]) * pitch[1] + (sx * h[1] / hmax - ox[1])] - 128;
-    const int cr = (int)p[2][(sy * v[2] / vmax - oy[2]) * pitch[2] + (sx * h[2] / hmax - ox[2])] - 128;
+    // sy * v / vmax with vmax a power of two (decode_kernels.py:551-558)
+    const int yv = p[0][(((sy * v[0]) >> lv) - oy[0]) * pitch[0] + (((sx * h[0]) >> lh) - ox[0])];
+    const int cb = (int)p[1][(((sy * v[1]) >> lv) - oy[1]) * pitch[1] + (((sx * h[1]) >> lh) - ox[1])] - 128;
+    const int cr = (int)p[2][(((sy * v[2]) >> lv) - oy[2]) * pitch[2] + (((sx * h[2]) >> lh) - ox[2])] - 128;
     r = clamp255(yv + ((91881 * cr + 32768) >> 16));
     g = clamp255(yv + ((-22554 * cb - 46802 * cr + 32768) >> 16));
     b = clamp255(yv + ((116130 * cb + 32768) >> 16));

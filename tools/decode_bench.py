@@ -16,8 +16,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-PHASES = ["setup", "crc", "parse", "destuff", "tables", "pass1", "fixpoint", "scan+tail",
-          "write", "idct"]
+# phase k = clock(k+1) - clock(k) of the PHASE() markers in decode.cu
+PHASES = ["stage", "crc", "parse", "destuff", "tables", "pass1", "fixpoint", "scan", "write"]
 
 
 def main():
@@ -44,8 +44,8 @@ def main():
     perm = E.epoch_permutation(0, 0, len(loader.handle))
     settings = [("spec", 1024, 1024)]
     if args.sweep:
-        settings = [("serial", 0, 0)] + [("spec", s, o) for s in (512, 1024, 2048, 4096)
-                                         for o in (0, 512, 1024, 2048)]
+        settings = [("serial", 0, 0)] + [("spec", s, o) for s in (512, 1024, 2048)
+                                         for o in (256, 512, 1024, 2048)]
     results = []
     for mode, sb, ov in settings:
         eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if mode == "serial"
@@ -65,16 +65,16 @@ def main():
         N.check(N.lib().essl_debug_stats(eng._ctx, N.ptr(dbg), args.n))
         dbg = dbg.reshape(args.n, 12)
         ph = np.diff(dbg[:, :10], axis=1)  # cycles per phase
-        ph = np.concatenate([ph, np.zeros((args.n, 1), np.int64)], axis=1)
         iters = dbg[:, 10]
         nseq = dbg[:, 11] & 0xFFFFFFFF
         redo = dbg[:, 11] >> 32
         row = {"mode": mode, "seq_bits": sb, "overlap": ov,
                "decode_ms": prof["decode"][0] / prof["decode"][1],
                "resize_ms": prof.get("resize", (0, 1))[0] / max(prof.get("resize", (0, 1))[1], 1),
-               "phase_kcycles_median": {PHASES[i + 1]: float(np.median(ph[:, i])) / 1e3
-                                        for i in range(8)},
-               "phase_kcycles_max": {PHASES[i + 1]: float(np.max(ph[:, i])) / 1e3 for i in range(8)},
+               "phase_kcycles_median": {PHASES[i]: round(float(np.median(ph[:, i])) / 1e3, 1)
+                                        for i in range(9)},
+               "phase_kcycles_max": {PHASES[i]: round(float(np.max(ph[:, i])) / 1e3, 1)
+                                     for i in range(9)},
                "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
                "nseq_mean": float(nseq.mean()), "redo_frac": float(redo.sum() / max(nseq.sum(), 1))}
         results.append(row)
