@@ -131,6 +131,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   {
     Prof pr(c, ESSL_K_DECODE, st);
     essl::launch_decode(p, st, max_len);
+    c->launches += 1;  // k_prep + k_entropy
   }
   CK(cudaGetLastError());
   return ESSL_OK;
@@ -176,6 +177,7 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   CKC(cudaMalloc(&c->s.plane, c->s.plane_cap));
   CKC(cudaMalloc(&c->s.counters, 4 * sizeof(unsigned long long)));
   CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
+  CKC(cudaMalloc(&c->s.hdr, essl::decode_hdr_bytes() * max_batch));
   CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
   for (int r = 0; r < kDescRing; r++) {
     CKC(cudaMallocHost(&c->h_desc[r], sizeof(essl_sample) * max_batch));
@@ -204,6 +206,7 @@ int essl_ctx_destroy(essl_ctx *c) {
   cudaFree(c->s.plane);
   cudaFree(c->s.counters);
   cudaFree(c->s.info);
+  cudaFree(c->s.hdr);
   cudaFree(c->d_offsets);
   for (int r = 0; r < kDescRing; r++) {
     if (c->h_desc[r]) cudaFreeHost(c->h_desc[r]);

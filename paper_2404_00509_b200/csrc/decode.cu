@@ -1,4 +1,4 @@
-// k_decode: one CTA per image.  Replaces, for a whole batch on the GPU,
+// k_prep + k_entropy: one CTA per image each.  Replace, for a whole batch,
 //   container.py:249-265   read_sample CRC check
 //   jpeg/codec.py:124-265  parse_stream + _finish_geometry
 //   jpeg/codec.py:272-320  _huff_lut / _destuff
@@ -6,10 +6,12 @@
 //   jpeg/codec.py:323-330  _check_consumed
 //   jpeg/decode_kernels.py:388-534 reconstruct_blocks (crop window only)
 //
-// Layout: the compressed payload is staged into shared memory with 16-byte
-// loads and destuffed into a second shared buffer; every later phase (CRC,
-// marker parse, Huffman decode) reads shared memory only.  Payloads too
-// large for shared memory use the same code on global memory (SMEM=false).
+// k_prep stages the compressed payload in shared memory (16-byte loads) and
+// does the byte-level work there: CRC32, marker parse, destuff (into a global
+// clean stream), Huffman table build, window zeroing.  It hands a per-image
+// DecodeHdr to k_entropy, whose small shared footprint (~37 KB, <=64 regs)
+// keeps 4 CTAs per SM resident so that several batches can be in flight.
+// Payloads too large for shared memory are read from global (SMEM=false).
 //
 // Entropy decoding of a restart-free baseline scan is inherently serial; it
 // is parallelised inside the CTA by self-synchronising speculative decode:
@@ -54,6 +56,25 @@ struct HuffTab {
   int dht_pos, nvals;  // where the DHT symbols live in the payload
 };
 
+
+// Geometry, stream location and tables handed from k_prep to k_entropy
+// (global, one per image; k_entropy keeps a copy in shared memory).
+struct DecodeHdr {
+  int32_t status, reason, offset;
+  int32_t ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ncomp, ntab;
+  uint32_t limit_blocks, clean_bits, clean_words, tab_index_word;
+  int32_t scan_ri, scan_start, scan_end, n_restarts, max_restarts;
+  int32_t slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
+  int32_t wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
+  int32_t quant_missing;  // -1: all dequantisation tables present
+  uint32_t rst_off;       // restart table, words from the clean region start
+  uint64_t coef_off[3], coef_base, clean_off;
+  uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
+  uint8_t zz[64];
+  int32_t q[3][64];  // dequantisation tables, natural order
+  HuffTab tab[kMaxTables];
+};
+
 struct SeqRec {
   uint32_t gp, gkb;  // entry state: bit position, k | b << 8
   uint32_t ep, ekb;  // exit state (ep == kErrP: decode error)
@@ -74,38 +95,27 @@ struct ParseState {
   int cmd, dstart;
 };
 
-struct __align__(16) Smem {
-  union {
-    struct {
-      uint32_t T[4][256];  // slice-by-4 CRC tables
-      uint32_t part[kNT];
-    } crc;
-    int32_t idct_tr[kNT / 32][4][64];
-  } u;
-  HuffTab tab[kMaxTables];
-  SeqRec seq[kNT];
+struct __align__(16) PrepSmem {
+  DecodeHdr h;
+  struct {
+    uint32_t T[4][256];  // slice-by-4 CRC tables
+    uint32_t part[kNT];
+  } crc;
   ParseState ps;
-  int32_t q[3][64];  // dequantisation tables, natural order
-  uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
-  int slot_dc[4], slot_ac[4];  // table index per slot
-  int slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
-  uint32_t tab_index_word;
-  uint8_t zz[64];
-  int ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ntab;
-  int wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
-  uint64_t coef_off[3];
-  uint64_t coef_base;
   uint32_t K[8];
-  uint32_t limit_blocks, clean_bits, clean_words;
-  uint64_t clean_off;
-  uint32_t rst_off;
-  int n_restarts, max_restarts;
+  uint32_t warp_tot[kNT / 32][4];
+  int stop;
+  long long t0;
+};
+
+struct __align__(16) EntSmem {
+  DecodeHdr h;
+  SeqRec seq[kNT];
+  int32_t idct_tr[kNT / 32][4][64];
+  uint32_t warp_tot[kNT / 32][4];
   int status, reason, offset;
   uint32_t p_final;
-  int coef_range;
-  int stop, red_i[2];
-  uint32_t warp_tot[kNT / 32][4];
-  int changed;
+  int coef_range, changed, red_i[2];
   long long t_ph[12];
 };
 
@@ -142,7 +152,7 @@ __device__ __forceinline__ bool has_ff(uint32_t w) { return __vcmpeq4(w, 0xFFFFF
 
 // Block-wide exclusive scan of four u32 values (kNT threads, warp shuffles).
 // Returns the block totals in tot[].
-__device__ void block_scan4(Smem &S, uint32_t v[4], uint32_t tot[4]) {
+__device__ void block_scan4(uint32_t (*warp_tot)[4], uint32_t v[4], uint32_t tot[4]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t inc[4];
 #pragma unroll
@@ -157,14 +167,14 @@ __device__ void block_scan4(Smem &S, uint32_t v[4], uint32_t tot[4]) {
   }
   if (lane == 31) {
 #pragma unroll
-    for (int q = 0; q < 4; q++) S.warp_tot[warp][q] = inc[q];
+    for (int q = 0; q < 4; q++) warp_tot[warp][q] = inc[q];
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     uint32_t before = 0, all = 0;
     for (int w = 0; w < kNT / 32; w++) {
-      const uint32_t t = S.warp_tot[w][q];
+      const uint32_t t = warp_tot[w][q];
       if (w < warp) before += t;
       all += t;
     }
@@ -374,7 +384,7 @@ enum { RUN_COUNT = 0, RUN_WRITE = 1, RUN_GUESS = 2 };
 // predicated code: lanes of a warp sit at different states (DC/AC, EOB,
 // refill) of different subsequences, so every branch would diverge.
 template <int MODE>
-__device__ void decode_run(const Smem &S, const uint32_t *words, uint32_t p0, int k0, int b0,
+__device__ void decode_run(const DecodeHdr &S, const uint32_t *words, uint32_t p0, int k0, int b0,
                            uint32_t end_bit, RunState &o, uint32_t blk, uint32_t limit,
                            int32_t *pred, int16_t *coef, uint32_t *p_final) {
   constexpr bool WRITE = MODE == RUN_WRITE;
@@ -628,7 +638,15 @@ __device__ void idct_block_8lanes(bool valid, const int16_t *coef, const int32_t
 
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void set_status(Smem &S, int st, int reason, int off) {
+__device__ __forceinline__ void hdr_status(DecodeHdr &H, int st, int reason, int off) {
+  if (H.status == 0) {
+    H.status = st;
+    H.reason = reason;
+    H.offset = off;
+  }
+}
+
+__device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int off) {
   if (S.status == 0) {
     S.status = st;
     S.reason = reason;
@@ -636,19 +654,26 @@ __device__ __forceinline__ void set_status(Smem &S, int st, int reason, int off)
   }
 }
 
-__device__ __forceinline__ int corrupt_offset(const ParseState &PS, uint32_t errp) {
+__device__ __forceinline__ int corrupt_offset(const DecodeHdr &H, uint32_t errp) {
   // _check_consumed: scan.start + min(vpos, seglen); the reference's reader
   // keeps >= 25 bits buffered, so vpos = ceil((p + 25) / 8) at the failing unit.
-  const uint32_t seglen = (uint32_t)(PS.scan_end - PS.scan_start);
+  const uint32_t seglen = (uint32_t)(H.scan_end - H.scan_start);
   const uint32_t vpos = (errp + 25 + 7) / 8;
-  return PS.scan_start + (int)min(vpos, seglen);
+  return H.scan_start + (int)min(vpos, seglen);
 }
 
+__device__ __forceinline__ DecodeHdr *hdr_of(const Scratch &s, int img) {
+  return reinterpret_cast<DecodeHdr *>(s.hdr) + img;
+}
+
+// ===========================================================================
+// k_prep: CRC, parse, destuff, tables, window zeroing (one CTA per image)
+// ===========================================================================
 template <bool SMEM>
-__global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
+__global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   extern __shared__ __align__(16) uint8_t dyn[];
-  __shared__ Smem S;
-#define PHASE(i) do { if (threadIdx.x == 0) S.t_ph[i] = clock64(); } while (0)
+  __shared__ PrepSmem S;
+  DecodeHdr &H = S.h;
   const int img = blockIdx.x;
   const int tid = threadIdx.x;
   const essl_sample smp = P.samples[img];
@@ -659,14 +684,13 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
   const uint8_t *raw = SMEM ? dyn : g;
   PayloadView pv{raw, n};
 
-  if (tid < 12) S.t_ph[tid] = 0;
-  if (tid < 64) S.zz[tid] = c_zz[tid];
+  if (tid < 64) H.zz[tid] = c_zz[tid];
   if (tid == 0) {
-    S.status = 0; S.reason = 0; S.offset = -1;
-    S.coef_range = 0;
-    S.p_final = kNoEnd;
+    S.t0 = clock64();
+    H.status = 0; H.reason = 0; H.offset = -1;
+    H.ntab = 0; H.ns = 0; H.ncomp = 0; H.quant_missing = -1;
+    H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0;
   }
-  PHASE(0);
   // ---- stage the payload into shared memory (16-byte loads) ----------------
   if (SMEM) {
     if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
@@ -680,25 +704,23 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
     }
     for (int i = n + tid; i < n_pad; i += kNT) dyn[i] = 0;
   }
-  // CRC tables (slice-by-4)
-  {
+  {  // CRC tables (slice-by-4)
     uint32_t c = tid;
 #pragma unroll
     for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-    S.u.crc.T[0][tid] = c;
+    S.crc.T[0][tid] = c;
   }
   __syncthreads();
   {
-    uint32_t c = S.u.crc.T[0][tid];
+    uint32_t c = S.crc.T[0][tid];
 #pragma unroll
     for (int t = 1; t < 4; t++) {
-      c = (c >> 8) ^ S.u.crc.T[0][c & 0xFF];
-      S.u.crc.T[t][tid] = c;
+      c = (c >> 8) ^ S.crc.T[0][c & 0xFF];
+      S.crc.T[t][tid] = c;
     }
   }
   __syncthreads();
 
-  PHASE(1);
   // ---- CRC32 (container.py:263) -------------------------------------------
   // The message is viewed as 256 chunks of L bytes (L % 4 == 0) with zeros
   // prepended (leading zeros do not change a zero-init CRC); the 0xFFFFFFFF
@@ -709,12 +731,13 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
     if (n < 4) {
       if (tid == 0) {
         uint32_t c = 0xFFFFFFFFu;
-        for (int i = 0; i < n; i++) c = S.u.crc.T[0][(c ^ raw[i]) & 0xFF] ^ (c >> 8);
+        for (int i = 0; i < n; i++) c = S.crc.T[0][(c ^ raw[i]) & 0xFF] ^ (c >> 8);
         crc = c ^ 0xFFFFFFFFu;
       }
     } else {
       const int L = ((n + kNT - 1) / kNT + 3) & ~3;
       const int pad = kNT * L - n;
+      if (tid < 8) S.K[tid] = x2nmodp((uint64_t)L << tid, 3);
       uint32_t c = 0;
       for (int j = 0; j < L; j += 4) {
         const int rp = tid * L + j - pad;
@@ -727,41 +750,39 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
           w |= byte << (8 * b);
         }
         c ^= w;
-        c = S.u.crc.T[3][c & 0xFF] ^ S.u.crc.T[2][(c >> 8) & 0xFF] ^
-            S.u.crc.T[1][(c >> 16) & 0xFF] ^ S.u.crc.T[0][c >> 24];
+        c = S.crc.T[3][c & 0xFF] ^ S.crc.T[2][(c >> 8) & 0xFF] ^ S.crc.T[1][(c >> 16) & 0xFF] ^
+            S.crc.T[0][c >> 24];
       }
-      S.u.crc.part[tid] = c;
-      if (tid < 8) S.K[tid] = x2nmodp((uint64_t)L << tid, 3);
+      S.crc.part[tid] = c;
       __syncthreads();
 #pragma unroll 1
       for (int j = 0; (1 << j) < kNT; j++) {
         const int stride = 1 << j;
         uint32_t v = 0;
         const bool act = (tid % (2 * stride)) == 0;
-        if (act) v = multmodp(S.K[j], S.u.crc.part[tid]) ^ S.u.crc.part[tid + stride];
+        if (act) v = multmodp(S.K[j], S.crc.part[tid]) ^ S.crc.part[tid + stride];
         __syncthreads();
-        if (act) S.u.crc.part[tid] = v;
+        if (act) S.crc.part[tid] = v;
         __syncthreads();
       }
-      crc = S.u.crc.part[0] ^ 0xFFFFFFFFu;
+      crc = S.crc.part[0] ^ 0xFFFFFFFFu;
     }
-    if (tid == 0 && crc != smp.crc32) set_status(S, ESSL_ST_CRC, 0, -1);
+    if (tid == 0 && crc != smp.crc32) hdr_status(H, ESSL_ST_CRC, 0, -1);
   }
   __syncthreads();
 
-  PHASE(2);
   // ---- parse (thread 0) + parallel entropy-segment end search --------------
   ParseState &PS = S.ps;
   if (tid == 0) {
     PS.pos = 2; PS.n = n; PS.ri = 0; PS.have_sof = 0; PS.progressive = 0;
     PS.ncomp = 0; PS.nscans = 0; PS.status = 0; PS.cmd = 0; PS.ns = 0;
-    PS.scan_start = 0; PS.scan_end = 0; PS.scan_ri = 0;
+    PS.scan_start = 0; PS.scan_end = 0; PS.scan_ri = 0; PS.width = 0; PS.height = 0;
     for (int i = 0; i < 16; i++) { PS.quant_pos[i] = -1; PS.huff_pos[0][i] = -1; PS.huff_pos[1][i] = -1; }
     if (n < 4 || raw[0] != 0xFF || raw[1] != 0xD8) parse_fail(PS, R_NO_SOI, 0);
     else PS.cmd = 3;  // continue
   }
   __syncthreads();
-  if (S.status == 0) {
+  if (H.status == 0) {
 #pragma unroll 1
     while (true) {
       if (tid == 0 && PS.cmd != 2) parse_until_sos(PS, pv);
@@ -795,120 +816,128 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       }
       __syncthreads();
     }
-    if (tid == 0 && PS.cmd == 2) set_status(S, PS.status, PS.reason, PS.offset);
+    if (tid == 0 && PS.cmd == 2) hdr_status(H, PS.status, PS.reason, PS.offset);
   }
   __syncthreads();
 
   // ---- geometry, validation (codec.py:254-265, 448-482) --------------------
-  if (tid == 0 && S.status == 0) {
+  if (tid == 0) {
     int hmax = 1, vmax = 1;
     for (int i = 0; i < PS.ncomp; i++) {
       hmax = max(hmax, PS.comp_h[i]);
       vmax = max(vmax, PS.comp_v[i]);
     }
-    const int W = PS.width, H = PS.height;
-    const int mcus_x = (W + 8 * hmax - 1) / (8 * hmax), mcus_y = (H + 8 * vmax - 1) / (8 * vmax);
-    for (int i = 0; i < PS.ncomp; i++) {
-      const int cw = (W * PS.comp_h[i] + hmax - 1) / hmax, ch = (H * PS.comp_v[i] + vmax - 1) / vmax;
-      S.bw[i] = (cw + 7) / 8;
-      S.bh[i] = (ch + 7) / 8;
-    }
-    info->width = W; info->height = H; info->ncomp = PS.ncomp;
+    const int W = PS.width, Hh = PS.height;
+    info->width = W; info->height = Hh; info->ncomp = PS.ncomp;
     info->hmax = hmax; info->vmax = vmax;
     for (int i = 0; i < 3; i++) {
       info->comp_h[i] = i < PS.ncomp ? PS.comp_h[i] : 1;
       info->comp_v[i] = i < PS.ncomp ? PS.comp_v[i] : 1;
     }
-    const int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
-    if (w < 1 || h < 1 || x < 0 || y < 0 || x + w > W || y + h > H) {
-      set_status(S, ESSL_ST_RECT, 0, -1);
-    } else if (PS.progressive) {
-      set_status(S, ESSL_ST_UNSUPPORTED, R_PROGRESSIVE, -1);
-    } else if (PS.nscans != 1 || PS.ns != PS.ncomp) {
-      set_status(S, ESSL_ST_UNSUPPORTED, R_MULTI_SCAN, -1);
-    } else {
-      const int ns = PS.ns;
-      S.ns = ns;
-      int mcu_w, mcu_h;
-      if (ns == 1) {
-        S.gx = S.bw[PS.slot_comp[0]];
-        S.gy = S.bh[PS.slot_comp[0]];
-        mcu_w = mcu_h = 8;
+    info->rx = smp.x; info->ry = smp.y; info->rw = smp.w; info->rh = smp.h;
+    info->flip = smp.flip;
+    H.ncomp = PS.ncomp;
+    H.scan_ri = PS.scan_ri;
+    H.scan_start = PS.scan_start;
+    H.scan_end = PS.scan_end;
+    if (H.status == 0) {
+      const int mcus_x = (W + 8 * hmax - 1) / (8 * hmax), mcus_y = (Hh + 8 * vmax - 1) / (8 * vmax);
+      for (int i = 0; i < PS.ncomp; i++) {
+        const int cw = (W * PS.comp_h[i] + hmax - 1) / hmax, ch = (Hh * PS.comp_v[i] + vmax - 1) / vmax;
+        H.bw[i] = (cw + 7) / 8;
+        H.bh[i] = (ch + 7) / 8;
+      }
+      const int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
+      if (w < 1 || h < 1 || x < 0 || y < 0 || x + w > W || y + h > Hh) {
+        hdr_status(H, ESSL_ST_RECT, 0, -1);
+      } else if (PS.progressive) {
+        hdr_status(H, ESSL_ST_UNSUPPORTED, R_PROGRESSIVE, -1);
+      } else if (PS.nscans != 1 || PS.ns != PS.ncomp) {
+        hdr_status(H, ESSL_ST_UNSUPPORTED, R_MULTI_SCAN, -1);
       } else {
-        S.gx = mcus_x;
-        S.gy = mcus_y;
-        mcu_w = 8 * hmax;
-        mcu_h = 8 * vmax;
+        const int ns = PS.ns;
+        H.ns = ns;
+        int mcu_w, mcu_h;
+        if (ns == 1) {
+          H.gx = H.bw[PS.slot_comp[0]];
+          H.gy = H.bh[PS.slot_comp[0]];
+          mcu_w = mcu_h = 8;
+        } else {
+          H.gx = mcus_x;
+          H.gy = mcus_y;
+          mcu_w = 8 * hmax;
+          mcu_h = 8 * vmax;
+        }
+        int bpm = 0;
+        for (int s = 0; s < ns; s++) {
+          const int c = PS.slot_comp[s];
+          const int hh = ns > 1 ? PS.comp_h[c] : 1, vv = ns > 1 ? PS.comp_v[c] : 1;
+          H.slot_comp[s] = c; H.slot_h[s] = hh; H.slot_v[s] = vv; H.slot_nb[s] = hh * vv;
+          for (int dy = 0; dy < vv; dy++)
+            for (int dx = 0; dx < hh; dx++) {
+              H.blk_slot[bpm] = s; H.blk_dy[bpm] = dy; H.blk_dx[bpm] = dx;
+              bpm++;
+            }
+        }
+        for (int s = ns; s < 4; s++) { H.slot_nb[s] = 64; H.slot_comp[s] = 0; H.slot_h[s] = 1; H.slot_v[s] = 1; }
+        H.bpm = bpm;
+        H.mx0 = x / mcu_w; H.mx1 = (x + w - 1) / mcu_w;
+        H.my0 = y / mcu_h; H.my1 = (y + h - 1) / mcu_h;
+        H.row_stop = H.my1 + 1;
+        H.limit_blocks = (uint32_t)H.row_stop * H.gx * bpm;
+        info->mcus_entropy = H.row_stop * H.gx;
+        info->mcus_recon = (H.my1 - H.my0 + 1) * (H.mx1 - H.mx0 + 1);
+        uint64_t total = 0;
+        for (int c = 0; c < 3; c++) { H.wbh[c] = 0; H.wbw[c] = 0; H.wby0[c] = 0; H.wbx0[c] = 0; H.coef_off[c] = 0; }
+        for (int s = 0; s < ns; s++) {
+          const int c = H.slot_comp[s];
+          H.wby0[c] = H.my0 * H.slot_v[s];
+          H.wbx0[c] = H.mx0 * H.slot_h[s];
+          H.wbh[c] = (H.my1 - H.my0 + 1) * H.slot_v[s];
+          H.wbw[c] = (H.mx1 - H.mx0 + 1) * H.slot_h[s];
+          H.coef_off[c] = total;
+          total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
+        }
+        const unsigned long long cbase = atomicAdd(&P.s.counters[1], (unsigned long long)total);
+        if (cbase + total > P.s.coef_cap) {
+          hdr_status(H, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+        } else {
+          for (int c = 0; c < 3; c++) H.coef_off[c] += cbase;
+          H.coef_base = cbase;
+        }
+        // global region: clean bytes + restart table
+        const int seglen = PS.scan_end - PS.scan_start;
+        H.max_restarts = PS.scan_ri ? (H.gx * H.gy) / PS.scan_ri : 0;
+        const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
+        const uint64_t clean_bytes = ((uint64_t)seglen + 16 + 15) / 16 * 16;
+        const uint64_t alloc = (clean_bytes + 4ull * max_r + 16 + 15) / 16 * 16;
+        const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)alloc);
+        if (base + alloc > P.s.clean_cap) hdr_status(H, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+        H.clean_off = base;
+        H.rst_off = (uint32_t)(clean_bytes / 4);
+        // dequantisation tables (the reference checks them after decoding)
+        for (int i = 0; i < PS.ncomp; i++) {
+          const int tq = PS.comp_tq[i];
+          if (tq > 15 || PS.quant_pos[tq] < 0) { H.quant_missing = tq; break; }
+        }
       }
-      int bpm = 0;
-      for (int s = 0; s < ns; s++) {
-        const int c = PS.slot_comp[s];
-        const int hh = ns > 1 ? PS.comp_h[c] : 1, vv = ns > 1 ? PS.comp_v[c] : 1;
-        S.slot_comp[s] = c; S.slot_h[s] = hh; S.slot_v[s] = vv; S.slot_nb[s] = hh * vv;
-        for (int dy = 0; dy < vv; dy++)
-          for (int dx = 0; dx < hh; dx++) {
-            S.blk_slot[bpm] = s; S.blk_dy[bpm] = dy; S.blk_dx[bpm] = dx;
-            bpm++;
-          }
-      }
-      for (int s = ns; s < 4; s++) { S.slot_nb[s] = 64; S.slot_dc[s] = 0; S.slot_ac[s] = 0; }
-      S.bpm = bpm;
-      S.mx0 = x / mcu_w; S.mx1 = (x + w - 1) / mcu_w;
-      S.my0 = y / mcu_h; S.my1 = (y + h - 1) / mcu_h;
-      S.row_stop = S.my1 + 1;
-      S.limit_blocks = (uint32_t)S.row_stop * S.gx * bpm;
-      info->mcus_entropy = S.row_stop * S.gx;
-      info->mcus_recon = (S.my1 - S.my0 + 1) * (S.mx1 - S.mx0 + 1);
-      uint64_t total = 0;
-      for (int c = 0; c < 3; c++) { S.wbh[c] = 0; S.wbw[c] = 0; S.wby0[c] = 0; S.wbx0[c] = 0; }
-      for (int s = 0; s < ns; s++) {
-        const int c = S.slot_comp[s];
-        S.wby0[c] = S.my0 * S.slot_v[s];
-        S.wbx0[c] = S.mx0 * S.slot_h[s];
-        S.wbh[c] = (S.my1 - S.my0 + 1) * S.slot_v[s];
-        S.wbw[c] = (S.mx1 - S.mx0 + 1) * S.slot_h[s];
-        S.coef_off[c] = total;
-        total += (uint64_t)S.wbh[c] * S.wbw[c] * 64;
-      }
-      const unsigned long long cbase = atomicAdd(&P.s.counters[1], (unsigned long long)total);
-      if (cbase + total > P.s.coef_cap) {
-        set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
-      } else {
-        for (int c = 0; c < 3; c++) S.coef_off[c] += cbase;
-        S.coef_base = cbase;
-      }
-      // global region: clean bytes (global variant) + restart table
-      const int seglen = PS.scan_end - PS.scan_start;
-      S.max_restarts = PS.scan_ri ? (S.gx * S.gy) / PS.scan_ri : 0;
-      const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
-      const uint64_t clean_bytes = SMEM ? 0 : ((uint64_t)seglen + 16 + 15) / 16 * 16;
-      const uint64_t alloc = (clean_bytes + 4ull * max_r + 16 + 15) / 16 * 16;
-      const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)alloc);
-      if (base + alloc > P.s.clean_cap) set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
-      S.clean_off = base;
-      S.rst_off = (uint32_t)(clean_bytes / 4);
     }
   }
   __syncthreads();
-
-  // ---- dequantisation tables (values; the check happens after decoding) ----
-  if (S.status == 0) {
+  if (H.status == 0) {
     for (int e = tid; e < PS.ncomp * 64; e += kNT) {
       const int c = e >> 6, k = e & 63;
       const int tq = PS.comp_tq[c];
       const int pos = tq <= 15 ? PS.quant_pos[tq] : -1;
       int v = 0;
       if (pos >= 0) v = PS.quant_pq[tq] == 1 ? ((raw[pos + 2 * k] << 8) | raw[pos + 2 * k + 1]) : raw[pos + k];
-      S.q[c][c_zz[k]] = v;
+      H.q[c][c_zz[k]] = v;
     }
   }
 
-  PHASE(3);
-  // ---- destuff (decode_kernels.py:27-61) ------------------------------------
-  uint8_t *gclean = P.s.clean + S.clean_off;
-  uint8_t *clean = SMEM ? dyn + n_pad : gclean;
-  uint32_t *rst_tab = reinterpret_cast<uint32_t *>(gclean) + S.rst_off;
-  if (S.status == 0) {
+  // ---- destuff (decode_kernels.py:27-61) into the global clean region -------
+  uint8_t *clean = P.s.clean + H.clean_off;
+  if (H.status == 0) {
     const int seg0 = PS.scan_start, seg1 = PS.scan_end;
     const int segn = seg1 - seg0;
     const int per = ((segn + kNT - 1) / kNT + 3) & ~3;
@@ -948,8 +977,9 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       cnt[1] += rst;
       i++;
     }
-    block_scan4(S, cnt, tot);
-    const int max_r = PS.scan_ri ? S.max_restarts + 2 : 0;
+    block_scan4(S.warp_tot, cnt, tot);
+    const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
+    uint32_t *rst_tab = reinterpret_cast<uint32_t *>(clean) + H.rst_off;
     uint32_t kept = cnt[0], nrst = cnt[1];
     for (int i = a; i < e2; i++) {
       const int v = raw[i];
@@ -963,42 +993,41 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       }
     }
     const uint32_t tk = tot[0], tr = tot[1];
-    __syncthreads();
     if (tid < 16) clean[tk + tid] = 0xFF;  // 0xFF padding past the end (_br_fill)
     if (tid == 0) {
-      S.clean_bits = tk * 8;
-      S.clean_words = (tk + 3) / 4;
-      S.n_restarts = (int)tr;
-      if (PS.scan_ri == 0 && tr > 0) set_status(S, ESSL_ST_MALFORMED, R_RST_NO_DRI, seg0);
-      else if ((int)tr > S.max_restarts + 2) set_status(S, ESSL_ST_MALFORMED, R_TOO_MANY_RST, seg0);
+      H.clean_bits = tk * 8;
+      H.clean_words = (tk + 3) / 4;
+      H.n_restarts = (int)tr;
+      if (PS.scan_ri == 0 && tr > 0) hdr_status(H, ESSL_ST_MALFORMED, R_RST_NO_DRI, seg0);
+      else if ((int)tr > H.max_restarts + 2) hdr_status(H, ESSL_ST_MALFORMED, R_TOO_MANY_RST, seg0);
     }
   }
   __syncthreads();
 
-  PHASE(4);
   // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
-  if (tid == 0 && S.status == 0) {
+  if (tid == 0 && H.status == 0) {
     int ntab = 0;
     int tab_pos[kMaxTables];
-    for (int pass = 0; pass < 2 && S.status == 0; pass++) {
-      for (int s = 0; s < S.ns && S.status == 0; s++) {
+    int slot_dc[4] = {0, 0, 0, 0}, slot_ac[4] = {0, 0, 0, 0};
+    for (int pass = 0; pass < 2 && H.status == 0; pass++) {
+      for (int s = 0; s < H.ns && H.status == 0; s++) {
         const int pos = pass == 0 ? PS.slot_dpos[s] : PS.slot_apos[s];
         const int tot = pass == 0 ? PS.slot_dtot[s] : PS.slot_atot[s];
-        if (pos < 0) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_UNDEFINED, -1); break; }
-        if (tot > 256) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_TOO_MANY, -1); break; }
+        if (pos < 0) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_UNDEFINED, -1); break; }
+        if (tot > 256) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_TOO_MANY, -1); break; }
         int ti = -1;
         for (int t = 0; t < ntab; t++) if (tab_pos[t] == pos) ti = t;
         if (ti < 0) {
           ti = ntab++;
           tab_pos[ti] = pos;
-          HuffTab &T = S.tab[ti];
+          HuffTab &T = H.tab[ti];
           int code = 0, vi = 0;
           T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
           for (int L = 1; L <= 16; L++) {
             const int cnt = raw[pos + L - 1];
             T.first[L] = code;
             T.vptr[L] = (int16_t)vi;
-            if (cnt && code + cnt > (1 << L)) { set_status(S, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
+            if (cnt && code + cnt > (1 << L)) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
             code += cnt;
             vi += cnt;
             T.lim[L] = code;
@@ -1007,26 +1036,26 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
           T.dht_pos = pos;
           T.nvals = tot;
         }
-        if (pass == 0) S.slot_dc[s] = ti; else S.slot_ac[s] = ti;
+        if (pass == 0) slot_dc[s] = ti; else slot_ac[s] = ti;
       }
     }
-    S.ntab = ntab;
+    H.ntab = ntab;
     uint32_t w = 0;
-    for (int q = 0; q < 3; q++) w |= (uint32_t)(S.slot_dc[q] & 15) << (4 * q);
-    for (int q = 0; q < 3; q++) w |= (uint32_t)(S.slot_ac[q] & 15) << (4 * (q + 3));
-    S.tab_index_word = w;
+    for (int q = 0; q < 3; q++) w |= (uint32_t)(slot_dc[q] & 15) << (4 * q);
+    for (int q = 0; q < 3; q++) w |= (uint32_t)(slot_ac[q] & 15) << (4 * (q + 3));
+    H.tab_index_word = w;
   }
   __syncthreads();
-  if (S.status == 0) {
-    const int ntab = S.ntab;
+  if (H.status == 0) {
+    const int ntab = H.ntab;
     for (int e = tid; e < ntab * 256; e += kNT) {
-      HuffTab &T = S.tab[e >> 8];
+      HuffTab &T = H.tab[e >> 8];
       const int v = e & 255;
       T.vals[v] = v < T.nvals ? (uint8_t)raw[T.dht_pos + 16 + v] : 0;
     }
     __syncthreads();
     for (int t = 0; t < ntab; t++) {
-      HuffTab &T = S.tab[t];
+      HuffTab &T = H.tab[t];
       int lim[kFastBits + 1], first[kFastBits + 1], vptr[kFastBits + 1];
 #pragma unroll
       for (int L = 1; L <= kFastBits; L++) {
@@ -1037,7 +1066,7 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       for (int e = tid; e < (1 << kFastBits); e += kNT) {
         uint16_t ent = 0;
 #pragma unroll
-        for (int L = kFastBits; L >= 1; L--) {  // shortest match wins (prefix-free)
+        for (int L = kFastBits; L >= 1; L--) {  // prefix-free: at most one length matches
           const int c = e >> (kFastBits - L);
           if (c < lim[L] && c >= first[L])
             ent = (uint16_t)((T.vals[vptr[L] + c - first[L]] << 5) | L);
@@ -1045,42 +1074,85 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
         T.fast[e] = ent;
       }
     }
-  }
-  __syncthreads();
-
-  // ---- zero the coefficient window ------------------------------------------
-  if (S.status == 0) {
+    // zero the coefficient window (k_entropy scatters nonzeros into it)
     uint64_t total = 0;
-    for (int c = 0; c < 3; c++) total += (uint64_t)S.wbh[c] * S.wbw[c] * 64;
-    int4 *z = reinterpret_cast<int4 *>(P.s.coef + S.coef_base);
+    for (int c = 0; c < 3; c++) total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
+    int4 *z = reinterpret_cast<int4 *>(P.s.coef + H.coef_base);
     const uint64_t n16 = total / 8;
     for (uint64_t i = tid; i < n16; i += kNT) z[i] = make_int4(0, 0, 0, 0);
   }
   __syncthreads();
+  // ---- hand over: header (+ used tables) to global ---------------------------
+  {
+    DecodeHdr *G = hdr_of(P.s, img);
+    const int words = (int)((offsetof(DecodeHdr, tab) + (H.status == 0 ? H.ntab : 0) * sizeof(HuffTab)) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(&H);
+    int4 *dst = reinterpret_cast<int4 *>(G);
+    for (int i = tid; i < words; i += kNT) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    info->dbg[0] = S.t0;
+    info->dbg[1] = clock64();
+  }
+}
 
-  PHASE(5);
-  // ---- entropy decode ---------------------------------------------------------
+// ===========================================================================
+// k_entropy: entropy decode + IDCT (one CTA per image)
+// ===========================================================================
+__global__ void __launch_bounds__(kNT, 4) k_entropy(DecodeParams P) {
+  __shared__ EntSmem S;
+#define PHASE(i) do { if (threadIdx.x == 0) S.t_ph[i] = clock64(); } while (0)
+  const int img = blockIdx.x;
+  const int tid = threadIdx.x;
+  ImgInfo *info = P.s.info + img;
+  const DecodeHdr *G = hdr_of(P.s, img);
+  DecodeHdr &H = S.h;
+  if (tid < 12) S.t_ph[tid] = 0;
+  PHASE(0);
+  {
+    const int head = (int)(offsetof(DecodeHdr, tab) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(G);
+    int4 *dst = reinterpret_cast<int4 *>(&H);
+    for (int i = tid; i < head; i += kNT) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (H.status == 0) {
+    const int words = (int)(H.ntab * sizeof(HuffTab) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(G->tab);
+    int4 *dst = reinterpret_cast<int4 *>(H.tab);
+    for (int i = tid; i < words; i += kNT) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    S.status = H.status; S.reason = H.reason; S.offset = H.offset;
+    S.coef_range = 0;
+    S.p_final = kNoEnd;
+  }
+  __syncthreads();
+  PHASE(1);
+
+  const uint8_t *clean = P.s.clean + H.clean_off;
   const uint32_t *words = reinterpret_cast<const uint32_t *>(clean);
+  const uint32_t *rst_tab = words + H.rst_off;
   int16_t *coef = P.s.coef;
-  if (S.status == 0 && PS.scan_ri > 0) {
+  if (S.status == 0 && H.scan_ri > 0) {
     // DRI: one restart interval per thread, exact entry states
     // (decode_kernels.py:130-138).
-    const uint32_t ri = PS.scan_ri;
-    const uint32_t lim_mcu = (uint32_t)S.row_stop * S.gx;
+    const uint32_t ri = H.scan_ri;
+    const uint32_t lim_mcu = (uint32_t)H.row_stop * H.gx;
     const uint32_t nint = (lim_mcu + ri - 1) / ri;
     if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
     __syncthreads();
     for (uint32_t j = tid; j < nint; j += kNT) {
-      if (j >= 1 && (int)(j - 1) >= S.n_restarts) {  // status 3
+      if (j >= 1 && (int)(j - 1) >= H.n_restarts) {  // status 3
         atomicMin(&S.red_i[0], (int)(2 * j + 1));
         continue;
       }
       const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
       int32_t pred[3] = {0, 0, 0};
       RunState o;
-      const uint32_t blk0 = j * ri * S.bpm;
-      const uint32_t lim = min((j + 1) * ri, lim_mcu) * S.bpm;
-      decode_run<RUN_WRITE>(S, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
+      const uint32_t blk0 = j * ri * H.bpm;
+      const uint32_t lim = min((j + 1) * ri, lim_mcu) * H.bpm;
+      decode_run<RUN_WRITE>(H, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
       if (o.err) atomicMin(&S.red_i[0], (int)(2 * j));
       if (o.coef_range) S.coef_range = 1;
     }
@@ -1090,30 +1162,30 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       if (code != 0x7FFFFFFF) {
         const uint32_t j = code >> 1;
         if (code & 1) {
-          set_status(S, ESSL_ST_MISSING_RST, 0, PS.scan_start);
+          ent_status(S, ESSL_ST_MISSING_RST, 0, H.scan_start);
         } else {
           const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
           RunState o;
-          decode_run<RUN_COUNT>(S, words, p0, 0, 0, kNoEnd, o, 0, 0, nullptr, nullptr, nullptr);
-          set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
+          decode_run<RUN_COUNT>(H, words, p0, 0, 0, kNoEnd, o, 0, 0, nullptr, nullptr, nullptr);
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
         }
-      } else if (S.p_final != kNoEnd && S.p_final > S.clean_bits) {
-        set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      } else if (S.p_final != kNoEnd && S.p_final > H.clean_bits) {
+        ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
       }
     }
   } else if (S.status == 0 && P.mode == ESSL_DECODE_SERIAL) {
     if (tid == 0) {
       int32_t pred[3] = {0, 0, 0};
       RunState o;
-      decode_run<RUN_WRITE>(S, words, 0, 0, 0, kNoEnd, o, 0, S.limit_blocks, pred, coef,
+      decode_run<RUN_WRITE>(H, words, 0, 0, 0, kNoEnd, o, 0, H.limit_blocks, pred, coef,
                             &S.p_final);
-      if (o.err) set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
-      else if (S.p_final > S.clean_bits) set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      if (o.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
+      else if (S.p_final > H.clean_bits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
       if (o.coef_range) S.coef_range = 1;
     }
   } else if (S.status == 0) {
-    // ---- speculative parallel decode --------------------------------------
-    const uint32_t cbits = S.clean_bits;
+    // ---- speculative parallel decode ------------------------
+    const uint32_t cbits = H.clean_bits;
     int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
     nseq = max(1, min(nseq, kNT));
     const uint32_t slen = (cbits + nseq - 1) / nseq;
@@ -1126,10 +1198,10 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       int gk = 0, gb = 0;
       if (tid > 0) {  // warm-up from a guessed state
         const uint32_t wp = sbeg > (uint32_t)P.overlap_bits ? sbeg - P.overlap_bits : 0;
-        decode_run<RUN_GUESS>(S, words, wp, 0, 0, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
+        decode_run<RUN_GUESS>(H, words, wp, 0, 0, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
         gp = o.p; gk = o.k; gb = o.b;
       }
-      decode_run<RUN_COUNT>(S, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
+      decode_run<RUN_COUNT>(H, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
       R.gp = gp; R.gkb = gk | (gb << 8);
       R.ep = o.p; R.ekb = o.k | (o.b << 8);
       R.nblk = o.nblk;
@@ -1138,7 +1210,7 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
     }
     if (tid == 0) S.red_i[1] = 0;
     __syncthreads();
-    PHASE(6);
+    PHASE(2);
     int n_iter = 0;
     // fixpoint: re-decode subsequences whose entry differs from a valid
     // predecessor exit (an erroring predecessor is left alone: it is either
@@ -1159,7 +1231,7 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
         atomicAdd(&S.red_i[1], 1);
         R.gp = pp; R.gkb = pkb;
         RunState o;
-        decode_run<RUN_COUNT>(S, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr,
+        decode_run<RUN_COUNT>(H, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr,
                               nullptr);
         R.ep = o.p; R.ekb = o.k | (o.b << 8);
         R.nblk = o.nblk;
@@ -1170,58 +1242,52 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       n_iter++;
       if (!S.changed) break;
     }
-    PHASE(7);
+    PHASE(3);
     if (tid == 0) { S.t_ph[10] = n_iter; S.t_ph[11] = nseq | ((long long)S.red_i[1] << 32); }
     // prefix sums: block index and DC predictors at each subsequence entry
     uint32_t v4[4] = {tid < nseq ? R.nblk : 0u, tid < nseq ? (uint32_t)R.dc[0] : 0u,
                       tid < nseq ? (uint32_t)R.dc[1] : 0u, tid < nseq ? (uint32_t)R.dc[2] : 0u};
     uint32_t t4[4];
-    block_scan4(S, v4, t4);
+    block_scan4(S.warp_tot, v4, t4);
     const uint32_t my_entry = v4[0], tnb = t4[0];
     if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
     __syncthreads();
     if (tid < nseq && R.err == 1) atomicMin(&S.red_i[0], tid);
     __syncthreads();
     const int tstar = S.red_i[0];  // first subsequence whose true path errors
-    if (tid == tstar && my_entry + R.errblk < S.limit_blocks)
-      set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, R.errp));
+    if (tid == tstar && my_entry + R.errblk < H.limit_blocks)
+      ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, R.errp));
     __syncthreads();
-    if (tid == 0 && S.status == 0 && tstar == 0x7FFFFFFF && tnb < S.limit_blocks) {
+    if (tid == 0 && S.status == 0 && tstar == 0x7FFFFFFF && tnb < H.limit_blocks) {
       // the data ends before the crop's last MCU row: continue serially into
       // the 0xFF padding to classify corrupt (1) vs truncated (4)
       const SeqRec &Lr = S.seq[nseq - 1];
       RunState o;
       int32_t pred[3] = {0, 0, 0};
-      decode_run<RUN_WRITE>(S, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
-                            S.limit_blocks, pred, nullptr, nullptr);
-      if (o.err) set_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(PS, o.errp));
-      else set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+      decode_run<RUN_WRITE>(H, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
+                            H.limit_blocks, pred, nullptr, nullptr);
+      if (o.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
+      else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
     }
     __syncthreads();
-    PHASE(8);
+    PHASE(4);
     // write pass: crop-window coefficients, stopping at row_stop
-    if (S.status == 0 && tid < nseq && my_entry < S.limit_blocks && tid <= tstar) {
+    if (S.status == 0 && tid < nseq && my_entry < H.limit_blocks && tid <= tstar) {
       RunState o;
       int32_t pred[3] = {(int32_t)v4[1], (int32_t)v4[2], (int32_t)v4[3]};
-      decode_run<RUN_WRITE>(S, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
-                            S.limit_blocks, pred, coef, &S.p_final);
+      decode_run<RUN_WRITE>(H, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
+                            H.limit_blocks, pred, coef, &S.p_final);
       if (o.coef_range) S.coef_range = 1;
     }
     __syncthreads();
-    if (tid == 0 && S.status == 0 && S.p_final != kNoEnd && S.p_final > S.clean_bits)
-      set_status(S, ESSL_ST_TRUNCATED, 0, PS.scan_end);
+    if (tid == 0 && S.status == 0 && S.p_final != kNoEnd && S.p_final > H.clean_bits)
+      ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
   }
   __syncthreads();
-  PHASE(9);
-  if (tid == 0 && S.status == 0 && S.coef_range) set_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
-
-  // ---- quantisation table check (codec.py:405-409) ---------------------------
-  if (tid == 0 && S.status == 0) {
-    for (int i = 0; i < PS.ncomp; i++) {
-      const int tq = PS.comp_tq[i];
-      if (tq > 15 || PS.quant_pos[tq] < 0) { set_status(S, ESSL_ST_QUANT, 0, tq); break; }
-    }
-  }
+  PHASE(5);
+  if (tid == 0 && S.status == 0 && S.coef_range) ent_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
+  if (tid == 0 && S.status == 0 && H.quant_missing >= 0)
+    ent_status(S, ESSL_ST_QUANT, 0, H.quant_missing);  // codec.py:405-409
   __syncthreads();
 
   // ---- reconstruct crop-window blocks -> planes -------------------------------
@@ -1231,45 +1297,45 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       uint64_t off[3];
       for (int c = 0; c < 3; c++) {
         off[c] = total;
-        total += (uint64_t)S.wbh[c] * 8 * S.wbw[c] * 8;
+        total += (uint64_t)H.wbh[c] * 8 * H.wbw[c] * 8;
       }
       const unsigned long long base = atomicAdd(&P.s.counters[2], (unsigned long long)((total + 15) / 16 * 16));
       if (base + total > P.s.plane_cap) {
-        set_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+        ent_status(S, ESSL_ST_CAPACITY, R_SCRATCH, -1);
       } else {
         for (int c = 0; c < 3; c++) {
           info->plane_off[c] = base + off[c];
-          info->plane_pitch[c] = S.wbw[c] * 8;
-          info->wby0[c] = S.wby0[c]; info->wbx0[c] = S.wbx0[c];
-          info->wbh[c] = S.wbh[c]; info->wbw[c] = S.wbw[c];
-          info->coef_off[c] = S.coef_off[c];
+          info->plane_pitch[c] = H.wbw[c] * 8;
+          info->wby0[c] = H.wby0[c]; info->wbx0[c] = H.wbx0[c];
+          info->wbh[c] = H.wbh[c]; info->wbw[c] = H.wbw[c];
+          info->coef_off[c] = H.coef_off[c];
         }
       }
     }
     info->status = S.status;
     info->reason = S.reason;
     info->offset = S.offset;
-    info->rx = smp.x; info->ry = smp.y; info->rw = smp.w; info->rh = smp.h;
-    info->flip = smp.flip;
-    for (int i = 0; i < 12; i++) info->dbg[i] = S.t_ph[i];
+    for (int i = 0; i < 6; i++) info->dbg[2 + i] = S.t_ph[i];
+    info->dbg[10] = S.t_ph[10];
+    info->dbg[11] = S.t_ph[11];
     if (P.results) {
       essl_result r;
       r.status = S.status; r.reason = S.reason; r.offset = S.offset;
       r.mcus_entropy_decoded = S.status == 0 ? info->mcus_entropy : 0;
       r.mcus_reconstructed = S.status == 0 ? info->mcus_recon : 0;
-      r.width = PS.width; r.height = PS.height; r.ncomp = PS.ncomp;
+      r.width = info->width; r.height = info->height; r.ncomp = info->ncomp;
       P.results[img] = r;
     }
   }
   __syncthreads();
   if (S.status != 0) return;
   // 4 blocks per warp, 8 lanes per block
-  int32_t *tr = S.u.idct_tr[tid >> 5][(tid >> 3) & 3];
-  for (int c = 0; c < PS.ncomp; c++) {
-    const int hb = min(S.wby0[c] + S.wbh[c], S.bh[c]) - S.wby0[c];
-    const int wb = min(S.wbx0[c] + S.wbw[c], S.bw[c]) - S.wbx0[c];
+  int32_t *tr = S.idct_tr[tid >> 5][(tid >> 3) & 3];
+  for (int c = 0; c < H.ncomp; c++) {
+    const int hb = min(H.wby0[c] + H.wbh[c], H.bh[c]) - H.wby0[c];
+    const int wb = min(H.wbx0[c] + H.wbw[c], H.bw[c]) - H.wbx0[c];
     if (hb <= 0 || wb <= 0) continue;
-    const int pitch = S.wbw[c] * 8;
+    const int pitch = H.wbw[c] * 8;
     uint8_t *plane = P.s.plane + info->plane_off[c];
     const int nblk = hb * wb;
     const int rounds = (nblk + kNT / 8 - 1) / (kNT / 8);
@@ -1277,34 +1343,29 @@ __global__ void __launch_bounds__(kNT, 2) k_decode(DecodeParams P) {
       const int jb = rd * (kNT / 8) + (tid >> 3);
       const bool valid = jb < nblk;
       const int byr = valid ? jb / wb : 0, bxr = valid ? jb % wb : 0;
-      const int16_t *cf = coef + S.coef_off[c] + ((uint64_t)byr * S.wbw[c] + bxr) * 64;
-      idct_block_8lanes(valid, cf, S.q[c], plane + (uint64_t)byr * 8 * pitch + bxr * 8, pitch, tr);
+      const int16_t *cf = coef + H.coef_off[c] + ((uint64_t)byr * H.wbw[c] + bxr) * 64;
+      idct_block_8lanes(valid, cf, H.q[c], plane + (uint64_t)byr * 8 * pitch + bxr * 8, pitch, tr);
     }
   }
 #undef PHASE
 }
 
-// Shared-memory budget for the payload + clean stream of one image.
+// Shared-memory budget for k_prep's staged payload.
 constexpr int kMaxDynSmem = 160 * 1024;
 
-int decode_dyn_smem(int max_len) {
-  const int n_pad = (max_len + 15) / 16 * 16 + 16;
-  return 2 * n_pad + 64;
-}
+size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
 
 void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len) {
   if (p.n <= 0) return;
-  const int dyn = decode_dyn_smem(max_len);
-  if (dyn <= kMaxDynSmem) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-      attr = true;
-    }
-    k_decode<true><<<p.n, kNT, dyn, st>>>(p);
-  } else {
-    k_decode<false><<<p.n, kNT, 0, st>>>(p);
+  const int dyn = (max_len + 15) / 16 * 16 + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    attr = true;
   }
+  if (dyn <= kMaxDynSmem) k_prep<true><<<p.n, kNT, dyn, st>>>(p);
+  else k_prep<false><<<p.n, kNT, 0, st>>>(p);
+  k_entropy<<<p.n, kNT, 0, st>>>(p);
 }
 
 void init_crc_tables() {

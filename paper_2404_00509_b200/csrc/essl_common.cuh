@@ -54,6 +54,7 @@ struct Scratch {
   uint64_t plane_cap;
   unsigned long long *counters;  // [0] clean bytes, [1] coef elems, [2] plane bytes
   ImgInfo *info;
+  uint8_t *hdr;  // per-image DecodeHdr handed from k_prep to k_entropy
 };
 
 struct DecodeParams {
@@ -96,6 +97,7 @@ __host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t ep
 
 // launch wrappers (defined in the .cu files)
 void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len);
+size_t decode_hdr_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);

@@ -100,7 +100,7 @@ class ImageBatch:
         return int(self.pixels.shape[0])
 
 
-_GPU_KEYS = ("device", "out_dtype", "rank", "world_size", "resident", "prefetch")
+_GPU_KEYS = ("device", "out_dtype", "rank", "world_size", "resident", "prefetch", "streams")
 
 
 @dataclass
@@ -126,6 +126,7 @@ class LoaderConfig:
     world_size: int = 1
     resident: bool = True
     prefetch: int = 2
+    streams: int = 2
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
@@ -165,6 +166,8 @@ class LoaderConfig:
             raise ConfigError(f"out_dtype must be float32 or bfloat16, got {self.out_dtype!r}")
         if self.world_size < 1 or not 0 <= self.rank < self.world_size:
             raise ConfigError(f"bad rank/world_size {self.rank}/{self.world_size}")
+        if self.streams < 1 or self.prefetch < 1:
+            raise ConfigError("streams and prefetch must be >= 1")
 
 
 @dataclass
@@ -201,10 +204,17 @@ class Loader:
         if dev is None:
             dev = f"cuda:{torch.cuda.current_device()}"
         w, h = self.handle.max_dims()
-        self.engine = engine if engine is not None else Engine(
-            dev, max_batch=config.batch_size, max_side=max(w, h, 16),
-            max_payload=self.handle.max_payload())
+        # one libessl context (own scratch) + one CUDA stream per batch in
+        # flight: consecutive batches overlap on the GPU
+        self._engines = [engine] if engine is not None else []
+        while len(self._engines) < config.streams:
+            self._engines.append(Engine(dev, max_batch=config.batch_size,
+                                        max_side=max(w, h, 16),
+                                        max_payload=self.handle.max_payload()))
+        self.engine = self._engines[0]
         self.device = self.engine.device
+        self._streams = [torch.cuda.Stream(self.device) for _ in self._engines]
+        self._rr = 0
         self.workers = config.workers if config.workers > 0 else (os.cpu_count() or 1)
         rec = self.handle.records
         self._widths = np.ascontiguousarray(rec["width"], np.uint16)
@@ -215,7 +225,7 @@ class Loader:
         self._labels = torch.from_numpy(rec["label"].astype(np.int64))
         self._blob = self.handle.to_device(self.device) if config.resident else None
         self._host_base = self.handle.bytes.ctypes.data if not config.resident else 0
-        self._slot = 0
+        self._slots = [0] * len(self._engines)
         self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
 
     @classmethod
@@ -273,11 +283,16 @@ class Loader:
                                        self.rrc.ratio[1], N.ptr(s)), "essl_rrc_batch")
         return s
 
-    def enqueue(self, epoch: int, idxs: np.ndarray, stream=None) -> _Pending:
-        """Issue one batch on the device (asynchronous)."""
+    def enqueue(self, epoch: int, idxs: np.ndarray) -> _Pending:
+        """Issue one batch on the device (asynchronous, on the next of the
+        loader's streams)."""
         import torch
         cfg = self.config
-        eng = self.engine
+        j = self._rr
+        self._rr = (j + 1) % len(self._engines)
+        eng, st = self._engines[j], self._streams[j]
+        cur = torch.cuda.current_stream(self.device)
+        st.wait_stream(cur)  # outputs come from the consumer stream's pool
         idxs = np.ascontiguousarray(idxs, np.int64)
         b, res = len(idxs), cfg.res
         samples = self._descriptors(epoch, idxs)
@@ -285,36 +300,68 @@ class Loader:
             blob_ptr = self._blob.data_ptr()
         else:
             ptrs = np.uint64(self._host_base) + samples["offset"].astype(np.uint64)
-            blob_ptr = eng.stage(self._slot, ptrs, samples["length"].copy(), samples,
-                                 nthreads=min(self.workers, 16), stream=stream)
-            self._slot ^= 1
+            blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
+                                 nthreads=min(self.workers, 16), stream=st)
+            self._slots[j] ^= 1
         dev = self.device
         pixels = torch.empty((b, 3, res, res), dtype=self._out_dtype, device=dev)
         u8 = torch.empty((b, res, res, 3), dtype=torch.uint8, device=dev) if cfg.keep_uint8 else None
         results = eng.new_results(b)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
-        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=stream)
-        indices = torch.from_numpy(idxs).to(dev, non_blocking=True)
-        labels = self._labels[torch.from_numpy(idxs)].to(dev, non_blocking=True)
+        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st)
+        with torch.cuda.stream(st):
+            indices = torch.from_numpy(idxs).to(dev, non_blocking=True)
+            labels = self._labels[torch.from_numpy(idxs)].to(dev, non_blocking=True)
         mask = keep = restore = None
         if self.mask_spec is not None:
             T, k = self.mask_spec.tokens, self.mask_spec.masked_count
             mask = torch.empty((b, k), dtype=torch.int32, device=dev)
             keep = torch.empty((b, T - k), dtype=torch.int64, device=dev)
             restore = torch.empty((b, T), dtype=torch.int64, device=dev)
-            eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=stream)
+            eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=st)
         res_host = torch.empty(results.shape, dtype=torch.int32, pin_memory=True)
-        res_host.copy_(results, non_blocking=True)
+        with torch.cuda.stream(st):
+            res_host.copy_(results, non_blocking=True)
+        for t in (pixels, u8, results, mask, keep, restore, indices, labels):
+            if t is not None:
+                t.record_stream(st)
         ev = torch.cuda.Event()
-        ev.record(stream if stream is not None else eng.stream())
+        ev.record(st)
         batch = ImageBatch(pixels, labels, indices, epoch, mask, u8, keep, restore)
         return _Pending(batch, samples, idxs, res_host, ev)
 
+    def join(self, p: _Pending) -> None:
+        """Make the consumer stream wait for a batch (no host sync)."""
+        import torch
+        torch.cuda.current_stream(self.device).wait_event(p.event)
+
     def finish(self, p: _Pending) -> ImageBatch:
         """Wait for a batch and raise the reference exception on failure."""
+        self.join(p)
         p.event.synchronize()
         self.engine.raise_for(p.results_host.numpy(), p.samples, p.indices)
         return p.batch
+
+    @property
+    def engines(self):
+        return list(self._engines)
+
+    def set_option(self, option: int, value: int) -> None:
+        """libessl context option (include/essl.h ESSL_OPT_*) on every stream."""
+        for e in self._engines:
+            e.set_option(option, value)
+
+    @property
+    def launches(self) -> int:
+        return sum(e.launches for e in self._engines)
+
+    def profile_read(self) -> dict:
+        tot: dict = {}
+        for e in self._engines:
+            for k, (ms, n) in e.profile_read().items():
+                a, b = tot.get(k, (0.0, 0))
+                tot[k] = (a + ms, b + n)
+        return tot
 
     def epoch(self, epoch: int):
         """Yield the batches of one epoch (this rank's shard) in permutation order."""
@@ -325,7 +372,7 @@ class Loader:
         starts = range(0, len(perm), B)
         q: deque = deque()
         it = iter(starts)
-        depth = max(1, cfg.prefetch)
+        depth = max(cfg.prefetch, len(self._engines))
         for s in it:
             q.append(self.enqueue(epoch, perm[s:s + B]))
             if len(q) >= depth:

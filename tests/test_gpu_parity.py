@@ -238,8 +238,8 @@ def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, overlap
             cfg = E.LoaderConfig(data=str(path), batch_size=32, res=160, scale=scale,
                                  mask_ratio=0.75, keep_uint8=True)
             loader = E.Loader(cfg, container=h)
-            loader.engine.set_option(N.ESSL_OPT_SEQ_BITS, seq_bits)
-            loader.engine.set_option(N.ESSL_OPT_OVERLAP_BITS, overlap)
+            loader.set_option(N.ESSL_OPT_SEQ_BITS, seq_bits)
+            loader.set_option(N.ESSL_OPT_OVERLAP_BITS, overlap)
             for b in loader.epoch(3):
                 idx = b.indices.cpu().numpy()
                 pix, u8, mask, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 3, 160,

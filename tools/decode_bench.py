@@ -16,8 +16,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-# phase k = clock(k+1) - clock(k) of the PHASE() markers in decode.cu
-PHASES = ["stage", "crc", "parse", "destuff", "tables", "pass1", "fixpoint", "scan", "write"]
+# dbg[0..1]: k_prep start/end; dbg[2..7]: k_entropy PHASE(0..5)
+PHASES = ["prep", "hdr_load", "pass1", "fixpoint", "scan_tail", "write"]
 
 
 def main():
@@ -38,7 +38,7 @@ def main():
     path = d / "pool.essl"
     E.build_synthetic(path, args.pool, args.side, args.q, seed=3)
     cfg = E.LoaderConfig(data=str(path), batch_size=args.n, res=224, out_dtype="bfloat16",
-                         mask_ratio=0.75)
+                         mask_ratio=0.75, streams=1)
     loader = E.Loader(cfg)
     eng = loader.engine
     perm = E.epoch_permutation(0, 0, len(loader.handle))
@@ -64,7 +64,7 @@ def main():
         dbg = np.zeros(12 * args.n, np.int64)
         N.check(N.lib().essl_debug_stats(eng._ctx, N.ptr(dbg), args.n))
         dbg = dbg.reshape(args.n, 12)
-        ph = np.diff(dbg[:, :10], axis=1)  # cycles per phase
+        ph = np.stack([dbg[:, 1] - dbg[:, 0]] + [dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)], 1)
         iters = dbg[:, 10]
         nseq = dbg[:, 11] & 0xFFFFFFFF
         redo = dbg[:, 11] >> 32
@@ -72,9 +72,9 @@ def main():
                "decode_ms": prof["decode"][0] / prof["decode"][1],
                "resize_ms": prof.get("resize", (0, 1))[0] / max(prof.get("resize", (0, 1))[1], 1),
                "phase_kcycles_median": {PHASES[i]: round(float(np.median(ph[:, i])) / 1e3, 1)
-                                        for i in range(9)},
+                                        for i in range(6)},
                "phase_kcycles_max": {PHASES[i]: round(float(np.max(ph[:, i])) / 1e3, 1)
-                                     for i in range(9)},
+                                     for i in range(6)},
                "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
                "nseq_mean": float(nseq.mean()), "redo_frac": float(redo.sum() / max(nseq.sum(), 1))}
         results.append(row)
