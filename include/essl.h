@@ -116,7 +116,7 @@ int64_t essl_ctx_launch_count(const essl_ctx *ctx);
  * count[ESSL_K_COUNT], and clear the record. */
 int essl_ctx_profile_read(essl_ctx *ctx, double *ms, int64_t *count);
 /* Debug: per-image decode phase clocks / counters of the last batch
- * (int64[12*n]: clock64 at 9 phase boundaries, fixpoint iterations,
+ * (int64[16*n]: k_prep/k_entropy phase clocks, fixpoint iterations,
  * subsequence count | redo count << 32).  Synchronous. */
 int essl_debug_stats(essl_ctx *ctx, int64_t *out, int n);
 const char *essl_last_error(void);

@@ -253,7 +253,7 @@ int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
   if (!c || !out || n < 0 || n > c->max_batch) return fail(ESSL_E_ARG, "essl_debug_stats: bad arguments");
   std::vector<essl::ImgInfo> info(n);
   CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
-  for (int i = 0; i < n; i++) std::memcpy(out + 12 * i, info[i].dbg, 12 * sizeof(int64_t));
+  for (int i = 0; i < n; i++) std::memcpy(out + 16 * i, info[i].dbg, 16 * sizeof(int64_t));
   return ESSL_OK;
 }
 

@@ -42,12 +42,18 @@ __constant__ uint8_t c_zz[64] = {
 
 // x^(2^k) mod P (reflected CRC-32), k = 0..31; filled by init_crc_tables().
 __constant__ uint32_t c_x2n[32];
+// Multiply-by-x^(8*kCrcChunk*2^j) mod P as 4 byte tables per level j
+// (GF(2)-linear map), global memory, filled by init_crc_tables().
+constexpr int kCrcChunk = 132;  // 33 words: lanes hit distinct smem banks
+constexpr int kCrcLevels = 16;
+__constant__ const uint32_t *c_crc_mul;  // [kCrcLevels][4][256]
+constexpr int kCrcMaxChunks = 2048;      // payloads <= 256 KB use the table tree
 
 constexpr uint32_t kErrP = 0xFFFFFFFFu;  // error exit-state marker
 constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
 constexpr int kNT = kDecodeThreads;
 
-struct HuffTab {
+struct __align__(16) HuffTab {
   uint16_t fast[1 << kFastBits];  // (sym << 5) | len, len in 1..kFastBits; 0 = slow path
   int32_t lim[17];                // first[L] + count[L]
   int32_t first[17];
@@ -59,7 +65,7 @@ struct HuffTab {
 
 // Geometry, stream location and tables handed from k_prep to k_entropy
 // (global, one per image; k_entropy keeps a copy in shared memory).
-struct DecodeHdr {
+struct __align__(16) DecodeHdr {
   int32_t status, reason, offset;
   int32_t ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ncomp, ntab;
   uint32_t limit_blocks, clean_bits, clean_words, tab_index_word;
@@ -99,8 +105,9 @@ struct __align__(16) PrepSmem {
   DecodeHdr h;
   struct {
     uint32_t T[4][256];  // slice-by-4 CRC tables
-    uint32_t part[kNT];
+    uint32_t part[kCrcMaxChunks];
   } crc;
+  long long ph[8];
   ParseState ps;
   uint32_t K[8];
   uint32_t warp_tot[kNT / 32][4];
@@ -662,6 +669,8 @@ __device__ __forceinline__ int corrupt_offset(const DecodeHdr &H, uint32_t errp)
   return H.scan_start + (int)min(vpos, seglen);
 }
 
+static_assert(sizeof(DecodeHdr) % 16 == 0 && offsetof(DecodeHdr, tab) % 16 == 0, "hdr copy");
+
 __device__ __forceinline__ DecodeHdr *hdr_of(const Scratch &s, int img) {
   return reinterpret_cast<DecodeHdr *>(s.hdr) + img;
 }
@@ -722,47 +731,58 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   __syncthreads();
 
   // ---- CRC32 (container.py:263) -------------------------------------------
-  // The message is viewed as 256 chunks of L bytes (L % 4 == 0) with zeros
-  // prepended (leading zeros do not change a zero-init CRC); the 0xFFFFFFFF
-  // init is applied by complementing the first 4 message bytes; chunk CRCs
-  // combine in a tree with multiplication by x^(8 L 2^j) mod P.
+  // The message is zero-prepended to C2 (a power of two) chunks of 132 bytes
+  // (leading zeros do not change a zero-init CRC); the 0xFFFFFFFF init is
+  // applied by complementing the first 4 message bytes.  Chunk CRCs
+  // (slice-by-4) combine in a binary tree; the left operand is multiplied by
+  // x^(8 * 132 * 2^j) mod P through precomputed byte tables (GF(2)-linear).
+  if (tid == 0) S.ph[0] = clock64();
   if (smp.check_crc) {
+    const int C = (n + kCrcChunk - 1) / kCrcChunk;
+    int C2 = 1, lv = 0;
+    while (C2 < C) { C2 <<= 1; lv++; }
     uint32_t crc = 0;
-    if (n < 4) {
-      if (tid == 0) {
+    if (n < 4 || C2 > kCrcMaxChunks) {
+      if (tid == 0) {  // tiny or huge payloads: serial bytewise CRC
         uint32_t c = 0xFFFFFFFFu;
         for (int i = 0; i < n; i++) c = S.crc.T[0][(c ^ raw[i]) & 0xFF] ^ (c >> 8);
         crc = c ^ 0xFFFFFFFFu;
       }
     } else {
-      const int L = ((n + kNT - 1) / kNT + 3) & ~3;
-      const int pad = kNT * L - n;
-      if (tid < 8) S.K[tid] = x2nmodp((uint64_t)L << tid, 3);
-      uint32_t c = 0;
-      for (int j = 0; j < L; j += 4) {
-        const int rp = tid * L + j - pad;
-        uint32_t w = 0;
+      const int Z = C2 * kCrcChunk - n;
+      for (int ch = tid; ch < C2; ch += kNT) {
+        uint32_t c = 0;
+        const int base = ch * kCrcChunk - Z;
+        if (base + kCrcChunk > 0) {
+#pragma unroll 3
+          for (int j = 0; j < kCrcChunk; j += 4) {
+            uint32_t w = 0;
 #pragma unroll
-        for (int b = 0; b < 4; b++) {
-          const int r = rp + b;
-          uint32_t byte = (r >= 0 && r < n) ? raw[r] : 0u;
-          if (r >= 0 && r < 4) byte ^= 0xFF;
-          w |= byte << (8 * b);
+            for (int b = 0; b < 4; b++) {
+              const int r = base + j + b;
+              uint32_t byte = r >= 0 ? raw[r] : 0u;
+              if (r >= 0 && r < 4) byte ^= 0xFF;
+              w |= byte << (8 * b);
+            }
+            c ^= w;
+            c = S.crc.T[3][c & 0xFF] ^ S.crc.T[2][(c >> 8) & 0xFF] ^ S.crc.T[1][(c >> 16) & 0xFF] ^
+                S.crc.T[0][c >> 24];
+          }
         }
-        c ^= w;
-        c = S.crc.T[3][c & 0xFF] ^ S.crc.T[2][(c >> 8) & 0xFF] ^ S.crc.T[1][(c >> 16) & 0xFF] ^
-            S.crc.T[0][c >> 24];
+        S.crc.part[ch] = c;
       }
-      S.crc.part[tid] = c;
       __syncthreads();
+      const uint32_t *M = c_crc_mul;
 #pragma unroll 1
-      for (int j = 0; (1 << j) < kNT; j++) {
+      for (int j = 0; j < lv; j++) {
         const int stride = 1 << j;
-        uint32_t v = 0;
-        const bool act = (tid % (2 * stride)) == 0;
-        if (act) v = multmodp(S.K[j], S.crc.part[tid]) ^ S.crc.part[tid + stride];
-        __syncthreads();
-        if (act) S.crc.part[tid] = v;
+        const uint32_t *T = M + j * 1024;
+        for (int i = tid * 2 * stride; i < C2; i += kNT * 2 * stride) {
+          const uint32_t a = S.crc.part[i];
+          const uint32_t m = __ldg(T + (a & 0xFF)) ^ __ldg(T + 256 + ((a >> 8) & 0xFF)) ^
+                             __ldg(T + 512 + ((a >> 16) & 0xFF)) ^ __ldg(T + 768 + (a >> 24));
+          S.crc.part[i] = m ^ S.crc.part[i + stride];
+        }
         __syncthreads();
       }
       crc = S.crc.part[0] ^ 0xFFFFFFFFu;
@@ -770,6 +790,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     if (tid == 0 && crc != smp.crc32) hdr_status(H, ESSL_ST_CRC, 0, -1);
   }
   __syncthreads();
+  if (tid == 0) S.ph[1] = clock64();
 
   // ---- parse (thread 0) + parallel entropy-segment end search --------------
   ParseState &PS = S.ps;
@@ -793,19 +814,20 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
       if (tid == 0) S.stop = n;
       __syncthreads();
       const int d0 = PS.dstart;
-      const int per = ((n - d0 + kNT - 1) / kNT + 3) & ~3;
-      const int a = d0 + tid * per, e = min(a + per, n - 1);
-      for (int i = a; i < e;) {
-        if (SMEM && (i & 3) == 0 && i + 4 <= e &&
-            !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
-          i += 4;
-          continue;
+      for (int r0 = d0 & ~15; r0 < n - 1; r0 += kNT * 16) {
+        const int a = max(r0 + tid * 16, d0), e = min(r0 + tid * 16 + 16, n - 1);
+        for (int i = a; i < e;) {
+          if (SMEM && (i & 3) == 0 && i + 4 <= e &&
+              !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
+            i += 4;
+            continue;
+          }
+          if (raw[i] == 0xFF) {
+            const int m = raw[i + 1];
+            if (!(m == 0x00 || is_rst(m) || m == 0xFF)) { atomicMin(&S.stop, i); break; }
+          }
+          i++;
         }
-        if (raw[i] == 0xFF) {
-          const int m = raw[i + 1];
-          if (!(m == 0x00 || is_rst(m) || m == 0xFF)) { atomicMin(&S.stop, i); break; }
-        }
-        i++;
       }
       __syncthreads();
       if (tid == 0) {
@@ -935,65 +957,94 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     }
   }
 
-  // ---- destuff (decode_kernels.py:27-61) into the global clean region -------
-  uint8_t *clean = P.s.clean + H.clean_off;
+  if (tid == 0) S.ph[2] = clock64();
+  // ---- destuff (decode_kernels.py:27-61) into shared memory, then one
+  //      coalesced copy to the global clean region ---------------------------
+  uint8_t *gclean = P.s.clean + H.clean_off;
+  uint8_t *clean = SMEM ? dyn + n_pad : gclean;
   if (H.status == 0) {
+    // Rounds of kNT x 16 bytes: thread t owns bytes [16t, 16t+16) of the
+    // round (16-byte shared loads, conflict-free); a block scan per round
+    // places the kept bytes.
     const int seg0 = PS.scan_start, seg1 = PS.scan_end;
-    const int segn = seg1 - seg0;
-    const int per = ((segn + kNT - 1) / kNT + 3) & ~3;
-    const int a = seg0 + tid * per, e = min(a + per, seg1);
+    constexpr int kRound = kNT * 16;
     if (tid == 0) S.stop = seg1;
     __syncthreads();
-    for (int i = a; i < e;) {
-      if (SMEM && (i & 3) == 0 && i + 4 <= e &&
-          !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
-        i += 4;
-        continue;
-      }
-      if (raw[i] == 0xFF) {
-        if (i + 1 >= seg1) { atomicMin(&S.stop, i); break; }
-        const int m = raw[i + 1];
-        if (!(m == 0x00 || is_rst(m))) { atomicMin(&S.stop, i); break; }
-      }
-      i++;
-    }
-    __syncthreads();
-    const int stop = S.stop;
-    const int e2 = min(e, stop);
-    uint32_t cnt[4] = {0, 0, 0, 0}, tot[4];
-    for (int i = a; i < e2;) {
-      if (SMEM && (i & 3) == 0 && i + 4 <= e2) {
-        const uint32_t w = *reinterpret_cast<const uint32_t *>(raw + i);
-        if (!has_ff(w)) {
-          cnt[0] += 4 - (i > seg0 && raw[i - 1] == 0xFF);
+    const int rbeg = seg0 & ~15;  // rounds start 16-byte aligned (uint4 loads)
+    for (int r0 = rbeg; r0 < seg1; r0 += kRound) {  // stop: FF not followed by 00/RSTn
+      const int g0 = r0 + tid * 16;
+      const int a = max(g0, seg0), e = min(g0 + 16, seg1);
+      for (int i = a; i < e;) {
+        if (SMEM && (i & 3) == 0 && i + 4 <= e &&
+            !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
           i += 4;
           continue;
         }
+        if (raw[i] == 0xFF) {
+          if (i + 1 >= seg1) { atomicMin(&S.stop, i); break; }
+          const int m = raw[i + 1];
+          if (!(m == 0x00 || is_rst(m))) { atomicMin(&S.stop, i); break; }
+        }
+        i++;
       }
-      const int v = raw[i];
-      const bool second = i > seg0 && raw[i - 1] == 0xFF;
-      const bool rst = v == 0xFF && is_rst(raw[i + 1]);
-      cnt[0] += (!second && !rst);
-      cnt[1] += rst;
-      i++;
     }
-    block_scan4(S.warp_tot, cnt, tot);
+    __syncthreads();
+    const int stop = S.stop;
     const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
-    uint32_t *rst_tab = reinterpret_cast<uint32_t *>(clean) + H.rst_off;
-    uint32_t kept = cnt[0], nrst = cnt[1];
-    for (int i = a; i < e2; i++) {
-      const int v = raw[i];
-      const bool second = i > seg0 && raw[i - 1] == 0xFF;
-      const bool rst = v == 0xFF && is_rst(raw[i + 1]);
-      if (rst) {
-        if ((int)nrst < max_r) rst_tab[nrst] = kept;
-        nrst++;
-      } else if (!second) {
-        clean[kept++] = (uint8_t)v;
+    uint32_t *rst_tab = reinterpret_cast<uint32_t *>(gclean) + H.rst_off;
+    uint32_t kbase = 0, rbase = 0;
+    for (int r0 = rbeg; r0 < stop; r0 += kRound) {
+      const int g0 = r0 + tid * 16;
+      const int a = max(g0, seg0), e = min(g0 + 16, stop);
+      uint32_t cnt[4] = {0, 0, 0, 0}, tot[4];
+      bool fast = false;
+      if (SMEM && a == g0 && e == a + 16) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(raw + a);
+        fast = !has_ff(w.x) && !has_ff(w.y) && !has_ff(w.z) && !has_ff(w.w) &&
+               !(a > seg0 && raw[a - 1] == 0xFF);
       }
+      if (fast) {
+        cnt[0] = 16;
+      } else {
+        for (int i = a; i < e; i++) {
+          const int v = raw[i];
+          const bool second = i > seg0 && raw[i - 1] == 0xFF;
+          const bool rst = v == 0xFF && is_rst(raw[i + 1]);
+          cnt[0] += (!second && !rst);
+          cnt[1] += rst;
+        }
+      }
+      block_scan4(S.warp_tot, cnt, tot);
+      uint32_t kept = kbase + cnt[0], nrst = rbase + cnt[1];
+      if (fast) {
+#pragma unroll
+        for (int i = 0; i < 16; i++) clean[kept + i] = raw[a + i];
+      } else {
+        for (int i = a; i < e; i++) {
+          const int v = raw[i];
+          const bool second = i > seg0 && raw[i - 1] == 0xFF;
+          const bool rst = v == 0xFF && is_rst(raw[i + 1]);
+          if (rst) {
+            if ((int)nrst < max_r) rst_tab[nrst] = kept;
+            nrst++;
+          } else if (!second) {
+            clean[kept++] = (uint8_t)v;
+          }
+        }
+      }
+      kbase += tot[0];
+      rbase += tot[1];
     }
-    const uint32_t tk = tot[0], tr = tot[1];
+    const uint32_t tk = kbase, tr = rbase;
+    __syncthreads();
     if (tid < 16) clean[tk + tid] = 0xFF;  // 0xFF padding past the end (_br_fill)
+    if (SMEM) {
+      __syncthreads();
+      const int n16 = (int)((tk + 16 + 15) / 16);
+      const int4 *src = reinterpret_cast<const int4 *>(clean);
+      int4 *dst = reinterpret_cast<int4 *>(gclean);
+      for (int i = tid; i < n16; i += kNT) dst[i] = src[i];
+    }
     if (tid == 0) {
       H.clean_bits = tk * 8;
       H.clean_words = (tk + 3) / 4;
@@ -1003,6 +1054,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     }
   }
   __syncthreads();
+  if (tid == 0) S.ph[3] = clock64();
 
   // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
   if (tid == 0 && H.status == 0) {
@@ -1093,6 +1145,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   if (tid == 0) {
     info->dbg[0] = S.t0;
     info->dbg[1] = clock64();
+    for (int i = 0; i < 4; i++) info->dbg[12 + i] = S.ph[i];
   }
 }
 
@@ -1357,7 +1410,7 @@ size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
 
 void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len) {
   if (p.n <= 0) return;
-  const int dyn = (max_len + 15) / 16 * 16 + 16;
+  const int dyn = 2 * ((max_len + 15) / 16 * 16 + 16) + 32;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
@@ -1382,6 +1435,28 @@ void init_crc_tables() {
   x2n[0] = p;
   for (int k = 1; k < 32; k++) x2n[k] = p = mul(p, p);
   cudaMemcpyToSymbol(c_x2n, x2n, sizeof(x2n));
+  // multiply-by-x^(8*kCrcChunk*2^j) byte tables
+  static uint32_t host[kCrcLevels][4][256];
+  uint32_t K = 0x80000000u;  // x^0
+  {
+    uint64_t e = 8ull * kCrcChunk;  // K_0 = x^(8*chunk)
+    int k = 0;
+    while (e) {
+      if (e & 1) K = mul(x2n[k & 31], K);
+      e >>= 1;
+      k++;
+    }
+  }
+  for (int j = 0; j < kCrcLevels; j++) {
+    for (int m = 0; m < 4; m++)
+      for (int v = 0; v < 256; v++) host[j][m][v] = mul(K, (uint32_t)v << (8 * m));
+    K = mul(K, K);
+  }
+  uint32_t *d = nullptr;
+  cudaMalloc(&d, sizeof(host));
+  cudaMemcpy(d, host, sizeof(host), cudaMemcpyHostToDevice);
+  const uint32_t *dc = d;
+  cudaMemcpyToSymbol(c_crc_mul, &dc, sizeof(dc));
 }
 
 }  // namespace essl

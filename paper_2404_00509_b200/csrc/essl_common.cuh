@@ -39,7 +39,7 @@ struct ImgInfo {
   uint64_t coef_off[3];   // int16 elements into Scratch::coef
   int32_t mcus_entropy, mcus_recon;
   int32_t rx, ry, rw, rh, flip;
-  int64_t dbg[12];  // phase clocks / counters (essl_debug_stats)
+  int64_t dbg[16];  // phase clocks / counters (essl_debug_stats)
 };
 
 // Device scratch owned by the context; per-image regions are carved with

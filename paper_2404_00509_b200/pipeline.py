@@ -20,6 +20,7 @@ staged per batch through a pinned double buffer.
 
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 import os
@@ -170,6 +171,29 @@ class LoaderConfig:
             raise ConfigError("streams and prefetch must be >= 1")
 
 
+class _HostRing:
+    """Pinned host buffers reused round-robin by one stream's batches
+    (indices, labels, per-image results), so the hot loop never allocates
+    page-locked memory."""
+
+    def __init__(self, depth: int, batch: int, result_words: int):
+        import torch
+        self.depth = depth
+        self.idx = [torch.empty(batch, dtype=torch.int64, pin_memory=True) for _ in range(depth)]
+        self.lab = [torch.empty(batch, dtype=torch.int64, pin_memory=True) for _ in range(depth)]
+        self.res = [torch.empty((batch, result_words), dtype=torch.int32, pin_memory=True)
+                    for _ in range(depth)]
+        self.ev = [None] * depth
+        self.next = 0
+
+    def take(self):
+        i = self.next
+        self.next = (i + 1) % self.depth
+        if self.ev[i] is not None:
+            self.ev[i].synchronize()  # the batch that used this slot is done
+        return i
+
+
 @dataclass
 class _Pending:
     batch: ImageBatch
@@ -214,6 +238,8 @@ class Loader:
         self.engine = self._engines[0]
         self.device = self.engine.device
         self._streams = [torch.cuda.Stream(self.device) for _ in self._engines]
+        self._rings = [_HostRing(2 * max(config.prefetch, config.streams) + 2, config.batch_size,
+                                 ctypes.sizeof(N.EsslResult) // 4) for _ in self._engines]
         self._rr = 0
         self.workers = config.workers if config.workers > 0 else (os.cpu_count() or 1)
         rec = self.handle.records
@@ -222,7 +248,7 @@ class Loader:
         self._offsets = np.ascontiguousarray(rec["payload_offset"], np.uint64)
         self._lengths = np.ascontiguousarray(rec["payload_length"], np.uint32)
         self._crcs = np.ascontiguousarray(rec["checksum"], np.uint32)
-        self._labels = torch.from_numpy(rec["label"].astype(np.int64))
+        self._labels_np = rec["label"].astype(np.int64)
         self._blob = self.handle.to_device(self.device) if config.resident else None
         self._host_base = self.handle.bytes.ctypes.data if not config.resident else 0
         self._slots = [0] * len(self._engines)
@@ -309,9 +335,14 @@ class Loader:
         results = eng.new_results(b)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
         eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st)
-        with torch.cuda.stream(st):
-            indices = torch.from_numpy(idxs).to(dev, non_blocking=True)
-            labels = self._labels[torch.from_numpy(idxs)].to(dev, non_blocking=True)
+        ring = self._rings[j]
+        slot = ring.take()
+        hidx, hlab, res_host = ring.idx[slot][:b], ring.lab[slot][:b], ring.res[slot][:b]
+        hidx.numpy()[:] = idxs
+        hlab.numpy()[:] = self._labels_np[idxs]
+        with torch.cuda.stream(st):  # pinned sources: truly asynchronous copies
+            indices = hidx.to(dev, non_blocking=True)
+            labels = hlab.to(dev, non_blocking=True)
         mask = keep = restore = None
         if self.mask_spec is not None:
             T, k = self.mask_spec.tokens, self.mask_spec.masked_count
@@ -319,7 +350,6 @@ class Loader:
             keep = torch.empty((b, T - k), dtype=torch.int64, device=dev)
             restore = torch.empty((b, T), dtype=torch.int64, device=dev)
             eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=st)
-        res_host = torch.empty(results.shape, dtype=torch.int32, pin_memory=True)
         with torch.cuda.stream(st):
             res_host.copy_(results, non_blocking=True)
         for t in (pixels, u8, results, mask, keep, restore, indices, labels):
@@ -327,6 +357,7 @@ class Loader:
                 t.record_stream(st)
         ev = torch.cuda.Event()
         ev.record(st)
+        ring.ev[slot] = ev
         batch = ImageBatch(pixels, labels, indices, epoch, mask, u8, keep, restore)
         return _Pending(batch, samples, idxs, res_host, ev)
 

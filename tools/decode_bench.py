@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 # dbg[0..1]: k_prep start/end; dbg[2..7]: k_entropy PHASE(0..5)
-PHASES = ["prep", "hdr_load", "pass1", "fixpoint", "scan_tail", "write"]
+PHASES = ["prep", "hdr_load", "pass1", "fixpoint", "scan_tail", "write", "p_crc", "p_parse", "p_destuff", "p_tables"]
 
 
 def main():
@@ -61,10 +61,12 @@ def main():
             loader.finish(loader.enqueue(0, perm[(r * args.n) % len(perm):][:args.n]))
         prof = eng.profile_read()
         eng.set_option(N.ESSL_OPT_PROFILE, 0)
-        dbg = np.zeros(12 * args.n, np.int64)
+        dbg = np.zeros(16 * args.n, np.int64)
         N.check(N.lib().essl_debug_stats(eng._ctx, N.ptr(dbg), args.n))
-        dbg = dbg.reshape(args.n, 12)
-        ph = np.stack([dbg[:, 1] - dbg[:, 0]] + [dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)], 1)
+        dbg = dbg.reshape(args.n, 16)
+        ph = np.stack([dbg[:, 1] - dbg[:, 0]] + [dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)]
+                      + [dbg[:, 13] - dbg[:, 12], dbg[:, 14] - dbg[:, 13], dbg[:, 15] - dbg[:, 14],
+                         dbg[:, 1] - dbg[:, 15]], 1)
         iters = dbg[:, 10]
         nseq = dbg[:, 11] & 0xFFFFFFFF
         redo = dbg[:, 11] >> 32
@@ -72,9 +74,9 @@ def main():
                "decode_ms": prof["decode"][0] / prof["decode"][1],
                "resize_ms": prof.get("resize", (0, 1))[0] / max(prof.get("resize", (0, 1))[1], 1),
                "phase_kcycles_median": {PHASES[i]: round(float(np.median(ph[:, i])) / 1e3, 1)
-                                        for i in range(6)},
+                                        for i in range(10)},
                "phase_kcycles_max": {PHASES[i]: round(float(np.max(ph[:, i])) / 1e3, 1)
-                                     for i in range(6)},
+                                     for i in range(10)},
                "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
                "nseq_mean": float(nseq.mean()), "redo_frac": float(redo.sum() / max(nseq.sum(), 1))}
         results.append(row)
