@@ -234,8 +234,8 @@ def run_gpu(args, wl):
     loader = E.Loader(cfg)
     if args.seq_bits > 0:
         loader.set_option(N.ESSL_OPT_SEQ_BITS, args.seq_bits)
-    if args.overlap_bits >= 0:
-        loader.set_option(N.ESSL_OPT_OVERLAP_BITS, args.overlap_bits)
+    if args.warm_bits >= 0:
+        loader.set_option(N.ESSL_OPT_WARMUP_BITS, args.warm_bits)
     handle = loader.handle
     perm_epochs = {}
 
@@ -384,7 +384,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
-    ap.add_argument("--overlap-bits", type=int, default=-1, help="speculative warm-up bits (-1: default)")
+    ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
     ap.add_argument("--streams", type=int, default=3,
                     help="batches in flight (one libessl context + CUDA stream each)")
     args = ap.parse_args()

@@ -62,9 +62,10 @@ extern "C" {
 #define ESSL_DECODE_SERIAL 1      /* one thread per image (validation) */
 
 #define ESSL_OPT_DECODE_MODE 1
-#define ESSL_OPT_SEQ_BITS 2     /* subsequence length target (bits) */
-#define ESSL_OPT_OVERLAP_BITS 3 /* speculative warm-up (bits) */
+#define ESSL_OPT_SEQ_BITS 2        /* minimum subsequence length per lane (bits, >= 32) */
+#define ESSL_OPT_CHECKPOINT_BITS 3 /* minimum checkpoint spacing (bits) */
 #define ESSL_OPT_PROFILE 4      /* 1: bracket every launch with CUDA events */
+#define ESSL_OPT_WARMUP_BITS 5  /* lanes start this far before their subsequence (0..4096) */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0
@@ -73,7 +74,10 @@ extern "C" {
 #define ESSL_K_MASK 3
 #define ESSL_K_GATHER 4
 #define ESSL_K_DUMP 5
-#define ESSL_K_COUNT 6
+#define ESSL_K_PREP 6    /* k_prep: CRC, parse, destuff, tables */
+#define ESSL_K_ENTROPY 7 /* k_entropy: Huffman decode */
+#define ESSL_K_IDCT 8    /* k_idct: dequant + IDCT */
+#define ESSL_K_COUNT 9
 
 typedef struct essl_ctx essl_ctx;
 
@@ -104,7 +108,8 @@ typedef struct {
  * Replaces: Loader.__init__ (pipeline.py:181-195) resource setup.  The
  * context owns device scratch sized for `max_batch` images of at most
  * `max_side` pixels per side and `max_payload` bytes each, plus pinned
- * staging for `max_batch * max_payload` bytes (double-buffered). */
+ * staging for `max_batch * max_payload` bytes (double-buffered).
+ * max_payload <= 4 MiB. */
 int essl_ctx_create(int device, int max_batch, int max_side, int max_payload,
                     int flags, essl_ctx **out);
 int essl_ctx_destroy(essl_ctx *ctx);
@@ -115,6 +120,12 @@ int64_t essl_ctx_launch_count(const essl_ctx *ctx);
  * kernel's device time (ms) and launch count into ms[ESSL_K_COUNT] /
  * count[ESSL_K_COUNT], and clear the record. */
 int essl_ctx_profile_read(essl_ctx *ctx, double *ms, int64_t *count);
+/* Profiling timeline: record a process-wide reference point on `stream`;
+ * essl_ctx_profile_timeline then returns (without clearing) up to `max`
+ * recorded launches as kernel id + start/end in ms after that reference.
+ * Returns the number written (>= 0) or a negative error. */
+int essl_profile_mark(void *stream);
+int essl_ctx_profile_timeline(essl_ctx *ctx, int32_t *kid, double *t0_ms, double *t1_ms, int max);
 /* Debug: per-image decode phase clocks / counters of the last batch
  * (int64[16*n]: k_prep/k_entropy phase clocks, fixpoint iterations,
  * subsequence count | redo count << 32).  Synchronous. */

@@ -15,13 +15,14 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libessl.so"
 ESSL_OK = 0
 ESSL_OUT_BF16_NCHW, ESSL_OUT_F32_NCHW, ESSL_OUT_NONE = 0, 1, 2
 ESSL_DECODE_SPECULATIVE, ESSL_DECODE_SERIAL = 0, 1
-ESSL_OPT_DECODE_MODE, ESSL_OPT_SEQ_BITS, ESSL_OPT_OVERLAP_BITS, ESSL_OPT_PROFILE = 1, 2, 3, 4
-KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs")
+ESSL_OPT_DECODE_MODE, ESSL_OPT_SEQ_BITS, ESSL_OPT_CHECKPOINT_BITS, ESSL_OPT_PROFILE = 1, 2, 3, 4
+ESSL_OPT_WARMUP_BITS = 5
+KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep", "entropy", "idct")
 
 # Every symbol include/essl.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
     "essl_ctx_create", "essl_ctx_destroy", "essl_ctx_set_option", "essl_ctx_launch_count",
-    "essl_ctx_profile_read", "essl_debug_stats",
+    "essl_ctx_profile_read", "essl_profile_mark", "essl_ctx_profile_timeline", "essl_debug_stats",
     "essl_last_error", "essl_version", "essl_stage", "essl_decode_rrc", "essl_decode_crop_u8",
     "essl_dump_coefs", "essl_mask", "essl_mask_from_states", "essl_gather_visible", "essl_resize_u8",
     "essl_normalize_u8", "essl_rng_init", "essl_rng_next", "essl_rng_random",
@@ -85,6 +86,8 @@ def lib():
         "essl_ctx_set_option": (i32, [P, i32, i64]),
         "essl_ctx_launch_count": (i64, [P]),
         "essl_ctx_profile_read": (i32, [P, P, P]),
+        "essl_profile_mark": (i32, [P]),
+        "essl_ctx_profile_timeline": (i32, [P, P, P, P, i32]),
         "essl_debug_stats": (i32, [P, P, i32]),
         "essl_last_error": (ctypes.c_char_p, []),
         "essl_version": (ctypes.c_char_p, []),

@@ -56,8 +56,9 @@ struct essl_ctx {
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = ESSL_DECODE_SPECULATIVE;
-  int seq_bits = 1024;
-  int overlap_bits = 1024;
+  int seq_bits = 2048;
+  int ck_bits = 64;
+  int warm_bits = 1024;
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
@@ -126,12 +127,20 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   p.s = c->s;
   p.mode = c->mode;
   p.seq_bits = c->seq_bits;
-  p.overlap_bits = c->overlap_bits;
+  p.ck_bits = c->ck_bits;
+  p.warm_bits = c->warm_bits;
   p.results = results;
   {
-    Prof pr(c, ESSL_K_DECODE, st);
-    essl::launch_decode(p, st, max_len);
-    c->launches += 1;  // k_prep + k_entropy
+    Prof pr(c, ESSL_K_PREP, st);
+    essl::launch_prep(p, st, max_len);
+  }
+  {
+    Prof pr(c, ESSL_K_ENTROPY, st);
+    essl::launch_entropy(p, st);
+  }
+  {
+    Prof pr(c, ESSL_K_IDCT, st);
+    essl::launch_idct(p, st);
   }
   CK(cudaGetLastError());
   return ESSL_OK;
@@ -147,7 +156,7 @@ const char *essl_version(void) { return "essl-b200 0.1 (sm_100a)"; }
 int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, int flags,
                     essl_ctx **out) {
   (void)flags;
-  if (!out || max_batch < 1 || max_side < 1 || max_payload < 4)
+  if (!out || max_batch < 1 || max_side < 1 || max_payload < 4 || max_payload > (1 << 22))
     return fail(ESSL_E_ARG, "essl_ctx_create: bad arguments");
   CK(cudaSetDevice(device));
   essl_ctx *c = new essl_ctx();
@@ -159,7 +168,7 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   const uint64_t side_blocks = (uint64_t)(max_side + 7) / 8 + 4;
   const uint64_t blocks = 3 * side_blocks * side_blocks;
   const uint64_t mcus = ((uint64_t)max_side + 7) / 8 * (((uint64_t)max_side + 7) / 8);
-  c->s.clean_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 64 + 4 * (mcus + 2) + 64 + 15) / 16 * 16);
+  c->s.clean_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 128 + 4 * (mcus + 2) + 64 + 15) / 16 * 16);
   c->s.coef_cap = (uint64_t)max_batch * blocks * 64;
   c->s.plane_cap = (uint64_t)max_batch * blocks * 64 + 16 * (uint64_t)max_batch;
   auto cleanup = [&](int code) {
@@ -178,6 +187,13 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   CKC(cudaMalloc(&c->s.counters, 4 * sizeof(unsigned long long)));
   CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
   CKC(cudaMalloc(&c->s.hdr, essl::decode_hdr_bytes() * max_batch));
+  CKC(cudaMalloc(&c->s.ck, essl::ckpt_bytes() * essl::kEntropyLanes * essl::kCheckpoints * max_batch));
+  // unit lists: per image <= lanes x ((slen + warm)/4 + slack + 12) entries,
+  // lanes x slen <= 8 x payload bits
+  c->s.list_cap = (uint64_t)max_batch *
+                  (2ull * max_payload + (uint64_t)essl::kEntropyLanes *
+                                            (essl::kMaxWarmBits / 4 + essl::kListSlackEntries + 12) + 8);
+  CKC(cudaMalloc(&c->s.list, c->s.list_cap * sizeof(uint32_t)));
   CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
   for (int r = 0; r < kDescRing; r++) {
     CKC(cudaMallocHost(&c->h_desc[r], sizeof(essl_sample) * max_batch));
@@ -207,6 +223,8 @@ int essl_ctx_destroy(essl_ctx *c) {
   cudaFree(c->s.counters);
   cudaFree(c->s.info);
   cudaFree(c->s.hdr);
+  cudaFree(c->s.ck);
+  cudaFree(c->s.list);
   cudaFree(c->d_offsets);
   for (int r = 0; r < kDescRing; r++) {
     if (c->h_desc[r]) cudaFreeHost(c->h_desc[r]);
@@ -236,12 +254,16 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       if (value < 32 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad seq bits");
       c->seq_bits = (int)value;
       return ESSL_OK;
+    case ESSL_OPT_WARMUP_BITS:
+      if (value < 0 || value > essl::kMaxWarmBits) return fail(ESSL_E_ARG, "bad warm-up bits");
+      c->warm_bits = (int)value;
+      return ESSL_OK;
     case ESSL_OPT_PROFILE:
       c->profile = value != 0;
       return ESSL_OK;
-    case ESSL_OPT_OVERLAP_BITS:
-      if (value < 0 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad overlap bits");
-      c->overlap_bits = (int)value;
+    case ESSL_OPT_CHECKPOINT_BITS:
+      if (value < 1 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad checkpoint bits");
+      c->ck_bits = (int)value;
       return ESSL_OK;
   }
   return fail(ESSL_E_ARG, "unknown option");
@@ -255,6 +277,33 @@ int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
   CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; i++) std::memcpy(out + 16 * i, info[i].dbg, 16 * sizeof(int64_t));
   return ESSL_OK;
+}
+
+static cudaEvent_t g_mark = nullptr;
+
+int essl_profile_mark(void *stream) {
+  if (!g_mark) CK(cudaEventCreate(&g_mark));
+  CK(cudaEventRecord(g_mark, (cudaStream_t)stream));
+  return ESSL_OK;
+}
+
+int essl_ctx_profile_timeline(essl_ctx *c, int32_t *kid, double *t0_ms, double *t1_ms, int max) {
+  if (!c || !kid || !t0_ms || !t1_ms || max < 0) return fail(ESSL_E_ARG, "essl_ctx_profile_timeline: bad arguments");
+  if (!g_mark) return fail(ESSL_E_ARG, "essl_profile_mark was not called");
+  CK(cudaEventSynchronize(g_mark));
+  int n = 0;
+  for (auto &r : c->recs) {
+    if (n >= max) break;
+    CK(cudaEventSynchronize(r.b));
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, g_mark, r.a));
+    CK(cudaEventElapsedTime(&b, g_mark, r.b));
+    kid[n] = r.kid;
+    t0_ms[n] = a;
+    t1_ms[n] = b;
+    n++;
+  }
+  return n;
 }
 
 int essl_ctx_profile_read(essl_ctx *c, double *ms, int64_t *count) {

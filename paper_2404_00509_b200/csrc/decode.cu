@@ -1,4 +1,4 @@
-// k_prep + k_entropy: one CTA per image each.  Replace, for a whole batch,
+// k_prep + k_entropy + k_idct.  Replace, for a whole batch,
 //   container.py:249-265   read_sample CRC check
 //   jpeg/codec.py:124-265  parse_stream + _finish_geometry
 //   jpeg/codec.py:272-320  _huff_lut / _destuff
@@ -6,28 +6,30 @@
 //   jpeg/codec.py:323-330  _check_consumed
 //   jpeg/decode_kernels.py:388-534 reconstruct_blocks (crop window only)
 //
-// k_prep stages the compressed payload in shared memory (16-byte loads) and
-// does the byte-level work there: CRC32, marker parse, destuff (into a global
-// clean stream), Huffman table build, window zeroing.  It hands a per-image
-// DecodeHdr to k_entropy, whose small shared footprint (~37 KB, <=64 regs)
-// keeps 4 CTAs per SM resident so that several batches can be in flight.
-// Payloads too large for shared memory are read from global (SMEM=false).
+// k_prep (one 256-thread CTA per image) stages the compressed payload in
+// shared memory (16-byte loads) and does the byte-level work there: CRC32,
+// marker parse, destuff (into a global clean stream of big-endian words),
+// Huffman table build, window zeroing.  It hands a per-image DecodeHdr to
+// k_entropy.  Payloads too large for shared memory run on global (SMEM=false).
 //
-// Entropy decoding of a restart-free baseline scan is inherently serial; it
-// is parallelised inside the CTA by self-synchronising speculative decode:
-// the clean bitstream is cut into <=256 subsequences; thread t guesses its
-// entry state by decoding `overlap_bits` before its boundary from a guessed
-// state (k=0, first block of an MCU; impossible codes re-guess one bit
-// later), decodes its subsequence counting blocks and DC differences, then a
-// fixpoint pass re-decodes every subsequence whose entry state differs from
-// its predecessor's exit state.  At the fixpoint every entry state up to the
-// first true error equals the exit state of a verified predecessor, so by
-// induction from the exact start all entry states are the reference decoder's
-// states.  A prefix scan gives each subsequence its absolute
-// block index and DC predictors, and a final pass writes coefficients of
-// crop-window blocks only, stopping at the last MCU row the crop needs
-// (codec.py:483-500 row_stop).  Streams with restart intervals (DRI) are
-// decoded one interval per thread (exact entry states).
+// k_entropy decodes one image per warp.  A restart-free baseline scan is a
+// serial chain: the decoder state (bit position, zig-zag index k, block in
+// MCU b) at any point depends on everything before it.  The clean stream is
+// cut into <= 32 subsequences; lane t decodes its subsequence from a guessed
+// state (k=0, b=0) -- a count pass that records sparse checkpoints (bit
+// position, b, blocks so far) at block starts -- then continues past its end
+// until its path reaches a checkpoint of a later lane with the same state.
+// Two decoders in the same state produce the same future, so the exact path
+// (lane 0 starts exactly) is lane 0's path, then the path of the lane it
+// merged into from the merge checkpoint, and so on.  A
+// write pass re-decodes each segment of the exact path, storing crop-window
+// coefficients only up to the last MCU row the crop needs (codec.py:483-500
+// row_stop), with DC values relative to the segment start; a warp prefix of
+// the segments' DC sums fixes them up.  Streams with restart intervals (DRI)
+// decode one interval per lane (exact entry states).
+//
+// k_idct dequantises + inverse-transforms the crop-window blocks with all
+// threads of the GPU (8 lanes per block).
 #include <cstdint>
 
 #include "essl_common.cuh"
@@ -49,19 +51,49 @@ constexpr int kCrcLevels = 16;
 __constant__ const uint32_t *c_crc_mul;  // [kCrcLevels][4][256]
 constexpr int kCrcMaxChunks = 2048;      // payloads <= 256 KB use the table tree
 
-constexpr uint32_t kErrP = 0xFFFFFFFFu;  // error exit-state marker
 constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
 constexpr int kNT = kDecodeThreads;
+constexpr int kLanes = kEntropyLanes;
+constexpr int kCk = kCheckpoints;  // checkpoints per lane
+constexpr uint32_t kListSlack = kListSlackEntries;
+
+// Huffman decode tables.  One 16-bit entry per kFastBits-bit lookahead:
+//   bits 0-4   tot  = code length + magnitude bits (0: see below)
+//   bits 5-11  kinc = zig-zag advance: DC 1; AC run+1, ZRL 16, EOB 64;
+//                     127 marks a DC category > 15 (decode error)
+//   bits 12-15 size = magnitude bits
+// tot == 0: entry 0 is an invalid code; otherwise bits 5-15 hold 1 + the
+// index of a second-level table for codes longer than kFastBits (indexed by
+// the next kSubBits bits), or kSubCanon (canonical maxcode walk, only for
+// hostile tables with more than kSubTabs long-code prefixes).  Symbol
+// semantics are those of the 16-bit LUT of codec.py:272-295 and the scan
+// loop of decode_kernels.py:139-177.
+constexpr int kSubBits = 16 - kFastBits;
+constexpr int kSubTabs = 8;
+constexpr uint32_t kSubCanon = 0x7FF;
 
 struct __align__(16) HuffTab {
-  uint16_t fast[1 << kFastBits];  // (sym << 5) | len, len in 1..kFastBits; 0 = slow path
-  int32_t lim[17];                // first[L] + count[L]
+  uint16_t fast[1 << kFastBits];
+  uint16_t sub[kSubTabs << kSubBits];
+  int32_t lim[17];  // first[L] + count[L]
   int32_t first[17];
   int16_t vptr[17];
   uint8_t vals[256];
-  int dht_pos, nvals;  // where the DHT symbols live in the payload
+  int dht_pos, nvals, is_dc, nsub;
 };
 
+__host__ __device__ __forceinline__ uint32_t huff_entry(bool dc, int sym, int len) {
+  int size, kinc;
+  if (dc) {
+    size = sym > 15 ? 1 : sym;
+    kinc = sym > 15 ? 127 : 1;
+  } else {
+    const int run = sym >> 4;
+    size = sym & 15;
+    kinc = size ? run + 1 : (run == 15 ? 16 : 64);
+  }
+  return (uint32_t)(len + size) | ((uint32_t)kinc << 5) | ((uint32_t)size << 12);
+}
 
 // Geometry, stream location and tables handed from k_prep to k_entropy
 // (global, one per image; k_entropy keeps a copy in shared memory).
@@ -69,6 +101,7 @@ struct __align__(16) DecodeHdr {
   int32_t status, reason, offset;
   int32_t ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ncomp, ntab;
   uint32_t limit_blocks, clean_bits, clean_words, tab_index_word;
+  uint32_t wmax;  // last readable word of the clean stream (0xFF padding)
   int32_t scan_ri, scan_start, scan_end, n_restarts, max_restarts;
   int32_t slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
   int32_t wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
@@ -79,15 +112,6 @@ struct __align__(16) DecodeHdr {
   uint8_t zz[64];
   int32_t q[3][64];  // dequantisation tables, natural order
   HuffTab tab[kMaxTables];
-};
-
-struct SeqRec {
-  uint32_t gp, gkb;  // entry state: bit position, k | b << 8
-  uint32_t ep, ekb;  // exit state (ep == kErrP: decode error)
-  uint32_t nblk;     // blocks completed inside the subsequence
-  int32_t dc[3];     // sum of DC differences per scan slot
-  uint32_t errblk, errp;
-  int32_t err;
 };
 
 struct ParseState {
@@ -111,19 +135,9 @@ struct __align__(16) PrepSmem {
   ParseState ps;
   uint32_t K[8];
   uint32_t warp_tot[kNT / 32][4];
+  uint16_t sub_pf[kMaxTables][kSubTabs];
   int stop;
   long long t0;
-};
-
-struct __align__(16) EntSmem {
-  DecodeHdr h;
-  SeqRec seq[kNT];
-  int32_t idct_tr[kNT / 32][4][64];
-  uint32_t warp_tot[kNT / 32][4];
-  int status, reason, offset;
-  uint32_t p_final;
-  int coef_range, changed, red_i[2];
-  long long t_ph[12];
 };
 
 // ---------------------------------------------------------------------------
@@ -319,37 +333,35 @@ __device__ void parse_until_sos(ParseState &P, const PayloadView &d) {
 }
 
 // ---------------------------------------------------------------------------
-// entropy decoding
+// entropy decoding primitives (decode_kernels.py:64-179)
 
-struct BitReader {
-  const uint32_t *w;  // big-endian byte stream as words (smem or global)
-  uint32_t nw;        // words holding data (+0xFF padding); beyond -> 0xFFFFFFFF
+struct Reader {
+  const uint32_t *w;  // clean stream as big-endian words (k_prep byte-swaps)
+  uint32_t wmax;      // last word index; reads clamp to it (all-0xFF padding)
   uint64_t buf;       // left-aligned bit buffer
   int n;              // valid bits in buf
-  uint32_t wi;        // index of `nextw`
+  uint32_t wi;        // index of nextw
   uint32_t nextw;     // prefetched next word (hides the load latency)
   uint32_t p;         // absolute bit position of buf's MSB
-  __device__ __forceinline__ uint32_t load(uint32_t i) const {
-    return i < nw ? __byte_perm(w[i], 0, 0x0123) : 0xFFFFFFFFu;
-  }
+  __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(w + min(i, wmax)); }
   __device__ __forceinline__ void init(uint32_t pos) {
     const uint32_t i = pos >> 5;
     const int off = pos & 31;
-    const uint64_t a = load(i), b = load(i + 1);
-    buf = ((a << 32) | b) << off;
+    buf = (((uint64_t)ld(i) << 32) | ld(i + 1)) << off;
     n = 64 - off;
     wi = i + 2;
-    nextw = load(wi);
+    nextw = ld(wi);
     p = pos;
   }
+  // keeps >= 33 bits buffered: one unit (code + magnitude) is <= 31 bits
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
       buf |= (uint64_t)nextw << (32 - n);
       n += 32;
-      nextw = load(++wi);
+      nextw = ld(++wi);
     }
   }
-  __device__ __forceinline__ uint32_t peek(int bits) const { return (uint32_t)(buf >> (64 - bits)); }
+  __device__ __forceinline__ uint32_t hi() const { return (uint32_t)(buf >> 32); }
   __device__ __forceinline__ void skip(int bits) {
     buf <<= bits;
     n -= bits;
@@ -357,145 +369,405 @@ struct BitReader {
   }
 };
 
-// Slow path of the Huffman decode: codes longer than kFastBits
-// (canonical maxcode walk, same symbols as the 16-bit LUT of
-// codec.py:272-295).  Returns (sym << 5) | len, or 0 for an invalid code.
-__device__ __noinline__ uint32_t decode_slow(const HuffTab &T, uint32_t code16) {
+// Long codes of a table whose long-code prefixes overflow the sub-tables
+// (hostile DHT only): canonical maxcode walk, same symbols as codec.py:272-295.
+// Long codes (rare: a divergent branch): second-level table, or the canonical
+// maxcode walk for hostile tables with more long-code prefixes than
+// sub-tables (same symbols as codec.py:272-295).
+__device__ __forceinline__ uint32_t lookup_long(const HuffTab &T, uint32_t e, uint32_t hi) {
+  const uint32_t si = e >> 5, code16 = hi >> 16;
+  if (si <= (uint32_t)kSubTabs) return T.sub[((si - 1) << kSubBits) | (code16 & ((1u << kSubBits) - 1))];
 #pragma unroll 1
   for (int L = kFastBits + 1; L <= 16; L++) {
     const int c = (int)(code16 >> (16 - L));
-    if (c < T.lim[L]) return ((uint32_t)T.vals[T.vptr[L] + c - T.first[L]] << 5) | (uint32_t)L;
+    if (c < T.lim[L] && c >= T.first[L]) return huff_entry(T.is_dc, T.vals[T.vptr[L] + c - T.first[L]], L);
   }
   return 0;
 }
 
-struct RunState {
-  uint32_t p;
-  int k, b;
-  uint32_t nblk;
-  int32_t dc[3];
-  int err;
-  uint32_t errblk, errp;
-  int coef_range;
+// Per-image decode context held in registers by every lane.
+struct EntCtx {
+  const uint8_t *tabs;  // HuffTab array (shared memory)
+  uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
+  int c1, c2, bpm, gx;
+  uint32_t cbits, limit, ck_bits;
+  const uint32_t *words;
+  uint32_t wmax;
+  __device__ __forceinline__ uint32_t tab_off(int k, int b) const {
+    const bool s1 = b >= c1, s2 = b >= c2;
+    const uint32_t d = s2 ? d2 : (s1 ? d1 : d0);
+    const uint32_t a = s2 ? a2 : (s1 ? a1 : a0);
+    return k == 0 ? d : a;
+  }
+  // first-level entry (tot == 0: long code pointer or invalid)
+  __device__ __forceinline__ uint32_t lookup_fast(int k, int b, uint32_t hi) const {
+    return reinterpret_cast<const HuffTab *>(tabs + tab_off(k, b))->fast[hi >> (32 - kFastBits)];
+  }
+  __device__ __forceinline__ uint32_t lookup_long(int k, int b, uint32_t e, uint32_t hi) const {
+    return essl::lookup_long(*reinterpret_cast<const HuffTab *>(tabs + tab_off(k, b)), e, hi);
+  }
+  __device__ __forceinline__ uint32_t lookup(int k, int b, uint32_t hi) const {
+    uint32_t e = lookup_fast(k, b, hi);
+    if ((e & 31) == 0 && e != 0) e = lookup_long(k, b, e, hi);
+    return e;
+  }
+  __device__ __forceinline__ void reader(Reader &r, uint32_t pos) const {
+    r.w = words;
+    r.wmax = wmax;
+    r.init(pos);
+  }
 };
 
-enum { RUN_COUNT = 0, RUN_WRITE = 1, RUN_GUESS = 2 };
+// One decoded unit's fields; bad <=> decode_kernels.py would return status 1
+// (invalid code, DC category > 15, or k + run > 63).
+#define UNIT_FIELDS(e, k)                                     \
+  const int tot = (int)((e) & 31);                            \
+  const int kinc = (int)(((e) >> 5) & 127);                   \
+  const int size = (int)((e) >> 12);                          \
+  const int knew = (k) + kinc;                                \
+  const bool bad = tot == 0 || (size != 0 && knew > 64)
 
-// Decode units from (p0, k0, b0) while p < end_bit (decode_kernels.py:139-177).
-//  RUN_COUNT: count completed blocks and DC differences; stop at an error.
-//  RUN_GUESS: speculative warm-up; an impossible code re-guesses (k=0, b=0)
-//             one bit after the failing unit's start.
-//  RUN_WRITE: also track the absolute block index (stop at `limit`), DC
-//             predictors, and store crop-window coefficients (natural order).
-// One unit (Huffman code + magnitude bits) per iteration as straight-line
-// predicated code: lanes of a warp sit at different states (DC/AC, EOB,
-// refill) of different subsequences, so every branch would diverge.
-template <int MODE>
-__device__ void decode_run(const DecodeHdr &S, const uint32_t *words, uint32_t p0, int k0, int b0,
-                           uint32_t end_bit, RunState &o, uint32_t blk, uint32_t limit,
-                           int32_t *pred, int16_t *coef, uint32_t *p_final) {
-  constexpr bool WRITE = MODE == RUN_WRITE;
-  BitReader br;
-  br.w = words;
-  br.nw = S.clean_words;
-  br.init(p0);
-  // register-resident per-image constants
-  const int bpm = S.bpm;
-  const int c1 = S.slot_nb[0], c2 = S.slot_nb[0] + S.slot_nb[1];
-  const uint32_t tix = S.tab_index_word;  // 4 bits per (dc/ac, slot) table index
-  int k = k0, b = b0;
-  uint32_t nblk = 0;
-  int32_t dc0 = 0, dc1 = 0, dc2 = 0;
-  o.err = 0;
-  o.coef_range = 0;
-  int mx = 0, my = 0;
-  int16_t *cur = nullptr;
-  auto locate = [&]() {
-    cur = nullptr;
-    if (coef && my >= S.my0 && my <= S.my1 && mx >= S.mx0 && mx <= S.mx1) {
-      const int s = S.blk_slot[b];
-      const int c = S.slot_comp[s];
-      const int byr = (my - S.my0) * S.slot_v[s] + S.blk_dy[b];
-      const int bxr = (mx - S.mx0) * S.slot_h[s] + S.blk_dx[b];
-      cur = coef + S.coef_off[c] + ((uint64_t)byr * S.wbw[c] + bxr) * 64;
-    }
-  };
-  if (WRITE) {
-    const uint32_t mcu = blk / bpm;
-    my = mcu / S.gx;
-    mx = mcu % S.gx;
-    locate();
+// Magnitude bits -> signed value (decode_kernels.py:101-108); size 0 -> 0.
+__device__ __forceinline__ int unit_value(uint32_t hi, int tot, int size) {
+  const uint32_t raw = (uint32_t)((uint64_t)(hi << (tot - size)) >> (32 - size));
+  const uint32_t half = (1u << size) >> 1;
+  return raw < half ? (int)raw - (int)((1u << size) - 1u) : (int)raw;
+}
+
+// Unit list entry: value (int16) << 16 | natural index << 1 | is_dc.  Every
+// unit is stored (EOB / ZRL as a zero at a position the block leaves zero);
+// a DC entry starts a block.
+__device__ __forceinline__ uint32_t unit_entry(int v, int nat, bool dc) {
+  return ((uint32_t)v << 16) | ((uint32_t)nat << 1) | (dc ? 1u : 0u);
+}
+
+// Checkpoint: the decoder state at a block start of a lane's path, with the
+// path's unit-list index and block count there.
+struct __align__(16) Ckpt {
+  uint32_t pb;   // bit position << 6 | block-in-MCU
+  uint32_t idx;  // unit-list index of the block's DC entry
+  uint32_t nblk;
+  uint32_t pad;
+};
+
+// Per-lane record (shared memory).
+struct LaneRec {
+  // phase 1 (decode from a guess): stop state, blocks, checkpoints, list
+  // length, lane-0 error
+  uint32_t xp, nblk, nck, errp, nlist;
+  int32_t xk, xb, err, ovf, xbe;
+  // phase 2 (continuation): 0 merged into checkpoint (cj, cm), 1 decode error
+  // at cp, 2 end of data at cp (state ek, eb)
+  int32_t cst, cbe;
+  uint32_t cj, cm, cn, cp, ek, eb;
+  // resolution: the lane's segment of the exact path
+  uint32_t w_idx, w_p, w_b, w_A, w_nb;
+};
+
+// Phase 1 (CONT=false): decode [p0, send) from the guess (k=0, b=0), storing
+// every unit in the lane's list and recording a checkpoint at the first block
+// start after every ck_bits.  Lane 0 starts at the exact state, so an error
+// there is the reference's error; other lanes re-guess one bit later and drop
+// their list and checkpoints (the path before an error is not a decode path).
+// Phase 2 (CONT=true): from the phase-1 stop state, decode on (appending to
+// the list) until the path reaches a checkpoint of a later lane with the same
+// (bit position, block-in-MCU) at a block start -- two decoders in the same
+// state produce the same future -- or errors, or runs off the data.
+template <bool CONT>
+__device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t send,
+                         uint32_t *list, uint32_t cap, const uint8_t *zz, Ckpt *ck_all, LaneRec *Ls,
+                         LaneRec &R) {
+  Reader r;
+  int k, b;
+  uint32_t nblk, nl, nck = 0, ck_next = p0;
+  int be = 0;
+  Ckpt *ck = ck_all + lane * kCk;
+  // continuation cursor over later lanes' checkpoints
+  int j = lane + 1;
+  uint32_t m = 0, jn = 0, cand = 0xFFFFFFFFu;
+  if (CONT) {
+    C.reader(r, R.xp);
+    k = R.xk;
+    b = R.xb;
+    nblk = 0;
+    nl = R.nlist;
+    jn = Ls[j].nck;
+    send = C.cbits;
+  } else {
+    C.reader(r, p0);
+    k = 0;
+    b = 0;
+    nblk = 0;
+    nl = 0;
   }
+  auto seek = [&](uint32_t q) {
 #pragma unroll 1
-  while (br.p < end_bit) {
-    if (WRITE && blk >= limit) break;
-    br.refill();
-    const uint32_t hi = (uint32_t)(br.buf >> 32);
-    const int s = (b >= c1) + (b >= c2);
-    const bool isdc = k == 0;
-    const int ti = (tix >> (4 * (isdc ? s : s + 3))) & 15;
-    uint32_t e = S.tab[ti].fast[hi >> (32 - kFastBits)];
-    if ((e & 31) == 0) e = decode_slow(S.tab[ti], hi >> 16);
-    const int len = e & 31;
-    const int sym = (int)(e >> 5);
-    const int size = isdc ? sym : (sym & 15);
-    const int run = sym >> 4;
-    const int kac = k + run;
-    const bool zsz = size == 0;
-    const bool bad = len == 0 || (isdc ? sym > 15 : (!zsz && kac > 63));
-    if (bad) {
-      if (MODE == RUN_GUESS) {
-        const uint32_t q = br.p + 1;
-        k = 0;
-        b = 0;
-        br.init(q);
+    while (true) {
+      if (m >= jn) {
+        if (++j >= nseq) { cand = 0xFFFFFFFFu; return; }
+        m = 0;
+        jn = Ls[j].nck;
         continue;
       }
-      o.err = 1;
-      o.errblk = nblk;
-      o.errp = br.p;
-      break;
+      cand = ck_all[j * kCk + m].pb;
+      if ((cand >> 6) >= q) return;
+      m++;
     }
-    const int total = len + size;  // <= 31: code + magnitude bits, all in `hi`
-    const uint32_t mask = (1u << size) - 1u;
-    const uint32_t raw = (hi >> (32 - total)) & mask;
-    const uint32_t half = (1u << size) >> 1;
-    const int v = raw < half ? (int)raw - (int)mask : (int)raw;  // decode_kernels.py:101-108
-    const int dv = isdc ? v : 0;
-    dc0 += s == 0 ? dv : 0;
-    dc1 += s == 1 ? dv : 0;
-    dc2 += s == 2 ? dv : 0;
-    if (WRITE) {
-      if (isdc) {
-        const int32_t pv = pred[s] + v;
-        pred[s] = pv;
-        if (cur) {
-          if (pv < -32768 || pv > 32767) o.coef_range = 1;
-          cur[0] = (int16_t)pv;
+  };
+  if (CONT) seek(r.p);
+  int st = 2;
+#pragma unroll 1
+  while (r.p < send) {
+    r.refill();
+    const uint32_t hi = r.hi();
+    uint32_t e = C.lookup_fast(k, b, hi);
+    int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
+    int knew = k + kinc;
+    if (tot == 0 || (size != 0 && knew > 64)) {  // long code or decode error (rare)
+      if (tot == 0 && e != 0) {
+        e = C.lookup_long(k, b, e, hi);
+        tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
+        knew = k + kinc;
+      }
+      if (tot == 0 || (size != 0 && knew > 64)) {
+        if (CONT || lane == 0) {
+          st = 1;
+          R.errp = r.p;
+          break;
         }
-      } else if (!zsz && cur) {
-        cur[S.zz[kac]] = (int16_t)v;
+        r.init(r.p + 1);
+        k = 0;
+        b = 0;
+        nblk = 0;
+        nl = 0;
+        nck = 0;
+        ck_next = r.p;
+        continue;
       }
     }
-    const int knew = isdc ? 1 : (zsz ? (run == 15 ? k + 16 : 64) : kac + 1);
-    br.skip(total);
-    const bool be = knew >= 64;
-    k = be ? 0 : knew;
-    nblk += be;
-    const int bn = b + 1 == bpm ? 0 : b + 1;
-    b = be ? bn : b;
-    if (WRITE && be) {
-      blk++;
-      if (b == 0 && ++mx == S.gx) { mx = 0; my++; }
-      if (blk == S.limit_blocks && p_final) *p_final = br.p;
-      locate();
+    const int v = unit_value(hi, tot, size);
+    const bool isdc = k == 0;
+    list[min(nl, cap)] = unit_entry(v, isdc ? 0 : zz[min(knew, 64) - 1], isdc);  // slot cap: sink
+    nl++;
+    r.skip(tot);
+    be = knew >= 64;
+    if (be) {
+      k = 0;
+      b = b + 1 == C.bpm ? 0 : b + 1;
+      nblk++;
+      const uint32_t pb = (r.p << 6) | (uint32_t)b;
+      if (CONT) {
+        if ((cand >> 6) < r.p) seek(r.p);
+        if (cand == pb) { st = 0; break; }
+      } else if (r.p >= ck_next && nck < (uint32_t)kCk) {
+        ck[nck] = Ckpt{pb, nl, nblk, 0u};
+        nck++;
+        ck_next = r.p + C.ck_bits;
+      }
+    } else {
+      k = knew;
     }
   }
-  o.p = o.err ? kErrP : br.p;
-  o.k = k;
-  o.b = b;
-  o.nblk = nblk;
-  o.dc[0] = dc0; o.dc[1] = dc1; o.dc[2] = dc2;
+  if (CONT) {
+    R.cst = st;
+    R.cj = (uint32_t)j;
+    R.cm = m;
+    R.cn = nblk;
+    R.cp = st == 1 ? R.errp : r.p;
+    R.ek = (uint32_t)k;
+    R.eb = (uint32_t)b;
+    R.cbe = be;
+    R.nlist = nl;
+    if (nl > cap) R.ovf = 1;
+  } else {
+    R.err = st == 1;
+    R.xp = r.p;
+    R.xk = k;
+    R.xb = b;
+    R.xbe = be;
+    R.nblk = nblk;
+    R.nck = nck;
+    R.nlist = nl;
+    R.ovf = nl > cap;
+  }
+}
+
+// Serial decode from (p, k, b) until `need` more blocks complete or a decode
+// error: returns the error's unit position or kNoEnd.  Used to classify a
+// stream whose data ends before the crop's last row (corrupt vs truncated).
+__device__ uint32_t tail_run(const EntCtx &C, uint32_t p, int k, int b, uint32_t need) {
+  Reader r;
+  C.reader(r, p);
+#pragma unroll 1
+  while (need > 0) {
+    r.refill();
+    const uint32_t e = C.lookup(k, b, r.hi());
+    UNIT_FIELDS(e, k);
+    if (bad) return r.p;
+    r.skip(tot);
+    if (knew >= 64) {
+      k = 0;
+      b = b + 1 == C.bpm ? 0 : b + 1;
+      need--;
+    } else {
+      k = knew;
+    }
+  }
+  return kNoEnd;
+}
+
+struct WriteOut {
+  int err, range;
+  uint32_t errp;
+};
+
+// Crop-window coefficient pointer of block (mx, my, b), or null outside.
+__device__ __forceinline__ int16_t *window_block(const DecodeHdr &H, int16_t *coef, int mx, int my, int b) {
+  if (my < H.my0 || my > H.my1 || mx < H.mx0 || mx > H.mx1) return nullptr;
+  const int s = H.blk_slot[b];
+  const int c = H.slot_comp[s];
+  const int byr = (my - H.my0) * H.slot_v[s] + H.blk_dy[b];
+  const int bxr = (mx - H.mx0) * H.slot_h[s] + H.blk_dx[b];
+  return coef + H.coef_off[c] + ((uint64_t)byr * H.wbw[c] + bxr) * 64;
+}
+
+// Re-decoding write pass (restart intervals, serial mode, list overflow):
+// decode `nb` blocks from (p0, k=0, b0) whose absolute block index is A,
+// storing crop-window coefficients (natural order, int16); DC predictors
+// start from pred[] (decode_kernels.py:150-177).  The block reaching `limit`
+// records the bit position after it (p_final).
+__device__ void write_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, uint32_t p0, int b0,
+                          uint32_t A, uint32_t nb, int32_t pred[3], WriteOut &o, uint32_t *p_final) {
+  Reader r;
+  C.reader(r, p0);
+  int k = 0, b = b0;
+  uint32_t blk = A;
+  const uint32_t end = A + nb;
+  const uint32_t mcu = A / (uint32_t)C.bpm;
+  int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
+  int16_t *cur = window_block(H, coef, mx, my, b);
+  int32_t pr0 = pred[0], pr1 = pred[1], pr2 = pred[2];
+  o.err = 0;
+  o.range = 0;
+#pragma unroll 1
+  while (blk < end) {
+    r.refill();
+    const uint32_t hi = r.hi();
+    const uint32_t e = C.lookup(k, b, hi);
+    UNIT_FIELDS(e, k);
+    if (bad) {
+      o.err = 1;
+      o.errp = r.p;
+      break;
+    }
+    const int v = unit_value(hi, tot, size);
+    if (k == 0) {
+      const int s = (b >= C.c1) + (b >= C.c2);
+      const int32_t pv = (s == 0 ? pr0 : (s == 1 ? pr1 : pr2)) + v;
+      pr0 = s == 0 ? pv : pr0;
+      pr1 = s == 1 ? pv : pr1;
+      pr2 = s == 2 ? pv : pr2;
+      if (cur) {
+        if (pv < -32768 || pv > 32767) o.range = 1;
+        cur[0] = (int16_t)pv;
+      }
+    } else if (size != 0 && cur) {
+      cur[H.zz[knew - 1]] = (int16_t)v;
+    }
+    r.skip(tot);
+    if (knew >= 64) {
+      k = 0;
+      blk++;
+      b = b + 1 == C.bpm ? 0 : b + 1;
+      if (b == 0 && ++mx == C.gx) { mx = 0; my++; }
+      if (blk == C.limit && p_final) *p_final = r.p;
+      cur = window_block(H, coef, mx, my, b);
+    } else {
+      k = knew;
+    }
+  }
+  pred[0] = pr0;
+  pred[1] = pr1;
+  pred[2] = pr2;
+}
+
+// Scatter pass: place `nb` blocks of a unit list (starting at the DC entry at
+// idx, block-in-MCU b0, absolute block A) into the crop window.  DC values
+// are stored relative to the run start (pred[] returns the run's DC sums);
+// the list is read as 16-byte vectors, one vector ahead.
+__device__ void scatter_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, const uint32_t *list,
+                            uint32_t idx, uint32_t end, int b0, uint32_t A, uint32_t nb,
+                            int32_t pred[3], int &range) {
+  const uint32_t mcu = A / (uint32_t)C.bpm;
+  int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
+  int b = b0;
+  int32_t pr0 = 0, pr1 = 0, pr2 = 0;
+  int16_t *cur = nullptr;
+  uint32_t done = 0;
+  bool first = true, active = true;
+  const uint4 *vec = reinterpret_cast<const uint4 *>(list);
+  uint32_t g = idx >> 2;
+  uint4 nxt = vec[g];
+#pragma unroll 1
+  for (; active && g * 4 < end; g++) {
+    const uint4 cur4 = nxt;
+    nxt = vec[g + 1];  // region slack keeps this in bounds
+    const uint32_t ev[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const uint32_t i = g * 4 + q;
+      const uint32_t e = ev[q];
+      if (!active || i < idx || i >= end) continue;
+      if (e & 1) {  // DC entry: next block
+        if (!first) {
+          if (++done == nb) { active = false; continue; }
+          b = b + 1 == C.bpm ? 0 : b + 1;
+          if (b == 0 && ++mx == C.gx) { mx = 0; my++; }
+        }
+        first = false;
+        cur = window_block(H, coef, mx, my, b);
+        const int v = (int32_t)e >> 16;
+        const int s = (b >= C.c1) + (b >= C.c2);
+        const int32_t pv = (s == 0 ? pr0 : (s == 1 ? pr1 : pr2)) + v;
+        pr0 = s == 0 ? pv : pr0;
+        pr1 = s == 1 ? pv : pr1;
+        pr2 = s == 2 ? pv : pr2;
+        if (cur) {
+          if (pv < -32768 || pv > 32767) range = 1;
+          cur[0] = (int16_t)pv;
+        }
+      } else if (cur) {
+        cur[(e >> 1) & 63] = (int16_t)((int32_t)e >> 16);
+      }
+    }
+  }
+  pred[0] = pr0;
+  pred[1] = pr1;
+  pred[2] = pr2;
+}
+
+// Adds base[slot] to the DC of every crop-window block among `nb` blocks from
+// absolute block A (block-in-MCU b0): turns run-relative DC into the
+// reference's predictor values.
+__device__ void dc_fixup(const EntCtx &C, const DecodeHdr &H, int16_t *coef, int b0, uint32_t A,
+                         uint32_t nb, const int32_t base[3], int &range) {
+  const uint32_t mcu = A / (uint32_t)C.bpm;
+  int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
+  int b = b0;
+#pragma unroll 1
+  for (uint32_t i = 0; i < nb && my <= H.my1; i++) {
+    int16_t *cur = window_block(H, coef, mx, my, b);
+    if (cur) {
+      const int s = (b >= C.c1) + (b >= C.c2);
+      const int32_t v = (int32_t)cur[0] + (s == 0 ? base[0] : (s == 1 ? base[1] : base[2]));
+      if (v < -32768 || v > 32767) range = 1;
+      cur[0] = (int16_t)v;
+    }
+    if (++b == C.bpm) {
+      b = 0;
+      if (++mx == C.gx) { mx = 0; my++; }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -653,14 +925,6 @@ __device__ __forceinline__ void hdr_status(DecodeHdr &H, int st, int reason, int
   }
 }
 
-__device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int off) {
-  if (S.status == 0) {
-    S.status = st;
-    S.reason = reason;
-    S.offset = off;
-  }
-}
-
 __device__ __forceinline__ int corrupt_offset(const DecodeHdr &H, uint32_t errp) {
   // _check_consumed: scan.start + min(vpos, seglen); the reference's reader
   // keeps >= 25 bits buffered, so vpos = ceil((p + 25) / 8) at the failing unit.
@@ -698,7 +962,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     S.t0 = clock64();
     H.status = 0; H.reason = 0; H.offset = -1;
     H.ntab = 0; H.ns = 0; H.ncomp = 0; H.quant_missing = -1;
-    H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0;
+    H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0; H.wmax = 0;
   }
   // ---- stage the payload into shared memory (16-byte loads) ----------------
   if (SMEM) {
@@ -931,7 +1195,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         const int seglen = PS.scan_end - PS.scan_start;
         H.max_restarts = PS.scan_ri ? (H.gx * H.gy) / PS.scan_ri : 0;
         const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
-        const uint64_t clean_bytes = ((uint64_t)seglen + 16 + 15) / 16 * 16;
+        const uint64_t clean_bytes = ((uint64_t)seglen + 48 + 15) / 16 * 16;
         const uint64_t alloc = (clean_bytes + 4ull * max_r + 16 + 15) / 16 * 16;
         const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)alloc);
         if (base + alloc > P.s.clean_cap) hdr_status(H, ESSL_ST_CAPACITY, R_SCRATCH, -1);
@@ -1037,16 +1301,28 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     }
     const uint32_t tk = kbase, tr = rbase;
     __syncthreads();
-    if (tid < 16) clean[tk + tid] = 0xFF;  // 0xFF padding past the end (_br_fill)
+    // 0xFF padding past the end (_br_fill), >= 2 whole words; the clean
+    // stream goes to global as big-endian words (the bit reader's order)
+    if (tid < 24) clean[tk + tid] = 0xFF;
+    __syncthreads();
+    const int nwords = (int)((tk + 3) / 4 + 2);
     if (SMEM) {
-      __syncthreads();
-      const int n16 = (int)((tk + 16 + 15) / 16);
-      const int4 *src = reinterpret_cast<const int4 *>(clean);
-      int4 *dst = reinterpret_cast<int4 *>(gclean);
-      for (int i = tid; i < n16; i += kNT) dst[i] = src[i];
+      const int n16 = (nwords + 3) / 4;
+      const uint4 *src = reinterpret_cast<const uint4 *>(clean);
+      uint4 *dst = reinterpret_cast<uint4 *>(gclean);
+      for (int i = tid; i < n16; i += kNT) {
+        uint4 v = src[i];
+        v.x = __byte_perm(v.x, 0, 0x0123); v.y = __byte_perm(v.y, 0, 0x0123);
+        v.z = __byte_perm(v.z, 0, 0x0123); v.w = __byte_perm(v.w, 0, 0x0123);
+        dst[i] = v;
+      }
+    } else {
+      uint32_t *w = reinterpret_cast<uint32_t *>(gclean);
+      for (int i = tid; i < nwords; i += kNT) w[i] = __byte_perm(w[i], 0, 0x0123);
     }
     if (tid == 0) {
       H.clean_bits = tk * 8;
+      H.wmax = (uint32_t)nwords - 1;
       H.clean_words = (tk + 3) / 4;
       H.n_restarts = (int)tr;
       if (PS.scan_ri == 0 && tr > 0) hdr_status(H, ESSL_ST_MALFORMED, R_RST_NO_DRI, seg0);
@@ -1057,6 +1333,8 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   if (tid == 0) S.ph[3] = clock64();
 
   // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
+  // Canonical first/lim/vptr per distinct (class,id) table; the long-code
+  // prefixes (codes longer than kFastBits) get second-level sub-tables.
   if (tid == 0 && H.status == 0) {
     int ntab = 0;
     int tab_pos[kMaxTables];
@@ -1087,6 +1365,19 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
           }
           T.dht_pos = pos;
           T.nvals = tot;
+          T.is_dc = pass == 0;
+          // distinct kFastBits-bit prefixes of the long codes, in code order
+          int nsub = 0, last = -1;
+          for (int L = kFastBits + 1; L <= 16; L++)
+            for (int c = T.first[L]; c < T.lim[L]; c++) {
+              const int pf = c >> (L - kFastBits);
+              if (pf != last) {
+                if (nsub < kSubTabs) S.sub_pf[ti][nsub] = (uint16_t)pf;
+                nsub++;
+                last = pf;
+              }
+            }
+          T.nsub = nsub;  // > kSubTabs: overflow, long codes use the canonical walk
         }
         if (pass == 0) slot_dc[s] = ti; else slot_ac[s] = ti;
       }
@@ -1108,22 +1399,48 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     __syncthreads();
     for (int t = 0; t < ntab; t++) {
       HuffTab &T = H.tab[t];
-      int lim[kFastBits + 1], first[kFastBits + 1], vptr[kFastBits + 1];
+      int lim[17], first[17], vptr[17];
 #pragma unroll
-      for (int L = 1; L <= kFastBits; L++) {
+      for (int L = 1; L <= 16; L++) {
         lim[L] = T.lim[L];
         first[L] = T.first[L];
         vptr[L] = T.vptr[L];
       }
+      const bool dc = T.is_dc;
+      const int nsub = T.nsub;
       for (int e = tid; e < (1 << kFastBits); e += kNT) {
-        uint16_t ent = 0;
+        uint32_t ent = 0;
+        bool found = false;
 #pragma unroll
         for (int L = kFastBits; L >= 1; L--) {  // prefix-free: at most one length matches
           const int c = e >> (kFastBits - L);
-          if (c < lim[L] && c >= first[L])
-            ent = (uint16_t)((T.vals[vptr[L] + c - first[L]] << 5) | L);
+          if (c < lim[L] && c >= first[L]) {
+            ent = huff_entry(dc, T.vals[vptr[L] + c - first[L]], L);
+            found = true;
+          }
         }
-        T.fast[e] = ent;
+        if (!found) {
+          if (nsub > kSubTabs) {
+            ent = (uint32_t)kSubCanon << 5;  // canonical walk decides (incl. invalid)
+          } else {
+            for (int q = 0; q < nsub; q++)
+              if (S.sub_pf[t][q] == e) ent = (uint32_t)(q + 1) << 5;  // sub-table q
+            // ent == 0: no code has this prefix (invalid)
+          }
+        }
+        T.fast[e] = (uint16_t)ent;
+      }
+      // sub-tables: the (16 - kFastBits) bits after each long-code prefix
+      const int ns = min(nsub, kSubTabs);
+      for (int e = tid; e < (ns << kSubBits); e += kNT) {
+        const int code16 = ((int)S.sub_pf[t][e >> kSubBits] << kSubBits) | (e & ((1 << kSubBits) - 1));
+        uint32_t ent = 0;
+#pragma unroll
+        for (int L = 16; L > kFastBits; L--) {
+          const int c = code16 >> (16 - L);
+          if (c < lim[L] && c >= first[L]) ent = huff_entry(dc, T.vals[vptr[L] + c - first[L]], L);
+        }
+        T.sub[e] = (uint16_t)ent;
       }
     }
     // zero the coefficient window (k_entropy scatters nonzeros into it)
@@ -1150,201 +1467,251 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
 }
 
 // ===========================================================================
-// k_entropy: entropy decode + IDCT (one CTA per image)
+// k_entropy: entropy decode, one warp per image
 // ===========================================================================
-__global__ void __launch_bounds__(kNT, 4) k_entropy(DecodeParams P) {
+struct __align__(16) EntSmem {
+  DecodeHdr h;
+  LaneRec lane[kLanes];
+  int status, reason, offset;
+  uint32_t p_final;
+  int coef_range, red;
+  unsigned long long lbase;
+  int32_t dcsum[kLanes * 3];
+  uint32_t sink[kLanes];
+  long long t_ph[8];
+};
+
+__device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int off) {
+  if (S.status == 0) {
+    S.status = st;
+    S.reason = reason;
+    S.offset = off;
+  }
+}
+
+__global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   __shared__ EntSmem S;
-#define PHASE(i) do { if (threadIdx.x == 0) S.t_ph[i] = clock64(); } while (0)
   const int img = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x;
   ImgInfo *info = P.s.info + img;
   const DecodeHdr *G = hdr_of(P.s, img);
   DecodeHdr &H = S.h;
-  if (tid < 12) S.t_ph[tid] = 0;
+#define PHASE(i) do { if (lane == 0) S.t_ph[i] = clock64(); } while (0)
+  if (lane < 8) S.t_ph[lane] = 0;
+  __syncthreads();
   PHASE(0);
   {
     const int head = (int)(offsetof(DecodeHdr, tab) / 16);
     const int4 *src = reinterpret_cast<const int4 *>(G);
     int4 *dst = reinterpret_cast<int4 *>(&H);
-    for (int i = tid; i < head; i += kNT) dst[i] = src[i];
+    for (int i = lane; i < head; i += kLanes) dst[i] = src[i];
   }
   __syncthreads();
   if (H.status == 0) {
     const int words = (int)(H.ntab * sizeof(HuffTab) / 16);
     const int4 *src = reinterpret_cast<const int4 *>(G->tab);
     int4 *dst = reinterpret_cast<int4 *>(H.tab);
-    for (int i = tid; i < words; i += kNT) dst[i] = src[i];
+    for (int i = lane; i < words; i += kLanes) dst[i] = src[i];
   }
-  if (tid == 0) {
+  if (lane == 0) {
     S.status = H.status; S.reason = H.reason; S.offset = H.offset;
     S.coef_range = 0;
     S.p_final = kNoEnd;
   }
+  LaneRec &R = S.lane[lane];
+  R.w_nb = 0;
+  R.nck = 0;
   __syncthreads();
   PHASE(1);
 
-  const uint8_t *clean = P.s.clean + H.clean_off;
-  const uint32_t *words = reinterpret_cast<const uint32_t *>(clean);
-  const uint32_t *rst_tab = words + H.rst_off;
+  EntCtx C;
+  C.tabs = reinterpret_cast<const uint8_t *>(H.tab);
+  {
+    const uint32_t w = H.tab_index_word;
+    const uint32_t sz = (uint32_t)sizeof(HuffTab);
+    C.d0 = (w & 15) * sz; C.d1 = ((w >> 4) & 15) * sz; C.d2 = ((w >> 8) & 15) * sz;
+    C.a0 = ((w >> 12) & 15) * sz; C.a1 = ((w >> 16) & 15) * sz; C.a2 = ((w >> 20) & 15) * sz;
+  }
+  C.c1 = H.slot_nb[0];
+  C.c2 = H.slot_nb[0] + H.slot_nb[1];
+  C.bpm = H.bpm;
+  C.gx = H.gx;
+  C.cbits = H.clean_bits;
+  C.limit = H.limit_blocks;
+  C.words = reinterpret_cast<const uint32_t *>(P.s.clean + H.clean_off);
+  C.wmax = H.wmax;
+  C.ck_bits = 0;
   int16_t *coef = P.s.coef;
+  const uint32_t *rst_tab = C.words + H.rst_off;
+  uint32_t dbg_nseq = 0, dbg_cont = 0;
+  WriteOut wo;
+  wo.range = 0;
+
   if (S.status == 0 && H.scan_ri > 0) {
-    // DRI: one restart interval per thread, exact entry states
-    // (decode_kernels.py:130-138).
+    // DRI: restart intervals decode independently from exact entry states
+    // (decode_kernels.py:130-138); lanes take intervals round-robin.
     const uint32_t ri = H.scan_ri;
     const uint32_t lim_mcu = (uint32_t)H.row_stop * H.gx;
     const uint32_t nint = (lim_mcu + ri - 1) / ri;
-    if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
+    if (lane == 0) S.red = 0x7FFFFFFF;
     __syncthreads();
-    for (uint32_t j = tid; j < nint; j += kNT) {
+    for (uint32_t j = lane; j < nint; j += kLanes) {
       if (j >= 1 && (int)(j - 1) >= H.n_restarts) {  // status 3
-        atomicMin(&S.red_i[0], (int)(2 * j + 1));
+        atomicMin(&S.red, (int)(2 * j + 1));
         continue;
       }
       const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
-      int32_t pred[3] = {0, 0, 0};
-      RunState o;
-      const uint32_t blk0 = j * ri * H.bpm;
-      const uint32_t lim = min((j + 1) * ri, lim_mcu) * H.bpm;
-      decode_run<RUN_WRITE>(H, words, p0, 0, 0, kNoEnd, o, blk0, lim, pred, coef, &S.p_final);
-      if (o.err) atomicMin(&S.red_i[0], (int)(2 * j));
-      if (o.coef_range) S.coef_range = 1;
+      const uint32_t b0 = j * ri * H.bpm;
+      const uint32_t b1 = min((j + 1) * ri, lim_mcu) * H.bpm;
+      int32_t pr[3] = {0, 0, 0};
+      write_run(C, H, coef, p0, 0, b0, b1 - b0, pr, wo, &S.p_final);
+      if (wo.err) atomicMin(&S.red, (int)(2 * j));
+      if (wo.range) S.coef_range = 1;
     }
     __syncthreads();
-    if (tid == 0) {
-      const int code = S.red_i[0];
+    if (lane == 0) {
+      const int code = S.red;
       if (code != 0x7FFFFFFF) {
         const uint32_t j = code >> 1;
         if (code & 1) {
           ent_status(S, ESSL_ST_MISSING_RST, 0, H.scan_start);
         } else {
           const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
-          RunState o;
-          decode_run<RUN_COUNT>(H, words, p0, 0, 0, kNoEnd, o, 0, 0, nullptr, nullptr, nullptr);
-          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
+          const uint32_t errp = tail_run(C, p0, 0, 0, 0xFFFFFFFFu);
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
         }
       } else if (S.p_final != kNoEnd && S.p_final > H.clean_bits) {
         ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
       }
     }
   } else if (S.status == 0 && P.mode == ESSL_DECODE_SERIAL) {
-    if (tid == 0) {
+    if (lane == 0) {
       int32_t pred[3] = {0, 0, 0};
-      RunState o;
-      decode_run<RUN_WRITE>(H, words, 0, 0, 0, kNoEnd, o, 0, H.limit_blocks, pred, coef,
-                            &S.p_final);
-      if (o.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
+      write_run(C, H, coef, 0, 0, 0, H.limit_blocks, pred, wo, &S.p_final);
+      if (wo.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, wo.errp));
       else if (S.p_final > H.clean_bits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
-      if (o.coef_range) S.coef_range = 1;
+      if (wo.range) S.coef_range = 1;
     }
   } else if (S.status == 0) {
-    // ---- speculative parallel decode ------------------------
-    const uint32_t cbits = H.clean_bits;
+    // ---- checkpoint-merge parallel decode, each unit decoded once ---------
+    const uint32_t cbits = C.cbits;
     int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
-    nseq = max(1, min(nseq, kNT));
+    nseq = max(1, min(nseq, kLanes));
     const uint32_t slen = (cbits + nseq - 1) / nseq;
-    const uint32_t sbeg = tid * slen;
-    const uint32_t send = tid == nseq - 1 ? cbits : min(cbits, (tid + 1) * slen);
-    SeqRec &R = S.seq[tid];
-    if (tid < nseq) {
-      RunState o;
-      uint32_t gp = 0;
-      int gk = 0, gb = 0;
-      if (tid > 0) {  // warm-up from a guessed state
-        const uint32_t wp = sbeg > (uint32_t)P.overlap_bits ? sbeg - P.overlap_bits : 0;
-        decode_run<RUN_GUESS>(H, words, wp, 0, 0, sbeg, o, 0, 0, nullptr, nullptr, nullptr);
-        gp = o.p; gk = o.k; gb = o.b;
-      }
-      decode_run<RUN_COUNT>(H, words, gp, gk, gb, send, o, 0, 0, nullptr, nullptr, nullptr);
-      R.gp = gp; R.gkb = gk | (gb << 8);
-      R.ep = o.p; R.ekb = o.k | (o.b << 8);
-      R.nblk = o.nblk;
-      R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
-      R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
+    const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
+    C.ck_bits = max((uint32_t)P.ck_bits, (slen + warm + kCk - 9) / (kCk - 8));
+    Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
+    // unit lists: one region per lane (16-byte aligned, 8 entries of slack
+    // for the scatter's read-ahead), carved per image
+    const uint32_t cap = ((slen + warm) / 4 + kListSlack + 3) & ~3u;
+    const uint32_t stride = cap + 8;
+    if (lane == 0) {
+      const unsigned long long need = (unsigned long long)nseq * stride;
+      const unsigned long long b = atomicAdd(&P.s.counters[3], need + 4);
+      const unsigned long long b4 = (b + 3) & ~3ull;
+      S.lbase = b4 + need > P.s.list_cap ? ~0ull : b4;
+      S.red = 0;
     }
-    if (tid == 0) S.red_i[1] = 0;
+    __syncthreads();
+    const bool lists_ok = S.lbase != ~0ull;
+    // (no room: one-entry sink per lane, every owner re-decodes)
+    uint32_t *list = lists_ok ? P.s.list + S.lbase + (unsigned long long)lane * stride : S.sink + lane;
+    const uint32_t lcap = lists_ok ? cap : 0u;  // no room: every owner re-decodes
+    if (lane < nseq) {
+      const uint32_t sbeg = lane * slen;
+      const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
+      const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
+      run_path<false>(C, lane, nseq, p0, send, list, lcap, H.zz, ck_all, S.lane, R);
+    }
     __syncthreads();
     PHASE(2);
-    int n_iter = 0;
-    // fixpoint: re-decode subsequences whose entry differs from a valid
-    // predecessor exit (an erroring predecessor is left alone: it is either
-    // fixed later or it is the true error, past which nothing is needed)
-#pragma unroll 1
-    for (int it = 0; it < nseq; it++) {
-      uint32_t pp = 0, pkb = 0;
-      bool redo = false;
-      if (tid > 0 && tid < nseq) {
-        pp = S.seq[tid - 1].ep;
-        pkb = S.seq[tid - 1].ekb;
-        redo = pp != kErrP && !(pp == R.gp && pkb == R.gkb);
-      }
-      if (tid == 0) S.changed = 0;
-      __syncthreads();
-      if (redo) {
-        S.changed = 1;
-        atomicAdd(&S.red_i[1], 1);
-        R.gp = pp; R.gkb = pkb;
-        RunState o;
-        decode_run<RUN_COUNT>(H, words, pp, pkb & 0xFF, pkb >> 8, send, o, 0, 0, nullptr, nullptr,
-                              nullptr);
-        R.ep = o.p; R.ekb = o.k | (o.b << 8);
-        R.nblk = o.nblk;
-        R.dc[0] = o.dc[0]; R.dc[1] = o.dc[1]; R.dc[2] = o.dc[2];
-        R.err = o.err; R.errblk = o.errblk; R.errp = o.errp;
-      }
-      __syncthreads();
-      n_iter++;
-      if (!S.changed) break;
-    }
+    const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
+    if (cont) run_path<true>(C, lane, nseq, 0, 0, list, lcap, H.zz, ck_all, S.lane, R);
+    dbg_nseq = (uint32_t)nseq;
+    if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
+    __syncthreads();
+    dbg_cont = (uint32_t)S.red;
     PHASE(3);
-    if (tid == 0) { S.t_ph[10] = n_iter; S.t_ph[11] = nseq | ((long long)S.red_i[1] << 32); }
-    // prefix sums: block index and DC predictors at each subsequence entry
-    uint32_t v4[4] = {tid < nseq ? R.nblk : 0u, tid < nseq ? (uint32_t)R.dc[0] : 0u,
-                      tid < nseq ? (uint32_t)R.dc[1] : 0u, tid < nseq ? (uint32_t)R.dc[2] : 0u};
-    uint32_t t4[4];
-    block_scan4(S.warp_tot, v4, t4);
-    const uint32_t my_entry = v4[0], tnb = t4[0];
-    if (tid == 0) S.red_i[0] = 0x7FFFFFFF;
-    __syncthreads();
-    if (tid < nseq && R.err == 1) atomicMin(&S.red_i[0], tid);
-    __syncthreads();
-    const int tstar = S.red_i[0];  // first subsequence whose true path errors
-    if (tid == tstar && my_entry + R.errblk < H.limit_blocks)
-      ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, R.errp));
-    __syncthreads();
-    if (tid == 0 && S.status == 0 && tstar == 0x7FFFFFFF && tnb < H.limit_blocks) {
-      // the data ends before the crop's last MCU row: continue serially into
-      // the 0xFF padding to classify corrupt (1) vs truncated (4)
-      const SeqRec &Lr = S.seq[nseq - 1];
-      RunState o;
-      int32_t pred[3] = {0, 0, 0};
-      decode_run<RUN_WRITE>(H, words, Lr.ep, Lr.ekb & 0xFF, Lr.ekb >> 8, kNoEnd, o, tnb,
-                            H.limit_blocks, pred, nullptr, nullptr);
-      if (o.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, o.errp));
-      else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+    // resolution: follow the exact path from lane 0 through the merges
+    if (lane == 0) {
+      uint32_t A = 0, sidx = 0, sp = 0, sb = 0, snb = 0;
+      int o = 0;
+      const uint32_t limit = C.limit;
+#pragma unroll 1
+      for (int hop = 0; hop < nseq; hop++) {
+        LaneRec &L = S.lane[o];
+        const uint32_t own = L.nblk - snb;
+        L.w_idx = sidx; L.w_p = sp; L.w_b = sb; L.w_A = A;
+        if (L.err) {  // error on the exact path (phase 1 of lane 0)
+          L.w_nb = min(own, limit - A);
+          if (A + own < limit) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.errp));
+          break;
+        }
+        const bool last = o == nseq - 1;
+        const uint32_t seg = own + (last ? 0u : L.cn);
+        L.w_nb = min(seg, limit - A);
+        const uint32_t end_p = last ? L.xp : L.cp;
+        const int end_be = last ? L.xbe : L.cbe;
+        if (A + seg >= limit) {
+          // the block reaching the limit ends past the data (_check_consumed)
+          if (A + seg == limit && end_be && end_p > cbits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+          break;
+        }
+        if (last || L.cst == 2) {
+          // the data ends before the crop's last MCU row: continue serially
+          // into the 0xFF padding to classify corrupt (1) vs truncated (4)
+          const uint32_t errp = tail_run(C, end_p, last ? L.xk : (int)L.ek, last ? L.xb : (int)L.eb,
+                                         limit - (A + seg));
+          if (errp != kNoEnd) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
+          else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+          break;
+        }
+        if (L.cst == 1) {
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.cp));
+          break;
+        }
+        A += seg;
+        const Ckpt c = ck_all[L.cj * kCk + L.cm];
+        o = (int)L.cj;
+        sidx = c.idx; sp = c.pb >> 6; sb = c.pb & 63; snb = c.nblk;
+      }
     }
     __syncthreads();
     PHASE(4);
-    // write pass: crop-window coefficients, stopping at row_stop
-    if (S.status == 0 && tid < nseq && my_entry < H.limit_blocks && tid <= tstar) {
-      RunState o;
-      int32_t pred[3] = {(int32_t)v4[1], (int32_t)v4[2], (int32_t)v4[3]};
-      decode_run<RUN_WRITE>(H, words, R.gp, R.gkb & 0xFF, R.gkb >> 8, send, o, my_entry,
-                            H.limit_blocks, pred, coef, &S.p_final);
-      if (o.coef_range) S.coef_range = 1;
+    // scatter the exact path's units into the crop window (DC relative to
+    // each segment), then add each segment's DC base: the prefix of the
+    // earlier segments' DC sums (segments are in lane order)
+    int32_t pred[3] = {0, 0, 0};
+    int range = 0;
+    const bool own = S.status == 0 && R.w_nb > 0;
+    if (own) {
+      if (!R.ovf && lists_ok) {
+        scatter_run(C, H, coef, list, R.w_idx, R.nlist, (int)R.w_b, R.w_A, R.w_nb, pred, range);
+      } else {
+        write_run(C, H, coef, R.w_p, (int)R.w_b, R.w_A, R.w_nb, pred, wo, nullptr);
+        range = wo.range;
+      }
     }
+    int32_t *dcs = reinterpret_cast<int32_t *>(S.dcsum);
+    for (int q = 0; q < 3; q++) dcs[lane * 3 + q] = own ? pred[q] : 0;
     __syncthreads();
-    if (tid == 0 && S.status == 0 && S.p_final != kNoEnd && S.p_final > H.clean_bits)
-      ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+    if (own) {
+      int32_t base[3] = {0, 0, 0};
+      for (int t = 0; t < lane; t++)
+        for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
+      if (base[0] | base[1] | base[2]) dc_fixup(C, H, coef, (int)R.w_b, R.w_A, R.w_nb, base, range);
+    }
+    if (range) S.coef_range = 1;
   }
   __syncthreads();
   PHASE(5);
-  if (tid == 0 && S.status == 0 && S.coef_range) ent_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
-  if (tid == 0 && S.status == 0 && H.quant_missing >= 0)
+  if (lane == 0 && S.status == 0 && S.coef_range) ent_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
+  if (lane == 0 && S.status == 0 && H.quant_missing >= 0)
     ent_status(S, ESSL_ST_QUANT, 0, H.quant_missing);  // codec.py:405-409
   __syncthreads();
 
-  // ---- reconstruct crop-window blocks -> planes -------------------------------
-  if (tid == 0) {
+  // ---- crop-plane allocation + per-image results ----------------------------
+  if (lane == 0) {
     if (S.status == 0) {
       uint64_t total = 0;
       uint64_t off[3];
@@ -1369,8 +1736,8 @@ __global__ void __launch_bounds__(kNT, 4) k_entropy(DecodeParams P) {
     info->reason = S.reason;
     info->offset = S.offset;
     for (int i = 0; i < 6; i++) info->dbg[2 + i] = S.t_ph[i];
-    info->dbg[10] = S.t_ph[10];
-    info->dbg[11] = S.t_ph[11];
+    info->dbg[10] = dbg_nseq;
+    info->dbg[11] = dbg_cont;
     if (P.results) {
       essl_result r;
       r.status = S.status; r.reason = S.reason; r.offset = S.offset;
@@ -1380,35 +1747,56 @@ __global__ void __launch_bounds__(kNT, 4) k_entropy(DecodeParams P) {
       P.results[img] = r;
     }
   }
-  __syncthreads();
-  if (S.status != 0) return;
-  // 4 blocks per warp, 8 lanes per block
-  int32_t *tr = S.idct_tr[tid >> 5][(tid >> 3) & 3];
-  for (int c = 0; c < H.ncomp; c++) {
-    const int hb = min(H.wby0[c] + H.wbh[c], H.bh[c]) - H.wby0[c];
-    const int wb = min(H.wbx0[c] + H.wbw[c], H.bw[c]) - H.wbx0[c];
-    if (hb <= 0 || wb <= 0) continue;
-    const int pitch = H.wbw[c] * 8;
-    uint8_t *plane = P.s.plane + info->plane_off[c];
-    const int nblk = hb * wb;
-    const int rounds = (nblk + kNT / 8 - 1) / (kNT / 8);
-    for (int rd = 0; rd < rounds; rd++) {
-      const int jb = rd * (kNT / 8) + (tid >> 3);
-      const bool valid = jb < nblk;
-      const int byr = valid ? jb / wb : 0, bxr = valid ? jb % wb : 0;
-      const int16_t *cf = coef + H.coef_off[c] + ((uint64_t)byr * H.wbw[c] + bxr) * 64;
-      idct_block_8lanes(valid, cf, H.q[c], plane + (uint64_t)byr * 8 * pitch + bxr * 8, pitch, tr);
-    }
-  }
 #undef PHASE
+}
+
+// ===========================================================================
+// k_idct: dequant + islow IDCT of the crop-window blocks -> Y/Cb/Cr planes
+// (decode_kernels.py:388-534 via codec.py:412-419).  grid (kIdctCtas, n).
+// ===========================================================================
+constexpr int kIdctCtas = 8;
+
+__global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
+  __shared__ int32_t q[3][64];
+  __shared__ int32_t tr[8][4][64];
+  const int img = blockIdx.y;
+  const ImgInfo &I = P.s.info[img];
+  if (I.status != 0) return;
+  const DecodeHdr *G = hdr_of(P.s, img);
+  const int tid = threadIdx.x;
+  const int ncomp = I.ncomp;
+  for (int e = tid; e < ncomp * 64; e += 256) q[e >> 6][e & 63] = G->q[e >> 6][e & 63];
+  int nb[3] = {0, 0, 0}, wb[3] = {1, 1, 1};
+  for (int c = 0; c < ncomp; c++) {
+    const int hb = min(I.wby0[c] + I.wbh[c], G->bh[c]) - I.wby0[c];
+    const int w = min(I.wbx0[c] + I.wbw[c], G->bw[c]) - I.wbx0[c];
+    if (hb > 0 && w > 0) { nb[c] = hb * w; wb[c] = w; }
+  }
+  __syncthreads();
+  const int total = nb[0] + nb[1] + nb[2];
+  int32_t *t = tr[tid >> 5][(tid >> 3) & 3];
+  for (int r0 = blockIdx.x * 32; r0 < total; r0 += kIdctCtas * 32) {
+    int jb = r0 + (tid >> 3);
+    const bool valid = jb < total;
+    int c = 0;
+    if (valid) {
+      if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
+    }
+    const int byr = valid ? jb / wb[c] : 0, bxr = valid ? jb % wb[c] : 0;
+    const int pitch = I.plane_pitch[c];
+    const int16_t *cf = P.s.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
+    uint8_t *dst = P.s.plane + I.plane_off[c] + (uint64_t)byr * 8 * pitch + bxr * 8;
+    idct_block_8lanes(valid, cf, q[c], dst, pitch, t);
+  }
 }
 
 // Shared-memory budget for k_prep's staged payload.
 constexpr int kMaxDynSmem = 160 * 1024;
 
 size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
+size_t ckpt_bytes() { return sizeof(Ckpt); }
 
-void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len) {
+void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len) {
   if (p.n <= 0) return;
   const int dyn = 2 * ((max_len + 15) / 16 * 16 + 16) + 32;
   static bool attr = false;
@@ -1418,7 +1806,14 @@ void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len) {
   }
   if (dyn <= kMaxDynSmem) k_prep<true><<<p.n, kNT, dyn, st>>>(p);
   else k_prep<false><<<p.n, kNT, 0, st>>>(p);
-  k_entropy<<<p.n, kNT, 0, st>>>(p);
+}
+
+void launch_entropy(const DecodeParams &p, cudaStream_t st) {
+  if (p.n > 0) k_entropy<<<p.n, kLanes, 0, st>>>(p);
+}
+
+void launch_idct(const DecodeParams &p, cudaStream_t st) {
+  if (p.n > 0) k_idct<<<dim3(kIdctCtas, p.n), 256, 0, st>>>(p);
 }
 
 void init_crc_tables() {

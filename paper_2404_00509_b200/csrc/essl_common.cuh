@@ -7,7 +7,13 @@
 
 namespace essl {
 
-constexpr int kDecodeThreads = 256;  // one CTA per image, one subsequence per thread
+struct Ckpt;
+
+constexpr int kDecodeThreads = 256;  // k_prep: one CTA per image
+constexpr int kCheckpoints = 64;     // k_entropy: checkpoints per lane
+constexpr int kEntropyLanes = 64;     // k_entropy: subsequences (threads) per image
+constexpr int kListSlackEntries = 1024;  // k_entropy: unit-list entries per lane beyond (slen+warm)/4
+constexpr int kMaxWarmBits = 4096;
 constexpr int kFastBits = 10;        // first-level Huffman lookahead
 constexpr int kMaxTables = 6;        // distinct (class,id) tables a 3-slot scan can use
 constexpr int kMaxBpm = 48;          // blocks per MCU (h,v <= 4, 3 components)
@@ -52,9 +58,12 @@ struct Scratch {
   uint64_t coef_cap;  // elements
   uint8_t *plane;
   uint64_t plane_cap;
-  unsigned long long *counters;  // [0] clean bytes, [1] coef elems, [2] plane bytes
+  unsigned long long *counters;  // [0] clean bytes, [1] coef elems, [2] plane bytes, [3] list entries
   ImgInfo *info;
   uint8_t *hdr;  // per-image DecodeHdr handed from k_prep to k_entropy
+  struct Ckpt *ck;  // per-image checkpoints [32 lanes][kCheckpoints] (k_entropy)
+  uint32_t *list;   // unit lists (k_entropy), carved per image with counters[3]
+  uint64_t list_cap;  // entries
 };
 
 struct DecodeParams {
@@ -63,8 +72,9 @@ struct DecodeParams {
   int n;
   Scratch s;
   int mode;          // ESSL_DECODE_*
-  int seq_bits;      // speculative subsequence target length
-  int overlap_bits;  // speculative warm-up before each subsequence
+  int seq_bits;      // minimum subsequence length per lane (bits)
+  int ck_bits;       // minimum checkpoint spacing (bits)
+  int warm_bits;     // each lane (but lane 0) starts this far before its subsequence
   essl_result *results;  // optional
 };
 
@@ -96,8 +106,11 @@ __host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t ep
 }
 
 // launch wrappers (defined in the .cu files)
-void launch_decode(const DecodeParams &p, cudaStream_t st, int max_len);
+void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len);
+void launch_entropy(const DecodeParams &p, cudaStream_t st);
+void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
+size_t ckpt_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);

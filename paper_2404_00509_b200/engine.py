@@ -79,11 +79,25 @@ class Engine:
 
     def profile_read(self) -> dict:
         """{kernel: (total_ms, launches)} since the last read (ESSL_OPT_PROFILE)."""
-        ms = np.zeros(6, np.float64)
-        cnt = np.zeros(6, np.int64)
+        ms = np.zeros(len(N.KERNELS), np.float64)
+        cnt = np.zeros(len(N.KERNELS), np.int64)
         N.check(N.lib().essl_ctx_profile_read(self._ctx, N.ptr(ms), N.ptr(cnt)),
                 "essl_ctx_profile_read")
-        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(N.KERNELS) if cnt[i]}
+        out = {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(N.KERNELS) if cnt[i]}
+        parts = [out[k] for k in ("prep", "entropy", "idct") if k in out]
+        if parts:  # the whole decode stage: k_prep + k_entropy + k_idct
+            out["decode"] = (sum(p[0] for p in parts), max(p[1] for p in parts))
+        return out
+
+    def profile_timeline(self, max_records: int = 1 << 16) -> list:
+        """[(kernel, start_ms, end_ms)] after the last essl_profile_mark
+        (ESSL_OPT_PROFILE on; call before profile_read, which clears)."""
+        kid = np.zeros(max_records, np.int32)
+        t0 = np.zeros(max_records, np.float64)
+        t1 = np.zeros(max_records, np.float64)
+        n = N.lib().essl_ctx_profile_timeline(self._ctx, N.ptr(kid), N.ptr(t0), N.ptr(t1), max_records)
+        N.check(min(n, 0), "essl_ctx_profile_timeline")
+        return [(N.KERNELS[kid[i]], float(t0[i]), float(t1[i])) for i in range(n)]
 
     def stream(self):
         return _torch().cuda.current_stream(self.device)

@@ -35,15 +35,30 @@ def E(cuda):
     return E
 
 
-@pytest.fixture(params=["speculative", "serial"])
+# speculative: library defaults; spec_dense: every lane on every stream, a
+# checkpoint at every block start, no warm-up; spec_sparse: few, far-apart
+# checkpoints (late merges, long continuations) and the longest warm-up;
+# serial: one lane (validation mode).
+MODES = {"speculative": (None, None, None), "spec_dense": (32, 1, 0), "spec_sparse": (64, 4096, 4096),
+         "serial": None}
+
+
+@pytest.fixture(params=list(MODES))
 def mode(request, E):
     from paper_2404_00509_b200 import _native as N
     from paper_2404_00509_b200.engine import default_engine
     eng = default_engine()
-    eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if request.param == "serial"
-                   else N.ESSL_DECODE_SPECULATIVE)
+    m = MODES[request.param]
+    eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if m is None else N.ESSL_DECODE_SPECULATIVE)
+    if m and m[0]:
+        eng.set_option(N.ESSL_OPT_SEQ_BITS, m[0])
+        eng.set_option(N.ESSL_OPT_CHECKPOINT_BITS, m[1])
+        eng.set_option(N.ESSL_OPT_WARMUP_BITS, m[2])
     yield request.param
     eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SPECULATIVE)
+    eng.set_option(N.ESSL_OPT_SEQ_BITS, 2048)
+    eng.set_option(N.ESSL_OPT_CHECKPOINT_BITS, 64)
+    eng.set_option(N.ESSL_OPT_WARMUP_BITS, 1024)
 
 
 @pytest.mark.parametrize("name", STREAMS)
@@ -124,6 +139,30 @@ def test_truncation_every_cut(E, oracle):
         except Exception as e:  # noqa: BLE001
             got = str(e)
         assert got == ref, cut
+
+
+def test_corruption_every_flip(E, oracle, mode):
+    """Flip entropy-coded bytes at many points: GPU status/offset or pixels ==
+    oracle (corrupt codes on the exact path, inside merges, near the end)."""
+    from paper_2404_00509_b200.errors import status_error
+    data = stream_bytes("q92")
+    info = oracle.jpeg_info(data)
+    for rect in ((0, 0, 64, 40), (0, 0, info["width"], info["height"])):
+        for pos in range(info["scan_start"] + 3, info["scan_end"] - 1, 331):
+            d = bytearray(data)
+            d[pos] ^= 0x5A
+            d = bytes(d)
+            try:
+                ref, ref_err = oracle.decode_crop(d, rect)[0], None
+            except oracle.OracleError as e:
+                ref, ref_err = None, str(status_error(e.status, e.reason, e.offset))
+            try:
+                got, got_err = E.decode_crop(d, E.CropRect(*rect))[0], None
+            except Exception as e:  # noqa: BLE001
+                got, got_err = None, str(e)
+            assert got_err == ref_err, (pos, rect, mode)
+            if ref is not None:
+                assert np.array_equal(np.asarray(got.cpu() if hasattr(got, "cpu") else got), ref), (pos, rect, mode)
 
 
 def _golden_loader(E, golden, key, dtype="float32"):
@@ -228,10 +267,11 @@ def synth_sets(E, tmp_path_factory):
     return a, b, c
 
 
-@pytest.mark.parametrize("seq_bits,overlap", [(1024, 1024), (64, 0), (4096, 256), (300, 5000)])
-def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, overlap):
-    """Synthetic datasets (random crops, all rows) through the speculative
-    decoder with adversarial subsequence settings == the oracle, bit for bit."""
+@pytest.mark.parametrize("seq_bits,ck_bits,warm", [(2048, 64, 1024), (32, 1, 0), (4096, 256, 4096),
+                                                   (300, 5000, 300)])
+def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, ck_bits, warm):
+    """Synthetic datasets (random crops, all rows) through the checkpoint-merge
+    decoder with adversarial lane / checkpoint settings == the oracle, bit for bit."""
     from paper_2404_00509_b200 import _native as N
     for path, scale in zip(synth_sets, ((0.08, 1.0), (0.2, 1.0), (0.08, 1.0))):
         with E.open_container(path) as h:
@@ -239,7 +279,8 @@ def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, overlap
                                  mask_ratio=0.75, keep_uint8=True)
             loader = E.Loader(cfg, container=h)
             loader.set_option(N.ESSL_OPT_SEQ_BITS, seq_bits)
-            loader.set_option(N.ESSL_OPT_OVERLAP_BITS, overlap)
+            loader.set_option(N.ESSL_OPT_CHECKPOINT_BITS, ck_bits)
+            loader.set_option(N.ESSL_OPT_WARMUP_BITS, warm)
             for b in loader.epoch(3):
                 idx = b.indices.cpu().numpy()
                 pix, u8, mask, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 3, 160,

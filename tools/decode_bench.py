@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 # dbg[0..1]: k_prep start/end; dbg[2..7]: k_entropy PHASE(0..5)
-PHASES = ["prep", "hdr_load", "pass1", "fixpoint", "scan_tail", "write", "p_crc", "p_parse", "p_destuff", "p_tables"]
+PHASES = ["prep", "hdr_load", "count", "continuation", "resolve", "write_fixup", "p_crc", "p_parse", "p_destuff", "p_tables"]
 
 
 def main():
@@ -42,17 +42,17 @@ def main():
     loader = E.Loader(cfg)
     eng = loader.engine
     perm = E.epoch_permutation(0, 0, len(loader.handle))
-    settings = [("spec", 1024, 1024)]
+    settings = [("spec", 2048, 1024)]
     if args.sweep:
-        settings = [("serial", 0, 0)] + [("spec", s, o) for s in (512, 1024, 2048)
-                                         for o in (256, 512, 1024, 2048)]
+        settings = [("serial", 0, 0)] + [("spec", s, w) for s in (2048, 4096, 8192)
+                                         for w in (0, 1024, 2048, 4096)]
     results = []
     for mode, sb, ov in settings:
         eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SERIAL if mode == "serial"
                        else N.ESSL_DECODE_SPECULATIVE)
         if mode == "spec":
             eng.set_option(N.ESSL_OPT_SEQ_BITS, sb)
-            eng.set_option(N.ESSL_OPT_OVERLAP_BITS, ov)
+            eng.set_option(N.ESSL_OPT_WARMUP_BITS, ov)
         idx = perm[:args.n]
         loader.finish(loader.enqueue(0, idx))  # warm
         eng.set_option(N.ESSL_OPT_PROFILE, 1)
@@ -67,18 +67,17 @@ def main():
         ph = np.stack([dbg[:, 1] - dbg[:, 0]] + [dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)]
                       + [dbg[:, 13] - dbg[:, 12], dbg[:, 14] - dbg[:, 13], dbg[:, 15] - dbg[:, 14],
                          dbg[:, 1] - dbg[:, 15]], 1)
-        iters = dbg[:, 10]
-        nseq = dbg[:, 11] & 0xFFFFFFFF
-        redo = dbg[:, 11] >> 32
-        row = {"mode": mode, "seq_bits": sb, "overlap": ov,
+        nseq = dbg[:, 10]
+        cont = dbg[:, 11]
+        row = {"mode": mode, "seq_bits": sb, "warm_bits": ov,
                "decode_ms": prof["decode"][0] / prof["decode"][1],
                "resize_ms": prof.get("resize", (0, 1))[0] / max(prof.get("resize", (0, 1))[1], 1),
                "phase_kcycles_median": {PHASES[i]: round(float(np.median(ph[:, i])) / 1e3, 1)
                                         for i in range(10)},
                "phase_kcycles_max": {PHASES[i]: round(float(np.max(ph[:, i])) / 1e3, 1)
                                      for i in range(10)},
-               "iters_mean": float(iters.mean()), "iters_max": int(iters.max()),
-               "nseq_mean": float(nseq.mean()), "redo_frac": float(redo.sum() / max(nseq.sum(), 1))}
+               "nseq_mean": float(nseq.mean()), "cont_bits_max_median": float(np.median(cont)),
+               "cont_bits_max_max": int(cont.max())}
         results.append(row)
         print(json.dumps(row), flush=True)
     if args.out:
