@@ -56,9 +56,10 @@ struct essl_ctx {
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = ESSL_DECODE_SPECULATIVE;
-  int seq_bits = 2048;
+  int seq_bits = 4096;
   int ck_bits = 64;
-  int warm_bits = 1024;
+  int warm_bits = 2048;
+  int stage_max = 64 * 1024;
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
@@ -129,6 +130,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   p.seq_bits = c->seq_bits;
   p.ck_bits = c->ck_bits;
   p.warm_bits = c->warm_bits;
+  p.stage_bytes = c->stage_max;
   p.results = results;
   {
     Prof pr(c, ESSL_K_PREP, st);
@@ -136,7 +138,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   }
   {
     Prof pr(c, ESSL_K_ENTROPY, st);
-    essl::launch_entropy(p, st);
+    essl::launch_entropy(p, st, max_len);
   }
   {
     Prof pr(c, ESSL_K_IDCT, st);
@@ -188,11 +190,11 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
   CKC(cudaMalloc(&c->s.hdr, essl::decode_hdr_bytes() * max_batch));
   CKC(cudaMalloc(&c->s.ck, essl::ckpt_bytes() * essl::kEntropyLanes * essl::kCheckpoints * max_batch));
-  // unit lists: per image <= lanes x ((slen + warm)/4 + slack + 12) entries,
-  // lanes x slen <= 8 x payload bits
+  // unit lists + block records per image: lanes x (cap + 8 + 2 (cap/2 + 10))
+  // u32, cap = (slen + warm + continuation)/4 + 68, lanes x slen <= 8 x payload
   c->s.list_cap = (uint64_t)max_batch *
-                  (2ull * max_payload + (uint64_t)essl::kEntropyLanes *
-                                            (essl::kMaxWarmBits / 4 + essl::kListSlackEntries + 12) + 8);
+                  (4ull * max_payload + (uint64_t)essl::kEntropyLanes *
+                                            (2ull * ((essl::kMaxWarmBits + essl::kContinuationBits) / 4 + 68) + 32) + 8);
   CKC(cudaMalloc(&c->s.list, c->s.list_cap * sizeof(uint32_t)));
   CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
   for (int r = 0; r < kDescRing; r++) {
@@ -257,6 +259,10 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
     case ESSL_OPT_WARMUP_BITS:
       if (value < 0 || value > essl::kMaxWarmBits) return fail(ESSL_E_ARG, "bad warm-up bits");
       c->warm_bits = (int)value;
+      return ESSL_OK;
+    case ESSL_OPT_STAGE_BYTES:
+      if (value < 0 || value > (1 << 20)) return fail(ESSL_E_ARG, "bad stage bytes");
+      c->stage_max = (int)value;
       return ESSL_OK;
     case ESSL_OPT_PROFILE:
       c->profile = value != 0;
@@ -440,7 +446,7 @@ int essl_dump_coefs(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
   CK(cudaMemcpyAsync(c->d_offsets, out_offsets, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, st));
   {
     Prof pr(c, ESSL_K_DUMP, st);
-    essl::launch_dump_coefs(c->s.info, c->s.coef, n, out, c->d_offsets, st);
+    essl::launch_dump_coefs(c->s, n, out, c->d_offsets, st);
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev_desc[ring], st));

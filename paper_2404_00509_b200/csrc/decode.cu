@@ -55,7 +55,7 @@ constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
 constexpr int kNT = kDecodeThreads;
 constexpr int kLanes = kEntropyLanes;
 constexpr int kCk = kCheckpoints;  // checkpoints per lane
-constexpr uint32_t kListSlack = kListSlackEntries;
+constexpr uint32_t kContBits = kContinuationBits;
 
 // Huffman decode tables.  One 16-bit entry per kFastBits-bit lookahead:
 //   bits 0-4   tot  = code length + magnitude bits (0: see below)
@@ -335,30 +335,43 @@ __device__ void parse_until_sos(ParseState &P, const PayloadView &d) {
 // ---------------------------------------------------------------------------
 // entropy decoding primitives (decode_kernels.py:64-179)
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Bit reader over the clean stream (big-endian words; k_prep byte-swaps),
+// in shared memory (SH, staged by k_entropy) or global memory (payloads too
+// large to stage).  Reads past the end clamp to the last word, which is all
+// 0xFF padding (_br_fill, decode_kernels.py:64-74).
+template <bool SH>
 struct Reader {
-  const uint32_t *w;  // clean stream as big-endian words (k_prep byte-swaps)
-  uint32_t wmax;      // last word index; reads clamp to it (all-0xFF padding)
+  const uint32_t *w;  // global words (!SH)
+  uint32_t ws;        // shared-window address of word 0 (SH)
+  uint32_t wmax;      // last word index
   uint64_t buf;       // left-aligned bit buffer
   int n;              // valid bits in buf
-  uint32_t wi;        // index of nextw
-  uint32_t nextw;     // prefetched next word (hides the load latency)
+  uint32_t wi;        // index of the next word to load
   uint32_t p;         // absolute bit position of buf's MSB
-  __device__ __forceinline__ uint32_t ld(uint32_t i) const { return __ldg(w + min(i, wmax)); }
+  __device__ __forceinline__ uint32_t ld(uint32_t i) const {
+    if (SH) return lds_u32(ws + (min(i, wmax) << 2));
+    return __ldg(w + min(i, wmax));
+  }
   __device__ __forceinline__ void init(uint32_t pos) {
     const uint32_t i = pos >> 5;
     const int off = pos & 31;
     buf = (((uint64_t)ld(i) << 32) | ld(i + 1)) << off;
     n = 64 - off;
     wi = i + 2;
-    nextw = ld(wi);
     p = pos;
   }
   // keeps >= 33 bits buffered: one unit (code + magnitude) is <= 31 bits
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      buf |= (uint64_t)nextw << (32 - n);
+      buf |= (uint64_t)ld(wi) << (32 - n);
       n += 32;
-      nextw = ld(++wi);
+      wi++;
     }
   }
   __device__ __forceinline__ uint32_t hi() const { return (uint32_t)(buf >> 32); }
@@ -385,13 +398,27 @@ __device__ __forceinline__ uint32_t lookup_long(const HuffTab &T, uint32_t e, ui
   return 0;
 }
 
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  unsigned short v;
+  asm("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
 // Per-image decode context held in registers by every lane.
 struct EntCtx {
   const uint8_t *tabs;  // HuffTab array (shared memory)
+  uint32_t tabs_s;      // the same, as a shared-window address
+  uint32_t zz_s;        // zig-zag -> natural table (shared-window address)
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
   int c1, c2, bpm, gx;
   uint32_t cbits, limit, ck_bits;
-  const uint32_t *words;
+  const uint32_t *words;  // clean stream (global)
+  uint32_t words_s;       // clean stream staged in shared memory (shared-window address)
   uint32_t wmax;
   __device__ __forceinline__ uint32_t tab_off(int k, int b) const {
     const bool s1 = b >= c1, s2 = b >= c2;
@@ -401,8 +428,9 @@ struct EntCtx {
   }
   // first-level entry (tot == 0: long code pointer or invalid)
   __device__ __forceinline__ uint32_t lookup_fast(int k, int b, uint32_t hi) const {
-    return reinterpret_cast<const HuffTab *>(tabs + tab_off(k, b))->fast[hi >> (32 - kFastBits)];
+    return lds_u16(tabs_s + tab_off(k, b) + ((hi >> (32 - kFastBits)) << 1));
   }
+  __device__ __forceinline__ uint32_t zz(int i) const { return lds_u8(zz_s + (uint32_t)i); }
   __device__ __forceinline__ uint32_t lookup_long(int k, int b, uint32_t e, uint32_t hi) const {
     return essl::lookup_long(*reinterpret_cast<const HuffTab *>(tabs + tab_off(k, b)), e, hi);
   }
@@ -411,8 +439,10 @@ struct EntCtx {
     if ((e & 31) == 0 && e != 0) e = lookup_long(k, b, e, hi);
     return e;
   }
-  __device__ __forceinline__ void reader(Reader &r, uint32_t pos) const {
+  template <bool SH>
+  __device__ __forceinline__ void reader(Reader<SH> &r, uint32_t pos) const {
     r.w = words;
+    r.ws = words_s;
     r.wmax = wmax;
     r.init(pos);
   }
@@ -445,7 +475,7 @@ __device__ __forceinline__ uint32_t unit_entry(int v, int nat, bool dc) {
 // path's unit-list index and block count there.
 struct __align__(16) Ckpt {
   uint32_t pb;   // bit position << 6 | block-in-MCU
-  uint32_t idx;  // unit-list index of the block's DC entry
+  uint32_t ord;  // index of the block's record in the lane's block list
   uint32_t nblk;
   uint32_t pad;
 };
@@ -454,14 +484,15 @@ struct __align__(16) Ckpt {
 struct LaneRec {
   // phase 1 (decode from a guess): stop state, blocks, checkpoints, list
   // length, lane-0 error
-  uint32_t xp, nblk, nck, errp, nlist;
+  uint32_t xp, nblk, nck, errp, nlist, nbs;
   int32_t xk, xb, err, ovf, xbe;
   // phase 2 (continuation): 0 merged into checkpoint (cj, cm), 1 decode error
   // at cp, 2 end of data at cp (state ek, eb)
   int32_t cst, cbe;
   uint32_t cj, cm, cn, cp, ek, eb;
   // resolution: the lane's segment of the exact path
-  uint32_t w_idx, w_p, w_b, w_A, w_nb;
+  uint32_t w_ord, w_p, w_b, w_A, w_nb;
+  uint32_t dbg_units, dbg_guess;
 };
 
 // Phase 1 (CONT=false): decode [p0, send) from the guess (k=0, b=0), storing
@@ -473,13 +504,13 @@ struct LaneRec {
 // the list) until the path reaches a checkpoint of a later lane with the same
 // (bit position, block-in-MCU) at a block start -- two decoders in the same
 // state produce the same future -- or errors, or runs off the data.
-template <bool CONT>
+template <bool CONT, bool SH>
 __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t send,
-                         uint32_t *list, uint32_t cap, const uint8_t *zz, Ckpt *ck_all, LaneRec *Ls,
-                         LaneRec &R) {
-  Reader r;
+                         uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, Ckpt *ck_all,
+                         LaneRec *Ls, LaneRec &R) {
+  Reader<SH> r;
   int k, b;
-  uint32_t nblk, nl, nck = 0, ck_next = p0;
+  uint32_t nblk, nl, nbs, nck = 0, ck_next = p0;
   int be = 0;
   Ckpt *ck = ck_all + lane * kCk;
   // continuation cursor over later lanes' checkpoints
@@ -491,6 +522,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     b = R.xb;
     nblk = 0;
     nl = R.nlist;
+    nbs = R.nbs;
     jn = Ls[j].nck;
     send = C.cbits;
   } else {
@@ -499,6 +531,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     b = 0;
     nblk = 0;
     nl = 0;
+    nbs = 0;
   }
   auto seek = [&](uint32_t q) {
 #pragma unroll 1
@@ -516,6 +549,9 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   };
   if (CONT) seek(r.p);
   int st = 2;
+  uint32_t dbg_units = 0, dbg_guess = 0;
+  uint32_t *lp = list + min(nl, cap);
+  uint2 *bp = bsl + min(nbs, bcap);
 #pragma unroll 1
   while (r.p < send) {
     r.refill();
@@ -536,38 +572,49 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
           break;
         }
         r.init(r.p + 1);
+        dbg_guess++;
         k = 0;
         b = 0;
         nblk = 0;
         nl = 0;
+        nbs = 0;
+        lp = list;
+        bp = bsl;
         nck = 0;
         ck_next = r.p;
         continue;
       }
     }
+    dbg_units++;
     const int v = unit_value(hi, tot, size);
     const bool isdc = k == 0;
-    list[min(nl, cap)] = unit_entry(v, isdc ? 0 : zz[min(knew, 64) - 1], isdc);  // slot cap: sink
+    *lp = unit_entry(v, isdc ? 0 : C.zz(min(knew, 64) - 1), isdc);
+    if (isdc) {  // block record: where the block's units start, its DC difference
+      *bp = make_uint2(nl, (uint32_t)v);
+      bp += nbs < bcap;
+      nbs++;
+    }
+    lp += nl < cap;  // past the capacity every store lands on the sink slot
     nl++;
     r.skip(tot);
     be = knew >= 64;
-    if (be) {
-      k = 0;
-      b = b + 1 == C.bpm ? 0 : b + 1;
-      nblk++;
-      const uint32_t pb = (r.p << 6) | (uint32_t)b;
-      if (CONT) {
+    const int bn = b + 1 == C.bpm ? 0 : b + 1;
+    k = be ? 0 : knew;
+    b = be ? bn : b;
+    nblk += be;
+    const uint32_t pb = (r.p << 6) | (uint32_t)b;
+    if (CONT) {
+      if (be) {
         if ((cand >> 6) < r.p) seek(r.p);
         if (cand == pb) { st = 0; break; }
-      } else if (r.p >= ck_next && nck < (uint32_t)kCk) {
-        ck[nck] = Ckpt{pb, nl, nblk, 0u};
-        nck++;
-        ck_next = r.p + C.ck_bits;
       }
-    } else {
-      k = knew;
+    } else if (be && r.p >= ck_next && nck < (uint32_t)kCk) {
+      ck[nck] = Ckpt{pb, nbs, nblk, 0u};
+      nck++;
+      ck_next = r.p + C.ck_bits;
     }
   }
+  const bool ovf = nl >= cap || nbs > bcap;  // (slot cap is the sink; keep one for the sentinel)
   if (CONT) {
     R.cst = st;
     R.cj = (uint32_t)j;
@@ -578,8 +625,11 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.eb = (uint32_t)b;
     R.cbe = be;
     R.nlist = nl;
-    if (nl > cap) R.ovf = 1;
+    R.nbs = nbs;
+    if (ovf) R.ovf = 1;
   } else {
+    R.dbg_units = dbg_units;
+    R.dbg_guess = dbg_guess;
     R.err = st == 1;
     R.xp = r.p;
     R.xk = k;
@@ -588,15 +638,18 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.nblk = nblk;
     R.nck = nck;
     R.nlist = nl;
-    R.ovf = nl > cap;
+    R.nbs = nbs;
+    R.ovf = ovf;
   }
+  if (!ovf) list[nl] = 1u;  // sentinel: a DC-flagged entry ends the last block
 }
 
 // Serial decode from (p, k, b) until `need` more blocks complete or a decode
 // error: returns the error's unit position or kNoEnd.  Used to classify a
 // stream whose data ends before the crop's last row (corrupt vs truncated).
+template <bool SH>
 __device__ uint32_t tail_run(const EntCtx &C, uint32_t p, int k, int b, uint32_t need) {
-  Reader r;
+  Reader<SH> r;
   C.reader(r, p);
 #pragma unroll 1
   while (need > 0) {
@@ -636,9 +689,10 @@ __device__ __forceinline__ int16_t *window_block(const DecodeHdr &H, int16_t *co
 // storing crop-window coefficients (natural order, int16); DC predictors
 // start from pred[] (decode_kernels.py:150-177).  The block reaching `limit`
 // records the bit position after it (p_final).
+template <bool SH>
 __device__ void write_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, uint32_t p0, int b0,
                           uint32_t A, uint32_t nb, int32_t pred[3], WriteOut &o, uint32_t *p_final) {
-  Reader r;
+  Reader<SH> r;
   C.reader(r, p0);
   int k = 0, b = b0;
   uint32_t blk = A;
@@ -691,77 +745,50 @@ __device__ void write_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, ui
   pred[2] = pr2;
 }
 
-// Scatter pass: place `nb` blocks of a unit list (starting at the DC entry at
-// idx, block-in-MCU b0, absolute block A) into the crop window.  DC values
-// are stored relative to the run start (pred[] returns the run's DC sums);
-// the list is read as 16-byte vectors, one vector ahead.
-__device__ void scatter_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, const uint32_t *list,
-                            uint32_t idx, uint32_t end, int b0, uint32_t A, uint32_t nb,
-                            int32_t pred[3], int &range) {
-  const uint32_t mcu = A / (uint32_t)C.bpm;
-  int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
+// DC pass A over a segment's block records (nb blocks from record `ord`,
+// block-in-MCU b0): the segment's DC-difference sums per scan slot.
+__device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int b0, uint32_t nb,
+                            int32_t sum[3]) {
   int b = b0;
-  int32_t pr0 = 0, pr1 = 0, pr2 = 0;
-  int16_t *cur = nullptr;
-  uint32_t done = 0;
-  bool first = true, active = true;
-  const uint4 *vec = reinterpret_cast<const uint4 *>(list);
-  uint32_t g = idx >> 2;
-  uint4 nxt = vec[g];
-#pragma unroll 1
-  for (; active && g * 4 < end; g++) {
-    const uint4 cur4 = nxt;
-    nxt = vec[g + 1];  // region slack keeps this in bounds
-    const uint32_t ev[4] = {cur4.x, cur4.y, cur4.z, cur4.w};
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const uint32_t i = g * 4 + q;
-      const uint32_t e = ev[q];
-      if (!active || i < idx || i >= end) continue;
-      if (e & 1) {  // DC entry: next block
-        if (!first) {
-          if (++done == nb) { active = false; continue; }
-          b = b + 1 == C.bpm ? 0 : b + 1;
-          if (b == 0 && ++mx == C.gx) { mx = 0; my++; }
-        }
-        first = false;
-        cur = window_block(H, coef, mx, my, b);
-        const int v = (int32_t)e >> 16;
-        const int s = (b >= C.c1) + (b >= C.c2);
-        const int32_t pv = (s == 0 ? pr0 : (s == 1 ? pr1 : pr2)) + v;
-        pr0 = s == 0 ? pv : pr0;
-        pr1 = s == 1 ? pv : pr1;
-        pr2 = s == 2 ? pv : pr2;
-        if (cur) {
-          if (pv < -32768 || pv > 32767) range = 1;
-          cur[0] = (int16_t)pv;
-        }
-      } else if (cur) {
-        cur[(e >> 1) & 63] = (int16_t)((int32_t)e >> 16);
-      }
-    }
+  int32_t s0 = 0, s1 = 0, s2 = 0;
+#pragma unroll 4
+  for (uint32_t i = 0; i < nb; i++) {
+    const int32_t v = (int32_t)bsl[ord + i].y;
+    const int s = (b >= C.c1) + (b >= C.c2);
+    s0 += s == 0 ? v : 0;
+    s1 += s == 1 ? v : 0;
+    s2 += s == 2 ? v : 0;
+    b = b + 1 == C.bpm ? 0 : b + 1;
   }
-  pred[0] = pr0;
-  pred[1] = pr1;
-  pred[2] = pr2;
+  sum[0] = s0;
+  sum[1] = s1;
+  sum[2] = s2;
 }
 
-// Adds base[slot] to the DC of every crop-window block among `nb` blocks from
-// absolute block A (block-in-MCU b0): turns run-relative DC into the
-// reference's predictor values.
-__device__ void dc_fixup(const EntCtx &C, const DecodeHdr &H, int16_t *coef, int b0, uint32_t A,
-                         uint32_t nb, const int32_t base[3], int &range) {
+// DC pass B: the reference's DC predictor of every block of the segment
+// (decode_kernels.py:150-153) continuing from base[]; each crop-window block
+// gets its table entry {global unit-list index of its DC entry, DC value} in
+// the first 8 bytes of its coefficient slot (k_idct gathers the block from
+// the list).
+__device__ void seg_table(const EntCtx &C, const DecodeHdr &H, int16_t *coef, const uint2 *bsl,
+                          uint32_t ord, uint32_t lgbase, int b0, uint32_t A, uint32_t nb,
+                          const int32_t base[3], int &range) {
   const uint32_t mcu = A / (uint32_t)C.bpm;
   int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
   int b = b0;
-#pragma unroll 1
-  for (uint32_t i = 0; i < nb && my <= H.my1; i++) {
+  int32_t p0 = base[0], p1 = base[1], p2 = base[2];
+#pragma unroll 4
+  for (uint32_t i = 0; i < nb; i++) {
+    const uint2 rec = bsl[ord + i];
+    const int s = (b >= C.c1) + (b >= C.c2);
+    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + (int32_t)rec.y;
+    p0 = s == 0 ? pv : p0;
+    p1 = s == 1 ? pv : p1;
+    p2 = s == 2 ? pv : p2;
     int16_t *cur = window_block(H, coef, mx, my, b);
     if (cur) {
-      const int s = (b >= C.c1) + (b >= C.c2);
-      const int32_t v = (int32_t)cur[0] + (s == 0 ? base[0] : (s == 1 ? base[1] : base[2]));
-      if (v < -32768 || v > 32767) range = 1;
-      cur[0] = (int16_t)v;
+      if (pv < -32768 || pv > 32767) range = 1;
+      *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + rec.x, (uint32_t)pv);
     }
     if (++b == C.bpm) {
       b = 0;
@@ -831,14 +858,15 @@ __device__ __forceinline__ int grp_max8(int v) {
 }
 
 // Must be called by all 32 lanes of a warp (lanes with valid=false idle).
-__device__ void idct_block_8lanes(bool valid, const int16_t *coef, const int32_t *q, uint8_t *dst,
+// blk: the block's 64 coefficients (natural order, int32, shared memory).
+__device__ void idct_block_8lanes(bool valid, const int32_t *blk, const int32_t *q, uint8_t *dst,
                                   int pitch, int32_t *tr /* 64 ints per 8-lane group */) {
   const int j = threadIdx.x & 7;
   int32_t d[8];
   int mabs = 0;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
-    d[r] = valid ? (int32_t)coef[8 * r + j] * q[8 * r + j] : 0;
+    d[r] = valid ? blk[8 * r + j] * q[8 * r + j] : 0;
     mabs = max(mabs, abs(d[r]));
   }
   const bool wide1 = grp_max8(mabs) > kIdctMax1;
@@ -1443,12 +1471,6 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         T.sub[e] = (uint16_t)ent;
       }
     }
-    // zero the coefficient window (k_entropy scatters nonzeros into it)
-    uint64_t total = 0;
-    for (int c = 0; c < 3; c++) total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
-    int4 *z = reinterpret_cast<int4 *>(P.s.coef + H.coef_base);
-    const uint64_t n16 = total / 8;
-    for (uint64_t i = tid; i < n16; i += kNT) z[i] = make_int4(0, 0, 0, 0);
   }
   __syncthreads();
   // ---- hand over: header (+ used tables) to global ---------------------------
@@ -1477,7 +1499,8 @@ struct __align__(16) EntSmem {
   int coef_range, red;
   unsigned long long lbase;
   int32_t dcsum[kLanes * 3];
-  uint32_t sink[kLanes];
+  uint32_t sink[kLanes * 2];
+  int fmt;
   long long t_ph[8];
 };
 
@@ -1487,6 +1510,204 @@ __device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int o
     S.reason = reason;
     S.offset = off;
   }
+}
+
+// Zero the image's crop-window coefficients (the re-decoding paths scatter
+// nonzeros into it).  Called by every thread of the CTA.
+__device__ void zero_window(const DecodeHdr &H, int16_t *coef, int lane) {
+  uint64_t total = 0;
+  for (int c = 0; c < 3; c++) total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
+  int4 *z = reinterpret_cast<int4 *>(coef + H.coef_base);
+  for (uint64_t i = lane; i < total / 8; i += kLanes) z[i] = make_int4(0, 0, 0, 0);
+}
+
+// Decode of one image by the CTA: restart intervals, serial mode, or the
+// checkpoint-merge parallel decode; SH: the clean stream is staged in shared
+// memory.
+template <bool SH>
+__device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, const EntCtx &C0,
+                                             int img, int lane, uint32_t &dbg_nseq,
+                                             uint32_t &dbg_cont) {
+  EntCtx C = C0;
+  DecodeHdr &H = S.h;
+  LaneRec &R = S.lane[lane];
+  int16_t *coef = P.s.coef;
+  const uint32_t *rst_tab = C.words + H.rst_off;
+  WriteOut wo;
+  wo.range = 0;
+#define PHASE(i) do { if (lane == 0) S.t_ph[i] = clock64(); } while (0)
+  if (S.status == 0 && H.scan_ri > 0) {
+    // DRI: restart intervals decode independently from exact entry states
+    // (decode_kernels.py:130-138); lanes take intervals round-robin.
+    const uint32_t ri = H.scan_ri;
+    const uint32_t lim_mcu = (uint32_t)H.row_stop * H.gx;
+    const uint32_t nint = (lim_mcu + ri - 1) / ri;
+    if (lane == 0) S.red = 0x7FFFFFFF;
+    zero_window(H, coef, lane);
+    __syncthreads();
+    for (uint32_t j = lane; j < nint; j += kLanes) {
+      if (j >= 1 && (int)(j - 1) >= H.n_restarts) {  // status 3
+        atomicMin(&S.red, (int)(2 * j + 1));
+        continue;
+      }
+      const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
+      const uint32_t b0 = j * ri * H.bpm;
+      const uint32_t b1 = min((j + 1) * ri, lim_mcu) * H.bpm;
+      int32_t pr[3] = {0, 0, 0};
+      write_run<SH>(C, H, coef, p0, 0, b0, b1 - b0, pr, wo, &S.p_final);
+      if (wo.err) atomicMin(&S.red, (int)(2 * j));
+      if (wo.range) S.coef_range = 1;
+    }
+    __syncthreads();
+    if (lane == 0) {
+      const int code = S.red;
+      if (code != 0x7FFFFFFF) {
+        const uint32_t j = code >> 1;
+        if (code & 1) {
+          ent_status(S, ESSL_ST_MISSING_RST, 0, H.scan_start);
+        } else {
+          const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
+          const uint32_t errp = tail_run<SH>(C, p0, 0, 0, 0xFFFFFFFFu);
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
+        }
+      } else if (S.p_final != kNoEnd && S.p_final > H.clean_bits) {
+        ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+      }
+    }
+  } else if (S.status == 0 && P.mode == ESSL_DECODE_SERIAL) {
+    zero_window(H, coef, lane);
+    __syncthreads();
+    if (lane == 0) {
+      int32_t pred[3] = {0, 0, 0};
+      write_run<SH>(C, H, coef, 0, 0, 0, H.limit_blocks, pred, wo, &S.p_final);
+      if (wo.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, wo.errp));
+      else if (S.p_final > H.clean_bits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+      if (wo.range) S.coef_range = 1;
+    }
+  } else if (S.status == 0) {
+    // ---- checkpoint-merge parallel decode, each unit decoded once ---------
+    const uint32_t cbits = C.cbits;
+    int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
+    nseq = max(1, min(nseq, kLanes));
+    const uint32_t slen = (cbits + nseq - 1) / nseq;
+    const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
+    C.ck_bits = max((uint32_t)P.ck_bits, (slen + warm + kCk - 9) / (kCk - 8));
+    Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
+    // unit lists + block records: one region per lane, carved per image.
+    // Lists hold every decoded unit; slot cap is a sink for overflow and the
+    // slot after the last unit holds a sentinel.  (No room: one-entry sinks,
+    // the image falls back to a serial re-decode.)
+    const uint32_t cap = ((slen + warm + kContBits) / 4 + 64 + 3) & ~3u;
+    const uint32_t bcap = cap / 2 + 8;  // a block has >= 2 units (DC + an AC unit)
+    const uint32_t stride = cap + 8 + ((2 * (bcap + 2) + 3) & ~3u);
+    if (lane == 0) {
+      const unsigned long long need = (unsigned long long)nseq * stride;
+      const unsigned long long b = atomicAdd(&P.s.counters[3], need + 4);
+      const unsigned long long b4 = (b + 3) & ~3ull;
+      S.lbase = b4 + need > P.s.list_cap ? ~0ull : b4;
+      S.red = 0;
+    }
+    __syncthreads();
+    const bool lists_ok = S.lbase != ~0ull;
+    const unsigned long long lreg = lists_ok ? S.lbase + (unsigned long long)lane * stride : 0ull;
+    uint32_t *list = lists_ok ? P.s.list + lreg : S.sink + 2 * lane;
+    uint2 *bsl = lists_ok ? reinterpret_cast<uint2 *>(P.s.list + lreg + cap + 8)
+                          : reinterpret_cast<uint2 *>(S.sink) + lane;
+    const uint32_t lcap = lists_ok ? cap : 0u, lbcap = lists_ok ? bcap : 0u;
+    if (lane < nseq) {
+      const uint32_t sbeg = lane * slen;
+      const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
+      const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
+      run_path<false, SH>(C, lane, nseq, p0, send, list, lcap, bsl, lbcap, ck_all, S.lane, R);
+    }
+    __syncthreads();
+    PHASE(2);
+    const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
+    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R);
+    dbg_nseq = (uint32_t)nseq;
+    if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
+    __syncthreads();
+    dbg_cont = (uint32_t)S.red;
+    PHASE(3);
+    // resolution: follow the exact path from lane 0 through the merges
+    if (lane == 0) {
+      uint32_t A = 0, sord = 0, sp = 0, sb = 0, snb = 0;
+      int o = 0;
+      const uint32_t limit = C.limit;
+      S.fmt = 1;
+#pragma unroll 1
+      for (int hop = 0; hop < nseq; hop++) {
+        LaneRec &L = S.lane[o];
+        const uint32_t own = L.nblk - snb;
+        L.w_ord = sord; L.w_p = sp; L.w_b = sb; L.w_A = A;
+        if (L.ovf) S.fmt = 0;  // an owner's list overflowed: serial re-decode
+        if (L.err) {  // error on the exact path (phase 1 of lane 0)
+          L.w_nb = min(own, limit - A);
+          if (A + own < limit) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.errp));
+          break;
+        }
+        const bool last = o == nseq - 1;
+        const uint32_t seg = own + (last ? 0u : L.cn);
+        L.w_nb = min(seg, limit - A);
+        const uint32_t end_p = last ? L.xp : L.cp;
+        const int end_be = last ? L.xbe : L.cbe;
+        if (A + seg >= limit) {
+          // the block reaching the limit ends past the data (_check_consumed)
+          if (A + seg == limit && end_be && end_p > cbits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+          break;
+        }
+        if (last || L.cst == 2) {
+          // the data ends before the crop's last MCU row: continue serially
+          // into the 0xFF padding to classify corrupt (1) vs truncated (4)
+          const uint32_t errp = tail_run<SH>(C, end_p, last ? L.xk : (int)L.ek, last ? L.xb : (int)L.eb,
+                                             limit - (A + seg));
+          if (errp != kNoEnd) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
+          else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+          break;
+        }
+        if (L.cst == 1) {
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.cp));
+          break;
+        }
+        A += seg;
+        const Ckpt c = ck_all[L.cj * kCk + L.cm];
+        o = (int)L.cj;
+        sord = c.ord; sp = c.pb >> 6; sb = c.pb & 63; snb = c.nblk;
+      }
+      if (!lists_ok) S.fmt = 0;
+    }
+    __syncthreads();
+    PHASE(4);
+    const bool own = S.status == 0 && R.w_nb > 0;
+    int range = 0;
+    if (S.status == 0 && S.fmt == 1) {
+      // block tables: each segment's DC continues from the earlier segments'
+      // DC sums (segments are in lane order)
+      int32_t sum[3] = {0, 0, 0};
+      if (own) seg_dc_sums(C, bsl, R.w_ord, (int)R.w_b, R.w_nb, sum);
+      int32_t *dcs = S.dcsum;
+      for (int q = 0; q < 3; q++) dcs[lane * 3 + q] = sum[q];
+      __syncthreads();
+      if (own) {
+        int32_t base[3] = {0, 0, 0};
+        for (int t = 0; t < lane; t++)
+          for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
+        seg_table(C, H, coef, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb, base, range);
+      }
+    } else if (S.status == 0) {
+      // fallback (an owner's unit list overflowed): serial re-decode into
+      // the zeroed coefficient window
+      zero_window(H, coef, lane);
+      __syncthreads();
+      if (lane == 0) {
+        int32_t pred[3] = {0, 0, 0};
+        write_run<SH>(C, H, coef, 0, 0, 0, C.limit, pred, wo, nullptr);
+        range = wo.range;
+      }
+    }
+    if (range) S.coef_range = 1;
+  }
+#undef PHASE
 }
 
 __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
@@ -1517,6 +1738,7 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
     S.status = H.status; S.reason = H.reason; S.offset = H.offset;
     S.coef_range = 0;
     S.p_final = kNoEnd;
+    S.fmt = 0;
   }
   LaneRec &R = S.lane[lane];
   R.w_nb = 0;
@@ -1526,6 +1748,8 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
 
   EntCtx C;
   C.tabs = reinterpret_cast<const uint8_t *>(H.tab);
+  C.tabs_s = (uint32_t)__cvta_generic_to_shared(H.tab);
+  C.zz_s = (uint32_t)__cvta_generic_to_shared(H.zz);
   {
     const uint32_t w = H.tab_index_word;
     const uint32_t sz = (uint32_t)sizeof(HuffTab);
@@ -1541,168 +1765,22 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   C.words = reinterpret_cast<const uint32_t *>(P.s.clean + H.clean_off);
   C.wmax = H.wmax;
   C.ck_bits = 0;
-  int16_t *coef = P.s.coef;
-  const uint32_t *rst_tab = C.words + H.rst_off;
   uint32_t dbg_nseq = 0, dbg_cont = 0;
-  WriteOut wo;
-  wo.range = 0;
-
-  if (S.status == 0 && H.scan_ri > 0) {
-    // DRI: restart intervals decode independently from exact entry states
-    // (decode_kernels.py:130-138); lanes take intervals round-robin.
-    const uint32_t ri = H.scan_ri;
-    const uint32_t lim_mcu = (uint32_t)H.row_stop * H.gx;
-    const uint32_t nint = (lim_mcu + ri - 1) / ri;
-    if (lane == 0) S.red = 0x7FFFFFFF;
-    __syncthreads();
-    for (uint32_t j = lane; j < nint; j += kLanes) {
-      if (j >= 1 && (int)(j - 1) >= H.n_restarts) {  // status 3
-        atomicMin(&S.red, (int)(2 * j + 1));
-        continue;
-      }
-      const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
-      const uint32_t b0 = j * ri * H.bpm;
-      const uint32_t b1 = min((j + 1) * ri, lim_mcu) * H.bpm;
-      int32_t pr[3] = {0, 0, 0};
-      write_run(C, H, coef, p0, 0, b0, b1 - b0, pr, wo, &S.p_final);
-      if (wo.err) atomicMin(&S.red, (int)(2 * j));
-      if (wo.range) S.coef_range = 1;
-    }
-    __syncthreads();
-    if (lane == 0) {
-      const int code = S.red;
-      if (code != 0x7FFFFFFF) {
-        const uint32_t j = code >> 1;
-        if (code & 1) {
-          ent_status(S, ESSL_ST_MISSING_RST, 0, H.scan_start);
-        } else {
-          const uint32_t p0 = j == 0 ? 0 : 8u * rst_tab[j - 1];
-          const uint32_t errp = tail_run(C, p0, 0, 0, 0xFFFFFFFFu);
-          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
-        }
-      } else if (S.p_final != kNoEnd && S.p_final > H.clean_bits) {
-        ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
-      }
-    }
-  } else if (S.status == 0 && P.mode == ESSL_DECODE_SERIAL) {
-    if (lane == 0) {
-      int32_t pred[3] = {0, 0, 0};
-      write_run(C, H, coef, 0, 0, 0, H.limit_blocks, pred, wo, &S.p_final);
-      if (wo.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, wo.errp));
-      else if (S.p_final > H.clean_bits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
-      if (wo.range) S.coef_range = 1;
-    }
-  } else if (S.status == 0) {
-    // ---- checkpoint-merge parallel decode, each unit decoded once ---------
-    const uint32_t cbits = C.cbits;
-    int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
-    nseq = max(1, min(nseq, kLanes));
-    const uint32_t slen = (cbits + nseq - 1) / nseq;
-    const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
-    C.ck_bits = max((uint32_t)P.ck_bits, (slen + warm + kCk - 9) / (kCk - 8));
-    Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
-    // unit lists: one region per lane (16-byte aligned, 8 entries of slack
-    // for the scatter's read-ahead), carved per image
-    const uint32_t cap = ((slen + warm) / 4 + kListSlack + 3) & ~3u;
-    const uint32_t stride = cap + 8;
-    if (lane == 0) {
-      const unsigned long long need = (unsigned long long)nseq * stride;
-      const unsigned long long b = atomicAdd(&P.s.counters[3], need + 4);
-      const unsigned long long b4 = (b + 3) & ~3ull;
-      S.lbase = b4 + need > P.s.list_cap ? ~0ull : b4;
-      S.red = 0;
-    }
-    __syncthreads();
-    const bool lists_ok = S.lbase != ~0ull;
-    // (no room: one-entry sink per lane, every owner re-decodes)
-    uint32_t *list = lists_ok ? P.s.list + S.lbase + (unsigned long long)lane * stride : S.sink + lane;
-    const uint32_t lcap = lists_ok ? cap : 0u;  // no room: every owner re-decodes
-    if (lane < nseq) {
-      const uint32_t sbeg = lane * slen;
-      const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
-      const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
-      run_path<false>(C, lane, nseq, p0, send, list, lcap, H.zz, ck_all, S.lane, R);
-    }
-    __syncthreads();
-    PHASE(2);
-    const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
-    if (cont) run_path<true>(C, lane, nseq, 0, 0, list, lcap, H.zz, ck_all, S.lane, R);
-    dbg_nseq = (uint32_t)nseq;
-    if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
-    __syncthreads();
-    dbg_cont = (uint32_t)S.red;
-    PHASE(3);
-    // resolution: follow the exact path from lane 0 through the merges
-    if (lane == 0) {
-      uint32_t A = 0, sidx = 0, sp = 0, sb = 0, snb = 0;
-      int o = 0;
-      const uint32_t limit = C.limit;
-#pragma unroll 1
-      for (int hop = 0; hop < nseq; hop++) {
-        LaneRec &L = S.lane[o];
-        const uint32_t own = L.nblk - snb;
-        L.w_idx = sidx; L.w_p = sp; L.w_b = sb; L.w_A = A;
-        if (L.err) {  // error on the exact path (phase 1 of lane 0)
-          L.w_nb = min(own, limit - A);
-          if (A + own < limit) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.errp));
-          break;
-        }
-        const bool last = o == nseq - 1;
-        const uint32_t seg = own + (last ? 0u : L.cn);
-        L.w_nb = min(seg, limit - A);
-        const uint32_t end_p = last ? L.xp : L.cp;
-        const int end_be = last ? L.xbe : L.cbe;
-        if (A + seg >= limit) {
-          // the block reaching the limit ends past the data (_check_consumed)
-          if (A + seg == limit && end_be && end_p > cbits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
-          break;
-        }
-        if (last || L.cst == 2) {
-          // the data ends before the crop's last MCU row: continue serially
-          // into the 0xFF padding to classify corrupt (1) vs truncated (4)
-          const uint32_t errp = tail_run(C, end_p, last ? L.xk : (int)L.ek, last ? L.xb : (int)L.eb,
-                                         limit - (A + seg));
-          if (errp != kNoEnd) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
-          else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
-          break;
-        }
-        if (L.cst == 1) {
-          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.cp));
-          break;
-        }
-        A += seg;
-        const Ckpt c = ck_all[L.cj * kCk + L.cm];
-        o = (int)L.cj;
-        sidx = c.idx; sp = c.pb >> 6; sb = c.pb & 63; snb = c.nblk;
-      }
-    }
-    __syncthreads();
-    PHASE(4);
-    // scatter the exact path's units into the crop window (DC relative to
-    // each segment), then add each segment's DC base: the prefix of the
-    // earlier segments' DC sums (segments are in lane order)
-    int32_t pred[3] = {0, 0, 0};
-    int range = 0;
-    const bool own = S.status == 0 && R.w_nb > 0;
-    if (own) {
-      if (!R.ovf && lists_ok) {
-        scatter_run(C, H, coef, list, R.w_idx, R.nlist, (int)R.w_b, R.w_A, R.w_nb, pred, range);
-      } else {
-        write_run(C, H, coef, R.w_p, (int)R.w_b, R.w_A, R.w_nb, pred, wo, nullptr);
-        range = wo.range;
-      }
-    }
-    int32_t *dcs = reinterpret_cast<int32_t *>(S.dcsum);
-    for (int q = 0; q < 3; q++) dcs[lane * 3 + q] = own ? pred[q] : 0;
-    __syncthreads();
-    if (own) {
-      int32_t base[3] = {0, 0, 0};
-      for (int t = 0; t < lane; t++)
-        for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
-      if (base[0] | base[1] | base[2]) dc_fixup(C, H, coef, (int)R.w_b, R.w_A, R.w_nb, base, range);
-    }
-    if (range) S.coef_range = 1;
+  // stage the clean stream in shared memory when it fits the launch's
+  // dynamic allocation (k_prep pads it with >= 2 words of 0xFF)
+  extern __shared__ __align__(16) uint32_t s_words[];
+  const uint32_t nwords = H.status == 0 ? H.wmax + 1 : 0u;
+  const bool staged = nwords * 4 <= P.stage_bytes;
+  if (staged && S.status == 0) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(C.words);
+    uint4 *dst = reinterpret_cast<uint4 *>(s_words);
+    for (uint32_t i = lane; i < (nwords + 3) / 4; i += kLanes) dst[i] = src[i];
   }
+  C.words_s = (uint32_t)__cvta_generic_to_shared(s_words);
+  __syncthreads();
+
+  if (staged) entropy_body<true>(P, S, C, img, lane, dbg_nseq, dbg_cont);
+  else entropy_body<false>(P, S, C, img, lane, dbg_nseq, dbg_cont);
   __syncthreads();
   PHASE(5);
   if (lane == 0 && S.status == 0 && S.coef_range) ent_status(S, ESSL_ST_UNSUPPORTED, R_COEF_RANGE, -1);
@@ -1735,9 +1813,18 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
     info->status = S.status;
     info->reason = S.reason;
     info->offset = S.offset;
+    info->fmt = S.fmt;
     for (int i = 0; i < 6; i++) info->dbg[2 + i] = S.t_ph[i];
     info->dbg[10] = dbg_nseq;
     info->dbg[11] = dbg_cont;
+    uint32_t su = 0, sg = 0, mu = 0;
+    for (int t = 0; t < (int)dbg_nseq; t++) {
+      su += S.lane[t].dbg_units;
+      sg += S.lane[t].dbg_guess;
+      mu = max(mu, S.lane[t].dbg_units);
+    }
+    info->dbg[8] = su | ((long long)sg << 32);
+    info->dbg[9] = mu | ((long long)(S.status == 0 && S.fmt == 0) << 32);
     if (P.results) {
       essl_result r;
       r.status = S.status; r.reason = S.reason; r.offset = S.offset;
@@ -1751,14 +1838,54 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
 }
 
 // ===========================================================================
-// k_idct: dequant + islow IDCT of the crop-window blocks -> Y/Cb/Cr planes
-// (decode_kernels.py:388-534 via codec.py:412-419).  grid (kIdctCtas, n).
+// k_idct: gather + dequant + islow IDCT of the crop-window blocks -> Y/Cb/Cr
+// planes (decode_kernels.py:388-534 via codec.py:412-419).  grid
+// (kIdctCtas, n), 8 lanes per block.
 // ===========================================================================
 constexpr int kIdctCtas = 8;
+
+// Gathers window block (c, byr, bxr) of an image into blk[64] (int32,
+// natural order, shared memory).  fmt 1: the block's table entry points at its
+// DC entry in a unit list; its AC units follow up to the next DC-flagged entry
+// (eight lanes read eight consecutive entries per round).  fmt 0: the int16
+// coefficient window.  Called by all 32 lanes of a warp.
+__device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, int c, int byr,
+                              int bxr, int32_t *blk) {
+  const int j = threadIdx.x & 7;
+  const int16_t *cf = sc.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
+#pragma unroll
+  for (int r = 0; r < 8; r++) blk[8 * j + r] = 0;
+  __syncwarp();
+  if (I.fmt == 0) {
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < 8; r++) blk[8 * r + j] = cf[8 * r + j];
+    }
+    __syncwarp();
+    return;
+  }
+  uint2 t = make_uint2(0, 0);
+  if (valid) t = *reinterpret_cast<const uint2 *>(cf);
+  if (valid && j == 0) blk[0] = (int32_t)t.y;
+  bool done = !valid;
+  const int gsh = threadIdx.x & 24;  // this group's bit offset in a warp ballot
+  uint32_t i = t.x + 1 + j;
+#pragma unroll 1
+  while (__any_sync(0xFFFFFFFFu, !done)) {
+    const uint32_t e = done ? 1u : __ldg(sc.list + i);
+    const uint32_t grp = (__ballot_sync(0xFFFFFFFFu, !done && (e & 1)) >> gsh) & 0xFFu;
+    const int first = grp ? __ffs(grp) - 1 : 8;
+    if (!done && j < first) blk[(e >> 1) & 63] = (int32_t)e >> 16;
+    done = done || first < 8;
+    i += 8;
+  }
+  __syncwarp();
+}
 
 __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
   __shared__ int32_t q[3][64];
   __shared__ int32_t tr[8][4][64];
+  __shared__ int32_t blks[32][64];
   const int img = blockIdx.y;
   const ImgInfo &I = P.s.info[img];
   if (I.status != 0) return;
@@ -1775,6 +1902,7 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
   __syncthreads();
   const int total = nb[0] + nb[1] + nb[2];
   int32_t *t = tr[tid >> 5][(tid >> 3) & 3];
+  int32_t *blk = blks[tid >> 3];
   for (int r0 = blockIdx.x * 32; r0 < total; r0 += kIdctCtas * 32) {
     int jb = r0 + (tid >> 3);
     const bool valid = jb < total;
@@ -1783,11 +1911,47 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
       if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
     }
     const int byr = valid ? jb / wb[c] : 0, bxr = valid ? jb % wb[c] : 0;
+    gather_block8(valid, I, P.s, c, byr, bxr, blk);
     const int pitch = I.plane_pitch[c];
-    const int16_t *cf = P.s.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
     uint8_t *dst = P.s.plane + I.plane_off[c] + (uint64_t)byr * 8 * pitch + bxr * 8;
-    idct_block_8lanes(valid, cf, q[c], dst, pitch, t);
+    idct_block_8lanes(valid, blk, q[c], dst, pitch, t);
   }
+}
+
+// Debug copy of the crop-window coefficients (components back to back,
+// natural order, int16), gathered like k_idct.
+__global__ void __launch_bounds__(256) k_dump_coefs(Scratch sc, int16_t *out, const uint64_t *offsets) {
+  __shared__ int32_t blks[32][64];
+  const int img = blockIdx.y;
+  const ImgInfo &I = sc.info[img];
+  if (I.status != 0) return;
+  const int tid = threadIdx.x;
+  int nb[3] = {0, 0, 0};
+  for (int c = 0; c < I.ncomp; c++) nb[c] = I.wbh[c] * I.wbw[c];
+  const int total = nb[0] + nb[1] + nb[2];
+  int32_t *blk = blks[tid >> 3];
+  for (int r0 = blockIdx.x * 32; r0 < total; r0 += gridDim.x * 32) {
+    int jb = r0 + (tid >> 3);
+    const bool valid = jb < total;
+    const int jall = jb;
+    int c = 0;
+    if (valid) {
+      if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
+    }
+    const int w = max(I.wbw[c], 1);
+    gather_block8(valid, I, sc, c, valid ? jb / w : 0, valid ? jb % w : 0, blk);
+    if (valid) {
+      int16_t *o = out + offsets[img] + (uint64_t)jall * 64;
+      const int j = tid & 7;
+#pragma unroll
+      for (int r = 0; r < 8; r++) o[8 * r + j] = (int16_t)blk[8 * r + j];
+    }
+  }
+}
+
+void launch_dump_coefs(const Scratch &sc, int n, int16_t *out, const uint64_t *offsets,
+                       cudaStream_t st) {
+  if (n > 0) k_dump_coefs<<<dim3(32, n), 256, 0, st>>>(sc, out, offsets);
 }
 
 // Shared-memory budget for k_prep's staged payload.
@@ -1808,8 +1972,21 @@ void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len) {
   else k_prep<false><<<p.n, kNT, 0, st>>>(p);
 }
 
-void launch_entropy(const DecodeParams &p, cudaStream_t st) {
-  if (p.n > 0) k_entropy<<<p.n, kLanes, 0, st>>>(p);
+// Dynamic shared memory for staging the clean stream in k_entropy; larger
+// payloads decode from global memory (same code, Reader<false>).
+constexpr int kMaxStage = 64 * 1024;
+
+void launch_entropy(const DecodeParams &p0, cudaStream_t st, int max_len) {
+  if (p0.n <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStage);
+    attr = true;
+  }
+  DecodeParams p = p0;  // p0.stage_bytes: the context's staging limit
+  const int need = (max_len + 15) / 16 * 16 + 64;
+  p.stage_bytes = need <= min(kMaxStage, p0.stage_bytes) ? need : 0;
+  k_entropy<<<p.n, kLanes, p.stage_bytes, st>>>(p);
 }
 
 void launch_idct(const DecodeParams &p, cudaStream_t st) {

@@ -12,7 +12,7 @@ struct Ckpt;
 constexpr int kDecodeThreads = 256;  // k_prep: one CTA per image
 constexpr int kCheckpoints = 64;     // k_entropy: checkpoints per lane
 constexpr int kEntropyLanes = 64;     // k_entropy: subsequences (threads) per image
-constexpr int kListSlackEntries = 1024;  // k_entropy: unit-list entries per lane beyond (slen+warm)/4
+constexpr int kContinuationBits = 8192;  // k_entropy: list room per lane for its continuation
 constexpr int kMaxWarmBits = 4096;
 constexpr int kFastBits = 10;        // first-level Huffman lookahead
 constexpr int kMaxTables = 6;        // distinct (class,id) tables a 3-slot scan can use
@@ -45,6 +45,7 @@ struct ImgInfo {
   uint64_t coef_off[3];   // int16 elements into Scratch::coef
   int32_t mcus_entropy, mcus_recon;
   int32_t rx, ry, rw, rh, flip;
+  int32_t fmt;  // 0: coefficient window (int16); 1: per-block tables into the unit lists
   int64_t dbg[16];  // phase clocks / counters (essl_debug_stats)
 };
 
@@ -75,6 +76,7 @@ struct DecodeParams {
   int seq_bits;      // minimum subsequence length per lane (bits)
   int ck_bits;       // minimum checkpoint spacing (bits)
   int warm_bits;     // each lane (but lane 0) starts this far before its subsequence
+  int stage_bytes;   // k_entropy dynamic shared memory for the clean stream (0: global)
   essl_result *results;  // optional
 };
 
@@ -107,7 +109,7 @@ __host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t ep
 
 // launch wrappers (defined in the .cu files)
 void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len);
-void launch_entropy(const DecodeParams &p, cudaStream_t st);
+void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
 size_t ckpt_bytes();
@@ -124,7 +126,7 @@ void launch_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, 
                       int flip, cudaStream_t st);
 void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStream_t st);
 void launch_results(const ImgInfo *info, int n, essl_result *res, cudaStream_t st);
-void launch_dump_coefs(const ImgInfo *info, const int16_t *coef, int n, int16_t *out,
-                       const uint64_t *offsets, cudaStream_t st);
+void launch_dump_coefs(const Scratch &sc, int n, int16_t *out, const uint64_t *offsets,
+                       cudaStream_t st);
 
 }  // namespace essl

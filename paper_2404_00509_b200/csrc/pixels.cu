@@ -373,27 +373,4 @@ void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStrea
   k_normalize_u8<<<148, 256, 0, st>>>(src, h, w, dst);
 }
 
-// Debug copy of the crop-window coefficients (components back to back).
-__global__ void k_dump_coefs(const ImgInfo *info, const int16_t *coef, int16_t *out,
-                             const uint64_t *offsets) {
-  const int img = blockIdx.y;
-  const ImgInfo &I = info[img];
-  if (I.status != 0) return;
-  int16_t *o = out + offsets[img];
-  uint64_t pos = 0;
-  for (int c = 0; c < I.ncomp; c++) {
-    const uint64_t cnt = (uint64_t)I.wbh[c] * I.wbw[c] * 64;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < cnt;
-         e += (uint64_t)gridDim.x * blockDim.x)
-      o[pos + e] = coef[I.coef_off[c] + e];
-    pos += cnt;
-  }
-}
-
-void launch_dump_coefs(const ImgInfo *info, const int16_t *coef, int n, int16_t *out,
-                       const uint64_t *offsets, cudaStream_t st) {
-  if (n <= 0) return;
-  k_dump_coefs<<<dim3(32, n), 256, 0, st>>>(info, coef, out, offsets);
-}
-
 }  // namespace essl

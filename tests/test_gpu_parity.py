@@ -37,10 +37,11 @@ def E(cuda):
 
 # speculative: library defaults; spec_dense: every lane on every stream, a
 # checkpoint at every block start, no warm-up; spec_sparse: few, far-apart
-# checkpoints (late merges, long continuations) and the longest warm-up;
+# checkpoints (late merges, long continuations), the longest warm-up, and the
+# clean stream read from global memory (no shared-memory staging);
 # serial: one lane (validation mode).
-MODES = {"speculative": (None, None, None), "spec_dense": (32, 1, 0), "spec_sparse": (64, 4096, 4096),
-         "serial": None}
+MODES = {"speculative": (None, None, None, None), "spec_dense": (32, 1, 0, 65536),
+         "spec_sparse": (64, 4096, 4096, 0), "serial": None}
 
 
 @pytest.fixture(params=list(MODES))
@@ -54,11 +55,13 @@ def mode(request, E):
         eng.set_option(N.ESSL_OPT_SEQ_BITS, m[0])
         eng.set_option(N.ESSL_OPT_CHECKPOINT_BITS, m[1])
         eng.set_option(N.ESSL_OPT_WARMUP_BITS, m[2])
+        eng.set_option(N.ESSL_OPT_STAGE_BYTES, m[3])
     yield request.param
     eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SPECULATIVE)
-    eng.set_option(N.ESSL_OPT_SEQ_BITS, 2048)
+    eng.set_option(N.ESSL_OPT_SEQ_BITS, 4096)
     eng.set_option(N.ESSL_OPT_CHECKPOINT_BITS, 64)
-    eng.set_option(N.ESSL_OPT_WARMUP_BITS, 1024)
+    eng.set_option(N.ESSL_OPT_WARMUP_BITS, 2048)
+    eng.set_option(N.ESSL_OPT_STAGE_BYTES, 65536)
 
 
 @pytest.mark.parametrize("name", STREAMS)
@@ -267,9 +270,9 @@ def synth_sets(E, tmp_path_factory):
     return a, b, c
 
 
-@pytest.mark.parametrize("seq_bits,ck_bits,warm", [(2048, 64, 1024), (32, 1, 0), (4096, 256, 4096),
-                                                   (300, 5000, 300)])
-def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, ck_bits, warm):
+@pytest.mark.parametrize("seq_bits,ck_bits,warm,stage", [(4096, 64, 2048, 65536), (32, 1, 0, 65536),
+                                                         (4096, 256, 4096, 0), (300, 5000, 300, 0)])
+def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, ck_bits, warm, stage):
     """Synthetic datasets (random crops, all rows) through the checkpoint-merge
     decoder with adversarial lane / checkpoint settings == the oracle, bit for bit."""
     from paper_2404_00509_b200 import _native as N
@@ -281,6 +284,7 @@ def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, ck_bits
             loader.set_option(N.ESSL_OPT_SEQ_BITS, seq_bits)
             loader.set_option(N.ESSL_OPT_CHECKPOINT_BITS, ck_bits)
             loader.set_option(N.ESSL_OPT_WARMUP_BITS, warm)
+            loader.set_option(N.ESSL_OPT_STAGE_BYTES, stage)
             for b in loader.epoch(3):
                 idx = b.indices.cpu().numpy()
                 pix, u8, mask, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 3, 160,

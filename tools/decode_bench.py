@@ -42,7 +42,7 @@ def main():
     loader = E.Loader(cfg)
     eng = loader.engine
     perm = E.epoch_permutation(0, 0, len(loader.handle))
-    settings = [("spec", 2048, 1024)]
+    settings = [("spec", 4096, 2048)]
     if args.sweep:
         settings = [("serial", 0, 0)] + [("spec", s, w) for s in (2048, 4096, 8192)
                                          for w in (0, 1024, 2048, 4096)]
@@ -76,6 +76,10 @@ def main():
                                         for i in range(10)},
                "phase_kcycles_max": {PHASES[i]: round(float(np.max(ph[:, i])) / 1e3, 1)
                                      for i in range(10)},
+               "units_phase1_mean": float((dbg[:, 8] & 0xFFFFFFFF).mean()),
+               "reguess_phase1_mean": float((dbg[:, 8] >> 32).mean()),
+               "units_phase1_lane_max_median": float(np.median(dbg[:, 9] & 0xFFFFFFFF)),
+               "fallback_images": int((dbg[:, 9] >> 32).sum()),
                "nseq_mean": float(nseq.mean()), "cont_bits_max_median": float(np.median(cont)),
                "cont_bits_max_max": int(cont.max())}
         results.append(row)
