@@ -84,7 +84,7 @@ def make_dataset(wl: dict, pool: int, out_dir: Path, seed: int = 1) -> Path:
 class Clocks:
     """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -92,6 +92,11 @@ class Clocks:
         self.idx = gpu_index
         self.proc = None
         self.path = None
+        self.marks = []
+
+    def mark(self) -> None:
+        """Bracket the timed region (wall clock, matched to sample timestamps)."""
+        self.marks.append(time.time())
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -112,26 +117,40 @@ class Clocks:
             self.proc.wait()
 
     def summary(self) -> dict:
+        import datetime
         rows = []
         try:
             for line in Path(self.path).read_text().splitlines():
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 9:
-                    rows.append(parts)
+                if len(parts) >= 10:
+                    try:
+                        ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    except ValueError:
+                        ts = None
+                    rows.append((ts, parts[1:]))
         except OSError:
             pass
         finally:
             if self.path:
                 Path(self.path).unlink(missing_ok=True)
-        if not rows:
+        if len(self.marks) >= 2 and rows:
+            a, b = self.marks[0], self.marks[-1]
+            inside = [r for t, r in rows if t is not None and a - 0.05 <= t <= b + 0.05]
+            if not inside:  # timed region shorter than the sampling period: nearest samples
+                near = sorted(rows, key=lambda x: abs((x[0] or 0) - (a + b) / 2))[:2]
+                inside = [r for _, r in near]
+            sel = inside
+        else:
+            sel = [r for _, r in rows]
+        if not sel:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in sel if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in sel if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in sel for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(sel)}
 
 
 def cpu_oracle_rate(path: Path, wl: dict, seconds: float, seed_epoch=(0, 0)) -> dict:
@@ -230,7 +249,7 @@ def run_gpu(args, wl):
     cfg = E.LoaderConfig(data=str(path), batch_size=B, res=res, scale=wl["scale"],
                          mask_ratio=wl["mask"], out_dtype="bfloat16", device=str(dev),
                          rank=rank, world_size=ws, resident=True, prefetch=args.streams,
-                         streams=args.streams)
+                         streams=args.streams, reuse_outputs=True)
     loader = E.Loader(cfg)
     if args.seq_bits > 0:
         loader.set_option(N.ESSL_OPT_SEQ_BITS, args.seq_bits)
@@ -247,38 +266,62 @@ def run_gpu(args, wl):
         return e, perm_epochs[e][j * B:(j + 1) * B]
 
     stream = torch.cuda.current_stream(dev)
-    # ---- warm-up ---------------------------------------------------------
-    for i in range(args.warmup):
+    # The clock sampler starts before the warm-up so that nvidia-smi's own
+    # start-up is not inside the timed region; it runs through it.
+    clk = Clocks(local).__enter__()
+    # ---- warm-up: the same pipelined issue pattern as the timed loop, so the
+    # caching allocator and every stream's context reach steady state
+    pend = []
+    ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2  # pipeline.py _HostRing (reused outputs)
+    for i in range(max(args.warmup, args.streams * (ring_depth + 1))):
         e, idx = batch_indices(i)
-        loader.finish(loader.enqueue(e, idx))
+        pend.append(loader.enqueue(e, idx))
+        if len(pend) > 2 * args.streams:
+            loader.finish(pend.pop(0))
+    for p in pend:
+        loader.finish(p)
     torch.cuda.synchronize(dev)
     # ---- timed region (device events, max over ranks) ----------------------
     loader.set_option(N.ESSL_OPT_PROFILE, 1)
     loader.profile_read()
     launches0 = loader.launches
     pend = []
-    with Clocks(local) as clk:
-        if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        n_img = 0
-        for i in range(args.steps):
-            e, idx = batch_indices(args.warmup + i)
-            pend.append(loader.enqueue(e, idx))
-            n_img += len(idx)
-            if len(pend) > 2 * args.streams:  # bounded run-ahead; statuses checked as we go
-                loader.finish(pend.pop(0))
-        for p in pend:  # join every in-flight batch before the end event
-            loader.join(p)
-        t1.record(stream)
-        torch.cuda.synchronize(dev)
-        if ws > 1:
-            dist.barrier()
+    if ws > 1:
+        dist.barrier()
+    import gc
+    gc.collect()
+    gc.freeze()  # long-lived objects (torch, numpy) out of the cyclic GC's way
+    torch.cuda.synchronize(dev)
+    clk.mark()
+    host_t = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    n_img = 0
+    for i in range(args.steps):
+        h0 = time.perf_counter()
+        e, idx = batch_indices(args.warmup + i)
+        pend.append(loader.enqueue(e, idx))
+        n_img += len(idx)
+        h1 = time.perf_counter()
+        if len(pend) > 2 * args.streams:  # bounded run-ahead; statuses checked as we go
+            loader.finish(pend.pop(0))
+        host_t.append((h1 - h0, time.perf_counter() - h1))
+    for p in pend:  # join every in-flight batch before the end event
+        loader.join(p)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk.mark()
+    if ws > 1:
+        dist.barrier()
+    clk.__exit__(None, None, None)
     for p in pend:
         loader.finish(p)
+    if os.environ.get("ESSL_BENCH_HOSTLOG"):
+        ht = np.array(host_t) * 1e3
+        log(f"[bench] host enqueue ms median {np.median(ht[:, 0]):.3f} max {ht[:, 0].max():.3f}; "
+            f"finish-wait median {np.median(ht[:, 1]):.3f} max {ht[:, 1].max():.3f} "
+            f"(argmax {int(ht[:, 0].argmax())}, {int(ht[:, 1].argmax())})")
     ms = t0.elapsed_time(t1)
     launches = loader.launches - launches0
     prof = loader.profile_read()
@@ -291,8 +334,9 @@ def run_gpu(args, wl):
         cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False})
         l2 = E.Loader(cfg2, container=handle, engine=loader.engine)
         steps_e2e = min(args.steps, max(1, len(handle) // ws // B))
-        it = l2.epoch(1)
-        b = next(it)  # warm the staging path
+        for k, b in enumerate(l2.epoch(1)):  # warm the staging pool and output ring
+            if k + 1 >= min(steps_e2e, 3 * cfg.streams + 3):
+                break
         torch.cuda.synchronize(dev)
         if ws > 1:
             dist.barrier()

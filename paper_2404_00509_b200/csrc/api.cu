@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -35,6 +38,70 @@ int fail(int code, const std::string &msg) {
 
 constexpr int kDescRing = 8;
 
+// Persistent host workers for payload staging (one pool per context): a
+// batch's copies are split into contiguous ranges, the caller thread takes
+// one range and waits for the rest.
+class StagePool {
+ public:
+  explicit StagePool(int n) {
+    for (int i = 0; i < n; i++) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~StagePool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : th_) t.join();
+  }
+  int size() const { return (int)th_.size(); }
+  // Runs fn(part, nparts) for part in [0, nparts): parts 1.. on the pool, part 0 here.
+  void run(int nparts, const std::function<void(int, int)> &fn) {
+    nparts = std::max(1, std::min(nparts, (int)th_.size() + 1));
+    {
+      std::lock_guard<std::mutex> g(m_);
+      fn_ = &fn;
+      parts_ = nparts;
+      pending_ = nparts - 1;
+      gen_++;
+    }
+    cv_.notify_all();
+    fn(0, nparts);
+    std::unique_lock<std::mutex> l(m_);
+    done_.wait(l, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void loop(int i) {
+    uint64_t seen = 0;
+    while (true) {
+      const std::function<void(int, int)> *fn;
+      int parts;
+      {
+        std::unique_lock<std::mutex> l(m_);
+        cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        fn = fn_;
+        parts = parts_;
+      }
+      if (i + 1 < parts) {
+        (*fn)(i + 1, parts);
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)> *fn_ = nullptr;
+  int parts_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 }  // namespace
 
 struct essl_ctx {
@@ -53,6 +120,7 @@ struct essl_ctx {
   uint64_t stage_cap = 0;
   cudaEvent_t ev_stage[2] = {};
   bool stage_used[2] = {};
+  std::unique_ptr<StagePool> stage_pool;  // created on first staged batch
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = ESSL_DECODE_SPECULATIVE;
@@ -345,16 +413,17 @@ int essl_stage(essl_ctx *c, int slot, const uint8_t *const *src, const uint32_t 
   off[n] = pos;
   uint8_t *h = c->h_stage[slot];
   nthreads = std::max(1, std::min(nthreads, n));
-  auto work = [&](int t) {
-    for (int i = t; i < n; i += nthreads) std::memcpy(h + off[i], src[i], len[i]);
+  if (nthreads > 1 && (!c->stage_pool || c->stage_pool->size() + 1 < nthreads))
+    c->stage_pool.reset(new StagePool(nthreads - 1));
+  // contiguous ranges of samples with about equal bytes per part
+  auto work = [&](int part, int parts) {
+    const uint64_t lo = pos * part / parts, hi = pos * (part + 1) / parts;
+    int i = (int)(std::upper_bound(off.begin(), off.begin() + n, lo) - off.begin()) - 1;
+    for (i = std::max(i, 0); i < n && off[i] < hi; i++)
+      if (off[i] >= lo) std::memcpy(h + off[i], src[i], len[i]);
   };
-  if (nthreads == 1) {
-    work(0);
-  } else {
-    std::vector<std::thread> th;
-    for (int t = 0; t < nthreads; t++) th.emplace_back(work, t);
-    for (auto &x : th) x.join();
-  }
+  if (nthreads == 1) work(0, 1);
+  else c->stage_pool->run(nthreads, work);
   for (int i = 0; i < n; i++) {
     samples[i].offset = off[i];
     samples[i].length = len[i];
@@ -388,6 +457,14 @@ int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
   pp.out = out;
   pp.out_stride = out_stride;
   pp.out_u8 = out_u8;
+  {
+    int words = 0;
+    for (int i = 0; i < n; i++)
+      words = std::max(words, essl::band_source_rows(samples[i].h, res) * std::max(samples[i].w, 1));
+    pp.src_words = (words + 3) / 4 * 4;
+    if ((size_t)pp.src_words * 4 + (size_t)res * 16 > 200 * 1024)
+      return fail(ESSL_E_CAPACITY, "crop too large for the resize kernel's shared staging");
+  }
   if (out_kind != ESSL_OUT_NONE || out_u8) {
     Prof pr(c, ESSL_K_RESIZE, st);
     essl::launch_resize(pp, st);

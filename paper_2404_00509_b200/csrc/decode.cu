@@ -368,7 +368,15 @@ struct Reader {
   }
   // keeps >= 33 bits buffered: one unit (code + magnitude) is <= 31 bits
   __device__ __forceinline__ void refill() {
-    if (n <= 32) {
+    if (SH) {
+      // shared memory: the next word is read every step, unconditionally (a
+      // short LDS, no branch -- in a warp some lane refills almost every step)
+      const uint32_t wv = ld(wi);
+      const bool rf = n <= 32;
+      buf |= rf ? (uint64_t)wv << (32 - n) : 0ull;
+      n += rf ? 32 : 0;
+      wi += rf ? 1u : 0u;
+    } else if (n <= 32) {
       buf |= (uint64_t)ld(wi) << (32 - n);
       n += 32;
       wi++;

@@ -88,6 +88,7 @@ struct PixelParams {
   void *out;
   int64_t out_stride;  // elements per sample
   uint8_t *out_u8;
+  int src_words;       // k_resize shared source rows: band source rows x widest crop
 };
 
 // splitmix64 (rng.py:27-31)
@@ -114,6 +115,7 @@ void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
 size_t ckpt_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
+int band_source_rows(int h, int res);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);
 void launch_mask(uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens,

@@ -89,114 +89,154 @@ __device__ __forceinline__ float norm_value(int c, int v) {
   return __fdiv_rn(__fsub_rn(__fmul_rn((float)v, inv255), mean), sd);
 }
 
-// grid: (ceil(res * ceil(res/8) / kPixThreads), n).  Thread = 8 consecutive
-// output pixels of one row, all three channels.
+// k_resize: one CTA per band of kBandRows output rows of one image.
+//  1. the source rows the band's bilinear taps touch are colour-converted
+//     once into shared memory (RGBX words, coalesced plane reads);
+//  2. per output column the x taps and weight (flip folded in) are tabulated;
+//  3. each thread produces 8 consecutive output pixels of a row: exact fp64
+//     bilinear from shared memory, normalize through a 256-entry LUT of the
+//     exact fp32 value, 128-bit bf16 (or fp32 / uint8) stores.
+// grid: (ceil(res / kBandRows), n); dynamic smem: P.band_src_rows x P.max_w
+// words + the column table.
+constexpr int kBandRows = 16;
+
 __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
+  extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ float lut[3][256];
   __shared__ __nv_bfloat16 lutb[3][256];
+  const int img = blockIdx.y;
+  const ImgInfo &I = P.info[img];
+  if (I.status != 0) return;
   for (int i = threadIdx.x; i < 768; i += kPixThreads) {
     const float f = norm_value(i >> 8, i & 255);
     lut[i >> 8][i & 255] = f;
     lutb[i >> 8][i & 255] = __float2bfloat16_rn(f);
   }
-  __syncthreads();
-  const int img = blockIdx.y;
-  const ImgInfo &I = P.info[img];
-  if (I.status != 0) return;
   const int res = P.res;
-  const int groups = (res + 7) >> 3;
-  const int t = blockIdx.x * kPixThreads + threadIdx.x;
-  if (t >= res * groups) return;
-  const int oy = t / groups, ox0 = (t % groups) * 8;
-  PlaneSrc S;
-  S.load(I, P.plane);
+  const int ob0 = blockIdx.x * kBandRows;
+  const int ob1 = min(ob0 + kBandRows, res);
   const int ih = I.rh, iw = I.rw;
   const double sy = __ddiv_rn((double)ih, (double)res), sx = __ddiv_rn((double)iw, (double)res);
-  int y0, y1;
-  double wy;
-  tap(oy, sy, ih, y0, y1, wy);
-  y0 += I.ry;
-  y1 += I.ry;
-  uint8_t px[8][3];
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const int ox = ox0 + i;
-    if (ox >= res) { px[i][0] = px[i][1] = px[i][2] = 0; continue; }
+  // source rows of the band (taps are monotone in the output row)
+  int ys0, ys1, dummy;
+  double wdum;
+  tap(ob0, sy, ih, ys0, dummy, wdum);
+  tap(ob1 - 1, sy, ih, dummy, ys1, wdum);
+  const int nrows = ys1 - ys0 + 1;
+  uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
+  double *cw = reinterpret_cast<double *>(dyn + (size_t)P.src_words * 4);   // [res] x weights
+  int2 *cx = reinterpret_cast<int2 *>(cw + res);                              // [res] x taps
+  PlaneSrc S;
+  S.load(I, P.plane);
+  for (int e = threadIdx.x; e < nrows * iw; e += kPixThreads) {
+    const int r = e / iw, x = e - r * iw;
+    int cr, cg, cb;
+    S.rgb(I.ry + ys0 + r, I.rx + x, cr, cg, cb);
+    src[e] = (uint32_t)cr | ((uint32_t)cg << 8) | ((uint32_t)cb << 16);
+  }
+  for (int ox = threadIdx.x; ox < res; ox += kPixThreads) {
     const int xs = I.flip ? res - 1 - ox : ox;  // hflip after resize
     int x0, x1;
     double wx;
     tap(xs, sx, iw, x0, x1, wx);
-    x0 += I.rx;
-    x1 += I.rx;
-    int r00, g00, b00, r01, g01, b01, r10, g10, b10, r11, g11, b11;
-    S.rgb(y0, x0, r00, g00, b00);
-    S.rgb(y0, x1, r01, g01, b01);
-    S.rgb(y1, x0, r10, g10, b10);
-    S.rgb(y1, x1, r11, g11, b11);
-    px[i][0] = (uint8_t)bilerp(wx, wy, r00, r01, r10, r11);
-    px[i][1] = (uint8_t)bilerp(wx, wy, g00, g01, g10, g11);
-    px[i][2] = (uint8_t)bilerp(wx, wy, b00, b01, b10, b11);
+    cw[ox] = wx;
+    cx[ox] = make_int2(x0, x1);
   }
+  __syncthreads();
+  const int groups = (res + 7) >> 3;
   const int64_t plane_sz = (int64_t)res * res;
   const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
-  const bool full = ox0 + 8 <= res && (res & 7) == 0;
-  if (P.out_kind == ESSL_OUT_BF16_NCHW) {
-    __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+  for (int t = threadIdx.x; t < (ob1 - ob0) * groups; t += kPixThreads) {
+    const int oy = ob0 + t / groups, ox0 = (t % groups) * 8;
+    int y0, y1;
+    double wy;
+    tap(oy, sy, ih, y0, y1, wy);
+    const uint32_t *r0 = src + (y0 - ys0) * iw, *r1 = src + (y1 - ys0) * iw;
+    uint8_t px[8][3];
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-      if (full) {
-        __align__(16) __nv_bfloat16 v[8];
+    for (int i = 0; i < 8; i++) {
+      const int ox = ox0 + i;
+      if (ox >= res) { px[i][0] = px[i][1] = px[i][2] = 0; continue; }
+      const int2 xx = cx[ox];
+      const double wx = cw[ox];
+      const uint32_t s00 = r0[xx.x], s01 = r0[xx.y], s10 = r1[xx.x], s11 = r1[xx.y];
 #pragma unroll
-        for (int i = 0; i < 8; i++) v[i] = lutb[c][px[i][c]];
-        *reinterpret_cast<int4 *>(o + c * plane_sz) = *reinterpret_cast<int4 *>(v);
-      } else {
-        for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lutb[c][px[i][c]];
+      for (int c = 0; c < 3; c++) {
+        const int sh = 8 * c;
+        px[i][c] = (uint8_t)bilerp(wx, wy, (s00 >> sh) & 255, (s01 >> sh) & 255, (s10 >> sh) & 255,
+                                   (s11 >> sh) & 255);
       }
     }
-  } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
-    float *o = reinterpret_cast<float *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+    const bool full = ox0 + 8 <= res && (res & 7) == 0;
+    if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + (int64_t)oy * res + ox0;
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-      if (full) {
-        float4 a = make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]);
-        float4 b = make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]);
-        reinterpret_cast<float4 *>(o + c * plane_sz)[0] = a;
-        reinterpret_cast<float4 *>(o + c * plane_sz)[1] = b;
-      } else {
-        for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lut[c][px[i][c]];
-      }
-    }
-  }
-  if (P.out_u8) {
-    uint8_t *o = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox0) * 3;
-    if (full) {
-      uint32_t w[6];
+      for (int c = 0; c < 3; c++) {
+        if (full) {
+          __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
-      for (int q = 0; q < 6; q++) {
-        uint32_t acc = 0;
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-          const int e = q * 4 + b;
-          acc |= (uint32_t)px[e / 3][e % 3] << (8 * b);
+          for (int i = 0; i < 8; i++) v[i] = lutb[c][px[i][c]];
+          *reinterpret_cast<int4 *>(o + c * plane_sz) = *reinterpret_cast<int4 *>(v);
+        } else {
+          for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lutb[c][px[i][c]];
         }
-        w[q] = acc;
       }
-      // 24 bytes at an 8-byte aligned address (res % 8 == 0)
-      reinterpret_cast<uint2 *>(o)[0] = make_uint2(w[0], w[1]);
-      reinterpret_cast<uint2 *>(o)[1] = make_uint2(w[2], w[3]);
-      reinterpret_cast<uint2 *>(o)[2] = make_uint2(w[4], w[5]);
-    } else {
-      for (int i = 0; i < 8 && ox0 + i < res; i++)
-        for (int c = 0; c < 3; c++) o[i * 3 + c] = px[i][c];
+    } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+      float *o = reinterpret_cast<float *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        if (full) {
+          float4 a = make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]);
+          float4 b = make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]);
+          reinterpret_cast<float4 *>(o + c * plane_sz)[0] = a;
+          reinterpret_cast<float4 *>(o + c * plane_sz)[1] = b;
+        } else {
+          for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lut[c][px[i][c]];
+        }
+      }
+    }
+    if (P.out_u8) {
+      uint8_t *o = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox0) * 3;
+      if (full) {
+        uint32_t w[6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          uint32_t acc = 0;
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const int e = q * 4 + b;
+            acc |= (uint32_t)px[e / 3][e % 3] << (8 * b);
+          }
+          w[q] = acc;
+        }
+        // 24 bytes at an 8-byte aligned address (res % 8 == 0)
+        reinterpret_cast<uint2 *>(o)[0] = make_uint2(w[0], w[1]);
+        reinterpret_cast<uint2 *>(o)[1] = make_uint2(w[2], w[3]);
+        reinterpret_cast<uint2 *>(o)[2] = make_uint2(w[4], w[5]);
+      } else {
+        for (int i = 0; i < 8 && ox0 + i < res; i++)
+          for (int c = 0; c < 3; c++) o[i * 3 + c] = px[i][c];
+      }
     }
   }
 }
 
+// Source rows a band of kBandRows output rows can touch for a crop of height
+// h resized to res (taps y0..y1 of rows ob0..ob0+15, imgops.py:33-41).
+int band_source_rows(int h, int res) {
+  return (int)(((int64_t)kBandRows * h + res - 1) / res) + 3;
+}
+
 void launch_resize(const PixelParams &p, cudaStream_t st) {
   if (p.n <= 0) return;
-  const int groups = (p.res + 7) / 8;
-  dim3 grid((p.res * groups + kPixThreads - 1) / kPixThreads, p.n);
-  k_resize<<<grid, kPixThreads, 0, st>>>(p);
+  const size_t dyn = (size_t)p.src_words * 4 + (size_t)p.res * 16;
+  static size_t attr = 48 * 1024;
+  if (dyn > attr) {
+    cudaFuncSetAttribute(k_resize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    attr = dyn;
+  }
+  dim3 grid((p.res + kBandRows - 1) / kBandRows, p.n);
+  k_resize<<<grid, kPixThreads, dyn, st>>>(p);
 }
 
 // decode_crop output: uint8 [h, w, 3] at out + offsets[img].

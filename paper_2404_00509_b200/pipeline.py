@@ -101,7 +101,7 @@ class ImageBatch:
         return int(self.pixels.shape[0])
 
 
-_GPU_KEYS = ("device", "out_dtype", "rank", "world_size", "resident", "prefetch", "streams")
+_GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch", "streams")
 
 
 @dataclass
@@ -128,6 +128,10 @@ class LoaderConfig:
     resident: bool = True
     prefetch: int = 2
     streams: int = 2
+    # Reuse a ring of output buffers (views valid until `prefetch + streams`
+    # later batches are issued, the reference bindings' "valid until the next
+    # step" contract) instead of allocating every batch.
+    reuse_outputs: bool = False
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
@@ -252,6 +256,7 @@ class Loader:
         self._blob = self.handle.to_device(self.device) if config.resident else None
         self._host_base = self.handle.bytes.ctypes.data if not config.resident else 0
         self._slots = [0] * len(self._engines)
+        self._out_ring: dict = {}
         self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
 
     @classmethod
@@ -327,28 +332,43 @@ class Loader:
         else:
             ptrs = np.uint64(self._host_base) + samples["offset"].astype(np.uint64)
             blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
-                                 nthreads=min(self.workers, 16), stream=st)
+                                 nthreads=min(self.workers, 8), stream=st)
             self._slots[j] ^= 1
         dev = self.device
-        pixels = torch.empty((b, 3, res, res), dtype=self._out_dtype, device=dev)
-        u8 = torch.empty((b, res, res, 3), dtype=torch.uint8, device=dev) if cfg.keep_uint8 else None
+        ring = self._rings[j]
+        slot = ring.take()  # the batch that last used this slot has completed
+        T = k = 0
+        if self.mask_spec is not None:
+            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
+
+        def out(name, shape, dtype):
+            if not cfg.reuse_outputs:
+                return torch.empty(shape, dtype=dtype, device=dev)
+            key = (j, slot, name)
+            t = self._out_ring.get(key)
+            if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+                t = torch.empty(shape, dtype=dtype, device=dev)
+                self._out_ring[key] = t
+            return t
+
+        pixels = out("pixels", (b, 3, res, res), self._out_dtype)
+        u8 = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
         results = eng.new_results(b)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
         eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st)
-        ring = self._rings[j]
-        slot = ring.take()
         hidx, hlab, res_host = ring.idx[slot][:b], ring.lab[slot][:b], ring.res[slot][:b]
         hidx.numpy()[:] = idxs
         hlab.numpy()[:] = self._labels_np[idxs]
         with torch.cuda.stream(st):  # pinned sources: truly asynchronous copies
-            indices = hidx.to(dev, non_blocking=True)
-            labels = hlab.to(dev, non_blocking=True)
+            indices = out("indices", (b,), torch.int64)
+            labels = out("labels", (b,), torch.int64)
+            indices.copy_(hidx, non_blocking=True)
+            labels.copy_(hlab, non_blocking=True)
         mask = keep = restore = None
         if self.mask_spec is not None:
-            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
-            mask = torch.empty((b, k), dtype=torch.int32, device=dev)
-            keep = torch.empty((b, T - k), dtype=torch.int64, device=dev)
-            restore = torch.empty((b, T), dtype=torch.int64, device=dev)
+            mask = out("mask", (b, k), torch.int32)
+            keep = out("keep", (b, T - k), torch.int64)
+            restore = out("restore", (b, T), torch.int64)
             eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=st)
         with torch.cuda.stream(st):
             res_host.copy_(results, non_blocking=True)
