@@ -344,18 +344,31 @@ def run_gpu(args, wl):
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         n2 = 0
-        it = l2.epoch(2)
-        perm2 = E.shard(E.epoch_permutation(cfg.seed, 2, len(handle)), rank, ws)
-        for k, b in enumerate(it):
-            n2 += len(b)
-            if k + 1 >= steps_e2e:
-                break
+        perm2 = []
+        e2e_host = []
+        ep = 2
+        hprev = time.perf_counter()
+        while n2 < args.steps * B:  # as many batches as the device-side timed region
+            perm2.append(E.shard(E.epoch_permutation(cfg.seed, ep, len(handle)), rank, ws))
+            for b in l2.epoch(ep):
+                n2 += len(b)
+                now = time.perf_counter()
+                e2e_host.append(now - hprev)
+                hprev = now
+                if n2 >= args.steps * B:
+                    break
+            ep += 1
+        perm2 = np.concatenate(perm2)
         s1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = s0.elapsed_time(s1)
+        steps_e2e = max(1, n2 // B)
         lens = handle.records["payload_length"][perm2[:n2]].astype(np.int64)
-        h2d = int(((lens + 63) // 64 * 64).sum()) // max(steps_e2e, 1) + \
-            B * ctypes_sizeof_sample() + 8 * B * 2
+        h2d = int(lens.sum()) // steps_e2e + B * (ctypes_sizeof_sample() + 24) + 8 * B * 2
+        if os.environ.get("ESSL_BENCH_HOSTLOG"):
+            eh = np.array(e2e_host) * 1e3
+            log(f"[bench] e2e per-batch host ms median {np.median(eh):.3f} max {eh.max():.3f} "
+                f"(argmax {int(eh.argmax())})")
         d2h = B * 32
         e2e_v = (n2, e2e_ms)
     # ---- reduce over ranks ---------------------------------------------------

@@ -144,6 +144,20 @@ const char *essl_version(void);
 int essl_stage(essl_ctx *ctx, int slot, const uint8_t *const *src,
                const uint32_t *len, int n, essl_sample *samples,
                int nthreads, void *stream, const uint8_t **dev_blob);
+/* Pinned-container staging (the e2e host->device path): the container's host
+ * bytes are page-locked once (essl_host_register: read-only, mapped
+ * registration of the file mapping; essl_host_device_ptr gives its device
+ * address).  Each batch's payloads are then gathered host->device by one
+ * light kernel reading the pinned container over the bus (k_host_gather)
+ * into the context's staging slot, with the same 64-byte packing and
+ * `samples` rewrite as essl_stage.  Replaces: ContainerHandle.read_sample's
+ * payload slice (container.py:249-265) for a whole batch. */
+int essl_host_register(void *ptr, uint64_t bytes, int readonly);
+int essl_host_unregister(void *ptr);
+int essl_host_device_ptr(void *ptr, void **dev_ptr);
+int essl_stage_pinned(essl_ctx *ctx, int slot, const uint8_t *dev_base, const uint64_t *src_off,
+                      const uint32_t *len, int n, essl_sample *samples, void *stream,
+                      const uint8_t **dev_blob);
 
 /* ---- the hot path --------------------------------------------------------
  * Replaces: Loader._fill_sample (pipeline.py:219-235) for a whole batch:

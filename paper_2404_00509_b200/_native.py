@@ -24,7 +24,8 @@ KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep"
 EXPORTS = (
     "essl_ctx_create", "essl_ctx_destroy", "essl_ctx_set_option", "essl_ctx_launch_count",
     "essl_ctx_profile_read", "essl_profile_mark", "essl_ctx_profile_timeline", "essl_debug_stats",
-    "essl_last_error", "essl_version", "essl_stage", "essl_decode_rrc", "essl_decode_crop_u8",
+    "essl_last_error", "essl_version", "essl_stage", "essl_stage_pinned", "essl_host_register",
+    "essl_host_unregister", "essl_host_device_ptr", "essl_decode_rrc", "essl_decode_crop_u8",
     "essl_dump_coefs", "essl_mask", "essl_mask_from_states", "essl_gather_visible", "essl_resize_u8",
     "essl_normalize_u8", "essl_rng_init", "essl_rng_next", "essl_rng_random",
     "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
@@ -93,6 +94,10 @@ def lib():
         "essl_last_error": (ctypes.c_char_p, []),
         "essl_version": (ctypes.c_char_p, []),
         "essl_stage": (i32, [P, i32, P, P, i32, P, i32, P, P]),
+        "essl_stage_pinned": (i32, [P, i32, P, P, P, i32, P, P, P]),
+        "essl_host_register": (i32, [P, ctypes.c_uint64, i32]),
+        "essl_host_unregister": (i32, [P]),
+        "essl_host_device_ptr": (i32, [P, P]),
         "essl_decode_rrc": (i32, [P, P, P, i32, i32, i32, P, i64, P, P, P]),
         "essl_decode_crop_u8": (i32, [P, P, P, i32, P, P, P, P]),
         "essl_dump_coefs": (i32, [P, P, P, i32, P, P, i64, P, P, P]),

@@ -64,6 +64,7 @@ class ContainerHandle:
             raise CroploadError(f"container not found: {self.path}")
         self._file = open(self.path, "rb")
         self._dev = {}
+        self._pinned = None
         try:
             self._size = os.fstat(self._file.fileno()).st_size
             head = self._file.read(_HEADER_SIZE)
@@ -106,6 +107,11 @@ class ContainerHandle:
 
     def close(self) -> None:
         self._dev.clear()
+        if getattr(self, "_pinned", None) is not None:
+            if self._pinned[1] is None:
+                from . import _native as N
+                N.lib().essl_host_unregister(ctypes.c_void_p(self._pinned[0]))
+            self._pinned = None
         self.bytes = None
         if getattr(self, "_mmap", None) is not None:
             try:
@@ -166,6 +172,29 @@ class ContainerHandle:
                 t[s:s + chunk].copy_(host[s:s + chunk], non_blocking=False)
             self._dev[key] = t
         return t
+
+    def pinned_host(self) -> int:
+        """Host address of the whole file, page-locked for copy-engine
+        gathers (essl_stage_pinned): the read-only file mapping registered in
+        place, or (where the driver refuses that) a pinned copy."""
+        if self._pinned is not None:
+            return self._pinned[2]
+        from . import _native as N
+        import torch
+        torch.cuda.init()
+        base = int(self.bytes.ctypes.data) if self._size else 0
+        if self._size and N.lib().essl_host_register(ctypes.c_void_p(base), self._size, 1) == 0:
+            host, buf = base, None
+        else:
+            buf = torch.empty(max(self._size, 1), dtype=torch.uint8, pin_memory=True)
+            if self._size:
+                buf.numpy()[:self._size] = self.bytes
+            host = int(buf.data_ptr())
+        dev = ctypes.c_void_p()
+        N.check(N.lib().essl_host_device_ptr(ctypes.c_void_p(host), ctypes.byref(dev)),
+                "essl_host_device_ptr")
+        self._pinned = (host, buf, int(dev.value))
+        return self._pinned[2]
 
     def max_dims(self) -> tuple[int, int]:
         if len(self) == 0:

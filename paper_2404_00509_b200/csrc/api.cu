@@ -121,6 +121,7 @@ struct essl_ctx {
   cudaEvent_t ev_stage[2] = {};
   bool stage_used[2] = {};
   std::unique_ptr<StagePool> stage_pool;  // created on first staged batch
+  essl::GatherDesc *h_gather[2] = {}, *d_gather[2] = {};  // pinned-container gathers
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = ESSL_DECODE_SPECULATIVE;
@@ -275,6 +276,8 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
     CKC(cudaMallocHost(&c->h_stage[r], c->stage_cap));
     CKC(cudaMalloc(&c->d_stage[r], c->stage_cap));
     CKC(cudaEventCreateWithFlags(&c->ev_stage[r], cudaEventDisableTiming));
+    CKC(cudaMallocHost(&c->h_gather[r], sizeof(essl::GatherDesc) * max_batch));
+    CKC(cudaMalloc(&c->d_gather[r], sizeof(essl::GatherDesc) * max_batch));
   }
 #undef CKC
   static std::once_flag once;
@@ -305,6 +308,8 @@ int essl_ctx_destroy(essl_ctx *c) {
     if (c->h_stage[r]) cudaFreeHost(c->h_stage[r]);
     if (c->d_stage[r]) cudaFree(c->d_stage[r]);
     if (c->ev_stage[r]) cudaEventDestroy(c->ev_stage[r]);
+    if (c->h_gather[r]) cudaFreeHost(c->h_gather[r]);
+    if (c->d_gather[r]) cudaFree(c->d_gather[r]);
   }
   for (auto &r : c->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->pool) cudaEventDestroy(e);
@@ -429,6 +434,59 @@ int essl_stage(essl_ctx *c, int slot, const uint8_t *const *src, const uint32_t 
     samples[i].length = len[i];
   }
   if (pos) CK(cudaMemcpyAsync(c->d_stage[slot], h, pos, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(c->ev_stage[slot], st));
+  c->stage_used[slot] = true;
+  *dev_blob = c->d_stage[slot];
+  return ESSL_OK;
+}
+
+int essl_host_register(void *ptr, uint64_t bytes, int readonly) {
+  if (!ptr || bytes == 0) return fail(ESSL_E_ARG, "essl_host_register: bad arguments");
+  const unsigned flags = cudaHostRegisterPortable | cudaHostRegisterMapped |
+                         (readonly ? cudaHostRegisterReadOnly : 0u);
+  const cudaError_t e = cudaHostRegister(ptr, bytes, flags);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // not sticky: leave no error for later launches
+    return fail(ESSL_E_CUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+  }
+  return ESSL_OK;
+}
+
+int essl_host_unregister(void *ptr) {
+  if (!ptr) return fail(ESSL_E_ARG, "essl_host_unregister: null");
+  CK(cudaHostUnregister(ptr));
+  return ESSL_OK;
+}
+
+int essl_host_device_ptr(void *ptr, void **dev_ptr) {
+  if (!ptr || !dev_ptr) return fail(ESSL_E_ARG, "essl_host_device_ptr: bad arguments");
+  CK(cudaHostGetDevicePointer(dev_ptr, ptr, 0));
+  return ESSL_OK;
+}
+
+int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint64_t *src_off,
+                      const uint32_t *len, int n, essl_sample *samples, void *stream,
+                      const uint8_t **dev_blob) {
+  if (!c || slot < 0 || slot > 1 || n < 0 || n > c->max_batch || !dev_blob || (n > 0 && (!dev_base || !src_off || !len)))
+    return fail(ESSL_E_ARG, "essl_stage_pinned: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
+  essl::GatherDesc *h = c->h_gather[slot];
+  uint64_t pos = 0;
+  for (int i = 0; i < n; i++) {
+    if ((int)len[i] > c->max_payload) return fail(ESSL_E_CAPACITY, "payload larger than max_payload");
+    h[i].src = src_off[i];
+    h[i].dst = pos;
+    h[i].len = len[i];
+    samples[i].offset = pos;
+    samples[i].length = len[i];
+    pos += ((uint64_t)len[i] + 63) / 64 * 64;
+  }
+  if (n > 0) {
+    CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
+    essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], st);
+    c->launches += 1;
+  }
   CK(cudaEventRecord(c->ev_stage[slot], st));
   c->stage_used[slot] = true;
   *dev_blob = c->d_stage[slot];

@@ -108,6 +108,12 @@ __host__ __device__ __forceinline__ uint64_t rng_init(uint64_t seed, uint64_t ep
   return h;
 }
 
+// One payload of a pinned-container gather (essl_stage_pinned).
+struct GatherDesc {
+  uint64_t src, dst;
+  uint32_t len, pad;
+};
+
 // launch wrappers (defined in the .cu files)
 void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len);
@@ -115,6 +121,7 @@ void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
 size_t ckpt_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
+void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, cudaStream_t st);
 int band_source_rows(int h, int res);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);

@@ -413,4 +413,38 @@ void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStrea
   k_normalize_u8<<<148, 256, 0, st>>>(src, h, w, dst);
 }
 
+// ---------------------------------------------------------------------------
+// Pinned-container gather: payload bytes read host->device over the bus by
+// a light kernel (no shared memory, so it co-runs with the decode kernels of
+// other batches).  One CTA per payload; each thread keeps four 16-byte loads
+// in flight to cover the bus latency.  Sources are 64-byte aligned in the
+// container (container.py:26); an unaligned source takes the byte path.
+__global__ void __launch_bounds__(128) k_host_gather(const uint8_t *src, const GatherDesc *desc,
+                                                     uint8_t *dst) {
+  const GatherDesc d = desc[blockIdx.x];
+  const uint8_t *s = src + d.src;
+  uint8_t *o = dst + d.dst;
+  if (((d.src | d.dst) & 15) == 0) {
+    const int4 *s4 = reinterpret_cast<const int4 *>(s);
+    int4 *o4 = reinterpret_cast<int4 *>(o);
+    const uint32_t n16 = d.len / 16;
+    for (uint32_t i = threadIdx.x; i < n16; i += 4 * 128) {
+      int4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i + u * 128 < n16) v[u] = s4[i + u * 128];
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (i + u * 128 < n16) o4[i + u * 128] = v[u];
+    }
+    for (uint32_t i = n16 * 16 + threadIdx.x; i < d.len; i += 128) o[i] = s[i];
+  } else {
+    for (uint32_t i = threadIdx.x; i < d.len; i += 128) o[i] = s[i];
+  }
+}
+
+void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, cudaStream_t st) {
+  if (n > 0) k_host_gather<<<n, 128, 0, st>>>(src, d, dst);
+}
+
 }  // namespace essl

@@ -124,6 +124,20 @@ class Engine:
                                    nthreads, self._st(stream), ctypes.byref(blob)), "essl_stage")
         return blob.value
 
+    def stage_pinned(self, slot: int, host_base: int, offsets: np.ndarray, lens: np.ndarray,
+                     samples: np.ndarray, stream=None):
+        """Gather payloads of a page-locked container (host_base + offsets)
+        host->device with one batched copy; fills samples['offset'/'length']."""
+        n = len(samples)
+        self._ensure(n, 0, int(lens.max()) if n else 0)
+        blob = ctypes.c_void_p()
+        o = np.ascontiguousarray(offsets, np.uint64)
+        ln = np.ascontiguousarray(lens, np.uint32)
+        N.check(N.lib().essl_stage_pinned(self._ctx, slot, ctypes.c_void_p(host_base), N.ptr(o), N.ptr(ln),
+                                          n, N.ptr(samples), self._st(stream), ctypes.byref(blob)),
+                "essl_stage_pinned")
+        return blob.value
+
     def decode_rrc(self, blob_ptr: int, samples: np.ndarray, res: int, out_kind: int,
                    out=None, out_u8=None, results=None, stream=None, max_side: int = 0):
         n = len(samples)

@@ -254,7 +254,7 @@ class Loader:
         self._crcs = np.ascontiguousarray(rec["checksum"], np.uint32)
         self._labels_np = rec["label"].astype(np.int64)
         self._blob = self.handle.to_device(self.device) if config.resident else None
-        self._host_base = self.handle.bytes.ctypes.data if not config.resident else 0
+        self._pinned_base = self.handle.pinned_host() if not config.resident else 0
         self._slots = [0] * len(self._engines)
         self._out_ring: dict = {}
         self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
@@ -329,10 +329,9 @@ class Loader:
         samples = self._descriptors(epoch, idxs)
         if self._blob is not None:
             blob_ptr = self._blob.data_ptr()
-        else:
-            ptrs = np.uint64(self._host_base) + samples["offset"].astype(np.uint64)
-            blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
-                                 nthreads=min(self.workers, 8), stream=st)
+        else:  # host container: one batched copy-engine gather from pinned memory
+            blob_ptr = eng.stage_pinned(self._slots[j], self._pinned_base, samples["offset"],
+                                        samples["length"].copy(), samples, stream=st)
             self._slots[j] ^= 1
         dev = self.device
         ring = self._rings[j]
