@@ -102,6 +102,7 @@ struct __align__(16) DecodeHdr {
   int32_t ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ncomp, ntab;
   uint32_t limit_blocks, clean_bits, clean_words, tab_index_word;
   uint32_t wmax;  // last readable word of the clean stream (0xFF padding)
+  uint32_t cpad;  // first 16-byte chunk of the clean stream that is all 0xFF padding
   int32_t scan_ri, scan_start, scan_end, n_restarts, max_restarts;
   int32_t slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
   int32_t wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
@@ -341,41 +342,75 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
-// Bit reader over the clean stream (big-endian words; k_prep byte-swaps),
-// in shared memory (SH, staged by k_entropy) or global memory (payloads too
-// large to stage).  Reads past the end clamp to the last word, which is all
-// 0xFF padding (_br_fill, decode_kernels.py:64-74).
+// Bit reader over the clean stream (big-endian words; k_prep byte-swaps).
+// SH: each lane reads through its own 64-byte ring in shared memory, filled
+// by cp.async four 16-byte chunks ahead of consumption -- refills are short
+// LDS reads with no global latency on the decode chain, and the footprint is
+// 64 bytes per lane whatever the payload size.  !SH: plain global loads
+// (validation path).  Words past the data read as 0xFF padding
+// (_br_fill, decode_kernels.py:64-74): global reads clamp to the last word,
+// ring chunks past the data clamp to chunk `cpad` (all 0xFF, k_prep).
 template <bool SH>
 struct Reader {
-  const uint32_t *w;  // global words (!SH)
-  uint32_t ws;        // shared-window address of word 0 (SH)
-  uint32_t wmax;      // last word index
+  const uint32_t *w;  // global words
+  uint32_t wmax;      // last word index (global path)
+  uint32_t cpad;      // first all-0xFF 16-byte chunk (ring path)
+  uint32_t rs;        // this lane's ring (shared-window address, 16 words)
   uint64_t buf;       // left-aligned bit buffer
   int n;              // valid bits in buf
   uint32_t wi;        // index of the next word to load
   uint32_t p;         // absolute bit position of buf's MSB
   __device__ __forceinline__ uint32_t ld(uint32_t i) const {
-    if (SH) return lds_u32(ws + (min(i, wmax) << 2));
+    if (SH) return lds_u32(rs + ((i & 15) << 2));
     return __ldg(w + min(i, wmax));
+  }
+  // ring: issue chunk c (4 words) into its slot; one commit group per chunk
+  __device__ __forceinline__ void issue(uint32_t c, bool pred) const {
+    const uint32_t dst = rs + ((c & 3) << 4);
+    const uint32_t *src = w + 4 * (size_t)min(c, cpad);
+    asm volatile(
+        "{ .reg .pred q; setp.ne.u32 q, %0, 0;\n"
+        "  @q cp.async.cg.shared.global [%1], [%2], 16;\n"
+        "  @q cp.async.commit_group;\n"
+        "  @q cp.async.wait_group 3; }" ::"r"((uint32_t)pred),
+        "r"(dst), "l"(src)
+        : "memory");
   }
   __device__ __forceinline__ void init(uint32_t pos) {
     const uint32_t i = pos >> 5;
     const int off = pos & 31;
+    if (SH) {
+      // drain this lane's copies still in flight: they target the same slots
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      const uint32_t c = i >> 2;
+#pragma unroll
+      for (uint32_t q = 0; q < 4; q++) {
+        const uint32_t dst = rs + (((c + q) & 3) << 4);
+        const uint32_t *src = w + 4 * (size_t)min(c + q, cpad);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n cp.async.commit_group;" ::"r"(dst),
+                     "l"(src)
+                     : "memory");
+      }
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     buf = (((uint64_t)ld(i) << 32) | ld(i + 1)) << off;
     n = 64 - off;
     wi = i + 2;
     p = pos;
+    if (SH && (wi & 3) < 2) issue((wi >> 2) + 3, true);  // consumed into a new chunk
   }
   // keeps >= 33 bits buffered: one unit (code + magnitude) is <= 31 bits
   __device__ __forceinline__ void refill() {
     if (SH) {
-      // shared memory: the next word is read every step, unconditionally (a
-      // short LDS, no branch -- in a warp some lane refills almost every step)
+      // the next word is read every step, unconditionally (a short LDS, no
+      // branch -- in a warp some lane refills almost every step)
       const uint32_t wv = ld(wi);
       const bool rf = n <= 32;
       buf |= rf ? (uint64_t)wv << (32 - n) : 0ull;
       n += rf ? 32 : 0;
       wi += rf ? 1u : 0u;
+      // entering a new chunk frees the oldest slot: fetch chunk + 3 into it
+      issue((wi >> 2) + 3, rf && (wi & 3) == 0);
     } else if (n <= 32) {
       buf |= (uint64_t)ld(wi) << (32 - n);
       n += 32;
@@ -426,8 +461,8 @@ struct EntCtx {
   int c1, c2, bpm, gx;
   uint32_t cbits, limit, ck_bits;
   const uint32_t *words;  // clean stream (global)
-  uint32_t words_s;       // clean stream staged in shared memory (shared-window address)
-  uint32_t wmax;
+  uint32_t ring_s;        // this lane's read ring (shared-window address)
+  uint32_t wmax, cpad;
   __device__ __forceinline__ uint32_t tab_off(int k, int b) const {
     const bool s1 = b >= c1, s2 = b >= c2;
     const uint32_t d = s2 ? d2 : (s1 ? d1 : d0);
@@ -450,8 +485,9 @@ struct EntCtx {
   template <bool SH>
   __device__ __forceinline__ void reader(Reader<SH> &r, uint32_t pos) const {
     r.w = words;
-    r.ws = words_s;
+    r.rs = ring_s;
     r.wmax = wmax;
+    r.cpad = cpad;
     r.init(pos);
   }
 };
@@ -998,7 +1034,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     S.t0 = clock64();
     H.status = 0; H.reason = 0; H.offset = -1;
     H.ntab = 0; H.ns = 0; H.ncomp = 0; H.quant_missing = -1;
-    H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0; H.wmax = 0;
+    H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0; H.wmax = 0; H.cpad = 0;
   }
   // ---- stage the payload into shared memory (16-byte loads) ----------------
   if (SMEM) {
@@ -1231,7 +1267,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         const int seglen = PS.scan_end - PS.scan_start;
         H.max_restarts = PS.scan_ri ? (H.gx * H.gy) / PS.scan_ri : 0;
         const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
-        const uint64_t clean_bytes = ((uint64_t)seglen + 48 + 15) / 16 * 16;
+        const uint64_t clean_bytes = ((uint64_t)seglen + 64 + 15) / 16 * 16;
         const uint64_t alloc = (clean_bytes + 4ull * max_r + 16 + 15) / 16 * 16;
         const unsigned long long base = atomicAdd(&P.s.counters[0], (unsigned long long)alloc);
         if (base + alloc > P.s.clean_cap) hdr_status(H, ESSL_ST_CAPACITY, R_SCRATCH, -1);
@@ -1339,9 +1375,10 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     __syncthreads();
     // 0xFF padding past the end (_br_fill), >= 2 whole words; the clean
     // stream goes to global as big-endian words (the bit reader's order)
-    if (tid < 24) clean[tk + tid] = 0xFF;
+    // (48 bytes: at least two whole words and one whole 16-byte chunk)
+    if (tid < 48) clean[tk + tid] = 0xFF;
     __syncthreads();
-    const int nwords = (int)((tk + 3) / 4 + 2);
+    const int nwords = (int)((tk + 48) / 4);
     if (SMEM) {
       const int n16 = (nwords + 3) / 4;
       const uint4 *src = reinterpret_cast<const uint4 *>(clean);
@@ -1359,6 +1396,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     if (tid == 0) {
       H.clean_bits = tk * 8;
       H.wmax = (uint32_t)nwords - 1;
+      H.cpad = (tk + 15) / 16;
       H.clean_words = (tk + 3) / 4;
       H.n_restarts = (int)tr;
       if (PS.scan_ri == 0 && tr > 0) hdr_status(H, ESSL_ST_MALFORMED, R_RST_NO_DRI, seg0);
@@ -1509,6 +1547,7 @@ struct __align__(16) EntSmem {
   int32_t dcsum[kLanes * 3];
   uint32_t sink[kLanes * 2];
   int fmt;
+  __align__(16) uint32_t ring[kLanes][16];
   long long t_ph[8];
 };
 
@@ -1774,19 +1813,12 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   C.wmax = H.wmax;
   C.ck_bits = 0;
   uint32_t dbg_nseq = 0, dbg_cont = 0;
-  // stage the clean stream in shared memory when it fits the launch's
-  // dynamic allocation (k_prep pads it with >= 2 words of 0xFF)
-  extern __shared__ __align__(16) uint32_t s_words[];
-  const uint32_t nwords = H.status == 0 ? H.wmax + 1 : 0u;
-  const bool staged = nwords * 4 <= P.stage_bytes;
-  if (staged && S.status == 0) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(C.words);
-    uint4 *dst = reinterpret_cast<uint4 *>(s_words);
-    for (uint32_t i = lane; i < (nwords + 3) / 4; i += kLanes) dst[i] = src[i];
-  }
-  C.words_s = (uint32_t)__cvta_generic_to_shared(s_words);
+  // per-lane read rings (cp.async) unless the validation option asks for
+  // plain global reads
+  const bool staged = P.stage_bytes != 0;
+  C.ring_s = (uint32_t)__cvta_generic_to_shared(&S.ring[lane][0]);
+  C.cpad = H.cpad;
   __syncthreads();
-
   if (staged) entropy_body<true>(P, S, C, img, lane, dbg_nseq, dbg_cont);
   else entropy_body<false>(P, S, C, img, lane, dbg_nseq, dbg_cont);
   __syncthreads();
@@ -1970,7 +2002,7 @@ size_t ckpt_bytes() { return sizeof(Ckpt); }
 
 void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len) {
   if (p.n <= 0) return;
-  const int dyn = 2 * ((max_len + 15) / 16 * 16 + 16) + 32;
+  const int dyn = 2 * ((max_len + 15) / 16 * 16 + 16) + 96;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
@@ -1980,21 +2012,9 @@ void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len) {
   else k_prep<false><<<p.n, kNT, 0, st>>>(p);
 }
 
-// Dynamic shared memory for staging the clean stream in k_entropy; larger
-// payloads decode from global memory (same code, Reader<false>).
-constexpr int kMaxStage = 64 * 1024;
-
-void launch_entropy(const DecodeParams &p0, cudaStream_t st, int max_len) {
-  if (p0.n <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_entropy, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxStage);
-    attr = true;
-  }
-  DecodeParams p = p0;  // p0.stage_bytes: the context's staging limit
-  const int need = (max_len + 15) / 16 * 16 + 64;
-  p.stage_bytes = need <= min(kMaxStage, p0.stage_bytes) ? need : 0;
-  k_entropy<<<p.n, kLanes, p.stage_bytes, st>>>(p);
+void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len) {
+  (void)max_len;
+  if (p.n > 0) k_entropy<<<p.n, kLanes, 0, st>>>(p);
 }
 
 void launch_idct(const DecodeParams &p, cudaStream_t st) {

@@ -296,6 +296,25 @@ def test_speculative_vs_oracle_at_scale(E, oracle, synth_sets, seq_bits, ck_bits
                 assert np.array_equal(b.mask.cpu().numpy(), mask)
 
 
+@pytest.mark.parametrize("stage", [65536, 0])
+def test_large_pool_vs_oracle(E, oracle, tmp_path, stage):
+    """1024 images of 256px q95 in batches of 256 (the bench's shape): every
+    image bit-exact against the oracle, through the read rings (stage) and
+    the plain global reader (0)."""
+    from paper_2404_00509_b200 import _native as N
+    path = tmp_path / "pool.essl"
+    E.build_synthetic(path, 1024, 256, 95, seed=3)
+    cfg = E.LoaderConfig(data=str(path), batch_size=256, res=224, streams=1, prefetch=1)
+    with E.open_container(path) as h:
+        loader = E.Loader(cfg, container=h)
+        loader.set_option(N.ESSL_OPT_STAGE_BYTES, stage)
+        for b in loader.epoch(0):
+            idx = b.indices.cpu().numpy()
+            pix, _, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 0, 224, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
+
+
 def test_staged_equals_resident(E, synth_sets):
     path = synth_sets[0]
     outs = []

@@ -35,7 +35,8 @@ def main():
     path = d / "pool.essl"
     E.build_synthetic(path, args.pool, 256, 95, seed=3)
     cfg = E.LoaderConfig(data=str(path), batch_size=256, res=224, out_dtype="bfloat16",
-                         mask_ratio=0.75, resident=True, streams=args.streams, prefetch=args.streams)
+                         mask_ratio=0.75, resident=True, streams=args.streams, prefetch=args.streams,
+                         reuse_outputs=True)
     loader = E.Loader(cfg)
     perm = E.epoch_permutation(0, 0, len(loader.handle))
     nb = len(perm) // 256
@@ -44,8 +45,17 @@ def main():
         j = i % nb
         return perm[j * 256:(j + 1) * 256]
 
-    for i in range(args.warmup):
-        loader.finish(loader.enqueue(0, idx(i)))
+    pend = []
+    ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2
+    for i in range(max(args.warmup, args.streams * (ring_depth + 1))):
+        pend.append(loader.enqueue(0, idx(i)))
+        if len(pend) > 2 * args.streams:
+            loader.finish(pend.pop(0))
+    for p in pend:
+        loader.finish(p)
+    import gc
+    gc.collect()
+    gc.freeze()
     torch.cuda.synchronize()
     loader.set_option(N.ESSL_OPT_PROFILE, 1)
     loader.profile_read()
