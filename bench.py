@@ -237,6 +237,7 @@ def run_gpu(args, wl):
 
     import paper_2404_00509_b200 as E
     from paper_2404_00509_b200 import _native as N
+    from paper_2404_00509_b200.ddp import rank_shard
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -262,7 +263,7 @@ def run_gpu(args, wl):
         per_epoch = len(handle) // ws // B
         e, j = divmod(i, max(per_epoch, 1))
         if e not in perm_epochs:
-            perm_epochs[e] = E.shard(E.epoch_permutation(cfg.seed, e, len(handle)), rank, ws)
+            perm_epochs[e] = rank_shard(cfg.seed, e, len(handle), rank, ws)
         return e, perm_epochs[e][j * B:(j + 1) * B]
 
     stream = torch.cuda.current_stream(dev)
@@ -372,16 +373,9 @@ def run_gpu(args, wl):
         d2h = B * 32
         e2e_v = (n2, e2e_ms)
     # ---- reduce over ranks ---------------------------------------------------
-    vals = torch.tensor([ms, float(n_img), e2e_v[1] if e2e_v else 0.0,
-                         float(e2e_v[0]) if e2e_v else 0.0], dtype=torch.float64, device=dev)
-    if ws > 1:
-        mx = vals.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = vals.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, total, e2e_ms_max, e2e_total = float(mx[0]), float(sm[1]), float(mx[2]), float(sm[3])
-    else:
-        ms_max, total, e2e_ms_max, e2e_total = float(vals[0]), float(vals[1]), float(vals[2]), float(vals[3])
+    from paper_2404_00509_b200.ddp import reduce_timing
+    ms_max, total, e2e_ms_max, e2e_total = reduce_timing(
+        [ms, n_img, e2e_v[1] if e2e_v else 0.0, e2e_v[0] if e2e_v else 0.0], device=dev)
     if rank == 0:
         value = total / (ms_max / 1e3)
         pk = peaks()
@@ -390,15 +384,22 @@ def run_gpu(args, wl):
             T = (res // 16) ** 2
             k = int(np.floor(wl["mask"] * T + 0.5))
             per_img += k * 4 + (T - k) * 8 + T * 8
-        dec_ms, dec_n = prof.get("decode", (0.0, 0))
-        imgs_per_launch = n_img / max(dec_n, 1)
-        achieved = per_img * imgs_per_launch / (dec_ms / max(dec_n, 1) / 1e3) / 1e9 if dec_n else None
-        roof = {"bound": "hbm", "kernel": "k_prep+k_entropy", "achieved": achieved, "peak": pk["hbm_gbs"],
+        # dominant kernel (largest device-time share): k_entropy
+        ent_ms, ent_n = prof.get("entropy", (0.0, 0))
+        imgs_per_launch = n_img / max(ent_n, 1)
+        achieved = per_img * imgs_per_launch / (ent_ms / max(ent_n, 1) / 1e3) / 1e9 if ent_n else None
+        traffic = None
+        tp = ROOT / "profiles" / "r1_ncu_k_entropy.json"
+        if tp.exists() and args.workload == "cfg2":  # one ncu --set full capture of this launch shape
+            traffic = json.loads(tp.read_text()).get("dram_bytes")
+        roof = {"bound": "hbm", "kernel": "k_entropy", "achieved": achieved, "peak": pk["hbm_gbs"],
                 "peak_src": pk["src"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"] if achieved else None,
-                "traffic": None, "bytes_per_image": per_img,
+                "traffic": traffic, "traffic_src": "profiles/r1_ncu_k_entropy.json (dram read+write "
+                                                    "bytes of one launch)" if traffic else None,
+                "bytes_per_image": per_img, "images_per_launch": imgs_per_launch,
                 "kernel_ms": {k: v[0] / max(v[1], 1) for k, v in prof.items()},
-                "kernel_share": {k: v[0] / ms for k, v in prof.items()}}
+                "kernel_share": {k: v[0] / ms for k, v in prof.items() if k != "decode"}}
         cpu = None
         if not args.no_cpu:
             cpu = cpu_oracle_rate(path, wl, args.cpu_seconds)
@@ -442,7 +443,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="batches in flight (one libessl context + CUDA stream each)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])

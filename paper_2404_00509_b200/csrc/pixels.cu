@@ -72,13 +72,18 @@ __device__ __forceinline__ void tap(int o, double scale, int in, int &i0, int &i
   w = __dsub_rn(f, (double)i0);
 }
 
-__device__ __forceinline__ int bilerp(double wx, double wy, int s00, int s01, int s10, int s11) {
-  const double ax = __dsub_rn(1.0, wx), ay = __dsub_rn(1.0, wy);
+__device__ __forceinline__ int bilerp2(double wx, double wy, double ax, double ay, int s00, int s01,
+                                       int s10, int s11) {
   const double top = __dadd_rn(__dmul_rn(ax, (double)s00), __dmul_rn(wx, (double)s01));
   const double bot = __dadd_rn(__dmul_rn(ax, (double)s10), __dmul_rn(wx, (double)s11));
   const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, top), __dmul_rn(wy, bot)), 0.5);
   const int iv = __double2int_rz(v);
   return iv > 255 ? 255 : iv;
+}
+
+// imgops.py:49-57 for one channel: weights' complements 1 - w as in the reference.
+__device__ __forceinline__ int bilerp(double wx, double wy, int s00, int s01, int s10, int s11) {
+  return bilerp2(wx, wy, __dsub_rn(1.0, wx), __dsub_rn(1.0, wy), s00, s01, s10, s11);
 }
 
 // imgops.py:231-240: (f32(v) * f32(1/255) - mean) / std, IEEE float32.
@@ -128,11 +133,22 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   int2 *cx = reinterpret_cast<int2 *>(cw + res);                              // [res] x taps
   PlaneSrc S;
   S.load(I, P.plane);
-  for (int e = threadIdx.x; e < nrows * iw; e += kPixThreads) {
-    const int r = e / iw, x = e - r * iw;
-    int cr, cg, cb;
-    S.rgb(I.ry + ys0 + r, I.rx + x, cr, cg, cb);
-    src[e] = (uint32_t)cr | ((uint32_t)cg << 8) | ((uint32_t)cb << 16);
+  // four source pixels per thread per round: their plane loads are
+  // independent, so they are in flight together
+  const int total = nrows * iw;
+  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kPixThreads) {
+    int rr[4], gg[4], bb[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int e = min(e0 + u * kPixThreads, total - 1);
+      const int r = e / iw, x = e - r * iw;
+      S.rgb(I.ry + ys0 + r, I.rx + x, rr[u], gg[u], bb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int e = e0 + u * kPixThreads;
+      if (e < total) src[e] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+    }
   }
   for (int ox = threadIdx.x; ox < res; ox += kPixThreads) {
     const int xs = I.flip ? res - 1 - ox : ox;  // hflip after resize
@@ -151,6 +167,7 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
     int y0, y1;
     double wy;
     tap(oy, sy, ih, y0, y1, wy);
+    const double ay = __dsub_rn(1.0, wy);
     const uint32_t *r0 = src + (y0 - ys0) * iw, *r1 = src + (y1 - ys0) * iw;
     uint8_t px[8][3];
 #pragma unroll
@@ -159,12 +176,13 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
       if (ox >= res) { px[i][0] = px[i][1] = px[i][2] = 0; continue; }
       const int2 xx = cx[ox];
       const double wx = cw[ox];
+      const double ax = __dsub_rn(1.0, wx);
       const uint32_t s00 = r0[xx.x], s01 = r0[xx.y], s10 = r1[xx.x], s11 = r1[xx.y];
 #pragma unroll
       for (int c = 0; c < 3; c++) {
         const int sh = 8 * c;
-        px[i][c] = (uint8_t)bilerp(wx, wy, (s00 >> sh) & 255, (s01 >> sh) & 255, (s10 >> sh) & 255,
-                                   (s11 >> sh) & 255);
+        px[i][c] = (uint8_t)bilerp2(wx, wy, ax, ay, (s00 >> sh) & 255, (s01 >> sh) & 255,
+                                    (s10 >> sh) & 255, (s11 >> sh) & 255);
       }
     }
     const bool full = ox0 + 8 <= res && (res & 7) == 0;
