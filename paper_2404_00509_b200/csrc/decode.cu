@@ -97,7 +97,7 @@ __host__ __device__ __forceinline__ uint32_t huff_entry(bool dc, int sym, int le
 
 // Geometry, stream location and tables handed from k_prep to k_entropy
 // (global, one per image; k_entropy keeps a copy in shared memory).
-struct __align__(16) DecodeHdr {
+struct __align__(16) DecodeHead {
   int32_t status, reason, offset;
   int32_t ns, bpm, gx, gy, row_stop, mx0, mx1, my0, my1, ncomp, ntab;
   uint32_t limit_blocks, clean_bits, clean_words, tab_index_word;
@@ -112,6 +112,9 @@ struct __align__(16) DecodeHdr {
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
   uint8_t zz[64];
   int32_t q[3][64];  // dequantisation tables, natural order
+};
+// + the Huffman tables (k_prep builds them in global memory directly)
+struct __align__(16) DecodeHdr : DecodeHead {
   HuffTab tab[kMaxTables];
 };
 
@@ -127,17 +130,16 @@ struct ParseState {
 };
 
 struct __align__(16) PrepSmem {
-  DecodeHdr h;
+  DecodeHead h;
   struct {
-    uint32_t T[4][256];  // slice-by-4 CRC tables
-    uint32_t part[kCrcMaxChunks];
+    uint32_t T[4][256];  // slice-by-4 CRC tables (chunk partials: dynamic smem)
   } crc;
   long long ph[8];
   ParseState ps;
   uint32_t K[8];
   uint32_t warp_tot[kNT / 32][4];
   uint16_t sub_pf[kMaxTables][kSubTabs];
-  int stop;
+  int stop, carry;
   long long t0;
 };
 
@@ -719,7 +721,7 @@ struct WriteOut {
 };
 
 // Crop-window coefficient pointer of block (mx, my, b), or null outside.
-__device__ __forceinline__ int16_t *window_block(const DecodeHdr &H, int16_t *coef, int mx, int my, int b) {
+__device__ __forceinline__ int16_t *window_block(const DecodeHead &H, int16_t *coef, int mx, int my, int b) {
   if (my < H.my0 || my > H.my1 || mx < H.mx0 || mx > H.mx1) return nullptr;
   const int s = H.blk_slot[b];
   const int c = H.slot_comp[s];
@@ -734,7 +736,7 @@ __device__ __forceinline__ int16_t *window_block(const DecodeHdr &H, int16_t *co
 // start from pred[] (decode_kernels.py:150-177).  The block reaching `limit`
 // records the bit position after it (p_final).
 template <bool SH>
-__device__ void write_run(const EntCtx &C, const DecodeHdr &H, int16_t *coef, uint32_t p0, int b0,
+__device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, uint32_t p0, int b0,
                           uint32_t A, uint32_t nb, int32_t pred[3], WriteOut &o, uint32_t *p_final) {
   Reader<SH> r;
   C.reader(r, p0);
@@ -814,7 +816,7 @@ __device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int
 // gets its table entry {global unit-list index of its DC entry, DC value} in
 // the first 8 bytes of its coefficient slot (k_idct gathers the block from
 // the list).
-__device__ void seg_table(const EntCtx &C, const DecodeHdr &H, int16_t *coef, const uint2 *bsl,
+__device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, const uint2 *bsl,
                           uint32_t ord, uint32_t lgbase, int b0, uint32_t A, uint32_t nb,
                           const int32_t base[3], int &range) {
   const uint32_t mcu = A / (uint32_t)C.bpm;
@@ -989,7 +991,7 @@ __device__ void idct_block_8lanes(bool valid, const int32_t *blk, const int32_t 
 
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void hdr_status(DecodeHdr &H, int st, int reason, int off) {
+__device__ __forceinline__ void hdr_status(DecodeHead &H, int st, int reason, int off) {
   if (H.status == 0) {
     H.status = st;
     H.reason = reason;
@@ -997,7 +999,7 @@ __device__ __forceinline__ void hdr_status(DecodeHdr &H, int st, int reason, int
   }
 }
 
-__device__ __forceinline__ int corrupt_offset(const DecodeHdr &H, uint32_t errp) {
+__device__ __forceinline__ int corrupt_offset(const DecodeHead &H, uint32_t errp) {
   // _check_consumed: scan.start + min(vpos, seglen); the reference's reader
   // keeps >= 25 bits buffered, so vpos = ceil((p + 25) / 8) at the failing unit.
   const uint32_t seglen = (uint32_t)(H.scan_end - H.scan_start);
@@ -1005,7 +1007,7 @@ __device__ __forceinline__ int corrupt_offset(const DecodeHdr &H, uint32_t errp)
   return H.scan_start + (int)min(vpos, seglen);
 }
 
-static_assert(sizeof(DecodeHdr) % 16 == 0 && offsetof(DecodeHdr, tab) % 16 == 0, "hdr copy");
+static_assert(sizeof(DecodeHead) % 16 == 0 && sizeof(HuffTab) % 16 == 0, "hdr copy");
 
 __device__ __forceinline__ DecodeHdr *hdr_of(const Scratch &s, int img) {
   return reinterpret_cast<DecodeHdr *>(s.hdr) + img;
@@ -1015,12 +1017,14 @@ __device__ __forceinline__ DecodeHdr *hdr_of(const Scratch &s, int img) {
 // k_prep: CRC, parse, destuff, tables, window zeroing (one CTA per image)
 // ===========================================================================
 template <bool SMEM>
-__global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
-  extern __shared__ __align__(16) uint8_t dyn[];
+__global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
+  extern __shared__ __align__(16) uint8_t dyn[];  // [payload (SMEM)][CRC chunk partials]
   __shared__ PrepSmem S;
-  DecodeHdr &H = S.h;
+  DecodeHead &H = S.h;
   const int img = blockIdx.x;
   const int tid = threadIdx.x;
+  DecodeHdr *G = hdr_of(P.s, img);  // tables are built here directly
+  uint32_t *crc_part = reinterpret_cast<uint32_t *>(dyn + P.prep_part_off);
   const essl_sample smp = P.samples[img];
   const uint8_t *g = P.blob + smp.offset;
   const int n = (int)smp.length;
@@ -1105,7 +1109,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
                 S.crc.T[0][c >> 24];
           }
         }
-        S.crc.part[ch] = c;
+        crc_part[ch] = c;
       }
       __syncthreads();
       const uint32_t *M = c_crc_mul;
@@ -1114,14 +1118,14 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         const int stride = 1 << j;
         const uint32_t *T = M + j * 1024;
         for (int i = tid * 2 * stride; i < C2; i += kNT * 2 * stride) {
-          const uint32_t a = S.crc.part[i];
+          const uint32_t a = crc_part[i];
           const uint32_t m = __ldg(T + (a & 0xFF)) ^ __ldg(T + 256 + ((a >> 8) & 0xFF)) ^
                              __ldg(T + 512 + ((a >> 16) & 0xFF)) ^ __ldg(T + 768 + (a >> 24));
-          S.crc.part[i] = m ^ S.crc.part[i + stride];
+          crc_part[i] = m ^ crc_part[i + stride];
         }
         __syncthreads();
       }
-      crc = S.crc.part[0] ^ 0xFFFFFFFFu;
+      crc = crc_part[0] ^ 0xFFFFFFFFu;
     }
     if (tid == 0 && crc != smp.crc32) hdr_status(H, ESSL_ST_CRC, 0, -1);
   }
@@ -1294,10 +1298,12 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   }
 
   if (tid == 0) S.ph[2] = clock64();
-  // ---- destuff (decode_kernels.py:27-61) into shared memory, then one
-  //      coalesced copy to the global clean region ---------------------------
+  // ---- destuff (decode_kernels.py:27-61), in place in shared memory (the
+  //      clean stream overwrites the scan bytes it came from: every kept byte
+  //      moves to a position <= its own), then one coalesced copy to the
+  //      global clean region ---------------------------------------------------
   uint8_t *gclean = P.s.clean + H.clean_off;
-  uint8_t *clean = SMEM ? dyn + n_pad : gclean;
+  uint8_t *clean = SMEM ? dyn + (PS.scan_start & ~15) : gclean;
   if (H.status == 0) {
     // Rounds of kNT x 16 bytes: thread t owns bytes [16t, 16t+16) of the
     // round (16-byte shared loads, conflict-free); a block scan per round
@@ -1324,6 +1330,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         i++;
       }
     }
+    if (tid == 0) S.carry = 0;
     __syncthreads();
     const int stop = S.stop;
     const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
@@ -1332,34 +1339,63 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
     for (int r0 = rbeg; r0 < stop; r0 += kRound) {
       const int g0 = r0 + tid * 16;
       const int a = max(g0, seg0), e = min(g0 + 16, stop);
+      // this thread's input bytes, the byte before and the byte after, in
+      // registers before any thread of the round writes
+      uint8_t in[16];
+      int prev = 0, next = 0;
+      if (g0 < stop) {
+        if (SMEM) {
+          const uint4 w = *reinterpret_cast<const uint4 *>(raw + g0);
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 16; q++) in[q] = (uint8_t)(ww[q >> 2] >> (8 * (q & 3)));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; q++) in[q] = raw[g0 + q];
+        }
+        prev = tid == 0 ? S.carry : (g0 > 0 ? raw[g0 - 1] : 0);  // (thread 0: saved by the last round)
+        next = raw[g0 + 16];
+      }
       uint32_t cnt[4] = {0, 0, 0, 0}, tot[4];
       bool fast = false;
-      if (SMEM && a == g0 && e == a + 16) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(raw + a);
-        fast = !has_ff(w.x) && !has_ff(w.y) && !has_ff(w.z) && !has_ff(w.w) &&
-               !(a > seg0 && raw[a - 1] == 0xFF);
+      if (a == g0 && e == a + 16) {
+        bool ff = false;
+#pragma unroll
+        for (int q = 0; q < 16; q++) ff |= in[q] == 0xFF;
+        fast = !ff && !(a > seg0 && prev == 0xFF);
       }
       if (fast) {
         cnt[0] = 16;
       } else {
-        for (int i = a; i < e; i++) {
-          const int v = raw[i];
-          const bool second = i > seg0 && raw[i - 1] == 0xFF;
-          const bool rst = v == 0xFF && is_rst(raw[i + 1]);
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          const int i = g0 + q;
+          if (i < a || i >= e) continue;
+          const int v = in[q];
+          const int pv = q == 0 ? prev : in[q == 0 ? 0 : q - 1];
+          const int nv = q == 15 ? next : in[q == 15 ? 15 : q + 1];
+          const bool second = i > seg0 && pv == 0xFF;
+          const bool rst = v == 0xFF && is_rst(nv);
           cnt[0] += (!second && !rst);
           cnt[1] += rst;
         }
       }
-      block_scan4(S.warp_tot, cnt, tot);
+      block_scan4(S.warp_tot, cnt, tot);  // (barriers: every read above is done)
+      if (tid == kNT - 1) S.carry = in[15];  // the round's last input byte
       uint32_t kept = kbase + cnt[0], nrst = rbase + cnt[1];
       if (fast) {
 #pragma unroll
-        for (int i = 0; i < 16; i++) clean[kept + i] = raw[a + i];
+        for (int q = 0; q < 16; q++) clean[kept + q] = in[q];
       } else {
-        for (int i = a; i < e; i++) {
-          const int v = raw[i];
-          const bool second = i > seg0 && raw[i - 1] == 0xFF;
-          const bool rst = v == 0xFF && is_rst(raw[i + 1]);
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          const int i = g0 + q;
+          if (i < a || i >= e) continue;
+          const int v = in[q];
+          const int pv = q == 0 ? prev : in[q == 0 ? 0 : q - 1];
+          const int nv = q == 15 ? next : in[q == 15 ? 15 : q + 1];
+          const bool second = i > seg0 && pv == 0xFF;
+          const bool rst = v == 0xFF && is_rst(nv);
           if (rst) {
             if ((int)nrst < max_r) rst_tab[nrst] = kept;
             nrst++;
@@ -1370,6 +1406,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
       }
       kbase += tot[0];
       rbase += tot[1];
+      __syncthreads();  // writes of this round before the next round's reads
     }
     const uint32_t tk = kbase, tr = rbase;
     __syncthreads();
@@ -1424,7 +1461,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
         if (ti < 0) {
           ti = ntab++;
           tab_pos[ti] = pos;
-          HuffTab &T = H.tab[ti];
+          HuffTab &T = G->tab[ti];
           int code = 0, vi = 0;
           T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
           for (int L = 1; L <= 16; L++) {
@@ -1466,13 +1503,13 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   if (H.status == 0) {
     const int ntab = H.ntab;
     for (int e = tid; e < ntab * 256; e += kNT) {
-      HuffTab &T = H.tab[e >> 8];
+      HuffTab &T = G->tab[e >> 8];
       const int v = e & 255;
       T.vals[v] = v < T.nvals ? (uint8_t)raw[T.dht_pos + 16 + v] : 0;
     }
     __syncthreads();
     for (int t = 0; t < ntab; t++) {
-      HuffTab &T = H.tab[t];
+      HuffTab &T = G->tab[t];
       int lim[17], first[17], vptr[17];
 #pragma unroll
       for (int L = 1; L <= 16; L++) {
@@ -1521,8 +1558,7 @@ __global__ void __launch_bounds__(kNT, 2) k_prep(DecodeParams P) {
   __syncthreads();
   // ---- hand over: header (+ used tables) to global ---------------------------
   {
-    DecodeHdr *G = hdr_of(P.s, img);
-    const int words = (int)((offsetof(DecodeHdr, tab) + (H.status == 0 ? H.ntab : 0) * sizeof(HuffTab)) / 16);
+    const int words = (int)(sizeof(DecodeHead) / 16);  // the tables are already in G
     const int4 *src = reinterpret_cast<const int4 *>(&H);
     int4 *dst = reinterpret_cast<int4 *>(G);
     for (int i = tid; i < words; i += kNT) dst[i] = src[i];
@@ -1561,7 +1597,7 @@ __device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int o
 
 // Zero the image's crop-window coefficients (the re-decoding paths scatter
 // nonzeros into it).  Called by every thread of the CTA.
-__device__ void zero_window(const DecodeHdr &H, int16_t *coef, int lane) {
+__device__ void zero_window(const DecodeHead &H, int16_t *coef, int lane) {
   uint64_t total = 0;
   for (int c = 0; c < 3; c++) total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
   int4 *z = reinterpret_cast<int4 *>(coef + H.coef_base);
@@ -1769,7 +1805,7 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   __syncthreads();
   PHASE(0);
   {
-    const int head = (int)(offsetof(DecodeHdr, tab) / 16);
+    const int head = (int)(sizeof(DecodeHead) / 16);
     const int4 *src = reinterpret_cast<const int4 *>(G);
     int4 *dst = reinterpret_cast<int4 *>(&H);
     for (int i = lane; i < head; i += kLanes) dst[i] = src[i];
@@ -2000,16 +2036,27 @@ constexpr int kMaxDynSmem = 160 * 1024;
 size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
 size_t ckpt_bytes() { return sizeof(Ckpt); }
 
-void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len) {
-  if (p.n <= 0) return;
-  const int dyn = 2 * ((max_len + 15) / 16 * 16 + 16) + 96;
+void launch_prep(const DecodeParams &p0, cudaStream_t st, int max_len) {
+  if (p0.n <= 0) return;
+  // dynamic shared memory: [payload, destuffed in place + 0xFF padding][CRC partials]
+  const int payload = (max_len + 15) / 16 * 16 + 128;
+  int c2 = 1;
+  while (c2 < (max_len + kCrcChunk - 1) / kCrcChunk && c2 < kCrcMaxChunks) c2 <<= 1;
+  const int part = 4 * c2;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+    cudaFuncSetAttribute(k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
     attr = true;
   }
-  if (dyn <= kMaxDynSmem) k_prep<true><<<p.n, kNT, dyn, st>>>(p);
-  else k_prep<false><<<p.n, kNT, 0, st>>>(p);
+  DecodeParams p = p0;
+  if (payload + part <= kMaxDynSmem) {
+    p.prep_part_off = payload;
+    k_prep<true><<<p.n, kNT, payload + part, st>>>(p);
+  } else {
+    p.prep_part_off = 0;
+    k_prep<false><<<p.n, kNT, part, st>>>(p);
+  }
 }
 
 void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len) {

@@ -76,7 +76,8 @@ struct DecodeParams {
   int seq_bits;      // minimum subsequence length per lane (bits)
   int ck_bits;       // minimum checkpoint spacing (bits)
   int warm_bits;     // each lane (but lane 0) starts this far before its subsequence
-  int stage_bytes;   // k_entropy dynamic shared memory for the clean stream (0: global)
+  int stage_bytes;   // k_entropy read rings (0: plain global reads)
+  int prep_part_off; // k_prep: byte offset of the CRC partials in dynamic smem
   essl_result *results;  // optional
 };
 
