@@ -78,7 +78,8 @@ extern "C" {
 #define ESSL_K_PREP 6    /* k_prep: CRC, parse, destuff, tables */
 #define ESSL_K_ENTROPY 7 /* k_entropy: Huffman decode */
 #define ESSL_K_IDCT 8    /* k_idct: dequant + IDCT */
-#define ESSL_K_COUNT 9
+#define ESSL_K_STAGE 9   /* k_host_gather: pinned-container payload gather */
+#define ESSL_K_COUNT 10
 
 typedef struct essl_ctx essl_ctx;
 

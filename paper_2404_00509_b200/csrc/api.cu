@@ -484,8 +484,10 @@ int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint
   }
   if (n > 0) {
     CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
-    essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], st);
-    c->launches += 1;
+    {
+      Prof pr(c, ESSL_K_STAGE, st);
+      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], st);
+    }
   }
   CK(cudaEventRecord(c->ev_stage[slot], st));
   c->stage_used[slot] = true;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--pool", type=int, default=4096)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--host", action="store_true", help="pinned-container bus gather (resident=False)")
     args = ap.parse_args()
     import ctypes
 
@@ -35,7 +36,8 @@ def main():
     path = d / "pool.essl"
     E.build_synthetic(path, args.pool, 256, 95, seed=3)
     cfg = E.LoaderConfig(data=str(path), batch_size=256, res=224, out_dtype="bfloat16",
-                         mask_ratio=0.75, resident=True, streams=args.streams, prefetch=args.streams,
+                         mask_ratio=0.75, resident=not args.host, streams=args.streams,
+                         prefetch=args.streams,
                          reuse_outputs=True)
     loader = E.Loader(cfg)
     perm = E.epoch_permutation(0, 0, len(loader.handle))
