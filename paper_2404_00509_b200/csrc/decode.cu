@@ -1943,17 +1943,38 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
   uint2 t = make_uint2(0, 0);
   if (valid) t = *reinterpret_cast<const uint2 *>(cf);
   if (valid && j == 0) blk[0] = (int32_t)t.y;
+  // The block's AC units follow its DC entry up to the next DC-flagged
+  // entry.  Each round the group reads 32 consecutive entries as eight
+  // 16-byte loads (lists are 16-byte aligned per lane; most blocks end in the
+  // first round) and stops at the first DC flag.
   bool done = !valid;
   const int gsh = threadIdx.x & 24;  // this group's bit offset in a warp ballot
-  uint32_t i = t.x + 1 + j;
+  const uint32_t i0 = t.x + 1;       // first AC entry
+  uint32_t base = i0 & ~3u;          // aligned chunk covering i0
 #pragma unroll 1
   while (__any_sync(0xFFFFFFFFu, !done)) {
-    const uint32_t e = done ? 1u : __ldg(sc.list + i);
-    const uint32_t grp = (__ballot_sync(0xFFFFFFFFu, !done && (e & 1)) >> gsh) & 0xFFu;
-    const int first = grp ? __ffs(grp) - 1 : 8;
-    if (!done && j < first) blk[(e >> 1) & 63] = (int32_t)e >> 16;
-    done = done || first < 8;
-    i += 8;
+    uint4 q = make_uint4(1u, 1u, 1u, 1u);
+    if (!done) q = __ldg(reinterpret_cast<const uint4 *>(sc.list + base) + j);
+    const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
+    // DC flags of this lane's four entries at or after i0
+    uint32_t m = 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t idx = base + 4 * j + u;
+      if (!done && idx >= i0 && (e4[u] & 1)) m |= 1u << u;
+    }
+    // first DC-flagged entry of the round, over the group (lanes in order)
+    const uint32_t any = (__ballot_sync(0xFFFFFFFFu, m != 0) >> gsh) & 0xFFu;
+    const int fl = any ? __ffs(any) - 1 : 8;                      // first lane with a flag
+    const int fu = __shfl_sync(0xFFFFFFFFu, m ? __ffs(m) - 1 : 4, (threadIdx.x & ~7) + (fl & 7));
+    const uint32_t stop = any ? base + 4 * fl + fu : 0xFFFFFFFFu;  // index of the next DC entry
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const uint32_t idx = base + 4 * j + u;
+      if (!done && idx >= i0 && idx < stop) blk[(e4[u] >> 1) & 63] = (int32_t)e4[u] >> 16;
+    }
+    done = done || any != 0;
+    base += 32;
   }
   __syncwarp();
 }
