@@ -273,7 +273,7 @@ def run_gpu(args, wl):
     # ---- warm-up: the same pipelined issue pattern as the timed loop, so the
     # caching allocator and every stream's context reach steady state
     pend = []
-    ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2  # pipeline.py _HostRing (reused outputs)
+    ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2  # pipeline.py _HostRing slots
     for i in range(max(args.warmup, args.streams * (ring_depth + 1))):
         e, idx = batch_indices(i)
         pend.append(loader.enqueue(e, idx))

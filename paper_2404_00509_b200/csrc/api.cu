@@ -264,7 +264,8 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   c->s.list_cap = (uint64_t)max_batch *
                   (4ull * max_payload + (uint64_t)essl::kEntropyLanes *
                                             (2ull * ((essl::kMaxWarmBits + essl::kContinuationBits) / 4 + 68) + 32) + 8);
-  CKC(cudaMalloc(&c->s.list, c->s.list_cap * sizeof(uint32_t)));
+  // (+ 4 words per entropy lane past the pool: overflow sinks)
+  CKC(cudaMalloc(&c->s.list, (c->s.list_cap + 4 * essl::kEntropyLanes) * sizeof(uint32_t)));
   CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
   for (int r = 0; r < kDescRing; r++) {
     CKC(cudaMallocHost(&c->h_desc[r], sizeof(essl_sample) * max_batch));

@@ -346,7 +346,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 
 // Bit reader over the clean stream (big-endian words; k_prep byte-swaps).
 // SH: each lane reads through its own 64-byte ring in shared memory, filled
-// by cp.async four 16-byte chunks ahead of consumption -- refills are short
+// by cp.async one pair of 16-byte chunks ahead of consumption -- refills are short
 // LDS reads with no global latency on the decode chain, and the footprint is
 // 64 bytes per lane whatever the payload size.  !SH: plain global loads
 // (validation path).  Words past the data read as 0xFF padding
@@ -366,16 +366,21 @@ struct Reader {
     if (SH) return lds_u32(rs + ((i & 15) << 2));
     return __ldg(w + min(i, wmax));
   }
-  // ring: issue chunk c (4 words) into its slot; one commit group per chunk
-  __device__ __forceinline__ void issue(uint32_t c, bool pred) const {
+  // ring: 4 chunks of 16 bytes, fetched in pairs (c, c+1), c even, one
+  // commit group per pair.  Entering an even chunk c frees the pair (c-2,
+  // c-1): fetch (c+2, c+3) into it, then wait until at most that newest pair
+  // is pending -- the pair (c, c+1), fetched one pair (~46 units) ago, is done.
+  __device__ __forceinline__ void issue_pair(uint32_t c, bool pred) const {
     const uint32_t dst = rs + ((c & 3) << 4);
-    const uint32_t *src = w + 4 * (size_t)min(c, cpad);
+    const uint32_t *s0 = w + 4 * (size_t)min(c, cpad);
+    const uint32_t *s1 = w + 4 * (size_t)min(c + 1, cpad);
     asm volatile(
         "{ .reg .pred q; setp.ne.u32 q, %0, 0;\n"
         "  @q cp.async.cg.shared.global [%1], [%2], 16;\n"
-        "  @q cp.async.commit_group;\n"
-        "  @q cp.async.wait_group 3; }" ::"r"((uint32_t)pred),
-        "r"(dst), "l"(src)
+        "  @q cp.async.cg.shared.global [%3], [%4], 16;\n"
+        "  cp.async.commit_group;\n"
+        "  cp.async.wait_group 1; }" ::"r"((uint32_t)pred),
+        "r"(dst), "l"(s0), "r"(dst + 16), "l"(s1)
         : "memory");
   }
   __device__ __forceinline__ void init(uint32_t pos) {
@@ -384,22 +389,22 @@ struct Reader {
     if (SH) {
       // drain this lane's copies still in flight: they target the same slots
       asm volatile("cp.async.wait_group 0;" ::: "memory");
-      const uint32_t c = i >> 2;
+      const uint32_t c = (i >> 2) & ~1u;  // the pair holding word i
 #pragma unroll
       for (uint32_t q = 0; q < 4; q++) {
         const uint32_t dst = rs + (((c + q) & 3) << 4);
         const uint32_t *src = w + 4 * (size_t)min(c + q, cpad);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n cp.async.commit_group;" ::"r"(dst),
-                     "l"(src)
-                     : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
       }
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
     }
     buf = (((uint64_t)ld(i) << 32) | ld(i + 1)) << off;
     n = 64 - off;
     wi = i + 2;
     p = pos;
-    if (SH && (wi & 3) < 2) issue((wi >> 2) + 3, true);  // consumed into a new chunk
+    // the ring holds chunks c..c+3 with c = 2*(i/8); if wi already entered
+    // the next pair, its crossing fetch (c+4, c+5) is due now
+    if (SH && (wi & ~7u) != (i & ~7u)) issue_pair((wi >> 2) + 2, true);
   }
   // keeps >= 33 bits buffered: one unit (code + magnitude) is <= 31 bits
   __device__ __forceinline__ void refill() {
@@ -411,8 +416,8 @@ struct Reader {
       buf |= rf ? (uint64_t)wv << (32 - n) : 0ull;
       n += rf ? 32 : 0;
       wi += rf ? 1u : 0u;
-      // entering a new chunk frees the oldest slot: fetch chunk + 3 into it
-      issue((wi >> 2) + 3, rf && (wi & 3) == 0);
+      const bool cross = rf && (wi & 7) == 0;  // entered an even chunk
+      if (__any_sync(__activemask(), cross)) issue_pair((wi >> 2) + 2, cross);
     } else if (n <= 32) {
       buf |= (uint64_t)ld(wi) << (32 - n);
       n += 32;
@@ -1581,7 +1586,6 @@ struct __align__(16) EntSmem {
   int coef_range, red;
   unsigned long long lbase;
   int32_t dcsum[kLanes * 3];
-  uint32_t sink[kLanes * 2];
   int fmt;
   __align__(16) uint32_t ring[kLanes][16];
   long long t_ph[8];
@@ -1693,9 +1697,9 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
     __syncthreads();
     const bool lists_ok = S.lbase != ~0ull;
     const unsigned long long lreg = lists_ok ? S.lbase + (unsigned long long)lane * stride : 0ull;
-    uint32_t *list = lists_ok ? P.s.list + lreg : S.sink + 2 * lane;
-    uint2 *bsl = lists_ok ? reinterpret_cast<uint2 *>(P.s.list + lreg + cap + 8)
-                          : reinterpret_cast<uint2 *>(S.sink) + lane;
+    uint32_t *sink = P.s.list + P.s.list_cap + 4 * lane;  // 4 words per lane past the pool
+    uint32_t *list = lists_ok ? P.s.list + lreg : sink;
+    uint2 *bsl = reinterpret_cast<uint2 *>(lists_ok ? P.s.list + lreg + cap + 8 : sink + 2);
     const uint32_t lcap = lists_ok ? cap : 0u, lbcap = lists_ok ? bcap : 0u;
     if (lane < nseq) {
       const uint32_t sbeg = lane * slen;

@@ -128,9 +128,10 @@ class LoaderConfig:
     resident: bool = True
     prefetch: int = 2
     streams: int = 2
-    # Reuse a ring of output buffers (views valid until `prefetch + streams`
-    # later batches are issued, the reference bindings' "valid until the next
-    # step" contract) instead of allocating every batch.
+    # Reuse a ring of output buffers (a batch's views stay valid while fewer
+    # than `prefetch + 2` later batches have been issued -- the reference
+    # bindings' "valid until the next step" contract) instead of
+    # allocating every batch.
     reuse_outputs: bool = False
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
@@ -257,6 +258,7 @@ class Loader:
         self._pinned_base = self.handle.pinned_host() if not config.resident else 0
         self._slots = [0] * len(self._engines)
         self._out_ring: dict = {}
+        self._out_next = [0] * len(self._engines)
         self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
 
     @classmethod
@@ -340,10 +342,17 @@ class Loader:
         if self.mask_spec is not None:
             T, k = self.mask_spec.tokens, self.mask_spec.masked_count
 
+        # reused outputs: R slots per stream, R * streams > batches in flight
+        # beyond the one the consumer holds (prefetch + 1)
+        n_st = len(self._engines)
+        R = max(2, -(-(max(cfg.prefetch, n_st) + 2) // n_st))
+        oslot = self._out_next[j] % R
+        self._out_next[j] += 1
+
         def out(name, shape, dtype):
             if not cfg.reuse_outputs:
                 return torch.empty(shape, dtype=dtype, device=dev)
-            key = (j, slot, name)
+            key = (j, oslot, name)
             t = self._out_ring.get(key)
             if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
                 t = torch.empty(shape, dtype=dtype, device=dev)
