@@ -82,6 +82,13 @@ struct __align__(16) HuffTab {
   int dht_pos, nvals, is_dc, nsub;
 };
 
+// The part of a HuffTab the entropy decoder keeps in shared memory (the
+// canonical arrays stay in global memory: only hostile tables reach them).
+struct __align__(16) HuffFast {
+  uint16_t fast[1 << kFastBits];
+  uint16_t sub[kSubTabs << kSubBits];
+};
+
 __host__ __device__ __forceinline__ uint32_t huff_entry(bool dc, int sym, int len) {
   int size, kinc;
   if (dc) {
@@ -437,9 +444,10 @@ struct Reader {
 // Long codes (rare: a divergent branch): second-level table, or the canonical
 // maxcode walk for hostile tables with more long-code prefixes than
 // sub-tables (same symbols as codec.py:272-295).
-__device__ __forceinline__ uint32_t lookup_long(const HuffTab &T, uint32_t e, uint32_t hi) {
+__device__ __forceinline__ uint32_t lookup_long(const HuffFast &F, const HuffTab &T, uint32_t e,
+                                                uint32_t hi) {
   const uint32_t si = e >> 5, code16 = hi >> 16;
-  if (si <= (uint32_t)kSubTabs) return T.sub[((si - 1) << kSubBits) | (code16 & ((1u << kSubBits) - 1))];
+  if (si <= (uint32_t)kSubTabs) return F.sub[((si - 1) << kSubBits) | (code16 & ((1u << kSubBits) - 1))];
 #pragma unroll 1
   for (int L = kFastBits + 1; L <= 16; L++) {
     const int c = (int)(code16 >> (16 - L));
@@ -461,7 +469,8 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 
 // Per-image decode context held in registers by every lane.
 struct EntCtx {
-  const uint8_t *tabs;  // HuffTab array (shared memory)
+  const uint8_t *tabs;  // HuffFast array (shared memory)
+  const HuffTab *gtab;  // the full tables (global memory)
   uint32_t tabs_s;      // the same, as a shared-window address
   uint32_t zz_s;        // zig-zag -> natural table (shared-window address)
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
@@ -482,7 +491,9 @@ struct EntCtx {
   }
   __device__ __forceinline__ uint32_t zz(int i) const { return lds_u8(zz_s + (uint32_t)i); }
   __device__ __forceinline__ uint32_t lookup_long(int k, int b, uint32_t e, uint32_t hi) const {
-    return essl::lookup_long(*reinterpret_cast<const HuffTab *>(tabs + tab_off(k, b)), e, hi);
+    const uint32_t off = tab_off(k, b);
+    return essl::lookup_long(*reinterpret_cast<const HuffFast *>(tabs + off),
+                             gtab[off / (uint32_t)sizeof(HuffFast)], e, hi);
   }
   __device__ __forceinline__ uint32_t lookup(int k, int b, uint32_t hi) const {
     uint32_t e = lookup_fast(k, b, hi);
@@ -543,7 +554,6 @@ struct LaneRec {
   uint32_t cj, cm, cn, cp, ek, eb;
   // resolution: the lane's segment of the exact path
   uint32_t w_ord, w_p, w_b, w_A, w_nb;
-  uint32_t dbg_units, dbg_guess;
 };
 
 // Phase 1 (CONT=false): decode [p0, send) from the guess (k=0, b=0), storing
@@ -558,7 +568,7 @@ struct LaneRec {
 template <bool CONT, bool SH>
 __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t send,
                          uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, Ckpt *ck_all,
-                         LaneRec *Ls, LaneRec &R) {
+                         LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
   Reader<SH> r;
   int k, b;
   uint32_t nblk, nl, nbs, nck = 0, ck_next = p0;
@@ -679,8 +689,9 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.nbs = nbs;
     if (ovf) R.ovf = 1;
   } else {
-    R.dbg_units = dbg_units;
-    R.dbg_guess = dbg_guess;
+    atomicAdd(dbg + 0, dbg_units);
+    atomicAdd(dbg + 1, dbg_guess);
+    atomicMax(dbg + 2, dbg_units);
     R.err = st == 1;
     R.xp = r.p;
     R.xk = k;
@@ -1579,11 +1590,13 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
 // k_entropy: entropy decode, one warp per image
 // ===========================================================================
 struct __align__(16) EntSmem {
-  DecodeHdr h;
+  DecodeHead h;
+  HuffFast tab[kMaxTables];
   LaneRec lane[kLanes];
   int status, reason, offset;
   uint32_t p_final;
   int coef_range, red;
+  unsigned int dbg_units, dbg_guess, dbg_umax;
   unsigned long long lbase;
   int32_t dcsum[kLanes * 3];
   int fmt;
@@ -1616,7 +1629,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
                                              int img, int lane, uint32_t &dbg_nseq,
                                              uint32_t &dbg_cont) {
   EntCtx C = C0;
-  DecodeHdr &H = S.h;
+  DecodeHead &H = S.h;
   LaneRec &R = S.lane[lane];
   int16_t *coef = P.s.coef;
   const uint32_t *rst_tab = C.words + H.rst_off;
@@ -1705,12 +1718,12 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
       const uint32_t sbeg = lane * slen;
       const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
       const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
-      run_path<false, SH>(C, lane, nseq, p0, send, list, lcap, bsl, lbcap, ck_all, S.lane, R);
+      run_path<false, SH>(C, lane, nseq, p0, send, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
     }
     __syncthreads();
     PHASE(2);
     const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
-    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R);
+    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
     dbg_nseq = (uint32_t)nseq;
     if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
     __syncthreads();
@@ -1803,7 +1816,7 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   const int lane = threadIdx.x;
   ImgInfo *info = P.s.info + img;
   const DecodeHdr *G = hdr_of(P.s, img);
-  DecodeHdr &H = S.h;
+  DecodeHead &H = S.h;
 #define PHASE(i) do { if (lane == 0) S.t_ph[i] = clock64(); } while (0)
   if (lane < 8) S.t_ph[lane] = 0;
   __syncthreads();
@@ -1815,17 +1828,19 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
     for (int i = lane; i < head; i += kLanes) dst[i] = src[i];
   }
   __syncthreads();
-  if (H.status == 0) {
-    const int words = (int)(H.ntab * sizeof(HuffTab) / 16);
-    const int4 *src = reinterpret_cast<const int4 *>(G->tab);
-    int4 *dst = reinterpret_cast<int4 *>(H.tab);
-    for (int i = lane; i < words; i += kLanes) dst[i] = src[i];
+  if (H.status == 0) {  // the fast tables of the used Huffman tables
+    const int per = (int)(sizeof(HuffFast) / 16);
+    for (int i = lane; i < H.ntab * per; i += kLanes) {
+      const int t = i / per, w = i % per;
+      reinterpret_cast<int4 *>(&S.tab[t])[w] = reinterpret_cast<const int4 *>(&G->tab[t])[w];
+    }
   }
   if (lane == 0) {
     S.status = H.status; S.reason = H.reason; S.offset = H.offset;
     S.coef_range = 0;
     S.p_final = kNoEnd;
     S.fmt = 0;
+    S.dbg_units = 0; S.dbg_guess = 0; S.dbg_umax = 0;
   }
   LaneRec &R = S.lane[lane];
   R.w_nb = 0;
@@ -1834,12 +1849,13 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   PHASE(1);
 
   EntCtx C;
-  C.tabs = reinterpret_cast<const uint8_t *>(H.tab);
-  C.tabs_s = (uint32_t)__cvta_generic_to_shared(H.tab);
+  C.tabs = reinterpret_cast<const uint8_t *>(S.tab);
+  C.gtab = G->tab;
+  C.tabs_s = (uint32_t)__cvta_generic_to_shared(S.tab);
   C.zz_s = (uint32_t)__cvta_generic_to_shared(H.zz);
   {
     const uint32_t w = H.tab_index_word;
-    const uint32_t sz = (uint32_t)sizeof(HuffTab);
+    const uint32_t sz = (uint32_t)sizeof(HuffFast);
     C.d0 = (w & 15) * sz; C.d1 = ((w >> 4) & 15) * sz; C.d2 = ((w >> 8) & 15) * sz;
     C.a0 = ((w >> 12) & 15) * sz; C.a1 = ((w >> 16) & 15) * sz; C.a2 = ((w >> 20) & 15) * sz;
   }
@@ -1897,12 +1913,7 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
     for (int i = 0; i < 6; i++) info->dbg[2 + i] = S.t_ph[i];
     info->dbg[10] = dbg_nseq;
     info->dbg[11] = dbg_cont;
-    uint32_t su = 0, sg = 0, mu = 0;
-    for (int t = 0; t < (int)dbg_nseq; t++) {
-      su += S.lane[t].dbg_units;
-      sg += S.lane[t].dbg_guess;
-      mu = max(mu, S.lane[t].dbg_units);
-    }
+    const uint32_t su = S.dbg_units, sg = S.dbg_guess, mu = S.dbg_umax;
     info->dbg[8] = su | ((long long)sg << 32);
     info->dbg[9] = mu | ((long long)(S.status == 0 && S.fmt == 0) << 32);
     if (P.results) {
