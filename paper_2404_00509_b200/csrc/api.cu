@@ -18,6 +18,7 @@
 
 namespace essl {
 void init_crc_tables();
+void init_norm_luts();
 }
 
 namespace {
@@ -282,7 +283,11 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   }
 #undef CKC
   static std::once_flag once;
-  std::call_once(once, [] { essl::init_crc_tables(); });
+  std::call_once(once, [] {
+    essl::init_crc_tables();
+    essl::init_norm_luts();
+    cudaDeviceSynchronize();  // tables ready before any stream's first batch
+  });
   *out = c;
   return ESSL_OK;
 }
@@ -523,7 +528,7 @@ int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
     for (int i = 0; i < n; i++)
       words = std::max(words, essl::band_source_rows(samples[i].h, res) * std::max(samples[i].w, 1));
     pp.src_words = (words + 3) / 4 * 4;
-    if ((size_t)pp.src_words * 4 + (size_t)res * 16 > 200 * 1024)
+    if ((size_t)pp.src_words * 4 > 200 * 1024)
       return fail(ESSL_E_CAPACITY, "crop too large for the resize kernel's shared staging");
   }
   if (out_kind != ESSL_OUT_NONE || out_u8) {

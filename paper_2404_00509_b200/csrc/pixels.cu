@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "essl_common.cuh"
 
@@ -104,24 +105,44 @@ __device__ __forceinline__ float norm_value(int c, int v) {
 // grid: (ceil(res / kBandRows), n); dynamic smem: P.band_src_rows x P.max_w
 // words + the column table.
 constexpr int kBandRows = 16;
+constexpr int kResizeMaxDyn = 200 * 1024;
+
+// The exact fp32 normalize value of every (channel, uint8) and its bf16 RNE,
+// computed once on the device (init_norm_luts) with the same IEEE ops.
+__device__ float g_norm_lut[768];
+__device__ __nv_bfloat16 g_norm_lutb[768];
+
+__global__ void k_init_norm_luts() {
+  const int i = threadIdx.x;
+  const float f = norm_value(i >> 8, i & 255);
+  g_norm_lut[i] = f;
+  g_norm_lutb[i] = __float2bfloat16_rn(f);
+}
+
+void init_norm_luts() { k_init_norm_luts<<<1, 768>>>(); }
 
 __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ float lut[3][256];
   __shared__ __nv_bfloat16 lutb[3][256];
+  __shared__ double s_scale[2];
   const int img = blockIdx.y;
   const ImgInfo &I = P.info[img];
   if (I.status != 0) return;
-  for (int i = threadIdx.x; i < 768; i += kPixThreads) {
-    const float f = norm_value(i >> 8, i & 255);
-    lut[i >> 8][i & 255] = f;
-    lutb[i >> 8][i & 255] = __float2bfloat16_rn(f);
-  }
   const int res = P.res;
+  const int ih = I.rh, iw = I.rw;
+  if (P.out_kind == ESSL_OUT_F32_NCHW)
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
+  else
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
+  if (threadIdx.x == 0) {  // imgops.py:35-36 scale factors, once per CTA
+    s_scale[0] = __ddiv_rn((double)ih, (double)res);
+    s_scale[1] = __ddiv_rn((double)iw, (double)res);
+  }
+  __syncthreads();
   const int ob0 = blockIdx.x * kBandRows;
   const int ob1 = min(ob0 + kBandRows, res);
-  const int ih = I.rh, iw = I.rw;
-  const double sy = __ddiv_rn((double)ih, (double)res), sx = __ddiv_rn((double)iw, (double)res);
+  const double sy = s_scale[0], sx = s_scale[1];
   // source rows of the band (taps are monotone in the output row)
   int ys0, ys1, dummy;
   double wdum;
@@ -129,8 +150,6 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   tap(ob1 - 1, sy, ih, dummy, ys1, wdum);
   const int nrows = ys1 - ys0 + 1;
   uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
-  double *cw = reinterpret_cast<double *>(dyn + (size_t)P.src_words * 4);   // [res] x weights
-  int2 *cx = reinterpret_cast<int2 *>(cw + res);                              // [res] x taps
   PlaneSrc S;
   S.load(I, P.plane);
   // four source pixels per thread per round: their plane loads are
@@ -150,90 +169,90 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
       if (e < total) src[e] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
     }
   }
-  for (int ox = threadIdx.x; ox < res; ox += kPixThreads) {
+  // row taps of the band (imgops.py:37-41), shared by every column
+  __shared__ int2 ry[kBandRows];
+  __shared__ double rw[kBandRows];
+  if (threadIdx.x < ob1 - ob0) {
+    int y0, y1;
+    double wy;
+    tap(ob0 + threadIdx.x, sy, ih, y0, y1, wy);
+    ry[threadIdx.x] = make_int2(y0 - ys0, y1 - ys0);
+    rw[threadIdx.x] = wy;
+  }
+  __syncthreads();
+  // Separable evaluation, exactly the reference's expressions: per output
+  // column the horizontal lerps top = (1-wx)*s(y,x0) + wx*s(y,x1) of the
+  // source rows y0/y1 (imgops.py:49-52) are kept in registers and reused
+  // while consecutive output rows share them; per output row only the
+  // vertical (1-wy)*top + wy*bot + 0.5 (imgops.py:53-56).  Small outputs
+  // split the band's rows over groups of threads.
+  const int ng = res >= kPixThreads ? 1 : kPixThreads / res;
+  const int g = ng > 1 ? threadIdx.x / res : 0;
+  const int cstart = ng > 1 ? threadIdx.x % res : threadIdx.x;
+  const int cstep = ng > 1 ? res : kPixThreads;
+  const int rpg = (ob1 - ob0 + ng - 1) / ng;
+  const int rb = g * rpg, re = min(ob1 - ob0, rb + rpg);
+  const int64_t plane_sz = (int64_t)res * res;
+  const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
+  if (g >= ng) return;
+  for (int ox = cstart; ox < res; ox += cstep) {
     const int xs = I.flip ? res - 1 - ox : ox;  // hflip after resize
     int x0, x1;
     double wx;
     tap(xs, sx, iw, x0, x1, wx);
-    cw[ox] = wx;
-    cx[ox] = make_int2(x0, x1);
-  }
-  __syncthreads();
-  const int groups = (res + 7) >> 3;
-  const int64_t plane_sz = (int64_t)res * res;
-  const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
-  for (int t = threadIdx.x; t < (ob1 - ob0) * groups; t += kPixThreads) {
-    const int oy = ob0 + t / groups, ox0 = (t % groups) * 8;
-    int y0, y1;
-    double wy;
-    tap(oy, sy, ih, y0, y1, wy);
-    const double ay = __dsub_rn(1.0, wy);
-    const uint32_t *r0 = src + (y0 - ys0) * iw, *r1 = src + (y1 - ys0) * iw;
-    uint8_t px[8][3];
+    const double ax = __dsub_rn(1.0, wx);
+    int cy0 = -1, cy1 = -1;
+    double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
+    auto hrow = [&](int y, double h[3]) {
+      const uint32_t a0 = src[y * iw + x0], a1 = src[y * iw + x1];
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-      const int ox = ox0 + i;
-      if (ox >= res) { px[i][0] = px[i][1] = px[i][2] = 0; continue; }
-      const int2 xx = cx[ox];
-      const double wx = cw[ox];
-      const double ax = __dsub_rn(1.0, wx);
-      const uint32_t s00 = r0[xx.x], s01 = r0[xx.y], s10 = r1[xx.x], s11 = r1[xx.y];
+      for (int c = 0; c < 3; c++)
+        h[c] = __dadd_rn(__dmul_rn(ax, (double)((a0 >> (8 * c)) & 255)),
+                         __dmul_rn(wx, (double)((a1 >> (8 * c)) & 255)));
+    };
+    for (int r = rb; r < re; r++) {
+      const int2 yy = ry[r];
+      const double wy = rw[r], ay = __dsub_rn(1.0, wy);
+      if (yy.x != cy0) {  // (uniform across the CTA's columns: no divergence)
+        if (yy.x == cy1) {
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        const int sh = 8 * c;
-        px[i][c] = (uint8_t)bilerp2(wx, wy, ax, ay, (s00 >> sh) & 255, (s01 >> sh) & 255,
-                                    (s10 >> sh) & 255, (s11 >> sh) & 255);
-      }
-    }
-    const bool full = ox0 + 8 <= res && (res & 7) == 0;
-    if (P.out_kind == ESSL_OUT_BF16_NCHW) {
-      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + (int64_t)oy * res + ox0;
-#pragma unroll
-      for (int c = 0; c < 3; c++) {
-        if (full) {
-          __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-          for (int i = 0; i < 8; i++) v[i] = lutb[c][px[i][c]];
-          *reinterpret_cast<int4 *>(o + c * plane_sz) = *reinterpret_cast<int4 *>(v);
+          for (int c = 0; c < 3; c++) h0[c] = h1[c];
         } else {
-          for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lutb[c][px[i][c]];
+          hrow(yy.x, h0);
         }
+        cy0 = yy.x;
       }
-    } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
-      float *o = reinterpret_cast<float *>(P.out) + img * stride + (int64_t)oy * res + ox0;
+      if (yy.y != cy1) {
+        if (yy.y == cy0) {
+#pragma unroll
+          for (int c = 0; c < 3; c++) h1[c] = h0[c];
+        } else {
+          hrow(yy.y, h1);
+        }
+        cy1 = yy.y;
+      }
+      int px[3];
 #pragma unroll
       for (int c = 0; c < 3; c++) {
-        if (full) {
-          float4 a = make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]);
-          float4 b = make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]);
-          reinterpret_cast<float4 *>(o + c * plane_sz)[0] = a;
-          reinterpret_cast<float4 *>(o + c * plane_sz)[1] = b;
-        } else {
-          for (int i = 0; i < 8 && ox0 + i < res; i++) o[c * plane_sz + i] = lut[c][px[i][c]];
-        }
+        const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, h0[c]), __dmul_rn(wy, h1[c])), 0.5);
+        const int iv = __double2int_rz(v);
+        px[c] = iv > 255 ? 255 : iv;
       }
-    }
-    if (P.out_u8) {
-      uint8_t *o = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox0) * 3;
-      if (full) {
-        uint32_t w[6];
+      const int oy = ob0 + r;
+      const int64_t o = img * stride + (int64_t)oy * res + ox;
+      if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+        __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
 #pragma unroll
-        for (int q = 0; q < 6; q++) {
-          uint32_t acc = 0;
+        for (int c = 0; c < 3; c++) out[c * plane_sz] = lutb[c][px[c]];
+      } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+        float *out = reinterpret_cast<float *>(P.out) + o;
 #pragma unroll
-          for (int b = 0; b < 4; b++) {
-            const int e = q * 4 + b;
-            acc |= (uint32_t)px[e / 3][e % 3] << (8 * b);
-          }
-          w[q] = acc;
-        }
-        // 24 bytes at an 8-byte aligned address (res % 8 == 0)
-        reinterpret_cast<uint2 *>(o)[0] = make_uint2(w[0], w[1]);
-        reinterpret_cast<uint2 *>(o)[1] = make_uint2(w[2], w[3]);
-        reinterpret_cast<uint2 *>(o)[2] = make_uint2(w[4], w[5]);
-      } else {
-        for (int i = 0; i < 8 && ox0 + i < res; i++)
-          for (int c = 0; c < 3; c++) o[i * 3 + c] = px[i][c];
+        for (int c = 0; c < 3; c++) out[c * plane_sz] = lut[c][px[c]];
+      }
+      if (P.out_u8) {
+        uint8_t *out = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[c];
       }
     }
   }
@@ -247,11 +266,11 @@ int band_source_rows(int h, int res) {
 
 void launch_resize(const PixelParams &p, cudaStream_t st) {
   if (p.n <= 0) return;
-  const size_t dyn = (size_t)p.src_words * 4 + (size_t)p.res * 16;
-  static size_t attr = 48 * 1024;
-  if (dyn > attr) {
-    cudaFuncSetAttribute(k_resize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    attr = dyn;
+  const size_t dyn = (size_t)p.src_words * 4;
+  static bool attr = false;  // opt in once to the largest dynamic size api.cu allows
+  if (!attr) {
+    cudaFuncSetAttribute(k_resize, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+    attr = true;
   }
   dim3 grid((p.res + kBandRows - 1) / kBandRows, p.n);
   k_resize<<<grid, kPixThreads, dyn, st>>>(p);
