@@ -519,19 +519,27 @@ struct EntCtx {
   const int knew = (k) + kinc;                                \
   const bool bad = tot == 0 || (size != 0 && knew > 64)
 
-// Magnitude bits -> signed value (decode_kernels.py:101-108); size 0 -> 0.
-__device__ __forceinline__ int unit_value(uint32_t hi, int tot, int size) {
-  const uint32_t raw = (uint32_t)((uint64_t)(hi << (tot - size)) >> (32 - size));
+
+// Magnitude bits of a unit, not yet sign-extended (size 0 -> 0).
+__device__ __forceinline__ uint32_t unit_raw(uint32_t hi, int tot, int size) {
+  return (uint32_t)((uint64_t)(hi << (tot - size)) >> (32 - size));
+}
+
+// JPEG sign extension of `size` magnitude bits (decode_kernels.py:101-108).
+__device__ __forceinline__ int extend_raw(uint32_t raw, int size) {
   const uint32_t half = (1u << size) >> 1;
   return raw < half ? (int)raw - (int)((1u << size) - 1u) : (int)raw;
 }
 
-// Unit list entry: value (int16) << 16 | natural index << 1 | is_dc.  Every
-// unit is stored (EOB / ZRL as a zero at a position the block leaves zero);
-// a DC entry starts a block.
-__device__ __forceinline__ uint32_t unit_entry(int v, int nat, bool dc) {
-  return ((uint32_t)v << 16) | ((uint32_t)nat << 1) | (dc ? 1u : 0u);
+// Unit list entry: is_dc | raw magnitude bits << 1 | size << 16 | zig-zag
+// index << 20.  Every unit is stored (EOB / ZRL as a zero at a position the
+// block leaves zero); a DC entry starts a block.  Sign extension and the
+// zig-zag -> natural mapping happen in the consumers (k_idct), off the
+// decode chain.
+__device__ __forceinline__ uint32_t unit_entry(uint32_t raw, int size, int zzk, bool dc) {
+  return (dc ? 1u : 0u) | (raw << 1) | ((uint32_t)size << 16) | ((uint32_t)zzk << 20);
 }
+__device__ __forceinline__ int entry_value(uint32_t e) { return extend_raw((e >> 1) & 0x7FFFu, (e >> 16) & 15); }
 
 // Checkpoint: the decoder state at a block start of a lane's path, with the
 // path's unit-list index and block count there.
@@ -647,11 +655,11 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
       }
     }
     dbg_units++;
-    const int v = unit_value(hi, tot, size);
+    const uint32_t raw = unit_raw(hi, tot, size);
     const bool isdc = k == 0;
-    *lp = unit_entry(v, isdc ? 0 : C.zz(min(knew, 64) - 1), isdc);
-    if (isdc) {  // block record: where the block's units start, its DC difference
-      *bp = make_uint2(nl, (uint32_t)v);
+    *lp = unit_entry(raw, size, isdc ? 0 : min(knew, 64) - 1, isdc);
+    if (isdc) {  // block record: where the block's units start, its DC difference (raw)
+      *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
       bp += nbs < bcap;
       nbs++;
     }
@@ -776,7 +784,7 @@ __device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, u
       o.errp = r.p;
       break;
     }
-    const int v = unit_value(hi, tot, size);
+    const int v = extend_raw(unit_raw(hi, tot, size), size);
     if (k == 0) {
       const int s = (b >= C.c1) + (b >= C.c2);
       const int32_t pv = (s == 0 ? pr0 : (s == 1 ? pr1 : pr2)) + v;
@@ -815,7 +823,8 @@ __device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int
   int32_t s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll 4
   for (uint32_t i = 0; i < nb; i++) {
-    const int32_t v = (int32_t)bsl[ord + i].y;
+    const uint32_t ry = bsl[ord + i].y;
+    const int32_t v = extend_raw(ry & 0x7FFFu, ry >> 16);
     const int s = (b >= C.c1) + (b >= C.c2);
     s0 += s == 0 ? v : 0;
     s1 += s == 1 ? v : 0;
@@ -843,7 +852,7 @@ __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, c
   for (uint32_t i = 0; i < nb; i++) {
     const uint2 rec = bsl[ord + i];
     const int s = (b >= C.c1) + (b >= C.c2);
-    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + (int32_t)rec.y;
+    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + extend_raw(rec.y & 0x7FFFu, rec.y >> 16);
     p0 = s == 0 ? pv : p0;
     p1 = s == 1 ? pv : p1;
     p2 = s == 2 ? pv : p2;
@@ -1941,7 +1950,7 @@ constexpr int kIdctCtas = 8;
 // (eight lanes read eight consecutive entries per round).  fmt 0: the int16
 // coefficient window.  Called by all 32 lanes of a warp.
 __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, int c, int byr,
-                              int bxr, int32_t *blk) {
+                              int bxr, int32_t *blk, const uint8_t *zz) {
   const int j = threadIdx.x & 7;
   const int16_t *cf = sc.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
 #pragma unroll
@@ -1986,7 +1995,7 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
 #pragma unroll
     for (int u = 0; u < 4; u++) {
       const uint32_t idx = base + 4 * j + u;
-      if (!done && idx >= i0 && idx < stop) blk[(e4[u] >> 1) & 63] = (int32_t)e4[u] >> 16;
+      if (!done && idx >= i0 && idx < stop) blk[zz[(e4[u] >> 20) & 63]] = entry_value(e4[u]);
     }
     done = done || any != 0;
     base += 32;
@@ -1995,6 +2004,7 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
 }
 
 __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
+  __shared__ uint8_t s_zz[64];
   __shared__ int32_t q[3][64];
   __shared__ int32_t tr[8][4][64];
   __shared__ int32_t blks[32][64];
@@ -2005,6 +2015,7 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
   const int tid = threadIdx.x;
   const int ncomp = I.ncomp;
   for (int e = tid; e < ncomp * 64; e += 256) q[e >> 6][e & 63] = G->q[e >> 6][e & 63];
+  if (tid < 64) s_zz[tid] = c_zz[tid];
   int nb[3] = {0, 0, 0}, wb[3] = {1, 1, 1};
   for (int c = 0; c < ncomp; c++) {
     const int hb = min(I.wby0[c] + I.wbh[c], G->bh[c]) - I.wby0[c];
@@ -2023,7 +2034,7 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
       if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
     }
     const int byr = valid ? jb / wb[c] : 0, bxr = valid ? jb % wb[c] : 0;
-    gather_block8(valid, I, P.s, c, byr, bxr, blk);
+    gather_block8(valid, I, P.s, c, byr, bxr, blk, s_zz);
     const int pitch = I.plane_pitch[c];
     uint8_t *dst = P.s.plane + I.plane_off[c] + (uint64_t)byr * 8 * pitch + bxr * 8;
     idct_block_8lanes(valid, blk, q[c], dst, pitch, t);
@@ -2034,10 +2045,13 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
 // natural order, int16), gathered like k_idct.
 __global__ void __launch_bounds__(256) k_dump_coefs(Scratch sc, int16_t *out, const uint64_t *offsets) {
   __shared__ int32_t blks[32][64];
+  __shared__ uint8_t s_zz[64];
   const int img = blockIdx.y;
   const ImgInfo &I = sc.info[img];
   if (I.status != 0) return;
   const int tid = threadIdx.x;
+  if (tid < 64) s_zz[tid] = c_zz[tid];
+  __syncthreads();
   int nb[3] = {0, 0, 0};
   for (int c = 0; c < I.ncomp; c++) nb[c] = I.wbh[c] * I.wbw[c];
   const int total = nb[0] + nb[1] + nb[2];
@@ -2051,7 +2065,7 @@ __global__ void __launch_bounds__(256) k_dump_coefs(Scratch sc, int16_t *out, co
       if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
     }
     const int w = max(I.wbw[c], 1);
-    gather_block8(valid, I, sc, c, valid ? jb / w : 0, valid ? jb % w : 0, blk);
+    gather_block8(valid, I, sc, c, valid ? jb / w : 0, valid ? jb % w : 0, blk, s_zz);
     if (valid) {
       int16_t *o = out + offsets[img] + (uint64_t)jall * 64;
       const int j = tid & 7;
