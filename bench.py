@@ -443,7 +443,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=6,
                     help="batches in flight (one libessl context + CUDA stream each)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
