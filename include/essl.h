@@ -79,7 +79,8 @@ extern "C" {
 #define ESSL_K_ENTROPY 7 /* k_entropy: Huffman decode */
 #define ESSL_K_IDCT 8    /* k_idct: dequant + IDCT */
 #define ESSL_K_STAGE 9   /* k_host_gather: pinned-container payload gather */
-#define ESSL_K_COUNT 10
+#define ESSL_K_AUG 10    /* k_aug_blur + k_aug_out: 3-Aug / 3-Aug+ */
+#define ESSL_K_COUNT 11
 
 typedef struct essl_ctx essl_ctx;
 
@@ -105,6 +106,32 @@ typedef struct {
   int32_t mcus_reconstructed;
   int32_t width, height, ncomp;
 } essl_result;
+
+/* ---- 3-Aug / 3-Aug+ (apply_aug, pipeline.py:78-101; imgops.py:75-227) ----
+ * Per-sample parameters of the augmentation applied after the flip.  Filled
+ * by essl_aug_draw / essl_aug_batch from the sample's pipeline stream,
+ * except `weights`: gaussian_blur's taps (imgops.py:157-160) are numpy exp
+ * values in the reference, so the caller evaluates them the same way
+ * (exp(-(x*x)/(2*sigma*sigma)) over x = -radius..radius, divided by their
+ * sum) and writes 2*radius+1 of them. */
+#define ESSL_AUG_SIMPLE 0     /* AugLevel.SIMPLE: flip only */
+#define ESSL_AUG_3AUG 1       /* + one of grayscale / solarize / blur */
+#define ESSL_AUG_3AUG_PLUS 2  /* + brightness, contrast, saturation jitter */
+#define ESSL_AUG_OP_NONE (-1)
+#define ESSL_AUG_OP_GRAY 0     /* imgops.py:75-91, BT.601 fixed point */
+#define ESSL_AUG_OP_SOLARIZE 1 /* imgops.py:94-108, v >= threshold -> 255 - v */
+#define ESSL_AUG_OP_BLUR 2     /* imgops.py:122-163, separable, reflect padding */
+#define ESSL_AUG_MAX_RADIUS 12
+typedef struct {
+  int32_t op;        /* ESSL_AUG_OP_* */
+  int32_t radius;    /* blur radius max(1, ceil(3 sigma)), <= ESSL_AUG_MAX_RADIUS */
+  int32_t jitter;    /* 1: adjust_brightness, _contrast, _saturation in order */
+  int32_t threshold; /* solarize threshold (SOLARIZE_THRESHOLD = 128) */
+  double sigma;      /* blur sigma ~ U[0.1, 2.0) (BLUR_SIGMA_RANGE) */
+  double factors[3]; /* brightness, contrast, saturation ~ U[0.7, 1.3) */
+  double weights[2 * ESSL_AUG_MAX_RADIUS + 1];
+  double reserved;
+} essl_aug;
 
 /* ---- context ------------------------------------------------------------
  * Replaces: Loader.__init__ (pipeline.py:181-195) resource setup.  The
@@ -175,6 +202,15 @@ int essl_decode_rrc(essl_ctx *ctx, const uint8_t *blob,
                     void *out, int64_t out_stride, uint8_t *out_u8,
                     essl_result *results, void *stream);
 
+/* Same with the 3-Aug / 3-Aug+ stage (pipeline.py:88-101) between the flip
+ * and normalize: aug is a HOST array of n essl_aug (NULL: simple).  The
+ * uint8 view (out_u8) holds the augmented image (ImageBatch.uint8 is the
+ * image normalize sees, pipeline.py:228-232). */
+int essl_decode_rrc_aug(essl_ctx *ctx, const uint8_t *blob,
+                        const essl_sample *samples, const essl_aug *aug, int n,
+                        int res, int out_kind, void *out, int64_t out_stride,
+                        uint8_t *out_u8, essl_result *results, void *stream);
+
 /* Replaces: decode_crop(bytes, CropRect) (codec.py:448-511) for a batch of
  * crops: writes each uint8 [h,w,3] region at out + out_offsets[i]
  * (device pointer + host offsets). */
@@ -227,6 +263,13 @@ int essl_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh,
                    int ow, int flip, void *stream);
 int essl_normalize_u8(const uint8_t *src, int h, int w, float *dst,
                       void *stream);
+/* apply_aug's pixel stage after the flip (pipeline.py:88-101) on n uint8
+ * HWC images [n,h,w,3] (DEVICE src/dst, may not alias); aug is a HOST
+ * array of n essl_aug.  Replaces grayscale / solarize / gaussian_blur /
+ * adjust_brightness / adjust_contrast / adjust_saturation (imgops.py:75-227)
+ * as a batch.  h, w <= the context's max_side. */
+int essl_augment_u8(essl_ctx *ctx, const uint8_t *src, int n, int h, int w,
+                    const essl_aug *aug, uint8_t *dst, void *stream);
 
 /* ---- host-side sampling (C++, glibc libm: bit-exact with CPython) ---------
  * Replace rng.py:27-87 and pipeline.py:51-87. */
@@ -248,6 +291,17 @@ int essl_rrc_batch(uint64_t seed, uint64_t epoch, const int64_t *indices,
                    double scale_lo, double scale_hi, double ratio_lo,
                    double ratio_hi, essl_sample *samples);
 int essl_mask_count(int tokens, double ratio); /* masking.py:43-45 */
+/* apply_aug's draws (pipeline.py:85-101) from a pipeline stream positioned
+ * after sample_rrc: flip, then for 3-Aug op = randint(3) and, for the blur,
+ * sigma = uniform(0.1, 2.0); for 3-Aug+ three uniform(0.7, 1.3) factors.
+ * Leaves aug->weights zero (see essl_aug). */
+int essl_aug_draw(uint64_t *state, int level, int32_t *flip, essl_aug *aug);
+/* essl_rrc_batch + essl_aug_draw per sample (aug may be NULL for SIMPLE). */
+int essl_aug_batch(uint64_t seed, uint64_t epoch, const int64_t *indices,
+                   int n, const uint16_t *widths, const uint16_t *heights,
+                   double scale_lo, double scale_hi, double ratio_lo,
+                   double ratio_hi, int level, essl_sample *samples,
+                   essl_aug *aug);
 
 /* ---- dataset builder (row f2; fixtures and benchmark inputs) --------------
  * encode_jpeg (codec.py:574-632): baseline 4:2:0, Annex-K tables, float64

@@ -945,6 +945,117 @@ ORC_API void orc_normalize(const uint8_t *img, int h, int w, float *out) {
 }
 
 /* ------------------------------------------------------------------ */
+/* 3-Aug / 3-Aug+ pixel ops (imgops.py:75-227) on uint8 HWC images      */
+/* ------------------------------------------------------------------ */
+static inline int luma601(int r, int g, int b) { /* imgops.py:78-81 */
+  return (19595 * r + 38470 * g + 7471 * b + 32768) >> 16;
+}
+
+/* imgops.py:75-91 grayscale. */
+ORC_API void orc_grayscale(const uint8_t *img, int h, int w, uint8_t *out) {
+  for (int64_t p = 0; p < (int64_t)h * w; p++) {
+    int v = luma601(img[3 * p], img[3 * p + 1], img[3 * p + 2]);
+    out[3 * p] = out[3 * p + 1] = out[3 * p + 2] = (uint8_t)v;
+  }
+}
+
+/* imgops.py:94-108 solarize (>= threshold inverts). */
+ORC_API void orc_solarize(const uint8_t *img, int h, int w, int threshold, uint8_t *out) {
+  for (int64_t i = 0; i < (int64_t)h * w * 3; i++)
+    out[i] = img[i] >= threshold ? (uint8_t)(255 - img[i]) : img[i];
+}
+
+/* imgops.py:111-119 _reflect (Python modulo). */
+static int reflect_idx(int i, int n) {
+  if (n == 1) return 0;
+  int period = 2 * n - 2;
+  i = ((i % period) + period) % period;
+  if (i >= n) i = period - i;
+  return i;
+}
+
+/* imgops.py:122-163 gaussian_blur given its normalised weights (ntaps =
+ * 2*radius+1; the weights are numpy's, computed by the caller exactly as
+ * imgops.py:157-160 does).  Horizontal float64 pass into tmp, vertical pass
+ * with int(acc + 0.5) capped at 255; sequential accumulation, no FMA. */
+ORC_API void orc_gaussian_blur(const uint8_t *img, int h, int w, const double *wts, int ntaps,
+                               uint8_t *out) {
+  int r = (ntaps - 1) / 2;
+  double *tmp = (double *)malloc(sizeof(double) * (size_t)h * w * 3);
+  for (int y = 0; y < h; y++)
+    for (int x = 0; x < w; x++)
+      for (int c = 0; c < 3; c++) {
+        double acc = 0.0;
+        for (int k = 0; k < ntaps; k++)
+          acc += wts[k] * (double)img[((int64_t)y * w + reflect_idx(x + k - r, w)) * 3 + c];
+        tmp[((int64_t)y * w + x) * 3 + c] = acc;
+      }
+  for (int y = 0; y < h; y++)
+    for (int x = 0; x < w; x++)
+      for (int c = 0; c < 3; c++) {
+        double acc = 0.0;
+        for (int k = 0; k < ntaps; k++)
+          acc += wts[k] * tmp[((int64_t)reflect_idx(y + k - r, h) * w + x) * 3 + c];
+        int v = (int)(acc + 0.5);
+        if (v > 255) v = 255;
+        out[((int64_t)y * w + x) * 3 + c] = (uint8_t)v;
+      }
+  free(tmp);
+}
+
+static inline uint8_t blend1(double factor, double v, double target) { /* imgops.py:170-178 */
+  int q = (int)floor(factor * v + (1.0 - factor) * target + 0.5);
+  return (uint8_t)(q < 0 ? 0 : q > 255 ? 255 : q);
+}
+
+/* imgops.py:199-210 _luma_mean. */
+ORC_API double orc_luma_mean(const uint8_t *img, int h, int w) {
+  double acc = 0.0;
+  for (int64_t p = 0; p < (int64_t)h * w; p++)
+    acc += luma601(img[3 * p], img[3 * p + 1], img[3 * p + 2]);
+  return acc / (double)((int64_t)h * w);
+}
+
+/* imgops.py:213-227 adjust_brightness (kind 0), adjust_contrast (1),
+ * adjust_saturation (2). */
+ORC_API void orc_adjust(const uint8_t *img, int h, int w, int kind, double factor, uint8_t *out) {
+  int64_t np_ = (int64_t)h * w;
+  double target = kind == 1 ? orc_luma_mean(img, h, w) : 0.0;
+  for (int64_t p = 0; p < np_; p++) {
+    double g = kind == 2 ? (double)luma601(img[3 * p], img[3 * p + 1], img[3 * p + 2]) : target;
+    for (int c = 0; c < 3; c++) out[3 * p + c] = blend1(factor, (double)img[3 * p + c], g);
+  }
+}
+
+/* Per-sample 3-Aug draw results (pipeline.py:88-101); weights come from
+ * numpy (see oracle.py blur_weights). */
+typedef struct {
+  int32_t op;     /* -1 none, 0 grayscale, 1 solarize, 2 blur */
+  int32_t ntaps;  /* blur: 2*radius+1 */
+  int32_t jitter; /* 1: brightness, contrast, saturation */
+  int32_t pad;
+  double factors[3];
+  double wts[32];
+} OrcAug;
+
+/* apply_aug after the flip (pipeline.py:88-101), in place on img. */
+ORC_API void orc_apply_aug_ops(uint8_t *img, int h, int w, const OrcAug *a) {
+  size_t nb = (size_t)h * w * 3;
+  uint8_t *t = (uint8_t *)malloc(nb);
+  if (a->op == 0) orc_grayscale(img, h, w, t);
+  else if (a->op == 1) orc_solarize(img, h, w, 128, t); /* SOLARIZE_THRESHOLD imgops.py:19 */
+  else if (a->op == 2) orc_gaussian_blur(img, h, w, a->wts, a->ntaps, t);
+  if (a->op >= 0) memcpy(img, t, nb);
+  if (a->jitter) {
+    for (int kind = 0; kind < 3; kind++) {
+      orc_adjust(img, h, w, kind, a->factors[kind], t);
+      memcpy(img, t, nb);
+    }
+  }
+  free(t);
+}
+
+/* ------------------------------------------------------------------ */
 /* Loader sample (pipeline.py:219-235) and a threaded batch driver      */
 /* ------------------------------------------------------------------ */
 typedef struct {
@@ -962,7 +1073,7 @@ ORC_API int orc_fill_sample(const uint8_t *payload, int len, uint32_t crc,
                             int img_w, int img_h, int64_t index,
                             const OrcLoaderCfg *cfg, float *pixels,
                             uint8_t *u8, int32_t *mask, int32_t *rect_out,
-                            int32_t *err) {
+                            const OrcAug *aug, int32_t *err) {
   if (orc_crc32(payload, len) != crc) {
     if (err) { err[0] = ST_CRC; err[1] = 0; err[2] = -1; }
     return ST_CRC;
@@ -995,6 +1106,7 @@ ORC_API int orc_fill_sample(const uint8_t *payload, int len, uint32_t crc,
         }
     }
   }
+  if (aug) orc_apply_aug_ops(img, res, res, aug); /* pipeline.py:88-101 */
   orc_normalize(img, res, res, pixels);
   if (u8) memcpy(u8, img, (size_t)res * res * 3);
   free(img);
@@ -1018,6 +1130,7 @@ typedef struct {
   float *pixels;
   uint8_t *u8;
   int32_t *mask;
+  const OrcAug *aug; /* per batch position, or NULL (simple) */
   int32_t *status;
   volatile int next;
 } BatchJob;
@@ -1035,7 +1148,7 @@ static void *batch_worker(void *arg) {
         j->widths[idx], j->heights[idx], idx, j->cfg,
         j->pixels + (int64_t)i * 3 * res * res,
         j->u8 ? j->u8 + (int64_t)i * res * res * 3 : NULL,
-        j->mask ? j->mask + (int64_t)i * k : NULL, NULL, e3);
+        j->mask ? j->mask + (int64_t)i * k : NULL, NULL, j->aug ? j->aug + i : NULL, e3);
   }
   return NULL;
 }
@@ -1048,10 +1161,10 @@ ORC_API int orc_loader_batch(const uint8_t *base, const uint64_t *offsets,
                              const uint16_t *widths, const uint16_t *heights,
                              const int64_t *indices, int n,
                              const OrcLoaderCfg *cfg, float *pixels,
-                             uint8_t *u8, int32_t *mask, int32_t *status,
-                             int nthreads) {
+                             uint8_t *u8, int32_t *mask, const OrcAug *aug,
+                             int32_t *status, int nthreads) {
   BatchJob j = {base, offsets, lengths, crcs, widths, heights, indices, n,
-                cfg, pixels, u8, mask, status, 0};
+                cfg, pixels, u8, mask, aug, status, 0};
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) {
     batch_worker(&j);

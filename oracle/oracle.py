@@ -10,6 +10,7 @@ Function names mirror the reference API they restate
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from pathlib import Path
@@ -82,9 +83,16 @@ def lib():
         L.orc_normalize.argtypes = [P, i32, i32, P]
         L.orc_fill_sample.restype = i32
         L.orc_fill_sample.argtypes = [P, i32, ctypes.c_uint32, i32, i32, i64,
-                                      P, P, P, P, P, P]
+                                      P, P, P, P, P, P, P]
         L.orc_loader_batch.restype = i32
-        L.orc_loader_batch.argtypes = [P, P, P, P, P, P, P, i32, P, P, P, P, P, i32]
+        L.orc_loader_batch.argtypes = [P, P, P, P, P, P, P, i32, P, P, P, P, P, P, i32]
+        L.orc_grayscale.argtypes = [P, i32, i32, P]
+        L.orc_solarize.argtypes = [P, i32, i32, i32, P]
+        L.orc_gaussian_blur.argtypes = [P, i32, i32, P, i32, P]
+        L.orc_luma_mean.restype = dbl
+        L.orc_luma_mean.argtypes = [P, i32, i32]
+        L.orc_adjust.argtypes = [P, i32, i32, i32, dbl, P]
+        L.orc_apply_aug_ops.argtypes = [P, i32, i32, P]
         _lib = L
     return _lib
 
@@ -242,9 +250,132 @@ def _cfg(seed, epoch, res, scale, ratio, mask_grid, mask_k):
                         scale[1], ratio[0], ratio[1], mask_grid, mask_k)
 
 
+# ---------------------------------------------------------------------------
+# 3-Aug / 3-Aug+ (imgops.py:75-227, pipeline.py:78-101)
+
+SOLARIZE_THRESHOLD = 128          # imgops.py:19
+BLUR_SIGMA_RANGE = (0.1, 2.0)     # imgops.py:20
+JITTER_STRENGTH = 0.3             # imgops.py:21
+AUG_LEVELS = ("simple", "3aug", "3aug+")
+
+
+class OrcAug(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("ntaps", ctypes.c_int32), ("jitter", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("factors", ctypes.c_double * 3),
+                ("wts", ctypes.c_double * 32)]
+
+
+def blur_weights(sigma: float) -> np.ndarray:
+    """gaussian_blur's weights, evaluated with numpy exactly as
+    imgops.py:157-160 does (numpy's exp is part of the reference algorithm)."""
+    radius = max(1, math.ceil(3.0 * sigma))
+    xs = np.arange(-radius, radius + 1, dtype=np.float64)
+    wts = np.exp(-(xs * xs) / (2.0 * sigma * sigma))
+    wts /= wts.sum()
+    return wts
+
+
+def aug_draws(rng: SampleRng, level: str) -> dict:
+    """apply_aug's draws in stream order (pipeline.py:85-101): flip, then
+    (3-Aug) op = randint(3) and sigma for the blur, then (3-Aug+) the three
+    jitter factors.  `rng` must be positioned after sample_rrc."""
+    d = {"flip": int(rng.random() < 0.5), "op": -1, "sigma": None, "factors": None}
+    if level != "simple":
+        d["op"] = rng.randint(3)
+        if d["op"] == 2:
+            lo, hi = BLUR_SIGMA_RANGE
+            d["sigma"] = lo + (hi - lo) * rng.random()           # rng.py:54-55
+    if level == "3aug+":
+        s = JITTER_STRENGTH
+        d["factors"] = [(1.0 - s) + ((1.0 + s) - (1.0 - s)) * rng.random() for _ in range(3)]
+    return d
+
+
+def orc_aug(d: dict) -> OrcAug:
+    a = OrcAug()
+    a.op = d["op"]
+    if d["op"] == 2:
+        w = blur_weights(d["sigma"])
+        a.ntaps = len(w)
+        for i, v in enumerate(w):
+            a.wts[i] = float(v)
+    if d["factors"] is not None:
+        a.jitter = 1
+        for i, v in enumerate(d["factors"]):
+            a.factors[i] = v
+    return a
+
+
+def grayscale(img):
+    src = np.ascontiguousarray(img, np.uint8)
+    out = np.empty_like(src)
+    lib().orc_grayscale(_p(src), src.shape[0], src.shape[1], _p(out))
+    return out
+
+
+def solarize(img, threshold=SOLARIZE_THRESHOLD):
+    src = np.ascontiguousarray(img, np.uint8)
+    out = np.empty_like(src)
+    lib().orc_solarize(_p(src), src.shape[0], src.shape[1], threshold, _p(out))
+    return out
+
+
+def gaussian_blur(img, sigma=None, weights=None):
+    src = np.ascontiguousarray(img, np.uint8)
+    w = np.ascontiguousarray(blur_weights(sigma) if weights is None else weights, np.float64)
+    out = np.empty_like(src)
+    lib().orc_gaussian_blur(_p(src), src.shape[0], src.shape[1], _p(w), len(w), _p(out))
+    return out
+
+
+def luma_mean(img):
+    src = np.ascontiguousarray(img, np.uint8)
+    return float(lib().orc_luma_mean(_p(src), src.shape[0], src.shape[1]))
+
+
+def _adjust(img, kind, factor):
+    src = np.ascontiguousarray(img, np.uint8)
+    out = np.empty_like(src)
+    lib().orc_adjust(_p(src), src.shape[0], src.shape[1], kind, factor, _p(out))
+    return out
+
+
+def adjust_brightness(img, factor):
+    return _adjust(img, 0, factor)
+
+
+def adjust_contrast(img, factor):
+    return _adjust(img, 1, factor)
+
+
+def adjust_saturation(img, factor):
+    return _adjust(img, 2, factor)
+
+
+def apply_aug(rng: SampleRng, img, level: str):
+    """pipeline.py:78-101 on an HWC uint8 image."""
+    d = aug_draws(rng, level)
+    out = np.ascontiguousarray(img[:, ::-1] if d["flip"] else img, np.uint8).copy()
+    a = orc_aug(d)
+    lib().orc_apply_aug_ops(_p(out), out.shape[0], out.shape[1], ctypes.byref(a))
+    return out
+
+
+def sample_augs(seed, epoch, indices, widths, heights, scale, ratio, level) -> list:
+    """Per-sample draws for a batch (rect draws replayed, then aug_draws)."""
+    out = []
+    for idx in indices:
+        r = SampleRng(seed, epoch, int(idx), 0)
+        rect = sample_rrc(r, int(widths[idx]), int(heights[idx]), scale, ratio)
+        d = aug_draws(r, level)
+        d["rect"] = rect
+        out.append(d)
+    return out
+
+
 def fill_sample(payload: bytes, crc: int, w: int, h: int, index: int, seed: int,
                 epoch: int, res: int, scale=(0.08, 1.0), ratio=(3 / 4, 4 / 3),
-                mask_ratio=0.0, patch=16):
+                mask_ratio=0.0, patch=16, aug="simple"):
     """pipeline.py:219-235 for one sample -> (pixels f32, u8, mask, rect+flip)."""
     grid = res // patch if mask_ratio > 0 else 0
     k = mask_count(grid * grid, mask_ratio) if grid else 0
@@ -254,9 +385,15 @@ def fill_sample(payload: bytes, crc: int, w: int, h: int, index: int, seed: int,
     mask = np.zeros(max(k, 1), np.int32)
     rect = np.zeros(5, np.int32)
     err = np.zeros(3, np.int32)
+    a = None
+    if aug != "simple":
+        r = SampleRng(seed, epoch, index, 0)
+        sample_rrc(r, w, h, scale, ratio)
+        a = orc_aug(aug_draws(r, aug))
     st = lib().orc_fill_sample(_p(_buf(payload)), len(payload), crc, w, h, index,
                                ctypes.byref(cfg), _p(pix), _p(u8), _p(mask),
-                               _p(rect), _p(err))
+                               _p(rect), ctypes.byref(a) if a is not None else None,
+                               _p(err))
     if st:
         raise OracleError(*err)
     return pix, u8, (mask[:k] if grid else None), tuple(int(v) for v in rect)
@@ -265,7 +402,8 @@ def fill_sample(payload: bytes, crc: int, w: int, h: int, index: int, seed: int,
 def loader_batch(blob: np.ndarray, records: np.ndarray, indices: np.ndarray,
                  seed: int, epoch: int, res: int, scale=(0.08, 1.0),
                  ratio=(3 / 4, 4 / 3), mask_ratio=0.0, patch=16, keep_uint8=False,
-                 nthreads: int | None = None, pixels: np.ndarray | None = None):
+                 nthreads: int | None = None, pixels: np.ndarray | None = None,
+                 aug="simple"):
     """A threaded oracle batch over a container mapped as `blob` (uint8)
     with the reference record table `records` (container.py:46-51)."""
     n = len(indices)
@@ -284,8 +422,13 @@ def loader_batch(blob: np.ndarray, records: np.ndarray, indices: np.ndarray,
     hs = np.ascontiguousarray(records["height"], np.uint16)
     idx = np.ascontiguousarray(indices, np.int64)
     nt = nthreads or os.cpu_count() or 1
+    augs = None
+    if aug != "simple":
+        augs = (OrcAug * max(n, 1))()
+        for i, d in enumerate(sample_augs(seed, epoch, idx, ws, hs, scale, ratio, aug)):
+            augs[i] = orc_aug(d)
     lib().orc_loader_batch(_p(blob), _p(offs), _p(lens), _p(crcs), _p(ws), _p(hs),
                            _p(idx), n, ctypes.byref(cfg), _p(pixels),
                            _p(u8) if u8 is not None else None,
-                           _p(mask) if mask is not None else None, _p(status), nt)
+                           _p(mask) if mask is not None else None, augs, _p(status), nt)
     return pixels, u8, mask, status

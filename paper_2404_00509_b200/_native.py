@@ -19,7 +19,10 @@ ESSL_OPT_DECODE_MODE, ESSL_OPT_SEQ_BITS, ESSL_OPT_CHECKPOINT_BITS, ESSL_OPT_PROF
 ESSL_OPT_WARMUP_BITS = 5
 ESSL_OPT_STAGE_BYTES = 6
 KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep", "entropy", "idct",
-           "stage")
+           "stage", "aug")
+ESSL_AUG_SIMPLE, ESSL_AUG_3AUG, ESSL_AUG_3AUG_PLUS = 0, 1, 2
+ESSL_AUG_OP_NONE, ESSL_AUG_OP_GRAY, ESSL_AUG_OP_SOLARIZE, ESSL_AUG_OP_BLUR = -1, 0, 1, 2
+ESSL_AUG_MAX_RADIUS = 12
 
 # Every symbol include/essl.h declares (checked by tests/test_native_abi.py).
 EXPORTS = (
@@ -30,7 +33,8 @@ EXPORTS = (
     "essl_dump_coefs", "essl_mask", "essl_mask_from_states", "essl_gather_visible", "essl_resize_u8",
     "essl_normalize_u8", "essl_rng_init", "essl_rng_next", "essl_rng_random",
     "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
-    "essl_mask_count", "essl_encode_jpeg", "essl_synth_image",
+    "essl_mask_count", "essl_encode_jpeg", "essl_synth_image", "essl_decode_rrc_aug",
+    "essl_augment_u8", "essl_aug_draw", "essl_aug_batch",
 )
 
 
@@ -52,10 +56,32 @@ class EsslResult(ctypes.Structure):
                 ("height", ctypes.c_int32), ("ncomp", ctypes.c_int32)]
 
 
+class EsslAug(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("radius", ctypes.c_int32), ("jitter", ctypes.c_int32),
+                ("threshold", ctypes.c_int32), ("sigma", ctypes.c_double),
+                ("factors", ctypes.c_double * 3),
+                ("weights", ctypes.c_double * (2 * ESSL_AUG_MAX_RADIUS + 1)),
+                ("reserved", ctypes.c_double)]
+
+
 SAMPLE_NP_DTYPE = None  # filled lazily (numpy view of EsslSample arrays)
 RESULT_NP_DTYPE = None
+AUG_NP_DTYPE = None
 
 _lib = None
+
+
+def aug_dtype():
+    """numpy view of EsslAug arrays."""
+    global AUG_NP_DTYPE
+    import numpy as np
+    if AUG_NP_DTYPE is None:
+        AUG_NP_DTYPE = np.dtype([("op", "<i4"), ("radius", "<i4"), ("jitter", "<i4"),
+                                 ("threshold", "<i4"), ("sigma", "<f8"), ("factors", "<f8", 3),
+                                 ("weights", "<f8", 2 * ESSL_AUG_MAX_RADIUS + 1),
+                                 ("reserved", "<f8")])
+        assert AUG_NP_DTYPE.itemsize == ctypes.sizeof(EsslAug)
+    return AUG_NP_DTYPE
 
 
 def _np_dtypes():
@@ -117,6 +143,10 @@ def lib():
         "essl_mask_count": (i32, [i32, dbl]),
         "essl_encode_jpeg": (i64, [P, i32, i32, i32, i32, P, i64]),
         "essl_synth_image": (i32, [u64, i32, i32, P]),
+        "essl_decode_rrc_aug": (i32, [P, P, P, P, i32, i32, i32, P, i64, P, P, P]),
+        "essl_augment_u8": (i32, [P, P, i32, i32, i32, P, P, P]),
+        "essl_aug_draw": (i32, [P, i32, P, P]),
+        "essl_aug_batch": (i32, [u64, u64, P, i32, P, P, dbl, dbl, dbl, dbl, i32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -115,6 +115,11 @@ struct essl_ctx {
   cudaEvent_t ev_desc[kDescRing] = {};
   bool desc_used[kDescRing] = {};
   int desc_next = 0;
+  essl_aug *h_aug[kDescRing] = {};  // 3-Aug parameters, same ring slots
+  essl_aug *d_aug[kDescRing] = {};
+  // 3-Aug scratch: resized uint8 images and their blurred copies (grown on demand)
+  uint8_t *aug_a = nullptr, *aug_b = nullptr;
+  uint64_t aug_cap = 0;
   // staging (pinned ring, two slots)
   uint8_t *h_stage[2] = {};
   uint8_t *d_stage[2] = {};
@@ -164,17 +169,57 @@ struct Prof {
 
 namespace {
 
-int pick_desc(essl_ctx *c, const essl_sample *samples, int n, cudaStream_t st,
-              essl_sample **d_out) {
+// Next descriptor ring slot, once the batch that last used it has completed
+// (its ev_desc was recorded after that batch's last kernel).
+int pick_slot(essl_ctx *c) {
   const int r = c->desc_next;
   c->desc_next = (c->desc_next + 1) % kDescRing;
   if (c->desc_used[r]) CK(cudaEventSynchronize(c->ev_desc[r]));
+  c->desc_used[r] = true;
+  return r;
+}
+
+int pick_desc(essl_ctx *c, const essl_sample *samples, int n, cudaStream_t st,
+              essl_sample **d_out) {
+  const int r = pick_slot(c);
+  if (r < 0) return r;
   std::memcpy(c->h_desc[r], samples, sizeof(essl_sample) * n);
   CK(cudaMemcpyAsync(c->d_desc[r], c->h_desc[r], sizeof(essl_sample) * n,
                      cudaMemcpyHostToDevice, st));
   *d_out = c->d_desc[r];
-  c->desc_used[r] = true;
   return r;
+}
+
+// Validate a host essl_aug array; *max_radius = largest blur radius (0: none).
+int check_aug(const essl_aug *aug, int n, int *max_radius, bool *any) {
+  *max_radius = 0;
+  *any = false;
+  for (int i = 0; i < n; i++) {
+    const essl_aug &a = aug[i];
+    if (a.op < ESSL_AUG_OP_NONE || a.op > ESSL_AUG_OP_BLUR || (a.jitter != 0 && a.jitter != 1))
+      return fail(ESSL_E_ARG, "essl_aug: bad op / jitter");
+    if (a.op == ESSL_AUG_OP_BLUR) {
+      if (a.radius < 1 || a.radius > ESSL_AUG_MAX_RADIUS)
+        return fail(ESSL_E_ARG, "essl_aug: blur radius out of [1, ESSL_AUG_MAX_RADIUS]");
+      *max_radius = std::max(*max_radius, a.radius);
+    }
+    *any = *any || a.op != ESSL_AUG_OP_NONE || a.jitter;
+  }
+  return ESSL_OK;
+}
+
+// Grow the 3-Aug scratch to `bytes` per buffer (cudaFree synchronises the
+// device, so no in-flight batch still reads the old buffers).
+int ensure_aug_scratch(essl_ctx *c, uint64_t bytes) {
+  if (bytes <= c->aug_cap) return ESSL_OK;
+  if (c->aug_a) CK(cudaFree(c->aug_a));
+  if (c->aug_b) CK(cudaFree(c->aug_b));
+  c->aug_a = c->aug_b = nullptr;
+  c->aug_cap = 0;
+  CK(cudaMalloc(&c->aug_a, bytes));
+  CK(cudaMalloc(&c->aug_b, bytes));
+  c->aug_cap = bytes;
+  return ESSL_OK;
 }
 
 int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
@@ -272,6 +317,8 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
     CKC(cudaMallocHost(&c->h_desc[r], sizeof(essl_sample) * max_batch));
     CKC(cudaMalloc(&c->d_desc[r], sizeof(essl_sample) * max_batch));
     CKC(cudaEventCreateWithFlags(&c->ev_desc[r], cudaEventDisableTiming));
+    CKC(cudaMallocHost(&c->h_aug[r], sizeof(essl_aug) * max_batch));
+    CKC(cudaMalloc(&c->d_aug[r], sizeof(essl_aug) * max_batch));
   }
   c->stage_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 63) / 64 * 64);
   for (int r = 0; r < 2; r++) {
@@ -309,7 +356,11 @@ int essl_ctx_destroy(essl_ctx *c) {
     if (c->h_desc[r]) cudaFreeHost(c->h_desc[r]);
     if (c->d_desc[r]) cudaFree(c->d_desc[r]);
     if (c->ev_desc[r]) cudaEventDestroy(c->ev_desc[r]);
+    if (c->h_aug[r]) cudaFreeHost(c->h_aug[r]);
+    if (c->d_aug[r]) cudaFree(c->d_aug[r]);
   }
+  if (c->aug_a) cudaFree(c->aug_a);
+  if (c->aug_b) cudaFree(c->aug_b);
   for (int r = 0; r < 2; r++) {
     if (c->h_stage[r]) cudaFreeHost(c->h_stage[r]);
     if (c->d_stage[r]) cudaFree(c->d_stage[r]);
@@ -504,12 +555,30 @@ int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint
 int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n, int res,
                     int out_kind, void *out, int64_t out_stride, uint8_t *out_u8,
                     essl_result *results, void *stream) {
+  return essl_decode_rrc_aug(c, blob, samples, nullptr, n, res, out_kind, out, out_stride, out_u8,
+                             results, stream);
+}
+
+int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *samples,
+                        const essl_aug *aug, int n, int res, int out_kind, void *out,
+                        int64_t out_stride, uint8_t *out_u8, essl_result *results,
+                        void *stream) {
   if (!c || n < 0 || res < 1 || (n > 0 && (!blob || !samples)))
     return fail(ESSL_E_ARG, "essl_decode_rrc: bad arguments");
   if (out_kind != ESSL_OUT_BF16_NCHW && out_kind != ESSL_OUT_F32_NCHW && out_kind != ESSL_OUT_NONE)
     return fail(ESSL_E_ARG, "bad out_kind");
   if (out_kind != ESSL_OUT_NONE && !out) return fail(ESSL_E_ARG, "null output");
   if (n == 0) return ESSL_OK;
+  int max_radius = 0;
+  bool any_aug = false;
+  if (aug) {
+    int rc = check_aug(aug, n, &max_radius, &any_aug);
+    if (rc) return rc;
+  }
+  if (any_aug) {
+    int rc = ensure_aug_scratch(c, (uint64_t)n * res * res * 3);
+    if (rc) return rc;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int ring = -1;
   int rc = run_decode(c, blob, samples, n, results, st, &ring);
@@ -519,10 +588,10 @@ int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
   pp.plane = c->s.plane;
   pp.n = n;
   pp.res = res;
-  pp.out_kind = out_kind;
+  pp.out_kind = any_aug ? ESSL_OUT_NONE : out_kind;
   pp.out = out;
   pp.out_stride = out_stride;
-  pp.out_u8 = out_u8;
+  pp.out_u8 = any_aug ? c->aug_a : out_u8;
   {
     int words = 0;
     for (int i = 0; i < n; i++)
@@ -531,12 +600,52 @@ int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
     if ((size_t)pp.src_words * 4 > 200 * 1024)
       return fail(ESSL_E_CAPACITY, "crop too large for the resize kernel's shared staging");
   }
-  if (out_kind != ESSL_OUT_NONE || out_u8) {
+  if (pp.out_kind != ESSL_OUT_NONE || pp.out_u8) {
     Prof pr(c, ESSL_K_RESIZE, st);
     essl::launch_resize(pp, st);
   }
+  if (any_aug && (out_kind != ESSL_OUT_NONE || out_u8)) {
+    std::memcpy(c->h_aug[ring], aug, sizeof(essl_aug) * n);
+    CK(cudaMemcpyAsync(c->d_aug[ring], c->h_aug[ring], sizeof(essl_aug) * n,
+                       cudaMemcpyHostToDevice, st));
+    essl::AugOutParams ap{c->aug_a, c->aug_b, c->d_aug[ring], n, res, res, out_kind, out,
+                          out_stride, out_u8};
+    Prof pr(c, ESSL_K_AUG, st);
+    essl::launch_aug(ap, max_radius, st);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev_desc[ring], st));
+  return ESSL_OK;
+}
+
+int essl_augment_u8(essl_ctx *c, const uint8_t *src, int n, int h, int w, const essl_aug *aug,
+                    uint8_t *dst, void *stream) {
+  if (!c || n < 0 || h < 1 || w < 1 || (n > 0 && (!src || !dst || !aug)) || src == dst)
+    return fail(ESSL_E_ARG, "essl_augment_u8: bad arguments");
+  if (n == 0) return ESSL_OK;
+  if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
+  if (h > c->max_side || w > c->max_side)
+    return fail(ESSL_E_CAPACITY, "image larger than context max_side");
+  int max_radius = 0;
+  bool any = false;
+  int rc = check_aug(aug, n, &max_radius, &any);
+  if (rc) return rc;
+  if (max_radius) {
+    rc = ensure_aug_scratch(c, (uint64_t)n * h * w * 3);
+    if (rc) return rc;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int r = pick_slot(c);
+  if (r < 0) return r;
+  std::memcpy(c->h_aug[r], aug, sizeof(essl_aug) * n);
+  CK(cudaMemcpyAsync(c->d_aug[r], c->h_aug[r], sizeof(essl_aug) * n, cudaMemcpyHostToDevice, st));
+  essl::AugOutParams ap{src, c->aug_b, c->d_aug[r], n, h, w, ESSL_OUT_NONE, nullptr, 0, dst};
+  {
+    Prof pr(c, ESSL_K_AUG, st);
+    essl::launch_aug(ap, max_radius, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_desc[r], st));
   return ESSL_OK;
 }
 

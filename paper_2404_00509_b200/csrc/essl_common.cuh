@@ -92,6 +92,19 @@ struct PixelParams {
   int src_words;       // k_resize shared source rows: band source rows x widest crop
 };
 
+// 3-Aug stage (k_aug_blur / k_aug_out): a = resized (flipped) uint8 HWC
+// images, b = blurred copies (written for blur images only).
+struct AugOutParams {
+  const uint8_t *a;
+  uint8_t *b;
+  const essl_aug *aug;  // device, n entries
+  int n, h, w;
+  int out_kind;
+  void *out;
+  int64_t out_stride;
+  uint8_t *out_u8;
+};
+
 // splitmix64 (rng.py:27-31)
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -122,6 +135,7 @@ void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
 size_t ckpt_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
+void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);
 void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, cudaStream_t st);
 int band_source_rows(int h, int res);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,

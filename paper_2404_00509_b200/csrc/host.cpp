@@ -5,6 +5,7 @@
 // Compiled with -ffp-contract=off: the reference evaluates every float64
 // expression with one rounding per operation (CPython semantics), and the
 // RRC uses glibc log/exp/sqrt exactly as CPython's math module does.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -116,6 +117,52 @@ int essl_rrc_batch(uint64_t seed, uint64_t epoch, const int64_t *indices, int n,
     if (rc) return rc;
     samples[i].x = r[0]; samples[i].y = r[1]; samples[i].w = r[2]; samples[i].h = r[3];
     samples[i].flip = rnd(&st) < 0.5 ? 1 : 0;
+  }
+  return ESSL_OK;
+}
+
+// apply_aug's draws (pipeline.py:85-101), after the RRC draws on the same
+// pipeline stream.  BLUR_SIGMA_RANGE / JITTER_STRENGTH: imgops.py:20-21.
+int essl_aug_draw(uint64_t *st, int level, int32_t *flip, essl_aug *aug) {
+  if (!st || level < ESSL_AUG_SIMPLE || level > ESSL_AUG_3AUG_PLUS) return ESSL_E_ARG;
+  const int32_t f = rnd(st) < 0.5 ? 1 : 0;
+  if (flip) *flip = f;
+  if (!aug) return level == ESSL_AUG_SIMPLE ? ESSL_OK : ESSL_E_ARG;
+  std::memset(aug, 0, sizeof(*aug));
+  aug->op = ESSL_AUG_OP_NONE;
+  aug->threshold = 128;  // SOLARIZE_THRESHOLD, imgops.py:19
+  if (level != ESSL_AUG_SIMPLE) {
+    aug->op = (int32_t)randint(st, 3);
+    if (aug->op == ESSL_AUG_OP_BLUR) {
+      aug->sigma = 0.1 + (2.0 - 0.1) * rnd(st);                 // rng.uniform(0.1, 2.0)
+      aug->radius = std::max(1, (int)std::ceil(3.0 * aug->sigma));  // imgops.py:156
+    }
+  }
+  if (level == ESSL_AUG_3AUG_PLUS) {
+    const double s = 0.3, lo = 1.0 - s, hi = 1.0 + s;
+    aug->jitter = 1;
+    for (int k = 0; k < 3; k++) aug->factors[k] = lo + (hi - lo) * rnd(st);
+  }
+  return ESSL_OK;
+}
+
+int essl_aug_batch(uint64_t seed, uint64_t epoch, const int64_t *indices, int n,
+                   const uint16_t *widths, const uint16_t *heights, double scale_lo,
+                   double scale_hi, double ratio_lo, double ratio_hi, int level,
+                   essl_sample *samples, essl_aug *aug) {
+  if (n < 0 || (n > 0 && (!indices || !widths || !heights || !samples)) ||
+      (level != ESSL_AUG_SIMPLE && n > 0 && !aug))
+    return ESSL_E_ARG;
+  for (int i = 0; i < n; i++) {
+    const int64_t idx = indices[i];
+    uint64_t st = essl_rng_init(seed, epoch, (uint64_t)idx, 0);
+    int32_t r[4];
+    int rc = essl_sample_rrc(&st, widths[idx], heights[idx], scale_lo, scale_hi, ratio_lo,
+                             ratio_hi, 10, r);
+    if (rc) return rc;
+    samples[i].x = r[0]; samples[i].y = r[1]; samples[i].w = r[2]; samples[i].h = r[3];
+    rc = essl_aug_draw(&st, level, &samples[i].flip, aug ? aug + i : nullptr);
+    if (rc) return rc;
   }
   return ESSL_OK;
 }

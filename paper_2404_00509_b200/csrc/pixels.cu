@@ -451,6 +451,181 @@ void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStrea
 }
 
 // ---------------------------------------------------------------------------
+// 3-Aug / 3-Aug+ stage (apply_aug after the flip, pipeline.py:88-101) on
+// uint8 HWC images: k_aug_blur (gaussian_blur, tiled) then k_aug_out (point
+// op, jitter, normalize / uint8 out).  All float64 arithmetic is one
+// rounding per operation in the reference's order (numba without
+// fastmath), so results are bit-identical.
+
+constexpr int kAugTile = 32;
+constexpr int kAugBlurThreads = 256;
+constexpr int kAugOutThreads = 512;
+
+__device__ __forceinline__ int reflect_idx(int i, int n) {  // imgops.py:111-119
+  if (n == 1) return 0;
+  const int period = 2 * n - 2;
+  i %= period;
+  if (i < 0) i += period;
+  return i >= n ? period - i : i;
+}
+
+__device__ __forceinline__ int luma601(int r, int g, int b) {  // imgops.py:78-81
+  return (19595 * r + 38470 * g + 7471 * b + 32768) >> 16;
+}
+
+// floor(factor * v + (1 - factor) * target + 0.5) clamped (imgops.py:166-196)
+__device__ __forceinline__ int blend1(double f, int v, double target) {
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(f, (double)v), __dmul_rn(__dsub_rn(1.0, f), target)),
+                             0.5);
+  return clamp255(__double2int_rd(s));
+}
+
+size_t aug_blur_smem(int radius) {
+  const int sh = kAugTile + 2 * radius;
+  return 32 * sizeof(double) + (size_t)sh * kAugTile * 3 * sizeof(double) + (size_t)sh * sh * 3;
+}
+
+// gaussian_blur (imgops.py:122-163) for one kAugTile^2 output tile: the
+// reflect-indexed source tile with its radius halo is staged in shared
+// memory, the float64 horizontal pass (imgops.py:122-134) fills a tile of
+// (th + 2r) rows, the vertical pass (:137-151) rounds int(acc + 0.5) capped
+// at 255.  grid: (tiles_x * tiles_y, n); images without the blur exit.
+__global__ void __launch_bounds__(kAugBlurThreads) k_aug_blur(const uint8_t *src, int h, int w,
+                                                              const essl_aug *aug, uint8_t *dst) {
+  const essl_aug &A = aug[blockIdx.y];
+  if (A.op != ESSL_AUG_OP_BLUR) return;
+  extern __shared__ __align__(16) unsigned char aug_sm[];
+  const int r = A.radius, nt = 2 * r + 1;
+  const int tiles_x = (w + kAugTile - 1) / kAugTile;
+  const int ty0 = (blockIdx.x / tiles_x) * kAugTile, tx0 = (blockIdx.x % tiles_x) * kAugTile;
+  const int th = min(kAugTile, h - ty0), tw = min(kAugTile, w - tx0);
+  const int sh = th + 2 * r, spitch = (tw + 2 * r) * 3, tpitch = tw * 3;
+  double *wt = reinterpret_cast<double *>(aug_sm);
+  double *tmp = wt + 32;
+  uint8_t *s = reinterpret_cast<uint8_t *>(tmp + (size_t)(kAugTile + 2 * r) * kAugTile * 3);
+  const size_t img_off = (size_t)blockIdx.y * h * w * 3;
+  const uint8_t *in = src + img_off;
+  if (threadIdx.x < nt) wt[threadIdx.x] = A.weights[threadIdx.x];
+  for (int i = threadIdx.x; i < sh * spitch; i += kAugBlurThreads) {
+    const int yy = i / spitch, rem = i - yy * spitch;
+    const int xx = rem / 3, c = rem - xx * 3;
+    s[i] = in[((size_t)reflect_idx(ty0 - r + yy, h) * w + reflect_idx(tx0 - r + xx, w)) * 3 + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < sh * tpitch; i += kAugBlurThreads) {
+    const int yy = i / tpitch, rem = i - yy * tpitch;
+    const uint8_t *row = s + yy * spitch + rem;  // tap k at row[3 k]
+    double acc = 0.0;
+    for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], (double)row[3 * k]));
+    tmp[i] = acc;
+  }
+  __syncthreads();
+  uint8_t *out = dst + img_off;
+  for (int i = threadIdx.x; i < th * tpitch; i += kAugBlurThreads) {
+    const int yy = i / tpitch, rem = i - yy * tpitch;
+    const double *col = tmp + yy * tpitch + rem;
+    double acc = 0.0;
+    for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], col[k * tpitch]));
+    const int v = __double2int_rz(__dadd_rn(acc, 0.5));
+    out[((size_t)(ty0 + yy) * w + tx0) * 3 + rem] = (uint8_t)(v > 255 ? 255 : v);
+  }
+}
+
+// Point op (grayscale / solarize; the blur was applied by k_aug_blur).
+__device__ __forceinline__ void aug_point(int op, int thr, const uint8_t *p, int px[3]) {
+  px[0] = p[0]; px[1] = p[1]; px[2] = p[2];
+  if (op == ESSL_AUG_OP_GRAY) {
+    px[0] = px[1] = px[2] = luma601(px[0], px[1], px[2]);
+  } else if (op == ESSL_AUG_OP_SOLARIZE) {
+#pragma unroll
+    for (int c = 0; c < 3; c++) px[c] = px[c] >= thr ? 255 - px[c] : px[c];
+  }
+}
+
+// One CTA per image: (3-Aug+) luma mean of the brightness-adjusted image
+// (imgops.py:199-216; integer sum, exact), then per pixel the point op,
+// brightness, contrast, saturation (imgops.py:213-227), normalize through the
+// exact LUT (imgops.py:231-240) into bf16/f32 NCHW and/or the uint8 view.
+__global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
+  const int img = blockIdx.x;
+  const essl_aug &A = P.aug[img];
+  const int op = A.op, thr = A.threshold, jitter = A.jitter;
+  const double fb = A.factors[0], fc = A.factors[1], fs = A.factors[2];
+  const int64_t npx = (int64_t)P.h * P.w;
+  const uint8_t *src = (op == ESSL_AUG_OP_BLUR ? P.b : P.a) + (size_t)img * npx * 3;
+  __shared__ float lut[3][256];
+  __shared__ __nv_bfloat16 lutb[3][256];
+  __shared__ unsigned long long part[kAugOutThreads / 32];
+  if (P.out_kind == ESSL_OUT_F32_NCHW)
+    for (int i = threadIdx.x; i < 768; i += kAugOutThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
+  else if (P.out_kind == ESSL_OUT_BF16_NCHW)
+    for (int i = threadIdx.x; i < 768; i += kAugOutThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
+  double mean = 0.0;
+  if (jitter) {
+    unsigned long long sum = 0;
+    for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
+      int px[3];
+      aug_point(op, thr, src + 3 * i, px);
+      sum += (unsigned)luma601(blend1(fb, px[0], 0.0), blend1(fb, px[1], 0.0), blend1(fb, px[2], 0.0));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
+  }
+  __syncthreads();
+  if (jitter) {
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int k = 0; k < kAugOutThreads / 32; k++) tot += part[k];
+    mean = __ddiv_rn((double)tot, (double)npx);  // acc / (h * w), acc an exact integer
+  }
+  const int64_t stride = P.out_stride ? P.out_stride : 3 * npx;
+  for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
+    int px[3];
+    aug_point(op, thr, src + 3 * i, px);
+    if (jitter) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) px[c] = blend1(fb, px[c], 0.0);           // brightness
+#pragma unroll
+      for (int c = 0; c < 3; c++) px[c] = blend1(fc, px[c], mean);          // contrast
+      const double g = (double)luma601(px[0], px[1], px[2]);
+#pragma unroll
+      for (int c = 0; c < 3; c++) px[c] = blend1(fs, px[c], g);             // saturation
+    }
+    if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + i;
+#pragma unroll
+      for (int c = 0; c < 3; c++) o[c * npx] = lutb[c][px[c]];
+    } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+      float *o = reinterpret_cast<float *>(P.out) + img * stride + i;
+#pragma unroll
+      for (int c = 0; c < 3; c++) o[c * npx] = lut[c][px[c]];
+    }
+    if (P.out_u8) {
+      uint8_t *o = P.out_u8 + ((size_t)img * npx + i) * 3;
+#pragma unroll
+      for (int c = 0; c < 3; c++) o[c] = (uint8_t)px[c];
+    }
+  }
+}
+
+void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st) {
+  if (p.n <= 0) return;
+  if (max_radius > 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_aug_blur, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)aug_blur_smem(ESSL_AUG_MAX_RADIUS));
+      attr = true;
+    }
+    const int tiles = ((p.h + kAugTile - 1) / kAugTile) * ((p.w + kAugTile - 1) / kAugTile);
+    k_aug_blur<<<dim3(tiles, p.n), kAugBlurThreads, aug_blur_smem(max_radius), st>>>(
+        p.a, p.h, p.w, p.aug, p.b);
+  }
+  k_aug_out<<<p.n, kAugOutThreads, 0, st>>>(p);
+}
+
+// ---------------------------------------------------------------------------
 // Pinned-container gather: payload bytes read host->device over the bus by
 // a light kernel (no shared memory, so it co-runs with the decode kernels of
 // other batches).  One CTA per payload; each thread keeps four 16-byte loads

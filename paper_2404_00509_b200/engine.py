@@ -139,12 +139,23 @@ class Engine:
         return blob.value
 
     def decode_rrc(self, blob_ptr: int, samples: np.ndarray, res: int, out_kind: int,
-                   out=None, out_u8=None, results=None, stream=None, max_side: int = 0):
+                   out=None, out_u8=None, results=None, stream=None, max_side: int = 0,
+                   aug: np.ndarray | None = None):
+        """Decode + RRC resize + flip (+ 3-Aug stage when ``aug``, an
+        N.aug_dtype() array with blur weights filled) + normalize."""
         n = len(samples)
         self._ensure(n, max_side, int(samples["length"].max()) if n else 0)
-        N.check(N.lib().essl_decode_rrc(self._ctx, ctypes.c_void_p(blob_ptr), N.ptr(samples), n,
-                                        res, out_kind, N.ptr(out), 0, N.ptr(out_u8),
-                                        N.ptr(results), self._st(stream)), "essl_decode_rrc")
+        N.check(N.lib().essl_decode_rrc_aug(self._ctx, ctypes.c_void_p(blob_ptr), N.ptr(samples),
+                                            N.ptr(aug), n, res, out_kind, N.ptr(out), 0,
+                                            N.ptr(out_u8), N.ptr(results), self._st(stream)),
+                "essl_decode_rrc")
+
+    def augment_u8(self, src, aug: np.ndarray, dst, stream=None):
+        """apply_aug's pixel stage on device uint8 [n,h,w,3] images."""
+        n, h, w = int(src.shape[0]), int(src.shape[1]), int(src.shape[2])
+        self._ensure(n, max(h, w), 0)
+        N.check(N.lib().essl_augment_u8(self._ctx, N.ptr(src), n, h, w, N.ptr(aug), N.ptr(dst),
+                                        self._st(stream)), "essl_augment_u8")
 
     def decode_crop_u8(self, blob_ptr: int, samples: np.ndarray, out, offsets: np.ndarray,
                        results=None, stream=None, max_side: int = 0):

@@ -1,6 +1,6 @@
-"""Standalone pixel ops on the GPU (mirror of cropload/imgops.py:16-17, 63-72,
-243-257).  Inputs may be numpy arrays (copied to the device and back) or
-CUDA tensors (stay on the device)."""
+"""Standalone pixel ops on the GPU (mirror of cropload/imgops.py:16-21, 63-72,
+75-227, 243-257).  Inputs may be numpy arrays (copied to the device and
+back) or CUDA tensors (stay on the device)."""
 
 from __future__ import annotations
 
@@ -11,6 +11,25 @@ from .engine import default_engine
 
 IMAGENET_MEAN = np.array([0.485, 0.456, 0.406], np.float32)
 IMAGENET_STD = np.array([0.229, 0.224, 0.225], np.float32)
+
+from .augment import (BLUR_SIGMA_RANGE, JITTER_STRENGTH, SOLARIZE_THRESHOLD,  # noqa: E402,F401
+                      gaussian_blur, grayscale, solarize)
+from .augment import color_jitter as _color_jitter  # noqa: E402
+
+
+def adjust_brightness(img, factor: float):
+    """imgops.py:213-216 (factor 1.0 leaves the other two stages identity)."""
+    return _color_jitter(img, factor, 1.0, 1.0)
+
+
+def adjust_contrast(img, factor: float):
+    """imgops.py:219-222: blend with the image's mean BT.601 luma."""
+    return _color_jitter(img, 1.0, factor, 1.0)
+
+
+def adjust_saturation(img, factor: float):
+    """imgops.py:225-227: blend with the per-pixel grayscale."""
+    return _color_jitter(img, 1.0, 1.0, factor)
 
 
 def _to_dev(a, eng):

@@ -8,11 +8,13 @@ seed, epoch, index), so batch content matches the reference bit for bit
 (float32 mode) no matter how work is scheduled.
 
 Per batch (pipeline.py:219-267):
-  host C++   : epoch permutation, DDP shard, RRC rect + flip per sample
-               (glibc libm, bit-exact with CPython), descriptor table
+  host C++   : epoch permutation, DDP shard, RRC rect + flip (+ 3-Aug draws)
+               per sample (glibc libm, bit-exact with CPython), descriptor
+               table; blur taps via numpy (the reference's own expression)
   GPU        : CRC32 -> parse -> destuff -> speculative Huffman decode of the
                crop's MCU rows -> IDCT of crop MCUs -> colour + bilinear +
-               flip + normalize -> bf16/f32 NCHW (+ uint8 NHWC) ;
+               flip [-> 3-Aug/3-Aug+ stage] -> normalize -> bf16/f32 NCHW
+               (+ uint8 NHWC) ;
                MAE mask + ids_keep/ids_restore
 Compressed bytes are either HBM-resident (the container uploaded once) or
 staged per batch through a pinned double buffer.
@@ -70,13 +72,17 @@ def sample_rrc(rng: SampleRng, src_w: int, src_h: int, cfg: RrcConfig) -> CropRe
 
 
 def apply_aug(rng: SampleRng, img, level: AugLevel):
-    """Simple augmentation: horizontal flip at p=0.5 (pipeline.py:78-87).
-    The 3-Aug levels (pipeline.py:88-101) are SURVEY 8(f) row f1 (next)."""
+    """Simple / 3-aug / 3-aug+ augmentation, all draws from ``rng``
+    (pipeline.py:78-101): flip at p=0.5, then (3-aug) one of grayscale,
+    solarize, gaussian blur, then (3-aug+) brightness / contrast /
+    saturation jitter.  Draws in host C++, pixels on the GPU (k_aug_*)."""
+    from . import augment
     from .imgops import hflip
-    if level is not AugLevel.SIMPLE:
-        raise ConfigError(f"aug level {level.value!r} is not implemented on the GPU path yet")
-    if rng.random() < 0.5:
+    flip, a = augment.draw(rng._state, level)
+    if flip:
         img = hflip(img)
+    if augment.any_work(a):
+        img = augment._run(img, a)
     return img
 
 
@@ -223,9 +229,6 @@ class Loader:
         self.handle.validate_all()
         self.rrc = RrcConfig(tuple(config.scale), tuple(config.ratio), config.res)
         self.aug_level = AugLevel(config.aug)
-        if self.aug_level is not AugLevel.SIMPLE:
-            raise ConfigError(f"aug level {config.aug!r} is not implemented on the GPU path yet "
-                              "(SURVEY 8(f) row f1)")
         self.mask_spec = (MaskSpec.from_resolution(config.res, config.patch, config.mask_ratio)
                           if config.mask_ratio > 0.0 else None)
         from .engine import Engine
@@ -303,18 +306,33 @@ class Loader:
         self.close()
 
     # ------------------------------------------------------------------
-    def _descriptors(self, epoch: int, idxs: np.ndarray) -> np.ndarray:
+    def _descriptors(self, epoch: int, idxs: np.ndarray):
+        """Per-sample descriptors: rect + flip (+ 3-Aug draws, blur weights
+        filled) from each sample's pipeline stream (pipeline.py:221-227)."""
+        from . import augment
         cfg = self.config
         s = self.engine.samples(len(idxs))
         s["offset"] = self._offsets[idxs]
         s["length"] = self._lengths[idxs]
         s["crc32"] = self._crcs[idxs]
         s["check_crc"] = 1
-        N.check(N.lib().essl_rrc_batch(cfg.seed & (2**64 - 1), epoch & (2**64 - 1), N.ptr(idxs),
-                                       len(idxs), N.ptr(self._widths), N.ptr(self._heights),
-                                       self.rrc.scale[0], self.rrc.scale[1], self.rrc.ratio[0],
-                                       self.rrc.ratio[1], N.ptr(s)), "essl_rrc_batch")
-        return s
+        aug = None
+        if self.aug_level is AugLevel.SIMPLE:
+            N.check(N.lib().essl_rrc_batch(cfg.seed & (2**64 - 1), epoch & (2**64 - 1),
+                                           N.ptr(idxs), len(idxs), N.ptr(self._widths),
+                                           N.ptr(self._heights), self.rrc.scale[0],
+                                           self.rrc.scale[1], self.rrc.ratio[0],
+                                           self.rrc.ratio[1], N.ptr(s)), "essl_rrc_batch")
+        else:
+            aug = augment.new_aug(len(idxs))
+            N.check(N.lib().essl_aug_batch(cfg.seed & (2**64 - 1), epoch & (2**64 - 1),
+                                           N.ptr(idxs), len(idxs), N.ptr(self._widths),
+                                           N.ptr(self._heights), self.rrc.scale[0],
+                                           self.rrc.scale[1], self.rrc.ratio[0],
+                                           self.rrc.ratio[1], augment.level_code(self.aug_level),
+                                           N.ptr(s), N.ptr(aug)), "essl_aug_batch")
+            augment.fill_weights(aug)
+        return s, aug
 
     def enqueue(self, epoch: int, idxs: np.ndarray) -> _Pending:
         """Issue one batch on the device (asynchronous, on the next of the
@@ -328,7 +346,7 @@ class Loader:
         st.wait_stream(cur)  # outputs come from the consumer stream's pool
         idxs = np.ascontiguousarray(idxs, np.int64)
         b, res = len(idxs), cfg.res
-        samples = self._descriptors(epoch, idxs)
+        samples, aug = self._descriptors(epoch, idxs)
         if self._blob is not None:
             blob_ptr = self._blob.data_ptr()
         else:  # host container: one batched copy-engine gather from pinned memory
@@ -363,7 +381,7 @@ class Loader:
         u8 = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
         results = eng.new_results(b)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
-        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st)
+        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st, aug=aug)
         hidx, hlab, res_host = ring.idx[slot][:b], ring.lab[slot][:b], ring.res[slot][:b]
         hidx.numpy()[:] = idxs
         hlab.numpy()[:] = self._labels_np[idxs]

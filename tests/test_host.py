@@ -181,3 +181,84 @@ def test_shard_partition(E):
     assert [len(p) for p in parts] == [251, 251, 251, 250]
     with pytest.raises(ValueError):
         E.shard(perm, 4, 4)
+
+
+# ---- 3-Aug draws and blur taps ---------------------------
+
+def _gaug():
+    import json
+    return json.loads((GOLDEN / "golden_aug.json").read_text())
+
+
+def test_aug_draws_match_reference(E):
+    """essl_aug_draw (host C++) reproduces apply_aug's draws (pipeline.py:85-101)."""
+    from paper_2404_00509_b200 import augment
+    for rec in _gaug()["apply_aug"]:
+        r = E.SampleRng(rec["seed"], rec["epoch"], rec["index"])
+        flip, a = augment.draw(r._state, rec["level"])
+        assert flip == rec["flip"] and int(a["op"][0]) == rec["op"]
+        if rec["sigma"] is not None:
+            assert float(a["sigma"][0]).hex() == rec["sigma"]
+            assert int(a["radius"][0]) == rec["radius"]
+        if rec["jitter"] is not None:
+            assert [float(v).hex() for v in a["factors"][0]] == rec["jitter"]
+        else:
+            assert int(a["jitter"][0]) == 0
+
+
+def test_aug_batch_matches_loader_golden(E, native):
+    """essl_aug_batch: rects, flips and aug draws of the reference Loader."""
+    from paper_2404_00509_b200 import augment
+    g = _gaug()
+    for key, spec in g["loader"].items():
+        cfg = spec["cfg"]
+        with E.open_container(GOLDEN / spec["data"]) as h:
+            ws = np.ascontiguousarray(h.records["width"], np.uint16)
+            hs = np.ascontiguousarray(h.records["height"], np.uint16)
+            for e in spec["epochs"]:
+                smp = [s for s in spec["samples"] if s["epoch"] == e]
+                idx = np.array([s["index"] for s in smp], np.int64)
+                s = np.zeros(len(idx), native._np_dtypes()[0])
+                a = augment.new_aug(len(idx))
+                sc = cfg.get("scale", (0.08, 1.0))
+                native.check(native.lib().essl_aug_batch(
+                    cfg["seed"], e, native.ptr(idx), len(idx), native.ptr(ws), native.ptr(hs),
+                    sc[0], sc[1], 3 / 4, 4 / 3, augment.level_code(cfg["aug"]), native.ptr(s),
+                    native.ptr(a)))
+                augment.fill_weights(a)
+                for i, ref in enumerate(smp):
+                    assert [int(s[f][i]) for f in "xywh"] == ref["rect"], key
+                    assert int(s["flip"][i]) == ref["flip"] and int(a["op"][i]) == ref["op"]
+                    if ref["sigma"] is not None:
+                        assert float(a["sigma"][i]).hex() == ref["sigma"]
+                        w = [float(v).hex() for v in a["weights"][i][:2 * ref["radius"] + 1]]
+                        assert w == ref["weights"], key
+                    if ref["jitter"] is not None:
+                        assert [float(v).hex() for v in a["factors"][i]] == ref["jitter"]
+
+
+def test_blur_weights_vectorised_equal_reference_expression(E):
+    """fill_weights groups a batch by radius into one numpy expression; it
+    must equal imgops.py:157-160 evaluated per sample, element for element."""
+    from paper_2404_00509_b200 import augment
+    rr = np.random.default_rng(9)
+    n = 4000
+    a = augment.new_aug(n)
+    a["op"] = 2
+    a["sigma"] = 0.1 + 1.9 * rr.random(n)
+    a["sigma"][:4] = (0.1, 1.0 / 3.0, 2.0 - 2 ** -52, 4.0)
+    a["radius"] = [augment.blur_radius(float(s)) for s in a["sigma"]]
+    augment.fill_weights(a)
+    for i in range(n):
+        w = augment.blur_weights(float(a["sigma"][i]))
+        assert np.array_equal(a["weights"][i][:len(w)], w)
+        assert not a["weights"][i][len(w):].any()
+
+
+def test_aug_config_levels(E):
+    from paper_2404_00509_b200 import augment
+    assert augment.level_code("simple") == 0 and augment.level_code("3aug+") == 2
+    with pytest.raises(ValueError):
+        augment.level_code("4aug")
+    with pytest.raises(E.ConfigError):
+        E.LoaderConfig(data="x", aug="bogus").validate()
