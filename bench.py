@@ -168,6 +168,7 @@ def cpu_oracle_rate(path: Path, wl: dict, seconds: float, seed_epoch=(0, 0)) -> 
             idx = perm[(i * B) % len(h):(i * B) % len(h) + B]
             _, _, _, st = O.loader_batch(h.bytes, h.records, idx, seed_epoch[0], seed_epoch[1],
                                          wl["res"], scale=wl["scale"], mask_ratio=wl["mask"],
+                                         aug=wl.get("aug", "simple"),
                                          nthreads=nthreads, pixels=pix[:len(idx)])
             assert (st == 0).all()
             done += len(idx)
@@ -206,6 +207,7 @@ def run_reference(args, wl):
             idx = perm[(i * B) % len(h):(i * B) % len(h) + B]
             _, _, _, st = O.loader_batch(h.bytes, h.records, idx, 0, 0, wl["res"],
                                          scale=wl["scale"], mask_ratio=wl["mask"],
+                                         aug=wl.get("aug", "simple"),
                                          nthreads=nthreads, pixels=pix[:len(idx)])
             assert (st == 0).all()
             return len(idx)
@@ -221,7 +223,7 @@ def run_reference(args, wl):
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": wl["batch"],
-                       "res": wl["res"], "mask_ratio": wl["mask"], "pool_images": args.pool},
+                       "res": wl["res"], "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool},
             "cpu_baseline": {"value": v, "unit": "images/s", "cores": nthreads, "kind": "port",
                              "sample": f"{args.steps} timed batches of {wl['batch']} after "
                                        f"{args.warmup} warm-up, C oracle (port of the reference "
@@ -248,7 +250,8 @@ def run_gpu(args, wl):
     path = make_dataset(wl, args.pool, data_dir)
     B, res = wl["batch"], wl["res"]
     cfg = E.LoaderConfig(data=str(path), batch_size=B, res=res, scale=wl["scale"],
-                         mask_ratio=wl["mask"], out_dtype="bfloat16", device=str(dev),
+                         mask_ratio=wl["mask"], aug=wl.get("aug", "simple"),
+                         out_dtype="bfloat16", device=str(dev),
                          rank=rank, world_size=ws, resident=True, prefetch=args.streams,
                          streams=args.streams, reuse_outputs=True)
     loader = E.Loader(cfg)
@@ -341,24 +344,26 @@ def run_gpu(args, wl):
         torch.cuda.synchronize(dev)
         if ws > 1:
             dist.barrier()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
         n2 = 0
         perm2 = []
         e2e_host = []
         ep = 2
+        # as many batches as the device-side timed region, through the public
+        # multi-epoch iterator (prefetch kept full across epoch boundaries)
+        n_ep = -(-args.steps * B // max(1, len(handle) // ws))
+        for e in range(ep, ep + n_ep + 1):  # (bookkeeping for the byte count only)
+            perm2.append(E.shard(E.epoch_permutation(cfg.seed, e, len(handle)), rank, ws))
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
         hprev = time.perf_counter()
-        while n2 < args.steps * B:  # as many batches as the device-side timed region
-            perm2.append(E.shard(E.epoch_permutation(cfg.seed, ep, len(handle)), rank, ws))
-            for b in l2.epoch(ep):
-                n2 += len(b)
-                now = time.perf_counter()
-                e2e_host.append(now - hprev)
-                hprev = now
-                if n2 >= args.steps * B:
-                    break
-            ep += 1
+        for b in l2.epochs(ep):
+            n2 += len(b)
+            now = time.perf_counter()
+            e2e_host.append(now - hprev)
+            hprev = now
+            if n2 >= args.steps * B:
+                break
         perm2 = np.concatenate(perm2)
         s1.record(stream)
         torch.cuda.synchronize(dev)
@@ -408,7 +413,7 @@ def run_gpu(args, wl):
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int32", "out_dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": B,
-                           "res": res, "mask_ratio": wl["mask"], "pool_images": args.pool,
+                           "res": res, "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool,
                            "mean_payload_bytes": float(np.mean(handle.records["payload_length"])),
                            "l2": "inputs > L2: 8192-image pool (~235 MB) visited in permutation "
                                  "order; outputs are fresh buffers each step",
@@ -445,8 +450,13 @@ def main():
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
     ap.add_argument("--streams", type=int, default=6,
                     help="batches in flight (one libessl context + CUDA stream each)")
+    ap.add_argument("--aug", default="simple", choices=["simple", "3aug", "3aug+"],
+                    help="augmentation level (finetune schemes use 3aug / 3aug+)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
+    if args.aug != "simple":
+        wl["aug"] = args.aug
+        wl["desc"] = wl["desc"].replace("+ flip +", f"+ flip + {args.aug} +")
     if args.impl == "reference":
         run_reference(args, wl)
     else:

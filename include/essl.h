@@ -67,6 +67,8 @@ extern "C" {
 #define ESSL_OPT_PROFILE 4      /* 1: bracket every launch with CUDA events */
 #define ESSL_OPT_WARMUP_BITS 5  /* lanes start this far before their subsequence (0..4096) */
 #define ESSL_OPT_STAGE_BYTES 6  /* largest clean stream staged in shared memory (0: never) */
+#define ESSL_OPT_GATHER_CTAS 7  /* k_host_gather CTAs (bus-read gather; 0: one per payload) */
+#define ESSL_OPT_GATHER_TMA 8   /* 1: bus-read gather with bulk (TMA) copies */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0

@@ -18,6 +18,8 @@ ESSL_DECODE_SPECULATIVE, ESSL_DECODE_SERIAL = 0, 1
 ESSL_OPT_DECODE_MODE, ESSL_OPT_SEQ_BITS, ESSL_OPT_CHECKPOINT_BITS, ESSL_OPT_PROFILE = 1, 2, 3, 4
 ESSL_OPT_WARMUP_BITS = 5
 ESSL_OPT_STAGE_BYTES = 6
+ESSL_OPT_GATHER_CTAS = 7
+ESSL_OPT_GATHER_TMA = 8
 KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep", "entropy", "idct",
            "stage", "aug")
 ESSL_AUG_SIMPLE, ESSL_AUG_3AUG, ESSL_AUG_3AUG_PLUS = 0, 1, 2

@@ -135,6 +135,8 @@ struct essl_ctx {
   int ck_bits = 64;
   int warm_bits = 2048;
   int stage_max = 64 * 1024;
+  int gather_ctas = 8;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
+  bool gather_tma = false;  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
@@ -394,6 +396,13 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       if (value < 0 || value > (1 << 20)) return fail(ESSL_E_ARG, "bad stage bytes");
       c->stage_max = (int)value;
       return ESSL_OK;
+    case ESSL_OPT_GATHER_CTAS:
+      if (value < 0 || value > 65535) return fail(ESSL_E_ARG, "bad gather CTA count");
+      c->gather_ctas = (int)value;
+      return ESSL_OK;
+    case ESSL_OPT_GATHER_TMA:
+      c->gather_tma = value != 0;
+      return ESSL_OK;
     case ESSL_OPT_PROFILE:
       c->profile = value != 0;
       return ESSL_OK;
@@ -543,7 +552,8 @@ int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint
     CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
     {
       Prof pr(c, ESSL_K_STAGE, st);
-      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], st);
+      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], c->gather_ctas,
+                               c->gather_tma, st);
     }
   }
   CK(cudaEventRecord(c->ev_stage[slot], st));

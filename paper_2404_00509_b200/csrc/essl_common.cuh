@@ -136,7 +136,8 @@ size_t decode_hdr_bytes();
 size_t ckpt_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);
-void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, cudaStream_t st);
+void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, int ctas,
+                        bool tma, cudaStream_t st);
 int band_source_rows(int h, int res);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);

@@ -627,36 +627,143 @@ void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------
 // Pinned-container gather: payload bytes read host->device over the bus by
-// a light kernel (no shared memory, so it co-runs with the decode kernels of
-// other batches).  One CTA per payload; each thread keeps four 16-byte loads
-// in flight to cover the bus latency.  Sources are 64-byte aligned in the
-// container (container.py:26); an unaligned source takes the byte path.
-__global__ void __launch_bounds__(128) k_host_gather(const uint8_t *src, const GatherDesc *desc,
-                                                     uint8_t *dst) {
-  const GatherDesc d = desc[blockIdx.x];
-  const uint8_t *s = src + d.src;
-  uint8_t *o = dst + d.dst;
-  if (((d.src | d.dst) & 15) == 0) {
-    const int4 *s4 = reinterpret_cast<const int4 *>(s);
-    int4 *o4 = reinterpret_cast<int4 *>(o);
-    const uint32_t n16 = d.len / 16;
-    for (uint32_t i = threadIdx.x; i < n16; i += 4 * 128) {
-      int4 v[4];
+// a light kernel.  Bus reads have microsecond latency and hold the SM's
+// outstanding-miss resources for that long, so the gather runs on a few
+// CTAs only (`ctas`, ESSL_OPT_GATHER_CTAS) that loop over the batch's
+// payloads with 8 x 16 B loads in flight per thread -- the other SMs' memory
+// pipelines (the decode kernels of other batches) stay unaffected.  Sources
+// are 64-byte aligned in the container (container.py:26); an unaligned
+// source takes the byte path.
+constexpr int kGatherThreads = 256;
+constexpr int kGatherLoads = 8;
+
+__global__ void __launch_bounds__(kGatherThreads) k_host_gather(const uint8_t *src,
+                                                                const GatherDesc *desc, int n,
+                                                                uint8_t *dst) {
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    const GatherDesc d = desc[j];
+    const uint8_t *s = src + d.src;
+    uint8_t *o = dst + d.dst;
+    if (((d.src | d.dst) & 15) == 0) {
+      const int4 *s4 = reinterpret_cast<const int4 *>(s);
+      int4 *o4 = reinterpret_cast<int4 *>(o);
+      const uint32_t n16 = d.len / 16;
+      for (uint32_t i = threadIdx.x; i < n16; i += kGatherLoads * kGatherThreads) {
+        int4 v[kGatherLoads];
 #pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (i + u * 128 < n16) v[u] = s4[i + u * 128];
+        for (int u = 0; u < kGatherLoads; u++)
+          if (i + u * kGatherThreads < n16) v[u] = s4[i + u * kGatherThreads];
 #pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (i + u * 128 < n16) o4[i + u * 128] = v[u];
+        for (int u = 0; u < kGatherLoads; u++)
+          if (i + u * kGatherThreads < n16) o4[i + u * kGatherThreads] = v[u];
+      }
+      for (uint32_t i = n16 * 16 + threadIdx.x; i < d.len; i += kGatherThreads) o[i] = s[i];
+    } else {
+      for (uint32_t i = threadIdx.x; i < d.len; i += kGatherThreads) o[i] = s[i];
     }
-    for (uint32_t i = n16 * 16 + threadIdx.x; i < d.len; i += 128) o[i] = s[i];
-  } else {
-    for (uint32_t i = threadIdx.x; i < d.len; i += 128) o[i] = s[i];
   }
 }
 
-void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, cudaStream_t st) {
-  if (n > 0) k_host_gather<<<n, 128, 0, st>>>(src, d, dst);
+// TMA variant: one thread per CTA drives a ring of bulk copies (cp.async.bulk
+// global->shared completing on an mbarrier, then shared->global): the bus
+// reads are tracked by the CTA's bulk-copy engine instead of the LSU miss
+// queues the co-resident decode kernels use.  16-byte-aligned body via TMA,
+// the (< 16 B) tail and unaligned payloads by the other lanes.
+constexpr int kTmaChunk = 16384;
+constexpr int kTmaStages = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__global__ void __launch_bounds__(32) k_host_gather_tma(const uint8_t *src, const GatherDesc *desc,
+                                                        int n, uint8_t *dst) {
+  extern __shared__ __align__(128) uint8_t gbuf[];
+  __shared__ __align__(8) uint64_t bar[kTmaStages];
+  const int lane = threadIdx.x;
+  if (lane == 0) {
+    for (int i = 0; i < kTmaStages; i++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {  // tails / unaligned payloads: lanes 1..31
+    const GatherDesc d = desc[j];
+    const bool al = ((d.src | d.dst) & 15) == 0;
+    for (uint32_t i = (al ? d.len & ~15u : 0u) + lane; i < d.len; i += 32) dst[d.dst + i] = src[d.src + i];
+  }
+  if (lane != 0) return;
+  // issue cursor (ji, oi) runs up to kTmaStages chunks ahead of the store cursor (js, os)
+  int ji = blockIdx.x, js = blockIdx.x;
+  uint32_t oi = 0, os = 0, issued = 0, stored = 0;
+  auto body = [&](int j) -> uint32_t {
+    const GatherDesc d = desc[j];
+    return ((d.src | d.dst) & 15) == 0 ? (d.len & ~15u) : 0u;
+  };
+  auto advance = [&](int &jj, uint32_t &oo) {  // next chunk start (skips empty bodies)
+    while (jj < n && oo >= body(jj)) {
+      jj += gridDim.x;
+      oo = 0;
+    }
+  };
+  advance(ji, oi);
+  advance(js, os);
+  while (js < n) {
+    while (ji < n && issued - stored < (uint32_t)kTmaStages) {
+      const GatherDesc d = desc[ji];
+      const uint32_t bytes = min((uint32_t)kTmaChunk, body(ji) - oi);
+      const int st = issued % kTmaStages;
+      if (issued >= (uint32_t)kTmaStages)  // the store that last read this buffer is done
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      const uint32_t b = smem_u32(&bar[st]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(gbuf + st * kTmaChunk)),
+          "l"(src + d.src + oi), "r"(bytes), "r"(b)
+          : "memory");
+      issued++;
+      oi += bytes;
+      advance(ji, oi);
+    }
+    const GatherDesc d = desc[js];
+    const uint32_t bytes = min((uint32_t)kTmaChunk, body(js) - os);
+    const int st = stored % kTmaStages;
+    const uint32_t b = smem_u32(&bar[st]);
+    const uint32_t phase = (stored / kTmaStages) & 1;
+    asm volatile(
+        "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W_%=;\n}" ::"r"(b),
+        "r"(phase)
+        : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + d.dst + os),
+                 "r"(smem_u32(gbuf + st * kTmaChunk)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    stored++;
+    os += bytes;
+    advance(js, os);
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, int ctas,
+                        bool tma, cudaStream_t st) {
+  if (n <= 0) return;
+  const int grid = ctas > 0 && ctas < n ? ctas : n;
+  if (tma) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_host_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kTmaChunk * kTmaStages);
+      attr = true;
+    }
+    k_host_gather_tma<<<grid, 32, kTmaChunk * kTmaStages, st>>>(src, d, n, dst);
+  } else {
+    k_host_gather<<<grid, kGatherThreads, 0, st>>>(src, d, n, dst);
+  }
 }
 
 }  // namespace essl

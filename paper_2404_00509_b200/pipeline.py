@@ -107,7 +107,8 @@ class ImageBatch:
         return int(self.pixels.shape[0])
 
 
-_GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch", "streams")
+_GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch",
+             "streams", "staging")
 
 
 @dataclass
@@ -132,6 +133,10 @@ class LoaderConfig:
     rank: int = 0
     world_size: int = 1
     resident: bool = True
+    # host container (resident=False) payload path: "gather" = a few-CTA
+    # kernel reads the page-locked container over the bus; "copy" = host
+    # threads gather into a pinned ring, one copy-engine transfer per batch
+    staging: str = "gather"
     prefetch: int = 2
     streams: int = 2
     # Reuse a ring of output buffers (a batch's views stay valid while fewer
@@ -178,6 +183,8 @@ class LoaderConfig:
             raise ConfigError(f"out_dtype must be float32 or bfloat16, got {self.out_dtype!r}")
         if self.world_size < 1 or not 0 <= self.rank < self.world_size:
             raise ConfigError(f"bad rank/world_size {self.rank}/{self.world_size}")
+        if self.staging not in ("gather", "copy"):
+            raise ConfigError(f"staging must be gather or copy, got {self.staging!r}")
         if self.streams < 1 or self.prefetch < 1:
             raise ConfigError("streams and prefetch must be >= 1")
 
@@ -258,7 +265,10 @@ class Loader:
         self._crcs = np.ascontiguousarray(rec["checksum"], np.uint32)
         self._labels_np = rec["label"].astype(np.int64)
         self._blob = self.handle.to_device(self.device) if config.resident else None
-        self._pinned_base = self.handle.pinned_host() if not config.resident else 0
+        self._pinned_base = (self.handle.pinned_host()
+                             if not config.resident and config.staging == "gather" else 0)
+        self._host_base = (int(self.handle.bytes.ctypes.data)
+                           if not config.resident and config.staging == "copy" else 0)
         self._slots = [0] * len(self._engines)
         self._out_ring: dict = {}
         self._out_next = [0] * len(self._engines)
@@ -349,9 +359,14 @@ class Loader:
         samples, aug = self._descriptors(epoch, idxs)
         if self._blob is not None:
             blob_ptr = self._blob.data_ptr()
-        else:  # host container: one batched copy-engine gather from pinned memory
+        elif cfg.staging == "gather":  # host container read over the bus by k_host_gather
             blob_ptr = eng.stage_pinned(self._slots[j], self._pinned_base, samples["offset"],
                                         samples["length"].copy(), samples, stream=st)
+            self._slots[j] ^= 1
+        else:  # host threads -> pinned ring -> one copy-engine transfer
+            ptrs = samples["offset"] + np.uint64(self._host_base)
+            blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
+                                 nthreads=min(8, self.workers), stream=st)
             self._slots[j] ^= 1
         dev = self.device
         ring = self._rings[j]
@@ -440,23 +455,39 @@ class Loader:
                 tot[k] = (a + ms, b + n)
         return tot
 
-    def epoch(self, epoch: int):
-        """Yield the batches of one epoch (this rank's shard) in permutation order."""
+    def _plan(self, epoch: int):
         cfg = self.config
         perm = shard(epoch_permutation(cfg.seed, epoch, len(self.handle)), cfg.rank,
                      cfg.world_size)
         B = cfg.batch_size
-        starts = range(0, len(perm), B)
+        for s in range(0, len(perm), B):
+            yield epoch, perm[s:s + B]
+
+    def _run(self, plan):
+        """Keep `depth` batches in flight over the (epoch, indices) plan."""
         q: deque = deque()
-        it = iter(starts)
-        depth = max(cfg.prefetch, len(self._engines))
-        for s in it:
-            q.append(self.enqueue(epoch, perm[s:s + B]))
+        depth = max(self.config.prefetch, len(self._engines))
+        it = iter(plan)
+        for e, idxs in it:
+            q.append(self.enqueue(e, idxs))
             if len(q) >= depth:
                 break
         while q:
             p = q.popleft()
             nxt = next(it, None)
             if nxt is not None:
-                q.append(self.enqueue(epoch, perm[nxt:nxt + B]))
+                q.append(self.enqueue(*nxt))
             yield self.finish(p)
+
+    def epoch(self, epoch: int):
+        """Yield the batches of one epoch (this rank's shard) in permutation order."""
+        return self._run(self._plan(epoch))
+
+    def epochs(self, first: int, count: int | None = None):
+        """Batches of epochs first, first+1, ... (count of them, or without
+        end) with the prefetch pipeline kept full across epoch boundaries --
+        the same batches as consecutive epoch() calls, without the drain /
+        refill bubble at each boundary (a persistent-worker DataLoader)."""
+        import itertools
+        es = itertools.count(first) if count is None else range(first, first + count)
+        return self._run(itertools.chain.from_iterable(self._plan(e) for e in es))

@@ -315,15 +315,21 @@ def test_large_pool_vs_oracle(E, oracle, tmp_path, stage):
             assert np.array_equal(b.pixels.cpu().numpy(), pix)
 
 
-def test_staged_equals_resident(E, synth_sets):
-    path = synth_sets[0]
+@pytest.mark.parametrize("gather", [(8, 0), (0, 0), (3, 1), (8, 1), (0, 1)])
+def test_staged_equals_resident(E, synth_sets, gather):
+    """Host-container paths (bus-read gather: LSU or bulk-copy variant, few
+    or one-per-payload CTAs; host-thread copy) == the HBM-resident container."""
+    from paper_2404_00509_b200 import _native as N
     outs = []
-    for resident in (True, False):
-        cfg = E.LoaderConfig(data=str(path), batch_size=40, res=224, out_dtype="bfloat16",
-                             resident=resident, prefetch=3)
+    for resident, staging in ((True, "gather"), (False, "gather"), (False, "copy")):
+        cfg = E.LoaderConfig(data=str(synth_sets[2]), batch_size=40, res=224,
+                             out_dtype="bfloat16", resident=resident, prefetch=3,
+                             staging=staging)
         with E.Loader(cfg) as loader:
+            loader.set_option(N.ESSL_OPT_GATHER_CTAS, gather[0])
+            loader.set_option(N.ESSL_OPT_GATHER_TMA, gather[1])
             outs.append([sha(b.pixels) for b in loader.epoch(1)])
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2]
 
 
 def test_ddp_shards_cover_epoch(E, synth_sets):
@@ -339,3 +345,21 @@ def test_ddp_shards_cover_epoch(E, synth_sets):
     with E.Loader(cfg) as loader:
         full = {int(b.indices[s]): sha(b.pixels[s]) for b in loader.epoch(2) for s in range(len(b))}
     assert seen == full
+
+
+def test_multi_epoch_iterator_equals_epochs(E, synth_sets):
+    """Loader.epochs(first, count) keeps the pipeline full across epoch
+    boundaries and yields exactly the batches of consecutive epoch() calls."""
+    path = synth_sets[2]
+    cfg = E.LoaderConfig(data=str(path), batch_size=16, res=96, out_dtype="bfloat16",
+                         mask_ratio=0.75, prefetch=3, streams=3)
+    with E.Loader(cfg) as loader:
+        a = [(sha(b.pixels), sha(b.indices), sha(b.mask)) for e in (4, 5, 6)
+             for b in loader.epoch(e)]
+        b = [(sha(x.pixels), sha(x.indices), sha(x.mask)) for x in loader.epochs(4, 3)]
+        c = []
+        for x in loader.epochs(4):
+            c.append((sha(x.pixels), sha(x.indices), sha(x.mask)))
+            if len(c) == len(a):
+                break
+    assert a == b == c

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--pool", type=int, default=4096)
     ap.add_argument("--out", default=None)
     ap.add_argument("--host", action="store_true", help="pinned-container bus gather (resident=False)")
+    ap.add_argument("--gather-ctas", type=int, default=-1, help="ESSL_OPT_GATHER_CTAS (-1: default)")
+    ap.add_argument("--staging", default="gather", choices=["gather", "copy"])
+    ap.add_argument("--gather-tma", type=int, default=-1)
     args = ap.parse_args()
     import ctypes
 
@@ -37,9 +40,14 @@ def main():
     E.build_synthetic(path, args.pool, 256, 95, seed=3)
     cfg = E.LoaderConfig(data=str(path), batch_size=256, res=224, out_dtype="bfloat16",
                          mask_ratio=0.75, resident=not args.host, streams=args.streams,
+                         staging=args.staging,
                          prefetch=args.streams,
                          reuse_outputs=True)
     loader = E.Loader(cfg)
+    if args.gather_ctas >= 0:
+        loader.set_option(N.ESSL_OPT_GATHER_CTAS, args.gather_ctas)
+    if args.gather_tma >= 0:
+        loader.set_option(N.ESSL_OPT_GATHER_TMA, args.gather_tma)
     perm = E.epoch_permutation(0, 0, len(loader.handle))
     nb = len(perm) // 256
 
@@ -103,7 +111,8 @@ def main():
     per = {}
     for r in recs:
         per.setdefault(r["kernel"], []).append(r["end"] - r["start"])
-    summ = {"streams": args.streams, "steps": args.steps, "total_ms": total,
+    summ = {"streams": args.streams, "steps": args.steps, "host": args.host,
+            "gather_ctas": args.gather_ctas, "gather_tma": args.gather_tma, "staging": args.staging, "total_ms": total,
             "ms_per_step": total / args.steps, "gpu_busy_frac": busy / total,
             "concurrency_ms": {k: round(v, 3) for k, v in sorted(conc.items())},
             "kernel_mean_ms": {k: round(float(np.mean(v)), 4) for k, v in per.items()},
