@@ -69,6 +69,7 @@ extern "C" {
 #define ESSL_OPT_STAGE_BYTES 6  /* largest clean stream staged in shared memory (0: never) */
 #define ESSL_OPT_GATHER_CTAS 7  /* k_host_gather CTAs (bus-read gather; 0: one per payload) */
 #define ESSL_OPT_GATHER_TMA 8   /* 1: bus-read gather with bulk (TMA) copies */
+#define ESSL_OPT_DEBUG_LANES 9  /* 1: record per-lane speculative-decode state (essl_debug_lanes) */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0
@@ -161,6 +162,11 @@ int essl_ctx_profile_timeline(essl_ctx *ctx, int32_t *kid, double *t0_ms, double
  * (int64[16*n]: k_prep/k_entropy phase clocks, fixpoint iterations,
  * subsequence count | redo count << 32).  Synchronous. */
 int essl_debug_stats(essl_ctx *ctx, int64_t *out, int n);
+/* Debug: per-lane records of the last speculative decode (ESSL_OPT_DEBUG_LANES
+ * on), int32[n][64][8]: {nseq, phase-1 stop bit, stop block slot, checkpoints,
+ * phase-1 error, continuation stop bit, continuation status (0 merged,
+ * 1 error, 2 end of data), merge lane} (-1 where not run).  Synchronous. */
+int essl_debug_lanes(essl_ctx *ctx, int32_t *out, int n);
 const char *essl_last_error(void);
 const char *essl_version(void);
 

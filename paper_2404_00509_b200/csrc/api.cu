@@ -136,7 +136,8 @@ struct essl_ctx {
   int warm_bits = 2048;
   int stage_max = 64 * 1024;
   int gather_ctas = 8;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
-  bool gather_tma = false;  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
+  bool gather_tma = false;
+  int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
@@ -249,6 +250,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   p.warm_bits = c->warm_bits;
   p.stage_bytes = c->stage_max;
   p.results = results;
+  p.dbg_lanes = c->dbg_lanes;
   {
     Prof pr(c, ESSL_K_PREP, st);
     essl::launch_prep(p, st, max_len);
@@ -361,6 +363,7 @@ int essl_ctx_destroy(essl_ctx *c) {
     if (c->h_aug[r]) cudaFreeHost(c->h_aug[r]);
     if (c->d_aug[r]) cudaFree(c->d_aug[r]);
   }
+  if (c->dbg_lanes) cudaFree(c->dbg_lanes);
   if (c->aug_a) cudaFree(c->aug_a);
   if (c->aug_b) cudaFree(c->aug_b);
   for (int r = 0; r < 2; r++) {
@@ -400,6 +403,15 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       if (value < 0 || value > 65535) return fail(ESSL_E_ARG, "bad gather CTA count");
       c->gather_ctas = (int)value;
       return ESSL_OK;
+    case ESSL_OPT_DEBUG_LANES:
+      if (value && !c->dbg_lanes) {
+        CK(cudaMalloc(&c->dbg_lanes, sizeof(int32_t) * 8 * essl::kEntropyLanes * c->max_batch));
+        CK(cudaMemset(c->dbg_lanes, 0xFF, sizeof(int32_t) * 8 * essl::kEntropyLanes * c->max_batch));
+      } else if (!value && c->dbg_lanes) {
+        CK(cudaFree(c->dbg_lanes));
+        c->dbg_lanes = nullptr;
+      }
+      return ESSL_OK;
     case ESSL_OPT_GATHER_TMA:
       c->gather_tma = value != 0;
       return ESSL_OK;
@@ -421,6 +433,14 @@ int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
   std::vector<essl::ImgInfo> info(n);
   CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; i++) std::memcpy(out + 16 * i, info[i].dbg, 16 * sizeof(int64_t));
+  return ESSL_OK;
+}
+
+int essl_debug_lanes(essl_ctx *c, int32_t *out, int n) {
+  if (!c || !out || n < 0 || n > c->max_batch || !c->dbg_lanes)
+    return fail(ESSL_E_ARG, "essl_debug_lanes: bad arguments (ESSL_OPT_DEBUG_LANES off?)");
+  CK(cudaMemcpy(out, c->dbg_lanes, sizeof(int32_t) * 8 * essl::kEntropyLanes * n,
+                cudaMemcpyDeviceToHost));
   return ESSL_OK;
 }
 

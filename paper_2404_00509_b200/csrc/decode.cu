@@ -568,7 +568,9 @@ struct LaneRec {
 // every unit in the lane's list and recording a checkpoint at the first block
 // start after every ck_bits.  Lane 0 starts at the exact state, so an error
 // there is the reference's error; other lanes re-guess one bit later and drop
-// their list and checkpoints (the path before an error is not a decode path).
+// their list and checkpoints (the path before an error is not a decode path),
+// except at the end of the data (the fill bits after the final block), where
+// the lane simply stops.
 // Phase 2 (CONT=true): from the phase-1 stop state, decode on (appending to
 // the list) until the path reaches a checkpoint of a later lane with the same
 // (bit position, block-in-MCU) at a block start -- two decoders in the same
@@ -640,6 +642,11 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
           R.errp = r.p;
           break;
         }
+        // the last lane reading past the final block into the fill bits /
+        // 0xFF padding: its path ends here (keep its list and checkpoints --
+        // dropping them would leave nothing for the previous lane to merge
+        // into and run that lane's continuation over this whole subsequence)
+        if (r.p + 8 > C.cbits) break;
         r.init(r.p + 1);
         dbg_guess++;
         k = 0;
@@ -1737,6 +1744,12 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
     if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
     __syncthreads();
     dbg_cont = (uint32_t)S.red;
+    if (P.dbg_lanes) {
+      int32_t *o = P.dbg_lanes + ((size_t)img * kLanes + lane) * 8;
+      o[0] = nseq; o[1] = (int32_t)R.xp; o[2] = (int32_t)R.xb; o[3] = (int32_t)R.nck;
+      o[4] = R.err; o[5] = cont ? (int32_t)R.cp : -1; o[6] = cont ? R.cst : -1;
+      o[7] = cont ? (int32_t)R.cj : -1;
+    }
     PHASE(3);
     // resolution: follow the exact path from lane 0 through the merges
     if (lane == 0) {

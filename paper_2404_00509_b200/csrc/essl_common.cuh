@@ -79,6 +79,7 @@ struct DecodeParams {
   int stage_bytes;   // k_entropy read rings (0: plain global reads)
   int prep_part_off; // k_prep: byte offset of the CRC partials in dynamic smem
   essl_result *results;  // optional
+  int32_t *dbg_lanes;    // optional per-lane decode records [n][kEntropyLanes][8]
 };
 
 struct PixelParams {
