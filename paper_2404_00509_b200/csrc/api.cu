@@ -225,8 +225,11 @@ int ensure_aug_scratch(essl_ctx *c, uint64_t bytes) {
   return ESSL_OK;
 }
 
+// All of a batch's host->device copies are issued before its kernels: a copy
+// queued behind this batch's kernels would hold up the copies (and so the
+// kernels) of batches on other streams on the shared copy engine.
 int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
-               essl_result *results, cudaStream_t st, int *ring) {
+               essl_result *results, cudaStream_t st, int *ring, const essl_aug *aug = nullptr) {
   if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
   int max_len = 0;
   for (int i = 0; i < n; i++) {
@@ -238,6 +241,10 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   int r = pick_desc(c, samples, n, st, &d_desc);
   if (r < 0) return r;
   *ring = r;
+  if (aug) {
+    std::memcpy(c->h_aug[r], aug, sizeof(essl_aug) * n);
+    CK(cudaMemcpyAsync(c->d_aug[r], c->h_aug[r], sizeof(essl_aug) * n, cudaMemcpyHostToDevice, st));
+  }
   CK(cudaMemsetAsync(c->s.counters, 0, 4 * sizeof(unsigned long long), st));
   essl::DecodeParams p;
   p.blob = blob;
@@ -611,7 +618,8 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   }
   cudaStream_t st = (cudaStream_t)stream;
   int ring = -1;
-  int rc = run_decode(c, blob, samples, n, results, st, &ring);
+  const bool aug_out = any_aug && (out_kind != ESSL_OUT_NONE || out_u8);
+  int rc = run_decode(c, blob, samples, n, results, st, &ring, aug_out ? aug : nullptr);
   if (rc) return rc;
   essl::PixelParams pp;
   pp.info = c->s.info;
@@ -634,10 +642,7 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
     Prof pr(c, ESSL_K_RESIZE, st);
     essl::launch_resize(pp, st);
   }
-  if (any_aug && (out_kind != ESSL_OUT_NONE || out_u8)) {
-    std::memcpy(c->h_aug[ring], aug, sizeof(essl_aug) * n);
-    CK(cudaMemcpyAsync(c->d_aug[ring], c->h_aug[ring], sizeof(essl_aug) * n,
-                       cudaMemcpyHostToDevice, st));
+  if (aug_out) {
     essl::AugOutParams ap{c->aug_a, c->aug_b, c->d_aug[ring], n, res, res, out_kind, out,
                           out_stride, out_u8};
     Prof pr(c, ESSL_K_AUG, st);

@@ -937,86 +937,101 @@ __device__ __forceinline__ int grp_max8(int v) {
 
 // Must be called by all 32 lanes of a warp (lanes with valid=false idle).
 // blk: the block's 64 coefficients (natural order, int32, shared memory).
-__device__ void idct_block_8lanes(bool valid, const int32_t *blk, const int32_t *q, uint8_t *dst,
-                                  int pitch, int32_t *tr /* 64 ints per 8-lane group */) {
+__device__ __forceinline__ void idct_pass2_64(const int64_t w64[8], int32_t *tr, uint32_t &lo,
+                                              uint32_t &hi) {
+  // int64 transpose through two 32-bit halves, then the int64 row pass
+  const int j = threadIdx.x & 7;
+  int64_t x[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(uint32_t)(w64[r] & 0xFFFFFFFF);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; i++) x[i] = (uint32_t)tr[j * 8 + i];
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(w64[r] >> 32);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; i++) x[i] |= (int64_t)tr[j * 8 + i] << 32;
+  __syncwarp();
+  lo = hi = 0;
+  if (!(x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7])) {
+    int64_t v = ((x[0] + 16) >> 5) + 128;
+    uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+    lo = hi = u * 0x01010101u;
+  } else {
+    int64_t o[8];
+    idct_1d<int64_t>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], o, 131072, 18);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      int64_t v = o[i] + 128;
+      uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+      if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
+    }
+  }
+}
+
+// Must be called by all 32 lanes of a warp (lanes with valid=false idle).
+// blk: the block's 64 dequantised coefficients (natural order, int32,
+// shared memory).
+__device__ void idct_block_8lanes(bool valid, const int32_t *blk, uint8_t *dst, int pitch,
+                                  int32_t *tr /* 64 ints per 8-lane group */) {
   const int j = threadIdx.x & 7;
   int32_t d[8];
   int mabs = 0;
 #pragma unroll
   for (int r = 0; r < 8; r++) {
-    d[r] = valid ? blk[8 * r + j] * q[8 * r + j] : 0;
+    d[r] = valid ? blk[8 * r + j] : 0;
     mabs = max(mabs, abs(d[r]));
   }
   const bool wide1 = grp_max8(mabs) > kIdctMax1;
-  int64_t w64[8];
-  int32_t w[8];
-  if (!(d[1] | d[2] | d[3] | d[4] | d[5] | d[6] | d[7])) {  // DC-only column (exact shortcut)
-#pragma unroll
-    for (int r = 0; r < 8; r++) { w64[r] = (int64_t)d[0] * 4; }
-  } else if (!wide1) {
-    int32_t o[8];
-    idct_1d<int32_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], o, 1024, 11);
-#pragma unroll
-    for (int r = 0; r < 8; r++) w64[r] = o[r];
-  } else {
-    idct_1d<int64_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], w64, 1024, 11);
-  }
-  int64_t m2 = 0;
-#pragma unroll
-  for (int r = 0; r < 8; r++) m2 = max(m2, w64[r] < 0 ? -w64[r] : w64[r]);
-  const bool wide2 = grp_max8(m2 > kIdctMax2 ? kIdctMax2 + 1 : (int)m2) > kIdctMax2;
   uint32_t lo = 0, hi = 0;
-  if (!wide2) {
-    // transpose: column j -> tr[r*8 + j]
+  if (!wide1) {
+    // int32 column pass (exact: |input| <= kIdctMax1)
+    int32_t w[8];
+    if (!(d[1] | d[2] | d[3] | d[4] | d[5] | d[6] | d[7])) {  // DC-only column (exact shortcut)
 #pragma unroll
-    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)w64[r];
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; i++) w[i] = tr[j * 8 + i];
-    __syncwarp();
-    if (!(w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7])) {
-      int v = ((w[0] + 16) >> 5) + 128;
-      uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
-      lo = hi = u * 0x01010101u;
+      for (int r = 0; r < 8; r++) w[r] = d[0] * 4;
     } else {
-      int32_t o[8];
-      idct_1d<int32_t>(w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], o, 131072, 18);
+      idct_1d<int32_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], w, 1024, 11);
+    }
+    int m2 = 0;
 #pragma unroll
-      for (int i = 0; i < 8; i++) {
-        int v = o[i] + 128;
+    for (int r = 0; r < 8; r++) m2 = max(m2, abs(w[r]));
+    if (grp_max8(m2) <= kIdctMax2) {
+      // transpose: column j -> tr[r*8 + j]; int32 row pass
+#pragma unroll
+      for (int r = 0; r < 8; r++) tr[r * 8 + j] = w[r];
+      __syncwarp();
+      int32_t x[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) x[i] = tr[j * 8 + i];
+      __syncwarp();
+      if (!(x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7])) {
+        int v = ((x[0] + 16) >> 5) + 128;
         uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
-        if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
+        lo = hi = u * 0x01010101u;
+      } else {
+        int32_t o[8];
+        idct_1d<int32_t>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], o, 131072, 18);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          int v = o[i] + 128;
+          uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
+          if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
+        }
       }
+    } else {
+      int64_t w64[8];
+#pragma unroll
+      for (int r = 0; r < 8; r++) w64[r] = w[r];
+      idct_pass2_64(w64, tr, lo, hi);
     }
   } else {
-    // int64 transpose through two 32-bit halves
-    int64_t x[8];
-#pragma unroll
-    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(uint32_t)(w64[r] & 0xFFFFFFFF);
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; i++) x[i] = (uint32_t)tr[j * 8 + i];
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 8; r++) tr[r * 8 + j] = (int32_t)(w64[r] >> 32);
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 8; i++) x[i] |= (int64_t)tr[j * 8 + i] << 32;
-    __syncwarp();
-    if (!(x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7])) {
-      int64_t v = ((x[0] + 16) >> 5) + 128;
-      uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
-      lo = hi = u * 0x01010101u;
-    } else {
-      int64_t o[8];
-      idct_1d<int64_t>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], o, 131072, 18);
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        int64_t v = o[i] + 128;
-        uint32_t u = (uint32_t)(v < 0 ? 0 : v > 255 ? 255 : v);
-        if (i < 4) lo |= u << (8 * i); else hi |= u << (8 * (i - 4));
-      }
-    }
+    // the reference's unbounded ints: int64 column pass, int64 row pass
+    int64_t w64[8];
+    idct_1d<int64_t>(d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], w64, 1024, 11);
+    idct_pass2_64(w64, tr, lo, hi);
   }
   if (valid) *reinterpret_cast<uint2 *>(dst + (int64_t)j * pitch) = make_uint2(lo, hi);
 }
@@ -1961,9 +1976,10 @@ constexpr int kIdctCtas = 8;
 // natural order, shared memory).  fmt 1: the block's table entry points at its
 // DC entry in a unit list; its AC units follow up to the next DC-flagged entry
 // (eight lanes read eight consecutive entries per round).  fmt 0: the int16
-// coefficient window.  Called by all 32 lanes of a warp.
+// coefficient window.  dq: dequantise on the way (k_idct) or raw (nullptr).
+// Called by all 32 lanes of a warp.
 __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, int c, int byr,
-                              int bxr, int32_t *blk, const uint8_t *zz) {
+                              int bxr, int32_t *blk, const uint8_t *zz, const int32_t *dq) {
   const int j = threadIdx.x & 7;
   const int16_t *cf = sc.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
 #pragma unroll
@@ -1972,14 +1988,14 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
   if (I.fmt == 0) {
     if (valid) {
 #pragma unroll
-      for (int r = 0; r < 8; r++) blk[8 * r + j] = cf[8 * r + j];
+      for (int r = 0; r < 8; r++) blk[8 * r + j] = dq ? cf[8 * r + j] * dq[8 * r + j] : cf[8 * r + j];
     }
     __syncwarp();
     return;
   }
   uint2 t = make_uint2(0, 0);
   if (valid) t = *reinterpret_cast<const uint2 *>(cf);
-  if (valid && j == 0) blk[0] = (int32_t)t.y;
+  if (valid && j == 0) blk[0] = dq ? (int32_t)t.y * dq[0] : (int32_t)t.y;
   // The block's AC units follow its DC entry up to the next DC-flagged
   // entry.  Each round the group reads 32 consecutive entries as eight
   // 16-byte loads (lists are 16-byte aligned per lane; most blocks end in the
@@ -2008,7 +2024,10 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
 #pragma unroll
     for (int u = 0; u < 4; u++) {
       const uint32_t idx = base + 4 * j + u;
-      if (!done && idx >= i0 && idx < stop) blk[zz[(e4[u] >> 20) & 63]] = entry_value(e4[u]);
+      if (!done && idx >= i0 && idx < stop) {
+        const int nat = zz[(e4[u] >> 20) & 63];
+        blk[nat] = dq ? entry_value(e4[u]) * dq[nat] : entry_value(e4[u]);
+      }
     }
     done = done || any != 0;
     base += 32;
@@ -2030,10 +2049,14 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
   for (int e = tid; e < ncomp * 64; e += 256) q[e >> 6][e & 63] = G->q[e >> 6][e & 63];
   if (tid < 64) s_zz[tid] = c_zz[tid];
   int nb[3] = {0, 0, 0}, wb[3] = {1, 1, 1};
-  for (int c = 0; c < ncomp; c++) {
+  uint32_t mg[3] = {0, 0, 0};  // ceil(2^32 / w), w >= 2: jb / w == umulhi(jb, mg) for jb * w < 2^31
+#pragma unroll
+  for (int c = 0; c < 3; c++) {
+    if (c >= ncomp) break;
     const int hb = min(I.wby0[c] + I.wbh[c], G->bh[c]) - I.wby0[c];
     const int w = min(I.wbx0[c] + I.wbw[c], G->bw[c]) - I.wbx0[c];
     if (hb > 0 && w > 0) { nb[c] = hb * w; wb[c] = w; }
+    mg[c] = (uint32_t)((0x100000000ull + (uint64_t)wb[c] - 1) / (uint64_t)wb[c]);
   }
   __syncthreads();
   const int total = nb[0] + nb[1] + nb[2];
@@ -2046,11 +2069,15 @@ __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
     if (valid) {
       if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
     }
-    const int byr = valid ? jb / wb[c] : 0, bxr = valid ? jb % wb[c] : 0;
-    gather_block8(valid, I, P.s, c, byr, bxr, blk, s_zz);
+    // (selects, not indexing: keeps the small arrays in registers)
+    const uint32_t m = c == 0 ? mg[0] : (c == 1 ? mg[1] : mg[2]);
+    const int w = c == 0 ? wb[0] : (c == 1 ? wb[1] : wb[2]);
+    const int byr = valid ? (w == 1 ? jb : (int)__umulhi((uint32_t)jb, m)) : 0;  // (2^32 / 1 overflows)
+    const int bxr = valid ? jb - byr * w : 0;
+    gather_block8(valid, I, P.s, c, byr, bxr, blk, s_zz, q[c]);  // dequantised
     const int pitch = I.plane_pitch[c];
     uint8_t *dst = P.s.plane + I.plane_off[c] + (uint64_t)byr * 8 * pitch + bxr * 8;
-    idct_block_8lanes(valid, blk, q[c], dst, pitch, t);
+    idct_block_8lanes(valid, blk, dst, pitch, t);
   }
 }
 
@@ -2078,7 +2105,7 @@ __global__ void __launch_bounds__(256) k_dump_coefs(Scratch sc, int16_t *out, co
       if (jb >= nb[0]) { jb -= nb[0]; c = 1; if (jb >= nb[1]) { jb -= nb[1]; c = 2; } }
     }
     const int w = max(I.wbw[c], 1);
-    gather_block8(valid, I, sc, c, valid ? jb / w : 0, valid ? jb % w : 0, blk, s_zz);
+    gather_block8(valid, I, sc, c, valid ? jb / w : 0, valid ? jb % w : 0, blk, s_zz, nullptr);
     if (valid) {
       int16_t *o = out + offsets[img] + (uint64_t)jall * 64;
       const int j = tid & 7;

@@ -48,14 +48,30 @@ struct PlaneSrc {
   // RGB of image pixel (sy, sx): replication upsampling + fixed-point
   // YCbCr->RGB (decode_kernels.py:551-576), gray replicated (579-589).
   __device__ __forceinline__ void rgb(int sy, int sx, int &r, int &g, int &b) const {
+    int ro[3], co[3];
+    row_off(sy, ro);
+    col_off(sx, co);
+    rgb_at(ro, co, r, g, b);
+  }
+  // sy * v / vmax and sx * h / hmax with vmax, hmax powers of two
+  // (decode_kernels.py:551-558), split into a row part and a column part
+  __device__ __forceinline__ void row_off(int sy, int ro[3]) const {
+#pragma unroll
+    for (int c = 0; c < 3; c++) ro[c] = (((sy * v[c]) >> lv) - oy[c]) * pitch[c];
+  }
+  __device__ __forceinline__ void col_off(int sx, int co[3]) const {
+#pragma unroll
+    for (int c = 0; c < 3; c++) co[c] = ((sx * h[c]) >> lh) - ox[c];
+  }
+  __device__ __forceinline__ void rgb_at(const int ro[3], const int co[3], int &r, int &g,
+                                         int &b) const {
+    const int yv = p[0][ro[0] + co[0]];
     if (ncomp == 1) {
-      r = g = b = p[0][(sy - oy[0]) * pitch[0] + (sx - ox[0])];
+      r = g = b = yv;
       return;
     }
-    // sy * v / vmax with vmax a power of two (decode_kernels.py:551-558)
-    const int yv = p[0][(((sy * v[0]) >> lv) - oy[0]) * pitch[0] + (((sx * h[0]) >> lh) - ox[0])];
-    const int cb = (int)p[1][(((sy * v[1]) >> lv) - oy[1]) * pitch[1] + (((sx * h[1]) >> lh) - ox[1])] - 128;
-    const int cr = (int)p[2][(((sy * v[2]) >> lv) - oy[2]) * pitch[2] + (((sx * h[2]) >> lh) - ox[2])] - 128;
+    const int cb = (int)p[1][ro[1] + co[1]] - 128;
+    const int cr = (int)p[2][ro[2] + co[2]] - 128;
     r = clamp255(yv + ((91881 * cr + 32768) >> 16));
     g = clamp255(yv + ((-22554 * cb - 46802 * cr + 32768) >> 16));
     b = clamp255(yv + ((116130 * cb + 32768) >> 16));
@@ -152,21 +168,31 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
   PlaneSrc S;
   S.load(I, P.plane);
-  // four source pixels per thread per round: their plane loads are
-  // independent, so they are in flight together
-  const int total = nrows * iw;
-  for (int e0 = threadIdx.x; e0 < total; e0 += 4 * kPixThreads) {
-    int rr[4], gg[4], bb[4];
+  // source rows -> RGBX words.  Each thread keeps one column (its plane
+  // column offsets fixed) and walks rows, four in flight; no per-pixel
+  // division.
+  {
+    const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
+    const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
+    const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
+    if (r0 < rpp) {
+      for (int x = x0; x < iw; x += cpr) {
+        int co[3];
+        S.col_off(I.rx + x, co);
+        for (int r = r0; r < nrows; r += 4 * rpp) {
+          int rr[4], gg[4], bb[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int e = min(e0 + u * kPixThreads, total - 1);
-      const int r = e / iw, x = e - r * iw;
-      S.rgb(I.ry + ys0 + r, I.rx + x, rr[u], gg[u], bb[u]);
-    }
+          for (int u = 0; u < 4; u++) {
+            int ro[3];
+            S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
+            S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
+          }
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int e = e0 + u * kPixThreads;
-      if (e < total) src[e] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+          for (int u = 0; u < 4; u++)
+            if (r + u * rpp < nrows)
+              src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+        }
+      }
     }
   }
   // row taps of the band (imgops.py:37-41), shared by every column
@@ -184,31 +210,44 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   // column the horizontal lerps top = (1-wx)*s(y,x0) + wx*s(y,x1) of the
   // source rows y0/y1 (imgops.py:49-52) are kept in registers and reused
   // while consecutive output rows share them; per output row only the
-  // vertical (1-wy)*top + wy*bot + 0.5 (imgops.py:53-56).  Small outputs
-  // split the band's rows over groups of threads.
-  const int ng = res >= kPixThreads ? 1 : kPixThreads / res;
-  const int g = ng > 1 ? threadIdx.x / res : 0;
-  const int cstart = ng > 1 ? threadIdx.x % res : threadIdx.x;
-  const int cstep = ng > 1 ? res : kPixThreads;
+  // vertical (1-wy)*top + wy*bot + 0.5 (imgops.py:53-56).  A thread owns a
+  // pair of adjacent output columns (paired bf16 / f32 stores); small
+  // outputs split the band's rows over groups of threads.
+  const int npair = (res + 1) >> 1;
+  const int ng = npair >= kPixThreads ? 1 : kPixThreads / npair;
+  const int g = ng > 1 ? threadIdx.x / npair : 0;
+  const int cstart = ng > 1 ? threadIdx.x % npair : threadIdx.x;
+  const int cstep = ng > 1 ? npair : kPixThreads;
   const int rpg = (ob1 - ob0 + ng - 1) / ng;
   const int rb = g * rpg, re = min(ob1 - ob0, rb + rpg);
   const int64_t plane_sz = (int64_t)res * res;
   const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
+  // paired stores need an even element offset for every (image, plane, row)
+  const bool pair_ok = (res & 1) == 0 && (stride & 1) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
   if (g >= ng) return;
-  for (int ox = cstart; ox < res; ox += cstep) {
-    const int xs = I.flip ? res - 1 - ox : ox;  // hflip after resize
-    int x0, x1;
-    double wx;
-    tap(xs, sx, iw, x0, x1, wx);
-    const double ax = __dsub_rn(1.0, wx);
-    int cy0 = -1, cy1 = -1;
-    double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
-    auto hrow = [&](int y, double h[3]) {
-      const uint32_t a0 = src[y * iw + x0], a1 = src[y * iw + x1];
+  for (int q = cstart; q < npair; q += cstep) {
+    const int oxa = 2 * q;
+    const bool two = oxa + 1 < res;
+    int x0[2], x1[2];
+    double wx[2], ax[2];
 #pragma unroll
-      for (int c = 0; c < 3; c++)
-        h[c] = __dadd_rn(__dmul_rn(ax, (double)((a0 >> (8 * c)) & 255)),
-                         __dmul_rn(wx, (double)((a1 >> (8 * c)) & 255)));
+    for (int j = 0; j < 2; j++) {
+      const int ox = min(oxa + j, res - 1);
+      tap(I.flip ? res - 1 - ox : ox, sx, iw, x0[j], x1[j], wx[j]);  // hflip after resize
+      ax[j] = __dsub_rn(1.0, wx[j]);
+    }
+    int cy0 = -1, cy1 = -1;
+    double h0[2][3], h1[2][3];
+    auto hrow = [&](int y, double h[2][3]) {
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const uint32_t a0 = src[y * iw + x0[j]], a1 = src[y * iw + x1[j]];
+#pragma unroll
+        for (int c = 0; c < 3; c++)
+          h[j][c] = __dadd_rn(__dmul_rn(ax[j], (double)((a0 >> (8 * c)) & 255)),
+                              __dmul_rn(wx[j], (double)((a1 >> (8 * c)) & 255)));
+      }
     };
     for (int r = rb; r < re; r++) {
       const int2 yy = ry[r];
@@ -216,7 +255,9 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
       if (yy.x != cy0) {  // (uniform across the CTA's columns: no divergence)
         if (yy.x == cy1) {
 #pragma unroll
-          for (int c = 0; c < 3; c++) h0[c] = h1[c];
+          for (int j = 0; j < 2; j++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) h0[j][c] = h1[j][c];
         } else {
           hrow(yy.x, h0);
         }
@@ -225,34 +266,62 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
       if (yy.y != cy1) {
         if (yy.y == cy0) {
 #pragma unroll
-          for (int c = 0; c < 3; c++) h1[c] = h0[c];
+          for (int j = 0; j < 2; j++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) h1[j][c] = h0[j][c];
         } else {
           hrow(yy.y, h1);
         }
         cy1 = yy.y;
       }
-      int px[3];
+      int px[2][3];
 #pragma unroll
-      for (int c = 0; c < 3; c++) {
-        const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, h0[c]), __dmul_rn(wy, h1[c])), 0.5);
-        const int iv = __double2int_rz(v);
-        px[c] = iv > 255 ? 255 : iv;
-      }
+      for (int j = 0; j < 2; j++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, h0[j][c]), __dmul_rn(wy, h1[j][c])), 0.5);
+          const int iv = __double2int_rz(v);
+          px[j][c] = iv > 255 ? 255 : iv;
+        }
       const int oy = ob0 + r;
-      const int64_t o = img * stride + (int64_t)oy * res + ox;
+      const int64_t o = img * stride + (int64_t)oy * res + oxa;
       if (P.out_kind == ESSL_OUT_BF16_NCHW) {
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
+        if (pair_ok) {
 #pragma unroll
-        for (int c = 0; c < 3; c++) out[c * plane_sz] = lutb[c][px[c]];
+          for (int c = 0; c < 3; c++) {
+            const uint32_t lo = __bfloat16_as_ushort(lutb[c][px[0][c]]);
+            const uint32_t hi = __bfloat16_as_ushort(lutb[c][px[1][c]]);
+            *reinterpret_cast<uint32_t *>(out + c * plane_sz) = lo | (hi << 16);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            out[c * plane_sz] = lutb[c][px[0][c]];
+            if (two) out[c * plane_sz + 1] = lutb[c][px[1][c]];
+          }
+        }
       } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
         float *out = reinterpret_cast<float *>(P.out) + o;
+        if (pair_ok) {
 #pragma unroll
-        for (int c = 0; c < 3; c++) out[c * plane_sz] = lut[c][px[c]];
+          for (int c = 0; c < 3; c++)
+            *reinterpret_cast<float2 *>(out + c * plane_sz) = make_float2(lut[c][px[0][c]], lut[c][px[1][c]]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            out[c * plane_sz] = lut[c][px[0][c]];
+            if (two) out[c * plane_sz + 1] = lut[c][px[1][c]];
+          }
+        }
       }
       if (P.out_u8) {
-        uint8_t *out = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + ox) * 3;
+        uint8_t *out = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
 #pragma unroll
-        for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[c];
+        for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[0][c];
+        if (two)
+#pragma unroll
+          for (int c = 0; c < 3; c++) out[3 + c] = (uint8_t)px[1][c];
       }
     }
   }

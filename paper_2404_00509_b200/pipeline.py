@@ -396,7 +396,8 @@ class Loader:
         u8 = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
         results = eng.new_results(b)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
-        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st, aug=aug)
+        # host->device copies first: a copy queued behind this batch's kernels
+        # would hold up later batches' copies on the shared copy engine
         hidx, hlab, res_host = ring.idx[slot][:b], ring.lab[slot][:b], ring.res[slot][:b]
         hidx.numpy()[:] = idxs
         hlab.numpy()[:] = self._labels_np[idxs]
@@ -405,6 +406,7 @@ class Loader:
             labels = out("labels", (b,), torch.int64)
             indices.copy_(hidx, non_blocking=True)
             labels.copy_(hlab, non_blocking=True)
+        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st, aug=aug)
         mask = keep = restore = None
         if self.mask_spec is not None:
             mask = out("mask", (b, k), torch.int32)

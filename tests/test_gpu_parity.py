@@ -363,3 +363,24 @@ def test_multi_epoch_iterator_equals_epochs(E, synth_sets):
             if len(c) == len(a):
                 break
     assert a == b == c
+
+
+@pytest.mark.parametrize("res", [97, 16, 300])
+def test_odd_and_extreme_resolutions_vs_oracle(E, oracle, synth_sets, res):
+    """Output sizes off the paired-store fast path (odd), tiny, and larger than
+    the crop (upscale, > the CTA's column count): float32 and the uint8 view
+    bit-exact, bf16 the RNE of the float32."""
+    import torch
+    path = synth_sets[2]
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=20, res=res, keep_uint8=True)
+        cfg16 = E.LoaderConfig(data=str(path), batch_size=20, res=res, out_dtype="bfloat16")
+        l32, l16 = E.Loader(cfg, container=h), E.Loader(cfg16, container=h)
+        for b, b16 in zip(l32.epoch(5), l16.epoch(5)):
+            idx = b.indices.cpu().numpy()
+            pix, u8, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 5, res,
+                                                 keep_uint8=True, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
+            assert torch.equal(b16.pixels, b.pixels.to(torch.bfloat16))

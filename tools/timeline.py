@@ -124,6 +124,15 @@ def main():
         rs = [r for r in recs if r["stream"] == s]
         gaps = [rs[i + 1]["start"] - rs[i]["end"] for i in range(len(rs) - 1)]
         print(f"stream {s}: launches {len(rs)}, gap mean {np.mean(gaps):.3f} ms, max {np.max(gaps):.3f} ms")
+    # gaps by transition (previous kernel -> next kernel on the same stream)
+    trans = {}
+    for st_ in range(args.streams):
+        rs = [r for r in recs if r["stream"] == st_]
+        for i in range(len(rs) - 1):
+            key = rs[i]["kernel"] + "->" + rs[i + 1]["kernel"]
+            trans.setdefault(key, []).append(rs[i + 1]["start"] - rs[i]["end"])
+    print("gaps by transition (ms):", {k: (round(float(np.mean(v)), 4), round(float(np.max(v)), 4), len(v))
+                                       for k, v in trans.items()})
     mid = len(recs) // 2
     for r in recs[mid:mid + 50]:
         print(f"  s{r['stream']} {r['kernel']:8s} {r['start']:8.3f} {r['end']:8.3f} ({r['end'] - r['start']:.3f})")
