@@ -259,6 +259,8 @@ def run_gpu(args, wl):
         loader.set_option(N.ESSL_OPT_SEQ_BITS, args.seq_bits)
     if args.warm_bits >= 0:
         loader.set_option(N.ESSL_OPT_WARMUP_BITS, args.warm_bits)
+    if args.stage_bytes >= 0:
+        loader.set_option(N.ESSL_OPT_STAGE_BYTES, args.stage_bytes)
     handle = loader.handle
     perm_epochs = {}
 
@@ -448,6 +450,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
+    ap.add_argument("--stage-bytes", type=int, default=-1,
+                    help="ESSL_OPT_STAGE_BYTES (0: entropy lanes read the clean stream from global)")
     ap.add_argument("--streams", type=int, default=6,
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--aug", default="simple", choices=["simple", "3aug", "3aug+"],

@@ -369,6 +369,7 @@ struct Reader {
   int n;              // valid bits in buf
   uint32_t wi;        // index of the next word to load
   uint32_t p;         // absolute bit position of buf's MSB
+  uint32_t nx0, nx1;  // global path: words wi, wi + 1, loaded ahead
   __device__ __forceinline__ uint32_t ld(uint32_t i) const {
     if (SH) return lds_u32(rs + ((i & 15) << 2));
     return __ldg(w + min(i, wmax));
@@ -409,6 +410,10 @@ struct Reader {
     n = 64 - off;
     wi = i + 2;
     p = pos;
+    if (!SH) {
+      nx0 = ld(wi);
+      nx1 = ld(wi + 1);
+    }
     // the ring holds chunks c..c+3 with c = 2*(i/8); if wi already entered
     // the next pair, its crossing fetch (c+4, c+5) is due now
     if (SH && (wi & ~7u) != (i & ~7u)) issue_pair((wi >> 2) + 2, true);
@@ -425,10 +430,16 @@ struct Reader {
       wi += rf ? 1u : 0u;
       const bool cross = rf && (wi & 7) == 0;  // entered an even chunk
       if (__any_sync(__activemask(), cross)) issue_pair((wi >> 2) + 2, cross);
-    } else if (n <= 32) {
-      buf |= (uint64_t)ld(wi) << (32 - n);
-      n += 32;
-      wi++;
+    } else {
+      // two words loaded ahead in registers: a load has ~8 units to land
+      const bool rf = n <= 32;
+      buf |= rf ? (uint64_t)nx0 << (32 - n) : 0ull;
+      n += rf ? 32 : 0;
+      if (rf) {
+        wi++;
+        nx0 = nx1;
+        nx1 = ld(wi + 1);
+      }
     }
   }
   __device__ __forceinline__ uint32_t hi() const { return (uint32_t)(buf >> 32); }
