@@ -8,9 +8,11 @@ entry point raises ``NativeUnavailable``.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libessl.so"
+# ESSL_LIB: an alternative build of the library (A/B experiments, tools/ab.py)
+LIB_PATH = Path(os.environ.get("ESSL_LIB") or Path(__file__).resolve().parent / "_lib" / "libessl.so")
 
 ESSL_OK = 0
 ESSL_OUT_BF16_NCHW, ESSL_OUT_F32_NCHW, ESSL_OUT_NONE = 0, 1, 2
