@@ -70,6 +70,7 @@ extern "C" {
 #define ESSL_OPT_GATHER_CTAS 7  /* k_host_gather CTAs (bus-read gather; 0: one per payload) */
 #define ESSL_OPT_GATHER_TMA 8   /* 1: bus-read gather with bulk (TMA) copies */
 #define ESSL_OPT_DEBUG_LANES 9  /* 1: record per-lane speculative-decode state (essl_debug_lanes) */
+#define ESSL_OPT_TRACE 10       /* n > 0: record up to n CTA executions (essl_trace_read); 0 off */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0
@@ -167,6 +168,11 @@ int essl_debug_stats(essl_ctx *ctx, int64_t *out, int n);
  * phase-1 error, continuation stop bit, continuation status (0 merged,
  * 1 error, 2 end of data), merge lane} (-1 where not run).  Synchronous. */
 int essl_debug_lanes(essl_ctx *ctx, int32_t *out, int n);
+/* Debug: CTA execution records since the last read (ESSL_OPT_TRACE on),
+ * uint64[max][4] = {start ns, end ns (globaltimer), kernel id (ESSL_K_*),
+ * SM id} for k_prep / k_entropy / k_idct / k_resize.  Synchronises the
+ * device; returns the number of records written. */
+int essl_trace_read(essl_ctx *ctx, uint64_t *out, int max);
 const char *essl_last_error(void);
 const char *essl_version(void);
 

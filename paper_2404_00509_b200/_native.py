@@ -23,6 +23,7 @@ ESSL_OPT_STAGE_BYTES = 6
 ESSL_OPT_GATHER_CTAS = 7
 ESSL_OPT_GATHER_TMA = 8
 ESSL_OPT_DEBUG_LANES = 9
+ESSL_OPT_TRACE = 10
 KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep", "entropy", "idct",
            "stage", "aug")
 ESSL_AUG_SIMPLE, ESSL_AUG_3AUG, ESSL_AUG_3AUG_PLUS = 0, 1, 2
@@ -40,6 +41,7 @@ EXPORTS = (
     "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
     "essl_mask_count", "essl_encode_jpeg", "essl_synth_image", "essl_decode_rrc_aug",
     "essl_augment_u8", "essl_aug_draw", "essl_aug_batch", "essl_debug_lanes",
+    "essl_trace_read",
 )
 
 
@@ -124,6 +126,7 @@ def lib():
         "essl_ctx_profile_timeline": (i32, [P, P, P, P, i32]),
         "essl_debug_stats": (i32, [P, P, i32]),
         "essl_debug_lanes": (i32, [P, P, i32]),
+        "essl_trace_read": (i32, [P, P, i32]),
         "essl_last_error": (ctypes.c_char_p, []),
         "essl_version": (ctypes.c_char_p, []),
         "essl_stage": (i32, [P, i32, P, P, i32, P, i32, P, P]),

@@ -137,7 +137,8 @@ struct essl_ctx {
   int stage_max = 64 * 1024;
   int gather_ctas = 8;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
   bool gather_tma = false;
-  int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
+  int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
+  essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
@@ -258,6 +259,7 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
   p.stage_bytes = c->stage_max;
   p.results = results;
   p.dbg_lanes = c->dbg_lanes;
+  p.trace = c->trace;
   {
     Prof pr(c, ESSL_K_PREP, st);
     essl::launch_prep(p, st, max_len);
@@ -371,6 +373,7 @@ int essl_ctx_destroy(essl_ctx *c) {
     if (c->d_aug[r]) cudaFree(c->d_aug[r]);
   }
   if (c->dbg_lanes) cudaFree(c->dbg_lanes);
+  if (c->trace.buf) { cudaFree(c->trace.buf); cudaFree(c->trace.count); }
   if (c->aug_a) cudaFree(c->aug_a);
   if (c->aug_b) cudaFree(c->aug_b);
   for (int r = 0; r < 2; r++) {
@@ -410,6 +413,20 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       if (value < 0 || value > 65535) return fail(ESSL_E_ARG, "bad gather CTA count");
       c->gather_ctas = (int)value;
       return ESSL_OK;
+    case ESSL_OPT_TRACE:
+      if (c->trace.buf) {
+        CK(cudaFree(c->trace.buf));
+        CK(cudaFree(c->trace.count));
+        c->trace = essl::CtaTrace{nullptr, nullptr, 0};
+      }
+      if (value > 0) {
+        if (value > (1 << 24)) return fail(ESSL_E_ARG, "trace capacity too large");
+        CK(cudaMalloc(&c->trace.buf, sizeof(unsigned long long) * 4 * (size_t)value));
+        CK(cudaMalloc(&c->trace.count, sizeof(unsigned int)));
+        CK(cudaMemset(c->trace.count, 0, sizeof(unsigned int)));
+        c->trace.cap = (unsigned int)value;
+      }
+      return ESSL_OK;
     case ESSL_OPT_DEBUG_LANES:
       if (value && !c->dbg_lanes) {
         CK(cudaMalloc(&c->dbg_lanes, sizeof(int32_t) * 8 * essl::kEntropyLanes * c->max_batch));
@@ -441,6 +458,18 @@ int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
   CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; i++) std::memcpy(out + 16 * i, info[i].dbg, 16 * sizeof(int64_t));
   return ESSL_OK;
+}
+
+int essl_trace_read(essl_ctx *c, uint64_t *out, int max) {
+  if (!c || !out || max < 0 || !c->trace.buf) return fail(ESSL_E_ARG, "essl_trace_read: tracing off");
+  CK(cudaDeviceSynchronize());
+  unsigned int n = 0;
+  CK(cudaMemcpy(&n, c->trace.count, sizeof(n), cudaMemcpyDeviceToHost));
+  n = std::min(n, c->trace.cap);
+  n = std::min(n, (unsigned int)max);
+  CK(cudaMemcpy(out, c->trace.buf, sizeof(uint64_t) * 4 * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(c->trace.count, 0, sizeof(unsigned int)));
+  return (int)n;
 }
 
 int essl_debug_lanes(essl_ctx *c, int32_t *out, int n) {
@@ -630,6 +659,7 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   pp.out = out;
   pp.out_stride = out_stride;
   pp.out_u8 = any_aug ? c->aug_a : out_u8;
+  pp.trace = c->trace;
   {
     int words = 0;
     for (int i = 0; i < n; i++)

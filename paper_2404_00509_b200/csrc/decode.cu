@@ -1076,6 +1076,7 @@ __device__ __forceinline__ DecodeHdr *hdr_of(const Scratch &s, int img) {
 // ===========================================================================
 template <bool SMEM>
 __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
+  TraceScope trace_(P.trace, ESSL_K_PREP);
   extern __shared__ __align__(16) uint8_t dyn[];  // [payload (SMEM)][CRC chunk partials]
   __shared__ PrepSmem S;
   DecodeHead &H = S.h;
@@ -1859,6 +1860,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
 }
 
 __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
+  TraceScope trace_(P.trace, ESSL_K_ENTROPY);
   __shared__ EntSmem S;
   const int img = blockIdx.x;
   const int lane = threadIdx.x;
@@ -2047,6 +2049,7 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
 }
 
 __global__ void __launch_bounds__(256) k_idct(DecodeParams P) {
+  TraceScope trace_(P.trace, ESSL_K_IDCT);
   __shared__ uint8_t s_zz[64];
   __shared__ int32_t q[3][64];
   __shared__ int32_t tr[8][4][64];

@@ -67,6 +67,41 @@ struct Scratch {
   uint64_t list_cap;  // entries
 };
 
+// Optional per-CTA execution trace (ESSL_OPT_TRACE): {start ns, end ns,
+// kernel id, SM id} per CTA, appended at an atomic cursor.
+struct CtaTrace {
+  unsigned long long *buf;
+  unsigned int *count;
+  unsigned int cap;
+};
+
+struct TraceScope {
+  const CtaTrace &t;
+  unsigned long long t0;
+  int kid;
+  __device__ __forceinline__ static unsigned long long now() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+  }
+  __device__ __forceinline__ TraceScope(const CtaTrace &t_, int kid_) : t(t_), t0(0), kid(kid_) {
+    if (t.buf && threadIdx.x == 0) t0 = now();
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    if (t.buf && threadIdx.x == 0) {
+      const unsigned int i = atomicAdd(t.count, 1u);
+      if (i < t.cap) {
+        unsigned int sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        t.buf[4 * i] = t0;
+        t.buf[4 * i + 1] = now();
+        t.buf[4 * i + 2] = (unsigned long long)kid;
+        t.buf[4 * i + 3] = sm;
+      }
+    }
+  }
+};
+
 struct DecodeParams {
   const uint8_t *blob;
   const essl_sample *samples;  // device copy of the batch descriptors
@@ -80,6 +115,7 @@ struct DecodeParams {
   int prep_part_off; // k_prep: byte offset of the CRC partials in dynamic smem
   essl_result *results;  // optional
   int32_t *dbg_lanes;    // optional per-lane decode records [n][kEntropyLanes][8]
+  CtaTrace trace;
 };
 
 struct PixelParams {
@@ -91,6 +127,7 @@ struct PixelParams {
   int64_t out_stride;  // elements per sample
   uint8_t *out_u8;
   int src_words;       // k_resize shared source rows: band source rows x widest crop
+  CtaTrace trace;
 };
 
 // 3-Aug stage (k_aug_blur / k_aug_out): a = resized (flipped) uint8 HWC
