@@ -1112,19 +1112,19 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     }
     for (int i = n + tid; i < n_pad; i += kNT) dyn[i] = 0;
   }
-  {  // CRC tables (slice-by-4)
-    uint32_t c = tid;
+  for (int e = tid; e < 256; e += kNT) {  // CRC tables (slice-by-4)
+    uint32_t c = e;
 #pragma unroll
     for (int k = 0; k < 8; k++) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
-    S.crc.T[0][tid] = c;
+    S.crc.T[0][e] = c;
   }
   __syncthreads();
-  {
-    uint32_t c = S.crc.T[0][tid];
+  for (int e = tid; e < 256; e += kNT) {
+    uint32_t c = S.crc.T[0][e];
 #pragma unroll
     for (int t = 1; t < 4; t++) {
       c = (c >> 8) ^ S.crc.T[0][c & 0xFF];
-      S.crc.T[t][tid] = c;
+      S.crc.T[t][e] = c;
     }
   }
   __syncthreads();
