@@ -478,11 +478,17 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
   return v;
 }
 
-// Per-image decode context held in registers by every lane.
+// Per-image decode context held in registers by every lane.  The table
+// offsets d0..a2 are byte offsets into the shared first-level tables
+// (kTabStride per table); TS (tables in shared memory) reads those, !TS reads
+// the same entries from the global HuffTab array (images using more than
+// kSmemTabs tables, and the validation path).  Second-level sub-tables and the
+// canonical arrays (long codes, rare) are always read from global memory.
+constexpr uint32_t kTabStride = (1u << kFastBits) * 2u;
+constexpr int kSmemTabs = 4;
 struct EntCtx {
-  const uint8_t *tabs;  // HuffFast array (shared memory)
   const HuffTab *gtab;  // the full tables (global memory)
-  uint32_t tabs_s;      // the same, as a shared-window address
+  uint32_t tabs_s;      // shared first-level tables, as a shared-window address
   uint32_t zz_s;        // zig-zag -> natural table (shared-window address)
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
   int c1, c2, bpm, gx;
@@ -497,17 +503,20 @@ struct EntCtx {
     return k == 0 ? d : a;
   }
   // first-level entry (tot == 0: long code pointer or invalid)
+  template <bool TS>
   __device__ __forceinline__ uint32_t lookup_fast(int k, int b, uint32_t hi) const {
-    return lds_u16(tabs_s + tab_off(k, b) + ((hi >> (32 - kFastBits)) << 1));
+    const uint32_t off = tab_off(k, b);
+    if (TS) return lds_u16(tabs_s + off + ((hi >> (32 - kFastBits)) << 1));
+    return __ldg(&gtab[off / kTabStride].fast[hi >> (32 - kFastBits)]);
   }
   __device__ __forceinline__ uint32_t zz(int i) const { return lds_u8(zz_s + (uint32_t)i); }
   __device__ __forceinline__ uint32_t lookup_long(int k, int b, uint32_t e, uint32_t hi) const {
-    const uint32_t off = tab_off(k, b);
-    return essl::lookup_long(*reinterpret_cast<const HuffFast *>(tabs + off),
-                             gtab[off / (uint32_t)sizeof(HuffFast)], e, hi);
+    const HuffTab &T = gtab[tab_off(k, b) / kTabStride];
+    return essl::lookup_long(*reinterpret_cast<const HuffFast *>(&T), T, e, hi);
   }
+  template <bool TS>
   __device__ __forceinline__ uint32_t lookup(int k, int b, uint32_t hi) const {
-    uint32_t e = lookup_fast(k, b, hi);
+    uint32_t e = lookup_fast<TS>(k, b, hi);
     if ((e & 31) == 0 && e != 0) e = lookup_long(k, b, e, hi);
     return e;
   }
@@ -638,7 +647,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   while (r.p < send) {
     r.refill();
     const uint32_t hi = r.hi();
-    uint32_t e = C.lookup_fast(k, b, hi);
+    uint32_t e = C.lookup_fast<SH>(k, b, hi);
     int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
     int knew = k + kinc;
     if (tot == 0 || (size != 0 && knew > 64)) {  // long code or decode error (rare)
@@ -742,7 +751,7 @@ __device__ uint32_t tail_run(const EntCtx &C, uint32_t p, int k, int b, uint32_t
 #pragma unroll 1
   while (need > 0) {
     r.refill();
-    const uint32_t e = C.lookup(k, b, r.hi());
+    const uint32_t e = C.lookup<SH>(k, b, r.hi());
     UNIT_FIELDS(e, k);
     if (bad) return r.p;
     r.skip(tot);
@@ -795,7 +804,7 @@ __device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, u
   while (blk < end) {
     r.refill();
     const uint32_t hi = r.hi();
-    const uint32_t e = C.lookup(k, b, hi);
+    const uint32_t e = C.lookup<SH>(k, b, hi);
     UNIT_FIELDS(e, k);
     if (bad) {
       o.err = 1;
@@ -1634,7 +1643,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
 // ===========================================================================
 struct __align__(16) EntSmem {
   DecodeHead h;
-  HuffFast tab[kMaxTables];
+  uint16_t tab[kSmemTabs][1 << kFastBits];  // first-level tables (<= kSmemTabs used)
   LaneRec lane[kLanes];
   int status, reason, offset;
   uint32_t p_final;
@@ -1859,7 +1868,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
 #undef PHASE
 }
 
-__global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
+__global__ void __launch_bounds__(kLanes, 10) k_entropy(DecodeParams P) {
   TraceScope trace_(P.trace, ESSL_K_ENTROPY);
   __shared__ EntSmem S;
   const int img = blockIdx.x;
@@ -1878,11 +1887,11 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
     for (int i = lane; i < head; i += kLanes) dst[i] = src[i];
   }
   __syncthreads();
-  if (H.status == 0) {  // the fast tables of the used Huffman tables
-    const int per = (int)(sizeof(HuffFast) / 16);
+  if (H.status == 0 && H.ntab <= kSmemTabs) {  // the first-level tables of the used Huffman tables
+    constexpr int per = (int)(kTabStride / 16);
     for (int i = lane; i < H.ntab * per; i += kLanes) {
       const int t = i / per, w = i % per;
-      reinterpret_cast<int4 *>(&S.tab[t])[w] = reinterpret_cast<const int4 *>(&G->tab[t])[w];
+      reinterpret_cast<int4 *>(S.tab[t])[w] = reinterpret_cast<const int4 *>(G->tab[t].fast)[w];
     }
   }
   if (lane == 0) {
@@ -1899,13 +1908,12 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   PHASE(1);
 
   EntCtx C;
-  C.tabs = reinterpret_cast<const uint8_t *>(S.tab);
   C.gtab = G->tab;
   C.tabs_s = (uint32_t)__cvta_generic_to_shared(S.tab);
   C.zz_s = (uint32_t)__cvta_generic_to_shared(H.zz);
   {
     const uint32_t w = H.tab_index_word;
-    const uint32_t sz = (uint32_t)sizeof(HuffFast);
+    const uint32_t sz = kTabStride;
     C.d0 = (w & 15) * sz; C.d1 = ((w >> 4) & 15) * sz; C.d2 = ((w >> 8) & 15) * sz;
     C.a0 = ((w >> 12) & 15) * sz; C.a1 = ((w >> 16) & 15) * sz; C.a2 = ((w >> 20) & 15) * sz;
   }
@@ -1921,7 +1929,7 @@ __global__ void __launch_bounds__(kLanes) k_entropy(DecodeParams P) {
   uint32_t dbg_nseq = 0, dbg_cont = 0;
   // per-lane read rings (cp.async) unless the validation option asks for
   // plain global reads
-  const bool staged = P.stage_bytes != 0;
+  const bool staged = P.stage_bytes != 0 && H.ntab <= kSmemTabs;
   C.ring_s = (uint32_t)__cvta_generic_to_shared(&S.ring[lane][0]);
   C.cpad = H.cpad;
   __syncthreads();
