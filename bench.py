@@ -299,6 +299,9 @@ def run_gpu(args, wl):
     gc.freeze()  # long-lived objects (torch, numpy) out of the cyclic GC's way
     torch.cuda.synchronize(dev)
     clk.mark()
+    prof_range = os.environ.get("ESSL_PROFILER_RANGE") == "1"  # ncu --replay-mode app-range
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStart()
     host_t = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
@@ -317,6 +320,8 @@ def run_gpu(args, wl):
         loader.join(p)
     t1.record(stream)
     torch.cuda.synchronize(dev)
+    if prof_range:
+        torch.cuda.cudart().cudaProfilerStop()
     clk.mark()
     if ws > 1:
         dist.barrier()
