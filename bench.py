@@ -459,10 +459,14 @@ def main():
                     help="ESSL_OPT_STAGE_BYTES (0: entropy lanes read the clean stream from global)")
     ap.add_argument("--streams", type=int, default=6,
                     help="batches in flight (one libessl context + CUDA stream each)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="images per step (0: the workload's batch; analysis knob)")
     ap.add_argument("--aug", default="simple", choices=["simple", "3aug", "3aug+"],
                     help="augmentation level (finetune schemes use 3aug / 3aug+)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
+    if args.batch > 0:
+        wl["batch"] = args.batch
     if args.aug != "simple":
         wl["aug"] = args.aug
         wl["desc"] = wl["desc"].replace("+ flip +", f"+ flip + {args.aug} +")

@@ -169,29 +169,99 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
   PlaneSrc S;
   S.load(I, P.plane);
-  // source rows -> RGBX words.  Each thread keeps one column (its plane
-  // column offsets fixed) and walks rows, four in flight; no per-pixel
-  // division.
-  {
-    const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
-    const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
-    const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
-    if (r0 < rpp) {
-      for (int x = x0; x < iw; x += cpr) {
-        int co[3];
-        S.col_off(I.rx + x, co);
-        for (int r = r0; r < nrows; r += 4 * rpp) {
-          int rr[4], gg[4], bb[4];
+  // source rows -> RGBX words in shared memory.
+  // Fast path (luma at full horizontal resolution, chroma at full or half:
+  // 4:2:0, 4:2:2, 4:4:4, gray): work items are (row, group of 4 image
+  // columns aligned to 4), so the luma plane is read 4 bytes at a time and
+  // half-resolution chroma 2 bytes at a time (planes are MCU-aligned windows:
+  // a group never leaves them), and each chroma sample's colour terms are
+  // computed once for the two pixels that replicate it (decode_kernels.py:
+  // 551-576: R = Y + (91881 Cr + 32768) >> 16, G = Y + (-22554 Cb - 46802 Cr
+  // + 32768) >> 16, B = Y + (116130 Cb + 32768) >> 16, clamped).
+  const bool fast = I.comp_h[0] == I.hmax &&
+                    (I.ncomp == 1 || ((2 * I.comp_h[1] == I.hmax || I.comp_h[1] == I.hmax) &&
+                                      (2 * I.comp_h[2] == I.hmax || I.comp_h[2] == I.hmax)));
+  if (fast) {
+    const int g0 = I.rx >> 2, ng = ((I.rx + iw + 3) >> 2) - g0;
+    const bool half1 = I.ncomp == 3 && 2 * I.comp_h[1] == I.hmax;
+    const bool half2 = I.ncomp == 3 && 2 * I.comp_h[2] == I.hmax;
+    for (int it = threadIdx.x; it < nrows * ng; it += kPixThreads) {
+      const int r = it / ng, G = g0 + (it - r * ng);
+      int ro[3];
+      S.row_off(I.ry + ys0 + r, ro);
+      const uint32_t y4 = *reinterpret_cast<const uint32_t *>(S.p[0] + ro[0] + 4 * G - S.ox[0]);
+      uint32_t w[4];
+      if (I.ncomp == 1) {
 #pragma unroll
-          for (int u = 0; u < 4; u++) {
-            int ro[3];
-            S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
-            S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
+        for (int i = 0; i < 4; i++) w[i] = ((y4 >> (8 * i)) & 255u) * 0x010101u;
+      } else {
+        // chroma bytes of the group's 4 pixels (replicated when half resolution)
+        uint32_t cb4, cr4;
+        if (half1) {
+          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[1] + ro[1] + 2 * G - S.ox[1]);
+          cb4 = __byte_perm(t, 0, 0x1100);
+        } else {
+          cb4 = *reinterpret_cast<const uint32_t *>(S.p[1] + ro[1] + 4 * G - S.ox[1]);
+        }
+        if (half2) {
+          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[2] + ro[2] + 2 * G - S.ox[2]);
+          cr4 = __byte_perm(t, 0, 0x1100);
+        } else {
+          cr4 = *reinterpret_cast<const uint32_t *>(S.p[2] + ro[2] + 4 * G - S.ox[2]);
+        }
+        // colour terms per distinct chroma pair (pixels 2k, 2k+1 share one
+        // when both chroma planes are half resolution)
+        int dr[4], dg[4], db[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          if (i & 1 && half1 && half2) {
+            dr[i] = dr[i - 1]; dg[i] = dg[i - 1]; db[i] = db[i - 1];
+            continue;
           }
+          const int cb = (int)((cb4 >> (8 * i)) & 255u) - 128;
+          const int cr = (int)((cr4 >> (8 * i)) & 255u) - 128;
+          dr[i] = (91881 * cr + 32768) >> 16;
+          dg[i] = (-22554 * cb - 46802 * cr + 32768) >> 16;
+          db[i] = (116130 * cb + 32768) >> 16;
+        }
 #pragma unroll
-          for (int u = 0; u < 4; u++)
-            if (r + u * rpp < nrows)
-              src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+        for (int i = 0; i < 4; i++) {
+          const int yv = (int)((y4 >> (8 * i)) & 255u);
+          w[i] = (uint32_t)clamp255(yv + dr[i]) | ((uint32_t)clamp255(yv + dg[i]) << 8) |
+                 ((uint32_t)clamp255(yv + db[i]) << 16);
+        }
+      }
+      const int x = 4 * G - I.rx;
+      uint32_t *row = src + r * iw;
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if ((unsigned)(x + i) < (unsigned)iw) row[x + i] = w[i];
+    }
+  } else {
+    // generic sampling factors: each thread keeps one column (its plane
+    // column offsets fixed) and walks rows, four in flight; no per-pixel
+    // division.
+    {
+      const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
+      const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
+      const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
+      if (r0 < rpp) {
+        for (int x = x0; x < iw; x += cpr) {
+          int co[3];
+          S.col_off(I.rx + x, co);
+          for (int r = r0; r < nrows; r += 4 * rpp) {
+            int rr[4], gg[4], bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              int ro[3];
+              S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
+              S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              if (r + u * rpp < nrows)
+                src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+          }
         }
       }
     }
@@ -199,21 +269,33 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   // row taps of the band (imgops.py:37-41), shared by every column
   __shared__ int2 ry[kBandRows];
   __shared__ double rw[kBandRows];
+  __shared__ float rwf[kBandRows];
   if (threadIdx.x < ob1 - ob0) {
     int y0, y1;
     double wy;
     tap(ob0 + threadIdx.x, sy, ih, y0, y1, wy);
     ry[threadIdx.x] = make_int2(y0 - ys0, y1 - ys0);
     rw[threadIdx.x] = wy;
+    rwf[threadIdx.x] = __double2float_rn(wy);
   }
   __syncthreads();
-  // Separable evaluation, exactly the reference's expressions: per output
-  // column the horizontal lerps top = (1-wx)*s(y,x0) + wx*s(y,x1) of the
-  // source rows y0/y1 (imgops.py:49-52) are kept in registers and reused
-  // while consecutive output rows share them; per output row only the
-  // vertical (1-wy)*top + wy*bot + 0.5 (imgops.py:53-56).  A thread owns a
-  // pair of adjacent output columns (paired bf16 / f32 stores); small
-  // outputs split the band's rows over groups of threads.
+  // Separable evaluation.  The reference value is float64 (imgops.py:49-56):
+  //   v = (1-wy)*((1-wx)*s00 + wx*s01) + wy*((1-wx)*s10 + wx*s11) + 0.5,
+  //   px = int(v) (v <= 255.5, so the min(., 255) never binds).
+  // It is evaluated here in float32, scaled by 4096 (exact for integer
+  // samples): T = 4096*s0 + 2048 + (4096*wx)*(s1 - s0) per source row (one
+  // fma, kept in registers while consecutive output rows share the row),
+  // V = T0 + wy*(T1 - T0).  Float32 error, in those units: wx, wy rounded to
+  // float32 (<= 2^-24 * 255 * 4096 = 0.0625 each), four roundings at
+  // magnitude < 2^20 (<= 0.03125 each): |V - 4096*v| < 0.25.  With
+  // x = round(V), |x - 4096*v| < 0.75, so x mod 4096 in [1, 4094] proves
+  // int(v) == x >> 12.  Otherwise (x within one unit of a multiple of 4096:
+  // ~0.05% of channels, more with dyadic weights giving integral values) the
+  // pixel is recomputed with the reference's float64 expression (bilerp2).
+  //   x + 1 = bits(V + 1.5*2^23 + 1) - 0x4B400000  (round to nearest through
+  //   the magic constant; V + 1.5*2^23 + 1 < 2^24 keeps unit spacing).
+  // A thread owns a pair of adjacent output columns (paired bf16 / f32
+  // stores); small outputs split the band's rows over groups of threads.
   const int npair = (res + 1) >> 1;
   const int ng = npair >= kPixThreads ? 1 : kPixThreads / npair;
   const int g = ng > 1 ? threadIdx.x / npair : 0;
@@ -227,32 +309,41 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
   const bool pair_ok = (res & 1) == 0 && (stride & 1) == 0 &&
                        ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
   if (g >= ng) return;
+  constexpr float kMagic1 = 12582913.0f;   // 1.5 * 2^23 + 1
+  constexpr int kMagicBits = 0x4B400000;   // bits of 1.5 * 2^23
+  constexpr float kByteBias = 8388608.0f;  // bits 0x4B000000 | byte == 2^23 + byte
   for (int q = cstart; q < npair; q += cstep) {
     const int oxa = 2 * q;
     const bool two = oxa + 1 < res;
     int x0[2], x1[2];
-    double wx[2], ax[2];
+    double wx[2];
+    float wxk[2];
 #pragma unroll
     for (int j = 0; j < 2; j++) {
       const int ox = min(oxa + j, res - 1);
       tap(I.flip ? res - 1 - ox : ox, sx, iw, x0[j], x1[j], wx[j]);  // hflip after resize
-      ax[j] = __dsub_rn(1.0, wx[j]);
+      wxk[j] = __fmul_rn(__double2float_rn(wx[j]), 4096.0f);
     }
     int cy0 = -1, cy1 = -1;
-    double h0[2][3], h1[2][3];
-    auto hrow = [&](int y, double h[2][3]) {
+    float h0[2][3], h1[2][3];
+    auto hrow = [&](int y, float h[2][3]) {
 #pragma unroll
       for (int j = 0; j < 2; j++) {
         const uint32_t a0 = src[y * iw + x0[j]], a1 = src[y * iw + x1[j]];
 #pragma unroll
-        for (int c = 0; c < 3; c++)
-          h[j][c] = __dadd_rn(__dmul_rn(ax[j], (double)((a0 >> (8 * c)) & 255)),
-                              __dmul_rn(wx[j], (double)((a1 >> (8 * c)) & 255)));
+        for (int c = 0; c < 3; c++) {
+          // 2^23 + byte, exactly (byte c of the RGBX word under exponent 0x4B)
+          const float f0 = __uint_as_float(__byte_perm(a0, 0x4B000000u, c | 0x7540));
+          const float f1 = __uint_as_float(__byte_perm(a1, 0x4B000000u, c | 0x7540));
+          // 4096*s0 + 2048 (exact) + (4096*wx) * (s1 - s0), one rounding
+          const float base = __fmaf_rn(f0, 4096.0f, 2048.0f - 4096.0f * kByteBias);
+          h[j][c] = __fmaf_rn(wxk[j], __fsub_rn(f1, f0), base);
+        }
       }
     };
     for (int r = rb; r < re; r++) {
       const int2 yy = ry[r];
-      const double wy = rw[r], ay = __dsub_rn(1.0, wy);
+      const float wy = rwf[r];
       if (yy.x != cy0) {  // (uniform across the CTA's columns: no divergence)
         if (yy.x == cy1) {
 #pragma unroll
@@ -276,13 +367,27 @@ __global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
         cy1 = yy.y;
       }
       int px[2][3];
+      int amb[2] = {4095, 4095};
 #pragma unroll
       for (int j = 0; j < 2; j++)
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-          const double v = __dadd_rn(__dadd_rn(__dmul_rn(ay, h0[j][c]), __dmul_rn(wy, h1[j][c])), 0.5);
-          const int iv = __double2int_rz(v);
-          px[j][c] = iv > 255 ? 255 : iv;
+          const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
+          const int y1 = __float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits;  // round(v) + 1
+          amb[j] = min(amb[j], y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
+          px[j][c] = y1 >> 12;              // == round(v) >> 12 when not ambiguous
+        }
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+        if (amb[j] == 0) {  // rare: the exact float64 expression (imgops.py:49-56)
+          const double wyd = rw[r];
+          const uint32_t a00 = src[yy.x * iw + x0[j]], a01 = src[yy.x * iw + x1[j]];
+          const uint32_t a10 = src[yy.y * iw + x0[j]], a11 = src[yy.y * iw + x1[j]];
+#pragma unroll
+          for (int c = 0; c < 3; c++)
+            px[j][c] = bilerp2(wx[j], wyd, __dsub_rn(1.0, wx[j]), __dsub_rn(1.0, wyd),
+                               (a00 >> (8 * c)) & 255, (a01 >> (8 * c)) & 255,
+                               (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
         }
       const int oy = ob0 + r;
       const int64_t o = img * stride + (int64_t)oy * res + oxa;

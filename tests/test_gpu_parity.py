@@ -384,3 +384,51 @@ def test_odd_and_extreme_resolutions_vs_oracle(E, oracle, synth_sets, res):
             assert np.array_equal(b.uint8.cpu().numpy(), u8)
             assert np.array_equal(b.pixels.cpu().numpy(), pix)
             assert torch.equal(b16.pixels, b.pixels.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("side,res", [(112, 224), (448, 224), (224, 112), (96, 160)])
+def test_resize_dyadic_weights_vs_oracle(E, oracle, tmp_path, side, res):
+    """Whole-image crops with power-of-two scale factors: the bilinear weights
+    are dyadic (0.25 / 0.5 / 0.75), so many float64 values land exactly on
+    integers -- the cases k_resize's float32 evaluation cannot decide and
+    recomputes in float64.  uint8 and float32 bit-exact vs the oracle."""
+    path = tmp_path / f"dy{side}.essl"
+    E.build_synthetic(path, 24, side, 95, seed=11)
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=24, res=res, scale=(1.0, 1.0),
+                             ratio=(1.0, 1.0), keep_uint8=True)
+        loader = E.Loader(cfg, container=h)
+        for b in loader.epoch(0):
+            idx = b.indices.cpu().numpy()
+            pix, u8, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 0, res,
+                                                 scale=(1.0, 1.0), ratio=(1.0, 1.0),
+                                                 keep_uint8=True, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
+
+
+@pytest.mark.parametrize("res", [64, 160, 224])
+def test_loader_sampling_layouts_vs_oracle(E, oracle, tmp_path, res):
+    """Every fixture stream layout (4:2:0, 4:2:2, 4:4:4, gray, restart
+    intervals, odd sizes, 1x1) packed in a container and run through the
+    loader (k_resize's colour-conversion paths): uint8 and float32 bit-exact
+    vs the oracle."""
+    from PIL import Image
+    import io
+    names = [n for n in STREAMS] * 3
+    pay = [stream_bytes(n) for n in names]
+    dims = [Image.open(io.BytesIO(b)).size for b in pay]
+    path = tmp_path / "layouts.essl"
+    E.write_container(path, pay, [d[0] for d in dims], [d[1] for d in dims],
+                      list(range(len(pay))), max_resolution=512, quality=95)
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=16, res=res, keep_uint8=True)
+        loader = E.Loader(cfg, container=h)
+        for b in loader.epoch(2):
+            idx = b.indices.cpu().numpy()
+            pix, u8, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 2, res,
+                                                 keep_uint8=True, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
