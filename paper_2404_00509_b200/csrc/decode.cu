@@ -596,7 +596,7 @@ struct LaneRec {
 // (bit position, block-in-MCU) at a block start -- two decoders in the same
 // state produce the same future -- or errors, or runs off the data.
 template <bool CONT, bool SH>
-__device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t send,
+__device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t sbeg, uint32_t send,
                          uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, Ckpt *ck_all,
                          LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
   Reader<SH> r;
@@ -641,6 +641,53 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   if (CONT) seek(r.p);
   int st = 2;
   uint32_t dbg_units = 0, dbg_guess = 0;
+  if (!CONT && p0 < sbeg) {
+    // Warm-up [p0, sbeg): decode only, nothing stored.  The path through it
+    // is never part of the exact path through this lane's list: the
+    // previous lane's continuation starts at sbeg, so it can only merge at
+    // a checkpoint at or after sbeg.  Stop at the first block start at or
+    // after sbeg and record a checkpoint there, where the list begins.
+    bool stop = false;
+#pragma unroll 1
+    while (true) {
+      r.refill();
+      const uint32_t hi = r.hi();
+      uint32_t e = C.lookup_fast<SH>(k, b, hi);
+      int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
+      int knew = k + kinc;
+      if (tot == 0 || (size != 0 && knew > 64)) {
+        if (tot == 0 && e != 0) {
+          e = C.lookup_long(k, b, e, hi);
+          tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
+          knew = k + kinc;
+        }
+        if (tot == 0 || (size != 0 && knew > 64)) {  // off the path: re-guess one bit on
+          if (r.p + 8 > C.cbits) { stop = true; break; }
+          r.init(r.p + 1);
+          dbg_guess++;
+          k = 0;
+          b = 0;
+          nblk = 0;
+          continue;
+        }
+      }
+      dbg_units++;
+      r.skip(tot);
+      const bool bend = knew >= 64;
+      const int bn = b + 1 == C.bpm ? 0 : b + 1;
+      k = bend ? 0 : knew;
+      b = bend ? bn : b;
+      nblk += bend;
+      if (bend && r.p >= sbeg) break;
+    }
+    if (stop) {
+      send = 0;  // the main loop does not run; the lane's path ends here
+    } else {
+      ck[0] = Ckpt{(r.p << 6) | (uint32_t)b, 0u, nblk, 0u};
+      nck = 1;
+      ck_next = r.p + C.ck_bits;
+    }
+  }
   uint32_t *lp = list + min(nl, cap);
   uint2 *bp = bsl + min(nbs, bcap);
 #pragma unroll 1
@@ -1743,7 +1790,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
     nseq = max(1, min(nseq, kLanes));
     const uint32_t slen = (cbits + nseq - 1) / nseq;
     const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
-    C.ck_bits = max((uint32_t)P.ck_bits, (slen + warm + kCk - 9) / (kCk - 8));
+    C.ck_bits = max((uint32_t)P.ck_bits, (slen + kCk - 9) / (kCk - 8));  // checkpoints cover [sbeg, send)
     Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
     // unit lists + block records: one region per lane, carved per image.
     // Lists hold every decoded unit; slot cap is a sink for overflow and the
@@ -1770,12 +1817,12 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
       const uint32_t sbeg = lane * slen;
       const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
       const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
-      run_path<false, SH>(C, lane, nseq, p0, send, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
+      run_path<false, SH>(C, lane, nseq, p0, sbeg, send, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
     }
     __syncthreads();
     PHASE(2);
     const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
-    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
+    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
     dbg_nseq = (uint32_t)nseq;
     if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
     __syncthreads();
