@@ -342,8 +342,10 @@ def run_gpu(args, wl):
     e2e_v = None
     h2d = d2h = 0
     if not args.no_e2e:
-        cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False})
+        cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False, "staging": args.staging})
         l2 = E.Loader(cfg2, container=handle, engine=loader.engine)
+        if args.gather_ctas >= 0:
+            l2.set_option(N.ESSL_OPT_GATHER_CTAS, args.gather_ctas)
         steps_e2e = min(args.steps, max(1, len(handle) // ws // B))
         for k, b in enumerate(l2.epoch(1)):  # warm the staging pool and output ring
             if k + 1 >= min(steps_e2e, 3 * cfg.streams + 3):
@@ -457,8 +459,12 @@ def main():
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
     ap.add_argument("--stage-bytes", type=int, default=-1,
                     help="ESSL_OPT_STAGE_BYTES (0: entropy lanes read the clean stream from global)")
-    ap.add_argument("--streams", type=int, default=6,
+    ap.add_argument("--streams", type=int, default=8,
                     help="batches in flight (one libessl context + CUDA stream each)")
+    ap.add_argument("--gather-ctas", type=int, default=-1,
+                    help="e2e: k_host_gather CTAs (ESSL_OPT_GATHER_CTAS; -1: library default)")
+    ap.add_argument("--staging", default="gather", choices=["gather", "copy"],
+                    help="e2e host staging: bus-read gather kernel or host threads + one copy")
     ap.add_argument("--batch", type=int, default=0,
                     help="images per step (0: the workload's batch; analysis knob)")
     ap.add_argument("--aug", default="simple", choices=["simple", "3aug", "3aug+"],

@@ -135,7 +135,7 @@ struct essl_ctx {
   int ck_bits = 64;
   int warm_bits = 2048;
   int stage_max = 64 * 1024;
-  int gather_ctas = 8;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
+  int gather_ctas = 4;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
   bool gather_tma = false;
   int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
   essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--stage", type=int, default=-1, help="ESSL_OPT_STAGE_BYTES (0: global reader)")
     args = ap.parse_args()
     import torch
 
@@ -41,6 +42,8 @@ def main():
                          mask_ratio=0.75, streams=1)
     loader = E.Loader(cfg)
     eng = loader.engine
+    if args.stage >= 0:
+        eng.set_option(N.ESSL_OPT_STAGE_BYTES, args.stage)
     perm = E.epoch_permutation(0, 0, len(loader.handle))
     settings = [("spec", 4096, 2048)]
     if args.sweep:
