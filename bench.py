@@ -55,6 +55,20 @@ WORKLOADS = {
     "cfg4": dict(side=512, quality=90, scale=(0.2, 1.0), batch=1024, res=224, mask=0.0,
                  desc="1024 synthetic 512px q90 JPEGs per batch, RRC(0.2,1)->224 + flip + "
                       "normalize (bf16 NCHW)"),
+    # progressive resolution (schedule.py custom scheme): the
+    # timed steps are split evenly over the stages, Loader.retarget between them
+    "cfg3": dict(side=256, quality=95, scale=(0.08, 1.0), batch=256, res=224, mask=0.75,
+                 schedule=(112, 160, 192, 224),
+                 desc="256 synthetic 256px q95 JPEGs per batch, progressive RRC(0.08,1) "
+                      "112->160->192->224 (equal steps per stage) + flip + normalize (bf16 "
+                      "NCHW) + MAE-B/16 mask 0.75"),
+    # epoch-scale stream: 1,281,167 records aliasing a pool
+    # of distinct cfg1-style payloads, DDP-sharded perm[r::world]
+    "cfg5": dict(side=256, quality=95, scale=(0.08, 1.0), batch=256, res=224, mask=0.75,
+                 records=1_281_167,
+                 desc="1,281,167-record container (ImageNet-1k size) aliasing the pool of "
+                      "256px q95 JPEGs, DDP-sharded epoch stream, batch 256 per GPU, "
+                      "RRC(0.08,1)->224 + flip + normalize (bf16 NCHW) + MAE-B/16 mask 0.75"),
 }
 
 
@@ -72,10 +86,12 @@ def peaks() -> dict:
 
 def make_dataset(wl: dict, pool: int, out_dir: Path, seed: int = 1) -> Path:
     from paper_2404_00509_b200 import build_synthetic
-    path = out_dir / f"pool_{wl['side']}_{wl['quality']}_{pool}.essl"
+    rec = wl.get("records")
+    path = out_dir / f"pool_{wl['side']}_{wl['quality']}_{pool}_{rec or pool}.essl"
     if not path.exists():
         t = time.perf_counter()
-        info = build_synthetic(path, pool, wl["side"], wl["quality"], classes=1000, seed=seed)
+        info = build_synthetic(path, pool, wl["side"], wl["quality"], classes=1000, seed=seed,
+                               n_records=rec)
         log(f"[bench] built {pool} images ({info['mean_payload']:.0f} B mean) in "
             f"{time.perf_counter() - t:.1f}s")
     return path
@@ -263,6 +279,8 @@ def run_gpu(args, wl):
         loader.set_option(N.ESSL_OPT_STAGE_BYTES, args.stage_bytes)
     handle = loader.handle
     perm_epochs = {}
+    if args.epoch:  # one full epoch of this rank's shard (whole batches)
+        args.steps = max(1, len(handle) // ws // B)
 
     def batch_indices(i):
         per_epoch = len(handle) // ws // B
@@ -279,7 +297,11 @@ def run_gpu(args, wl):
     # caching allocator and every stream's context reach steady state
     pend = []
     ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2  # pipeline.py _HostRing slots
-    for i in range(max(args.warmup, args.streams * (ring_depth + 1))):
+    n_warm = max(args.warmup, args.streams * (ring_depth + 1))
+    sched = wl.get("schedule")
+    for i in range(n_warm):
+        if sched:  # every stage's output ring allocated before the timed region
+            loader.retarget(res=sched[i * len(sched) // n_warm])
         e, idx = batch_indices(i)
         pend.append(loader.enqueue(e, idx))
         if len(pend) > 2 * args.streams:
@@ -292,6 +314,8 @@ def run_gpu(args, wl):
     loader.profile_read()
     launches0 = loader.launches
     pend = []
+    if sched:
+        loader.retarget(res=sched[0])
     if ws > 1:
         dist.barrier()
     import gc
@@ -309,6 +333,10 @@ def run_gpu(args, wl):
     n_img = 0
     for i in range(args.steps):
         h0 = time.perf_counter()
+        if sched:  # progressive stages: equal shares of the timed steps
+            r_i = sched[min(len(sched) - 1, i * len(sched) // args.steps)]
+            if r_i != loader.config.res:
+                loader.retarget(res=r_i)
         e, idx = batch_indices(args.warmup + i)
         pend.append(loader.enqueue(e, idx))
         n_img += len(idx)
@@ -393,11 +421,16 @@ def run_gpu(args, wl):
     if rank == 0:
         value = total / (ms_max / 1e3)
         pk = peaks()
-        per_img = float(np.mean(handle.records["payload_length"])) + 3 * res * res * 2
-        if wl["mask"] > 0:
-            T = (res // 16) ** 2
-            k = int(np.floor(wl["mask"] * T + 0.5))
-            per_img += k * 4 + (T - k) * 8 + T * 8
+        def bytes_out(r):
+            b = 3 * r * r * 2
+            if wl["mask"] > 0:
+                T = (r // 16) ** 2
+                k = int(np.floor(wl["mask"] * T + 0.5))
+                b += k * 4 + (T - k) * 8 + T * 8
+            return b
+        stages = wl.get("schedule") or (res,)
+        per_img = float(np.mean(handle.records["payload_length"])) + \
+            float(np.mean([bytes_out(r) for r in stages]))
         # dominant kernel (largest device-time share): k_entropy
         ent_ms, ent_n = prof.get("entropy", (0.0, 0))
         imgs_per_launch = n_img / max(ent_n, 1)
@@ -422,7 +455,9 @@ def run_gpu(args, wl):
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int32", "out_dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": B,
-                           "res": res, "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool,
+                           "res": list(wl["schedule"]) if wl.get("schedule") else res,
+                           "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool,
+                           "records": len(handle),
                            "mean_payload_bytes": float(np.mean(handle.records["payload_length"])),
                            "l2": "inputs > L2: 8192-image pool (~235 MB) visited in permutation "
                                  "order; outputs are fresh buffers each step",
@@ -451,6 +486,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--epoch", action="store_true",
+                    help="time one full epoch of this rank's shard (steps = batches per epoch)")
     ap.add_argument("--pool", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")

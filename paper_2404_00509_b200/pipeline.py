@@ -385,9 +385,11 @@ class Loader:
         def out(name, shape, dtype):
             if not cfg.reuse_outputs:
                 return torch.empty(shape, dtype=dtype, device=dev)
-            key = (j, oslot, name)
+            # keyed by shape too: progressive stages (retarget) keep their own
+            # rings instead of reallocating at every stage switch
+            key = (j, oslot, name, tuple(shape), dtype)
             t = self._out_ring.get(key)
-            if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
+            if t is None:
                 t = torch.empty(shape, dtype=dtype, device=dev)
                 self._out_ring[key] = t
             return t
