@@ -53,6 +53,9 @@ def _digest() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    override = os.environ.get("ESSL_LIB")
+    if override and not force:  # an A/B build chosen by the caller: never rebuild over it
+        return Path(override)
     OUT_DIR.mkdir(exist_ok=True)
     stamp = OUT_DIR / "libessl.sha256"
     dig = _digest()

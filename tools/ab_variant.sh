@@ -1,12 +1,16 @@
 #!/bin/bash
-# Build the working tree's library into _libB/ (variant B) and restore the
-# committed sources' build in paper_2404_00509_b200/_lib (variant A).
-# Usage: make the B edit, run tools/ab_variant.sh, then revert the edit is done here (git stash).
+# Build the working tree's library into _libB/ (variant B) and the committed
+# sources' (HEAD) into _libA/ (variant A); paper_2404_00509_b200/_lib is left
+# holding the working tree's build.  Compare with
+#   python tools/ab.py --a _libA/libessl.so --b _libB/libessl.so
+# (ESSL_LIB makes build() load that file and never rebuild over it).
 set -e
 cd "$(dirname "$0")/.."
 python -c "from paper_2404_00509_b200 import build; build.build()"
-mkdir -p _libB && cp paper_2404_00509_b200/_lib/libessl.so _libB/libessl.so
+mkdir -p _libB _libA && cp paper_2404_00509_b200/_lib/libessl.so _libB/libessl.so
 git stash -q
 python -c "from paper_2404_00509_b200 import build; build.build()"
+cp paper_2404_00509_b200/_lib/libessl.so _libA/libessl.so
 git stash pop -q
-echo "A: paper_2404_00509_b200/_lib/libessl.so (HEAD), B: _libB/libessl.so (working tree)"
+python -c "from paper_2404_00509_b200 import build; build.build()"
+echo "A: _libA/libessl.so (HEAD), B: _libB/libessl.so (working tree)"
