@@ -1915,7 +1915,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
 #undef PHASE
 }
 
-__global__ void __launch_bounds__(kLanes, 10) k_entropy(DecodeParams P) {
+__global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
   TraceScope trace_(P.trace, ESSL_K_ENTROPY);
   __shared__ EntSmem S;
   const int img = blockIdx.x;

@@ -137,7 +137,7 @@ __global__ void k_init_norm_luts() {
 
 void init_norm_luts() { k_init_norm_luts<<<1, 768>>>(); }
 
-__global__ void __launch_bounds__(kPixThreads) k_resize(PixelParams P) {
+__global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
   TraceScope trace_(P.trace, ESSL_K_RESIZE);
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ float lut[3][256];
