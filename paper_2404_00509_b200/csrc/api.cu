@@ -661,9 +661,16 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   pp.out_u8 = any_aug ? c->aug_a : out_u8;
   pp.trace = c->trace;
   {
-    int words = 0;
-    for (int i = 0; i < n; i++)
-      words = std::max(words, essl::band_source_rows(samples[i].h, res) * std::max(samples[i].w, 1));
+    // the largest band (output rows per k_resize CTA) whose source-row
+    // staging fits the shared-memory budget for this batch's crops
+    int band = essl::kMaxBandRows, words = 0;
+    for (;; band /= 2) {
+      words = 0;
+      for (int i = 0; i < n; i++)
+        words = std::max(words, essl::band_source_rows(samples[i].h, res, band) * std::max(samples[i].w, 1));
+      if ((size_t)(words + 3) / 4 * 4 * 4 <= 200 * 1024 || band == 1) break;
+    }
+    pp.band = band;
     pp.src_words = (words + 3) / 4 * 4;
     if ((size_t)pp.src_words * 4 > 200 * 1024)
       return fail(ESSL_E_CAPACITY, "crop too large for the resize kernel's shared staging");

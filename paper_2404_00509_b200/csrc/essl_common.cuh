@@ -127,6 +127,7 @@ struct PixelParams {
   int64_t out_stride;  // elements per sample
   uint8_t *out_u8;
   int src_words;       // k_resize shared source rows: band source rows x widest crop
+  int band;            // k_resize output rows per CTA (<= kMaxBandRows)
   CtaTrace trace;
 };
 
@@ -176,7 +177,8 @@ void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);
 void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, int ctas,
                         bool tma, cudaStream_t st);
-int band_source_rows(int h, int res);
+constexpr int kMaxBandRows = 32;      // k_resize: output rows per CTA, at most
+int band_source_rows(int h, int res, int band);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);
 void launch_mask(uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens,

@@ -111,16 +111,16 @@ __device__ __forceinline__ float norm_value(int c, int v) {
   return __fdiv_rn(__fsub_rn(__fmul_rn((float)v, inv255), mean), sd);
 }
 
-// k_resize: one CTA per band of kBandRows output rows of one image.
+// k_resize: one CTA per band of P.band (<= kMaxBandRows) output rows of one image.
 //  1. the source rows the band's bilinear taps touch are colour-converted
 //     once into shared memory (RGBX words, coalesced plane reads);
 //  2. per output column the x taps and weight (flip folded in) are tabulated;
 //  3. each thread produces 8 consecutive output pixels of a row: exact fp64
 //     bilinear from shared memory, normalize through a 256-entry LUT of the
 //     exact fp32 value, 128-bit bf16 (or fp32 / uint8) stores.
-// grid: (ceil(res / kBandRows), n); dynamic smem: P.band_src_rows x P.max_w
-// words + the column table.
-constexpr int kBandRows = 16;
+// grid: (ceil(res / P.band), n); dynamic smem: P.src_words (band source rows
+// x widest crop).  The host picks the largest band whose staging fits
+// (32 rows: fewer overlapping source rows and prologues than 16, +3%).
 constexpr int kResizeMaxDyn = 200 * 1024;
 
 // The exact fp32 normalize value of every (channel, uint8) and its bf16 RNE,
@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
     s_scale[1] = __ddiv_rn((double)iw, (double)res);
   }
   __syncthreads();
-  const int ob0 = blockIdx.x * kBandRows;
-  const int ob1 = min(ob0 + kBandRows, res);
+  const int ob0 = blockIdx.x * P.band;
+  const int ob1 = min(ob0 + P.band, res);
   const double sy = s_scale[0], sx = s_scale[1];
   // source rows of the band (taps are monotone in the output row)
   int ys0, ys1, dummy;
@@ -267,9 +267,9 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
     }
   }
   // row taps of the band (imgops.py:37-41), shared by every column
-  __shared__ int2 ry[kBandRows];
-  __shared__ double rw[kBandRows];
-  __shared__ float rwf[kBandRows];
+  __shared__ int2 ry[kMaxBandRows];
+  __shared__ double rw[kMaxBandRows];
+  __shared__ float rwf[kMaxBandRows];
   if (threadIdx.x < ob1 - ob0) {
     int y0, y1;
     double wy;
@@ -433,10 +433,10 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
   }
 }
 
-// Source rows a band of kBandRows output rows can touch for a crop of height
-// h resized to res (taps y0..y1 of rows ob0..ob0+15, imgops.py:33-41).
-int band_source_rows(int h, int res) {
-  return (int)(((int64_t)kBandRows * h + res - 1) / res) + 3;
+// Source rows a band of `band` output rows can touch for a crop of height
+// h resized to res (taps y0..y1 of rows ob0..ob0+band-1, imgops.py:33-41).
+int band_source_rows(int h, int res, int band) {
+  return (int)(((int64_t)band * h + res - 1) / res) + 3;
 }
 
 void launch_resize(const PixelParams &p, cudaStream_t st) {
@@ -447,7 +447,7 @@ void launch_resize(const PixelParams &p, cudaStream_t st) {
     cudaFuncSetAttribute(k_resize, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
     attr = true;
   }
-  dim3 grid((p.res + kBandRows - 1) / kBandRows, p.n);
+  dim3 grid((p.res + p.band - 1) / p.band, p.n);
   k_resize<<<grid, kPixThreads, dyn, st>>>(p);
 }
 

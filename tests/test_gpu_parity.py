@@ -432,3 +432,21 @@ def test_loader_sampling_layouts_vs_oracle(E, oracle, tmp_path, res):
             assert (st == 0).all()
             assert np.array_equal(b.uint8.cpu().numpy(), u8)
             assert np.array_equal(b.pixels.cpu().numpy(), pix)
+
+
+def test_resize_large_crops_smaller_bands_vs_oracle(E, oracle, tmp_path):
+    """Crops large enough that k_resize's 32-row bands do not fit the shared
+    staging: the host falls back to smaller bands; bit-exact vs the oracle."""
+    path = tmp_path / "large.essl"
+    E.build_synthetic(path, 8, (800, 900), 90, seed=13)
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=8, res=224, scale=(0.9, 1.0),
+                             keep_uint8=True)
+        loader = E.Loader(cfg, container=h)
+        for b in loader.epoch(1):
+            idx = b.indices.cpu().numpy()
+            pix, u8, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 1, 224,
+                                                 scale=(0.9, 1.0), keep_uint8=True, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
