@@ -917,7 +917,7 @@ __device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int
 // the list).
 __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, const uint2 *bsl,
                           uint32_t ord, uint32_t lgbase, int b0, uint32_t A, uint32_t nb,
-                          const int32_t base[3], int &range) {
+                          uint32_t nrec, uint32_t nlist, const int32_t base[3], int &range) {
   const uint32_t mcu = A / (uint32_t)C.bpm;
   int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
   int b = b0;
@@ -933,7 +933,11 @@ __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, c
     int16_t *cur = window_block(H, coef, mx, my, b);
     if (cur) {
       if (pv < -32768 || pv > 32767) range = 1;
-      *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + rec.x, (uint32_t)pv);
+      // the block's AC entries run up to the next block's DC entry (or the
+      // list's sentinel): their count rides in the entry's high half
+      const uint32_t next = ord + i + 1 < nrec ? bsl[ord + i + 1].x : nlist;
+      const uint32_t cnt = min(next - rec.x - 1u, 63u);
+      *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + rec.x, ((uint32_t)pv & 0xFFFFu) | (cnt << 16));
     }
     if (++b == C.bpm) {
       b = 0;
@@ -1897,7 +1901,8 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
         int32_t base[3] = {0, 0, 0};
         for (int t = 0; t < lane; t++)
           for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
-        seg_table(C, H, coef, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb, base, range);
+        seg_table(C, H, coef, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb,
+                  min(R.nbs, lbcap), R.nlist, base, range);
       }
     } else if (S.status == 0) {
       // fallback (an owner's unit list overflowed): serial re-decode into
@@ -2063,42 +2068,18 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
   }
   uint2 t = make_uint2(0, 0);
   if (valid) t = *reinterpret_cast<const uint2 *>(cf);
-  if (valid && j == 0) blk[0] = dq ? (int32_t)t.y * dq[0] : (int32_t)t.y;
-  // The block's AC units follow its DC entry up to the next DC-flagged
-  // entry.  Each round the group reads 32 consecutive entries as eight
-  // 16-byte loads (lists are 16-byte aligned per lane; most blocks end in the
-  // first round) and stops at the first DC flag.
-  bool done = !valid;
-  const int gsh = threadIdx.x & 24;  // this group's bit offset in a warp ballot
-  const uint32_t i0 = t.x + 1;       // first AC entry
-  uint32_t base = i0 & ~3u;          // aligned chunk covering i0
-#pragma unroll 1
-  while (__any_sync(0xFFFFFFFFu, !done)) {
-    uint4 q = make_uint4(1u, 1u, 1u, 1u);
-    if (!done) q = __ldg(reinterpret_cast<const uint4 *>(sc.list + base) + j);
-    const uint32_t e4[4] = {q.x, q.y, q.z, q.w};
-    // DC flags of this lane's four entries at or after i0
-    uint32_t m = 0;
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const uint32_t idx = base + 4 * j + u;
-      if (!done && idx >= i0 && (e4[u] & 1)) m |= 1u << u;
-    }
-    // first DC-flagged entry of the round, over the group (lanes in order)
-    const uint32_t any = (__ballot_sync(0xFFFFFFFFu, m != 0) >> gsh) & 0xFFu;
-    const int fl = any ? __ffs(any) - 1 : 8;                      // first lane with a flag
-    const int fu = __shfl_sync(0xFFFFFFFFu, m ? __ffs(m) - 1 : 4, (threadIdx.x & ~7) + (fl & 7));
-    const uint32_t stop = any ? base + 4 * fl + fu : 0xFFFFFFFFu;  // index of the next DC entry
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const uint32_t idx = base + 4 * j + u;
-      if (!done && idx >= i0 && idx < stop) {
-        const int nat = zz[(e4[u] >> 20) & 63];
-        blk[nat] = dq ? entry_value(e4[u]) * dq[nat] : entry_value(e4[u]);
-      }
-    }
-    done = done || any != 0;
-    base += 32;
+  const int32_t dc = (int32_t)(int16_t)(t.y & 0xFFFFu);
+  if (valid && j == 0) blk[0] = dq ? dc * dq[0] : dc;
+  // The block's AC entries (EOB / ZRL markers included, stored as zeros at
+  // positions the block leaves zero) are list[t.x + 1 .. t.x + cnt]: the
+  // group's eight lanes take every eighth one.
+  const uint32_t cnt = valid ? t.y >> 16 : 0u;
+  const uint32_t *ent = sc.list + t.x + 1;
+#pragma unroll 2
+  for (uint32_t u = j; u < cnt; u += 8) {
+    const uint32_t e = __ldg(ent + u);
+    const int nat = zz[(e >> 20) & 63];
+    blk[nat] = dq ? entry_value(e) * dq[nat] : entry_value(e);
   }
   __syncwarp();
 }
