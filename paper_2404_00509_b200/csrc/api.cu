@@ -131,7 +131,7 @@ struct essl_ctx {
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = ESSL_DECODE_SPECULATIVE;
-  int seq_bits = 4096;
+  int seq_bits = 3072;
   int ck_bits = 64;
   int warm_bits = 2048;
   int stage_max = 64 * 1024;
