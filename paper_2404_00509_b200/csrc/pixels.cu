@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
           for (int c = 0; c < 3; c++) {
             const uint32_t lo = __bfloat16_as_ushort(lutb[c][px[0][c]]);
             const uint32_t hi = __bfloat16_as_ushort(lutb[c][px[1][c]]);
-            *reinterpret_cast<uint32_t *>(out + c * plane_sz) = lo | (hi << 16);
+            // streaming store: the model's input is not re-read here; keep L2
+            // for the unit lists / planes of the batches in flight
+            __stcs(reinterpret_cast<unsigned int *>(out + c * plane_sz), lo | (hi << 16));
           }
         } else {
 #pragma unroll
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
         if (pair_ok) {
 #pragma unroll
           for (int c = 0; c < 3; c++)
-            *reinterpret_cast<float2 *>(out + c * plane_sz) = make_float2(lut[c][px[0][c]], lut[c][px[1][c]]);
+            __stcs(reinterpret_cast<float2 *>(out + c * plane_sz), make_float2(lut[c][px[0][c]], lut[c][px[1][c]]));
         } else {
 #pragma unroll
           for (int c = 0; c < 3; c++) {
