@@ -655,10 +655,14 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   pp.plane = c->s.plane;
   pp.n = n;
   pp.res = res;
-  pp.out_kind = any_aug ? ESSL_OUT_NONE : out_kind;
+  // 3-Aug: k_resize finishes the point-op images (writing out / out_u8) and
+  // leaves blur / jitter images in aug_a for k_aug_blur / k_aug_out
+  pp.out_kind = any_aug && !aug_out ? ESSL_OUT_NONE : out_kind;
   pp.out = out;
   pp.out_stride = out_stride;
-  pp.out_u8 = any_aug ? c->aug_a : out_u8;
+  pp.out_u8 = any_aug && !aug_out ? c->aug_a : out_u8;
+  pp.aug = aug_out ? c->d_aug[ring] : nullptr;
+  pp.aug_u8 = c->aug_a;
   pp.trace = c->trace;
   {
     // the largest band (output rows per k_resize CTA) whose source-row
@@ -681,7 +685,7 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   }
   if (aug_out) {
     essl::AugOutParams ap{c->aug_a, c->aug_b, c->d_aug[ring], n, res, res, out_kind, out,
-                          out_stride, out_u8};
+                          out_stride, out_u8, 1};
     Prof pr(c, ESSL_K_AUG, st);
     essl::launch_aug(ap, max_radius, st);
   }

@@ -128,6 +128,12 @@ struct PixelParams {
   uint8_t *out_u8;
   int src_words;       // k_resize shared source rows: band source rows x widest crop
   int band;            // k_resize output rows per CTA (<= kMaxBandRows)
+  // 3-Aug: per-image draws (device) or nullptr.  Images whose op is a point
+  // op (none / grayscale / solarize) without jitter are finished here (point
+  // op fused before normalize); blur or jitter images go to aug_u8 for
+  // k_aug_blur / k_aug_out.
+  const essl_aug *aug;
+  uint8_t *aug_u8;
   CtaTrace trace;
 };
 
@@ -142,6 +148,7 @@ struct AugOutParams {
   void *out;
   int64_t out_stride;
   uint8_t *out_u8;
+  int fused_points;  // 1: point-op-only images were finished by k_resize (skip them)
 };
 
 // splitmix64 (rng.py:27-31)

@@ -103,6 +103,10 @@ __device__ __forceinline__ int bilerp(double wx, double wy, int s00, int s01, in
   return bilerp2(wx, wy, __dsub_rn(1.0, wx), __dsub_rn(1.0, wy), s00, s01, s10, s11);
 }
 
+__device__ __forceinline__ int luma601(int r, int g, int b) {  // imgops.py:78-81
+  return (19595 * r + 38470 * g + 7471 * b + 32768) >> 16;
+}
+
 // imgops.py:231-240: (f32(v) * f32(1/255) - mean) / std, IEEE float32.
 __device__ __forceinline__ float norm_value(int c, int v) {
   const float inv255 = __fdiv_rn(1.0f, 255.0f);
@@ -137,6 +141,7 @@ __global__ void k_init_norm_luts() {
 
 void init_norm_luts() { k_init_norm_luts<<<1, 768>>>(); }
 
+template <bool AUG>
 __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
   TraceScope trace_(P.trace, ESSL_K_RESIZE);
   extern __shared__ __align__(16) uint8_t dyn[];
@@ -147,6 +152,20 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
   const ImgInfo &I = P.info[img];
   if (I.status != 0) return;
   const int res = P.res;
+  // 3-Aug (pipeline.py:88-101): point ops are finished here, blur / jitter
+  // images leave their uint8 resize to k_aug_blur / k_aug_out
+  int out_kind = P.out_kind, aop = ESSL_AUG_OP_NONE, athr = 0;
+  uint8_t *out_u8 = P.out_u8;
+  if (AUG) {
+    const essl_aug &A = P.aug[img];
+    if (A.op == ESSL_AUG_OP_BLUR || A.jitter) {
+      out_kind = ESSL_OUT_NONE;
+      out_u8 = P.aug_u8;
+    } else {
+      aop = A.op;
+      athr = A.threshold;
+    }
+  }
   const int ih = I.rh, iw = I.rw;
   if (P.out_kind == ESSL_OUT_F32_NCHW)
     for (int i = threadIdx.x; i < 768; i += kPixThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
@@ -389,9 +408,18 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
                                (a00 >> (8 * c)) & 255, (a01 >> (8 * c)) & 255,
                                (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
         }
+      if (AUG && aop == ESSL_AUG_OP_GRAY) {  // imgops.py:75-91
+#pragma unroll
+        for (int j = 0; j < 2; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
+      } else if (AUG && aop == ESSL_AUG_OP_SOLARIZE) {  // imgops.py:94-108
+#pragma unroll
+        for (int j = 0; j < 2; j++)
+#pragma unroll
+          for (int c = 0; c < 3; c++) px[j][c] = px[j][c] >= athr ? 255 - px[j][c] : px[j][c];
+      }
       const int oy = ob0 + r;
       const int64_t o = img * stride + (int64_t)oy * res + oxa;
-      if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+      if (out_kind == ESSL_OUT_BF16_NCHW) {
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
         if (pair_ok) {
 #pragma unroll
@@ -409,7 +437,7 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
             if (two) out[c * plane_sz + 1] = lutb[c][px[1][c]];
           }
         }
-      } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+      } else if (out_kind == ESSL_OUT_F32_NCHW) {
         float *out = reinterpret_cast<float *>(P.out) + o;
         if (pair_ok) {
 #pragma unroll
@@ -423,8 +451,8 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
           }
         }
       }
-      if (P.out_u8) {
-        uint8_t *out = P.out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
+      if (out_u8) {
+        uint8_t *out = out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
 #pragma unroll
         for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[0][c];
         if (two)
@@ -446,11 +474,13 @@ void launch_resize(const PixelParams &p, cudaStream_t st) {
   const size_t dyn = (size_t)p.src_words * 4;
   static bool attr = false;  // opt in once to the largest dynamic size api.cu allows
   if (!attr) {
-    cudaFuncSetAttribute(k_resize, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+    cudaFuncSetAttribute(k_resize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+    cudaFuncSetAttribute(k_resize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
     attr = true;
   }
   dim3 grid((p.res + p.band - 1) / p.band, p.n);
-  k_resize<<<grid, kPixThreads, dyn, st>>>(p);
+  if (p.aug) k_resize<true><<<grid, kPixThreads, dyn, st>>>(p);
+  else k_resize<false><<<grid, kPixThreads, dyn, st>>>(p);
 }
 
 // decode_crop output: uint8 [h, w, 3] at out + offsets[img].
@@ -646,9 +676,6 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {  // imgops.py:111-119
   return i >= n ? period - i : i;
 }
 
-__device__ __forceinline__ int luma601(int r, int g, int b) {  // imgops.py:78-81
-  return (19595 * r + 38470 * g + 7471 * b + 32768) >> 16;
-}
 
 // floor(factor * v + (1 - factor) * target + 0.5) clamped (imgops.py:166-196)
 __device__ __forceinline__ int blend1(double f, int v, double target) {
@@ -726,6 +753,7 @@ __device__ __forceinline__ void aug_point(int op, int thr, const uint8_t *p, int
 __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
   const int img = blockIdx.x;
   const essl_aug &A = P.aug[img];
+  if (P.fused_points && A.op != ESSL_AUG_OP_BLUR && !A.jitter) return;  // finished in k_resize
   const int op = A.op, thr = A.threshold, jitter = A.jitter;
   const double fb = A.factors[0], fc = A.factors[1], fs = A.factors[2];
   const int64_t npx = (int64_t)P.h * P.w;
