@@ -429,7 +429,7 @@ struct Reader {
       n += rf ? 32 : 0;
       wi += rf ? 1u : 0u;
       const bool cross = rf && (wi & 7) == 0;  // entered an even chunk
-      if (__any_sync(__activemask(), cross)) issue_pair((wi >> 2) + 2, cross);
+      if (cross) issue_pair((wi >> 2) + 2, true);
     } else {
       // two words loaded ahead in registers: a load has ~8 units to land
       const bool rf = n <= 32;
