@@ -666,13 +666,20 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   pp.trace = c->trace;
   {
     // the largest band (output rows per k_resize CTA) whose source-row
-    // staging fits the shared-memory budget for this batch's crops
-    int band = essl::kMaxBandRows, words = 0;
-    for (;; band /= 2) {
-      words = 0;
+    // staging for this batch's crops keeps 4 CTAs per SM (<= 48 KB), else
+    // the largest that fits the 200 KB budget at all
+    auto staging = [&](int b) {
+      int w = 0;
       for (int i = 0; i < n; i++)
-        words = std::max(words, essl::band_source_rows(samples[i].h, res, band) * std::max(samples[i].w, 1));
-      if ((size_t)(words + 3) / 4 * 4 * 4 <= 200 * 1024 || band == 1) break;
+        w = std::max(w, essl::band_source_rows(samples[i].h, res, b) * std::max(samples[i].w, 1));
+      return w;
+    };
+    int band = essl::kMaxBandRows, words = staging(band);
+    while (band > 1 && (size_t)(words + 3) / 4 * 4 * 4 > 48 * 1024) words = staging(band /= 2);
+    if ((size_t)(words + 3) / 4 * 4 * 4 > 48 * 1024) {
+      band = essl::kMaxBandRows;
+      words = staging(band);
+      while (band > 1 && (size_t)(words + 3) / 4 * 4 * 4 > 200 * 1024) words = staging(band /= 2);
     }
     pp.band = band;
     pp.src_words = (words + 3) / 4 * 4;
