@@ -175,6 +175,10 @@ int essl_debug_lanes(essl_ctx *ctx, int32_t *out, int n);
 int essl_trace_read(essl_ctx *ctx, uint64_t *out, int max);
 const char *essl_last_error(void);
 const char *essl_version(void);
+/* Stream-ordered copy of `bytes` between host (pinned) and device memory
+ * (cudaMemcpyDefault), for the loader's per-batch index / label / status
+ * transfers without switching the caller's current stream. */
+int essl_memcpy_async(void *dst, const void *src, uint64_t bytes, void *stream);
 
 /* ---- staging (host bytes -> device) -------------------------------------
  * Replaces: ContainerHandle.read_sample (container.py:249-265) bytes path.

@@ -41,7 +41,7 @@ EXPORTS = (
     "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
     "essl_mask_count", "essl_encode_jpeg", "essl_synth_image", "essl_decode_rrc_aug",
     "essl_augment_u8", "essl_aug_draw", "essl_aug_batch", "essl_debug_lanes",
-    "essl_trace_read",
+    "essl_trace_read", "essl_memcpy_async",
 )
 
 
@@ -128,6 +128,7 @@ def lib():
         "essl_debug_lanes": (i32, [P, P, i32]),
         "essl_trace_read": (i32, [P, P, i32]),
         "essl_last_error": (ctypes.c_char_p, []),
+        "essl_memcpy_async": (i32, [P, P, u64, P]),
         "essl_version": (ctypes.c_char_p, []),
         "essl_stage": (i32, [P, i32, P, P, i32, P, i32, P, P]),
         "essl_stage_pinned": (i32, [P, i32, P, P, P, i32, P, P, P]),

@@ -283,6 +283,13 @@ extern "C" {
 const char *essl_last_error(void) { return g_err.c_str(); }
 const char *essl_version(void) { return "essl-b200 0.1 (sm_100a)"; }
 
+int essl_memcpy_async(void *dst, const void *src, uint64_t bytes, void *stream) {
+  if (bytes && (!dst || !src)) return fail(ESSL_E_ARG, "essl_memcpy_async: null pointer");
+  if (!bytes) return ESSL_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return ESSL_OK;
+}
+
 int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, int flags,
                     essl_ctx **out) {
   (void)flags;

@@ -197,8 +197,9 @@ class _HostRing:
     def __init__(self, depth: int, batch: int, result_words: int):
         import torch
         self.depth = depth
-        self.idx = [torch.empty(batch, dtype=torch.int64, pin_memory=True) for _ in range(depth)]
-        self.lab = [torch.empty(batch, dtype=torch.int64, pin_memory=True) for _ in range(depth)]
+        # indices then labels of a batch of b, contiguous: one H2D copy
+        self.il = [torch.empty(2 * batch, dtype=torch.int64, pin_memory=True) for _ in range(depth)]
+        self.il_np = [t.numpy() for t in self.il]
         self.res = [torch.empty((batch, result_words), dtype=torch.int32, pin_memory=True)
                     for _ in range(depth)]
         self.ev = [None] * depth
@@ -396,18 +397,19 @@ class Loader:
 
         pixels = out("pixels", (b, 3, res, res), self._out_dtype)
         u8 = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
-        results = eng.new_results(b)
+        results = out("results", (b, ctypes.sizeof(N.EsslResult) // 4), torch.int32)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
-        # host->device copies first: a copy queued behind this batch's kernels
-        # would hold up later batches' copies on the shared copy engine
-        hidx, hlab, res_host = ring.idx[slot][:b], ring.lab[slot][:b], ring.res[slot][:b]
-        hidx.numpy()[:] = idxs
-        hlab.numpy()[:] = self._labels_np[idxs]
-        with torch.cuda.stream(st):  # pinned sources: truly asynchronous copies
-            indices = out("indices", (b,), torch.int64)
-            labels = out("labels", (b,), torch.int64)
-            indices.copy_(hidx, non_blocking=True)
-            labels.copy_(hlab, non_blocking=True)
+        # host->device copies first (a copy queued behind this batch's kernels
+        # would hold up later batches' copies on the shared copy engine):
+        # indices and labels in one pinned buffer, one stream-ordered copy
+        hil, hil_np, res_host = ring.il[slot], ring.il_np[slot], ring.res[slot][:b]
+        hil_np[:b] = idxs
+        hil_np[b:2 * b] = self._labels_np[idxs]
+        il = out("il", (2 * b,), torch.int64)
+        sp = ctypes.c_void_p(st.cuda_stream)
+        L = N.lib()
+        N.check(L.essl_memcpy_async(N.ptr(il), N.ptr(hil), 16 * b, sp), "essl_memcpy_async")
+        indices, labels = il[:b], il[b:]
         eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st, aug=aug)
         mask = keep = restore = None
         if self.mask_spec is not None:
@@ -415,11 +417,12 @@ class Loader:
             keep = out("keep", (b, T - k), torch.int64)
             restore = out("restore", (b, T), torch.int64)
             eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=st)
-        with torch.cuda.stream(st):
-            res_host.copy_(results, non_blocking=True)
-        for t in (pixels, u8, results, mask, keep, restore, indices, labels):
-            if t is not None:
-                t.record_stream(st)
+        N.check(L.essl_memcpy_async(N.ptr(res_host), N.ptr(results), results.numel() * 4, sp),
+                "essl_memcpy_async")
+        if not cfg.reuse_outputs:  # fresh tensors: tell the allocator about st
+            for t in (pixels, u8, results, mask, keep, restore, il):
+                if t is not None:
+                    t.record_stream(st)
         ev = torch.cuda.Event()
         ev.record(st)
         ring.ev[slot] = ev
