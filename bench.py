@@ -87,11 +87,12 @@ def peaks() -> dict:
 def make_dataset(wl: dict, pool: int, out_dir: Path, seed: int = 1) -> Path:
     from paper_2404_00509_b200 import build_synthetic
     rec = wl.get("records")
-    path = out_dir / f"pool_{wl['side']}_{wl['quality']}_{pool}_{rec or pool}.essl"
+    rst = wl.get("restart", 0)
+    path = out_dir / f"pool_{wl['side']}_{wl['quality']}_{pool}_{rec or pool}_r{rst}.essl"
     if not path.exists():
         t = time.perf_counter()
         info = build_synthetic(path, pool, wl["side"], wl["quality"], classes=1000, seed=seed,
-                               n_records=rec)
+                               n_records=rec, restart_interval=rst)
         log(f"[bench] built {pool} images ({info['mean_payload']:.0f} B mean) in "
             f"{time.perf_counter() - t:.1f}s")
     return path
@@ -502,6 +503,9 @@ def main():
                     help="e2e: k_host_gather CTAs (ESSL_OPT_GATHER_CTAS; -1: library default)")
     ap.add_argument("--staging", default="gather", choices=["gather", "copy"],
                     help="e2e host staging: bus-read gather kernel or host threads + one copy")
+    ap.add_argument("--restart", type=int, default=0,
+                    help="JPEGs with a restart marker every N MCUs (SURVEY 8(f) f3 variant; "
+                         "0: none, as the reference builder)")
     ap.add_argument("--batch", type=int, default=0,
                     help="images per step (0: the workload's batch; analysis knob)")
     ap.add_argument("--aug", default="simple", choices=["simple", "3aug", "3aug+"],
@@ -510,6 +514,9 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.batch > 0:
         wl["batch"] = args.batch
+    if args.restart > 0:
+        wl["restart"] = args.restart
+        wl["desc"] += f"; restart interval {args.restart} MCUs (f3 variant)"
     if args.aug != "simple":
         wl["aug"] = args.aug
         wl["desc"] = wl["desc"].replace("+ flip +", f"+ flip + {args.aug} +")

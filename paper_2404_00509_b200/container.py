@@ -299,17 +299,21 @@ def synth_image(seed: int, height: int, width: int) -> np.ndarray:
 
 def build_synthetic(out_path: str | Path, n_images: int, side: int | tuple[int, int],
                     quality: int, classes: int = 4, seed: int = 1,
-                    workers: int | None = None, n_records: int | None = None) -> dict:
+                    workers: int | None = None, n_records: int | None = None,
+                    restart_interval: int = 0) -> dict:
     """Synthetic benchmark container: ``n_images`` distinct payloads of
     side x side (or a (min, max) side range) at ``quality``.  With
-    ``n_records`` > n_images the record table aliases the pool (cfg5)."""
+    ``n_records`` > n_images the record table aliases the pool (cfg5).
+    ``restart_interval`` > 0 writes DRI + RSTn every that many MCUs (the
+    opt-in restart-marker variant; not byte-identical to
+    the reference builder's output, which has no restarts)."""
     lo, hi = (side, side) if isinstance(side, int) else side
     rng = np.random.default_rng(seed)
     dims = [(int(rng.integers(lo, hi + 1)), int(rng.integers(lo, hi + 1))) for _ in range(n_images)]
 
     def make(i):
         h, w = dims[i]
-        return encode_jpeg(synth_image(seed * 1_000_003 + i, h, w), quality)
+        return encode_jpeg(synth_image(seed * 1_000_003 + i, h, w), quality, restart_interval)
 
     with ThreadPoolExecutor(max_workers=workers or os.cpu_count() or 1) as pool:
         payloads = list(pool.map(make, range(n_images)))

@@ -450,3 +450,24 @@ def test_resize_large_crops_smaller_bands_vs_oracle(E, oracle, tmp_path):
             assert (st == 0).all()
             assert np.array_equal(b.uint8.cpu().numpy(), u8)
             assert np.array_equal(b.pixels.cpu().numpy(), pix)
+
+
+@pytest.mark.parametrize("ri", [1, 4, 16])
+def test_restart_variant_loader_vs_oracle(E, oracle, tmp_path, ri):
+    """The restart-marker container variant (DRI + RSTn every
+    ri MCUs): restart intervals decode from exact entry states, one per lane;
+    uint8 and float32 bit-exact vs the oracle."""
+    path = tmp_path / f"rst{ri}.essl"
+    E.build_synthetic(path, 24, (200, 300), 95, seed=17, restart_interval=ri)
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=12, res=160, keep_uint8=True,
+                             mask_ratio=0.75)
+        loader = E.Loader(cfg, container=h)
+        for b in loader.epoch(4):
+            idx = b.indices.cpu().numpy()
+            pix, u8, mask, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 4, 160,
+                                                    mask_ratio=0.75, keep_uint8=True, nthreads=8)
+            assert (st == 0).all()
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
+            assert np.array_equal(b.mask.cpu().numpy(), mask)
