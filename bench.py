@@ -276,6 +276,8 @@ def run_gpu(args, wl):
         loader.set_option(N.ESSL_OPT_SEQ_BITS, args.seq_bits)
     if args.warm_bits >= 0:
         loader.set_option(N.ESSL_OPT_WARMUP_BITS, args.warm_bits)
+    if args.ck_bits > 0:
+        loader.set_option(N.ESSL_OPT_CHECKPOINT_BITS, args.ck_bits)
     if args.stage_bytes >= 0:
         loader.set_option(N.ESSL_OPT_STAGE_BYTES, args.stage_bytes)
     handle = loader.handle
@@ -494,6 +496,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
+    ap.add_argument("--ck-bits", type=int, default=0,
+                    help="minimum checkpoint spacing in bits (ESSL_OPT_CHECKPOINT_BITS; 0: default)")
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
     ap.add_argument("--stage-bytes", type=int, default=-1,
                     help="ESSL_OPT_STAGE_BYTES (0: entropy lanes read the clean stream from global)")
