@@ -325,6 +325,8 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
   CKC(cudaMalloc(&c->s.hdr, essl::decode_hdr_bytes() * max_batch));
   CKC(cudaMalloc(&c->s.ck, essl::ckpt_bytes() * essl::kEntropyLanes * essl::kCheckpoints * max_batch));
+  CKC(cudaMalloc(&c->s.tabcache, essl::tabcache_bytes()));
+  CKC(cudaMemset(c->s.tabcache, 0, essl::tabcache_bytes()));
   // unit lists + block records per image: lanes x (cap + 8 + 2 (cap/2 + 10))
   // u32, cap = (slen + warm + continuation)/4 + 68, lanes x slen <= 8 x payload
   c->s.list_cap = (uint64_t)max_batch *
@@ -370,6 +372,7 @@ int essl_ctx_destroy(essl_ctx *c) {
   cudaFree(c->s.info);
   cudaFree(c->s.hdr);
   cudaFree(c->s.ck);
+  cudaFree(c->s.tabcache);
   cudaFree(c->s.list);
   cudaFree(c->d_offsets);
   for (int r = 0; r < kDescRing; r++) {

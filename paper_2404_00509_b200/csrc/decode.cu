@@ -125,6 +125,18 @@ struct __align__(16) DecodeHdr : DecodeHead {
   HuffTab tab[kMaxTables];
 };
 
+// Built Huffman tables reused across images (per context, persistent):
+// slot t caches the t-th distinct table of the first image that claimed it
+// (state 0 empty, 1 being written, 2 ready).  An image whose t-th table has
+// the same class and the same DHT counts + symbols copies the built table
+// instead of building it (a batch of images from one encoder shares them).
+struct __align__(16) TabCacheSlot {
+  unsigned int state;
+  int len, is_dc, pad;
+  uint8_t key[16 + 256];  // DHT counts + symbols
+  HuffTab tab;
+};
+
 struct ParseState {
   int pos, n, ri, have_sof, progressive, width, height, ncomp, nscans;
   int comp_id[3], comp_h[3], comp_v[3], comp_tq[3];
@@ -1619,15 +1631,43 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     H.tab_index_word = w;
   }
   __syncthreads();
+  // ---- table cache lookup: slot t <-> this image's t-th distinct table ----
+  __shared__ int s_hit[kMaxTables];
+  TabCacheSlot *cache = reinterpret_cast<TabCacheSlot *>(P.s.tabcache);
+  if (H.status == 0) {
+    for (int t = 0; t < H.ntab; t++) {
+      const HuffTab &T = G->tab[t];
+      const int len = 16 + T.nvals;
+      TabCacheSlot &C = cache[t];
+      unsigned int st;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(&C.state) : "memory");
+      bool eq = st == 2u && C.len == len && C.is_dc == T.is_dc;
+      for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == raw[T.dht_pos + i];
+      const int hit = __syncthreads_and(eq);
+      if (hit) {  // copy the built table (keep this image's own dht_pos)
+        const int4 *src = reinterpret_cast<const int4 *>(&C.tab);
+        int4 *dst = reinterpret_cast<int4 *>(&G->tab[t]);
+        const int pos = T.dht_pos;
+        __syncthreads();
+        for (int i = tid; i < (int)(sizeof(HuffTab) / 16); i += kNT) dst[i] = src[i];
+        __syncthreads();
+        if (tid == 0) G->tab[t].dht_pos = pos;
+      }
+      if (tid == 0) s_hit[t] = hit;
+    }
+  }
+  __syncthreads();
   if (H.status == 0) {
     const int ntab = H.ntab;
     for (int e = tid; e < ntab * 256; e += kNT) {
+      if (s_hit[e >> 8]) continue;
       HuffTab &T = G->tab[e >> 8];
       const int v = e & 255;
       T.vals[v] = v < T.nvals ? (uint8_t)raw[T.dht_pos + 16 + v] : 0;
     }
     __syncthreads();
     for (int t = 0; t < ntab; t++) {
+      if (s_hit[t]) continue;
       HuffTab &T = G->tab[t];
       int lim[17], first[17], vptr[17];
 #pragma unroll
@@ -1675,6 +1715,29 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     }
   }
   __syncthreads();
+  // ---- publish newly built tables to empty cache slots ----------------------
+  if (H.status == 0) {
+    __shared__ int s_claim;
+    for (int t = 0; t < H.ntab; t++) {
+      if (s_hit[t]) continue;
+      if (tid == 0) s_claim = atomicCAS(&cache[t].state, 0u, 1u) == 0u;
+      __syncthreads();
+      if (s_claim) {
+        TabCacheSlot &C = cache[t];
+        const HuffTab &T = G->tab[t];
+        const int len = 16 + T.nvals;
+        for (int i = tid; i < len; i += kNT) C.key[i] = raw[T.dht_pos + i];
+        const int4 *src = reinterpret_cast<const int4 *>(&T);
+        int4 *dst = reinterpret_cast<int4 *>(&C.tab);
+        for (int i = tid; i < (int)(sizeof(HuffTab) / 16); i += kNT) dst[i] = src[i];
+        if (tid == 0) { C.len = len; C.is_dc = T.is_dc; }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&C.state), "r"(2u) : "memory");
+      }
+      __syncthreads();
+    }
+  }
   // ---- hand over: header (+ used tables) to global ---------------------------
   {
     const int words = (int)(sizeof(DecodeHead) / 16);  // the tables are already in G
@@ -2175,6 +2238,7 @@ constexpr int kMaxDynSmem = 160 * 1024;
 
 size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
 size_t ckpt_bytes() { return sizeof(Ckpt); }
+size_t tabcache_bytes() { return sizeof(TabCacheSlot) * kMaxTables; }
 
 void launch_prep(const DecodeParams &p0, cudaStream_t st, int max_len) {
   if (p0.n <= 0) return;

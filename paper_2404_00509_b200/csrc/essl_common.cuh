@@ -65,6 +65,7 @@ struct Scratch {
   struct Ckpt *ck;  // per-image checkpoints [32 lanes][kCheckpoints] (k_entropy)
   uint32_t *list;   // unit lists (k_entropy), carved per image with counters[3]
   uint64_t list_cap;  // entries
+  uint8_t *tabcache;  // built Huffman tables reused across images (k_prep; tabcache_bytes())
 };
 
 // Optional per-CTA execution trace (ESSL_OPT_TRACE): {start ns, end ns,
@@ -180,6 +181,7 @@ void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
 size_t ckpt_bytes();
+size_t tabcache_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);
 void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, int ctas,
