@@ -1575,11 +1575,15 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
   if (tid == 0) S.ph[3] = clock64();
 
   // ---- Huffman tables (codec.py:272-304): DC slots first, then AC ----------
-  // Canonical first/lim/vptr per distinct (class,id) table; the long-code
-  // prefixes (codes longer than kFastBits) get second-level sub-tables.
+  // 1. thread 0 maps the scan's slots to distinct (class, id) tables;
+  // 2. each table is looked up in the context's table cache (slot t = the
+  //    t-th distinct table; same class + DHT counts + symbols -> copy);
+  // 3. thread 0 derives the canonical first/lim/vptr of the tables that
+  //    missed (and the kFastBits-bit prefixes of their long codes, which get
+  //    second-level sub-tables); 4. all threads fill the lookup tables.
+  __shared__ int s_tpos[kMaxTables], s_ttot[kMaxTables], s_tdc[kMaxTables], s_hit[kMaxTables];
   if (tid == 0 && H.status == 0) {
     int ntab = 0;
-    int tab_pos[kMaxTables];
     int slot_dc[4] = {0, 0, 0, 0}, slot_ac[4] = {0, 0, 0, 0};
     for (int pass = 0; pass < 2 && H.status == 0; pass++) {
       for (int s = 0; s < H.ns && H.status == 0; s++) {
@@ -1588,38 +1592,12 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
         if (pos < 0) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_UNDEFINED, -1); break; }
         if (tot > 256) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_TOO_MANY, -1); break; }
         int ti = -1;
-        for (int t = 0; t < ntab; t++) if (tab_pos[t] == pos) ti = t;
+        for (int t = 0; t < ntab; t++) if (s_tpos[t] == pos) ti = t;
         if (ti < 0) {
           ti = ntab++;
-          tab_pos[ti] = pos;
-          HuffTab &T = G->tab[ti];
-          int code = 0, vi = 0;
-          T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
-          for (int L = 1; L <= 16; L++) {
-            const int cnt = raw[pos + L - 1];
-            T.first[L] = code;
-            T.vptr[L] = (int16_t)vi;
-            if (cnt && code + cnt > (1 << L)) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
-            code += cnt;
-            vi += cnt;
-            T.lim[L] = code;
-            code <<= 1;
-          }
-          T.dht_pos = pos;
-          T.nvals = tot;
-          T.is_dc = pass == 0;
-          // distinct kFastBits-bit prefixes of the long codes, in code order
-          int nsub = 0, last = -1;
-          for (int L = kFastBits + 1; L <= 16; L++)
-            for (int c = T.first[L]; c < T.lim[L]; c++) {
-              const int pf = c >> (L - kFastBits);
-              if (pf != last) {
-                if (nsub < kSubTabs) S.sub_pf[ti][nsub] = (uint16_t)pf;
-                nsub++;
-                last = pf;
-              }
-            }
-          T.nsub = nsub;  // > kSubTabs: overflow, long codes use the canonical walk
+          s_tpos[ti] = pos;
+          s_ttot[ti] = tot;
+          s_tdc[ti] = pass == 0;
         }
         if (pass == 0) slot_dc[s] = ti; else slot_ac[s] = ti;
       }
@@ -1631,29 +1609,59 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     H.tab_index_word = w;
   }
   __syncthreads();
-  // ---- table cache lookup: slot t <-> this image's t-th distinct table ----
-  __shared__ int s_hit[kMaxTables];
   TabCacheSlot *cache = reinterpret_cast<TabCacheSlot *>(P.s.tabcache);
   if (H.status == 0) {
     for (int t = 0; t < H.ntab; t++) {
-      const HuffTab &T = G->tab[t];
-      const int len = 16 + T.nvals;
+      const int len = 16 + s_ttot[t], pos = s_tpos[t];
       TabCacheSlot &C = cache[t];
       unsigned int st;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(&C.state) : "memory");
-      bool eq = st == 2u && C.len == len && C.is_dc == T.is_dc;
-      for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == raw[T.dht_pos + i];
+      bool eq = st == 2u && C.len == len && C.is_dc == s_tdc[t];
+      for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == raw[pos + i];
       const int hit = __syncthreads_and(eq);
-      if (hit) {  // copy the built table (keep this image's own dht_pos)
+      if (hit) {  // copy the built table (with this image's own dht_pos)
         const int4 *src = reinterpret_cast<const int4 *>(&C.tab);
         int4 *dst = reinterpret_cast<int4 *>(&G->tab[t]);
-        const int pos = T.dht_pos;
-        __syncthreads();
         for (int i = tid; i < (int)(sizeof(HuffTab) / 16); i += kNT) dst[i] = src[i];
         __syncthreads();
         if (tid == 0) G->tab[t].dht_pos = pos;
       }
       if (tid == 0) s_hit[t] = hit;
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && H.status == 0) {
+    for (int ti = 0; ti < H.ntab && H.status == 0; ti++) {
+      if (s_hit[ti]) continue;
+      const int pos = s_tpos[ti];
+      HuffTab &T = G->tab[ti];
+      int code = 0, vi = 0;
+      T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
+      int nsub = 0, last = -1;
+      for (int L = 1; L <= 16; L++) {
+        const int cnt = raw[pos + L - 1];
+        T.first[L] = code;
+        T.vptr[L] = (int16_t)vi;
+        if (cnt && code + cnt > (1 << L)) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
+        // distinct kFastBits-bit prefixes of the long codes, in code order
+        if (L > kFastBits)
+          for (int c = code; c < code + cnt; c++) {
+            const int pf = c >> (L - kFastBits);
+            if (pf != last) {
+              if (nsub < kSubTabs) S.sub_pf[ti][nsub] = (uint16_t)pf;
+              nsub++;
+              last = pf;
+            }
+          }
+        code += cnt;
+        vi += cnt;
+        T.lim[L] = code;
+        code <<= 1;
+      }
+      T.dht_pos = pos;
+      T.nvals = s_ttot[ti];
+      T.is_dc = s_tdc[ti];
+      T.nsub = nsub;  // > kSubTabs: overflow, long codes use the canonical walk
     }
   }
   __syncthreads();
