@@ -377,6 +377,8 @@ def run_gpu(args, wl):
         l2 = E.Loader(cfg2, container=handle, engine=loader.engine)
         if args.gather_ctas >= 0:
             l2.set_option(N.ESSL_OPT_GATHER_CTAS, args.gather_ctas)
+        if args.gather_tma >= 0:
+            l2.set_option(N.ESSL_OPT_GATHER_TMA, args.gather_tma)
         steps_e2e = min(args.steps, max(1, len(handle) // ws // B))
         for k, b in enumerate(l2.epoch(1)):  # warm the staging pool and output ring
             if k + 1 >= min(steps_e2e, 3 * cfg.streams + 3):
@@ -505,6 +507,8 @@ def main():
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--gather-ctas", type=int, default=-1,
                     help="e2e: k_host_gather CTAs (ESSL_OPT_GATHER_CTAS; -1: library default)")
+    ap.add_argument("--gather-tma", type=int, default=-1,
+                    help="e2e: 1 = bus-read gather with bulk (TMA) copies (ESSL_OPT_GATHER_TMA)")
     ap.add_argument("--staging", default="gather", choices=["gather", "copy"],
                     help="e2e host staging: bus-read gather kernel or host threads + one copy")
     ap.add_argument("--restart", type=int, default=0,

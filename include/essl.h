@@ -68,7 +68,7 @@ extern "C" {
 #define ESSL_OPT_WARMUP_BITS 5  /* lanes start this far before their subsequence (0..4096) */
 #define ESSL_OPT_STAGE_BYTES 6  /* largest clean stream staged in shared memory (0: never) */
 #define ESSL_OPT_GATHER_CTAS 7  /* k_host_gather CTAs (bus-read gather; 0: one per payload) */
-#define ESSL_OPT_GATHER_TMA 8   /* 1: bus-read gather with bulk (TMA) copies */
+#define ESSL_OPT_GATHER_TMA 8   /* 1 (default): bus-read gather with bulk (TMA) copies; 0: LSU loads */
 #define ESSL_OPT_DEBUG_LANES 9  /* 1: record per-lane speculative-decode state (essl_debug_lanes) */
 #define ESSL_OPT_TRACE 10       /* n > 0: record up to n CTA executions (essl_trace_read); 0 off */
 

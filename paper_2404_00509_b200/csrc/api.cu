@@ -136,7 +136,7 @@ struct essl_ctx {
   int warm_bits = 2048;
   int stage_max = 64 * 1024;
   int gather_ctas = 4;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
-  bool gather_tma = false;
+  bool gather_tma = true;   // ESSL_OPT_GATHER_TMA: bulk (TMA) bus reads, e2e +9% over LSU loads
   int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
   essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
