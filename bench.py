@@ -260,7 +260,11 @@ def run_gpu(args, wl):
 
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl")
+        # ESSL_BENCH_BACKEND=gloo: functional check of the multi-rank path with
+        # ranks sharing GPUs (device = local rank mod device count); the data
+        # path has no collective either way, only the reporting reduction
+        dist.init_process_group(os.environ.get("ESSL_BENCH_BACKEND", "nccl"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     data_dir = Path(tempfile.mkdtemp(prefix=f"essl_bench_{rank}_"))

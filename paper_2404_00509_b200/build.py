@@ -48,7 +48,10 @@ def _digest() -> str:
         if f.suffix in (".cu", ".cuh", ".cpp", ".h"):
             h.update(f.name.encode() + f.read_bytes())
     h.update((ROOT / "include" / "essl.h").read_bytes())
-    h.update(" ".join(_flags("x.cu") + _flags("x.cpp")).encode())
+    # flags without the checkout's absolute path: a copied tree (the GPU box)
+    # sees the same digest and reuses the shipped library
+    flags = " ".join(_flags("x.cu") + _flags("x.cpp")).replace(str(ROOT), "<root>")
+    h.update(flags.encode())
     return h.hexdigest()
 
 
@@ -61,6 +64,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     dig = _digest()
     if LIB.exists() and stamp.exists() and stamp.read_text() == dig and not force:
         return LIB
+    # one builder at a time (torchrun ranks, parallel test workers): the
+    # others wait, then find the stamp current
+    import fcntl
+    with open(OUT_DIR / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if LIB.exists() and stamp.exists() and stamp.read_text() == dig and not force:
+            return LIB
+        return _build_locked(dig, stamp, verbose)
+
+
+def _build_locked(dig: str, stamp: Path, verbose: bool) -> Path:
     nvcc = _nvcc()
     objs = []
 
