@@ -710,28 +710,46 @@ __global__ void __launch_bounds__(kAugBlurThreads) k_aug_blur(const uint8_t *src
   const size_t img_off = (size_t)blockIdx.y * h * w * 3;
   const uint8_t *in = src + img_off;
   if (threadIdx.x < nt) wt[threadIdx.x] = A.weights[threadIdx.x];
-  for (int i = threadIdx.x; i < sh * spitch; i += kAugBlurThreads) {
-    const int yy = i / spitch, rem = i - yy * spitch;
-    const int xx = rem / 3, c = rem - xx * 3;
-    s[i] = in[((size_t)reflect_idx(ty0 - r + yy, h) * w + reflect_idx(tx0 - r + xx, w)) * 3 + c];
+  // rows by warp, bytes by lane (no per-element division); tiles whose halo
+  // lies inside the image copy rows straight, border tiles reflect-index
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kAugBlurThreads / 32;
+  const bool inner = ty0 - r >= 0 && ty0 + th + r <= h && tx0 - r >= 0 && tx0 + tw + r <= w;
+  for (int yy = warp; yy < sh; yy += nw) {
+    const int sy = inner ? ty0 - r + yy : reflect_idx(ty0 - r + yy, h);
+    const uint8_t *srow = in + (size_t)sy * w * 3;
+    uint8_t *drow = s + yy * spitch;
+    if (inner) {
+      const uint8_t *p = srow + (size_t)(tx0 - r) * 3;
+      for (int rem = lane; rem < spitch; rem += 32) drow[rem] = p[rem];
+    } else {
+      for (int rem = lane; rem < spitch; rem += 32) {
+        const int xx = rem / 3, c = rem - xx * 3;
+        drow[rem] = srow[reflect_idx(tx0 - r + xx, w) * 3 + c];
+      }
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < sh * tpitch; i += kAugBlurThreads) {
-    const int yy = i / tpitch, rem = i - yy * tpitch;
-    const uint8_t *row = s + yy * spitch + rem;  // tap k at row[3 k]
-    double acc = 0.0;
-    for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], (double)row[3 * k]));
-    tmp[i] = acc;
+  for (int yy = warp; yy < sh; yy += nw) {
+    const uint8_t *srow = s + yy * spitch;
+    double *trow = tmp + yy * tpitch;
+    for (int rem = lane; rem < tpitch; rem += 32) {
+      const uint8_t *row = srow + rem;  // tap k at row[3 k]
+      double acc = 0.0;
+      for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], (double)row[3 * k]));
+      trow[rem] = acc;
+    }
   }
   __syncthreads();
   uint8_t *out = dst + img_off;
-  for (int i = threadIdx.x; i < th * tpitch; i += kAugBlurThreads) {
-    const int yy = i / tpitch, rem = i - yy * tpitch;
-    const double *col = tmp + yy * tpitch + rem;
-    double acc = 0.0;
-    for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], col[k * tpitch]));
-    const int v = __double2int_rz(__dadd_rn(acc, 0.5));
-    out[((size_t)(ty0 + yy) * w + tx0) * 3 + rem] = (uint8_t)(v > 255 ? 255 : v);
+  for (int yy = warp; yy < th; yy += nw) {
+    uint8_t *orow = out + ((size_t)(ty0 + yy) * w + tx0) * 3;
+    for (int rem = lane; rem < tpitch; rem += 32) {
+      const double *col = tmp + yy * tpitch + rem;
+      double acc = 0.0;
+      for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, __dmul_rn(wt[k], col[k * tpitch]));
+      const int v = __double2int_rz(__dadd_rn(acc, 0.5));
+      orow[rem] = (uint8_t)(v > 255 ? 255 : v);
+    }
   }
 }
 
