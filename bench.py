@@ -383,9 +383,10 @@ def run_gpu(args, wl):
             l2.set_option(N.ESSL_OPT_GATHER_CTAS, args.gather_ctas)
         if args.gather_tma >= 0:
             l2.set_option(N.ESSL_OPT_GATHER_TMA, args.gather_tma)
-        steps_e2e = min(args.steps, max(1, len(handle) // ws // B))
-        for k, b in enumerate(l2.epoch(1)):  # warm the staging pool and output ring
-            if k + 1 >= min(steps_e2e, 3 * cfg.streams + 3):
+        # warm every stream's staging slots and output ring (across epoch
+        # boundaries: small shards have fewer batches per epoch than streams)
+        for k, b in enumerate(l2.epochs(100)):
+            if k + 1 >= 3 * cfg.streams + 3:
                 break
         torch.cuda.synchronize(dev)
         if ws > 1:
