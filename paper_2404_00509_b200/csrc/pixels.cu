@@ -768,6 +768,10 @@ __device__ __forceinline__ void aug_point(int op, int thr, const uint8_t *p, int
 // (imgops.py:199-216; integer sum, exact), then per pixel the point op,
 // brightness, contrast, saturation (imgops.py:213-227), normalize through the
 // exact LUT (imgops.py:231-240) into bf16/f32 NCHW and/or the uint8 view.
+// Brightness (target 0) and contrast (target the image mean) are functions
+// of one uint8 value, so each is tabulated once per image (256 float64
+// blends, the same operations as per pixel); only saturation, whose target
+// is the pixel's own luma, stays per pixel.
 __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
   const int img = blockIdx.x;
   const essl_aug &A = P.aug[img];
@@ -779,28 +783,33 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
   __shared__ float lut[3][256];
   __shared__ __nv_bfloat16 lutb[3][256];
   __shared__ unsigned long long part[kAugOutThreads / 32];
+  __shared__ uint8_t bri[256], con[256];
+  static_assert(kAugOutThreads >= 256, "one thread per table entry");
   if (P.out_kind == ESSL_OUT_F32_NCHW)
     for (int i = threadIdx.x; i < 768; i += kAugOutThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
   else if (P.out_kind == ESSL_OUT_BF16_NCHW)
     for (int i = threadIdx.x; i < 768; i += kAugOutThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
-  double mean = 0.0;
+  if (jitter && threadIdx.x < 256) bri[threadIdx.x] = (uint8_t)blend1(fb, threadIdx.x, 0.0);
+  __syncthreads();
   if (jitter) {
     unsigned long long sum = 0;
     for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
       int px[3];
       aug_point(op, thr, src + 3 * i, px);
-      sum += (unsigned)luma601(blend1(fb, px[0], 0.0), blend1(fb, px[1], 0.0), blend1(fb, px[2], 0.0));
+      sum += (unsigned)luma601(bri[px[0]], bri[px[1]], bri[px[2]]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = sum;
-  }
-  __syncthreads();
-  if (jitter) {
-    unsigned long long tot = 0;
+    __syncthreads();
+    if (threadIdx.x < 256) {
+      unsigned long long tot = 0;
 #pragma unroll
-    for (int k = 0; k < kAugOutThreads / 32; k++) tot += part[k];
-    mean = __ddiv_rn((double)tot, (double)npx);  // acc / (h * w), acc an exact integer
+      for (int k = 0; k < kAugOutThreads / 32; k++) tot += part[k];
+      const double mean = __ddiv_rn((double)tot, (double)npx);  // acc / (h * w), acc an exact integer
+      con[threadIdx.x] = (uint8_t)blend1(fc, threadIdx.x, mean);
+    }
+    __syncthreads();
   }
   const int64_t stride = P.out_stride ? P.out_stride : 3 * npx;
   for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
@@ -808,9 +817,7 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
     aug_point(op, thr, src + 3 * i, px);
     if (jitter) {
 #pragma unroll
-      for (int c = 0; c < 3; c++) px[c] = blend1(fb, px[c], 0.0);           // brightness
-#pragma unroll
-      for (int c = 0; c < 3; c++) px[c] = blend1(fc, px[c], mean);          // contrast
+      for (int c = 0; c < 3; c++) px[c] = con[bri[px[c]]];                  // brightness, contrast
       const double g = (double)luma601(px[0], px[1], px[2]);
 #pragma unroll
       for (int c = 0; c < 3; c++) px[c] = blend1(fs, px[c], g);             // saturation
