@@ -791,9 +791,28 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
     for (int i = threadIdx.x; i < 768; i += kAugOutThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
   if (jitter && threadIdx.x < 256) bri[threadIdx.x] = (uint8_t)blend1(fb, threadIdx.x, 0.0);
   __syncthreads();
+  // groups of 4 pixels (12 source bytes = 3 words; 4 outputs per channel =
+  // one 8-byte bf16 / 16-byte f32 store) when every address is aligned for
+  // it; the scalar loop takes the rest (odd sizes, the tail)
+  const int64_t stride = P.out_stride ? P.out_stride : 3 * npx;
+  const size_t osz = P.out_kind == ESSL_OUT_F32_NCHW ? 4 : 2;
+  const bool vec = (npx & 3) == 0 && ((uintptr_t)src & 3) == 0 && (stride & 3) == 0 &&
+                   ((uintptr_t)P.out & (4 * osz - 1)) == 0 && ((uintptr_t)P.out_u8 & 3) == 0;
+  const int64_t ngrp = vec ? npx >> 2 : 0;
+  const uint32_t *src4 = reinterpret_cast<const uint32_t *>(src);
   if (jitter) {
     unsigned long long sum = 0;
-    for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
+    for (int64_t g = threadIdx.x; g < ngrp; g += kAugOutThreads) {
+      uint8_t b[12];
+      *reinterpret_cast<uint3 *>(b) = make_uint3(src4[3 * g], src4[3 * g + 1], src4[3 * g + 2]);
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        int px[3];
+        aug_point(op, thr, b + 3 * j, px);
+        sum += (unsigned)luma601(bri[px[0]], bri[px[1]], bri[px[2]]);
+      }
+    }
+    for (int64_t i = 4 * ngrp + threadIdx.x; i < npx; i += kAugOutThreads) {
       int px[3];
       aug_point(op, thr, src + 3 * i, px);
       sum += (unsigned)luma601(bri[px[0]], bri[px[1]], bri[px[2]]);
@@ -811,10 +830,7 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
     }
     __syncthreads();
   }
-  const int64_t stride = P.out_stride ? P.out_stride : 3 * npx;
-  for (int64_t i = threadIdx.x; i < npx; i += kAugOutThreads) {
-    int px[3];
-    aug_point(op, thr, src + 3 * i, px);
+  auto finish = [&](int px[3]) {
     if (jitter) {
 #pragma unroll
       for (int c = 0; c < 3; c++) px[c] = con[bri[px[c]]];                  // brightness, contrast
@@ -822,6 +838,46 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
 #pragma unroll
       for (int c = 0; c < 3; c++) px[c] = blend1(fs, px[c], g);             // saturation
     }
+  };
+  for (int64_t g = threadIdx.x; g < ngrp; g += kAugOutThreads) {
+    uint8_t b[12];
+    *reinterpret_cast<uint3 *>(b) = make_uint3(src4[3 * g], src4[3 * g + 1], src4[3 * g + 2]);
+    int q[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      aug_point(op, thr, b + 3 * j, q[j]);
+      finish(q[j]);
+    }
+    const int64_t i = 4 * g;
+    if (P.out_kind == ESSL_OUT_BF16_NCHW) {
+      __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + i;
+#pragma unroll
+      for (int c = 0; c < 3; c++) {
+        __nv_bfloat162 lo = __halves2bfloat162(lutb[c][q[0][c]], lutb[c][q[1][c]]);
+        __nv_bfloat162 hi = __halves2bfloat162(lutb[c][q[2][c]], lutb[c][q[3][c]]);
+        *reinterpret_cast<uint2 *>(o + c * npx) =
+            make_uint2(*reinterpret_cast<uint32_t *>(&lo), *reinterpret_cast<uint32_t *>(&hi));
+      }
+    } else if (P.out_kind == ESSL_OUT_F32_NCHW) {
+      float *o = reinterpret_cast<float *>(P.out) + img * stride + i;
+#pragma unroll
+      for (int c = 0; c < 3; c++)
+        *reinterpret_cast<float4 *>(o + c * npx) =
+            make_float4(lut[c][q[0][c]], lut[c][q[1][c]], lut[c][q[2][c]], lut[c][q[3][c]]);
+    }
+    if (P.out_u8) {
+      uint8_t ob[12];
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) ob[3 * j + c] = (uint8_t)q[j][c];
+      *reinterpret_cast<uint3 *>(P.out_u8 + ((size_t)img * npx + i) * 3) = *reinterpret_cast<uint3 *>(ob);
+    }
+  }
+  for (int64_t i = 4 * ngrp + threadIdx.x; i < npx; i += kAugOutThreads) {
+    int px[3];
+    aug_point(op, thr, src + 3 * i, px);
+    finish(px);
     if (P.out_kind == ESSL_OUT_BF16_NCHW) {
       __nv_bfloat16 *o = reinterpret_cast<__nv_bfloat16 *>(P.out) + img * stride + i;
 #pragma unroll
