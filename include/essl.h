@@ -147,6 +147,8 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload,
                     int flags, essl_ctx **out);
 int essl_ctx_destroy(essl_ctx *ctx);
 int essl_ctx_set_option(essl_ctx *ctx, int option, int64_t value);
+/* The value a new context starts with for `option` (no device needed). */
+int essl_option_default(int option, int64_t *value);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t essl_ctx_launch_count(const essl_ctx *ctx);
 /* With ESSL_OPT_PROFILE on: synchronise the recorded events, add each
@@ -229,6 +231,21 @@ int essl_decode_rrc_aug(essl_ctx *ctx, const uint8_t *blob,
                         int res, int out_kind, void *out, int64_t out_stride,
                         uint8_t *out_u8, essl_result *results, void *stream);
 
+/* Same, plus the MAE visible tokens of every image (N1/a20: patchify
+ * 'nchpwq->nhwpqc' of the bf16 normalized pixels) written by
+ * the resize kernel itself: tokens_bf16 is DEVICE bf16 [n, n_keep,
+ * patch*patch*3] and row r of image i is the patch t with ids_restore[i][t]
+ * == r < n_keep (ids_restore: DEVICE int64 [n, (res/patch)^2], e.g. from
+ * essl_mask earlier on the same stream).  tokens_bf16 == NULL: no tokens
+ * (== essl_decode_rrc_aug). */
+int essl_decode_rrc_visible(essl_ctx *ctx, const uint8_t *blob,
+                            const essl_sample *samples, const essl_aug *aug,
+                            int n, int res, int out_kind, void *out,
+                            int64_t out_stride, uint8_t *out_u8, int patch,
+                            const int64_t *ids_restore, int n_keep,
+                            void *tokens_bf16, essl_result *results,
+                            void *stream);
+
 /* Replaces: decode_crop(bytes, CropRect) (codec.py:448-511) for a batch of
  * crops: writes each uint8 [h,w,3] region at out + out_offsets[i]
  * (device pointer + host offsets). */
@@ -288,6 +305,52 @@ int essl_normalize_u8(const uint8_t *src, int h, int w, float *dst,
  * as a batch.  h, w <= the context's max_side. */
 int essl_augment_u8(essl_ctx *ctx, const uint8_t *src, int n, int h, int w,
                     const essl_aug *aug, uint8_t *dst, void *stream);
+
+/* ---- native batch enqueue ---------------------------------------------------
+ * Replaces: Loader._fill_sample for a whole batch plus the batch assembly of
+ * Loader.epoch (pipeline.py:219-267) in ONE stream-ordered call, so the host
+ * side of a batch costs microseconds: descriptors from the record table +
+ * RandomResizedCrop / flip draws (host C++), index/label upload, optional
+ * pinned-container gather, MAE mask (before the pixels: the fused visible
+ * tokens read ids_restore), decode + resize + normalize, result download.
+ * The record table (container.py:46-51 RECORD_DTYPE columns) is copied once
+ * into an essl_dataset. */
+typedef struct essl_dataset essl_dataset;
+int essl_dataset_create(int64_t n, const uint64_t *offsets, const uint32_t *lengths,
+                        const uint32_t *crc32, const uint16_t *widths,
+                        const uint16_t *heights, const int64_t *labels,
+                        essl_dataset **out);
+int essl_dataset_destroy(essl_dataset *ds);
+
+typedef struct {
+  uint64_t seed, epoch;       /* SampleRng keys (rng.py:39-44) */
+  double scale[2], ratio[2];  /* RrcConfig (pipeline.py:31-48) */
+  int32_t res, out_kind;      /* output resolution, ESSL_OUT_* */
+  int32_t check_crc;          /* 1: verify each payload's CRC32 (container.py:263) */
+  int32_t tokens, masked;     /* MAE mask: N tokens, k masked (0 tokens: no mask) */
+  int32_t patch;              /* patch size (visible tokens) */
+} essl_batch_cfg;
+
+typedef struct {
+  const uint8_t *blob;         /* DEVICE resident container bytes, or NULL: */
+  const uint8_t *pinned_base;  /* DEVICE address of the page-locked container */
+  int32_t stage_slot;          /* staging slot (0/1) of the pinned gather */
+  int32_t pad;
+  const essl_aug *aug;         /* HOST n 3-Aug entries (essl_aug_batch), or NULL */
+  void *pixels;                /* DEVICE [n,3,res,res] out_kind, caller-owned */
+  int64_t pixel_stride;        /* elements between samples (0: dense) */
+  uint8_t *u8;                 /* DEVICE uint8 [n,res,res,3] view, or NULL */
+  int64_t *index_label;        /* DEVICE int64 [2n]: indices, then labels */
+  int32_t *mask;               /* DEVICE outputs of the mask (any may be NULL) */
+  int64_t *ids_keep, *ids_restore;
+  void *tokens;                /* DEVICE bf16 visible tokens [n, N-k, patch^2*3], or NULL */
+  essl_result *results;        /* DEVICE [n] */
+  essl_result *results_host;   /* HOST pinned [n] copy of results, or NULL */
+} essl_batch_io;
+
+int essl_batch_enqueue(essl_ctx *ctx, const essl_dataset *ds, const essl_batch_cfg *cfg,
+                       const int64_t *indices, int n, const essl_batch_io *io,
+                       void *stream);
 
 /* ---- host-side sampling (C++, glibc libm: bit-exact with CPython) ---------
  * Replace rng.py:27-87 and pipeline.py:51-87. */

@@ -41,7 +41,8 @@ EXPORTS = (
     "essl_rng_randint", "essl_epoch_permutation", "essl_sample_rrc", "essl_rrc_batch",
     "essl_mask_count", "essl_encode_jpeg", "essl_synth_image", "essl_decode_rrc_aug",
     "essl_augment_u8", "essl_aug_draw", "essl_aug_batch", "essl_debug_lanes",
-    "essl_trace_read", "essl_memcpy_async",
+    "essl_trace_read", "essl_memcpy_async", "essl_option_default",
+    "essl_decode_rrc_visible", "essl_dataset_create", "essl_dataset_destroy", "essl_batch_enqueue",
 )
 
 
@@ -69,6 +70,23 @@ class EsslAug(ctypes.Structure):
                 ("factors", ctypes.c_double * 3),
                 ("weights", ctypes.c_double * (2 * ESSL_AUG_MAX_RADIUS + 1)),
                 ("reserved", ctypes.c_double)]
+
+
+class EsslBatchCfg(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("epoch", ctypes.c_uint64),
+                ("scale", ctypes.c_double * 2), ("ratio", ctypes.c_double * 2),
+                ("res", ctypes.c_int32), ("out_kind", ctypes.c_int32), ("check_crc", ctypes.c_int32),
+                ("tokens", ctypes.c_int32), ("masked", ctypes.c_int32), ("patch", ctypes.c_int32)]
+
+
+class EsslBatchIo(ctypes.Structure):
+    _fields_ = [("blob", ctypes.c_void_p), ("pinned_base", ctypes.c_void_p),
+                ("stage_slot", ctypes.c_int32), ("pad", ctypes.c_int32), ("aug", ctypes.c_void_p),
+                ("pixels", ctypes.c_void_p), ("pixel_stride", ctypes.c_int64),
+                ("u8", ctypes.c_void_p), ("index_label", ctypes.c_void_p), ("mask", ctypes.c_void_p),
+                ("ids_keep", ctypes.c_void_p), ("ids_restore", ctypes.c_void_p),
+                ("tokens", ctypes.c_void_p), ("results", ctypes.c_void_p),
+                ("results_host", ctypes.c_void_p)]
 
 
 SAMPLE_NP_DTYPE = None  # filled lazily (numpy view of EsslSample arrays)
@@ -120,6 +138,7 @@ def lib():
         "essl_ctx_create": (i32, [i32, i32, i32, i32, i32, P]),
         "essl_ctx_destroy": (i32, [P]),
         "essl_ctx_set_option": (i32, [P, i32, i64]),
+        "essl_option_default": (i32, [i32, P]),
         "essl_ctx_launch_count": (i64, [P]),
         "essl_ctx_profile_read": (i32, [P, P, P]),
         "essl_profile_mark": (i32, [P]),
@@ -155,6 +174,11 @@ def lib():
         "essl_synth_image": (i32, [u64, i32, i32, P]),
         "essl_decode_rrc_aug": (i32, [P, P, P, P, i32, i32, i32, P, i64, P, P, P]),
         "essl_augment_u8": (i32, [P, P, i32, i32, i32, P, P, P]),
+        "essl_dataset_create": (i32, [i64, P, P, P, P, P, P, P]),
+        "essl_dataset_destroy": (i32, [P]),
+        "essl_batch_enqueue": (i32, [P, P, P, P, i32, P, P]),
+        "essl_decode_rrc_visible": (i32, [P, P, P, P, i32, i32, i32, P, i64, P, i32, P, i32, P,
+                                          P, P]),
         "essl_aug_draw": (i32, [P, i32, P, P]),
         "essl_aug_batch": (i32, [u64, u64, P, i32, P, P, dbl, dbl, dbl, dbl, i32, P, P]),
     }
@@ -164,6 +188,13 @@ def lib():
         fn.argtypes = args
     _lib = L
     return L
+
+
+def option_default(option: int) -> int:
+    """The value a new libessl context starts with for ESSL_OPT_* `option`."""
+    v = ctypes.c_int64()
+    check(lib().essl_option_default(option, ctypes.byref(v)), "essl_option_default")
+    return int(v.value)
 
 
 def check(rc: int, what: str = "libessl") -> None:

@@ -17,8 +17,8 @@
 #include "essl_common.cuh"
 
 namespace essl {
-void init_crc_tables();
-void init_norm_luts();
+void init_device_decode();
+void init_device_pixels();
 }
 
 namespace {
@@ -38,6 +38,15 @@ int fail(int code, const std::string &msg) {
   } while (0)
 
 constexpr int kDescRing = 8;
+
+// Context option defaults (essl_option_default reports them).
+constexpr int kDefMode = ESSL_DECODE_SPECULATIVE;
+constexpr int kDefSeqBits = 3072;
+constexpr int kDefCkBits = 64;
+constexpr int kDefWarmBits = 2048;
+constexpr int kDefStageBytes = 64 * 1024;
+constexpr int kDefGatherCtas = 4;
+constexpr bool kDefGatherTma = true;
 
 // Persistent host workers for payload staging (one pool per context): a
 // batch's copies are split into contiguous ranges, the caller thread takes
@@ -105,6 +114,13 @@ class StagePool {
 
 }  // namespace
 
+struct essl_dataset {  // record table of a container (essl_batch_enqueue)
+  std::vector<uint64_t> offset;
+  std::vector<uint32_t> length, crc;
+  std::vector<uint16_t> width, height;
+  std::vector<int64_t> label;
+};
+
 struct essl_ctx {
   int device = 0;
   int max_batch = 0, max_side = 0, max_payload = 0;
@@ -115,6 +131,7 @@ struct essl_ctx {
   cudaEvent_t ev_desc[kDescRing] = {};
   bool desc_used[kDescRing] = {};
   int desc_next = 0;
+  int64_t *h_il[kDescRing] = {};    // essl_batch_enqueue: indices + labels, same ring slots
   essl_aug *h_aug[kDescRing] = {};  // 3-Aug parameters, same ring slots
   essl_aug *d_aug[kDescRing] = {};
   // 3-Aug scratch: resized uint8 images and their blurred copies (grown on demand)
@@ -130,13 +147,13 @@ struct essl_ctx {
   essl::GatherDesc *h_gather[2] = {}, *d_gather[2] = {};  // pinned-container gathers
   // misc device buffers
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
-  int mode = ESSL_DECODE_SPECULATIVE;
-  int seq_bits = 3072;
-  int ck_bits = 64;
-  int warm_bits = 2048;
-  int stage_max = 64 * 1024;
-  int gather_ctas = 4;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
-  bool gather_tma = true;   // ESSL_OPT_GATHER_TMA: bulk (TMA) bus reads, e2e +9% over LSU loads
+  int mode = kDefMode;
+  int seq_bits = kDefSeqBits;
+  int ck_bits = kDefCkBits;
+  int warm_bits = kDefWarmBits;
+  int stage_max = kDefStageBytes;
+  int gather_ctas = kDefGatherCtas;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
+  bool gather_tma = kDefGatherTma;   // ESSL_OPT_GATHER_TMA: bulk (TMA) bus reads, e2e +9% over LSU loads
   int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
   essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
@@ -154,6 +171,22 @@ struct essl_ctx {
 };
 
 namespace {
+// Makes the context's device current for the duration of an entry point and
+// restores the caller's device (a context may live on a non-current device).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const essl_ctx *c) : DevGuard(c ? c->device : -1) {}
+  explicit DevGuard(int device) {
+    if (device < 0) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device && cudaSetDevice(device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Bracket a launch with events when profiling (ESSL_OPT_PROFILE).
 struct Prof {
   essl_ctx *c; int kid; cudaStream_t st; cudaEvent_t a = nullptr;
@@ -229,6 +262,43 @@ int ensure_aug_scratch(essl_ctx *c, uint64_t bytes) {
 // All of a batch's host->device copies are issued before its kernels: a copy
 // queued behind this batch's kernels would hold up the copies (and so the
 // kernels) of batches on other streams on the shared copy engine.
+int launch_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *d_desc, int n, int max_len,
+                  essl_result *results, cudaStream_t st);
+int rrc_impl(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int slot,
+             const essl_aug *aug, int n, int res, int out_kind, void *out, int64_t out_stride,
+             uint8_t *out_u8, int patch, const int64_t *ids_restore, int n_keep,
+             void *tokens_bf16, essl_result *results, cudaStream_t st);
+
+// Pinned-container gather of a batch: samples[i].offset holds the payload's
+// container offset on entry and its offset inside the staging slot on return.
+int stage_pinned_impl(essl_ctx *c, int slot, const uint8_t *dev_base, essl_sample *samples, int n,
+                      cudaStream_t st, const uint8_t **dev_blob) {
+  if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
+  essl::GatherDesc *h = c->h_gather[slot];
+  uint64_t pos = 0;
+  for (int i = 0; i < n; i++) {
+    const uint32_t len = samples[i].length;
+    if ((int)len > c->max_payload) return fail(ESSL_E_CAPACITY, "payload larger than max_payload");
+    h[i].src = samples[i].offset;
+    h[i].dst = pos;
+    h[i].len = len;
+    samples[i].offset = pos;
+    pos += ((uint64_t)len + 63) / 64 * 64;
+  }
+  if (n > 0) {
+    CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
+    {
+      Prof pr(c, ESSL_K_STAGE, st);
+      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], c->gather_ctas,
+                               c->gather_tma, st);
+    }
+  }
+  CK(cudaEventRecord(c->ev_stage[slot], st));
+  c->stage_used[slot] = true;
+  *dev_blob = c->d_stage[slot];
+  return ESSL_OK;
+}
+
 int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n,
                essl_result *results, cudaStream_t st, int *ring, const essl_aug *aug = nullptr) {
   if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
@@ -246,6 +316,12 @@ int run_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int
     std::memcpy(c->h_aug[r], aug, sizeof(essl_aug) * n);
     CK(cudaMemcpyAsync(c->d_aug[r], c->h_aug[r], sizeof(essl_aug) * n, cudaMemcpyHostToDevice, st));
   }
+  return launch_decode(c, blob, d_desc, n, max_len, results, st);
+}
+
+// k_prep -> k_entropy -> k_idct of a batch whose descriptors are on the device.
+int launch_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *d_desc, int n, int max_len,
+                  essl_result *results, cudaStream_t st) {
   CK(cudaMemsetAsync(c->s.counters, 0, 4 * sizeof(unsigned long long), st));
   essl::DecodeParams p;
   p.blob = blob;
@@ -295,7 +371,10 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   (void)flags;
   if (!out || max_batch < 1 || max_side < 1 || max_payload < 4 || max_payload > (1 << 22))
     return fail(ESSL_E_ARG, "essl_ctx_create: bad arguments");
-  CK(cudaSetDevice(device));
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ESSL_E_ARG, "essl_ctx_create: no such device");
+  DevGuard dg_(device);  // the caller's current device is restored on return
   essl_ctx *c = new essl_ctx();
   c->device = device;
   c->max_batch = max_batch;
@@ -340,6 +419,7 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
     CKC(cudaMalloc(&c->d_desc[r], sizeof(essl_sample) * max_batch));
     CKC(cudaEventCreateWithFlags(&c->ev_desc[r], cudaEventDisableTiming));
     CKC(cudaMallocHost(&c->h_aug[r], sizeof(essl_aug) * max_batch));
+    CKC(cudaMallocHost(&c->h_il[r], 2 * sizeof(int64_t) * max_batch));
     CKC(cudaMalloc(&c->d_aug[r], sizeof(essl_aug) * max_batch));
   }
   c->stage_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 63) / 64 * 64);
@@ -350,20 +430,28 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
     CKC(cudaMallocHost(&c->h_gather[r], sizeof(essl::GatherDesc) * max_batch));
     CKC(cudaMalloc(&c->d_gather[r], sizeof(essl::GatherDesc) * max_batch));
   }
+  // per-device state (CRC tables, normalize LUTs, shared-memory opt-ins) is
+  // set up once for every device a context lives on
+  {
+    static std::mutex m;
+    static std::vector<bool> done;
+    std::lock_guard<std::mutex> g(m);
+    if ((int)done.size() <= device) done.resize(device + 1, false);
+    if (!done[device]) {
+      essl::init_device_decode();
+      essl::init_device_pixels();
+      CKC(cudaDeviceSynchronize());  // tables ready before any stream's first batch
+      done[device] = true;
+    }
+  }
 #undef CKC
-  static std::once_flag once;
-  std::call_once(once, [] {
-    essl::init_crc_tables();
-    essl::init_norm_luts();
-    cudaDeviceSynchronize();  // tables ready before any stream's first batch
-  });
   *out = c;
   return ESSL_OK;
 }
 
 int essl_ctx_destroy(essl_ctx *c) {
   if (!c) return ESSL_OK;
-  cudaSetDevice(c->device);
+  DevGuard dg_(c);
   cudaDeviceSynchronize();
   cudaFree(c->s.clean);
   cudaFree(c->s.coef);
@@ -380,6 +468,7 @@ int essl_ctx_destroy(essl_ctx *c) {
     if (c->d_desc[r]) cudaFree(c->d_desc[r]);
     if (c->ev_desc[r]) cudaEventDestroy(c->ev_desc[r]);
     if (c->h_aug[r]) cudaFreeHost(c->h_aug[r]);
+    if (c->h_il[r]) cudaFreeHost(c->h_il[r]);
     if (c->d_aug[r]) cudaFree(c->d_aug[r]);
   }
   if (c->dbg_lanes) cudaFree(c->dbg_lanes);
@@ -401,6 +490,7 @@ int essl_ctx_destroy(essl_ctx *c) {
 
 int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
   if (!c) return fail(ESSL_E_ARG, "null context");
+  DevGuard dg_(c);
   switch (option) {
     case ESSL_OPT_DECODE_MODE:
       if (value != ESSL_DECODE_SPECULATIVE && value != ESSL_DECODE_SERIAL)
@@ -460,10 +550,28 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
   return fail(ESSL_E_ARG, "unknown option");
 }
 
+int essl_option_default(int option, int64_t *value) {
+  if (!value) return fail(ESSL_E_ARG, "essl_option_default: null value");
+  switch (option) {
+    case ESSL_OPT_DECODE_MODE: *value = kDefMode; return ESSL_OK;
+    case ESSL_OPT_SEQ_BITS: *value = kDefSeqBits; return ESSL_OK;
+    case ESSL_OPT_CHECKPOINT_BITS: *value = kDefCkBits; return ESSL_OK;
+    case ESSL_OPT_PROFILE: *value = 0; return ESSL_OK;
+    case ESSL_OPT_WARMUP_BITS: *value = kDefWarmBits; return ESSL_OK;
+    case ESSL_OPT_STAGE_BYTES: *value = kDefStageBytes; return ESSL_OK;
+    case ESSL_OPT_GATHER_CTAS: *value = kDefGatherCtas; return ESSL_OK;
+    case ESSL_OPT_GATHER_TMA: *value = kDefGatherTma ? 1 : 0; return ESSL_OK;
+    case ESSL_OPT_DEBUG_LANES: *value = 0; return ESSL_OK;
+    case ESSL_OPT_TRACE: *value = 0; return ESSL_OK;
+  }
+  return fail(ESSL_E_ARG, "unknown option");
+}
+
 int64_t essl_ctx_launch_count(const essl_ctx *c) { return c ? c->launches.load() : -1; }
 
 int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
   if (!c || !out || n < 0 || n > c->max_batch) return fail(ESSL_E_ARG, "essl_debug_stats: bad arguments");
+  DevGuard dg_(c);
   std::vector<essl::ImgInfo> info(n);
   CK(cudaMemcpy(info.data(), c->s.info, sizeof(essl::ImgInfo) * n, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; i++) std::memcpy(out + 16 * i, info[i].dbg, 16 * sizeof(int64_t));
@@ -472,6 +580,7 @@ int essl_debug_stats(essl_ctx *c, int64_t *out, int n) {
 
 int essl_trace_read(essl_ctx *c, uint64_t *out, int max) {
   if (!c || !out || max < 0 || !c->trace.buf) return fail(ESSL_E_ARG, "essl_trace_read: tracing off");
+  DevGuard dg_(c);
   CK(cudaDeviceSynchronize());
   unsigned int n = 0;
   CK(cudaMemcpy(&n, c->trace.count, sizeof(n), cudaMemcpyDeviceToHost));
@@ -485,6 +594,7 @@ int essl_trace_read(essl_ctx *c, uint64_t *out, int max) {
 int essl_debug_lanes(essl_ctx *c, int32_t *out, int n) {
   if (!c || !out || n < 0 || n > c->max_batch || !c->dbg_lanes)
     return fail(ESSL_E_ARG, "essl_debug_lanes: bad arguments (ESSL_OPT_DEBUG_LANES off?)");
+  DevGuard dg_(c);
   CK(cudaMemcpy(out, c->dbg_lanes, sizeof(int32_t) * 8 * essl::kEntropyLanes * n,
                 cudaMemcpyDeviceToHost));
   return ESSL_OK;
@@ -500,6 +610,7 @@ int essl_profile_mark(void *stream) {
 
 int essl_ctx_profile_timeline(essl_ctx *c, int32_t *kid, double *t0_ms, double *t1_ms, int max) {
   if (!c || !kid || !t0_ms || !t1_ms || max < 0) return fail(ESSL_E_ARG, "essl_ctx_profile_timeline: bad arguments");
+  DevGuard dg_(c);
   if (!g_mark) return fail(ESSL_E_ARG, "essl_profile_mark was not called");
   CK(cudaEventSynchronize(g_mark));
   int n = 0;
@@ -519,6 +630,7 @@ int essl_ctx_profile_timeline(essl_ctx *c, int32_t *kid, double *t0_ms, double *
 
 int essl_ctx_profile_read(essl_ctx *c, double *ms, int64_t *count) {
   if (!c || !ms || !count) return fail(ESSL_E_ARG, "essl_ctx_profile_read: bad arguments");
+  DevGuard dg_(c);
   for (auto &r : c->recs) {
     CK(cudaEventSynchronize(r.b));
     float t = 0.f;
@@ -538,6 +650,7 @@ int essl_stage(essl_ctx *c, int slot, const uint8_t *const *src, const uint32_t 
                essl_sample *samples, int nthreads, void *stream, const uint8_t **dev_blob) {
   if (!c || slot < 0 || slot > 1 || n < 0 || n > c->max_batch || !dev_blob)
     return fail(ESSL_E_ARG, "essl_stage: bad arguments");
+  DevGuard dg_(c);
   cudaStream_t st = (cudaStream_t)stream;
   if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
   std::vector<uint64_t> off(n + 1);
@@ -601,31 +714,12 @@ int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint
                       const uint8_t **dev_blob) {
   if (!c || slot < 0 || slot > 1 || n < 0 || n > c->max_batch || !dev_blob || (n > 0 && (!dev_base || !src_off || !len)))
     return fail(ESSL_E_ARG, "essl_stage_pinned: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
-  essl::GatherDesc *h = c->h_gather[slot];
-  uint64_t pos = 0;
+  DevGuard dg_(c);
   for (int i = 0; i < n; i++) {
-    if ((int)len[i] > c->max_payload) return fail(ESSL_E_CAPACITY, "payload larger than max_payload");
-    h[i].src = src_off[i];
-    h[i].dst = pos;
-    h[i].len = len[i];
-    samples[i].offset = pos;
+    samples[i].offset = src_off[i];
     samples[i].length = len[i];
-    pos += ((uint64_t)len[i] + 63) / 64 * 64;
   }
-  if (n > 0) {
-    CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
-    {
-      Prof pr(c, ESSL_K_STAGE, st);
-      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], c->gather_ctas,
-                               c->gather_tma, st);
-    }
-  }
-  CK(cudaEventRecord(c->ev_stage[slot], st));
-  c->stage_used[slot] = true;
-  *dev_blob = c->d_stage[slot];
-  return ESSL_OK;
+  return stage_pinned_impl(c, slot, dev_base, samples, n, (cudaStream_t)stream, dev_blob);
 }
 
 int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n, int res,
@@ -639,11 +733,39 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
                         const essl_aug *aug, int n, int res, int out_kind, void *out,
                         int64_t out_stride, uint8_t *out_u8, essl_result *results,
                         void *stream) {
+  return essl_decode_rrc_visible(c, blob, samples, aug, n, res, out_kind, out, out_stride, out_u8,
+                                 0, nullptr, 0, nullptr, results, stream);
+}
+
+int essl_decode_rrc_visible(essl_ctx *c, const uint8_t *blob, const essl_sample *samples,
+                            const essl_aug *aug, int n, int res, int out_kind, void *out,
+                            int64_t out_stride, uint8_t *out_u8, int patch,
+                            const int64_t *ids_restore, int n_keep, void *tokens_bf16,
+                            essl_result *results, void *stream) {
   if (!c || n < 0 || res < 1 || (n > 0 && (!blob || !samples)))
     return fail(ESSL_E_ARG, "essl_decode_rrc: bad arguments");
+  DevGuard dg_(c);
+  return rrc_impl(c, blob, samples, -1, aug, n, res, out_kind, out, out_stride, out_u8, patch,
+                  ids_restore, n_keep, tokens_bf16, results, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace {
+// The decode + pixel stage of a batch.  slot < 0: descriptors `samples`
+// (host) go through a fresh ring slot; slot >= 0: they are already in that
+// slot's pinned buffer (essl_batch_enqueue).
+int rrc_impl(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int slot,
+             const essl_aug *aug, int n, int res, int out_kind, void *out, int64_t out_stride,
+             uint8_t *out_u8, int patch, const int64_t *ids_restore, int n_keep,
+             void *tokens_bf16, essl_result *results, cudaStream_t st) {
   if (out_kind != ESSL_OUT_BF16_NCHW && out_kind != ESSL_OUT_F32_NCHW && out_kind != ESSL_OUT_NONE)
     return fail(ESSL_E_ARG, "bad out_kind");
   if (out_kind != ESSL_OUT_NONE && !out) return fail(ESSL_E_ARG, "null output");
+  const bool want_vis = tokens_bf16 != nullptr;
+  if (want_vis && (patch < 1 || res % patch || !ids_restore || n_keep < 0 ||
+                   n_keep > (res / patch) * (res / patch)))
+    return fail(ESSL_E_ARG, "essl_decode_rrc_visible: bad patch / ids_restore / n_keep");
   if (n == 0) return ESSL_OK;
   int max_radius = 0;
   bool any_aug = false;
@@ -651,14 +773,31 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
     int rc = check_aug(aug, n, &max_radius, &any_aug);
     if (rc) return rc;
   }
+  if (want_vis && any_aug && out_kind != ESSL_OUT_BF16_NCHW)
+    return fail(ESSL_E_ARG, "visible tokens with 3-Aug need the bf16 pixel output");
   if (any_aug) {
     int rc = ensure_aug_scratch(c, (uint64_t)n * res * res * 3);
     if (rc) return rc;
   }
-  cudaStream_t st = (cudaStream_t)stream;
   int ring = -1;
   const bool aug_out = any_aug && (out_kind != ESSL_OUT_NONE || out_u8);
-  int rc = run_decode(c, blob, samples, n, results, st, &ring, aug_out ? aug : nullptr);
+  int rc;
+  if (slot < 0) {
+    rc = run_decode(c, blob, samples, n, results, st, &ring, aug_out ? aug : nullptr);
+  } else {
+    ring = slot;
+    int max_len = 0;
+    for (int i = 0; i < n; i++) max_len = std::max(max_len, (int)samples[i].length);
+    if (max_len > c->max_payload) return fail(ESSL_E_CAPACITY, "payload larger than context max_payload");
+    CK(cudaMemcpyAsync(c->d_desc[slot], c->h_desc[slot], sizeof(essl_sample) * n,
+                       cudaMemcpyHostToDevice, st));
+    if (aug_out) {
+      std::memcpy(c->h_aug[slot], aug, sizeof(essl_aug) * n);
+      CK(cudaMemcpyAsync(c->d_aug[slot], c->h_aug[slot], sizeof(essl_aug) * n,
+                         cudaMemcpyHostToDevice, st));
+    }
+    rc = launch_decode(c, blob, c->d_desc[slot], n, max_len, results, st);
+  }
   if (rc) return rc;
   essl::PixelParams pp;
   pp.info = c->s.info;
@@ -673,30 +812,41 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
   pp.out_u8 = any_aug && !aug_out ? c->aug_a : out_u8;
   pp.aug = aug_out ? c->d_aug[ring] : nullptr;
   pp.aug_u8 = c->aug_a;
+  // visible tokens fused into k_resize (with 3-Aug they are gathered from
+  // the finished pixels after k_aug_out instead)
+  pp.vis = want_vis && !any_aug ? tokens_bf16 : nullptr;
+  pp.vis_restore = ids_restore;
+  pp.patch = want_vis ? patch : 0;
+  pp.n_keep = n_keep;
   pp.trace = c->trace;
   {
-    // the largest band (output rows per k_resize CTA) whose source-row
-    // staging for this batch's crops keeps 4 CTAs per SM (<= 48 KB), else
-    // the largest that fits the 200 KB budget at all
-    auto staging = [&](int b) {
+    // the largest band (output rows per k_resize CTA, <= kMaxBandRows) whose
+    // shared staging (source rows x widest crop + the column taps) for this
+    // batch's crops stays within 96 KB (two CTAs per SM), else the largest
+    // that fits the 200 KB budget; crops wider than that read the planes
+    // directly (no staging)
+    auto smem = [&](int b) {
       int w = 0;
       for (int i = 0; i < n; i++)
         w = std::max(w, essl::band_source_rows(samples[i].h, res, b) * std::max(samples[i].w, 1));
-      return w;
+      pp.band = b;
+      pp.src_words = (w + 3) / 4 * 4;
+      return essl::resize_smem(pp);
     };
-    int band = essl::kMaxBandRows, words = staging(band);
-    while (band > 1 && (size_t)(words + 3) / 4 * 4 * 4 > 48 * 1024) words = staging(band /= 2);
-    if ((size_t)(words + 3) / 4 * 4 * 4 > 48 * 1024) {
+    int band = essl::kMaxBandRows;
+    while (band > 8 && smem(band) > 96 * 1024) band /= 2;
+    if (smem(band) > 96 * 1024) {
       band = essl::kMaxBandRows;
-      words = staging(band);
-      while (band > 1 && (size_t)(words + 3) / 4 * 4 * 4 > 200 * 1024) words = staging(band /= 2);
+      while (band > 1 && smem(band) > 200 * 1024) band /= 2;
     }
-    pp.band = band;
-    pp.src_words = (words + 3) / 4 * 4;
-    if ((size_t)pp.src_words * 4 > 200 * 1024)
-      return fail(ESSL_E_CAPACITY, "crop too large for the resize kernel's shared staging");
+    if (smem(band) > 200 * 1024) {
+      pp.band = essl::kMaxBandRows;
+      pp.src_words = 0;  // unstaged: k_resize reads the planes directly
+      if (essl::resize_smem(pp) > 200 * 1024)
+        return fail(ESSL_E_CAPACITY, "output resolution too large for the resize kernel");
+    }
   }
-  if (pp.out_kind != ESSL_OUT_NONE || pp.out_u8) {
+  if (pp.out_kind != ESSL_OUT_NONE || pp.out_u8 || pp.vis) {
     Prof pr(c, ESSL_K_RESIZE, st);
     essl::launch_resize(pp, st);
   }
@@ -706,15 +856,25 @@ int essl_decode_rrc_aug(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
     Prof pr(c, ESSL_K_AUG, st);
     essl::launch_aug(ap, max_radius, st);
   }
+  if (want_vis && any_aug) {
+    if (out_stride && out_stride != 3ll * res * res)
+      return fail(ESSL_E_ARG, "visible tokens with 3-Aug need dense pixel output");
+    Prof pr(c, ESSL_K_GATHER, st);
+    essl::launch_gather_restore(out, n, res, patch, ids_restore, n_keep, tokens_bf16, st);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev_desc[ring], st));
   return ESSL_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int essl_augment_u8(essl_ctx *c, const uint8_t *src, int n, int h, int w, const essl_aug *aug,
                     uint8_t *dst, void *stream) {
   if (!c || n < 0 || h < 1 || w < 1 || (n > 0 && (!src || !dst || !aug)) || src == dst)
     return fail(ESSL_E_ARG, "essl_augment_u8: bad arguments");
+  DevGuard dg_(c);
   if (n == 0) return ESSL_OK;
   if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
   if (h > c->max_side || w > c->max_side)
@@ -747,6 +907,7 @@ int essl_decode_crop_u8(essl_ctx *c, const uint8_t *blob, const essl_sample *sam
                         void *stream) {
   if (!c || n < 0 || (n > 0 && (!blob || !samples || !out || !out_offsets)))
     return fail(ESSL_E_ARG, "essl_decode_crop_u8: bad arguments");
+  DevGuard dg_(c);
   if (n == 0) return ESSL_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int ring = -1;
@@ -768,6 +929,7 @@ int essl_dump_coefs(essl_ctx *c, const uint8_t *blob, const essl_sample *samples
                     essl_result *results, void *stream) {
   if (!c || n < 0 || (n > 0 && (!blob || !samples || !out || !out_offsets || !geometry)))
     return fail(ESSL_E_ARG, "essl_dump_coefs: bad arguments");
+  DevGuard dg_(c);
   if (n == 0) return ESSL_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int ring = -1;
@@ -803,6 +965,7 @@ int essl_mask(essl_ctx *c, uint64_t seed, uint64_t epoch, const int64_t *index, 
               int k, int32_t *mask_sorted, int64_t *ids_keep, int64_t *ids_restore, void *stream) {
   if (n < 0 || tokens < 1 || tokens > 4096 || k < 0 || k > tokens || (n > 0 && !index))
     return fail(ESSL_E_ARG, "essl_mask: bad arguments");
+  DevGuard dg_(c);
   {
     Prof pr(c, ESSL_K_MASK, (cudaStream_t)stream);
     essl::launch_mask(seed, epoch, index, n, tokens, k, mask_sorted, ids_keep, ids_restore,
@@ -817,6 +980,7 @@ int essl_mask_from_states(essl_ctx *c, const uint64_t *states, int n, int tokens
                           void *stream) {
   if (n < 0 || tokens < 1 || tokens > 4096 || k < 0 || k > tokens || (n > 0 && !states))
     return fail(ESSL_E_ARG, "essl_mask_from_states: bad arguments");
+  DevGuard dg_(c);
   {
     Prof pr(c, ESSL_K_MASK, (cudaStream_t)stream);
     essl::launch_mask_states(states, n, tokens, k, mask_sorted, ids_keep, ids_restore,
@@ -830,6 +994,7 @@ int essl_gather_visible(essl_ctx *c, const void *pixels_bf16, int n, int res, in
                         const int64_t *ids_keep, int n_keep, void *tokens_bf16, void *stream) {
   if (n < 0 || patch < 1 || res % patch || n_keep < 0 || (n > 0 && (!pixels_bf16 || !tokens_bf16)))
     return fail(ESSL_E_ARG, "essl_gather_visible: bad arguments");
+  DevGuard dg_(c);
   {
     Prof pr(c, ESSL_K_GATHER, (cudaStream_t)stream);
     essl::launch_gather(pixels_bf16, n, res, patch, ids_keep, n_keep, tokens_bf16,
@@ -852,6 +1017,90 @@ int essl_normalize_u8(const uint8_t *src, int h, int w, float *dst, void *stream
   if (!src || !dst || h < 1 || w < 1) return fail(ESSL_E_ARG, "essl_normalize_u8: bad arguments");
   essl::launch_normalize_u8(src, h, w, dst, (cudaStream_t)stream);
   CK(cudaGetLastError());
+  return ESSL_OK;
+}
+
+
+// ---- native batch enqueue ----------------------------------------------------
+
+int essl_dataset_create(int64_t n, const uint64_t *offsets, const uint32_t *lengths,
+                        const uint32_t *crc32, const uint16_t *widths, const uint16_t *heights,
+                        const int64_t *labels, essl_dataset **out) {
+  if (!out || n < 0 || (n > 0 && (!offsets || !lengths || !crc32 || !widths || !heights || !labels)))
+    return fail(ESSL_E_ARG, "essl_dataset_create: bad arguments");
+  essl_dataset *d = new essl_dataset();
+  d->offset.assign(offsets, offsets + n);
+  d->length.assign(lengths, lengths + n);
+  d->crc.assign(crc32, crc32 + n);
+  d->width.assign(widths, widths + n);
+  d->height.assign(heights, heights + n);
+  d->label.assign(labels, labels + n);
+  *out = d;
+  return ESSL_OK;
+}
+
+int essl_dataset_destroy(essl_dataset *d) {
+  delete d;
+  return ESSL_OK;
+}
+
+int essl_batch_enqueue(essl_ctx *c, const essl_dataset *ds, const essl_batch_cfg *cfg,
+                       const int64_t *indices, int n, const essl_batch_io *io, void *stream) {
+  if (!c || !ds || !cfg || !io || n < 0 || (n > 0 && !indices))
+    return fail(ESSL_E_ARG, "essl_batch_enqueue: bad arguments");
+  if (n > c->max_batch) return fail(ESSL_E_CAPACITY, "batch larger than context max_batch");
+  if (!io->blob && !io->pinned_base) return fail(ESSL_E_ARG, "essl_batch_enqueue: no payload source");
+  if (io->pinned_base && !io->blob && (io->stage_slot < 0 || io->stage_slot > 1))
+    return fail(ESSL_E_ARG, "essl_batch_enqueue: bad staging slot");
+  if (cfg->tokens > 0 && (cfg->masked < 0 || cfg->masked > cfg->tokens || cfg->tokens > 4096))
+    return fail(ESSL_E_ARG, "essl_batch_enqueue: bad mask geometry");
+  if (io->tokens && cfg->tokens <= 0) return fail(ESSL_E_ARG, "visible tokens need the mask");
+  const int64_t N = (int64_t)ds->offset.size();
+  for (int i = 0; i < n; i++)
+    if (indices[i] < 0 || indices[i] >= N) return fail(ESSL_E_ARG, "essl_batch_enqueue: index out of range");
+  DevGuard dg_(c);
+  if (n == 0) return ESSL_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int r = pick_slot(c);  // the batch that last used slot r has completed
+  if (r < 0) return r;
+  // descriptors: record fields + RRC rect and flip (host C++, pipeline.py:219-227)
+  essl_sample *smp = c->h_desc[r];
+  int64_t *il = c->h_il[r];
+  for (int i = 0; i < n; i++) {
+    const int64_t k = indices[i];
+    smp[i].offset = ds->offset[k];
+    smp[i].length = ds->length[k];
+    smp[i].crc32 = ds->crc[k];
+    smp[i].check_crc = cfg->check_crc;
+    il[i] = k;
+    il[n + i] = ds->label[k];
+  }
+  int rc = essl_rrc_batch(cfg->seed, cfg->epoch, indices, n, ds->width.data(), ds->height.data(),
+                          cfg->scale[0], cfg->scale[1], cfg->ratio[0], cfg->ratio[1], smp);
+  if (rc) return fail(rc, "essl_rrc_batch failed");
+  if (io->index_label) {
+    CK(cudaMemcpyAsync(io->index_label, il, 2 * sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  }
+  const uint8_t *blob = io->blob;
+  if (!blob) {
+    rc = stage_pinned_impl(c, io->stage_slot, io->pinned_base, smp, n, st, &blob);
+    if (rc) return rc;
+  }
+  // MAE mask first: the fused visible-token output reads ids_restore
+  if (cfg->tokens > 0) {
+    if (!io->index_label) return fail(ESSL_E_ARG, "the mask needs the device index copy");
+    Prof pr(c, ESSL_K_MASK, st);
+    essl::launch_mask(cfg->seed, cfg->epoch, io->index_label, n, cfg->tokens, cfg->masked, io->mask,
+                      io->ids_keep, io->ids_restore, st);
+  }
+  if (io->tokens && !io->ids_restore) return fail(ESSL_E_ARG, "visible tokens need ids_restore");
+  rc = rrc_impl(c, blob, smp, r, io->aug, n, cfg->res, cfg->out_kind, io->pixels, io->pixel_stride,
+                io->u8, cfg->patch, io->ids_restore, cfg->tokens - cfg->masked, io->tokens,
+                io->results, st);
+  if (rc) return rc;
+  if (io->results_host && io->results)
+    CK(cudaMemcpyAsync(io->results_host, io->results, sizeof(essl_result) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(c->ev_desc[r], st));  // (again: covers the results copy)
   return ESSL_OK;
 }
 

@@ -2255,12 +2255,6 @@ void launch_prep(const DecodeParams &p0, cudaStream_t st, int max_len) {
   int c2 = 1;
   while (c2 < (max_len + kCrcChunk - 1) / kCrcChunk && c2 < kCrcMaxChunks) c2 <<= 1;
   const int part = 4 * c2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    cudaFuncSetAttribute(k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
-    attr = true;
-  }
   DecodeParams p = p0;
   if (payload + part <= kMaxDynSmem) {
     p.prep_part_off = payload;
@@ -2278,6 +2272,16 @@ void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len) {
 
 void launch_idct(const DecodeParams &p, cudaStream_t st) {
   if (p.n > 0) k_idct<<<dim3(kIdctCtas, p.n), 256, 0, st>>>(p);
+}
+
+// Per-device one-time setup (api.cu calls it once for every device a context
+// is created on): the dynamic shared-memory opt-ins and the CRC tables are
+// per-device state.
+void init_crc_tables();
+void init_device_decode() {
+  cudaFuncSetAttribute(k_prep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaFuncSetAttribute(k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  init_crc_tables();
 }
 
 void init_crc_tables() {

@@ -135,6 +135,11 @@ struct PixelParams {
   // k_aug_blur / k_aug_out.
   const essl_aug *aug;
   uint8_t *aug_u8;
+  // MAE visible tokens (optional): bf16 [n, n_keep, patch*patch*3], rows
+  // placed by ids_restore (device int64 [n, (res/patch)^2])
+  void *vis;
+  const int64_t *vis_restore;
+  int patch, n_keep;
   CtaTrace trace;
 };
 
@@ -186,8 +191,9 @@ void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);
 void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t *dst, int ctas,
                         bool tma, cudaStream_t st);
-constexpr int kMaxBandRows = 32;      // k_resize: output rows per CTA, at most
+constexpr int kMaxBandRows = 64;      // k_resize: output rows per CTA, at most
 int band_source_rows(int h, int res, int band);
+size_t resize_smem(const PixelParams &p);
 void launch_crop_u8(const ImgInfo *info, const uint8_t *plane, int n, uint8_t *out,
                     const uint64_t *offsets, cudaStream_t st);
 void launch_mask(uint64_t seed, uint64_t epoch, const int64_t *index, int n, int tokens,
@@ -196,6 +202,8 @@ void launch_mask_states(const uint64_t *states, int n, int tokens, int k, int32_
                         int64_t *keep, int64_t *restore, cudaStream_t st);
 void launch_gather(const void *pix, int n, int res, int patch, const int64_t *keep,
                    int n_keep, void *tokens, cudaStream_t st);
+void launch_gather_restore(const void *pix, int n, int res, int patch, const int64_t *restore,
+                           int n_keep, void *tokens, cudaStream_t st);
 void launch_resize_u8(const uint8_t *src, int ih, int iw, uint8_t *dst, int oh, int ow,
                       int flip, cudaStream_t st);
 void launch_normalize_u8(const uint8_t *src, int h, int w, float *dst, cudaStream_t st);

@@ -115,20 +115,27 @@ __device__ __forceinline__ float norm_value(int c, int v) {
   return __fdiv_rn(__fsub_rn(__fmul_rn((float)v, inv255), mean), sd);
 }
 
-// k_resize: one CTA per band of P.band (<= kMaxBandRows) output rows of one image.
+// k_resize: one CTA per band of P.band (<= kMaxBandRows) output rows of one
+// image, 256 threads.
 //  1. the source rows the band's bilinear taps touch are colour-converted
-//     once into shared memory (RGBX words, coalesced plane reads);
-//  2. per output column the x taps and weight (flip folded in) are tabulated;
-//  3. each thread produces 8 consecutive output pixels of a row: exact fp64
-//     bilinear from shared memory, normalize through a 256-entry LUT of the
-//     exact fp32 value, 128-bit bf16 (or fp32 / uint8) stores.
-// grid: (ceil(res / P.band), n); dynamic smem: P.src_words (band source rows
-// x widest crop).  The host picks the largest band whose staging fits
-// (32 rows: fewer overlapping source rows and prologues than 16, +3%).
+//     once into shared memory (RGBX words, coalesced plane reads; crops too
+//     wide for the shared budget read the planes directly instead);
+//  2. the column taps (x0, x1, 4096*wx; flip folded in) are tabulated once per
+//     CTA in shared memory, the band's row taps likewise;
+//  3. a thread owns kCols = 8 consecutive output columns of a contiguous
+//     chunk of the band's rows: per source row the 8x3 horizontal
+//     interpolations stay in registers while consecutive output rows share
+//     the row; per output row it produces 8 pixels, normalizes them through a
+//     256-entry LUT of the exact fp32 value and writes one 128-bit store per
+//     channel (8 bf16; two for f32), plus optionally the uint8 NHWC view and
+//     the MAE visible tokens of the pixel's patch.
+// grid: (ceil(res / P.band), n); dynamic smem: P.src_words source words +
+// res column taps.
 constexpr int kResizeMaxDyn = 200 * 1024;
+constexpr int kCols = 8;
 
 // The exact fp32 normalize value of every (channel, uint8) and its bf16 RNE,
-// computed once on the device (init_norm_luts) with the same IEEE ops.
+// computed once per device (init_device_pixels) with the same IEEE ops.
 __device__ float g_norm_lut[768];
 __device__ __nv_bfloat16 g_norm_lutb[768];
 
@@ -139,56 +146,15 @@ __global__ void k_init_norm_luts() {
   g_norm_lutb[i] = __float2bfloat16_rn(f);
 }
 
-void init_norm_luts() { k_init_norm_luts<<<1, 768>>>(); }
+struct __align__(8) ColTap {
+  uint16_t x0, x1;  // source columns of the tap (crop-relative)
+  float wxk;        // float32(wx) * 4096
+};
 
-template <bool AUG>
-__global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
-  TraceScope trace_(P.trace, ESSL_K_RESIZE);
-  extern __shared__ __align__(16) uint8_t dyn[];
-  __shared__ float lut[3][256];
-  __shared__ __nv_bfloat16 lutb[3][256];
-  __shared__ double s_scale[2];
-  const int img = blockIdx.y;
-  const ImgInfo &I = P.info[img];
-  if (I.status != 0) return;
-  const int res = P.res;
-  // 3-Aug (pipeline.py:88-101): point ops are finished here, blur / jitter
-  // images leave their uint8 resize to k_aug_blur / k_aug_out
-  int out_kind = P.out_kind, aop = ESSL_AUG_OP_NONE, athr = 0;
-  uint8_t *out_u8 = P.out_u8;
-  if (AUG) {
-    const essl_aug &A = P.aug[img];
-    if (A.op == ESSL_AUG_OP_BLUR || A.jitter) {
-      out_kind = ESSL_OUT_NONE;
-      out_u8 = P.aug_u8;
-    } else {
-      aop = A.op;
-      athr = A.threshold;
-    }
-  }
-  const int ih = I.rh, iw = I.rw;
-  if (P.out_kind == ESSL_OUT_F32_NCHW)
-    for (int i = threadIdx.x; i < 768; i += kPixThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
-  else
-    for (int i = threadIdx.x; i < 768; i += kPixThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
-  if (threadIdx.x == 0) {  // imgops.py:35-36 scale factors, once per CTA
-    s_scale[0] = __ddiv_rn((double)ih, (double)res);
-    s_scale[1] = __ddiv_rn((double)iw, (double)res);
-  }
-  __syncthreads();
-  const int ob0 = blockIdx.x * P.band;
-  const int ob1 = min(ob0 + P.band, res);
-  const double sy = s_scale[0], sx = s_scale[1];
-  // source rows of the band (taps are monotone in the output row)
-  int ys0, ys1, dummy;
-  double wdum;
-  tap(ob0, sy, ih, ys0, dummy, wdum);
-  tap(ob1 - 1, sy, ih, dummy, ys1, wdum);
-  const int nrows = ys1 - ys0 + 1;
-  uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
-  PlaneSrc S;
-  S.load(I, P.plane);
-  // source rows -> RGBX words in shared memory.
+// Source rows [ys0, ys0 + nrows) of the crop -> RGBX words src[r * iw + x].
+__device__ __forceinline__ void stage_rows(const ImgInfo &I, const PlaneSrc &S, int ys0, int nrows,
+                                           uint32_t *src) {
+  const int iw = I.rw;
   // Fast path (luma at full horizontal resolution, chroma at full or half:
   // 4:2:0, 4:2:2, 4:4:4, gray): work items are (row, group of 4 image
   // columns aligned to 4), so the luma plane is read 4 bytes at a time and
@@ -260,35 +226,129 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
     // generic sampling factors: each thread keeps one column (its plane
     // column offsets fixed) and walks rows, four in flight; no per-pixel
     // division.
-    {
-      const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
-      const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
-      const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
-      if (r0 < rpp) {
-        for (int x = x0; x < iw; x += cpr) {
-          int co[3];
-          S.col_off(I.rx + x, co);
-          for (int r = r0; r < nrows; r += 4 * rpp) {
-            int rr[4], gg[4], bb[4];
+    const int cpr = iw < kPixThreads ? iw : kPixThreads;      // columns per pass
+    const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
+    const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
+    if (r0 < rpp) {
+      for (int x = x0; x < iw; x += cpr) {
+        int co[3];
+        S.col_off(I.rx + x, co);
+        for (int r = r0; r < nrows; r += 4 * rpp) {
+          int rr[4], gg[4], bb[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-              int ro[3];
-              S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
-              S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-              if (r + u * rpp < nrows)
-                src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+          for (int u = 0; u < 4; u++) {
+            int ro[3];
+            S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
+            S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
           }
+#pragma unroll
+          for (int u = 0; u < 4; u++)
+            if (r + u * rpp < nrows)
+              src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
         }
       }
     }
   }
-  // row taps of the band (imgops.py:37-41), shared by every column
+}
+
+// RGBX word of crop pixel (y, x) straight from the planes (crops whose
+// source rows do not fit the shared budget).
+__device__ __forceinline__ uint32_t plane_rgbx(const ImgInfo &I, const PlaneSrc &S, int y, int x) {
+  int r, g, b;
+  S.rgb(I.ry + y, I.rx + x, r, g, b);
+  return (uint32_t)r | ((uint32_t)g << 8) | ((uint32_t)b << 16);
+}
+
+// PLAIN: no 3-Aug, no uint8 view, no visible tokens -- each channel's 8
+// values are finished (and stored) on their own, which keeps the register
+// footprint at the two rows of interpolated values.
+// The exact float64 value of channel c of output pixel (row pair yy, column
+// ox) -- the ambiguous case of the float32 evaluation (imgops.py:49-56).
+template <bool STAGED>
+__device__ __noinline__ int exact_value(const ImgInfo &I, const PlaneSrc &S, const uint32_t *src,
+                                        int iw, int ys0, int2 yy, int ox, int res, double sx,
+                                        double wy, int c) {
+  int tx0, tx1;
+  double wx;
+  tap(I.flip ? res - 1 - ox : ox, sx, iw, tx0, tx1, wx);
+  uint32_t a00, a01, a10, a11;
+  if (STAGED) {
+    a00 = src[yy.x * iw + tx0]; a01 = src[yy.x * iw + tx1];
+    a10 = src[yy.y * iw + tx0]; a11 = src[yy.y * iw + tx1];
+  } else {
+    a00 = plane_rgbx(I, S, ys0 + yy.x, tx0); a01 = plane_rgbx(I, S, ys0 + yy.x, tx1);
+    a10 = plane_rgbx(I, S, ys0 + yy.y, tx0); a11 = plane_rgbx(I, S, ys0 + yy.y, tx1);
+  }
+  return bilerp2(wx, wy, __dsub_rn(1.0, wx), __dsub_rn(1.0, wy), (a00 >> (8 * c)) & 255,
+                 (a01 >> (8 * c)) & 255, (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
+}
+
+template <bool AUG, bool STAGED, bool PLAIN>
+__global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
+  TraceScope trace_(P.trace, ESSL_K_RESIZE);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ float lut[3][256];
+  __shared__ __nv_bfloat16 lutb[3][256];
+  __shared__ double s_scale[2];
   __shared__ int2 ry[kMaxBandRows];
   __shared__ double rw[kMaxBandRows];
   __shared__ float rwf[kMaxBandRows];
+  const int img = blockIdx.y;
+  const ImgInfo &I = P.info[img];
+  if (I.status != 0) return;
+  const int res = P.res;
+  // 3-Aug (pipeline.py:88-101): point ops are finished here, blur / jitter
+  // images leave their uint8 resize to k_aug_blur / k_aug_out
+  int out_kind = P.out_kind, aop = ESSL_AUG_OP_NONE, athr = 0;
+  uint8_t *out_u8 = P.out_u8;
+  bool vis = P.vis != nullptr;
+  if (AUG) {
+    const essl_aug &A = P.aug[img];
+    if (A.op == ESSL_AUG_OP_BLUR || A.jitter) {
+      out_kind = ESSL_OUT_NONE;
+      out_u8 = P.aug_u8;
+      vis = false;
+    } else {
+      aop = A.op;
+      athr = A.threshold;
+    }
+  }
+  const int ih = I.rh, iw = I.rw;
+  if (out_kind == ESSL_OUT_F32_NCHW)
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
+  if (out_kind == ESSL_OUT_BF16_NCHW || vis)
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
+  if (threadIdx.x == 0) {  // imgops.py:35-36 scale factors, once per CTA
+    s_scale[0] = __ddiv_rn((double)ih, (double)res);
+    s_scale[1] = __ddiv_rn((double)iw, (double)res);
+  }
+  __syncthreads();
+  const int ob0 = blockIdx.x * P.band;
+  const int ob1 = min(ob0 + P.band, res);
+  const double sy = s_scale[0], sx = s_scale[1];
+  // source rows of the band (taps are monotone in the output row)
+  int ys0, ys1, dummy;
+  double wdum;
+  tap(ob0, sy, ih, ys0, dummy, wdum);
+  tap(ob1 - 1, sy, ih, dummy, ys1, wdum);
+  const int nrows = ys1 - ys0 + 1;
+  uint32_t *src = reinterpret_cast<uint32_t *>(dyn);  // [nrows][iw] (STAGED)
+  ColTap *ctab = reinterpret_cast<ColTap *>(dyn + (size_t)P.src_words * 4);
+  PlaneSrc S;
+  S.load(I, P.plane);
+  if (STAGED) stage_rows(I, S, ys0, nrows, src);
+  // column taps (imgops.py:42-47; hflip after resize: output column ox reads
+  // the resize's column res-1-ox) and the band's row taps (imgops.py:37-41)
+  for (int ox = threadIdx.x; ox < res; ox += kPixThreads) {
+    int x0, x1;
+    double wx;
+    tap(I.flip ? res - 1 - ox : ox, sx, iw, x0, x1, wx);
+    ColTap t;
+    t.x0 = (uint16_t)x0;
+    t.x1 = (uint16_t)x1;
+    t.wxk = __fmul_rn(__double2float_rn(wx), 4096.0f);
+    ctab[ox] = t;
+  }
   if (threadIdx.x < ob1 - ob0) {
     int y0, y1;
     double wy;
@@ -310,45 +370,51 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
   // x = round(V), |x - 4096*v| < 0.75, so x mod 4096 in [1, 4094] proves
   // int(v) == x >> 12.  Otherwise (x within one unit of a multiple of 4096:
   // ~0.05% of channels, more with dyadic weights giving integral values) the
-  // pixel is recomputed with the reference's float64 expression (bilerp2).
+  // pixel is recomputed with the reference's float64 expression (exact_px).
   //   x + 1 = bits(V + 1.5*2^23 + 1) - 0x4B400000  (round to nearest through
   //   the magic constant; V + 1.5*2^23 + 1 < 2^24 keeps unit spacing).
-  // A thread owns a pair of adjacent output columns (paired bf16 / f32
-  // stores); small outputs split the band's rows over groups of threads.
-  const int npair = (res + 1) >> 1;
-  const int ng = npair >= kPixThreads ? 1 : kPixThreads / npair;
-  const int g = ng > 1 ? threadIdx.x / npair : 0;
-  const int cstart = ng > 1 ? threadIdx.x % npair : threadIdx.x;
-  const int cstep = ng > 1 ? npair : kPixThreads;
-  const int rpg = (ob1 - ob0 + ng - 1) / ng;
-  const int rb = g * rpg, re = min(ob1 - ob0, rb + rpg);
+  const int ngrp = (res + kCols - 1) / kCols;
+  const int band_rows = ob1 - ob0;
+  // slices of rows: thread (group g, slice s) owns rows [r0, r1) of the band
+  const int nsl = ngrp >= kPixThreads ? 1 : min(kPixThreads / ngrp, band_rows);
+  const int sl = ngrp >= kPixThreads ? 0 : threadIdx.x / ngrp;
+  if (sl >= nsl) return;
+  const int r0 = sl * band_rows / nsl, r1 = (sl + 1) * band_rows / nsl;
   const int64_t plane_sz = (int64_t)res * res;
   const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
-  // paired stores need an even element offset for every (image, plane, row)
-  const bool pair_ok = (res & 1) == 0 && (stride & 1) == 0 &&
-                       ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
-  if (g >= ng) return;
+  // 128-bit stores need every (image, plane, row, group) start 16-byte aligned
+  const int esz = out_kind == ESSL_OUT_F32_NCHW ? 4 : 2;
+  const bool vec = (res % kCols) == 0 && ((stride * esz) & 15) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(P.out) & 15) == 0);
+  const bool vec_u8 = (res % kCols) == 0 && ((reinterpret_cast<uintptr_t>(out_u8) & 7) == 0);
+  const int patch = P.patch, gp = patch > 0 ? res / patch : 0;
+  const int tok_dim = patch * patch * 3;
+  const bool vec_vis = patch % kCols == 0 && (reinterpret_cast<uintptr_t>(P.vis) & 15) == 0;
   constexpr float kMagic1 = 12582913.0f;   // 1.5 * 2^23 + 1
   constexpr int kMagicBits = 0x4B400000;   // bits of 1.5 * 2^23
   constexpr float kByteBias = 8388608.0f;  // bits 0x4B000000 | byte == 2^23 + byte
-  for (int q = cstart; q < npair; q += cstep) {
-    const int oxa = 2 * q;
-    const bool two = oxa + 1 < res;
-    int x0[2], x1[2];
-    double wx[2];
-    float wxk[2];
-#pragma unroll
-    for (int j = 0; j < 2; j++) {
-      const int ox = min(oxa + j, res - 1);
-      tap(I.flip ? res - 1 - ox : ox, sx, iw, x0[j], x1[j], wx[j]);  // hflip after resize
-      wxk[j] = __fmul_rn(__double2float_rn(wx[j]), 4096.0f);
-    }
+  for (int grp = ngrp >= kPixThreads ? threadIdx.x : threadIdx.x - sl * ngrp; grp < ngrp;
+       grp += ngrp >= kPixThreads ? kPixThreads : ngrp) {
+    const int oxa = grp * kCols;
+    const int ncol = min(kCols, res - oxa);
+    // (the group's column taps are re-read from shared memory per source
+    // row: registers go to the 2 x 24 interpolated values)
+    const ColTap *ct = ctab + oxa;
     int cy0 = -1, cy1 = -1;
-    float h0[2][3], h1[2][3];
-    auto hrow = [&](int y, float h[2][3]) {
+    float h0[kCols][3], h1[kCols][3];
+    auto hrow = [&](int y, float h[kCols][3]) {
 #pragma unroll
-      for (int j = 0; j < 2; j++) {
-        const uint32_t a0 = src[y * iw + x0[j]], a1 = src[y * iw + x1[j]];
+      for (int j = 0; j < kCols; j++) {
+        const ColTap t = ct[min(j, ncol - 1)];
+        const float wxkj = t.wxk;
+        uint32_t a0, a1;
+        if (STAGED) {
+          a0 = src[y * iw + t.x0];
+          a1 = src[y * iw + t.x1];
+        } else {
+          a0 = plane_rgbx(I, S, ys0 + y, t.x0);
+          a1 = plane_rgbx(I, S, ys0 + y, t.x1);
+        }
 #pragma unroll
         for (int c = 0; c < 3; c++) {
           // 2^23 + byte, exactly (byte c of the RGBX word under exponent 0x4B)
@@ -356,17 +422,17 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
           const float f1 = __uint_as_float(__byte_perm(a1, 0x4B000000u, c | 0x7540));
           // 4096*s0 + 2048 (exact) + (4096*wx) * (s1 - s0), one rounding
           const float base = __fmaf_rn(f0, 4096.0f, 2048.0f - 4096.0f * kByteBias);
-          h[j][c] = __fmaf_rn(wxk[j], __fsub_rn(f1, f0), base);
+          h[j][c] = __fmaf_rn(wxkj, __fsub_rn(f1, f0), base);
         }
       }
     };
-    for (int r = rb; r < re; r++) {
+    for (int r = r0; r < r1; r++) {
       const int2 yy = ry[r];
       const float wy = rwf[r];
-      if (yy.x != cy0) {  // (uniform across the CTA's columns: no divergence)
+      if (yy.x != cy0) {
         if (yy.x == cy1) {
 #pragma unroll
-          for (int j = 0; j < 2; j++)
+          for (int j = 0; j < kCols; j++)
 #pragma unroll
             for (int c = 0; c < 3; c++) h0[j][c] = h1[j][c];
         } else {
@@ -377,7 +443,7 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
       if (yy.y != cy1) {
         if (yy.y == cy0) {
 #pragma unroll
-          for (int j = 0; j < 2; j++)
+          for (int j = 0; j < kCols; j++)
 #pragma unroll
             for (int c = 0; c < 3; c++) h1[j][c] = h0[j][c];
         } else {
@@ -385,79 +451,196 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize(PixelParams P) {
         }
         cy1 = yy.y;
       }
-      int px[2][3];
-      int amb[2] = {4095, 4095};
+      const int oy = ob0 + r;
+      const int64_t o = img * stride + (int64_t)oy * res + oxa;
+      const bool full = ncol == kCols;
+      if (PLAIN) {
 #pragma unroll
-      for (int j = 0; j < 2; j++)
+        for (int c = 0; c < 3; c++) {
+          int pc[kCols];
+          int amb = 4095;
+#pragma unroll
+          for (int j = 0; j < kCols; j++) {
+            const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
+            const int y1 = __float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits;  // round(v) + 1
+            amb = min(amb, y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
+            pc[j] = y1 >> 12;           // == round(v) >> 12 when not ambiguous
+          }
+          if (amb == 0) {  // rare: the exact float64 expression for the ambiguous values
+#pragma unroll
+            for (int j = 0; j < kCols; j++) {
+              const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
+              if (((__float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits) & 4094) == 0)
+                pc[j] = exact_value<STAGED>(I, S, src, iw, ys0, yy, oxa + min(j, ncol - 1), res, sx, rw[r], c);
+            }
+          }
+          if (out_kind == ESSL_OUT_BF16_NCHW) {
+            __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o + c * plane_sz;
+            if (vec) {
+              uint32_t w[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++)
+                w[q] = (uint32_t)__bfloat16_as_ushort(lutb[c][pc[2 * q]]) |
+                       ((uint32_t)__bfloat16_as_ushort(lutb[c][pc[2 * q + 1]]) << 16);
+              // streaming store: the model's input is not re-read here; keep L2
+              // for the unit lists / planes of the batches in flight
+              __stcs(reinterpret_cast<uint4 *>(out), make_uint4(w[0], w[1], w[2], w[3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < kCols; j++)
+                if (j < ncol) out[j] = lutb[c][pc[j]];
+            }
+          } else if (out_kind == ESSL_OUT_F32_NCHW) {
+            float *out = reinterpret_cast<float *>(P.out) + o + c * plane_sz;
+            if (vec) {
+              __stcs(reinterpret_cast<float4 *>(out),
+                     make_float4(lut[c][pc[0]], lut[c][pc[1]], lut[c][pc[2]], lut[c][pc[3]]));
+              __stcs(reinterpret_cast<float4 *>(out + 4),
+                     make_float4(lut[c][pc[4]], lut[c][pc[5]], lut[c][pc[6]], lut[c][pc[7]]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < kCols; j++)
+                if (j < ncol) out[j] = lut[c][pc[j]];
+            }
+          }
+        }
+        continue;
+      }
+      int px[kCols][3];
+      int amb = 4095;
+#pragma unroll
+      for (int j = 0; j < kCols; j++)
 #pragma unroll
         for (int c = 0; c < 3; c++) {
           const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
           const int y1 = __float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits;  // round(v) + 1
-          amb[j] = min(amb[j], y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
-          px[j][c] = y1 >> 12;              // == round(v) >> 12 when not ambiguous
+          amb = min(amb, y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
+          px[j][c] = y1 >> 12;        // == round(v) >> 12 when not ambiguous
         }
+      if (amb == 0) {  // rare: the exact float64 expression for the ambiguous pixels
 #pragma unroll
-      for (int j = 0; j < 2; j++)
-        if (amb[j] == 0) {  // rare: the exact float64 expression (imgops.py:49-56)
-          const double wyd = rw[r];
-          const uint32_t a00 = src[yy.x * iw + x0[j]], a01 = src[yy.x * iw + x1[j]];
-          const uint32_t a10 = src[yy.y * iw + x0[j]], a11 = src[yy.y * iw + x1[j]];
+        for (int j = 0; j < kCols; j++) {
+          bool a = false;
 #pragma unroll
-          for (int c = 0; c < 3; c++)
-            px[j][c] = bilerp2(wx[j], wyd, __dsub_rn(1.0, wx[j]), __dsub_rn(1.0, wyd),
-                               (a00 >> (8 * c)) & 255, (a01 >> (8 * c)) & 255,
-                               (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
+          for (int c = 0; c < 3; c++) {
+            const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
+            a |= ((__float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits) & 4094) == 0;
+          }
+          if (a) {
+#pragma unroll
+            for (int c = 0; c < 3; c++)
+              px[j][c] = exact_value<STAGED>(I, S, src, iw, ys0, yy, oxa + min(j, ncol - 1), res, sx,
+                                             rw[r], c);
+          }
         }
+      }
       if (AUG && aop == ESSL_AUG_OP_GRAY) {  // imgops.py:75-91
 #pragma unroll
-        for (int j = 0; j < 2; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
+        for (int j = 0; j < kCols; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
       } else if (AUG && aop == ESSL_AUG_OP_SOLARIZE) {  // imgops.py:94-108
 #pragma unroll
-        for (int j = 0; j < 2; j++)
+        for (int j = 0; j < kCols; j++)
 #pragma unroll
           for (int c = 0; c < 3; c++) px[j][c] = px[j][c] >= athr ? 255 - px[j][c] : px[j][c];
       }
-      const int oy = ob0 + r;
-      const int64_t o = img * stride + (int64_t)oy * res + oxa;
       if (out_kind == ESSL_OUT_BF16_NCHW) {
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
-        if (pair_ok) {
+        if (vec) {
 #pragma unroll
           for (int c = 0; c < 3; c++) {
-            const uint32_t lo = __bfloat16_as_ushort(lutb[c][px[0][c]]);
-            const uint32_t hi = __bfloat16_as_ushort(lutb[c][px[1][c]]);
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              w[q] = (uint32_t)__bfloat16_as_ushort(lutb[c][px[2 * q][c]]) |
+                     ((uint32_t)__bfloat16_as_ushort(lutb[c][px[2 * q + 1][c]]) << 16);
             // streaming store: the model's input is not re-read here; keep L2
             // for the unit lists / planes of the batches in flight
-            __stcs(reinterpret_cast<unsigned int *>(out + c * plane_sz), lo | (hi << 16));
+            __stcs(reinterpret_cast<uint4 *>(out + c * plane_sz), make_uint4(w[0], w[1], w[2], w[3]));
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 3; c++) {
-            out[c * plane_sz] = lutb[c][px[0][c]];
-            if (two) out[c * plane_sz + 1] = lutb[c][px[1][c]];
-          }
+          for (int c = 0; c < 3; c++)
+#pragma unroll
+            for (int j = 0; j < kCols; j++)
+              if (j < ncol) out[c * plane_sz + j] = lutb[c][px[j][c]];
         }
       } else if (out_kind == ESSL_OUT_F32_NCHW) {
         float *out = reinterpret_cast<float *>(P.out) + o;
-        if (pair_ok) {
-#pragma unroll
-          for (int c = 0; c < 3; c++)
-            __stcs(reinterpret_cast<float2 *>(out + c * plane_sz), make_float2(lut[c][px[0][c]], lut[c][px[1][c]]));
-        } else {
+        if (vec) {
 #pragma unroll
           for (int c = 0; c < 3; c++) {
-            out[c * plane_sz] = lut[c][px[0][c]];
-            if (two) out[c * plane_sz + 1] = lut[c][px[1][c]];
+            __stcs(reinterpret_cast<float4 *>(out + c * plane_sz),
+                   make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]));
+            __stcs(reinterpret_cast<float4 *>(out + c * plane_sz + 4),
+                   make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]));
           }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; c++)
+#pragma unroll
+            for (int j = 0; j < kCols; j++)
+              if (j < ncol) out[c * plane_sz + j] = lut[c][px[j][c]];
         }
       }
       if (out_u8) {
         uint8_t *out = out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
+        if (vec_u8 && full) {
+          uint32_t w[6];
 #pragma unroll
-        for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[0][c];
-        if (two)
+          for (int q = 0; q < 6; q++) {
+            uint32_t v = 0;
 #pragma unroll
-          for (int c = 0; c < 3; c++) out[3 + c] = (uint8_t)px[1][c];
+            for (int b = 0; b < 4; b++) v |= (uint32_t)px[(4 * q + b) / 3][(4 * q + b) % 3] << (8 * b);
+            w[q] = v;
+          }
+#pragma unroll
+          for (int q = 0; q < 3; q++)
+            *reinterpret_cast<uint2 *>(out + 8 * q) = make_uint2(w[2 * q], w[2 * q + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < kCols; j++)
+            if (j < ncol)
+#pragma unroll
+              for (int c = 0; c < 3; c++) out[3 * j + c] = (uint8_t)px[j][c];
+        }
+      }
+      if (vis && patch > 0) {
+        // MAE visible tokens (patchify 'nchpwq->nhwpqc'): the
+        // pixel's patch is visible when ids_restore maps it below n_keep;
+        // its token row holds (q, c) pairs of patch row oy % patch
+        __nv_bfloat16 *tok = reinterpret_cast<__nv_bfloat16 *>(P.vis);
+        const int64_t *rest = P.vis_restore + (int64_t)img * gp * gp;
+        if (vec_vis && full) {
+          const int id = (oy / patch) * gp + oxa / patch;
+          const int64_t rk = rest[id];
+          if (rk < P.n_keep) {
+            __nv_bfloat16 *t = tok + ((int64_t)img * P.n_keep + rk) * tok_dim +
+                               ((oy % patch) * patch + oxa % patch) * 3;
+            uint32_t w[12];
+#pragma unroll
+            for (int q = 0; q < 12; q++) {
+              const int e0 = 2 * q, e1 = 2 * q + 1;
+              w[q] = (uint32_t)__bfloat16_as_ushort(lutb[e0 % 3][px[e0 / 3][e0 % 3]]) |
+                     ((uint32_t)__bfloat16_as_ushort(lutb[e1 % 3][px[e1 / 3][e1 % 3]]) << 16);
+            }
+#pragma unroll
+            for (int q = 0; q < 3; q++)
+              __stcs(reinterpret_cast<uint4 *>(t) + q,
+                     make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < kCols; j++) {
+            if (j >= ncol) continue;
+            const int ox = oxa + j;
+            const int64_t rk = rest[(oy / patch) * gp + ox / patch];
+            if (rk >= P.n_keep) continue;
+            __nv_bfloat16 *t = tok + ((int64_t)img * P.n_keep + rk) * tok_dim +
+                               ((oy % patch) * patch + ox % patch) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; c++) t[c] = lutb[c][px[j][c]];
+          }
+        }
       }
     }
   }
@@ -469,18 +652,26 @@ int band_source_rows(int h, int res, int band) {
   return (int)(((int64_t)band * h + res - 1) / res) + 3;
 }
 
+size_t resize_smem(const PixelParams &p) {
+  return (size_t)p.src_words * 4 + (size_t)p.res * sizeof(ColTap);
+}
+
 void launch_resize(const PixelParams &p, cudaStream_t st) {
   if (p.n <= 0) return;
-  const size_t dyn = (size_t)p.src_words * 4;
-  static bool attr = false;  // opt in once to the largest dynamic size api.cu allows
-  if (!attr) {
-    cudaFuncSetAttribute(k_resize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
-    cudaFuncSetAttribute(k_resize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
-    attr = true;
-  }
+  const size_t dyn = resize_smem(p);
   dim3 grid((p.res + p.band - 1) / p.band, p.n);
-  if (p.aug) k_resize<true><<<grid, kPixThreads, dyn, st>>>(p);
-  else k_resize<false><<<grid, kPixThreads, dyn, st>>>(p);
+  const bool staged = p.src_words > 0;
+  const bool plain = !p.aug && !p.out_u8 && !p.vis;
+  if (p.aug) {
+    if (staged) k_resize<true, true, false><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<true, false, false><<<grid, kPixThreads, dyn, st>>>(p);
+  } else if (plain) {
+    if (staged) k_resize<false, true, true><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<false, false, true><<<grid, kPixThreads, dyn, st>>>(p);
+  } else {
+    if (staged) k_resize<false, true, false><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<false, false, false><<<grid, kPixThreads, dyn, st>>>(p);
+  }
 }
 
 // decode_crop output: uint8 [h, w, 3] at out + offsets[img].
@@ -605,6 +796,31 @@ __global__ void k_gather(const __nv_bfloat16 *pix, int res, int patch, const int
     tok[(int64_t)s * total + e] =
         pix[(((int64_t)s * 3 + c) * res + ph * patch + pr) * res + pw * patch + pc];
   }
+}
+
+// Same tokens placed by ids_restore (token id -> row rank when < n_keep):
+// the 3-Aug path's gather from finished pixels.
+__global__ void k_gather_restore(const __nv_bfloat16 *pix, int res, int patch, const int64_t *restore,
+                                 int n_keep, __nv_bfloat16 *tok) {
+  const int s = blockIdx.x;
+  const int g = res / patch, T = g * g, dim = patch * patch * 3;
+  for (int64_t e = threadIdx.x; e < (int64_t)T * dim; e += blockDim.x) {
+    const int id = (int)(e / dim), w = (int)(e % dim);
+    const int64_t rk = restore[(int64_t)s * T + id];
+    if (rk >= n_keep) continue;
+    const int ph = id / g, pw = id % g;
+    const int pr = w / (patch * 3), rem = w % (patch * 3);
+    const int pc = rem / 3, c = rem % 3;
+    tok[((int64_t)s * n_keep + rk) * dim + w] =
+        pix[(((int64_t)s * 3 + c) * res + ph * patch + pr) * res + pw * patch + pc];
+  }
+}
+
+void launch_gather_restore(const void *pix, int n, int res, int patch, const int64_t *restore,
+                           int n_keep, void *tokens, cudaStream_t st) {
+  if (n <= 0 || n_keep <= 0) return;
+  k_gather_restore<<<n, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(pix), res, patch,
+                                      restore, n_keep, reinterpret_cast<__nv_bfloat16 *>(tokens));
 }
 
 void launch_gather(const void *pix, int n, int res, int patch, const int64_t *keep, int n_keep,
@@ -803,7 +1019,7 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
   if (jitter) {
     unsigned long long sum = 0;
     for (int64_t g = threadIdx.x; g < ngrp; g += kAugOutThreads) {
-      uint8_t b[12];
+      alignas(16) uint8_t b[12];
       *reinterpret_cast<uint3 *>(b) = make_uint3(src4[3 * g], src4[3 * g + 1], src4[3 * g + 2]);
 #pragma unroll
       for (int j = 0; j < 4; j++) {
@@ -840,7 +1056,7 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
     }
   };
   for (int64_t g = threadIdx.x; g < ngrp; g += kAugOutThreads) {
-    uint8_t b[12];
+    alignas(16) uint8_t b[12];
     *reinterpret_cast<uint3 *>(b) = make_uint3(src4[3 * g], src4[3 * g + 1], src4[3 * g + 2]);
     int q[4][3];
 #pragma unroll
@@ -866,7 +1082,7 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
             make_float4(lut[c][q[0][c]], lut[c][q[1][c]], lut[c][q[2][c]], lut[c][q[3][c]]);
     }
     if (P.out_u8) {
-      uint8_t ob[12];
+      alignas(16) uint8_t ob[12];
 #pragma unroll
       for (int j = 0; j < 4; j++)
 #pragma unroll
@@ -898,12 +1114,6 @@ __global__ void __launch_bounds__(kAugOutThreads) k_aug_out(AugOutParams P) {
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st) {
   if (p.n <= 0) return;
   if (max_radius > 0) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_aug_blur, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)aug_blur_smem(ESSL_AUG_MAX_RADIUS));
-      attr = true;
-    }
     const int tiles = ((p.h + kAugTile - 1) / kAugTile) * ((p.w + kAugTile - 1) / kAugTile);
     k_aug_blur<<<dim3(tiles, p.n), kAugBlurThreads, aug_blur_smem(max_radius), st>>>(
         p.a, p.h, p.w, p.aug, p.b);
@@ -1040,16 +1250,23 @@ void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t 
   if (n <= 0) return;
   const int grid = ctas > 0 && ctas < n ? ctas : n;
   if (tma) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_host_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kTmaChunk * kTmaStages);
-      attr = true;
-    }
     k_host_gather_tma<<<grid, 32, kTmaChunk * kTmaStages, st>>>(src, d, n, dst);
   } else {
     k_host_gather<<<grid, kGatherThreads, 0, st>>>(src, d, n, dst);
   }
+}
+
+// Per-device one-time setup (api.cu, once per device): the normalize LUTs
+// (__device__ arrays exist per device) and the dynamic shared-memory opt-ins.
+void init_device_pixels() {
+  k_init_norm_luts<<<1, 768>>>();
+  for (auto f : {k_resize<false, true, true>, k_resize<false, false, true>, k_resize<false, true, false>,
+                 k_resize<false, false, false>, k_resize<true, true, false>, k_resize<true, false, false>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+  cudaFuncSetAttribute(k_aug_blur, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)aug_blur_smem(ESSL_AUG_MAX_RADIUS));
+  cudaFuncSetAttribute(k_host_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kTmaChunk * kTmaStages);
 }
 
 }  // namespace essl

@@ -1,6 +1,6 @@
 """DDP plumbing of the loader: samples are independent and
 keyed by (seed, epoch, index), so rank r decodes perm[r::world] of the
-epoch permutation computed identically on every rank -- there is no
+(padded, DistributedSampler-style) epoch permutation computed identically on every rank -- there is no
 collective on the data path.  The only collective is the reporting
 reduction after a timed region (max time, summed work), over whatever
 process group is initialised (NCCL on the GPU box, gloo in the CPU tests).
@@ -13,10 +13,11 @@ import numpy as np
 from .rng import epoch_permutation, shard
 
 
-def rank_shard(seed: int, epoch: int, n: int, rank: int, world_size: int) -> np.ndarray:
-    """Indices rank `rank` decodes in `epoch` (pipeline.py:237-243 + DistributedSampler
-    striding, no padding)."""
-    return shard(epoch_permutation(seed, epoch, n), rank, world_size)
+def rank_shard(seed: int, epoch: int, n: int, rank: int, world_size: int,
+               mode: str = "pad") -> np.ndarray:
+    """Indices rank `rank` decodes in `epoch` (pipeline.py:237-243 +
+    DistributedSampler striding; rng.shard for the padding modes)."""
+    return shard(epoch_permutation(seed, epoch, n), rank, world_size, mode)
 
 
 def reduce_timing(values, device=None) -> tuple[float, float, float, float]:

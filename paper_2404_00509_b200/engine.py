@@ -140,15 +140,19 @@ class Engine:
 
     def decode_rrc(self, blob_ptr: int, samples: np.ndarray, res: int, out_kind: int,
                    out=None, out_u8=None, results=None, stream=None, max_side: int = 0,
-                   aug: np.ndarray | None = None):
+                   aug: np.ndarray | None = None, out_stride: int = 0, vis=None):
         """Decode + RRC resize + flip (+ 3-Aug stage when ``aug``, an
-        N.aug_dtype() array with blur weights filled) + normalize."""
+        N.aug_dtype() array with blur weights filled) + normalize.  ``vis``:
+        (patch, ids_restore, tokens) for the fused visible-token output."""
         n = len(samples)
         self._ensure(n, max_side, int(samples["length"].max()) if n else 0)
-        N.check(N.lib().essl_decode_rrc_aug(self._ctx, ctypes.c_void_p(blob_ptr), N.ptr(samples),
-                                            N.ptr(aug), n, res, out_kind, N.ptr(out), 0,
-                                            N.ptr(out_u8), N.ptr(results), self._st(stream)),
-                "essl_decode_rrc")
+        patch, restore, tokens = vis if vis is not None else (0, None, None)
+        n_keep = int(tokens.shape[1]) if tokens is not None else 0
+        N.check(N.lib().essl_decode_rrc_visible(
+            self._ctx, ctypes.c_void_p(blob_ptr), N.ptr(samples), N.ptr(aug), n, res, out_kind,
+            N.ptr(out), out_stride, N.ptr(out_u8), patch if tokens is not None else 0,
+            N.ptr(restore if tokens is not None else None), n_keep, N.ptr(tokens), N.ptr(results),
+            self._st(stream)), "essl_decode_rrc")
 
     def augment_u8(self, src, aug: np.ndarray, dst, stream=None):
         """apply_aug's pixel stage on device uint8 [n,h,w,3] images."""

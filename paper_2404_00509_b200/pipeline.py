@@ -37,7 +37,7 @@ from .container import ContainerHandle, open_container
 from .errors import ConfigError, CorruptionError
 from .jpeg import CropRect
 from .masking import MaskSpec
-from .rng import SampleRng, epoch_permutation, shard
+from .rng import SampleRng, epoch_permutation, shard, shard_len
 from .schedule import AugLevel
 
 
@@ -92,7 +92,8 @@ class ImageBatch:
 
     pixels: [b,3,h,h] float32 (reference dtype) or bfloat16; labels/indices
     int64 [b]; mask int32 [b,k] sorted masked ids; uint8 [b,h,h,3] view;
-    ids_keep int64 [b,N-k]; ids_restore int64 [b,N]."""
+    ids_keep int64 [b,N-k]; ids_restore int64 [b,N]; visible bf16
+    [b,N-k,p*p*3] (optional)."""
 
     pixels: object
     labels: object
@@ -102,13 +103,16 @@ class ImageBatch:
     uint8: object = None
     ids_keep: object = None
     ids_restore: object = None
+    # MAE visible tokens (LoaderConfig.visible): bf16 [b, N-k, patch*patch*3],
+    # patchify 'nchpwq->nhwpqc' of pixels gathered at ids_keep
+    visible: object = None
 
     def __len__(self) -> int:
         return int(self.pixels.shape[0])
 
 
 _GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch",
-             "streams", "staging")
+             "streams", "staging", "shard_mode", "visible")
 
 
 @dataclass
@@ -144,6 +148,12 @@ class LoaderConfig:
     # bindings' "valid until the next step" contract) instead of
     # allocating every batch.
     reuse_outputs: bool = False
+    # DDP partition of each epoch's permutation (rng.shard): "pad" (equal
+    # shards, DistributedSampler default), "drop" or "stride" (perm[r::world])
+    shard_mode: str = "pad"
+    # emit ImageBatch.visible: the MAE encoder's visible tokens, written by the
+    # resize kernel itself (needs mask_ratio > 0)
+    visible: bool = False
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
@@ -187,6 +197,10 @@ class LoaderConfig:
             raise ConfigError(f"staging must be gather or copy, got {self.staging!r}")
         if self.streams < 1 or self.prefetch < 1:
             raise ConfigError("streams and prefetch must be >= 1")
+        if self.visible and self.mask_ratio <= 0.0:
+            raise ConfigError("visible tokens need mask_ratio > 0")
+        if self.shard_mode not in ("pad", "drop", "stride"):
+            raise ConfigError(f"shard_mode must be pad, drop or stride, got {self.shard_mode!r}")
 
 
 class _HostRing:
@@ -202,24 +216,27 @@ class _HostRing:
         self.il_np = [t.numpy() for t in self.il]
         self.res = [torch.empty((batch, result_words), dtype=torch.int32, pin_memory=True)
                     for _ in range(depth)]
-        self.ev = [None] * depth
+        self.ev = [torch.cuda.Event() for _ in range(depth)]
+        self.used = [False] * depth
         self.next = 0
 
     def take(self):
         i = self.next
         self.next = (i + 1) % self.depth
-        if self.ev[i] is not None:
+        if self.used[i]:
             self.ev[i].synchronize()  # the batch that used this slot is done
+        self.used[i] = True
         return i
 
 
 @dataclass
 class _Pending:
     batch: ImageBatch
-    samples: np.ndarray
+    samples: np.ndarray | None  # None: descriptors were built natively (rebuilt on error)
     indices: np.ndarray
     results_host: object
     event: object
+    epoch: int = 0
     keep: list = field(default_factory=list)
 
 
@@ -274,6 +291,15 @@ class Loader:
         self._out_ring: dict = {}
         self._out_next = [0] * len(self._engines)
         self._out_dtype = torch.bfloat16 if config.out_dtype == "bfloat16" else torch.float32
+        # the record table, copied once into the native batch planner
+        self._ds = ctypes.c_void_p()
+        N.check(N.lib().essl_dataset_create(len(self._offsets), N.ptr(self._offsets),
+                                            N.ptr(self._lengths), N.ptr(self._crcs),
+                                            N.ptr(self._widths), N.ptr(self._heights),
+                                            N.ptr(self._labels_np), ctypes.byref(self._ds)),
+                "essl_dataset_create")
+        self._bcfg = N.EsslBatchCfg()
+        self._bio = N.EsslBatchIo()
 
     @classmethod
     def from_document(cls, doc) -> "Loader":
@@ -283,8 +309,8 @@ class Loader:
         return len(self.handle)
 
     def _shard_len(self) -> int:
-        n, r, w = len(self.handle), self.config.rank, self.config.world_size
-        return max(0, (n - r + w - 1) // w)
+        c = self.config
+        return shard_len(len(self.handle), c.rank, c.world_size, c.shard_mode)
 
     @property
     def batches_per_epoch(self) -> int:
@@ -307,6 +333,9 @@ class Loader:
                           if cfg.mask_ratio > 0.0 else None)
 
     def close(self) -> None:
+        if getattr(self, "_ds", None):
+            N.lib().essl_dataset_destroy(self._ds)
+            self._ds = ctypes.c_void_p()
         if self._own_handle:
             self.handle.close()
 
@@ -345,43 +374,18 @@ class Loader:
             augment.fill_weights(aug)
         return s, aug
 
-    def enqueue(self, epoch: int, idxs: np.ndarray) -> _Pending:
-        """Issue one batch on the device (asynchronous, on the next of the
-        loader's streams)."""
+    def _outputs(self, j: int, b: int, pixels=None):
+        """This batch's output tensors: caller-provided pixels, the reuse ring
+        (R slots per stream, R * streams > the batches in flight beyond the
+        one the consumer holds), or fresh tensors."""
         import torch
         cfg = self.config
-        j = self._rr
-        self._rr = (j + 1) % len(self._engines)
-        eng, st = self._engines[j], self._streams[j]
-        cur = torch.cuda.current_stream(self.device)
-        st.wait_stream(cur)  # outputs come from the consumer stream's pool
-        idxs = np.ascontiguousarray(idxs, np.int64)
-        b, res = len(idxs), cfg.res
-        samples, aug = self._descriptors(epoch, idxs)
-        if self._blob is not None:
-            blob_ptr = self._blob.data_ptr()
-        elif cfg.staging == "gather":  # host container read over the bus by k_host_gather
-            blob_ptr = eng.stage_pinned(self._slots[j], self._pinned_base, samples["offset"],
-                                        samples["length"].copy(), samples, stream=st)
-            self._slots[j] ^= 1
-        else:  # host threads -> pinned ring -> one copy-engine transfer
-            ptrs = samples["offset"] + np.uint64(self._host_base)
-            blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
-                                 nthreads=min(8, self.workers), stream=st)
-            self._slots[j] ^= 1
-        dev = self.device
-        ring = self._rings[j]
-        slot = ring.take()  # the batch that last used this slot has completed
-        T = k = 0
-        if self.mask_spec is not None:
-            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
-
-        # reused outputs: R slots per stream, R * streams > batches in flight
-        # beyond the one the consumer holds (prefetch + 1)
         n_st = len(self._engines)
         R = max(2, -(-(max(cfg.prefetch, n_st) + 2) // n_st))
         oslot = self._out_next[j] % R
         self._out_next[j] += 1
+        dev = self.device
+        res = cfg.res
 
         def out(name, shape, dtype):
             if not cfg.reuse_outputs:
@@ -395,39 +399,139 @@ class Loader:
                 self._out_ring[key] = t
             return t
 
-        pixels = out("pixels", (b, 3, res, res), self._out_dtype)
-        u8 = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
-        results = out("results", (b, ctypes.sizeof(N.EsslResult) // 4), torch.int32)
+        o = {}
+        if pixels is not None:
+            if tuple(pixels.shape) != (b, 3, res, res) or pixels.dtype != self._out_dtype or \
+                    pixels.device != dev or pixels.stride()[1:] != (res * res, res, 1):
+                raise ValueError(f"pixels buffer must be {self._out_dtype} [{b},3,{res},{res}] on "
+                                 f"{dev} with dense planes")
+            o["pixels"] = pixels
+        else:
+            o["pixels"] = out("pixels", (b, 3, res, res), self._out_dtype)
+        o["u8"] = out("u8", (b, res, res, 3), torch.uint8) if cfg.keep_uint8 else None
+        o["results"] = out("results", (b, ctypes.sizeof(N.EsslResult) // 4), torch.int32)
+        o["il"] = out("il", (2 * b,), torch.int64)
+        if self.mask_spec is not None:
+            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
+            o["mask"] = out("mask", (b, k), torch.int32)
+            o["keep"] = out("keep", (b, T - k), torch.int64)
+            o["restore"] = out("restore", (b, T), torch.int64)
+            if cfg.visible:
+                o["tokens"] = out("tokens", (b, T - k, cfg.patch * cfg.patch * 3), torch.bfloat16)
+        return o
+
+    def enqueue(self, epoch: int, idxs: np.ndarray, pixels=None) -> _Pending:
+        """Issue one batch on the device (asynchronous, on the next of the
+        loader's streams): ONE native call (essl_batch_enqueue) builds the
+        descriptors (RRC + flip draws), uploads indices/labels, gathers host
+        payloads when the container is not resident, runs the mask and the
+        decode/resize kernels and downloads the per-image results.
+        ``pixels``: optional caller-owned output buffer [b,3,res,res] (e.g. a
+        slice of the model's input buffer) written in place of the ring."""
+        import torch
+        cfg = self.config
+        if self._blob is None and cfg.staging == "copy":
+            return self._enqueue_py(epoch, idxs, pixels)
+        j = self._rr
+        self._rr = (j + 1) % len(self._engines)
+        eng, st = self._engines[j], self._streams[j]
+        st.wait_stream(torch.cuda.current_stream(self.device))  # outputs / the consumer's reads
+        idxs = np.ascontiguousarray(idxs, np.int64)
+        b = len(idxs)
+        o = self._outputs(j, b, pixels)
+        ring = self._rings[j]
+        slot = ring.take()  # the batch that last used this slot has completed
+        res_host = ring.res[slot][:b]
+        aug = None
+        if self.aug_level is not AugLevel.SIMPLE:
+            _, aug = self._descriptors(epoch, idxs)
+        c = self._bcfg
+        c.seed, c.epoch = cfg.seed & (2**64 - 1), epoch & (2**64 - 1)
+        c.scale[0], c.scale[1] = self.rrc.scale
+        c.ratio[0], c.ratio[1] = self.rrc.ratio
+        c.res = cfg.res
+        c.out_kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
+        c.check_crc = 1
+        T = k = 0
+        if self.mask_spec is not None:
+            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
+        c.tokens, c.masked, c.patch = T, k, cfg.patch
+        io = self._bio
+        if self._blob is not None:
+            io.blob, io.pinned_base, io.stage_slot = self._blob.data_ptr(), None, 0
+        else:
+            io.blob, io.pinned_base, io.stage_slot = None, self._pinned_base, self._slots[j]
+            self._slots[j] ^= 1
+        io.aug = None if aug is None else aug.ctypes.data
+
+        def dp(name):
+            t = o.get(name)
+            return None if t is None else t.data_ptr()
+
+        io.pixels, io.pixel_stride = o["pixels"].data_ptr(), int(o["pixels"].stride()[0])
+        io.u8, io.index_label = dp("u8"), o["il"].data_ptr()
+        io.mask, io.ids_keep, io.ids_restore, io.tokens = dp("mask"), dp("keep"), dp("restore"), dp("tokens")
+        io.results, io.results_host = o["results"].data_ptr(), res_host.data_ptr()
+        N.check(N.lib().essl_batch_enqueue(eng._ctx, self._ds, ctypes.byref(c), N.ptr(idxs), b,
+                                           ctypes.byref(io), ctypes.c_void_p(st.cuda_stream)),
+                "essl_batch_enqueue")
+        if not cfg.reuse_outputs and pixels is None:  # fresh tensors: tell the allocator about st
+            for t in o.values():
+                if t is not None:
+                    t.record_stream(st)
+        ev = ring.ev[slot]
+        ev.record(st)
+        il = o["il"]
+        batch = ImageBatch(o["pixels"], il[b:], il[:b], epoch, o.get("mask"), o["u8"], o.get("keep"),
+                           o.get("restore"), o.get("tokens"))
+        return _Pending(batch, None, idxs, res_host, ev, epoch)
+
+    def _enqueue_py(self, epoch: int, idxs: np.ndarray, pixels=None) -> _Pending:
+        """Host-thread staging path (staging="copy"): descriptors in numpy,
+        payloads gathered by host threads into a pinned ring, then the
+        decode / mask calls one by one."""
+        import torch
+        cfg = self.config
+        j = self._rr
+        self._rr = (j + 1) % len(self._engines)
+        eng, st = self._engines[j], self._streams[j]
+        st.wait_stream(torch.cuda.current_stream(self.device))
+        idxs = np.ascontiguousarray(idxs, np.int64)
+        b, res = len(idxs), cfg.res
+        samples, aug = self._descriptors(epoch, idxs)
+        ptrs = samples["offset"] + np.uint64(self._host_base)
+        blob_ptr = eng.stage(self._slots[j], ptrs, samples["length"].copy(), samples,
+                             nthreads=min(8, self.workers), stream=st)
+        self._slots[j] ^= 1
+        ring = self._rings[j]
+        slot = ring.take()
+        o = self._outputs(j, b, pixels)
         kind = N.ESSL_OUT_BF16_NCHW if self._out_dtype == torch.bfloat16 else N.ESSL_OUT_F32_NCHW
-        # host->device copies first (a copy queued behind this batch's kernels
-        # would hold up later batches' copies on the shared copy engine):
-        # indices and labels in one pinned buffer, one stream-ordered copy
         hil, hil_np, res_host = ring.il[slot], ring.il_np[slot], ring.res[slot][:b]
         hil_np[:b] = idxs
         hil_np[b:2 * b] = self._labels_np[idxs]
-        il = out("il", (2 * b,), torch.int64)
+        il = o["il"]
         sp = ctypes.c_void_p(st.cuda_stream)
         L = N.lib()
         N.check(L.essl_memcpy_async(N.ptr(il), N.ptr(hil), 16 * b, sp), "essl_memcpy_async")
         indices, labels = il[:b], il[b:]
-        eng.decode_rrc(blob_ptr, samples, res, kind, pixels, u8, results, stream=st, aug=aug)
-        mask = keep = restore = None
         if self.mask_spec is not None:
-            mask = out("mask", (b, k), torch.int32)
-            keep = out("keep", (b, T - k), torch.int64)
-            restore = out("restore", (b, T), torch.int64)
-            eng.mask(cfg.seed, epoch, indices, T, k, mask, keep, restore, stream=st)
-        N.check(L.essl_memcpy_async(N.ptr(res_host), N.ptr(results), results.numel() * 4, sp),
+            T, k = self.mask_spec.tokens, self.mask_spec.masked_count
+            eng.mask(cfg.seed, epoch, indices, T, k, o["mask"], o["keep"], o["restore"], stream=st)
+        eng.decode_rrc(blob_ptr, samples, res, kind, o["pixels"], o["u8"], o["results"], stream=st,
+                       aug=aug, out_stride=int(o["pixels"].stride()[0]),
+                       vis=(cfg.patch, o.get("restore"), o.get("tokens")))
+        N.check(L.essl_memcpy_async(N.ptr(res_host), N.ptr(o["results"]), o["results"].numel() * 4, sp),
                 "essl_memcpy_async")
-        if not cfg.reuse_outputs:  # fresh tensors: tell the allocator about st
-            for t in (pixels, u8, results, mask, keep, restore, il):
+        if not cfg.reuse_outputs and pixels is None:
+            for t in o.values():
                 if t is not None:
                     t.record_stream(st)
-        ev = torch.cuda.Event()
+        ev = ring.ev[slot]
         ev.record(st)
-        ring.ev[slot] = ev
-        batch = ImageBatch(pixels, labels, indices, epoch, mask, u8, keep, restore)
-        return _Pending(batch, samples, idxs, res_host, ev)
+        batch = ImageBatch(o["pixels"], labels, indices, epoch, o.get("mask"), o["u8"], o.get("keep"),
+                           o.get("restore"), o.get("tokens"))
+        return _Pending(batch, samples, idxs, res_host, ev, epoch)
 
     def join(self, p: _Pending) -> None:
         """Make the consumer stream wait for a batch (no host sync)."""
@@ -438,7 +542,10 @@ class Loader:
         """Wait for a batch and raise the reference exception on failure."""
         self.join(p)
         p.event.synchronize()
-        self.engine.raise_for(p.results_host.numpy(), p.samples, p.indices)
+        r = p.results_host.numpy()
+        if r[:, 0].any():
+            samples = p.samples if p.samples is not None else self._descriptors(p.epoch, p.indices)[0]
+            self.engine.raise_for(r, samples, p.indices)
         return p.batch
 
     @property
@@ -465,36 +572,55 @@ class Loader:
     def _plan(self, epoch: int):
         cfg = self.config
         perm = shard(epoch_permutation(cfg.seed, epoch, len(self.handle)), cfg.rank,
-                     cfg.world_size)
+                     cfg.world_size, cfg.shard_mode)
         B = cfg.batch_size
         for s in range(0, len(perm), B):
             yield epoch, perm[s:s + B]
 
-    def _run(self, plan):
+    def _run(self, plan, into=None):
         """Keep `depth` batches in flight over the (epoch, indices) plan."""
         q: deque = deque()
         depth = max(self.config.prefetch, len(self._engines))
+        if into is not None and len(into) < depth + 1:
+            raise ValueError(f"into: need at least {depth + 1} buffers for {depth} batches in flight")
         it = iter(plan)
+        nb = 0
+
+        def issue(e, idxs):
+            nonlocal nb
+            buf = None
+            if into is not None:
+                buf = into[nb % len(into)]
+                buf = buf[:len(idxs)] if buf.shape[0] != len(idxs) else buf
+            nb += 1
+            return self.enqueue(e, idxs, buf)
+
         for e, idxs in it:
-            q.append(self.enqueue(e, idxs))
+            q.append(issue(e, idxs))
             if len(q) >= depth:
                 break
         while q:
             p = q.popleft()
             nxt = next(it, None)
             if nxt is not None:
-                q.append(self.enqueue(*nxt))
+                q.append(issue(*nxt))
             yield self.finish(p)
 
-    def epoch(self, epoch: int):
-        """Yield the batches of one epoch (this rank's shard) in permutation order."""
-        return self._run(self._plan(epoch))
+    def epoch(self, epoch: int, into=None):
+        """Yield the batches of one epoch (this rank's shard) in permutation order.
 
-    def epochs(self, first: int, count: int | None = None):
+        ``into``: optional sequence of caller-owned pixel buffers
+        [batch_size,3,res,res] (e.g. the model's input buffers), used round
+        robin; a batch's pixels are written straight into its buffer, which
+        must not be reused before the batch has been consumed (pass at least
+        prefetch + 2 buffers)."""
+        return self._run(self._plan(epoch), into)
+
+    def epochs(self, first: int, count: int | None = None, into=None):
         """Batches of epochs first, first+1, ... (count of them, or without
         end) with the prefetch pipeline kept full across epoch boundaries --
         the same batches as consecutive epoch() calls, without the drain /
         refill bubble at each boundary (a persistent-worker DataLoader)."""
         import itertools
         es = itertools.count(first) if count is None else range(first, first + count)
-        return self._run(itertools.chain.from_iterable(self._plan(e) for e in es))
+        return self._run(itertools.chain.from_iterable(self._plan(e) for e in es), into)

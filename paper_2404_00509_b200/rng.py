@@ -54,9 +54,37 @@ def epoch_permutation(seed: int, epoch: int, n: int) -> np.ndarray:
     return out
 
 
-def shard(perm: np.ndarray, rank: int, world_size: int) -> np.ndarray:
-    """DDP partition of an epoch permutation: rank r takes perm[r::world]
-    (DistributedSampler-style, no padding)."""
+def shard(perm: np.ndarray, rank: int, world_size: int, mode: str = "pad") -> np.ndarray:
+    """DDP partition of an epoch permutation, rank r taking
+    every world_size-th entry from position r:
+
+    - ``"pad"`` (default, torch DistributedSampler semantics): the
+      permutation is extended by wrapping to a multiple of world_size first,
+      so every rank gets ceil(n / world) samples and the same number of
+      batches (no rank waits in a collective on an extra last batch); the
+      first few samples of the epoch are seen twice;
+    - ``"drop"``: truncated to a multiple of world_size (DistributedSampler
+      drop_last), every rank gets floor(n / world);
+    - ``"stride"``: plain perm[r::world], an exact partition whose shard
+      lengths differ by up to one.
+    With world_size == 1 all three are the whole permutation."""
     if world_size < 1 or not 0 <= rank < world_size:
         raise ValueError(f"bad rank/world_size {rank}/{world_size}")
+    n = len(perm)
+    if mode == "pad" and n % world_size:
+        total = -(-n // world_size) * world_size
+        perm = np.concatenate([perm, np.resize(perm, total - n)]) if n else perm
+    elif mode == "drop":
+        perm = perm[:n - n % world_size]
+    elif mode not in ("pad", "stride"):
+        raise ValueError(f"shard mode must be pad, drop or stride, got {mode!r}")
     return perm[rank::world_size]
+
+
+def shard_len(n: int, rank: int, world_size: int, mode: str = "pad") -> int:
+    """len(shard(perm of n, rank, world_size, mode)) without building it."""
+    if mode == "pad":
+        return -(-n // world_size)
+    if mode == "drop":
+        return n // world_size
+    return max(0, (n - rank + world_size - 1) // world_size)

@@ -57,11 +57,10 @@ def mode(request, E):
         eng.set_option(N.ESSL_OPT_WARMUP_BITS, m[2])
         eng.set_option(N.ESSL_OPT_STAGE_BYTES, m[3])
     yield request.param
-    eng.set_option(N.ESSL_OPT_DECODE_MODE, N.ESSL_DECODE_SPECULATIVE)
-    eng.set_option(N.ESSL_OPT_SEQ_BITS, 4096)
-    eng.set_option(N.ESSL_OPT_CHECKPOINT_BITS, 64)
-    eng.set_option(N.ESSL_OPT_WARMUP_BITS, 2048)
-    eng.set_option(N.ESSL_OPT_STAGE_BYTES, 65536)
+    # back to the library's own defaults (the default engine is shared)
+    for opt in (N.ESSL_OPT_DECODE_MODE, N.ESSL_OPT_SEQ_BITS, N.ESSL_OPT_CHECKPOINT_BITS,
+                N.ESSL_OPT_WARMUP_BITS, N.ESSL_OPT_STAGE_BYTES):
+        eng.set_option(opt, N.option_default(opt))
 
 
 @pytest.mark.parametrize("name", STREAMS)
@@ -336,7 +335,8 @@ def test_ddp_shards_cover_epoch(E, synth_sets):
     path = synth_sets[2]
     seen = {}
     for r in range(3):
-        cfg = E.LoaderConfig(data=str(path), batch_size=7, res=64, rank=r, world_size=3)
+        cfg = E.LoaderConfig(data=str(path), batch_size=7, res=64, rank=r, world_size=3,
+                             shard_mode="stride")
         with E.Loader(cfg) as loader:
             for b in loader.epoch(2):
                 for s in range(len(b)):

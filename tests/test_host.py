@@ -31,6 +31,10 @@ def test_native_exports_every_declared_symbol(native):
     for name in declared:
         assert getattr(L, name) is not None
     assert b"sm_100a" in L.essl_version()
+    # option defaults are readable without a device (the GPU tests restore them)
+    assert native.option_default(native.ESSL_OPT_SEQ_BITS) == 3072
+    assert native.option_default(native.ESSL_OPT_WARMUP_BITS) == 2048
+    assert native.option_default(native.ESSL_OPT_DECODE_MODE) == native.ESSL_DECODE_SPECULATIVE
 
 
 def test_rng_and_permutation(E, golden, arrays):
@@ -175,12 +179,26 @@ def test_loader_config_validation(E):
 
 
 def test_shard_partition(E):
+    from paper_2404_00509_b200.rng import shard_len
     perm = E.epoch_permutation(0, 3, 1003)
-    parts = [E.shard(perm, r, 4) for r in range(4)]
+    parts = [E.shard(perm, r, 4, "stride") for r in range(4)]
     assert sorted(np.concatenate(parts).tolist()) == list(range(1003))
     assert [len(p) for p in parts] == [251, 251, 251, 250]
+    # default "pad": equal shards (every rank the same batch count), the
+    # permutation wrapped around -- DistributedSampler semantics
+    padded = [E.shard(perm, r, 4) for r in range(4)]
+    assert [len(p) for p in padded] == [251] * 4
+    assert padded[3][:-1].tolist() == parts[3].tolist() and padded[3][-1] == perm[0]
+    assert set(np.concatenate(padded).tolist()) == set(range(1003))
+    dropped = [E.shard(perm, r, 4, "drop") for r in range(4)]
+    assert [len(p) for p in dropped] == [250] * 4
+    for mode, ps in (("stride", parts), ("pad", padded), ("drop", dropped)):
+        assert [shard_len(1003, r, 4, mode) for r in range(4)] == [len(p) for p in ps]
+    assert E.shard(perm, 0, 1).tolist() == perm.tolist()
     with pytest.raises(ValueError):
         E.shard(perm, 4, 4)
+    with pytest.raises(ValueError):
+        E.shard(perm, 0, 4, "bogus")
 
 
 # ---- 3-Aug draws and blur taps ---------------------------

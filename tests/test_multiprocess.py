@@ -31,7 +31,7 @@ def _worker(rank, ws, port, q):
     from paper_2404_00509_b200 import _native as N
     from paper_2404_00509_b200.ddp import rank_shard, reduce_timing
     n, seed, epoch = 1000, 7, 3
-    idx = rank_shard(seed, epoch, n, rank, ws)
+    idx = rank_shard(seed, epoch, n, rank, ws, "stride")
     gathered = [None] * ws
     dist.all_gather_object(gathered, idx.tolist())
     # host descriptors of this rank's shard (rects/flips keyed by index)
