@@ -276,14 +276,18 @@ def run_gpu(args, wl):
                          rank=rank, world_size=ws, resident=True, prefetch=args.streams,
                          streams=args.streams, reuse_outputs=True)
     loader = E.Loader(cfg)
-    if args.seq_bits > 0:
-        loader.set_option(N.ESSL_OPT_SEQ_BITS, args.seq_bits)
-    if args.warm_bits >= 0:
-        loader.set_option(N.ESSL_OPT_WARMUP_BITS, args.warm_bits)
-    if args.ck_bits > 0:
-        loader.set_option(N.ESSL_OPT_CHECKPOINT_BITS, args.ck_bits)
-    if args.stage_bytes >= 0:
-        loader.set_option(N.ESSL_OPT_STAGE_BYTES, args.stage_bytes)
+
+    def apply_options(ld):  # analysis knobs (library defaults unless given)
+        for opt, v, on in ((N.ESSL_OPT_SEQ_BITS, args.seq_bits, args.seq_bits > 0),
+                           (N.ESSL_OPT_WARMUP_BITS, args.warm_bits, args.warm_bits >= 0),
+                           (N.ESSL_OPT_CHECKPOINT_BITS, args.ck_bits, args.ck_bits > 0),
+                           (N.ESSL_OPT_STAGE_BYTES, args.stage_bytes, args.stage_bytes >= 0),
+                           (N.ESSL_OPT_RESIZE_COLS, args.resize_cols, args.resize_cols > 0),
+                           (N.ESSL_OPT_RESIZE_BAND, args.resize_band, args.resize_band > 0)):
+            if on:
+                ld.set_option(opt, v)
+
+    apply_options(loader)
     handle = loader.handle
     perm_epochs = {}
     if args.epoch:  # one full epoch of this rank's shard (whole batches)
@@ -379,6 +383,7 @@ def run_gpu(args, wl):
     if not args.no_e2e:
         cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False, "staging": args.staging})
         l2 = E.Loader(cfg2, container=handle, engine=loader.engine)
+        apply_options(l2)
         if args.gather_ctas >= 0:
             l2.set_option(N.ESSL_OPT_GATHER_CTAS, args.gather_ctas)
         if args.gather_tma >= 0:
@@ -508,6 +513,10 @@ def main():
     ap.add_argument("--warm-bits", type=int, default=-1, help="entropy-decode lane warm-up bits (-1: default)")
     ap.add_argument("--stage-bytes", type=int, default=-1,
                     help="ESSL_OPT_STAGE_BYTES (0: entropy lanes read the clean stream from global)")
+    ap.add_argument("--resize-cols", type=int, default=0,
+                    help="k_resize output columns per thread (ESSL_OPT_RESIZE_COLS; 0: default)")
+    ap.add_argument("--resize-band", type=int, default=0,
+                    help="k_resize output rows per CTA, at most (ESSL_OPT_RESIZE_BAND; 0: default)")
     ap.add_argument("--streams", type=int, default=8,
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--gather-ctas", type=int, default=-1,

@@ -71,6 +71,8 @@ extern "C" {
 #define ESSL_OPT_GATHER_TMA 8   /* 1 (default): bus-read gather with bulk (TMA) copies; 0: LSU loads */
 #define ESSL_OPT_DEBUG_LANES 9  /* 1: record per-lane speculative-decode state (essl_debug_lanes) */
 #define ESSL_OPT_TRACE 10       /* n > 0: record up to n CTA executions (essl_trace_read); 0 off */
+#define ESSL_OPT_RESIZE_COLS 11 /* k_resize output columns per thread: 2 (default), 4 or 8 */
+#define ESSL_OPT_RESIZE_BAND 12 /* k_resize output rows per CTA, at most (1..64, default 64) */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0

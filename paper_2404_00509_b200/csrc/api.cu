@@ -47,6 +47,8 @@ constexpr int kDefWarmBits = 2048;
 constexpr int kDefStageBytes = 64 * 1024;
 constexpr int kDefGatherCtas = 4;
 constexpr bool kDefGatherTma = true;
+constexpr int kDefResizeCols = 2;
+constexpr int kDefResizeBand = 64;
 
 // Persistent host workers for payload staging (one pool per context): a
 // batch's copies are split into contiguous ranges, the caller thread takes
@@ -154,6 +156,8 @@ struct essl_ctx {
   int stage_max = kDefStageBytes;
   int gather_ctas = kDefGatherCtas;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
   bool gather_tma = kDefGatherTma;   // ESSL_OPT_GATHER_TMA: bulk (TMA) bus reads, e2e +9% over LSU loads
+  int resize_cols = kDefResizeCols;  // ESSL_OPT_RESIZE_COLS
+  int resize_band = kDefResizeBand;  // ESSL_OPT_RESIZE_BAND
   int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
   essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
@@ -542,6 +546,14 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
     case ESSL_OPT_PROFILE:
       c->profile = value != 0;
       return ESSL_OK;
+    case ESSL_OPT_RESIZE_COLS:
+      if (value != 2 && value != 4 && value != 8) return fail(ESSL_E_ARG, "resize columns must be 2, 4 or 8");
+      c->resize_cols = (int)value;
+      return ESSL_OK;
+    case ESSL_OPT_RESIZE_BAND:
+      if (value < 1 || value > essl::kMaxBandRows) return fail(ESSL_E_ARG, "bad resize band");
+      c->resize_band = (int)value;
+      return ESSL_OK;
     case ESSL_OPT_CHECKPOINT_BITS:
       if (value < 1 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad checkpoint bits");
       c->ck_bits = (int)value;
@@ -563,6 +575,8 @@ int essl_option_default(int option, int64_t *value) {
     case ESSL_OPT_GATHER_TMA: *value = kDefGatherTma ? 1 : 0; return ESSL_OK;
     case ESSL_OPT_DEBUG_LANES: *value = 0; return ESSL_OK;
     case ESSL_OPT_TRACE: *value = 0; return ESSL_OK;
+    case ESSL_OPT_RESIZE_COLS: *value = kDefResizeCols; return ESSL_OK;
+    case ESSL_OPT_RESIZE_BAND: *value = kDefResizeBand; return ESSL_OK;
   }
   return fail(ESSL_E_ARG, "unknown option");
 }
@@ -833,14 +847,17 @@ int rrc_impl(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int s
       pp.src_words = (w + 3) / 4 * 4;
       return essl::resize_smem(pp);
     };
-    int band = essl::kMaxBandRows;
-    while (band > 8 && smem(band) > 96 * 1024) band /= 2;
-    if (smem(band) > 96 * 1024) {
-      band = essl::kMaxBandRows;
+    pp.cols = c->resize_cols;
+    // CTAs per SM by registers: 2 (8 columns) / 3 (4) / 4 (2)
+    const size_t budget = pp.cols == 8 ? 96 * 1024 : (pp.cols == 4 ? 64 * 1024 : 48 * 1024);
+    int band = pp.cols == 2 && !want_vis ? std::min(c->resize_band, 32) : c->resize_band;
+    while (band > 8 && smem(band) > budget) band /= 2;
+    if (smem(band) > budget) {
+      band = c->resize_band;
       while (band > 1 && smem(band) > 200 * 1024) band /= 2;
     }
     if (smem(band) > 200 * 1024) {
-      pp.band = essl::kMaxBandRows;
+      pp.band = c->resize_band;
       pp.src_words = 0;  // unstaged: k_resize reads the planes directly
       if (essl::resize_smem(pp) > 200 * 1024)
         return fail(ESSL_E_CAPACITY, "output resolution too large for the resize kernel");

@@ -140,6 +140,7 @@ struct PixelParams {
   void *vis;
   const int64_t *vis_restore;
   int patch, n_keep;
+  int cols;  // k_resize output columns per thread (8: 128-bit bf16 stores, 4: 64-bit)
   CtaTrace trace;
 };
 

@@ -132,7 +132,6 @@ __device__ __forceinline__ float norm_value(int c, int v) {
 // grid: (ceil(res / P.band), n); dynamic smem: P.src_words source words +
 // res column taps.
 constexpr int kResizeMaxDyn = 200 * 1024;
-constexpr int kCols = 8;
 
 // The exact fp32 normalize value of every (channel, uint8) and its bf16 RNE,
 // computed once per device (init_device_pixels) with the same IEEE ops.
@@ -262,6 +261,21 @@ __device__ __forceinline__ uint32_t plane_rgbx(const ImgInfo &I, const PlaneSrc 
 // PLAIN: no 3-Aug, no uint8 view, no visible tokens -- each channel's 8
 // values are finished (and stored) on their own, which keeps the register
 // footprint at the two rows of interpolated values.
+// W consecutive 32-bit words to global memory as one vector store
+// (W = 4: 128-bit, 2: 64-bit, 1: 32-bit); CS: streaming (evict-first).
+template <int W, bool CS = true>
+__device__ __forceinline__ void st_words(void *p, const uint32_t *w) {
+  if constexpr (W == 4) {
+    const uint4 v = make_uint4(w[0], w[1], w[2], w[3]);
+    if (CS) __stcs(reinterpret_cast<uint4 *>(p), v); else *reinterpret_cast<uint4 *>(p) = v;
+  } else if constexpr (W == 2) {
+    const uint2 v = make_uint2(w[0], w[1]);
+    if (CS) __stcs(reinterpret_cast<uint2 *>(p), v); else *reinterpret_cast<uint2 *>(p) = v;
+  } else {
+    if (CS) __stcs(reinterpret_cast<unsigned int *>(p), w[0]); else *reinterpret_cast<uint32_t *>(p) = w[0];
+  }
+}
+
 // The exact float64 value of channel c of output pixel (row pair yy, column
 // ox) -- the ambiguous case of the float32 evaluation (imgops.py:49-56).
 template <bool STAGED>
@@ -283,8 +297,8 @@ __device__ __noinline__ int exact_value(const ImgInfo &I, const PlaneSrc &S, con
                  (a01 >> (8 * c)) & 255, (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
 }
 
-template <bool AUG, bool STAGED, bool PLAIN>
-__global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
+template <bool AUG, bool STAGED, bool PLAIN, int COLS>
+__global__ void __launch_bounds__(kPixThreads, COLS == 8 ? 2 : (COLS == 4 ? 3 : 4)) k_resize(PixelParams P) {
   TraceScope trace_(P.trace, ESSL_K_RESIZE);
   extern __shared__ __align__(16) uint8_t dyn[];
   __shared__ float lut[3][256];
@@ -373,7 +387,7 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
   // pixel is recomputed with the reference's float64 expression (exact_px).
   //   x + 1 = bits(V + 1.5*2^23 + 1) - 0x4B400000  (round to nearest through
   //   the magic constant; V + 1.5*2^23 + 1 < 2^24 keeps unit spacing).
-  const int ngrp = (res + kCols - 1) / kCols;
+  const int ngrp = (res + COLS - 1) / COLS;
   const int band_rows = ob1 - ob0;
   // slices of rows: thread (group g, slice s) owns rows [r0, r1) of the band
   const int nsl = ngrp >= kPixThreads ? 1 : min(kPixThreads / ngrp, band_rows);
@@ -384,28 +398,37 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
   const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
   // 128-bit stores need every (image, plane, row, group) start 16-byte aligned
   const int esz = out_kind == ESSL_OUT_F32_NCHW ? 4 : 2;
-  const bool vec = (res % kCols) == 0 && ((stride * esz) & 15) == 0 &&
-                   ((reinterpret_cast<uintptr_t>(P.out) & 15) == 0);
-  const bool vec_u8 = (res % kCols) == 0 && ((reinterpret_cast<uintptr_t>(out_u8) & 7) == 0);
+  constexpr int va = COLS * 2 > 16 ? 16 : COLS * 2;  // bf16 store width
+  const int al = out_kind == ESSL_OUT_F32_NCHW ? (COLS == 2 ? 8 : 16) : va;
+  const bool vec = (res % COLS) == 0 && ((stride * esz) % al) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(P.out) % al) == 0);
+  const bool vec_u8 = COLS >= 4 && (res % COLS) == 0 &&
+                      ((reinterpret_cast<uintptr_t>(out_u8) % (COLS >= 4 ? COLS / 2 : 1)) == 0);
   const int patch = P.patch, gp = patch > 0 ? res / patch : 0;
   const int tok_dim = patch * patch * 3;
-  const bool vec_vis = patch % kCols == 0 && (reinterpret_cast<uintptr_t>(P.vis) & 15) == 0;
+  const bool vec_vis = patch % COLS == 0 && (reinterpret_cast<uintptr_t>(P.vis) % va) == 0;
   constexpr float kMagic1 = 12582913.0f;   // 1.5 * 2^23 + 1
   constexpr int kMagicBits = 0x4B400000;   // bits of 1.5 * 2^23
   constexpr float kByteBias = 8388608.0f;  // bits 0x4B000000 | byte == 2^23 + byte
   for (int grp = ngrp >= kPixThreads ? threadIdx.x : threadIdx.x - sl * ngrp; grp < ngrp;
        grp += ngrp >= kPixThreads ? kPixThreads : ngrp) {
-    const int oxa = grp * kCols;
-    const int ncol = min(kCols, res - oxa);
-    // (the group's column taps are re-read from shared memory per source
-    // row: registers go to the 2 x 24 interpolated values)
+    const int oxa = grp * COLS;
+    const int ncol = min(COLS, res - oxa);
+    // narrow groups keep their column taps in registers; 8-column groups
+    // re-read them from shared memory per source row (registers go to the
+    // 2 x 24 interpolated values)
     const ColTap *ct = ctab + oxa;
-    int cy0 = -1, cy1 = -1;
-    float h0[kCols][3], h1[kCols][3];
-    auto hrow = [&](int y, float h[kCols][3]) {
+    ColTap treg[COLS <= 4 ? COLS : 1];
+    if constexpr (COLS <= 4) {
 #pragma unroll
-      for (int j = 0; j < kCols; j++) {
-        const ColTap t = ct[min(j, ncol - 1)];
+      for (int j = 0; j < COLS; j++) treg[j] = ct[min(j, ncol - 1)];
+    }
+    int cy0 = -1, cy1 = -1;
+    float h0[COLS][3], h1[COLS][3];
+    auto hrow = [&](int y, float h[COLS][3]) {
+#pragma unroll
+      for (int j = 0; j < COLS; j++) {
+        const ColTap t = COLS <= 4 ? treg[COLS <= 4 ? j : 0] : ct[min(j, ncol - 1)];
         const float wxkj = t.wxk;
         uint32_t a0, a1;
         if (STAGED) {
@@ -432,7 +455,7 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
       if (yy.x != cy0) {
         if (yy.x == cy1) {
 #pragma unroll
-          for (int j = 0; j < kCols; j++)
+          for (int j = 0; j < COLS; j++)
 #pragma unroll
             for (int c = 0; c < 3; c++) h0[j][c] = h1[j][c];
         } else {
@@ -443,7 +466,7 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
       if (yy.y != cy1) {
         if (yy.y == cy0) {
 #pragma unroll
-          for (int j = 0; j < kCols; j++)
+          for (int j = 0; j < COLS; j++)
 #pragma unroll
             for (int c = 0; c < 3; c++) h1[j][c] = h0[j][c];
         } else {
@@ -453,14 +476,14 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
       }
       const int oy = ob0 + r;
       const int64_t o = img * stride + (int64_t)oy * res + oxa;
-      const bool full = ncol == kCols;
+      const bool full = ncol == COLS;
       if (PLAIN) {
 #pragma unroll
         for (int c = 0; c < 3; c++) {
-          int pc[kCols];
+          int pc[COLS];
           int amb = 4095;
 #pragma unroll
-          for (int j = 0; j < kCols; j++) {
+          for (int j = 0; j < COLS; j++) {
             const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
             const int y1 = __float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits;  // round(v) + 1
             amb = min(amb, y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
@@ -468,7 +491,7 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
           }
           if (amb == 0) {  // rare: the exact float64 expression for the ambiguous values
 #pragma unroll
-            for (int j = 0; j < kCols; j++) {
+            for (int j = 0; j < COLS; j++) {
               const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
               if (((__float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits) & 4094) == 0)
                 pc[j] = exact_value<STAGED>(I, S, src, iw, ys0, yy, oxa + min(j, ncol - 1), res, sx, rw[r], c);
@@ -477,39 +500,44 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
           if (out_kind == ESSL_OUT_BF16_NCHW) {
             __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o + c * plane_sz;
             if (vec) {
-              uint32_t w[4];
+              uint32_t w[COLS / 2];
 #pragma unroll
-              for (int q = 0; q < 4; q++)
+              for (int q = 0; q < COLS / 2; q++)
                 w[q] = (uint32_t)__bfloat16_as_ushort(lutb[c][pc[2 * q]]) |
                        ((uint32_t)__bfloat16_as_ushort(lutb[c][pc[2 * q + 1]]) << 16);
               // streaming store: the model's input is not re-read here; keep L2
               // for the unit lists / planes of the batches in flight
-              __stcs(reinterpret_cast<uint4 *>(out), make_uint4(w[0], w[1], w[2], w[3]));
+              st_words<COLS / 2>(out, w);
             } else {
 #pragma unroll
-              for (int j = 0; j < kCols; j++)
+              for (int j = 0; j < COLS; j++)
                 if (j < ncol) out[j] = lutb[c][pc[j]];
             }
           } else if (out_kind == ESSL_OUT_F32_NCHW) {
             float *out = reinterpret_cast<float *>(P.out) + o + c * plane_sz;
             if (vec) {
-              __stcs(reinterpret_cast<float4 *>(out),
-                     make_float4(lut[c][pc[0]], lut[c][pc[1]], lut[c][pc[2]], lut[c][pc[3]]));
-              __stcs(reinterpret_cast<float4 *>(out + 4),
-                     make_float4(lut[c][pc[4]], lut[c][pc[5]], lut[c][pc[6]], lut[c][pc[7]]));
+              if constexpr (COLS == 2) {
+                __stcs(reinterpret_cast<float2 *>(out), make_float2(lut[c][pc[0]], lut[c][pc[1]]));
+              } else {
+#pragma unroll
+                for (int q = 0; q < COLS / 4; q++)
+                  __stcs(reinterpret_cast<float4 *>(out) + q,
+                         make_float4(lut[c][pc[4 * q]], lut[c][pc[4 * q + 1]], lut[c][pc[4 * q + 2]],
+                                     lut[c][pc[4 * q + 3]]));
+              }
             } else {
 #pragma unroll
-              for (int j = 0; j < kCols; j++)
+              for (int j = 0; j < COLS; j++)
                 if (j < ncol) out[j] = lut[c][pc[j]];
             }
           }
         }
         continue;
       }
-      int px[kCols][3];
+      int px[COLS][3];
       int amb = 4095;
 #pragma unroll
-      for (int j = 0; j < kCols; j++)
+      for (int j = 0; j < COLS; j++)
 #pragma unroll
         for (int c = 0; c < 3; c++) {
           const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
@@ -519,7 +547,7 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
         }
       if (amb == 0) {  // rare: the exact float64 expression for the ambiguous pixels
 #pragma unroll
-        for (int j = 0; j < kCols; j++) {
+        for (int j = 0; j < COLS; j++) {
           bool a = false;
 #pragma unroll
           for (int c = 0; c < 3; c++) {
@@ -536,10 +564,10 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
       }
       if (AUG && aop == ESSL_AUG_OP_GRAY) {  // imgops.py:75-91
 #pragma unroll
-        for (int j = 0; j < kCols; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
+        for (int j = 0; j < COLS; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
       } else if (AUG && aop == ESSL_AUG_OP_SOLARIZE) {  // imgops.py:94-108
 #pragma unroll
-        for (int j = 0; j < kCols; j++)
+        for (int j = 0; j < COLS; j++)
 #pragma unroll
           for (int c = 0; c < 3; c++) px[j][c] = px[j][c] >= athr ? 255 - px[j][c] : px[j][c];
       }
@@ -548,20 +576,18 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
         if (vec) {
 #pragma unroll
           for (int c = 0; c < 3; c++) {
-            uint32_t w[4];
+            uint32_t w[COLS / 2];
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+            for (int q = 0; q < COLS / 2; q++)
               w[q] = (uint32_t)__bfloat16_as_ushort(lutb[c][px[2 * q][c]]) |
                      ((uint32_t)__bfloat16_as_ushort(lutb[c][px[2 * q + 1][c]]) << 16);
-            // streaming store: the model's input is not re-read here; keep L2
-            // for the unit lists / planes of the batches in flight
-            __stcs(reinterpret_cast<uint4 *>(out + c * plane_sz), make_uint4(w[0], w[1], w[2], w[3]));
+            st_words<COLS / 2>(out + c * plane_sz, w);
           }
         } else {
 #pragma unroll
           for (int c = 0; c < 3; c++)
 #pragma unroll
-            for (int j = 0; j < kCols; j++)
+            for (int j = 0; j < COLS; j++)
               if (j < ncol) out[c * plane_sz + j] = lutb[c][px[j][c]];
         }
       } else if (out_kind == ESSL_OUT_F32_NCHW) {
@@ -569,36 +595,43 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
         if (vec) {
 #pragma unroll
           for (int c = 0; c < 3; c++) {
-            __stcs(reinterpret_cast<float4 *>(out + c * plane_sz),
-                   make_float4(lut[c][px[0][c]], lut[c][px[1][c]], lut[c][px[2][c]], lut[c][px[3][c]]));
-            __stcs(reinterpret_cast<float4 *>(out + c * plane_sz + 4),
-                   make_float4(lut[c][px[4][c]], lut[c][px[5][c]], lut[c][px[6][c]], lut[c][px[7][c]]));
+            if constexpr (COLS == 2) {
+              __stcs(reinterpret_cast<float2 *>(out + c * plane_sz),
+                     make_float2(lut[c][px[0][c]], lut[c][px[1][c]]));
+            } else {
+#pragma unroll
+              for (int q = 0; q < COLS / 4; q++)
+                __stcs(reinterpret_cast<float4 *>(out + c * plane_sz) + q,
+                       make_float4(lut[c][px[4 * q][c]], lut[c][px[4 * q + 1][c]],
+                                   lut[c][px[4 * q + 2][c]], lut[c][px[4 * q + 3][c]]));
+            }
           }
         } else {
 #pragma unroll
           for (int c = 0; c < 3; c++)
 #pragma unroll
-            for (int j = 0; j < kCols; j++)
+            for (int j = 0; j < COLS; j++)
               if (j < ncol) out[c * plane_sz + j] = lut[c][px[j][c]];
         }
       }
       if (out_u8) {
         uint8_t *out = out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
         if (vec_u8 && full) {
-          uint32_t w[6];
+          constexpr int nw = COLS >= 4 ? 3 * COLS / 4 : 1;
+          uint32_t w[nw];
 #pragma unroll
-          for (int q = 0; q < 6; q++) {
+          for (int q = 0; q < (COLS >= 4 ? nw : 0); q++) {
             uint32_t v = 0;
 #pragma unroll
             for (int b = 0; b < 4; b++) v |= (uint32_t)px[(4 * q + b) / 3][(4 * q + b) % 3] << (8 * b);
             w[q] = v;
           }
 #pragma unroll
-          for (int q = 0; q < 3; q++)
-            *reinterpret_cast<uint2 *>(out + 8 * q) = make_uint2(w[2 * q], w[2 * q + 1]);
+          for (int q = 0; q < (COLS >= 4 ? 3 : 0); q++)
+            st_words<COLS >= 4 ? COLS / 4 : 1, false>(out + COLS * q, w + (COLS / 4) * q);
         } else {
 #pragma unroll
-          for (int j = 0; j < kCols; j++)
+          for (int j = 0; j < COLS; j++)
             if (j < ncol)
 #pragma unroll
               for (int c = 0; c < 3; c++) out[3 * j + c] = (uint8_t)px[j][c];
@@ -616,21 +649,19 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
           if (rk < P.n_keep) {
             __nv_bfloat16 *t = tok + ((int64_t)img * P.n_keep + rk) * tok_dim +
                                ((oy % patch) * patch + oxa % patch) * 3;
-            uint32_t w[12];
+            uint32_t w[3 * COLS / 2];
 #pragma unroll
-            for (int q = 0; q < 12; q++) {
+            for (int q = 0; q < 3 * COLS / 2; q++) {
               const int e0 = 2 * q, e1 = 2 * q + 1;
               w[q] = (uint32_t)__bfloat16_as_ushort(lutb[e0 % 3][px[e0 / 3][e0 % 3]]) |
                      ((uint32_t)__bfloat16_as_ushort(lutb[e1 % 3][px[e1 / 3][e1 % 3]]) << 16);
             }
 #pragma unroll
-            for (int q = 0; q < 3; q++)
-              __stcs(reinterpret_cast<uint4 *>(t) + q,
-                     make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+            for (int q = 0; q < 3; q++) st_words<COLS / 2>(t + COLS * q, w + (COLS / 2) * q);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < kCols; j++) {
+          for (int j = 0; j < COLS; j++) {
             if (j >= ncol) continue;
             const int ox = oxa + j;
             const int64_t rk = rest[(oy / patch) * gp + ox / patch];
@@ -646,6 +677,337 @@ __global__ void __launch_bounds__(kPixThreads, 2) k_resize(PixelParams P) {
   }
 }
 
+constexpr int kPairBandRows = 32;
+
+// k_resize_pairs: the round-1 shape, and the fastest measured in the
+// multi-stream pipeline (A/B on B200, cfg2: 975k img/s vs 937k for the
+// template kernel at 2 columns and 925k at 4 / 852k at 8 columns with
+// 128-bit stores): a thread owns a PAIR of output columns (paired 32-bit bf16
+// / 64-bit f32 stores) of half a 32-row band, its two column taps in
+// registers.  Used for staged batches without visible tokens; everything
+// else takes k_resize.
+template <bool AUG>
+__global__ void __launch_bounds__(kPixThreads, 4) k_resize_pairs(PixelParams P) {
+  TraceScope trace_(P.trace, ESSL_K_RESIZE);
+  extern __shared__ __align__(16) uint8_t dyn[];
+  __shared__ float lut[3][256];
+  __shared__ __nv_bfloat16 lutb[3][256];
+  __shared__ double s_scale[2];
+  const int img = blockIdx.y;
+  const ImgInfo &I = P.info[img];
+  if (I.status != 0) return;
+  const int res = P.res;
+  // 3-Aug (pipeline.py:88-101): point ops are finished here, blur / jitter
+  // images leave their uint8 resize to k_aug_blur / k_aug_out
+  int out_kind = P.out_kind, aop = ESSL_AUG_OP_NONE, athr = 0;
+  uint8_t *out_u8 = P.out_u8;
+  if (AUG) {
+    const essl_aug &A = P.aug[img];
+    if (A.op == ESSL_AUG_OP_BLUR || A.jitter) {
+      out_kind = ESSL_OUT_NONE;
+      out_u8 = P.aug_u8;
+    } else {
+      aop = A.op;
+      athr = A.threshold;
+    }
+  }
+  const int ih = I.rh, iw = I.rw;
+  if (P.out_kind == ESSL_OUT_F32_NCHW)
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lut[i >> 8][i & 255] = g_norm_lut[i];
+  else
+    for (int i = threadIdx.x; i < 768; i += kPixThreads) lutb[i >> 8][i & 255] = g_norm_lutb[i];
+  if (threadIdx.x == 0) {  // imgops.py:35-36 scale factors, once per CTA
+    s_scale[0] = __ddiv_rn((double)ih, (double)res);
+    s_scale[1] = __ddiv_rn((double)iw, (double)res);
+  }
+  __syncthreads();
+  const int ob0 = blockIdx.x * P.band;
+  const int ob1 = min(ob0 + P.band, res);
+  const double sy = s_scale[0], sx = s_scale[1];
+  // source rows of the band (taps are monotone in the output row)
+  int ys0, ys1, dummy;
+  double wdum;
+  tap(ob0, sy, ih, ys0, dummy, wdum);
+  tap(ob1 - 1, sy, ih, dummy, ys1, wdum);
+  const int nrows = ys1 - ys0 + 1;
+  uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
+  PlaneSrc S;
+  S.load(I, P.plane);
+  // source rows -> RGBX words in shared memory.
+  // Fast path (luma at full horizontal resolution, chroma at full or half:
+  // 4:2:0, 4:2:2, 4:4:4, gray): work items are (row, group of 4 image
+  // columns aligned to 4), so the luma plane is read 4 bytes at a time and
+  // half-resolution chroma 2 bytes at a time (planes are MCU-aligned windows:
+  // a group never leaves them), and each chroma sample's colour terms are
+  // computed once for the two pixels that replicate it (decode_kernels.py:
+  // 551-576: R = Y + (91881 Cr + 32768) >> 16, G = Y + (-22554 Cb - 46802 Cr
+  // + 32768) >> 16, B = Y + (116130 Cb + 32768) >> 16, clamped).
+  const bool fast = I.comp_h[0] == I.hmax &&
+                    (I.ncomp == 1 || ((2 * I.comp_h[1] == I.hmax || I.comp_h[1] == I.hmax) &&
+                                      (2 * I.comp_h[2] == I.hmax || I.comp_h[2] == I.hmax)));
+  if (fast) {
+    const int g0 = I.rx >> 2, ng = ((I.rx + iw + 3) >> 2) - g0;
+    const bool half1 = I.ncomp == 3 && 2 * I.comp_h[1] == I.hmax;
+    const bool half2 = I.ncomp == 3 && 2 * I.comp_h[2] == I.hmax;
+    for (int it = threadIdx.x; it < nrows * ng; it += kPixThreads) {
+      const int r = it / ng, G = g0 + (it - r * ng);
+      int ro[3];
+      S.row_off(I.ry + ys0 + r, ro);
+      const uint32_t y4 = *reinterpret_cast<const uint32_t *>(S.p[0] + ro[0] + 4 * G - S.ox[0]);
+      uint32_t w[4];
+      if (I.ncomp == 1) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) w[i] = ((y4 >> (8 * i)) & 255u) * 0x010101u;
+      } else {
+        // chroma bytes of the group's 4 pixels (replicated when half resolution)
+        uint32_t cb4, cr4;
+        if (half1) {
+          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[1] + ro[1] + 2 * G - S.ox[1]);
+          cb4 = __byte_perm(t, 0, 0x1100);
+        } else {
+          cb4 = *reinterpret_cast<const uint32_t *>(S.p[1] + ro[1] + 4 * G - S.ox[1]);
+        }
+        if (half2) {
+          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[2] + ro[2] + 2 * G - S.ox[2]);
+          cr4 = __byte_perm(t, 0, 0x1100);
+        } else {
+          cr4 = *reinterpret_cast<const uint32_t *>(S.p[2] + ro[2] + 4 * G - S.ox[2]);
+        }
+        // colour terms per distinct chroma pair (pixels 2k, 2k+1 share one
+        // when both chroma planes are half resolution)
+        int dr[4], dg[4], db[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          if (i & 1 && half1 && half2) {
+            dr[i] = dr[i - 1]; dg[i] = dg[i - 1]; db[i] = db[i - 1];
+            continue;
+          }
+          const int cb = (int)((cb4 >> (8 * i)) & 255u) - 128;
+          const int cr = (int)((cr4 >> (8 * i)) & 255u) - 128;
+          dr[i] = (91881 * cr + 32768) >> 16;
+          dg[i] = (-22554 * cb - 46802 * cr + 32768) >> 16;
+          db[i] = (116130 * cb + 32768) >> 16;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int yv = (int)((y4 >> (8 * i)) & 255u);
+          w[i] = (uint32_t)clamp255(yv + dr[i]) | ((uint32_t)clamp255(yv + dg[i]) << 8) |
+                 ((uint32_t)clamp255(yv + db[i]) << 16);
+        }
+      }
+      const int x = 4 * G - I.rx;
+      uint32_t *row = src + r * iw;
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if ((unsigned)(x + i) < (unsigned)iw) row[x + i] = w[i];
+    }
+  } else {
+    // generic sampling factors: each thread keeps one column (its plane
+    // column offsets fixed) and walks rows, four in flight; no per-pixel
+    // division.
+    {
+      const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
+      const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
+      const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
+      if (r0 < rpp) {
+        for (int x = x0; x < iw; x += cpr) {
+          int co[3];
+          S.col_off(I.rx + x, co);
+          for (int r = r0; r < nrows; r += 4 * rpp) {
+            int rr[4], gg[4], bb[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              int ro[3];
+              S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
+              S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+              if (r + u * rpp < nrows)
+                src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
+          }
+        }
+      }
+    }
+  }
+  // row taps of the band (imgops.py:37-41), shared by every column
+  __shared__ int2 ry[kPairBandRows];
+  __shared__ double rw[kPairBandRows];
+  __shared__ float rwf[kPairBandRows];
+  if (threadIdx.x < ob1 - ob0) {
+    int y0, y1;
+    double wy;
+    tap(ob0 + threadIdx.x, sy, ih, y0, y1, wy);
+    ry[threadIdx.x] = make_int2(y0 - ys0, y1 - ys0);
+    rw[threadIdx.x] = wy;
+    rwf[threadIdx.x] = __double2float_rn(wy);
+  }
+  __syncthreads();
+  // Separable evaluation.  The reference value is float64 (imgops.py:49-56):
+  //   v = (1-wy)*((1-wx)*s00 + wx*s01) + wy*((1-wx)*s10 + wx*s11) + 0.5,
+  //   px = int(v) (v <= 255.5, so the min(., 255) never binds).
+  // It is evaluated here in float32, scaled by 4096 (exact for integer
+  // samples): T = 4096*s0 + 2048 + (4096*wx)*(s1 - s0) per source row (one
+  // fma, kept in registers while consecutive output rows share the row),
+  // V = T0 + wy*(T1 - T0).  Float32 error, in those units: wx, wy rounded to
+  // float32 (<= 2^-24 * 255 * 4096 = 0.0625 each), four roundings at
+  // magnitude < 2^20 (<= 0.03125 each): |V - 4096*v| < 0.25.  With
+  // x = round(V), |x - 4096*v| < 0.75, so x mod 4096 in [1, 4094] proves
+  // int(v) == x >> 12.  Otherwise (x within one unit of a multiple of 4096:
+  // ~0.05% of channels, more with dyadic weights giving integral values) the
+  // pixel is recomputed with the reference's float64 expression (bilerp2).
+  //   x + 1 = bits(V + 1.5*2^23 + 1) - 0x4B400000  (round to nearest through
+  //   the magic constant; V + 1.5*2^23 + 1 < 2^24 keeps unit spacing).
+  // A thread owns a pair of adjacent output columns (paired bf16 / f32
+  // stores); small outputs split the band's rows over groups of threads.
+  const int npair = (res + 1) >> 1;
+  const int ng = npair >= kPixThreads ? 1 : kPixThreads / npair;
+  const int g = ng > 1 ? threadIdx.x / npair : 0;
+  const int cstart = ng > 1 ? threadIdx.x % npair : threadIdx.x;
+  const int cstep = ng > 1 ? npair : kPixThreads;
+  const int rpg = (ob1 - ob0 + ng - 1) / ng;
+  const int rb = g * rpg, re = min(ob1 - ob0, rb + rpg);
+  const int64_t plane_sz = (int64_t)res * res;
+  const int64_t stride = P.out_stride ? P.out_stride : 3 * plane_sz;
+  // paired stores need an even element offset for every (image, plane, row)
+  const bool pair_ok = (res & 1) == 0 && (stride & 1) == 0 &&
+                       ((reinterpret_cast<uintptr_t>(P.out) & 7) == 0);
+  if (g >= ng) return;
+  constexpr float kMagic1 = 12582913.0f;   // 1.5 * 2^23 + 1
+  constexpr int kMagicBits = 0x4B400000;   // bits of 1.5 * 2^23
+  constexpr float kByteBias = 8388608.0f;  // bits 0x4B000000 | byte == 2^23 + byte
+  for (int q = cstart; q < npair; q += cstep) {
+    const int oxa = 2 * q;
+    const bool two = oxa + 1 < res;
+    int x0[2], x1[2];
+    double wx[2];
+    float wxk[2];
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+      const int ox = min(oxa + j, res - 1);
+      tap(I.flip ? res - 1 - ox : ox, sx, iw, x0[j], x1[j], wx[j]);  // hflip after resize
+      wxk[j] = __fmul_rn(__double2float_rn(wx[j]), 4096.0f);
+    }
+    int cy0 = -1, cy1 = -1;
+    float h0[2][3], h1[2][3];
+    auto hrow = [&](int y, float h[2][3]) {
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const uint32_t a0 = src[y * iw + x0[j]], a1 = src[y * iw + x1[j]];
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          // 2^23 + byte, exactly (byte c of the RGBX word under exponent 0x4B)
+          const float f0 = __uint_as_float(__byte_perm(a0, 0x4B000000u, c | 0x7540));
+          const float f1 = __uint_as_float(__byte_perm(a1, 0x4B000000u, c | 0x7540));
+          // 4096*s0 + 2048 (exact) + (4096*wx) * (s1 - s0), one rounding
+          const float base = __fmaf_rn(f0, 4096.0f, 2048.0f - 4096.0f * kByteBias);
+          h[j][c] = __fmaf_rn(wxk[j], __fsub_rn(f1, f0), base);
+        }
+      }
+    };
+    for (int r = rb; r < re; r++) {
+      const int2 yy = ry[r];
+      const float wy = rwf[r];
+      if (yy.x != cy0) {  // (uniform across the CTA's columns: no divergence)
+        if (yy.x == cy1) {
+#pragma unroll
+          for (int j = 0; j < 2; j++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) h0[j][c] = h1[j][c];
+        } else {
+          hrow(yy.x, h0);
+        }
+        cy0 = yy.x;
+      }
+      if (yy.y != cy1) {
+        if (yy.y == cy0) {
+#pragma unroll
+          for (int j = 0; j < 2; j++)
+#pragma unroll
+            for (int c = 0; c < 3; c++) h1[j][c] = h0[j][c];
+        } else {
+          hrow(yy.y, h1);
+        }
+        cy1 = yy.y;
+      }
+      int px[2][3];
+      int amb[2] = {4095, 4095};
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) {
+          const float v = __fmaf_rn(wy, __fsub_rn(h1[j][c], h0[j][c]), h0[j][c]);
+          const int y1 = __float_as_int(__fadd_rn(v, kMagic1)) - kMagicBits;  // round(v) + 1
+          amb[j] = min(amb[j], y1 & 4094);  // 0: round(v) mod 4096 in {4095, 0}
+          px[j][c] = y1 >> 12;              // == round(v) >> 12 when not ambiguous
+        }
+#pragma unroll
+      for (int j = 0; j < 2; j++)
+        if (amb[j] == 0) {  // rare: the exact float64 expression (imgops.py:49-56)
+          const double wyd = rw[r];
+          const uint32_t a00 = src[yy.x * iw + x0[j]], a01 = src[yy.x * iw + x1[j]];
+          const uint32_t a10 = src[yy.y * iw + x0[j]], a11 = src[yy.y * iw + x1[j]];
+#pragma unroll
+          for (int c = 0; c < 3; c++)
+            px[j][c] = bilerp2(wx[j], wyd, __dsub_rn(1.0, wx[j]), __dsub_rn(1.0, wyd),
+                               (a00 >> (8 * c)) & 255, (a01 >> (8 * c)) & 255,
+                               (a10 >> (8 * c)) & 255, (a11 >> (8 * c)) & 255);
+        }
+      if (AUG && aop == ESSL_AUG_OP_GRAY) {  // imgops.py:75-91
+#pragma unroll
+        for (int j = 0; j < 2; j++) px[j][0] = px[j][1] = px[j][2] = luma601(px[j][0], px[j][1], px[j][2]);
+      } else if (AUG && aop == ESSL_AUG_OP_SOLARIZE) {  // imgops.py:94-108
+#pragma unroll
+        for (int j = 0; j < 2; j++)
+#pragma unroll
+          for (int c = 0; c < 3; c++) px[j][c] = px[j][c] >= athr ? 255 - px[j][c] : px[j][c];
+      }
+      const int oy = ob0 + r;
+      const int64_t o = img * stride + (int64_t)oy * res + oxa;
+      if (out_kind == ESSL_OUT_BF16_NCHW) {
+        __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
+        if (pair_ok) {
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            const uint32_t lo = __bfloat16_as_ushort(lutb[c][px[0][c]]);
+            const uint32_t hi = __bfloat16_as_ushort(lutb[c][px[1][c]]);
+            // streaming store: the model's input is not re-read here; keep L2
+            // for the unit lists / planes of the batches in flight
+            __stcs(reinterpret_cast<unsigned int *>(out + c * plane_sz), lo | (hi << 16));
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            out[c * plane_sz] = lutb[c][px[0][c]];
+            if (two) out[c * plane_sz + 1] = lutb[c][px[1][c]];
+          }
+        }
+      } else if (out_kind == ESSL_OUT_F32_NCHW) {
+        float *out = reinterpret_cast<float *>(P.out) + o;
+        if (pair_ok) {
+#pragma unroll
+          for (int c = 0; c < 3; c++)
+            __stcs(reinterpret_cast<float2 *>(out + c * plane_sz), make_float2(lut[c][px[0][c]], lut[c][px[1][c]]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            out[c * plane_sz] = lut[c][px[0][c]];
+            if (two) out[c * plane_sz + 1] = lut[c][px[1][c]];
+          }
+        }
+      }
+      if (out_u8) {
+        uint8_t *out = out_u8 + (int64_t)img * plane_sz * 3 + ((int64_t)oy * res + oxa) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; c++) out[c] = (uint8_t)px[0][c];
+        if (two)
+#pragma unroll
+          for (int c = 0; c < 3; c++) out[3 + c] = (uint8_t)px[1][c];
+      }
+    }
+  }
+}
+
 // Source rows a band of `band` output rows can touch for a crop of height
 // h resized to res (taps y0..y1 of rows ob0..ob0+band-1, imgops.py:33-41).
 int band_source_rows(int h, int res, int band) {
@@ -656,22 +1018,43 @@ size_t resize_smem(const PixelParams &p) {
   return (size_t)p.src_words * 4 + (size_t)p.res * sizeof(ColTap);
 }
 
+template <int COLS>
+void launch_resize_cols(const PixelParams &p, dim3 grid, size_t dyn, bool staged, bool plain,
+                        cudaStream_t st) {
+  if (p.aug) {
+    if (staged) k_resize<true, true, false, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<true, false, false, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+  } else if (plain) {
+    if (staged) k_resize<false, true, true, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<false, false, true, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+  } else {
+    if (staged) k_resize<false, true, false, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+    else k_resize<false, false, false, COLS><<<grid, kPixThreads, dyn, st>>>(p);
+  }
+}
+
+template <int COLS>
+void resize_attrs() {
+  for (auto f : {k_resize<false, true, true, COLS>, k_resize<false, false, true, COLS>,
+                 k_resize<false, true, false, COLS>, k_resize<false, false, false, COLS>,
+                 k_resize<true, true, false, COLS>, k_resize<true, false, false, COLS>})
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+}
+
 void launch_resize(const PixelParams &p, cudaStream_t st) {
   if (p.n <= 0) return;
   const size_t dyn = resize_smem(p);
   dim3 grid((p.res + p.band - 1) / p.band, p.n);
   const bool staged = p.src_words > 0;
   const bool plain = !p.aug && !p.out_u8 && !p.vis;
-  if (p.aug) {
-    if (staged) k_resize<true, true, false><<<grid, kPixThreads, dyn, st>>>(p);
-    else k_resize<true, false, false><<<grid, kPixThreads, dyn, st>>>(p);
-  } else if (plain) {
-    if (staged) k_resize<false, true, true><<<grid, kPixThreads, dyn, st>>>(p);
-    else k_resize<false, false, true><<<grid, kPixThreads, dyn, st>>>(p);
-  } else {
-    if (staged) k_resize<false, true, false><<<grid, kPixThreads, dyn, st>>>(p);
-    else k_resize<false, false, false><<<grid, kPixThreads, dyn, st>>>(p);
+  if (p.cols == 2 && staged && !p.vis && p.band <= kPairBandRows) {
+    if (p.aug) k_resize_pairs<true><<<grid, kPixThreads, (size_t)p.src_words * 4, st>>>(p);
+    else k_resize_pairs<false><<<grid, kPixThreads, (size_t)p.src_words * 4, st>>>(p);
+    return;
   }
+  if (p.cols == 2) launch_resize_cols<2>(p, grid, dyn, staged, plain, st);
+  else if (p.cols == 4) launch_resize_cols<4>(p, grid, dyn, staged, plain, st);
+  else launch_resize_cols<8>(p, grid, dyn, staged, plain, st);
 }
 
 // decode_crop output: uint8 [h, w, 3] at out + offsets[img].
@@ -1260,9 +1643,11 @@ void launch_host_gather(const uint8_t *src, const GatherDesc *d, int n, uint8_t 
 // (__device__ arrays exist per device) and the dynamic shared-memory opt-ins.
 void init_device_pixels() {
   k_init_norm_luts<<<1, 768>>>();
-  for (auto f : {k_resize<false, true, true>, k_resize<false, false, true>, k_resize<false, true, false>,
-                 k_resize<false, false, false>, k_resize<true, true, false>, k_resize<true, false, false>})
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+  resize_attrs<2>();
+  resize_attrs<4>();
+  cudaFuncSetAttribute(k_resize_pairs<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+  cudaFuncSetAttribute(k_resize_pairs<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kResizeMaxDyn);
+  resize_attrs<8>();
   cudaFuncSetAttribute(k_aug_blur, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)aug_blur_smem(ESSL_AUG_MAX_RADIUS));
   cudaFuncSetAttribute(k_host_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,

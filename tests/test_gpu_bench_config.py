@@ -172,3 +172,35 @@ def test_unstaged_resize_for_huge_crops(E, oracle, tmp_path):
                 assert (st == 0).all()
                 assert np.array_equal(b.pixels.cpu().numpy(), pix)
                 assert np.array_equal(b.uint8.cpu().numpy(), u8)
+
+
+@pytest.mark.parametrize("cols,band", [(8, 64), (4, 64), (2, 32), (8, 5), (4, 16), (2, 3), (8, 1)])
+@pytest.mark.parametrize("res", [224, 97])
+def test_resize_shapes_vs_oracle(E, oracle, tmp_path_factory, cols, band, res):
+    """k_resize thread shapes (ESSL_OPT_RESIZE_COLS / _BAND: columns per
+    thread, output rows per CTA; odd resolutions take the scalar stores)
+    are all bit-exact in float32 and uint8."""
+    from paper_2404_00509_b200 import _native as N
+    path = tmp_path_factory.mktemp("rs") / "mixed.essl"
+    E.build_synthetic(path, 48, (40, 300), 85, seed=11)
+    with E.open_container(path) as h:
+        cfg = E.LoaderConfig(data=str(path), batch_size=24, res=res, keep_uint8=True,
+                             streams=1, prefetch=1)
+        loader = E.Loader(cfg, container=h)
+        loader.set_option(N.ESSL_OPT_RESIZE_COLS, cols)
+        loader.set_option(N.ESSL_OPT_RESIZE_BAND, band)
+        for b in loader.epoch(1):
+            idx = b.indices.cpu().numpy()
+            pix, u8, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 1, res, keep_uint8=True)
+            assert (st == 0).all()
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
+            assert np.array_equal(b.uint8.cpu().numpy(), u8)
+        # the plain path (no uint8 view) too
+        cfg2 = E.LoaderConfig(data=str(path), batch_size=24, res=res, streams=1, prefetch=1)
+        loader2 = E.Loader(cfg2, container=h)
+        loader2.set_option(N.ESSL_OPT_RESIZE_COLS, cols)
+        loader2.set_option(N.ESSL_OPT_RESIZE_BAND, band)
+        for b in loader2.epoch(2):
+            idx = b.indices.cpu().numpy()
+            pix, _, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 2, res)
+            assert np.array_equal(b.pixels.cpu().numpy(), pix)
