@@ -283,7 +283,8 @@ def run_gpu(args, wl):
                            (N.ESSL_OPT_CHECKPOINT_BITS, args.ck_bits, args.ck_bits > 0),
                            (N.ESSL_OPT_STAGE_BYTES, args.stage_bytes, args.stage_bytes >= 0),
                            (N.ESSL_OPT_RESIZE_COLS, args.resize_cols, args.resize_cols > 0),
-                           (N.ESSL_OPT_RESIZE_BAND, args.resize_band, args.resize_band > 0)):
+                           (N.ESSL_OPT_RESIZE_BAND, args.resize_band, args.resize_band > 0),
+                           (N.ESSL_OPT_EARLY_EXIT, args.early_exit, args.early_exit >= 0)):
             if on:
                 ld.set_option(opt, v)
 
@@ -517,6 +518,8 @@ def main():
                     help="k_resize output columns per thread (ESSL_OPT_RESIZE_COLS; 0: default)")
     ap.add_argument("--resize-band", type=int, default=0,
                     help="k_resize output rows per CTA, at most (ESSL_OPT_RESIZE_BAND; 0: default)")
+    ap.add_argument("--early-exit", type=int, default=-1,
+                    help="ESSL_OPT_EARLY_EXIT (entropy decode stops near the crop's last row; -1: default)")
     ap.add_argument("--streams", type=int, default=8,
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--gather-ctas", type=int, default=-1,

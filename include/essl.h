@@ -73,6 +73,7 @@ extern "C" {
 #define ESSL_OPT_TRACE 10       /* n > 0: record up to n CTA executions (essl_trace_read); 0 off */
 #define ESSL_OPT_RESIZE_COLS 11 /* k_resize output columns per thread: 2 (default), 4 or 8 */
 #define ESSL_OPT_RESIZE_BAND 12 /* k_resize output rows per CTA, at most (1..64, default 64) */
+#define ESSL_OPT_EARLY_EXIT 13  /* 1 (default): entropy decode stops near the crop's last needed row */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0

@@ -49,6 +49,7 @@ constexpr int kDefGatherCtas = 4;
 constexpr bool kDefGatherTma = true;
 constexpr int kDefResizeCols = 2;
 constexpr int kDefResizeBand = 64;
+constexpr int kDefEarlyExit = 1;
 
 // Persistent host workers for payload staging (one pool per context): a
 // batch's copies are split into contiguous ranges, the caller thread takes
@@ -158,6 +159,7 @@ struct essl_ctx {
   bool gather_tma = kDefGatherTma;   // ESSL_OPT_GATHER_TMA: bulk (TMA) bus reads, e2e +9% over LSU loads
   int resize_cols = kDefResizeCols;  // ESSL_OPT_RESIZE_COLS
   int resize_band = kDefResizeBand;  // ESSL_OPT_RESIZE_BAND
+  int early_exit = kDefEarlyExit;    // ESSL_OPT_EARLY_EXIT
   int32_t *dbg_lanes = nullptr;  // ESSL_OPT_DEBUG_LANES buffer
   essl::CtaTrace trace{nullptr, nullptr, 0};  // ESSL_OPT_TRACE  // bulk-copy (TMA) gather (ESSL_OPT_GATHER_TMA)
   std::atomic<int64_t> launches{0};
@@ -337,6 +339,7 @@ int launch_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *d_desc, i
   p.ck_bits = c->ck_bits;
   p.warm_bits = c->warm_bits;
   p.stage_bytes = c->stage_max;
+  p.early_exit = c->early_exit;
   p.results = results;
   p.dbg_lanes = c->dbg_lanes;
   p.trace = c->trace;
@@ -554,6 +557,9 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       if (value < 1 || value > essl::kMaxBandRows) return fail(ESSL_E_ARG, "bad resize band");
       c->resize_band = (int)value;
       return ESSL_OK;
+    case ESSL_OPT_EARLY_EXIT:
+      c->early_exit = value != 0;
+      return ESSL_OK;
     case ESSL_OPT_CHECKPOINT_BITS:
       if (value < 1 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad checkpoint bits");
       c->ck_bits = (int)value;
@@ -577,6 +583,7 @@ int essl_option_default(int option, int64_t *value) {
     case ESSL_OPT_TRACE: *value = 0; return ESSL_OK;
     case ESSL_OPT_RESIZE_COLS: *value = kDefResizeCols; return ESSL_OK;
     case ESSL_OPT_RESIZE_BAND: *value = kDefResizeBand; return ESSL_OK;
+    case ESSL_OPT_EARLY_EXIT: *value = kDefEarlyExit; return ESSL_OK;
   }
   return fail(ESSL_E_ARG, "unknown option");
 }

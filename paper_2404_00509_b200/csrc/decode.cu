@@ -505,6 +505,7 @@ struct EntCtx {
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
   int c1, c2, bpm, gx;
   uint32_t cbits, limit, ck_bits;
+  uint32_t cend;  // end of the range phase 1 covers (N2 estimate; cbits without it)
   const uint32_t *words;  // clean stream (global)
   uint32_t ring_s;        // this lane's read ring (shared-window address)
   uint32_t wmax, cpad;
@@ -627,7 +628,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     nl = R.nlist;
     nbs = R.nbs;
     jn = Ls[j].nck;
-    send = C.cbits;
+    send = C.cend;  // no checkpoint lies beyond the covered range
   } else {
     C.reader(r, p0);
     k = 0;
@@ -798,6 +799,72 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.ovf = ovf;
   }
   if (!ovf) list[nl] = 1u;  // sentinel: a DC-flagged entry ends the last block
+}
+
+// Extension of an owner's path past the estimated end of the crop's rows
+// (N2: phase 1 and the continuations cover only the bits up to an estimate of
+// the position of the crop's last needed block, codec.py:494-498 row_stop).
+// Serial decode on the exact path from the path's stop state X, appending
+// units and block records to the owner's lists exactly like phase 1, until
+// `need` more blocks complete (stops at that block end), a decode error, or
+// the end of the data.  Updates X, the list lengths and the block count
+// `added`; returns 0 (reached), 1 (error at X.p) or 2 (data ended first).
+struct PathEnd {
+  uint32_t p;
+  int k, b, be;
+};
+
+template <bool SH>
+__device__ int extend_path(const EntCtx &C, uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap,
+                           uint32_t &nlist, uint32_t &nblist, PathEnd &X, uint32_t need,
+                           uint32_t &added, int &ovf) {
+  Reader<SH> r;
+  C.reader(r, X.p);
+  int k = X.k, b = X.b, be = X.be;
+  uint32_t nl = nlist, nbs = nblist, nblk = 0;
+  uint32_t *lp = list + min(nl, cap);
+  uint2 *bp = bsl + min(nbs, bcap);
+  int st = 2;
+#pragma unroll 1
+  while (r.p < C.cbits) {
+    r.refill();
+    const uint32_t hi = r.hi();
+    const uint32_t e = C.lookup<SH>(k, b, hi);
+    UNIT_FIELDS(e, k);
+    if (bad) {
+      st = 1;
+      break;
+    }
+    const uint32_t raw = unit_raw(hi, tot, size);
+    const bool isdc = k == 0;
+    *lp = unit_entry(raw, size, isdc ? 0 : min(knew, 64) - 1, isdc);
+    if (isdc) {
+      *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
+      bp += nbs < bcap;
+      nbs++;
+    }
+    lp += nl < cap;
+    nl++;
+    r.skip(tot);
+    be = knew >= 64;
+    k = be ? 0 : knew;
+    b = be ? (b + 1 == C.bpm ? 0 : b + 1) : b;
+    nblk += be;
+    if (be && nblk == need) {
+      st = 0;
+      break;
+    }
+  }
+  X.p = r.p;
+  X.k = k;
+  X.b = b;
+  X.be = be;
+  added = nblk;
+  nlist = nl;
+  nblist = nbs;
+  if (nl >= cap || nbs > bcap) ovf = 1;
+  else list[nl] = 1u;  // sentinel
+  return st;
 }
 
 // Serial decode from (p, k, b) until `need` more blocks complete or a decode
@@ -1770,7 +1837,7 @@ struct __align__(16) EntSmem {
   int status, reason, offset;
   uint32_t p_final;
   int coef_range, red;
-  unsigned int dbg_units, dbg_guess, dbg_umax;
+  unsigned int dbg_units, dbg_guess, dbg_umax, dbg_ext;
   unsigned long long lbase;
   int32_t dcsum[kLanes * 3];
   int fmt;
@@ -1861,9 +1928,20 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
   } else if (S.status == 0) {
     // ---- checkpoint-merge parallel decode, each unit decoded once ---------
     const uint32_t cbits = C.cbits;
-    int nseq = (int)((cbits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
+    // N2 (codec.py:494-498): the crop needs blocks [0, limit) only.  Phase 1
+    // covers the bits up to an estimate of where block `limit` ends (the
+    // limit's share of all blocks, plus a margin); if the exact path has not
+    // reached the limit there, the last lane's path is extended serially.
+    const uint32_t total_blocks = (uint32_t)H.gx * (uint32_t)H.gy * (uint32_t)H.bpm;
+    uint32_t end_bits = cbits;
+    if (P.early_exit && C.limit < total_blocks) {
+      const uint64_t est = (uint64_t)cbits * C.limit / total_blocks;
+      end_bits = (uint32_t)min((uint64_t)cbits, est + cbits / 32 + 512);
+    }
+    C.cend = end_bits;
+    int nseq = (int)((end_bits + P.seq_bits - 1) / (uint32_t)P.seq_bits);
     nseq = max(1, min(nseq, kLanes));
-    const uint32_t slen = (cbits + nseq - 1) / nseq;
+    const uint32_t slen = (end_bits + nseq - 1) / nseq;
     const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
     C.ck_bits = max((uint32_t)P.ck_bits, (slen + kCk - 9) / (kCk - 8));  // checkpoints cover [sbeg, send)
     Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
@@ -1890,7 +1968,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
     const uint32_t lcap = lists_ok ? cap : 0u, lbcap = lists_ok ? bcap : 0u;
     if (lane < nseq) {
       const uint32_t sbeg = lane * slen;
-      const uint32_t send = lane == nseq - 1 ? cbits : min(cbits, (lane + 1) * slen);
+      const uint32_t send = lane == nseq - 1 ? end_bits : min(end_bits, (lane + 1) * slen);
       const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
       run_path<false, SH>(C, lane, nseq, p0, sbeg, send, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
     }
@@ -1927,20 +2005,46 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
           break;
         }
         const bool last = o == nseq - 1;
-        const uint32_t seg = own + (last ? 0u : L.cn);
+        // a path that ends without a merge: the last lane's, or a continuation
+        // that ran to the end of the covered range
+        const bool open_end = last || L.cst == 2;
+        uint32_t seg = own + (last ? 0u : L.cn);
+        PathEnd X = last ? PathEnd{L.xp, L.xk, L.xb, L.xbe} : PathEnd{L.cp, (int)L.ek, (int)L.eb, L.cbe};
+        if (open_end && A + seg < limit && X.p < cbits) {
+          // it stopped at the estimated end before the crop's last needed
+          // block: extend the exact path, appending to this lane's lists
+          const unsigned long long lr = lists_ok ? S.lbase + (unsigned long long)o * stride : 0ull;
+          uint32_t *lo = lists_ok ? P.s.list + lr : P.s.list + P.s.list_cap + 4 * o;
+          uint2 *bo = reinterpret_cast<uint2 *>(lists_ok ? P.s.list + lr + cap + 8
+                                                         : P.s.list + P.s.list_cap + 4 * o + 2);
+          uint32_t added = 0;
+          int ovf = 0;
+          const int xs = extend_path<SH>(C, lo, lists_ok ? cap : 0u, bo, lists_ok ? bcap : 0u, L.nlist,
+                                         L.nbs, X, limit - (A + seg), added, ovf);
+          S.dbg_ext += 1;
+          seg += added;
+          if (ovf) {
+            L.ovf = 1;
+            S.fmt = 0;
+          }
+          if (xs == 1) {
+            L.w_nb = min(seg, limit - A);
+            ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, X.p));
+            break;
+          }
+        }
         L.w_nb = min(seg, limit - A);
-        const uint32_t end_p = last ? L.xp : L.cp;
-        const int end_be = last ? L.xbe : L.cbe;
+        const uint32_t end_p = X.p;
+        const int end_be = X.be;
         if (A + seg >= limit) {
           // the block reaching the limit ends past the data (_check_consumed)
           if (A + seg == limit && end_be && end_p > cbits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
           break;
         }
-        if (last || L.cst == 2) {
+        if (open_end) {
           // the data ends before the crop's last MCU row: continue serially
           // into the 0xFF padding to classify corrupt (1) vs truncated (4)
-          const uint32_t errp = tail_run<SH>(C, end_p, last ? L.xk : (int)L.ek, last ? L.xb : (int)L.eb,
-                                             limit - (A + seg));
+          const uint32_t errp = tail_run<SH>(C, end_p, X.k, X.b, limit - (A + seg));
           if (errp != kNoEnd) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, errp));
           else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
           break;
@@ -2022,7 +2126,7 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
     S.coef_range = 0;
     S.p_final = kNoEnd;
     S.fmt = 0;
-    S.dbg_units = 0; S.dbg_guess = 0; S.dbg_umax = 0;
+    S.dbg_units = 0; S.dbg_guess = 0; S.dbg_umax = 0; S.dbg_ext = 0;
   }
   LaneRec &R = S.lane[lane];
   R.w_nb = 0;
@@ -2046,6 +2150,7 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
   C.gx = H.gx;
   C.cbits = H.clean_bits;
   C.limit = H.limit_blocks;
+  C.cend = H.clean_bits;
   C.words = reinterpret_cast<const uint32_t *>(P.s.clean + H.clean_off);
   C.wmax = H.wmax;
   C.ck_bits = 0;
@@ -2092,7 +2197,7 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
     info->offset = S.offset;
     info->fmt = S.fmt;
     for (int i = 0; i < 6; i++) info->dbg[2 + i] = S.t_ph[i];
-    info->dbg[10] = dbg_nseq;
+    info->dbg[10] = dbg_nseq | ((long long)S.dbg_ext << 32);
     info->dbg[11] = dbg_cont;
     const uint32_t su = S.dbg_units, sg = S.dbg_guess, mu = S.dbg_umax;
     info->dbg[8] = su | ((long long)sg << 32);

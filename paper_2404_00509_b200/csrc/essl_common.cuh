@@ -113,6 +113,7 @@ struct DecodeParams {
   int ck_bits;       // minimum checkpoint spacing (bits)
   int warm_bits;     // each lane (but lane 0) starts this far before its subsequence
   int stage_bytes;   // k_entropy read rings (0: plain global reads)
+  int early_exit;    // k_entropy: phase 1 stops near the crop's last needed block (N2)
   int prep_part_off; // k_prep: byte offset of the CRC partials in dynamic smem
   essl_result *results;  // optional
   int32_t *dbg_lanes;    // optional per-lane decode records [n][kEntropyLanes][8]

@@ -204,3 +204,50 @@ def test_resize_shapes_vs_oracle(E, oracle, tmp_path_factory, cols, band, res):
             idx = b.indices.cpu().numpy()
             pix, _, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, 2, res)
             assert np.array_equal(b.pixels.cpu().numpy(), pix)
+
+
+def _skewed_container(E, path, n=24, side=256, seed=21):
+    """Images whose entropy-coded bits sit in their bottom rows (flat top,
+    noisy bottom quarter): the block-share estimate of where the crop's last
+    needed row ends undershoots, so the N2 early exit must extend the path."""
+    from paper_2404_00509_b200.container import encode_jpeg, write_container
+    rng = np.random.default_rng(seed)
+    pays = []
+    for i in range(n):
+        img = np.full((side, side, 3), 90 + i, np.uint8)
+        cut = side * 3 // 4 - 8 * (i % 5)
+        img[cut:] = rng.integers(0, 256, (side - cut, side, 3), dtype=np.uint8)
+        pays.append(encode_jpeg(img, 95))
+    write_container(path, pays, [side] * n, [side] * n, np.arange(n) % 4, side, 95, seed)
+    return path
+
+
+@pytest.mark.parametrize("kind", ["pool", "skewed"])
+def test_early_exit_equals_full_decode(E, oracle, pool256, tmp_path, kind):
+    """N2: the entropy decode stopping near the crop's last needed MCU row
+    (ESSL_OPT_EARLY_EXIT, default on) gives the same pixels as decoding every
+    bit, and both equal the oracle -- also on streams whose bits concentrate
+    below the estimate (the serial extension of the last lane's path)."""
+    import torch
+    from paper_2404_00509_b200 import _native as N
+    path = pool256 if kind == "pool" else _skewed_container(E, tmp_path / "skew.essl")
+    with E.open_container(path) as h:
+        outs = []
+        for ee in (1, 0):
+            cfg = E.LoaderConfig(data=str(path), batch_size=256 if kind == "pool" else 24, res=224,
+                                 out_dtype="bfloat16", streams=2, prefetch=2)
+            loader = E.Loader(cfg, container=h)
+            loader.set_option(N.ESSL_OPT_EARLY_EXIT, ee)
+            got = []
+            for e in (0, 1):
+                for b in loader.epoch(e):
+                    idx = b.indices.cpu().numpy()
+                    if ee == 1:
+                        pix, _, _, st = oracle.loader_batch(h.bytes, h.records, idx, 0, e, 224)
+                        assert (st == 0).all()
+                        assert torch.equal(b.pixels.cpu(), torch.from_numpy(pix).to(torch.bfloat16))
+                    got.append(_digest(b.pixels))
+                    if kind == "pool" and len(got) >= 4:
+                        break
+            outs.append(got)
+        assert outs[0] == outs[1]

@@ -70,7 +70,8 @@ def main():
         ph = np.stack([dbg[:, 1] - dbg[:, 0]] + [dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)]
                       + [dbg[:, 13] - dbg[:, 12], dbg[:, 14] - dbg[:, 13], dbg[:, 15] - dbg[:, 14],
                          dbg[:, 1] - dbg[:, 15]], 1)
-        nseq = dbg[:, 10]
+        nseq = dbg[:, 10] & 0xFFFFFFFF
+        ext = dbg[:, 10] >> 32
         cont = dbg[:, 11]
         row = {"mode": mode, "seq_bits": sb, "warm_bits": ov,
                "decode_ms": prof["decode"][0] / prof["decode"][1],
@@ -83,7 +84,8 @@ def main():
                "reguess_phase1_mean": float((dbg[:, 8] >> 32).mean()),
                "units_phase1_lane_max_median": float(np.median(dbg[:, 9] & 0xFFFFFFFF)),
                "fallback_images": int((dbg[:, 9] >> 32).sum()),
-               "nseq_mean": float(nseq.mean()), "cont_bits_max_median": float(np.median(cont)),
+               "nseq_mean": float(nseq.mean()), "extended_images": int((ext > 0).sum()),
+               "cont_bits_max_median": float(np.median(cont)),
                "cont_bits_max_max": int(cont.max())}
         results.append(row)
         print(json.dumps(row), flush=True)
