@@ -84,6 +84,28 @@ def peaks() -> dict:
     return {"hbm_gbs": 6650.0, "src": "fallback"}
 
 
+def config_dict(args, wl: dict, records: int, mean_payload: float) -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": f"{args.workload}: {wl['desc']}", "batch": wl["batch"],
+            "res": list(wl["schedule"]) if wl.get("schedule") else wl["res"],
+            "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool,
+            "records": records, "mean_payload_bytes": mean_payload,
+            "l2": f"inputs > L2: {args.pool}-image pool (~{args.pool * mean_payload / 1e6:.0f} MB of "
+                  "JPEG bytes, 126 MB L2) visited in permutation order; outputs: a reused ring of "
+                  "16 output buffers per loader (each written once per 16 steps)",
+            "parallelism": "ddp per GPU (rank shards perm[r::world], no collective on the path)"}
+
+
+def dataset_dir(rank: int, ws: int) -> Path:
+    """One synthetic dataset per job: under torchrun every rank opens the
+    file rank 0 wrote (the other ranks wait on a barrier)."""
+    d = Path(tempfile.gettempdir()) / f"essl_bench_{os.environ.get('TORCHELASTIC_RUN_ID', os.getpid())}"
+    if ws == 1:
+        d = Path(tempfile.mkdtemp(prefix="essl_bench_"))
+    d.mkdir(parents=True, exist_ok=True)
+    return d
+
+
 def make_dataset(wl: dict, pool: int, out_dir: Path, seed: int = 1) -> Path:
     from paper_2404_00509_b200 import build_synthetic
     rec = wl.get("records")
@@ -205,6 +227,25 @@ def dist_env():
     return ws, rank, local
 
 
+def reference_loader_rates(path: Path, wl: dict, args) -> dict:
+    """The unmodified reference cropload.pipeline.Loader (baseline/_ref) on
+    this host's cores over the same container: workers = all cores (the
+    primary CPU baseline of BASELINE.md section 3), workers = 1, and one
+    process per core (upper bound); tools/ref_loader_rate.py, bounded samples."""
+    out = {}
+    for mode in ("threads", "single", "procs"):
+        cmd = [sys.executable, str(ROOT / "tools" / "ref_loader_rate.py"), "--data", str(path),
+               "--batch", str(wl["batch"]), "--res", str(wl["res"]), "--scale", str(wl["scale"][0]),
+               str(wl["scale"][1]), "--mask", str(wl["mask"]), "--seconds",
+               str(args.ref_loader_seconds), "--mode", mode]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, never fatal: the port is the timed arm
+            out[mode] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    return out
+
+
 def run_reference(args, wl):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -234,13 +275,15 @@ def run_reference(args, wl):
         t0 = time.perf_counter()
         n = sum(step(args.warmup + i) for i in range(args.steps))
         el = time.perf_counter() - t0
+        records, mean_payload = len(h), float(np.mean(h.records["payload_length"]))
     v = n / el
+    ref_loader = reference_loader_rates(path, wl, args) if args.ref_loader_seconds > 0 else None
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "images/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": wl["batch"],
-                       "res": wl["res"], "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool},
+            "vs_baseline": None, "dtype": "int32", "out_dtype": "f32", "data": "synthetic",
+            "config": config_dict(args, wl, records, mean_payload),
+            "reference_loader": ref_loader,
             "cpu_baseline": {"value": v, "unit": "images/s", "cores": nthreads, "kind": "port",
                              "sample": f"{args.steps} timed batches of {wl['batch']} after "
                                        f"{args.warmup} warm-up, C oracle (port of the reference "
@@ -267,8 +310,12 @@ def run_gpu(args, wl):
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    data_dir = Path(tempfile.mkdtemp(prefix=f"essl_bench_{rank}_"))
-    path = make_dataset(wl, args.pool, data_dir)
+    data_dir = dataset_dir(rank, ws)
+    if rank == 0:
+        path = make_dataset(wl, args.pool, data_dir)
+    if ws > 1:
+        dist.barrier()  # rank 0 has written the dataset; the others open the same file
+        path = make_dataset(wl, args.pool, data_dir)  # (exists: no rebuild)
     B, res = wl["batch"], wl["res"]
     cfg = E.LoaderConfig(data=str(path), batch_size=B, res=res, scale=wl["scale"],
                          mask_ratio=wl["mask"], aug=wl.get("aug", "simple"),
@@ -447,22 +494,7 @@ def run_gpu(args, wl):
         stages = wl.get("schedule") or (res,)
         per_img = float(np.mean(handle.records["payload_length"])) + \
             float(np.mean([bytes_out(r) for r in stages]))
-        # dominant kernel (largest device-time share): k_entropy
-        ent_ms, ent_n = prof.get("entropy", (0.0, 0))
-        imgs_per_launch = n_img / max(ent_n, 1)
-        achieved = per_img * imgs_per_launch / (ent_ms / max(ent_n, 1) / 1e3) / 1e9 if ent_n else None
-        traffic = None
-        tp = ROOT / "profiles" / "r1_ncu_k_entropy.json"
-        if tp.exists() and args.workload == "cfg2":  # one ncu --set full capture of this launch shape
-            traffic = json.loads(tp.read_text()).get("dram_bytes")
-        roof = {"bound": "hbm", "kernel": "k_entropy", "achieved": achieved, "peak": pk["hbm_gbs"],
-                "peak_src": pk["src"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"] if achieved else None,
-                "traffic": traffic, "traffic_src": "profiles/r1_ncu_k_entropy.json (dram read+write "
-                                                    "bytes of one launch)" if traffic else None,
-                "bytes_per_image": per_img, "images_per_launch": imgs_per_launch,
-                "kernel_ms": {k: v[0] / max(v[1], 1) for k, v in prof.items()},
-                "kernel_share": {k: v[0] / ms for k, v in prof.items() if k != "decode"}}
+        roof = roofline_block(args, prof, ms, n_img, per_img, value, clocks, pk)
         cpu = None
         if not args.no_cpu:
             cpu = cpu_oracle_rate(path, wl, args.cpu_seconds)
@@ -470,14 +502,8 @@ def run_gpu(args, wl):
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "int32", "out_dtype": "bf16", "data": "synthetic",
-                "config": {"workload": f"{args.workload}: {wl['desc']}", "batch": B,
-                           "res": list(wl["schedule"]) if wl.get("schedule") else res,
-                           "mask_ratio": wl["mask"], "aug": wl.get("aug", "simple"), "pool_images": args.pool,
-                           "records": len(handle),
-                           "mean_payload_bytes": float(np.mean(handle.records["payload_length"])),
-                           "l2": "inputs > L2: 8192-image pool (~235 MB) visited in permutation "
-                                 "order; outputs are fresh buffers each step",
-                           "parallelism": f"ddp{ws} (rank shards, no collective on path)"},
+                "config": config_dict(args, wl, len(handle),
+                                      float(np.mean(handle.records["payload_length"]))),
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_total / (e2e_ms_max / 1e3) if e2e_v else None,
                         "unit": "images/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -486,6 +512,62 @@ def run_gpu(args, wl):
     loader.close()
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _profile(name: str) -> dict | None:
+    """A committed ncu summary (profiles/), newest round first."""
+    for tag in ("r2", "r1"):
+        p = ROOT / "profiles" / f"{tag}_{name}.json"
+        if p.exists():
+            d = json.loads(p.read_text())
+            d["_src"] = str(p.relative_to(ROOT))
+            return d
+    return None
+
+
+def roofline_block(args, prof: dict, ms: float, n_img: int, per_img: float, value: float,
+                   clocks: dict, pk: dict) -> dict:
+    """HBM roofline of the path: algorithmic bytes per image =
+    payload in + bf16 NCHW out (+ mask/ids).  frac: the dominant kernel
+    (k_entropy) per the contract -- algorithmic bytes of one launch / its mean
+    CUDA-event launch duration inside the timed region (a latency figure:
+    8 batches overlap); job_frac: whole-job bytes / time; issue_frac: the
+    binding resource, warp instructions per image (pipeline-range ncu) x
+    img/s over the issue slots (148 SMs x 4 schedulers x clock); per kernel:
+    the isolated ncu launch (256 images) against the same bytes."""
+    peak = pk["hbm_gbs"]
+    ent_ms, ent_n = prof.get("entropy", (0.0, 0))
+    ipl = n_img / max(ent_n, 1)
+    achieved = per_img * ipl / (ent_ms / max(ent_n, 1) / 1e3) / 1e9 if ent_n else None
+    ent = _profile("ncu_k_entropy") if args.workload == "cfg2" else None
+    rng = _profile("ncu_pipeline_range") if args.workload == "cfg2" else None
+    sm_hz = (clocks.get("sm_mhz") or 0) * 1e6 or (rng or {}).get("sm_clock_ghz", 1.965) * 1e9
+    wipi = (rng or {}).get("warp_instructions_per_image")
+    roof = {"bound": "hbm", "kernel": "k_entropy", "achieved": achieved, "peak": peak,
+            "peak_src": pk["src"], "unit": "GB/s", "frac": achieved / peak if achieved else None,
+            "traffic": (ent or {}).get("dram_bytes"),
+            "traffic_src": f"{ent['_src']} (dram read+write bytes of one 256-image launch)" if ent else None,
+            "bytes_per_image": per_img, "images_per_launch": ipl,
+            "job_achieved": per_img * value / 1e9,
+            "job_frac": per_img * value / 1e9 / peak,
+            "traffic_pipeline_per_image": (rng or {}).get("dram_bytes_per_image"),
+            "issue_frac": wipi * value / (148 * 4 * sm_hz) if wipi else None,
+            "warp_instructions_per_image": wipi,
+            "issue_src": f"{rng['_src']} x value / (148 SMs x 4 x {sm_hz / 1e6:.0f} MHz)" if rng else None,
+            "kernel_ms": {k: v[0] / max(v[1], 1) for k, v in prof.items()},
+            "kernel_share": {k: v[0] / ms for k, v in prof.items() if k != "decode"},
+            "kernels_isolated": {}}
+    if args.workload == "cfg2":
+        for k in ("k_prep", "k_entropy", "k_idct", "k_resize", "k_mask"):
+            d = _profile(f"ncu_{k}")
+            if d and d.get("duration_ns"):
+                imgs = 256
+                roof["kernels_isolated"][k] = {
+                    "us": d["duration_ns"] / 1e3, "images": imgs,
+                    "frac": per_img * imgs / (d["duration_ns"] * 1e-9) / 1e9 / peak,
+                    "warp_instructions_per_image": d.get("warp_instructions", 0) / imgs,
+                    "dram_bytes_per_image": d.get("dram_bytes", 0) / imgs, "src": d["_src"]}
+    return roof
 
 
 def ctypes_sizeof_sample():
@@ -506,6 +588,8 @@ def main():
                     help="time one full epoch of this rank's shard (steps = batches per epoch)")
     ap.add_argument("--pool", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--ref-loader-seconds", type=float, default=6.0,
+                    help="reference arm: bounded sample per reference-Loader measurement (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seq-bits", type=int, default=0, help="speculative subsequence bits (0: library default)")
