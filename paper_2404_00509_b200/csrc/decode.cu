@@ -114,6 +114,12 @@ struct __align__(16) DecodeHead {
   int32_t slot_comp[4], slot_h[4], slot_v[4], slot_nb[4];
   int32_t wby0[3], wbx0[3], wbh[3], wbw[3], bw[3], bh[3];
   int32_t quant_missing;  // -1: all dequantisation tables present
+  // multi-scan streams (progressive / several scans): full decode of every
+  // scan into full coefficient arrays (k_entropy multiscan path)
+  int32_t multiscan, progressive;
+  int32_t comp_id[3];     // component identifiers (SOF)
+  int32_t comp_hv[3];     // h << 4 | v per component
+  int32_t coef_pitch[3];  // blocks per coefficient-array row (window width; BW when multiscan)
   uint32_t rst_off;       // restart table, words from the clean region start
   uint64_t coef_off[3], coef_base, clean_off;
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
@@ -1237,6 +1243,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     H.status = 0; H.reason = 0; H.offset = -1;
     H.ntab = 0; H.ns = 0; H.ncomp = 0; H.quant_missing = -1;
     H.limit_blocks = 0; H.clean_bits = 0; H.clean_words = 0; H.scan_ri = 0; H.wmax = 0; H.cpad = 0;
+    H.multiscan = 0; H.progressive = 0;
   }
   // ---- stage the payload into shared memory (16-byte loads) ----------------
   if (SMEM) {
@@ -1410,10 +1417,50 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       const int x = smp.x, y = smp.y, w = smp.w, h = smp.h;
       if (w < 1 || h < 1 || x < 0 || y < 0 || x + w > W || y + h > Hh) {
         hdr_status(H, ESSL_ST_RECT, 0, -1);
-      } else if (PS.progressive) {
-        hdr_status(H, ESSL_ST_UNSUPPORTED, R_PROGRESSIVE, -1);
-      } else if (PS.nscans != 1 || PS.ns != PS.ncomp) {
-        hdr_status(H, ESSL_ST_UNSUPPORTED, R_MULTI_SCAN, -1);
+      } else if (PS.progressive || PS.nscans != 1 || PS.ns != PS.ncomp) {
+        // the reference's full-decode fallback (codec.py:461-469): every scan
+        // decoded in full into full coefficient arrays [BH][BW][64] per
+        // component (int16, carved here), the crop window reconstructed from
+        // them; stats count every MCU (codec.py:466-469)
+        H.multiscan = 1;
+        H.progressive = PS.progressive;
+        H.gx = mcus_x;
+        H.gy = mcus_y;
+        const int mcu_w = 8 * hmax, mcu_h = 8 * vmax;
+        H.mx0 = x / mcu_w; H.mx1 = (x + w - 1) / mcu_w;
+        H.my0 = y / mcu_h; H.my1 = (y + h - 1) / mcu_h;
+        H.row_stop = mcus_y;
+        const int total_mcus = PS.ncomp > 1 ? mcus_x * mcus_y : H.bw[0] * H.bh[0];
+        info->mcus_entropy = total_mcus;
+        info->mcus_recon = total_mcus;
+        uint64_t total = 0;
+        for (int c = 0; c < 3; c++) {
+          H.wbh[c] = 0; H.wbw[c] = 0; H.wby0[c] = 0; H.wbx0[c] = 0; H.coef_off[c] = 0;
+          H.coef_pitch[c] = 0; H.comp_hv[c] = 0; H.comp_id[c] = -1;
+        }
+        for (int c = 0; c < PS.ncomp; c++) {
+          const int BW = mcus_x * PS.comp_h[c], BH = mcus_y * PS.comp_v[c];
+          H.comp_hv[c] = (PS.comp_h[c] << 4) | PS.comp_v[c];
+          H.comp_id[c] = PS.comp_id[c];
+          H.wby0[c] = H.my0 * PS.comp_v[c];
+          H.wbx0[c] = H.mx0 * PS.comp_h[c];
+          H.wbh[c] = (H.my1 - H.my0 + 1) * PS.comp_v[c];
+          H.wbw[c] = (H.mx1 - H.mx0 + 1) * PS.comp_h[c];
+          H.coef_pitch[c] = BW;
+          H.coef_off[c] = total;
+          total += (uint64_t)BH * BW * 64;
+        }
+        const unsigned long long cbase = atomicAdd(&P.s.counters[1], (unsigned long long)total);
+        if (cbase + total > P.s.coef_cap) {
+          hdr_status(H, ESSL_ST_CAPACITY, R_SCRATCH, -1);
+        } else {
+          for (int c = 0; c < 3; c++) H.coef_off[c] += cbase;
+          H.coef_base = cbase;
+        }
+        for (int i = 0; i < PS.ncomp; i++) {
+          const int tq = PS.comp_tq[i];
+          if (tq > 15 || PS.quant_pos[tq] < 0) { H.quant_missing = tq; break; }
+        }
       } else {
         const int ns = PS.ns;
         H.ns = ns;
@@ -1456,6 +1503,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
           H.wbh[c] = (H.my1 - H.my0 + 1) * H.slot_v[s];
           H.wbw[c] = (H.mx1 - H.mx0 + 1) * H.slot_h[s];
           H.coef_off[c] = total;
+          H.coef_pitch[c] = H.wbw[c];
           total += (uint64_t)H.wbh[c] * H.wbw[c] * 64;
         }
         const unsigned long long cbase = atomicAdd(&P.s.counters[1], (unsigned long long)total);
@@ -1502,7 +1550,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
   //      global clean region ---------------------------------------------------
   uint8_t *gclean = P.s.clean + H.clean_off;
   uint8_t *clean = SMEM ? dyn + (PS.scan_start & ~15) : gclean;
-  if (H.status == 0) {
+  if (H.status == 0 && !H.multiscan) {
     // Rounds of kNT x 16 bytes: thread t owns bytes [16t, 16t+16) of the
     // round (16-byte shared loads, conflict-free); a block scan per round
     // places the kept bytes.
@@ -1841,6 +1889,7 @@ struct __align__(16) EntSmem {
   unsigned long long lbase;
   int32_t dcsum[kLanes * 3];
   int fmt;
+  int ms_nscan, ms_nlevel, ms_range;
   __align__(16) uint32_t ring[kLanes][16];
   long long t_ph[8];
 };
@@ -1862,6 +1911,528 @@ __device__ void zero_window(const DecodeHead &H, int16_t *coef, int lane) {
   for (uint64_t i = lane; i < total / 8; i += kLanes) z[i] = make_int4(0, 0, 0, 0);
 }
 
+// ===========================================================================
+// Multi-scan streams (progressive, or sequential with several scans): the
+// reference's full-decode fallback (codec.py:352-399 _decode_scans_full,
+// decode_kernels.py:111-385) on the GPU.  Every scan is decoded in full into
+// the image's full coefficient arrays (int16 [BH][BW][64] per component,
+// carved by k_prep); k_idct then reconstructs the crop window from them.
+// Scans that touch disjoint coefficients (other components, other spectral
+// bands) are independent, so the CTA's lanes decode them in parallel waves
+// (a scan waits for every earlier scan it shares a component and band with;
+// refinement scans therefore follow the scans they refine).  Errors are the
+// reference's: the first failing scan in file order decides, with the same
+// message and offset.
+// ===========================================================================
+constexpr int kMsMaxScans = 64;
+constexpr int kMsMaxTabs = 16;
+
+struct MsScan {
+  int32_t start, end, ri;       // entropy-coded bytes [start, end) of the payload; DRI in force
+  int32_t err, reason, off;     // pre-decode error (status, reason, offset) or 0
+  int32_t level;                // dependency wave
+  int32_t status, errp;         // decode result: status (0/1/3/4) and failing bit position
+  int32_t dpos[3], apos[3];     // DHT definitions in force at the SOS (payload offsets, -1: none)
+  uint8_t ns, ss, se, ah, al, pad0;
+  uint8_t comp[3];
+  int8_t dt[3], at[3];          // decoder index of the used tables (-1: unused)
+  uint8_t pad1;
+};
+
+struct MsTab {  // canonical Huffman decoder of one DHT definition (codec.py:272-295)
+  int32_t maxcode[18];   // largest code of each length (-1: none)
+  int32_t mincode[17];
+  int16_t valptr[17];
+  int16_t pad;
+  int32_t vals;          // payload offset of the symbol values
+};
+static_assert(sizeof(MsScan) * kMsMaxScans + sizeof(MsTab) * kMsMaxTabs <= kSmemTabs * 2048,
+              "multi-scan state must fit the shared first-level table area");
+
+// Clean-stream bit reader over the RAW scan bytes (destuff_scan semantics,
+// decode_kernels.py:27-61, on the fly): FF00 -> FF, RSTn skipped, any other
+// FFxx ends the data; past the end the reader supplies 0xFF (_br_fill).  p is
+// the number of clean bits consumed (the reference's 8*vpos - cnt).
+struct MsReader {
+  const uint8_t *raw;
+  int rpos, rend;
+  bool ended;
+  uint64_t buf;  // left-aligned
+  int n;
+  uint32_t p;
+  __device__ __forceinline__ uint32_t next_byte() {
+#pragma unroll 1
+    while (!ended) {
+      if (rpos >= rend) { ended = true; break; }
+      const uint32_t b = raw[rpos];
+      if (b != 0xFF) { rpos++; return b; }
+      if (rpos + 1 >= rend) { ended = true; break; }
+      const uint32_t m = raw[rpos + 1];
+      if (m == 0x00) { rpos += 2; return 0xFF; }
+      if (m >= 0xD0 && m <= 0xD7) { rpos += 2; continue; }
+      ended = true;
+    }
+    return 0xFF;
+  }
+  __device__ __forceinline__ void anchor(int raw_pos, uint32_t clean_bit) {
+    rpos = raw_pos;
+    ended = false;
+    buf = 0;
+    n = 0;
+    p = clean_bit;
+  }
+  __device__ __forceinline__ void fill(int need) {
+#pragma unroll 1
+    while (n < need) {
+      buf |= (uint64_t)next_byte() << (56 - n);
+      n += 8;
+    }
+  }
+  __device__ __forceinline__ uint32_t peek16() { fill(32); return (uint32_t)(buf >> 48); }
+  __device__ __forceinline__ void skip(int k) { buf <<= k; n -= k; p += k; }
+  __device__ __forceinline__ uint32_t bits(int k) {  // _gb (k <= 16)
+    if (k == 0) return 0;
+    fill(32);
+    const uint32_t v = (uint32_t)(buf >> (64 - k));
+    skip(k);
+    return v;
+  }
+  // _hd: the symbol, or -1 for a code the table does not assign
+  __device__ __forceinline__ int sym(const MsTab &T, const uint8_t *payload) {
+    const uint32_t c16 = peek16();
+#pragma unroll 1
+    for (int L = 1; L <= 16; L++) {
+      const int code = (int)(c16 >> (16 - L));
+      if (code <= T.maxcode[L]) {
+        skip(L);
+        return payload[T.vals + T.valptr[L] + code - T.mincode[L]];
+      }
+    }
+    return -1;
+  }
+};
+
+// Restart-interval cursor: the clean offset and raw position just after the
+// next RSTn of the scan (restarts[] of destuff_scan, found incrementally).
+struct MsRst {
+  int raw;       // raw position to search from
+  uint32_t clean;  // clean bytes before `raw`
+  __device__ __forceinline__ bool next(const uint8_t *d, int end, int &raw_after, uint32_t &clean_at) {
+#pragma unroll 1
+    while (raw < end) {
+      const uint32_t b = d[raw];
+      if (b != 0xFF) { raw++; clean++; continue; }
+      if (raw + 1 >= end) return false;
+      const uint32_t m = d[raw + 1];
+      if (m == 0x00) { raw += 2; clean++; continue; }
+      if (m >= 0xD0 && m <= 0xD7) {
+        raw += 2;
+        raw_after = raw;
+        clean_at = clean;
+        return true;
+      }
+      return false;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ bool ms_store(int16_t *c, int v) {
+  *c = (int16_t)v;
+  return v >= -32768 && v <= 32767;
+}
+
+// One scan, one thread (decode_scan_baseline / _dc_first / _dc_refine /
+// _ac_first / _ac_refine).  Returns the status; errp = the clean bit position
+// of the failing symbol (status 1).
+__device__ int ms_decode_scan(const DecodeHead &H, const MsScan &sc, const MsTab *tabs,
+                              const uint8_t *payload, int16_t *coef, bool progressive,
+                              uint32_t &errp, int &range_bad) {
+  MsReader r;
+  r.raw = payload;
+  r.rend = sc.end;
+  r.anchor(sc.start, 0);
+  MsRst rc{sc.start, 0};
+  int nrst_used = 0;
+  const int ns = sc.ns;
+  // _scan_units (codec.py:333-349): one component steps over its true block
+  // grid, an interleaved scan over the frame's MCUs with each component's
+  // sampling factors
+  int gx = H.gx, gy = H.gy;
+  int hh[3] = {1, 1, 1}, vv[3] = {1, 1, 1};
+  if (ns == 1) {
+    gx = H.bw[sc.comp[0]];
+    gy = H.bh[sc.comp[0]];
+  } else {
+    for (int s = 0; s < ns && s < 3; s++) { hh[s] = H.comp_hv[sc.comp[s]] >> 4; vv[s] = H.comp_hv[sc.comp[s]] & 15; }
+  }
+  int32_t pred[3] = {0, 0, 0};
+  int eobrun = 0;
+  const int ri = sc.ri;
+  const bool is_dc = progressive && sc.ss == 0;
+  const int al = sc.al, ss = sc.ss, se = sc.se;
+  const int p1 = 1 << al, m1 = -(1 << al);
+  int unit = 0;
+  auto restart = [&]() -> bool {  // at an interval boundary: jump to the next RSTn (status 3 if none)
+    int ra;
+    uint32_t cl;
+    if (!rc.next(payload, sc.end, ra, cl)) return false;
+    nrst_used++;
+    r.anchor(ra, 8u * cl);
+    pred[0] = pred[1] = pred[2] = 0;
+    eobrun = 0;
+    return true;
+  };
+  for (int my = 0; my < gy; my++) {
+    for (int mx = 0; mx < gx; mx++, unit++) {
+      if (ri > 0 && unit > 0 && unit % ri == 0 && !restart()) return 3;
+      if (!progressive || is_dc) {
+        // MCU of blocks: baseline (DC + AC) or progressive DC
+        for (int s = 0; s < ns; s++) {
+          const int c = sc.comp[s];
+          const int pitch = H.coef_pitch[c];
+          int16_t *base = coef + H.coef_off[c];
+          for (int by = 0; by < vv[s]; by++)
+            for (int bx = 0; bx < hh[s]; bx++) {
+              int16_t *blk = base + ((uint64_t)(my * vv[s] + by) * pitch + (mx * hh[s] + bx)) * 64;
+              if (progressive && sc.ah != 0) {  // DC refine: one bit
+                if (r.bits(1)) range_bad |= !ms_store(blk, blk[0] | p1);
+                continue;
+              }
+              const uint32_t pstart = r.p;
+              const int t = r.sym(tabs[sc.dt[s]], payload);
+              if (t < 0 || t > 15) { errp = pstart; return 1; }
+              const uint32_t v = r.bits(t);
+              pred[s] += extend_bits(v, t);
+              if (progressive) {  // DC first
+                range_bad |= !ms_store(blk, pred[s] * p1);
+                continue;
+              }
+              range_bad |= !ms_store(blk, pred[s]);
+              for (int k = 1; k < 64;) {  // decode_kernels.py:155-177
+                const uint32_t q0 = r.p;
+                const int rs = r.sym(tabs[sc.at[s]], payload);
+                if (rs < 0) { errp = q0; return 1; }
+                const int run = rs >> 4, sz = rs & 15;
+                if (sz == 0) {
+                  if (run == 15) { k += 16; continue; }
+                  break;
+                }
+                k += run;
+                if (k > 63) { errp = q0; return 1; }
+                range_bad |= !ms_store(blk + c_zz[k], extend_bits(r.bits(sz), sz));
+                k++;
+              }
+            }
+        }
+        continue;
+      }
+      // progressive AC, one component, one block per unit
+      const int c = sc.comp[0];
+      int16_t *blk = coef + H.coef_off[c] + ((uint64_t)my * H.coef_pitch[c] + mx) * 64;
+      const MsTab &T = tabs[sc.at[0]];
+      if (sc.ah == 0) {  // AC first (decode_kernels.py:259-309)
+        if (eobrun > 0) { eobrun--; continue; }
+        for (int k = ss; k <= se;) {
+          const uint32_t q0 = r.p;
+          const int rs = r.sym(T, payload);
+          if (rs < 0) { errp = q0; return 1; }
+          const int run = rs >> 4, sz = rs & 15;
+          if (sz == 0) {
+            if (run != 15) {
+              eobrun = (1 << run) - 1 + (int)r.bits(run);
+              break;
+            }
+            k += 16;
+            continue;
+          }
+          k += run;
+          if (k > se) { errp = q0; return 1; }
+          range_bad |= !ms_store(blk + c_zz[k], extend_bits(r.bits(sz), sz) * p1);
+          k++;
+        }
+        continue;
+      }
+      // AC refine (decode_kernels.py:312-385)
+      int k = ss;
+      if (eobrun == 0) {
+        while (k <= se) {
+          const uint32_t q0 = r.p;
+          const int rs = r.sym(T, payload);
+          if (rs < 0) { errp = q0; return 1; }
+          int run = rs >> 4;
+          const int sz = rs & 15;
+          int newval = 0;
+          if (sz == 0) {
+            if (run != 15) {
+              eobrun = (1 << run) + (int)r.bits(run);
+              break;
+            }
+          } else {
+            newval = r.bits(1) ? p1 : m1;
+          }
+          while (k <= se) {
+            int16_t *cp = blk + c_zz[k];
+            const int cur = *cp;
+            if (cur != 0) {
+              if (r.bits(1) && (cur & p1) == 0) range_bad |= !ms_store(cp, cur + (cur >= 0 ? p1 : m1));
+            } else {
+              if (run == 0) break;
+              run--;
+            }
+            k++;
+          }
+          if (newval != 0 && k <= se) range_bad |= !ms_store(blk + c_zz[k], newval);
+          k++;
+        }
+      }
+      if (eobrun > 0) {
+        while (k <= se) {
+          int16_t *cp = blk + c_zz[k];
+          const int cur = *cp;
+          if (cur != 0 && r.bits(1) && (cur & p1) == 0) range_bad |= !ms_store(cp, cur + (cur >= 0 ? p1 : m1));
+          k++;
+        }
+        eobrun--;
+      }
+    }
+  }
+  (void)nrst_used;
+  // _check_consumed: bits consumed beyond the clean length -> truncated
+  uint32_t clean_len = 0;
+  {
+    MsRst cnt{sc.start, 0};
+    int ra;
+    uint32_t cl;
+    while (cnt.next(payload, sc.end, ra, cl)) {}
+    // cnt stopped at the end of the clean data: clean bytes counted so far
+    clean_len = cnt.clean;
+  }
+  if (r.p > 8u * clean_len) return 4;
+  return 0;
+}
+
+// Parse of every scan of a multi-scan stream (thread 0; parse_stream,
+// codec.py:124-251 -- the stream passed k_prep's marker walk already) plus
+// each scan's pre-decode checks in the reference's order (_scan_units,
+// _destuff, the progressive scan rules, _huff_lut / _lut_stack,
+// codec.py:333-399) and the dependency wave of every scan.
+__device__ void ms_parse(const DecodeHead &H, const uint8_t *d, int n, MsScan *scans, MsTab *tabs,
+                         int &nscan_out, int &nlevel_out) {
+  int huff_pos[2][16];
+  for (int i = 0; i < 16; i++) huff_pos[0][i] = huff_pos[1][i] = -1;
+  int tab_pos[kMsMaxTabs];
+  int ntab = 0, nscan = 0, ri = 0, pos = 2;
+  auto tab_of = [&](int tpos) -> int {  // canonical decoder of the DHT definition at tpos
+    if (tpos < 0) return -1;
+    for (int t = 0; t < ntab; t++)
+      if (tab_pos[t] == tpos) return t;
+    if (ntab >= kMsMaxTabs) return -2;
+    const int t = ntab++;
+    tab_pos[t] = tpos;
+    MsTab &T = tabs[t];
+    int code = 0, vi = 0;
+    T.pad = 0;
+    for (int L = 1; L <= 16; L++) {
+      const int cnt = d[tpos + L - 1];
+      T.mincode[L] = code;
+      T.valptr[L] = (int16_t)vi;
+      if (cnt && code + cnt > (1 << L)) T.pad = 1;  // code overflow (codec.py:287-288)
+      code += cnt;
+      vi += cnt;
+      T.maxcode[L] = cnt ? code - 1 : -1;
+      code <<= 1;
+    }
+    T.maxcode[17] = 0x7FFFFFFF;
+    T.vals = tpos + 16;
+    return t;
+  };
+  while (pos < n && nscan <= kMsMaxScans) {
+    if (d[pos] != 0xFF) break;
+    while (pos < n && d[pos] == 0xFF) pos++;
+    if (pos >= n) break;
+    const int marker = d[pos++];
+    if (marker == 0xD9) break;
+    if (marker == 0x01 || (marker >= 0xD0 && marker <= 0xD7)) continue;
+    if (pos + 2 > n) break;
+    const int seglen = (d[pos] << 8) | d[pos + 1];
+    const int body = pos + 2, end = pos + seglen;
+    if (marker == 0xC4) {
+      int p = body;
+      while (p + 17 <= end) {
+        const int tc = d[p] >> 4, th = d[p] & 15;
+        int tot = 0;
+        for (int i = 0; i < 16; i++) tot += d[p + 1 + i];
+        if (tc < 2) huff_pos[tc][th] = p + 1;
+        p += 17 + tot;
+      }
+    } else if (marker == 0xDD) {
+      ri = (d[body] << 8) | d[body + 1];
+    } else if (marker == 0xDA) {
+      if (nscan >= kMsMaxScans) { nscan++; break; }
+      MsScan &S = scans[nscan];
+      const int ns = d[body];
+      int p = body + 1;
+      S.ns = (uint8_t)ns;
+      for (int s = 0; s < ns && s < 3; s++) {
+        const int cs = d[p], td = d[p + 1] >> 4, ta = d[p + 1] & 15;
+        int idx = 0;
+        for (int i = 0; i < H.ncomp; i++)
+          if (H.comp_id[i] == cs) { idx = i; break; }
+        S.comp[s] = (uint8_t)idx;
+        S.dpos[s] = huff_pos[0][td];
+        S.apos[s] = huff_pos[1][ta];
+        S.dt[s] = S.at[s] = -1;
+        p += 2;
+      }
+      p = body + 1 + 2 * ns;
+      S.ss = d[p]; S.se = d[p + 1]; S.ah = d[p + 2] >> 4; S.al = d[p + 2] & 15;
+      S.ri = ri;
+      S.start = end;
+      // _entropy_end (codec.py:109-121)
+      int q = end;
+      while (true) {
+        while (q < n && d[q] != 0xFF) q++;
+        if (q >= n || q + 1 >= n) { q = n; break; }
+        const int m = d[q + 1];
+        if (m == 0x00 || (m >= 0xD0 && m <= 0xD7) || m == 0xFF) { q += m != 0xFF ? 2 : 1; continue; }
+        break;
+      }
+      S.end = q;
+      S.err = 0; S.reason = 0; S.off = -1; S.status = 0; S.errp = 0;
+      nscan++;
+      pos = q;
+      continue;
+    }
+    pos = end;
+  }
+  // pre-decode checks and waves
+  int nlevel = 0;
+  const int nsc = min(nscan, kMsMaxScans);
+  for (int j = 0; j < nsc; j++) {
+    MsScan &S = scans[j];
+    auto fail = [&](int st, int reason, int off) {
+      if (!S.err) { S.err = st; S.reason = reason; S.off = off; }
+    };
+    if (S.ns != 1 && S.ns != H.ncomp) {
+      fail(ESSL_ST_MALFORMED, R_PARTIAL_INTERLEAVE, -1);
+    } else {
+      // _destuff: restart markers of the scan
+      int gx = H.gx, gy = H.gy;
+      if (S.ns == 1) { gx = H.bw[S.comp[0]]; gy = H.bh[S.comp[0]]; }
+      const int max_r = S.ri ? (gx * gy) / S.ri : 0;
+      MsRst rc{S.start, 0};
+      int ra, nr = 0;
+      uint32_t cl;
+      while (rc.next(d, S.end, ra, cl)) nr++;
+      if (S.ri == 0 && nr > 0) fail(ESSL_ST_MALFORMED, R_RST_NO_DRI, S.start);
+      else if (nr > max_r + 2) fail(ESSL_ST_MALFORMED, R_TOO_MANY_RST, S.start);
+      auto need = [&](int tpos) -> int8_t {  // _huff_lut of a table the scan uses
+        const int t = tab_of(tpos);
+        if (t == -2) fail(ESSL_ST_UNSUPPORTED, R_TOO_MANY_SCANS, -1);
+        else if (t < 0) fail(ESSL_ST_HUFFTABLE, R_HUFF_UNDEFINED, -1);
+        else if (tabs[t].pad) fail(ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1);
+        return (int8_t)t;
+      };
+      if (!H.progressive) {
+        for (int s = 0; s < S.ns; s++) S.dt[s] = need(S.dpos[s]);
+        for (int s = 0; s < S.ns; s++) S.at[s] = need(S.apos[s]);
+      } else if (S.ss == 0) {
+        if (S.se != 0) fail(ESSL_ST_MALFORMED, R_PROG_DC_SE, -1);
+        else if (S.ah == 0)
+          for (int s = 0; s < S.ns; s++) S.dt[s] = need(S.dpos[s]);
+      } else {
+        if (S.ns != 1) fail(ESSL_ST_MALFORMED, R_PROG_AC_NCOMP, -1);
+        else S.at[0] = need(S.apos[0]);
+      }
+    }
+    // wave: after every earlier scan sharing a component and a coefficient
+    int lv = 0;
+    const int lo = H.progressive ? S.ss : 0, hi = H.progressive ? S.se : 63;
+    for (int i = 0; i < j; i++) {
+      const MsScan &O = scans[i];
+      const int olo = H.progressive ? O.ss : 0, ohi = H.progressive ? O.se : 63;
+      bool share = false;
+      for (int a = 0; a < S.ns && a < 3; a++)
+        for (int b = 0; b < O.ns && b < 3; b++) share |= S.comp[a] == O.comp[b];
+      if (share && olo <= hi && lo <= ohi) lv = max(lv, O.level + 1);
+    }
+    S.level = lv;
+    nlevel = max(nlevel, lv + 1);
+    if (S.err) {  // the reference stops at the first failing scan
+      nscan_out = j + 1;
+      nlevel_out = nlevel;
+      return;
+    }
+  }
+  nscan_out = nscan > kMsMaxScans ? -1 : nsc;
+  nlevel_out = nlevel;
+}
+
+// The multi-scan decode of one image by its k_entropy CTA.
+__device__ void multiscan_body(const DecodeParams &P, EntSmem &S, int img, int lane) {
+  DecodeHead &H = S.h;
+  MsScan *scans = reinterpret_cast<MsScan *>(&S.tab[0][0]);
+  MsTab *tabs = reinterpret_cast<MsTab *>(reinterpret_cast<uint8_t *>(&S.tab[0][0]) +
+                                          sizeof(MsScan) * kMsMaxScans);
+  const essl_sample smp = P.samples[img];
+  const uint8_t *d = P.blob + smp.offset;
+  const int n = (int)smp.length;
+  int16_t *coef = P.s.coef;
+  // every coefficient starts at zero (_alloc_coefs)
+  uint64_t total = 0;
+  for (int c = 0; c < H.ncomp; c++)
+    total += (uint64_t)H.gy * (H.comp_hv[c] & 15) * H.coef_pitch[c] * 64;
+  int4 *z = reinterpret_cast<int4 *>(coef + H.coef_base);
+  for (uint64_t i = lane; i < total / 8; i += kLanes) z[i] = make_int4(0, 0, 0, 0);
+  if (lane == 0) {
+    int ns, nl;
+    ms_parse(H, d, n, scans, tabs, ns, nl);
+    S.ms_nscan = ns;
+    S.ms_nlevel = nl;
+    S.ms_range = 0;
+  }
+  __syncthreads();
+  const int nscan = S.ms_nscan;
+  if (nscan < 0) {
+    if (lane == 0) ent_status(S, ESSL_ST_UNSUPPORTED, R_TOO_MANY_SCANS, -1);
+    return;
+  }
+  // waves of independent scans, one lane per scan
+  for (int w = 0; w < S.ms_nlevel; w++) {
+    int rank = 0;
+    for (int j = 0; j < nscan; j++) {
+      MsScan &sc = scans[j];
+      if (sc.level != w || sc.err) continue;
+      if ((rank++ % kLanes) != lane) continue;
+      uint32_t errp = 0;
+      int bad = 0;
+      sc.status = ms_decode_scan(H, sc, tabs, d, coef, H.progressive, errp, bad);
+      sc.errp = (int32_t)errp;
+      if (bad) S.ms_range = 1;
+    }
+    __syncthreads();
+  }
+  if (lane == 0) {  // the first failing scan in file order (_check_consumed, codec.py:323-330)
+    for (int j = 0; j < nscan; j++) {
+      const MsScan &sc = scans[j];
+      if (sc.err) {
+        ent_status(S, sc.err, sc.reason, sc.off);
+        break;
+      }
+      if (sc.status == 1) {
+        const uint32_t vpos = (sc.errp + 25u + 7u) / 8u;
+        ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, sc.start + (int)min(vpos, (uint32_t)(sc.end - sc.start)));
+        break;
+      }
+      if (sc.status == 3) { ent_status(S, ESSL_ST_MISSING_RST, 0, sc.start); break; }
+      if (sc.status == 4) { ent_status(S, ESSL_ST_TRUNCATED, 0, sc.end); break; }
+    }
+    if (S.ms_range) S.coef_range = 1;
+    S.fmt = 0;
+  }
+}
+
 // Decode of one image by the CTA: restart intervals, serial mode, or the
 // checkpoint-merge parallel decode; SH: the clean stream is staged in shared
 // memory.
@@ -1877,7 +2448,9 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
   WriteOut wo;
   wo.range = 0;
 #define PHASE(i) do { if (lane == 0) S.t_ph[i] = clock64(); } while (0)
-  if (S.status == 0 && H.scan_ri > 0) {
+  if (S.status == 0 && H.multiscan) {
+    multiscan_body(P, S, img, lane);
+  } else if (S.status == 0 && H.scan_ri > 0) {
     // DRI: restart intervals decode independently from exact entry states
     // (decode_kernels.py:130-138); lanes take intervals round-robin.
     const uint32_t ri = H.scan_ri;
@@ -2188,7 +2761,9 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
           info->plane_pitch[c] = H.wbw[c] * 8;
           info->wby0[c] = H.wby0[c]; info->wbx0[c] = H.wbx0[c];
           info->wbh[c] = H.wbh[c]; info->wbw[c] = H.wbw[c];
-          info->coef_off[c] = H.coef_off[c];
+          info->coef_off[c] = H.coef_off[c] + ((uint64_t)H.wby0[c] * H.coef_pitch[c] + H.wbx0[c]) * 64 *
+                                                 (H.multiscan ? 1 : 0);
+          info->coef_pitch[c] = H.coef_pitch[c];
         }
       }
     }
@@ -2204,7 +2779,9 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
     info->dbg[9] = mu | ((long long)(S.status == 0 && S.fmt == 0) << 32);
     if (P.results) {
       essl_result r;
-      r.status = S.status; r.reason = S.reason; r.offset = S.offset;
+      // (status 0: reason 1 flags the full-decode path of a multi-scan stream,
+      // DecodeStats.fallback_full, codec.py:461-469)
+      r.status = S.status; r.reason = S.status == 0 ? (H.multiscan ? 1 : 0) : S.reason; r.offset = S.offset;
       r.mcus_entropy_decoded = S.status == 0 ? info->mcus_entropy : 0;
       r.mcus_reconstructed = S.status == 0 ? info->mcus_recon : 0;
       r.width = info->width; r.height = info->height; r.ncomp = info->ncomp;
@@ -2230,7 +2807,7 @@ constexpr int kIdctCtas = 2;  // fewer, longer CTAs at 48 registers: +3% over 8 
 __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, int c, int byr,
                               int bxr, int32_t *blk, const uint8_t *zz, const int32_t *dq) {
   const int j = threadIdx.x & 7;
-  const int16_t *cf = sc.coef + I.coef_off[c] + ((uint64_t)byr * I.wbw[c] + bxr) * 64;
+  const int16_t *cf = sc.coef + I.coef_off[c] + ((uint64_t)byr * I.coef_pitch[c] + bxr) * 64;
 #pragma unroll
   for (int r = 0; r < 8; r++) blk[8 * j + r] = 0;
   __syncwarp();

@@ -28,7 +28,8 @@ enum Reason : int32_t {
   R_NO_IMAGE = 15, R_RST_NO_DRI = 16, R_TOO_MANY_RST = 17,
   R_PROGRESSIVE = 18, R_MULTI_SCAN = 19, R_HUFF_UNDEFINED = 20,
   R_HUFF_OVERFLOW = 21, R_HUFF_TOO_MANY = 22, R_SEGMENT = 23,
-  R_COEF_RANGE = 24, R_SCRATCH = 25,
+  R_COEF_RANGE = 24, R_SCRATCH = 25, R_PROG_DC_SE = 26, R_PROG_AC_NCOMP = 27,
+  R_PARTIAL_INTERLEAVE = 28, R_TOO_MANY_SCANS = 29,
 };
 
 // Per-image decode products consumed by the pixel kernels.  Written by
@@ -42,7 +43,8 @@ struct ImgInfo {
   int32_t wby0[3], wbx0[3], wbh[3], wbw[3];
   int32_t plane_pitch[3];
   uint64_t plane_off[3];  // bytes into Scratch::plane
-  uint64_t coef_off[3];   // int16 elements into Scratch::coef
+  uint64_t coef_off[3];   // int16 elements into Scratch::coef (the window's first block)
+  int32_t coef_pitch[3];  // blocks per coefficient-array row
   int32_t mcus_entropy, mcus_recon;
   int32_t rx, ry, rw, rh, flip;
   int32_t fmt;  // 0: coefficient window (int16); 1: per-block tables into the unit lists

@@ -32,8 +32,8 @@ class ConfigError(CroploadError):
 
 
 class UnsupportedStreamError(DecodeError):
-    """Progressive / multi-scan streams: the reference falls back to a full CPU
-    decode (codec.py:461-469); this GPU-only path has no CPU fallback."""
+    """Streams outside the GPU decoder's limits (hostile streams only:
+    coefficients outside int16, more than 64 scans / 24 Huffman tables)."""
 
 
 ST_OK, ST_CORRUPT_HUFFMAN, ST_MISSING_RST, ST_TRUNCATED = 0, 1, 3, 4
@@ -67,6 +67,10 @@ _REASONS = {
     23: ("marker segment shorter than its fields", True),
     24: ("coefficient out of int16 range", False),
     25: ("image exceeds the context scratch capacity", False),
+    26: ("progressive DC scan with Se != 0", False),
+    27: ("progressive AC scan must be single-component", False),
+    28: ("partially interleaved scans are not supported", False),
+    29: ("too many scans or Huffman tables for the GPU decoder", False),
 }
 
 

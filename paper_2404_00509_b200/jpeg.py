@@ -31,8 +31,9 @@ class CropRect:
 
 @dataclass
 class DecodeStats:
-    """Work counters (codec.py:59-71).  fallback_full is always False: the
-    GPU decoder has no full-decode fallback (unsupported streams raise)."""
+    """Work counters (codec.py:59-71).  fallback_full: a multi-scan
+    (progressive) stream took the full decode of every scan, as in the
+    reference (codec.py:461-469) -- on the GPU too."""
 
     mcus_entropy_decoded: int
     mcus_reconstructed: int
@@ -105,7 +106,7 @@ def decode_crops(items: list[tuple[bytes, CropRect]], device=None):
                                rect=r, dims=(int(rh[i, 5]), int(rh[i, 6])))
         o = int(out_off[i])
         rgb = host[o:o + r.w * r.h * 3].reshape(r.h, r.w, 3).copy()
-        outs.append((rgb, DecodeStats(int(rh[i, 3]), int(rh[i, 4]), False)))
+        outs.append((rgb, DecodeStats(int(rh[i, 3]), int(rh[i, 4]), bool(rh[i, 1] == 1))))
     return outs
 
 
@@ -115,7 +116,8 @@ def decode_crop(data: bytes, rect: CropRect, device=None):
 
 
 def decode_full(data: bytes, device=None):
-    """Whole-image decode (codec.py:434-445) == full-rect crop decode."""
+    """Whole-image decode (codec.py:434-445) == full-rect crop decode (its
+    stats never flag the fallback, as the reference's decode_full)."""
     dims = peek_dims(bytes(data))
     rect = CropRect(0, 0, dims[0], dims[1]) if dims else CropRect(0, 0, 1, 1)
     if dims is None or dims[0] == 0 or dims[1] == 0:
@@ -125,4 +127,5 @@ def decode_full(data: bytes, device=None):
         except ValueError as exc:
             raise DecodeError(str(exc)) from exc
         raise DecodeError("no image data found")
-    return decode_crops([(bytes(data), rect)], device)[0]
+    rgb, st = decode_crops([(bytes(data), rect)], device)[0]
+    return rgb, DecodeStats(st.mcus_entropy_decoded, st.mcus_reconstructed, False)

@@ -117,9 +117,18 @@ def test_stream_errors_match_reference(E, golden, name, mode):
     assert str(e.value) == ent["msg"]
 
 
-def test_progressive_unsupported(E):
-    with pytest.raises(E.UnsupportedStreamError):
-        E.decode_full(stream_bytes("pil_progressive"))
+def test_progressive_decodes_like_reference(E, golden, mode):
+    """Multi-scan streams take the reference's full-decode path on the GPU
+    (codec.py:461-469): crops and stats (fallback_full set) == the goldens."""
+    ent = golden["streams"]["pil_progressive"]
+    data = stream_bytes("pil_progressive")
+    full, st = E.decode_full(data)
+    assert sha(full) == ent["full"]["sha"]
+    assert [st.mcus_entropy_decoded, st.mcus_reconstructed, st.fallback_full] == ent["full"]["stats"]
+    items = [(data, E.CropRect(*c["rect"])) for c in ent["crops"]]
+    for (crop, cs), c in zip(E.decode_crops(items), ent["crops"]):
+        assert sha(crop) == c["sha"], c["rect"]
+        assert [cs.mcus_entropy_decoded, cs.mcus_reconstructed, cs.fallback_full] == c["stats"]
 
 
 def test_truncation_every_cut(E, oracle):
