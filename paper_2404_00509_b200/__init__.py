@@ -9,6 +9,8 @@ libessl (include/essl.h).  No CPU fallback.
 from . import imgops  # noqa: F401
 from .container import (ContainerHandle, RECORD_DTYPE, build_synthetic, encode_jpeg,
                         open_container, synth_image, verify_crcs, write_container)
+from .builder import (BuildSpec, BuildSummary, build_container, fit_to_resolution,
+                      scan_source_tree)
 from .errors import (ConfigError, CorruptionError, CroploadError, DecodeError, FormatError,
                      UnsupportedStreamError)
 from .jpeg import CropRect, DecodeStats, decode_crop, decode_crops, decode_full
