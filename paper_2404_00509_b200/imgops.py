@@ -36,7 +36,10 @@ def _to_dev(a, eng):
     import torch
     if isinstance(a, torch.Tensor):
         return a.to(eng.device).contiguous(), False
-    return torch.from_numpy(np.ascontiguousarray(a, np.uint8)).to(eng.device), True
+    a = np.ascontiguousarray(a, np.uint8)
+    if not a.flags.writeable:  # (read-only views, e.g. Pillow buffers: copy before wrapping)
+        a = a.copy()
+    return torch.from_numpy(a).to(eng.device), True
 
 
 def resize_bilinear(region, out_h: int, out_w: int | None = None, flip: bool = False,
