@@ -26,6 +26,8 @@ def reduce_timing(values, device=None) -> tuple[float, float, float, float]:
     when no process group is initialised)."""
     import torch
     import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_backend() == "gloo":
+        device = "cpu"  # (gloo reduces host tensors)
     v = torch.tensor([float(x) for x in values], dtype=torch.float64, device=device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         mx = v.clone()

@@ -85,3 +85,78 @@ def test_ddp_shards_and_reduction_gloo():
         for i, rect in zip(gathered[r], all_rects[r]):
             assert single[i] == rect
     assert red == (11.0, 300.0, 20.0, 21.0)
+
+
+def _gpu_worker(rank, ws, port, path, q):
+    """One DDP rank (own process, own CUDA context on the one GPU): its shard
+    of an epoch through the GPU loader, digests per dataset index, then the
+    bench's reporting reduction over gloo."""
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import hashlib
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import paper_2404_00509_b200 as E
+    from paper_2404_00509_b200.ddp import reduce_timing
+    torch.cuda.set_device(0)
+    cfg = E.LoaderConfig(data=path, batch_size=8, res=96, mask_ratio=0.75, rank=rank,
+                         world_size=ws, shard_mode="stride", out_dtype="bfloat16")
+    out, nb = {}, 0
+    with E.Loader(cfg) as loader:
+        for b in loader.epoch(4):
+            nb += 1
+            for s in range(len(b)):
+                out[int(b.indices[s])] = (
+                    hashlib.sha256(b.pixels[s].cpu().view(torch.int16).numpy().tobytes()).hexdigest(),
+                    b.mask[s].cpu().tolist())
+    red = reduce_timing([1.0 + rank, float(len(out)), 0.0, 0.0])
+    gathered = [None] * ws
+    dist.all_gather_object(gathered, out)
+    if rank == 0:
+        q.put((gathered, red, nb))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_gpu_equal_single_process(tmp_path):
+    """2 DDP ranks (gloo for the reporting collective, no collective on the
+    data path) decode disjoint shards whose union equals the single-process
+    epoch, sample for sample."""
+    sys.path.insert(0, str(ROOT))
+    import hashlib
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_00509_b200 as E
+    path = str(tmp_path / "d.essl")
+    E.build_synthetic(path, 37, 256, 95, seed=8)
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, ws, port, path, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    gathered, red, nb = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    union = {}
+    for g in gathered:
+        assert not set(g) & set(union)  # disjoint shards
+        union.update(g)
+    cfg = E.LoaderConfig(data=path, batch_size=8, res=96, mask_ratio=0.75, out_dtype="bfloat16")
+    single = {}
+    with E.Loader(cfg) as loader:
+        for b in loader.epoch(4):
+            for s in range(len(b)):
+                single[int(b.indices[s])] = (
+                    hashlib.sha256(b.pixels[s].cpu().view(torch.int16).numpy().tobytes()).hexdigest(),
+                    b.mask[s].cpu().tolist())
+    assert union == single
+    assert red == (2.0, 37.0, 0.0, 0.0)
