@@ -31,6 +31,7 @@
 // k_idct dequantises + inverse-transforms the crop-window blocks with all
 // threads of the GPU (8 lanes per block).
 #include <cstdint>
+#include <type_traits>
 
 #include "essl_common.cuh"
 
@@ -468,6 +469,99 @@ struct Reader {
   }
 };
 
+// Phase-1 / continuation reader (run_path, the hot loops): a 32-word window
+// [lo, lo + 32) of the clean stream per lane in a shared-memory ring, filled
+// by cp.async a quarter (8 words) at a time, and three words of it in
+// registers: w0 (the word holding bit p), w1, w2.  Per unit: one funnel shift
+// for the 32-bit lookahead, and on crossing a word boundary a shift of the
+// register words and one LDS of the next (the LDS feeds w2, read two words
+// later, off the decode chain).  Ring maintenance runs once per group of
+// kGroup units (top_up, the same step for every lane of the warp): quarters
+// whose words are all in registers are refetched kRingWords ahead, and the
+// lane waits only for the quarters the next group can reach (a group moves p
+// by < 8 words; units are at most 31 bits).
+constexpr int kRingWords = 32;
+constexpr int kGroup = 16;
+
+struct RingReader {
+  const uint32_t *w;  // global words
+  uint32_t cpad;      // first all-0xFF 16-byte chunk
+  uint32_t rs;        // this lane's ring (shared-window address)
+  uint32_t w0, w1, w2;
+  uint32_t o, q, p;   // bit offset in w0, word index of w0, bit position (32 q + o)
+  uint32_t lo, pend;  // ring window start (words, multiple of 8); quarters in flight
+  __device__ __forceinline__ uint32_t ld(uint32_t i) const { return lds_u32(rs + ((i & (kRingWords - 1)) << 2)); }
+  // quarter j = words [8j, 8j + 8) = 16-byte chunks 2j, 2j + 1 (clamped to the
+  // all-0xFF padding chunk past the data), one commit group
+  __device__ __forceinline__ void fetch(uint32_t j, bool pred) const {
+    const uint32_t dst = rs + (((8u * j) & (kRingWords - 1)) << 2);
+    const uint32_t *s0 = w + 4 * (size_t)min(2u * j, cpad);
+    const uint32_t *s1 = w + 4 * (size_t)min(2u * j + 1u, cpad);
+    asm volatile(
+        "{ .reg .pred q; setp.ne.u32 q, %0, 0;\n"
+        "  @q cp.async.cg.shared.global [%1], [%2], 16;\n"
+        "  @q cp.async.cg.shared.global [%3], [%4], 16;\n"
+        "  @q cp.async.commit_group; }" ::"r"((uint32_t)pred),
+        "r"(dst), "l"(s0), "r"(dst + 16), "l"(s1)
+        : "memory");
+  }
+  __device__ __forceinline__ void init(uint32_t pos) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // this lane's copies in flight target the ring
+    q = pos >> 5;
+    o = pos & 31;
+    p = pos;
+    lo = q & ~7u;
+#pragma unroll
+    for (uint32_t j = 0; j < kRingWords / 8; j++) fetch(lo / 8 + j, true);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    pend = 0;
+    w0 = ld(q);
+    w1 = ld(q + 1);
+    w2 = ld(q + 2);
+  }
+  __device__ __forceinline__ void top_up() {
+    // quarters below q + 3 are in registers or consumed: refetch them ahead
+    // (a group advances q by at most kGroup words)
+    const bool f0 = lo + 8 <= q + 3;
+    fetch(lo / 8 + kRingWords / 8, f0);
+    lo += f0 ? 8u : 0u;
+    pend += f0 ? 1u : 0u;
+#pragma unroll 1
+    while (lo + 8 <= q + 3) {
+      fetch(lo / 8 + kRingWords / 8, true);
+      lo += 8;
+      pend++;
+    }
+    // the next group loads words up to q + 2 + kGroup: the newest pending
+    // quarters starting beyond that may stay in flight, the others must be
+    // complete
+    const uint32_t top = lo + kRingWords;  // quarter starts: top - 8, top - 16, ...
+    const uint32_t reach = q + 2 + kGroup;
+    uint32_t allow = 0;
+    if (pend >= 1 && top - 8 > reach) allow = 1;
+    if (pend >= 2 && top - 16 > reach) allow = 2;
+    if (allow < pend) {
+      if (allow == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      else if (allow == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 2;" ::: "memory");
+      pend = allow;
+    }
+    static_assert(kGroup <= 24, "the ring must hold a group's reach");
+  }
+  __device__ __forceinline__ uint32_t hi() const { return __funnelshift_l(w1, w0, o); }
+  __device__ __forceinline__ void skip(int bits) {
+    o += bits;
+    p += bits;
+    if (o >= 32) {
+      o -= 32;
+      q++;
+      w0 = w1;
+      w1 = w2;
+      w2 = ld(q + 2);
+    }
+  }
+};
+
 // Long codes of a table whose long-code prefixes overflow the sub-tables
 // (hostile DHT only): canonical maxcode walk, same symbols as codec.py:272-295.
 // Long codes (rare: a divergent branch): second-level table, or the canonical
@@ -547,6 +641,12 @@ struct EntCtx {
     r.cpad = cpad;
     r.init(pos);
   }
+  __device__ __forceinline__ void reader(RingReader &r, uint32_t pos) const {
+    r.w = words;
+    r.rs = ring_s;
+    r.cpad = cpad;
+    r.init(pos);
+  }
 };
 
 // One decoded unit's fields; bad <=> decode_kernels.py would return status 1
@@ -559,9 +659,11 @@ struct EntCtx {
   const bool bad = tot == 0 || (size != 0 && knew > 64)
 
 
-// Magnitude bits of a unit, not yet sign-extended (size 0 -> 0).
+// Magnitude bits of a unit, not yet sign-extended (size 0 -> 0): the
+// `size` bits after the code, (hi << code_len) >> (32 - size) as one funnel
+// shift of (0 : hi << code_len).
 __device__ __forceinline__ uint32_t unit_raw(uint32_t hi, int tot, int size) {
-  return (uint32_t)((uint64_t)(hi << (tot - size)) >> (32 - size));
+  return __funnelshift_l(hi << (tot - size), 0u, size);
 }
 
 // JPEG sign extension of `size` magnitude bits (decode_kernels.py:101-108).
@@ -570,15 +672,18 @@ __device__ __forceinline__ int extend_raw(uint32_t raw, int size) {
   return raw < half ? (int)raw - (int)((1u << size) - 1u) : (int)raw;
 }
 
-// Unit list entry: is_dc | raw magnitude bits << 1 | size << 16 | zig-zag
-// index << 20.  Every unit is stored (EOB / ZRL as a zero at a position the
-// block leaves zero); a DC entry starts a block.  Sign extension and the
-// zig-zag -> natural mapping happen in the consumers (k_idct), off the
-// decode chain.
-__device__ __forceinline__ uint32_t unit_entry(uint32_t raw, int size, int zzk, bool dc) {
-  return (dc ? 1u : 0u) | (raw << 1) | ((uint32_t)size << 16) | ((uint32_t)zzk << 20);
+// Unit list entry: raw magnitude bits | size << 16 | knew << 20, knew = the
+// zig-zag index after the unit (1..127: a DC unit has knew == 1, an AC
+// coefficient sits at zig-zag index knew - 1, EOB / ZRL are zeros stored at
+// min(knew, 64) - 1, a position the block leaves zero).  Every unit is
+// stored; sign extension and the zig-zag -> natural mapping happen in the
+// consumers (k_idct), off the decode chain.
+__device__ __forceinline__ uint32_t unit_entry(uint32_t raw, int size, int knew) {
+  return raw | ((uint32_t)size << 16) | ((uint32_t)knew << 20);
 }
-__device__ __forceinline__ int entry_value(uint32_t e) { return extend_raw((e >> 1) & 0x7FFFu, (e >> 16) & 15); }
+__device__ __forceinline__ int entry_value(uint32_t e) { return extend_raw(e & 0xFFFFu, (e >> 16) & 15); }
+__device__ __forceinline__ int entry_zz(uint32_t e) { return (int)min(e >> 20, 64u) - 1; }
+constexpr uint32_t kEntrySentinel = 1u << 20;  // a DC entry: ends the last block
 
 // Checkpoint: the decoder state at a block start of a lane's path, with the
 // path's unit-list index and block count there.
@@ -614,11 +719,21 @@ struct LaneRec {
 // the list) until the path reaches a checkpoint of a later lane with the same
 // (bit position, block-in-MCU) at a block start -- two decoders in the same
 // state produce the same future -- or errors, or runs off the data.
+// Per-group maintenance (ring reader) and per-unit refill (the global-memory
+// validation reader keeps its 64-bit buffer topped up before every unit).
+__device__ __forceinline__ void top_up_of(Reader<false> &) {}
+__device__ __forceinline__ void top_up_of(RingReader &r) { r.top_up(); }
+__device__ __forceinline__ void refill_of(Reader<false> &r) { r.refill(); }
+__device__ __forceinline__ void refill_of(RingReader &) {}
+
 template <bool CONT, bool SH>
 __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t sbeg, uint32_t send,
                          uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, Ckpt *ck_all,
                          LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
-  Reader<SH> r;
+  // SH: the ring reader (shared-memory window, grouped maintenance); !SH:
+  // plain global reads (validation)
+  using Rd = typename std::conditional<SH, RingReader, Reader<false>>::type;
+  Rd r;
   int k, b;
   uint32_t nblk, nl, nbs, nck = 0, ck_next = p0;
   int be = 0;
@@ -659,45 +774,48 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   };
   if (CONT) seek(r.p);
   int st = 2;
-  uint32_t dbg_units = 0, dbg_guess = 0;
+  uint32_t dbg_guess = 0;
   if (!CONT && p0 < sbeg) {
     // Warm-up [p0, sbeg): decode only, nothing stored.  The path through it
     // is never part of the exact path through this lane's list: the
     // previous lane's continuation starts at sbeg, so it can only merge at
     // a checkpoint at or after sbeg.  Stop at the first block start at or
     // after sbeg and record a checkpoint there, where the list begins.
-    bool stop = false;
+    bool stop = false, done = false;
 #pragma unroll 1
-    while (true) {
-      r.refill();
-      const uint32_t hi = r.hi();
-      uint32_t e = C.lookup_fast<SH>(k, b, hi);
-      int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
-      int knew = k + kinc;
-      if (tot == 0 || (size != 0 && knew > 64)) {
-        if (tot == 0 && e != 0) {
-          e = C.lookup_long(k, b, e, hi);
-          tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
-          knew = k + kinc;
+    while (!done) {
+      top_up_of(r);
+#pragma unroll 1
+      for (int u = 0; u < kGroup; u++) {
+        refill_of(r);
+        const uint32_t hi = r.hi();
+        uint32_t e = C.lookup_fast<SH>(k, b, hi);
+        int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
+        int knew = k + kinc;
+        if (tot == 0 || (size != 0 && knew > 64)) {
+          if (tot == 0 && e != 0) {
+            e = C.lookup_long(k, b, e, hi);
+            tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
+            knew = k + kinc;
+          }
+          if (tot == 0 || (size != 0 && knew > 64)) {  // off the path: re-guess one bit on
+            if (r.p + 8 > C.cbits) { stop = true; done = true; break; }
+            C.reader(r, r.p + 1);
+            dbg_guess++;
+            k = 0;
+            b = 0;
+            nblk = 0;
+            break;  // (a fresh ring: maintenance restarts)
+          }
         }
-        if (tot == 0 || (size != 0 && knew > 64)) {  // off the path: re-guess one bit on
-          if (r.p + 8 > C.cbits) { stop = true; break; }
-          r.init(r.p + 1);
-          dbg_guess++;
-          k = 0;
-          b = 0;
-          nblk = 0;
-          continue;
-        }
+        r.skip(tot);
+        const bool bend = knew >= 64;
+        const int bn = b + 1 == C.bpm ? 0 : b + 1;
+        k = bend ? 0 : knew;
+        b = bend ? bn : b;
+        nblk += bend;
+        if (bend && r.p >= sbeg) { done = true; break; }
       }
-      dbg_units++;
-      r.skip(tot);
-      const bool bend = knew >= 64;
-      const int bn = b + 1 == C.bpm ? 0 : b + 1;
-      k = bend ? 0 : knew;
-      b = bend ? bn : b;
-      nblk += bend;
-      if (bend && r.p >= sbeg) break;
     }
     if (stop) {
       send = 0;  // the main loop does not run; the lane's path ends here
@@ -709,71 +827,77 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   }
   uint32_t *lp = list + min(nl, cap);
   uint2 *bp = bsl + min(nbs, bcap);
+  bool run = r.p < send;
 #pragma unroll 1
-  while (r.p < send) {
-    r.refill();
-    const uint32_t hi = r.hi();
-    uint32_t e = C.lookup_fast<SH>(k, b, hi);
-    int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
-    int knew = k + kinc;
-    if (tot == 0 || (size != 0 && knew > 64)) {  // long code or decode error (rare)
-      if (tot == 0 && e != 0) {
-        e = C.lookup_long(k, b, e, hi);
-        tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
-        knew = k + kinc;
-      }
-      if (tot == 0 || (size != 0 && knew > 64)) {
-        if (CONT || lane == 0) {
-          st = 1;
-          R.errp = r.p;
-          break;
+  while (run) {
+    top_up_of(r);
+#pragma unroll 1
+    for (int u = 0; u < kGroup; u++) {
+      refill_of(r);
+      const uint32_t hi = r.hi();
+      uint32_t e = C.lookup_fast<SH>(k, b, hi);
+      int tot = (int)(e & 31), kinc = (int)((e >> 5) & 127), size = (int)(e >> 12);
+      int knew = k + kinc;
+      if (tot == 0 || (size != 0 && knew > 64)) {  // long code or decode error (rare)
+        if (tot == 0 && e != 0) {
+          e = C.lookup_long(k, b, e, hi);
+          tot = (int)(e & 31); kinc = (int)((e >> 5) & 127); size = (int)(e >> 12);
+          knew = k + kinc;
         }
-        // the last lane reading past the final block into the fill bits /
-        // 0xFF padding: its path ends here (keep its list and checkpoints --
-        // dropping them would leave nothing for the previous lane to merge
-        // into and run that lane's continuation over this whole subsequence)
-        if (r.p + 8 > C.cbits) break;
-        r.init(r.p + 1);
-        dbg_guess++;
-        k = 0;
-        b = 0;
-        nblk = 0;
-        nl = 0;
-        nbs = 0;
-        lp = list;
-        bp = bsl;
-        nck = 0;
-        ck_next = r.p;
-        continue;
+        if (tot == 0 || (size != 0 && knew > 64)) {
+          if (CONT || lane == 0) {
+            st = 1;
+            R.errp = r.p;
+            run = false;
+            break;
+          }
+          // the last lane reading past the final block into the fill bits /
+          // 0xFF padding: its path ends here (keep its list and checkpoints --
+          // dropping them would leave nothing for the previous lane to merge
+          // into and run that lane's continuation over this whole subsequence)
+          if (r.p + 8 > C.cbits) { run = false; break; }
+          C.reader(r, r.p + 1);
+          dbg_guess++;
+          k = 0;
+          b = 0;
+          nblk = 0;
+          nl = 0;
+          nbs = 0;
+          lp = list;
+          bp = bsl;
+          nck = 0;
+          ck_next = r.p;
+          run = r.p < send;
+          break;  // (a fresh ring: maintenance restarts)
+        }
       }
-    }
-    dbg_units++;
-    const uint32_t raw = unit_raw(hi, tot, size);
-    const bool isdc = k == 0;
-    *lp = unit_entry(raw, size, isdc ? 0 : min(knew, 64) - 1, isdc);
-    if (isdc) {  // block record: where the block's units start, its DC difference (raw)
-      *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
-      bp += nbs < bcap;
-      nbs++;
-    }
-    lp += nl < cap;  // past the capacity every store lands on the sink slot
-    nl++;
-    r.skip(tot);
-    be = knew >= 64;
-    const int bn = b + 1 == C.bpm ? 0 : b + 1;
-    k = be ? 0 : knew;
-    b = be ? bn : b;
-    nblk += be;
-    const uint32_t pb = (r.p << 6) | (uint32_t)b;
-    if (CONT) {
-      if (be) {
-        if ((cand >> 6) < r.p) seek(r.p);
-        if (cand == pb) { st = 0; break; }
+      const uint32_t raw = unit_raw(hi, tot, size);
+      *lp = unit_entry(raw, size, knew);
+      if (k == 0) {  // block record: where the block's units start, its DC difference (raw)
+        *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
+        bp += nbs < bcap;
+        nbs++;
       }
-    } else if (be && r.p >= ck_next && nck < (uint32_t)kCk) {
-      ck[nck] = Ckpt{pb, nbs, nblk, 0u};
-      nck++;
-      ck_next = r.p + C.ck_bits;
+      lp += nl < cap;  // past the capacity every store lands on the sink slot
+      nl++;
+      r.skip(tot);
+      be = knew >= 64;
+      const int bn = b + 1 == C.bpm ? 0 : b + 1;
+      k = be ? 0 : knew;
+      b = be ? bn : b;
+      nblk += be;
+      const uint32_t pb = (r.p << 6) | (uint32_t)b;
+      if (CONT) {
+        if (be) {
+          if ((cand >> 6) < r.p) seek(r.p);
+          if (cand == pb) { st = 0; run = false; break; }
+        }
+      } else if (be && r.p >= ck_next && nck < (uint32_t)kCk) {
+        ck[nck] = Ckpt{pb, nbs, nblk, 0u};
+        nck++;
+        ck_next = r.p + C.ck_bits;
+      }
+      if (r.p >= send) { run = false; break; }
     }
   }
   const bool ovf = nl >= cap || nbs > bcap;  // (slot cap is the sink; keep one for the sentinel)
@@ -790,9 +914,9 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.nbs = nbs;
     if (ovf) R.ovf = 1;
   } else {
-    atomicAdd(dbg + 0, dbg_units);
+    atomicAdd(dbg + 0, nl);  // (units stored in phase 1)
     atomicAdd(dbg + 1, dbg_guess);
-    atomicMax(dbg + 2, dbg_units);
+    atomicMax(dbg + 2, nl);
     R.err = st == 1;
     R.xp = r.p;
     R.xk = k;
@@ -804,7 +928,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.nbs = nbs;
     R.ovf = ovf;
   }
-  if (!ovf) list[nl] = 1u;  // sentinel: a DC-flagged entry ends the last block
+  if (!ovf) list[nl] = kEntrySentinel;  // sentinel: a DC entry ends the last block
 }
 
 // Extension of an owner's path past the estimated end of the crop's rows
@@ -843,7 +967,7 @@ __device__ int extend_path(const EntCtx &C, uint32_t *list, uint32_t cap, uint2 
     }
     const uint32_t raw = unit_raw(hi, tot, size);
     const bool isdc = k == 0;
-    *lp = unit_entry(raw, size, isdc ? 0 : min(knew, 64) - 1, isdc);
+    *lp = unit_entry(raw, size, knew);
     if (isdc) {
       *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
       bp += nbs < bcap;
@@ -869,7 +993,7 @@ __device__ int extend_path(const EntCtx &C, uint32_t *list, uint32_t cap, uint2 
   nlist = nl;
   nblist = nbs;
   if (nl >= cap || nbs > bcap) ovf = 1;
-  else list[nl] = 1u;  // sentinel
+  else list[nl] = kEntrySentinel;  // sentinel
   return st;
 }
 
@@ -1890,7 +2014,7 @@ struct __align__(16) EntSmem {
   int32_t dcsum[kLanes * 3];
   int fmt;
   int ms_nscan, ms_nlevel, ms_range;
-  __align__(16) uint32_t ring[kLanes][16];
+  __align__(16) uint32_t ring[kLanes][kRingWords];
   long long t_ph[8];
 };
 
@@ -2831,7 +2955,7 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
 #pragma unroll 2
   for (uint32_t u = j; u < cnt; u += 8) {
     const uint32_t e = __ldg(ent + u);
-    const int nat = zz[(e >> 20) & 63];
+    const int nat = zz[entry_zz(e)];
     blk[nat] = dq ? entry_value(e) * dq[nat] : entry_value(e);
   }
   __syncwarp();
