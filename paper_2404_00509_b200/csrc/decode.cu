@@ -12,21 +12,23 @@
 // Huffman table build, window zeroing.  It hands a per-image DecodeHdr to
 // k_entropy.  Payloads too large for shared memory run on global (SMEM=false).
 //
-// k_entropy decodes one image per warp.  A restart-free baseline scan is a
-// serial chain: the decoder state (bit position, zig-zag index k, block in
-// MCU b) at any point depends on everything before it.  The clean stream is
-// cut into <= 32 subsequences; lane t decodes its subsequence from a guessed
-// state (k=0, b=0) -- a count pass that records sparse checkpoints (bit
-// position, b, blocks so far) at block starts -- then continues past its end
-// until its path reaches a checkpoint of a later lane with the same state.
-// Two decoders in the same state produce the same future, so the exact path
-// (lane 0 starts exactly) is lane 0's path, then the path of the lane it
-// merged into from the merge checkpoint, and so on.  A
-// write pass re-decodes each segment of the exact path, storing crop-window
-// coefficients only up to the last MCU row the crop needs (codec.py:483-500
-// row_stop), with DC values relative to the segment start; a warp prefix of
-// the segments' DC sums fixes them up.  Streams with restart intervals (DRI)
-// decode one interval per lane (exact entry states).
+// k_entropy decodes one image per 64-thread CTA.  A restart-free baseline
+// scan is a serial chain: the decoder state (bit position, zig-zag index k,
+// block in MCU b) at any point depends on everything before it.  The clean
+// stream (up to an estimate of where the crop's last needed block ends,
+// codec.py:494-498 row_stop) is cut into <= 64 subsequences; lane t decodes
+// its subsequence from a guessed state (k=0, b=0) after a warm-up, storing
+// every unit in its list and recording checkpoints (bit position, b, blocks
+// so far) at block starts, then continues past its end until its path
+// reaches a checkpoint of a later lane with the same state.  Two decoders in
+// the same state produce the same future, so the exact path (lane 0 starts
+// exactly) is lane 0's path, then the path of the lane it merged into from
+// the merge checkpoint, and so on; each unit is decoded once.
+// Per-segment DC sums give every crop-window block its predictor and list
+// position (k_idct gathers from the lists).  Streams with restart intervals
+// (DRI) decode one interval per lane; multi-scan streams (progressive,
+// sequential non-interleaved) decode every scan in dependency waves into
+// full coefficient arrays.
 //
 // k_idct dequantises + inverse-transforms the crop-window blocks with all
 // threads of the GPU (8 lanes per block).
