@@ -369,6 +369,11 @@ def run_gpu(args, wl):
         loader.finish(p)
     torch.cuda.synchronize(dev)
     # ---- timed region (device events, max over ranks) ----------------------
+    # live CUDA-event durations of the dominant kernel only (k_entropy): the
+    # roofline needs them from the timed region; bracketing every launch
+    # would add host work to every step (--profile-all for the full set)
+    if not args.profile_all:
+        loader.set_option(N.ESSL_OPT_PROFILE_KERNELS, 1 << N.ESSL_K_ENTROPY)
     loader.set_option(N.ESSL_OPT_PROFILE, 1)
     loader.profile_read()
     launches0 = loader.launches
@@ -457,13 +462,12 @@ def run_gpu(args, wl):
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         hprev = time.perf_counter()
-        for b in l2.epochs(ep):
+        # exactly `steps` batches are issued (no run-ahead past the timed work)
+        for b in l2.epochs(ep, steps=args.steps):
             n2 += len(b)
             now = time.perf_counter()
             e2e_host.append(now - hprev)
             hprev = now
-            if n2 >= args.steps * B:
-                break
         perm2 = np.concatenate(perm2)
         s1.record(stream)
         torch.cuda.synchronize(dev)
@@ -602,6 +606,8 @@ def main():
                     help="k_resize output columns per thread (ESSL_OPT_RESIZE_COLS; 0: default)")
     ap.add_argument("--resize-band", type=int, default=0,
                     help="k_resize output rows per CTA, at most (ESSL_OPT_RESIZE_BAND; 0: default)")
+    ap.add_argument("--profile-all", action="store_true",
+                    help="bracket every launch with CUDA events in the timed region (kernel_ms of all kernels)")
     ap.add_argument("--early-exit", type=int, default=-1,
                     help="ESSL_OPT_EARLY_EXIT (entropy decode stops near the crop's last row; -1: default)")
     ap.add_argument("--streams", type=int, default=8,

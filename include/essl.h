@@ -74,6 +74,7 @@ extern "C" {
 #define ESSL_OPT_RESIZE_COLS 11 /* k_resize output columns per thread: 2 (default), 4 or 8 */
 #define ESSL_OPT_RESIZE_BAND 12 /* k_resize output rows per CTA, at most (1..64, default 64) */
 #define ESSL_OPT_EARLY_EXIT 13  /* 1 (default): entropy decode stops near the crop's last needed row */
+#define ESSL_OPT_PROFILE_KERNELS 14 /* bitmask of ESSL_K_* launches ESSL_OPT_PROFILE brackets (default all) */
 
 /* kernel ids for essl_ctx_profile_read */
 #define ESSL_K_DECODE 0

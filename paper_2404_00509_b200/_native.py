@@ -27,6 +27,8 @@ ESSL_OPT_TRACE = 10
 ESSL_OPT_RESIZE_COLS = 11
 ESSL_OPT_RESIZE_BAND = 12
 ESSL_OPT_EARLY_EXIT = 13
+ESSL_OPT_PROFILE_KERNELS = 14
+ESSL_K_ENTROPY = 7
 KERNELS = ("decode", "resize", "crop_u8", "mask", "gather", "dump_coefs", "prep", "entropy", "idct",
            "stage", "aug")
 ESSL_AUG_SIMPLE, ESSL_AUG_3AUG, ESSL_AUG_3AUG_PLUS = 0, 1, 2

@@ -165,6 +165,7 @@ struct essl_ctx {
   std::atomic<int64_t> launches{0};
   // profiling: event pairs per launch
   bool profile = false;
+  uint32_t profile_mask = 0xFFFFFFFFu;  // ESSL_OPT_PROFILE_KERNELS: which launches are bracketed
   struct Rec { int kid; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
@@ -196,12 +197,14 @@ struct DevGuard {
 // Bracket a launch with events when profiling (ESSL_OPT_PROFILE).
 struct Prof {
   essl_ctx *c; int kid; cudaStream_t st; cudaEvent_t a = nullptr;
-  Prof(essl_ctx *c_, int k, cudaStream_t s) : c(c_), kid(k), st(s) {
-    if (c && c->profile) { a = c->take(); cudaEventRecord(a, st); }
+  bool on;
+  Prof(essl_ctx *c_, int k, cudaStream_t s)
+      : c(c_), kid(k), st(s), on(c_ && c_->profile && ((c_->profile_mask >> k) & 1u)) {
+    if (on) { a = c->take(); cudaEventRecord(a, st); }
   }
   ~Prof() {
     if (c) c->launches += 1;
-    if (c && c->profile) {
+    if (on) {
       cudaEvent_t b = c->take();
       cudaEventRecord(b, st);
       c->recs.push_back({kid, a, b});
@@ -560,6 +563,9 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
     case ESSL_OPT_EARLY_EXIT:
       c->early_exit = value != 0;
       return ESSL_OK;
+    case ESSL_OPT_PROFILE_KERNELS:
+      c->profile_mask = (uint32_t)value;
+      return ESSL_OK;
     case ESSL_OPT_CHECKPOINT_BITS:
       if (value < 1 || value > (1 << 24)) return fail(ESSL_E_ARG, "bad checkpoint bits");
       c->ck_bits = (int)value;
@@ -584,6 +590,7 @@ int essl_option_default(int option, int64_t *value) {
     case ESSL_OPT_RESIZE_COLS: *value = kDefResizeCols; return ESSL_OK;
     case ESSL_OPT_RESIZE_BAND: *value = kDefResizeBand; return ESSL_OK;
     case ESSL_OPT_EARLY_EXIT: *value = kDefEarlyExit; return ESSL_OK;
+    case ESSL_OPT_PROFILE_KERNELS: *value = 0xFFFFFFFF; return ESSL_OK;
   }
   return fail(ESSL_E_ARG, "unknown option");
 }

@@ -616,11 +616,16 @@ class Loader:
         prefetch + 2 buffers)."""
         return self._run(self._plan(epoch), into)
 
-    def epochs(self, first: int, count: int | None = None, into=None):
+    def epochs(self, first: int, count: int | None = None, into=None, steps: int | None = None):
         """Batches of epochs first, first+1, ... (count of them, or without
         end) with the prefetch pipeline kept full across epoch boundaries --
         the same batches as consecutive epoch() calls, without the drain /
-        refill bubble at each boundary (a persistent-worker DataLoader)."""
+        refill bubble at each boundary (a persistent-worker DataLoader).
+        ``steps``: stop after that many batches (nothing is decoded ahead
+        past the last one -- a training run of a fixed step count)."""
         import itertools
         es = itertools.count(first) if count is None else range(first, first + count)
-        return self._run(itertools.chain.from_iterable(self._plan(e) for e in es), into)
+        plan = itertools.chain.from_iterable(self._plan(e) for e in es)
+        if steps is not None:
+            plan = itertools.islice(plan, steps)
+        return self._run(plan, into)

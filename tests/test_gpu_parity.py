@@ -371,7 +371,9 @@ def test_multi_epoch_iterator_equals_epochs(E, synth_sets):
             c.append((sha(x.pixels), sha(x.indices), sha(x.mask)))
             if len(c) == len(a):
                 break
+        d = [(sha(x.pixels), sha(x.indices), sha(x.mask)) for x in loader.epochs(4, steps=len(a) - 1)]
     assert a == b == c
+    assert d == a[:-1]
 
 
 @pytest.mark.parametrize("res", [97, 16, 300])
