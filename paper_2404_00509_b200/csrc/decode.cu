@@ -167,7 +167,7 @@ struct __align__(16) PrepSmem {
   uint32_t K[8];
   uint32_t warp_tot[kNT / 32][4];
   uint16_t sub_pf[kMaxTables][kSubTabs];
-  int stop, carry;
+  int stop, carry, dstop;
   long long t0;
 };
 
@@ -201,6 +201,32 @@ __device__ uint32_t x2nmodp(uint64_t n, int k) {  // x^(n * 2^k) mod P
 
 __device__ __forceinline__ bool is_rst(uint32_t m) { return m >= 0xD0 && m <= 0xD7; }
 __device__ __forceinline__ bool has_ff(uint32_t w) { return __vcmpeq4(w, 0xFFFFFFFFu) != 0; }
+
+// 0x80 in each byte of t that is zero, 0 elsewhere (exact: no cross-byte carries)
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t t) {
+  const uint32_t y = (t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+  return ~(y | t | 0x7F7F7F7Fu);
+}
+// the four 0x80 byte flags of zero_bytes() -> a 4-bit mask (bit q = byte q)
+__device__ __forceinline__ uint32_t byte_flags(uint32_t f80) { return ((f80 >> 7) * 0x01020408u) >> 24; }
+// 16-byte group masks: bytes == 0xFF, bytes in RST0..RST7 (0xD0-0xD7)
+__device__ __forceinline__ void group_masks(const uint32_t w[4], uint32_t &ff, uint32_t &rst) {
+  ff = 0;
+  rst = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    ff |= byte_flags(zero_bytes(~w[k])) << (4 * k);
+    rst |= byte_flags(zero_bytes((w[k] & 0xF8F8F8F8u) ^ 0xD0D0D0D0u)) << (4 * k);
+  }
+}
+// any byte of the four words == 0xFF (a filter: false positives are fine)
+__device__ __forceinline__ bool any_ff4(const uint4 v) {
+  const uint32_t t = (~v.x - 0x01010101u) & v.x;  // high bit of a byte of ~x zero ...
+  const uint32_t u = (~v.y - 0x01010101u) & v.y;
+  const uint32_t q = (~v.z - 0x01010101u) & v.z;
+  const uint32_t r = (~v.w - 0x01010101u) & v.w;
+  return ((t | u | q | r) & 0x80808080u) != 0;
+}
 
 // Block-wide exclusive scan of four u32 values (kNT threads, warp shuffles).
 // Returns the block totals in tot[].
@@ -1424,7 +1450,22 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       for (int ch = tid; ch < C2; ch += kNT) {
         uint32_t c = 0;
         const int base = ch * kCrcChunk - Z;
-        if (base + kCrcChunk > 0) {
+        if (SMEM && base >= 4 && base + kCrcChunk <= n) {
+          // a chunk inside the message past its first 4 bytes: its words
+          // come from aligned shared-memory words by one funnel shift each
+          // (kCrcChunk is a multiple of 4, so every chunk has the same shift)
+          const uint32_t *w32 = reinterpret_cast<const uint32_t *>(raw) + (base >> 2);
+          const uint32_t sh = 8u * (uint32_t)(base & 3);
+          uint32_t lo = w32[0];
+#pragma unroll 3
+          for (int j = 0; j < kCrcChunk / 4; j++) {
+            const uint32_t hi = w32[j + 1];
+            c ^= __funnelshift_r(lo, hi, sh);
+            lo = hi;
+            c = S.crc.T[3][c & 0xFF] ^ S.crc.T[2][(c >> 8) & 0xFF] ^ S.crc.T[1][(c >> 16) & 0xFF] ^
+                S.crc.T[0][c >> 24];
+          }
+        } else if (base + kCrcChunk > 0) {
 #pragma unroll 3
           for (int j = 0; j < kCrcChunk; j += 4) {
             uint32_t w = 0;
@@ -1480,24 +1521,28 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       if (tid == 0 && PS.cmd != 2) parse_until_sos(PS, pv);
       __syncthreads();
       if (PS.cmd != 1) break;
-      // entropy_end (codec.py:109-121): first FF followed by a byte that is
-      // not 00, RSTn or FF.
-      if (tid == 0) S.stop = n;
+      // entropy_end (codec.py:109-121): the first FF followed by a byte that
+      // is not 00, RSTn or FF.  For the first scan the same pass finds where
+      // destuff_scan stops (decode_kernels.py:27-61): the first FF followed by
+      // a byte that is not 00 or RSTn (FF FF fill bytes end the clean data).
+      const bool first = PS.nscans == 0;
+      if (tid == 0) { S.stop = n; if (first) S.dstop = n; }
       __syncthreads();
       const int d0 = PS.dstart;
       for (int r0 = d0 & ~15; r0 < n - 1; r0 += kNT * 16) {
-        const int a = max(r0 + tid * 16, d0), e = min(r0 + tid * 16 + 16, n - 1);
-        for (int i = a; i < e;) {
-          if (SMEM && (i & 3) == 0 && i + 4 <= e &&
-              !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
-            i += 4;
-            continue;
-          }
-          if (raw[i] == 0xFF) {
-            const int m = raw[i + 1];
-            if (!(m == 0x00 || is_rst(m) || m == 0xFF)) { atomicMin(&S.stop, i); break; }
-          }
-          i++;
+        const int g0 = r0 + tid * 16;
+        const int a = max(g0, d0), e = min(g0 + 16, n - 1);
+        if (a >= e) continue;
+        // 16 bytes per thread per round: one 16-byte shared load filters out
+        // the (common) groups without an FF byte
+        if (SMEM && !any_ff4(*reinterpret_cast<const uint4 *>(raw + g0))) continue;
+        bool d_found = !first;
+        for (int i = a; i < e; i++) {
+          if (raw[i] != 0xFF) continue;
+          const int m = raw[i + 1];
+          if (m == 0x00 || is_rst(m)) continue;
+          if (!d_found) { atomicMin(&S.dstop, i); d_found = true; }
+          if (m != 0xFF) { atomicMin(&S.stop, i); break; }
         }
       }
       __syncthreads();
@@ -1682,28 +1727,17 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     // places the kept bytes.
     const int seg0 = PS.scan_start, seg1 = PS.scan_end;
     constexpr int kRound = kNT * 16;
-    if (tid == 0) S.stop = seg1;
+    // where destuff_scan stops: found by the entropy-end pass (first FF not
+    // followed by 00 / RSTn), or the segment's last byte when that is an FF
+    // (decode_kernels.py:37-38: `if i + 1 >= n: break`)
+    if (tid == 0) {
+      int st = min(S.dstop, seg1);
+      if (st == seg1 && seg1 > seg0 && raw[seg1 - 1] == 0xFF) st = seg1 - 1;
+      S.stop = st;
+      S.carry = 0;
+    }
     __syncthreads();
     const int rbeg = seg0 & ~15;  // rounds start 16-byte aligned (uint4 loads)
-    for (int r0 = rbeg; r0 < seg1; r0 += kRound) {  // stop: FF not followed by 00/RSTn
-      const int g0 = r0 + tid * 16;
-      const int a = max(g0, seg0), e = min(g0 + 16, seg1);
-      for (int i = a; i < e;) {
-        if (SMEM && (i & 3) == 0 && i + 4 <= e &&
-            !has_ff(*reinterpret_cast<const uint32_t *>(raw + i))) {
-          i += 4;
-          continue;
-        }
-        if (raw[i] == 0xFF) {
-          if (i + 1 >= seg1) { atomicMin(&S.stop, i); break; }
-          const int m = raw[i + 1];
-          if (!(m == 0x00 || is_rst(m))) { atomicMin(&S.stop, i); break; }
-        }
-        i++;
-      }
-    }
-    if (tid == 0) S.carry = 0;
-    __syncthreads();
     const int stop = S.stop;
     const int max_r = PS.scan_ri ? H.max_restarts + 2 : 0;
     uint32_t *rst_tab = reinterpret_cast<uint32_t *>(gclean) + H.rst_off;
@@ -1711,69 +1745,57 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     for (int r0 = rbeg; r0 < stop; r0 += kRound) {
       const int g0 = r0 + tid * 16;
       const int a = max(g0, seg0), e = min(g0 + 16, stop);
-      // this thread's input bytes, the byte before and the byte after, in
+      // this thread's 16 input bytes, the byte before and the byte after, in
       // registers before any thread of the round writes
-      uint8_t in[16];
+      uint32_t w[4] = {0, 0, 0, 0};
       int prev = 0, next = 0;
       if (g0 < stop) {
         if (SMEM) {
-          const uint4 w = *reinterpret_cast<const uint4 *>(raw + g0);
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int q = 0; q < 16; q++) in[q] = (uint8_t)(ww[q >> 2] >> (8 * (q & 3)));
+          const uint4 v = *reinterpret_cast<const uint4 *>(raw + g0);
+          w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
         } else {
 #pragma unroll
-          for (int q = 0; q < 16; q++) in[q] = raw[g0 + q];
+          for (int q = 0; q < 16; q++) w[q >> 2] |= (uint32_t)raw[g0 + q] << (8 * (q & 3));
         }
         prev = tid == 0 ? S.carry : (g0 > 0 ? raw[g0 - 1] : 0);  // (thread 0: saved by the last round)
         next = raw[g0 + 16];
       }
-      uint32_t cnt[4] = {0, 0, 0, 0}, tot[4];
+      // bit masks over the group (bit q = byte g0 + q): destuff_scan keeps a
+      // byte unless it follows an FF (the 00 of FF00, the marker byte of an
+      // RSTn) or is the FF of an RSTn, which records a restart offset
+      uint32_t range = 0, keep = 0, rstm = 0;
       bool fast = false;
-      if (a == g0 && e == a + 16) {
-        bool ff = false;
-#pragma unroll
-        for (int q = 0; q < 16; q++) ff |= in[q] == 0xFF;
-        fast = !ff && !(a > seg0 && prev == 0xFF);
+      if (a < e) {
+        range = ((1u << (e - g0)) - 1u) & ~((1u << (a - g0)) - 1u);
+        uint32_t ffm, rsm;
+        group_masks(w, ffm, rsm);
+        fast = ffm == 0 && !(a > seg0 && prev == 0xFF) && range == 0xFFFFu;
+        // (i > seg0 && previous byte FF); the segment's first byte never is
+        uint32_t second = ((ffm << 1) | (prev == 0xFF ? 1u : 0u)) & 0xFFFFu;
+        if (a == seg0) second &= ~(1u << (a - g0));
+        rstm = ffm & ((rsm >> 1) | (is_rst(next) ? 0x8000u : 0u)) & range;
+        keep = range & ~second & ~rstm;
       }
-      if (fast) {
-        cnt[0] = 16;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; q++) {
-          const int i = g0 + q;
-          if (i < a || i >= e) continue;
-          const int v = in[q];
-          const int pv = q == 0 ? prev : in[q == 0 ? 0 : q - 1];
-          const int nv = q == 15 ? next : in[q == 15 ? 15 : q + 1];
-          const bool second = i > seg0 && pv == 0xFF;
-          const bool rst = v == 0xFF && is_rst(nv);
-          cnt[0] += (!second && !rst);
-          cnt[1] += rst;
-        }
-      }
+      uint32_t cnt[4] = {(uint32_t)__popc(keep), (uint32_t)__popc(rstm), 0, 0}, tot[4];
       block_scan4(S.warp_tot, cnt, tot);  // (barriers: every read above is done)
-      if (tid == kNT - 1) S.carry = in[15];  // the round's last input byte
+      if (tid == kNT - 1) S.carry = (w[3] >> 24) & 0xFF;  // the round's last input byte
       uint32_t kept = kbase + cnt[0], nrst = rbase + cnt[1];
       if (fast) {
 #pragma unroll
-        for (int q = 0; q < 16; q++) clean[kept + q] = in[q];
+        for (int q = 0; q < 16; q++) clean[kept + q] = (uint8_t)(w[q >> 2] >> (8 * (q & 3)));
       } else {
-#pragma unroll
-        for (int q = 0; q < 16; q++) {
-          const int i = g0 + q;
-          if (i < a || i >= e) continue;
-          const int v = in[q];
-          const int pv = q == 0 ? prev : in[q == 0 ? 0 : q - 1];
-          const int nv = q == 15 ? next : in[q == 15 ? 15 : q + 1];
-          const bool second = i > seg0 && pv == 0xFF;
-          const bool rst = v == 0xFF && is_rst(nv);
-          if (rst) {
-            if ((int)nrst < max_r) rst_tab[nrst] = kept;
-            nrst++;
-          } else if (!second) {
-            clean[kept++] = (uint8_t)v;
-          }
+        const uint32_t base = kept;
+#pragma unroll 1
+        for (uint32_t m = rstm; m; m &= m - 1) {  // restart offsets (clean position of the marker)
+          const int q = __ffs(m) - 1;
+          if ((int)nrst < max_r) rst_tab[nrst] = base + __popc(keep & ((1u << q) - 1u));
+          nrst++;
+        }
+#pragma unroll 1
+        for (uint32_t m = keep; m; m &= m - 1) {
+          const int q = __ffs(m) - 1;
+          const uint32_t wd = (q & 8) ? ((q & 4) ? w[3] : w[2]) : ((q & 4) ? w[1] : w[0]);
+          clean[kept++] = (uint8_t)(wd >> (8 * (q & 3)));
         }
       }
       kbase += tot[0];
