@@ -1535,8 +1535,26 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
         if (a >= e) continue;
         // 16 bytes per thread per round: one 16-byte shared load filters out
         // the (common) groups without an FF byte
-        if (SMEM && !any_ff4(*reinterpret_cast<const uint4 *>(raw + g0))) continue;
         bool d_found = !first;
+        if (SMEM) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(raw + g0);
+          if (!any_ff4(v)) continue;
+          // exact FF positions of the group inside [a, e), then only those
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          uint32_t ffm = 0;
+#pragma unroll
+          for (int k = 0; k < 4; k++) ffm |= byte_flags(zero_bytes(~w[k])) << (4 * k);
+          ffm &= ((1u << (e - g0)) - 1u) & ~((1u << (a - g0)) - 1u);
+#pragma unroll 1
+          for (; ffm; ffm &= ffm - 1) {
+            const int i = g0 + __ffs(ffm) - 1;
+            const int m = raw[i + 1];
+            if (m == 0x00 || is_rst(m)) continue;
+            if (!d_found) { atomicMin(&S.dstop, i); d_found = true; }
+            if (m != 0xFF) { atomicMin(&S.stop, i); break; }
+          }
+          continue;
+        }
         for (int i = a; i < e; i++) {
           if (raw[i] != 0xFF) continue;
           const int m = raw[i + 1];
@@ -1791,11 +1809,9 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
           if ((int)nrst < max_r) rst_tab[nrst] = base + __popc(keep & ((1u << q) - 1u));
           nrst++;
         }
-#pragma unroll 1
-        for (uint32_t m = keep; m; m &= m - 1) {
-          const int q = __ffs(m) - 1;
-          const uint32_t wd = (q & 8) ? ((q & 4) ? w[3] : w[2]) : ((q & 4) ? w[1] : w[0]);
-          clean[kept++] = (uint8_t)(wd >> (8 * (q & 3)));
+#pragma unroll
+        for (int q = 0; q < 16; q++) {  // (predicated stores: no per-byte branches)
+          if ((keep >> q) & 1u) clean[kept++] = (uint8_t)(w[q >> 2] >> (8 * (q & 3)));
         }
       }
       kbase += tot[0];
