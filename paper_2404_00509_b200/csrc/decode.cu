@@ -2992,8 +2992,25 @@ __device__ void gather_block8(bool valid, const ImgInfo &I, const Scratch &sc, i
   // group's eight lanes take every eighth one.
   const uint32_t cnt = valid ? t.y >> 16 : 0u;
   const uint32_t *ent = sc.list + t.x + 1;
-#pragma unroll 2
-  for (uint32_t u = j; u < cnt; u += 8) {
+  // the first 32 entries (almost every block) as four independent loads per
+  // lane, all in flight before the first use; longer blocks loop on
+  constexpr int kFirst = 4;
+  uint32_t ev[kFirst];
+#pragma unroll
+  for (int k = 0; k < kFirst; k++) {
+    const uint32_t u = j + 8u * k;
+    ev[k] = u < cnt ? __ldg(ent + u) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kFirst; k++) {
+    if (j + 8u * k < cnt) {
+      const uint32_t e = ev[k];
+      const int nat = zz[entry_zz(e)];
+      blk[nat] = dq ? entry_value(e) * dq[nat] : entry_value(e);
+    }
+  }
+#pragma unroll 1
+  for (uint32_t u = j + 8u * kFirst; u < cnt; u += 8) {
     const uint32_t e = __ldg(ent + u);
     const int nat = zz[entry_zz(e)];
     blk[nat] = dq ? entry_value(e) * dq[nat] : entry_value(e);
