@@ -393,6 +393,7 @@ def run_gpu(args, wl):
     host_t = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("bench.timed")
     t0.record(stream)
     n_img = 0
     for i in range(args.steps):
@@ -411,6 +412,7 @@ def run_gpu(args, wl):
     for p in pend:  # join every in-flight batch before the end event
         loader.join(p)
     t1.record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize(dev)
     if prof_range:
         torch.cuda.cudart().cudaProfilerStop()

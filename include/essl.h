@@ -179,6 +179,13 @@ int essl_debug_lanes(essl_ctx *ctx, int32_t *out, int n);
  * SM id} for k_prep / k_entropy / k_idct / k_resize.  Synchronises the
  * device; returns the number of records written. */
 int essl_trace_read(essl_ctx *ctx, uint64_t *out, int max);
+/* Bounds-check counters of a checked build (ESSL_CHECKED): out[i] = the
+ * number of out-of-bounds accesses caught by check i (scratch lists,
+ * coefficient windows, multi-scan arrays, planes, clean streams, resize
+ * staging, outputs, checkpoints) on the current device since the last reset.
+ * Returns 1 for a checked build, 0 otherwise (the counters stay 0), <0 on
+ * error.  Synchronous. */
+int essl_check_read(uint32_t *out, int n, int reset);
 const char *essl_last_error(void);
 const char *essl_version(void);
 /* Stream-ordered copy of `bytes` between host (pinned) and device memory

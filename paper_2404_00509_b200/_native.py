@@ -48,6 +48,7 @@ EXPORTS = (
     "essl_augment_u8", "essl_aug_draw", "essl_aug_batch", "essl_debug_lanes",
     "essl_trace_read", "essl_memcpy_async", "essl_option_default",
     "essl_decode_rrc_visible", "essl_dataset_create", "essl_dataset_destroy", "essl_batch_enqueue",
+    "essl_check_read",
 )
 
 
@@ -182,6 +183,7 @@ def lib():
         "essl_dataset_create": (i32, [i64, P, P, P, P, P, P, P]),
         "essl_dataset_destroy": (i32, [P]),
         "essl_batch_enqueue": (i32, [P, P, P, P, i32, P, P]),
+        "essl_check_read": (i32, [P, i32, i32]),
         "essl_decode_rrc_visible": (i32, [P, P, P, P, i32, i32, i32, P, i64, P, i32, P, i32, P,
                                           P, P]),
         "essl_aug_draw": (i32, [P, i32, P, P]),

@@ -33,9 +33,17 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; libessl cannot be built")
 
 
+CHECKED = os.environ.get("ESSL_CHECKED") == "1"  # bounds-checked variant (_lib/checked/)
+if CHECKED:
+    OUT_DIR = PKG / "_lib" / "checked"
+    LIB = OUT_DIR / "libessl.so"
+
+
 def _flags(src: str) -> list[str]:
     common = ["-std=c++17", "-O3", "-lineinfo", f"-I{ROOT / 'include'}", f"-I{CSRC}",
               "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math,-fvisibility=hidden"]
+    if CHECKED:
+        common.append("-DESSL_CHECKED")
     if src.endswith(".cu"):
         # -fmad=false: float64/float32 parity stages must not contract to FMA
         return common + [ARCH, "-fmad=false", "-Xptxas", "-warn-spills"]
@@ -57,7 +65,7 @@ def _digest() -> str:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     override = os.environ.get("ESSL_LIB")
-    if override and not force:  # an A/B build chosen by the caller: never rebuild over it
+    if override and not force and not CHECKED:  # an A/B build chosen by the caller: never rebuild over it
         return Path(override)
     OUT_DIR.mkdir(exist_ok=True)
     stamp = OUT_DIR / "libessl.sha256"

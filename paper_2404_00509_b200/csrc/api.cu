@@ -13,6 +13,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "essl.h"
 #include "essl_common.cuh"
 
@@ -178,6 +180,13 @@ struct essl_ctx {
 };
 
 namespace {
+// NVTX range over a host-side stage (header-only NVTX3: a no-op unless a
+// profiler is attached), visible in Nsight Systems next to the kernels.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Makes the context's device current for the duration of an entry point and
 // restores the caller's device (a context may live on a non-current device).
 struct DevGuard {
@@ -572,6 +581,20 @@ int essl_ctx_set_option(essl_ctx *c, int option, int64_t value) {
       return ESSL_OK;
   }
   return fail(ESSL_E_ARG, "unknown option");
+}
+
+int essl_check_read(uint32_t *out, int n, int reset) {
+  if (!out || n < 1) return fail(ESSL_E_ARG, "essl_check_read: bad arguments");
+  unsigned int d[essl::CK_COUNT], p[essl::CK_COUNT];
+  essl::check_read_decode(d, reset != 0);
+  essl::check_read_pixels(p, reset != 0);
+  for (int i = 0; i < n && i < essl::CK_COUNT; i++) out[i] = d[i] + p[i];
+  CK(cudaGetLastError());
+#ifdef ESSL_CHECKED
+  return 1;
+#else
+  return 0;
+#endif
 }
 
 int essl_option_default(int option, int64_t *value) {
@@ -1091,6 +1114,7 @@ int essl_batch_enqueue(essl_ctx *c, const essl_dataset *ds, const essl_batch_cfg
     if (indices[i] < 0 || indices[i] >= N) return fail(ESSL_E_ARG, "essl_batch_enqueue: index out of range");
   DevGuard dg_(c);
   if (n == 0) return ESSL_OK;
+  NvtxRange nv_("essl_batch_enqueue");
   cudaStream_t st = (cudaStream_t)stream;
   const int r = pick_slot(c);  // the batch that last used slot r has completed
   if (r < 0) return r;

@@ -39,6 +39,16 @@
 
 namespace essl {
 
+__device__ unsigned int g_check_dec[CK_COUNT];  // ESSL_CHECK counters (checked builds)
+
+void check_read_decode(unsigned int *out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_check_dec, sizeof(unsigned int) * CK_COUNT);
+  if (reset) {
+    static const unsigned int zero[CK_COUNT] = {};
+    cudaMemcpyToSymbol(g_check_dec, zero, sizeof(zero));
+  }
+}
+
 __constant__ uint8_t c_zz[64] = {
     0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
     12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
@@ -634,6 +644,8 @@ struct EntCtx {
   int c1, c2, bpm, gx;
   uint32_t cbits, limit, ck_bits;
   uint32_t cend;  // end of the range phase 1 covers (N2 estimate; cbits without it)
+  const uint32_t *list_lo, *list_hi;  // the unit-list pool incl. overflow sinks (ESSL_CHECK)
+  const int16_t *coef_lo, *coef_hi;   // the coefficient scratch (ESSL_CHECK)
   const uint32_t *words;  // clean stream (global)
   uint32_t ring_s;        // this lane's read ring (shared-window address)
   uint32_t wmax, cpad;
@@ -900,8 +912,10 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
         }
       }
       const uint32_t raw = unit_raw(hi, tot, size);
+      ESSL_CHECK(g_check_dec, lp >= C.list_lo && lp < C.list_hi, CK_LIST);
       *lp = unit_entry(raw, size, knew);
       if (k == 0) {  // block record: where the block's units start, its DC difference (raw)
+        ESSL_CHECK(g_check_dec, (const uint32_t *)bp >= C.list_lo && (const uint32_t *)(bp + 1) <= C.list_hi, CK_LIST);
         *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
         bp += nbs < bcap;
         nbs++;
@@ -921,6 +935,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
           if (cand == pb) { st = 0; run = false; break; }
         }
       } else if (be && r.p >= ck_next && nck < (uint32_t)kCk) {
+        ESSL_CHECK(g_check_dec, nck < (uint32_t)kCk, CK_CKPT);
         ck[nck] = Ckpt{pb, nbs, nblk, 0u};
         nck++;
         ck_next = r.p + C.ck_bits;
@@ -956,6 +971,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     R.nbs = nbs;
     R.ovf = ovf;
   }
+  ESSL_CHECK(g_check_dec, ovf || (list + nl >= C.list_lo && list + nl < C.list_hi), CK_LIST);
   if (!ovf) list[nl] = kEntrySentinel;  // sentinel: a DC entry ends the last block
 }
 
@@ -995,8 +1011,10 @@ __device__ int extend_path(const EntCtx &C, uint32_t *list, uint32_t cap, uint2 
     }
     const uint32_t raw = unit_raw(hi, tot, size);
     const bool isdc = k == 0;
+    ESSL_CHECK(g_check_dec, lp >= C.list_lo && lp < C.list_hi, CK_LIST);
     *lp = unit_entry(raw, size, knew);
     if (isdc) {
+      ESSL_CHECK(g_check_dec, (const uint32_t *)bp >= C.list_lo && (const uint32_t *)(bp + 1) <= C.list_hi, CK_LIST);
       *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
       bp += nbs < bcap;
       nbs++;
@@ -1104,9 +1122,11 @@ __device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, u
       pr2 = s == 2 ? pv : pr2;
       if (cur) {
         if (pv < -32768 || pv > 32767) o.range = 1;
+        ESSL_CHECK(g_check_dec, cur >= C.coef_lo && cur + 64 <= C.coef_hi, CK_COEF);
         cur[0] = (int16_t)pv;
       }
     } else if (size != 0 && cur) {
+      ESSL_CHECK(g_check_dec, cur >= C.coef_lo && cur + 64 <= C.coef_hi, CK_COEF);
       cur[H.zz[knew - 1]] = (int16_t)v;
     }
     r.skip(tot);
@@ -1174,6 +1194,7 @@ __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, c
       // list's sentinel): their count rides in the entry's high half
       const uint32_t next = ord + i + 1 < nrec ? bsl[ord + i + 1].x : nlist;
       const uint32_t cnt = min(next - rec.x - 1u, 63u);
+      ESSL_CHECK(g_check_dec, cur >= C.coef_lo && cur + 4 <= C.coef_hi, CK_COEF);
       *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + rec.x, ((uint32_t)pv & 0xFFFFu) | (cnt << 16));
     }
     if (++b == C.bpm) {
@@ -1826,6 +1847,11 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
     if (tid < 48) clean[tk + tid] = 0xFF;
     __syncthreads();
     const int nwords = (int)((tk + 48) / 4);
+    if (tid == 0) {
+      const uint64_t clean_bytes = ((uint64_t)(PS.scan_end - PS.scan_start) + 64 + 15) / 16 * 16;
+      ESSL_CHECK(g_check_dec, (uint64_t)(nwords + 3) / 4 * 16 <= clean_bytes, CK_CLEAN);
+      ESSL_CHECK(g_check_dec, H.clean_off + clean_bytes <= P.s.clean_cap, CK_CLEAN);
+    }
     if (SMEM) {
       const int n16 = (nwords + 3) / 4;
       const uint4 *src = reinterpret_cast<const uint4 *>(clean);
@@ -2234,6 +2260,10 @@ __device__ int ms_decode_scan(const DecodeHead &H, const MsScan &sc, const MsTab
   int eobrun = 0;
   const int ri = sc.ri;
   const bool is_dc = progressive && sc.ss == 0;
+  uint64_t ms_total = 0;  // (the image's full arrays, for ESSL_CHECK)
+  for (int c = 0; c < H.ncomp; c++) ms_total += (uint64_t)H.gy * (H.comp_hv[c] & 15) * H.coef_pitch[c] * 64;
+  const int16_t *ms_end = coef + H.coef_base + ms_total;
+  (void)ms_end;
   const int al = sc.al, ss = sc.ss, se = sc.se;
   const int p1 = 1 << al, m1 = -(1 << al);
   int unit = 0;
@@ -2259,6 +2289,7 @@ __device__ int ms_decode_scan(const DecodeHead &H, const MsScan &sc, const MsTab
           for (int by = 0; by < vv[s]; by++)
             for (int bx = 0; bx < hh[s]; bx++) {
               int16_t *blk = base + ((uint64_t)(my * vv[s] + by) * pitch + (mx * hh[s] + bx)) * 64;
+              ESSL_CHECK(g_check_dec, blk >= coef + H.coef_base && blk + 64 <= ms_end, CK_MS_COEF);
               if (progressive && sc.ah != 0) {  // DC refine: one bit
                 if (r.bits(1)) range_bad |= !ms_store(blk, blk[0] | p1);
                 continue;
@@ -2294,6 +2325,7 @@ __device__ int ms_decode_scan(const DecodeHead &H, const MsScan &sc, const MsTab
       // progressive AC, one component, one block per unit
       const int c = sc.comp[0];
       int16_t *blk = coef + H.coef_off[c] + ((uint64_t)my * H.coef_pitch[c] + mx) * 64;
+      ESSL_CHECK(g_check_dec, blk >= coef + H.coef_base && blk + 64 <= ms_end, CK_MS_COEF);
       const MsTab &T = tabs[sc.at[0]];
       if (sc.ah == 0) {  // AC first (decode_kernels.py:259-309)
         if (eobrun > 0) { eobrun--; continue; }
@@ -2888,6 +2920,10 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
   C.cbits = H.clean_bits;
   C.limit = H.limit_blocks;
   C.cend = H.clean_bits;
+  C.list_lo = P.s.list;
+  C.list_hi = P.s.list + P.s.list_cap + 4 * kLanes;
+  C.coef_lo = P.s.coef;
+  C.coef_hi = P.s.coef + P.s.coef_cap;
   C.words = reinterpret_cast<const uint32_t *>(P.s.clean + H.clean_off);
   C.wmax = H.wmax;
   C.ck_bits = 0;
@@ -3061,6 +3097,8 @@ __global__ void __launch_bounds__(256, 5) k_idct(DecodeParams P) {
     gather_block8(valid, I, P.s, c, byr, bxr, blk, s_zz, q[c]);  // dequantised
     const int pitch = I.plane_pitch[c];
     uint8_t *dst = P.s.plane + I.plane_off[c] + (uint64_t)byr * 8 * pitch + bxr * 8;
+    ESSL_CHECK(g_check_dec, !valid || (dst >= P.s.plane && dst + 7 * (uint64_t)pitch + 8 <= P.s.plane + P.s.plane_cap),
+               CK_PLANE);
     idct_block_8lanes(valid, blk, dst, pitch, t);
   }
 }

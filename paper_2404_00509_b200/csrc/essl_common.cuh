@@ -7,6 +7,35 @@
 
 namespace essl {
 
+// Bounds-checked builds (ESSL_CHECKED, `ESSL_CHECKED=1 python -m
+// paper_2404_00509_b200.build`): every scratch / output access named by a
+// check id is verified on the device and violations are counted (no trap:
+// the run continues and the count is read back with essl_check_read).  This
+// stands in for compute-sanitizer, which is closed on the GPU pool.
+enum CheckId : int {
+  CK_LIST = 0,     // k_entropy unit-list / block-record / sentinel stores
+  CK_COEF = 1,     // coefficient window / table stores (k_entropy)
+  CK_MS_COEF = 2,  // multi-scan full coefficient arrays
+  CK_PLANE = 3,    // k_idct plane stores
+  CK_CLEAN = 4,    // k_prep clean-stream bytes / restart table
+  CK_SRC = 5,      // k_resize shared source-row staging
+  CK_OUT = 6,      // k_resize output stores
+  CK_CKPT = 7,     // k_entropy checkpoints
+  CK_COUNT = 16,
+};
+#ifdef ESSL_CHECKED
+#define ESSL_CHECK(table, cond, id) \
+  do {                                \
+    if (!(cond)) atomicAdd(&(table)[(id)], 1u); \
+  } while (0)
+#else
+#define ESSL_CHECK(table, cond, id) \
+  do {                                \
+  } while (0)
+#endif
+void check_read_decode(unsigned int *out, bool reset);
+void check_read_pixels(unsigned int *out, bool reset);
+
 struct Ckpt;
 
 constexpr int kDecodeThreads = 256;  // k_prep: one CTA per image

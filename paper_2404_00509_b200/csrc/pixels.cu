@@ -20,6 +20,16 @@
 
 namespace essl {
 
+__device__ unsigned int g_check_pix[CK_COUNT];  // ESSL_CHECK counters (checked builds)
+
+void check_read_pixels(unsigned int *out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_check_pix, sizeof(unsigned int) * CK_COUNT);
+  if (reset) {
+    static const unsigned int zero[CK_COUNT] = {};
+    cudaMemcpyToSymbol(g_check_pix, zero, sizeof(zero));
+  }
+}
+
 constexpr int kPixThreads = 256;
 
 __device__ __forceinline__ int clamp255(int v) { return v < 0 ? 0 : (v > 255 ? 255 : v); }
@@ -152,7 +162,8 @@ struct __align__(8) ColTap {
 
 // Source rows [ys0, ys0 + nrows) of the crop -> RGBX words src[r * iw + x].
 __device__ __forceinline__ void stage_rows(const ImgInfo &I, const PlaneSrc &S, int ys0, int nrows,
-                                           uint32_t *src) {
+                                           uint32_t *src, int src_words) {
+  (void)src_words;
   const int iw = I.rw;
   // Fast path (luma at full horizontal resolution, chroma at full or half:
   // 4:2:0, 4:2:2, 4:4:4, gray): work items are (row, group of 4 image
@@ -217,6 +228,7 @@ __device__ __forceinline__ void stage_rows(const ImgInfo &I, const PlaneSrc &S, 
       }
       const int x = 4 * G - I.rx;
       uint32_t *row = src + r * iw;
+      ESSL_CHECK(g_check_pix, (r + 1) * iw <= src_words, CK_SRC);
 #pragma unroll
       for (int i = 0; i < 4; i++)
         if ((unsigned)(x + i) < (unsigned)iw) row[x + i] = w[i];
@@ -350,7 +362,7 @@ __global__ void __launch_bounds__(kPixThreads, COLS == 8 ? 2 : (COLS == 4 ? 3 : 
   ColTap *ctab = reinterpret_cast<ColTap *>(dyn + (size_t)P.src_words * 4);
   PlaneSrc S;
   S.load(I, P.plane);
-  if (STAGED) stage_rows(I, S, ys0, nrows, src);
+  if (STAGED) stage_rows(I, S, ys0, nrows, src, P.src_words);
   // column taps (imgops.py:42-47; hflip after resize: output column ox reads
   // the resize's column res-1-ox) and the band's row taps (imgops.py:37-41)
   for (int ox = threadIdx.x; ox < res; ox += kPixThreads) {
@@ -797,6 +809,7 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize_pairs(PixelParams P) 
       }
       const int x = 4 * G - I.rx;
       uint32_t *row = src + r * iw;
+      ESSL_CHECK(g_check_pix, (r + 1) * iw <= P.src_words, CK_SRC);
 #pragma unroll
       for (int i = 0; i < 4; i++)
         if ((unsigned)(x + i) < (unsigned)iw) row[x + i] = w[i];
@@ -964,6 +977,7 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize_pairs(PixelParams P) 
       }
       const int oy = ob0 + r;
       const int64_t o = img * stride + (int64_t)oy * res + oxa;
+      ESSL_CHECK(g_check_pix, out_kind == ESSL_OUT_NONE || (o >= 0 && o + 2 * plane_sz + (two ? 2 : 1) <= (int64_t)P.n * stride), CK_OUT);
       if (out_kind == ESSL_OUT_BF16_NCHW) {
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(P.out) + o;
         if (pair_ok) {

@@ -55,3 +55,29 @@ def cuda():
     from paper_2404_00509_b200 import build
     build.build()
     return torch.device("cuda", 0)
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """With a bounds-checked library (ESSL_CHECKED build selected through
+    ESSL_LIB), fail the run if any device-side bounds check fired; the
+    counters are written to gpurun_out/bounds_check.json."""
+    import os
+    if not os.environ.get("ESSL_LIB", "").endswith("checked/libessl.so"):
+        return
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return
+        from paper_2404_00509_b200 import _native as N
+        out = np.zeros(16, np.uint32)
+        rc = N.lib().essl_check_read(N.ptr(out), 16, 0)
+    except Exception as exc:  # (reported, not raised from a hook)
+        print(f"bounds check read failed: {exc}")
+        return
+    names = ["list", "coef", "ms_coef", "plane", "clean", "src", "out", "ckpt"]
+    res = {"checked_build": rc == 1, "violations": {n: int(out[i]) for i, n in enumerate(names)}}
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "bounds_check.json").write_text(json.dumps(res, indent=1))
+    print("bounds check:", res)
+    if rc != 1 or int(out.sum()) != 0:
+        session.exitstatus = 1
