@@ -180,8 +180,14 @@ __device__ __forceinline__ void stage_rows(const ImgInfo &I, const PlaneSrc &S, 
     const int g0 = I.rx >> 2, ng = ((I.rx + iw + 3) >> 2) - g0;
     const bool half1 = I.ncomp == 3 && 2 * I.comp_h[1] == I.hmax;
     const bool half2 = I.ncomp == 3 && 2 * I.comp_h[2] == I.hmax;
-    for (int it = threadIdx.x; it < nrows * ng; it += kPixThreads) {
-      const int r = it / ng, G = g0 + (it - r * ng);
+    // a thread keeps one group of 4 columns (its column offsets fixed) and
+    // walks rows rpp apart: no per-item division or column arithmetic
+    const int cpr = ng < kPixThreads ? ng : kPixThreads;  // groups per pass
+    const int rpp = kPixThreads / cpr;                    // rows per pass
+    const int rt = threadIdx.x / cpr, gt = threadIdx.x - rt * cpr;
+    for (int Gi = gt; rt < rpp && Gi < ng; Gi += cpr)
+    for (int r = rt; r < nrows; r += rpp) {
+      const int G = g0 + Gi;
       int ro[3];
       S.row_off(I.ry + ys0 + r, ro);
       const uint32_t y4 = *reinterpret_cast<const uint32_t *>(S.p[0] + ro[0] + 4 * G - S.ox[0]);
@@ -749,104 +755,8 @@ __global__ void __launch_bounds__(kPixThreads, 4) k_resize_pairs(PixelParams P) 
   uint32_t *src = reinterpret_cast<uint32_t *>(dyn);                         // [nrows][iw]
   PlaneSrc S;
   S.load(I, P.plane);
-  // source rows -> RGBX words in shared memory.
-  // Fast path (luma at full horizontal resolution, chroma at full or half:
-  // 4:2:0, 4:2:2, 4:4:4, gray): work items are (row, group of 4 image
-  // columns aligned to 4), so the luma plane is read 4 bytes at a time and
-  // half-resolution chroma 2 bytes at a time (planes are MCU-aligned windows:
-  // a group never leaves them), and each chroma sample's colour terms are
-  // computed once for the two pixels that replicate it (decode_kernels.py:
-  // 551-576: R = Y + (91881 Cr + 32768) >> 16, G = Y + (-22554 Cb - 46802 Cr
-  // + 32768) >> 16, B = Y + (116130 Cb + 32768) >> 16, clamped).
-  const bool fast = I.comp_h[0] == I.hmax &&
-                    (I.ncomp == 1 || ((2 * I.comp_h[1] == I.hmax || I.comp_h[1] == I.hmax) &&
-                                      (2 * I.comp_h[2] == I.hmax || I.comp_h[2] == I.hmax)));
-  if (fast) {
-    const int g0 = I.rx >> 2, ng = ((I.rx + iw + 3) >> 2) - g0;
-    const bool half1 = I.ncomp == 3 && 2 * I.comp_h[1] == I.hmax;
-    const bool half2 = I.ncomp == 3 && 2 * I.comp_h[2] == I.hmax;
-    for (int it = threadIdx.x; it < nrows * ng; it += kPixThreads) {
-      const int r = it / ng, G = g0 + (it - r * ng);
-      int ro[3];
-      S.row_off(I.ry + ys0 + r, ro);
-      const uint32_t y4 = *reinterpret_cast<const uint32_t *>(S.p[0] + ro[0] + 4 * G - S.ox[0]);
-      uint32_t w[4];
-      if (I.ncomp == 1) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) w[i] = ((y4 >> (8 * i)) & 255u) * 0x010101u;
-      } else {
-        // chroma bytes of the group's 4 pixels (replicated when half resolution)
-        uint32_t cb4, cr4;
-        if (half1) {
-          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[1] + ro[1] + 2 * G - S.ox[1]);
-          cb4 = __byte_perm(t, 0, 0x1100);
-        } else {
-          cb4 = *reinterpret_cast<const uint32_t *>(S.p[1] + ro[1] + 4 * G - S.ox[1]);
-        }
-        if (half2) {
-          const uint32_t t = *reinterpret_cast<const uint16_t *>(S.p[2] + ro[2] + 2 * G - S.ox[2]);
-          cr4 = __byte_perm(t, 0, 0x1100);
-        } else {
-          cr4 = *reinterpret_cast<const uint32_t *>(S.p[2] + ro[2] + 4 * G - S.ox[2]);
-        }
-        // colour terms per distinct chroma pair (pixels 2k, 2k+1 share one
-        // when both chroma planes are half resolution)
-        int dr[4], dg[4], db[4];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          if (i & 1 && half1 && half2) {
-            dr[i] = dr[i - 1]; dg[i] = dg[i - 1]; db[i] = db[i - 1];
-            continue;
-          }
-          const int cb = (int)((cb4 >> (8 * i)) & 255u) - 128;
-          const int cr = (int)((cr4 >> (8 * i)) & 255u) - 128;
-          dr[i] = (91881 * cr + 32768) >> 16;
-          dg[i] = (-22554 * cb - 46802 * cr + 32768) >> 16;
-          db[i] = (116130 * cb + 32768) >> 16;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const int yv = (int)((y4 >> (8 * i)) & 255u);
-          w[i] = (uint32_t)clamp255(yv + dr[i]) | ((uint32_t)clamp255(yv + dg[i]) << 8) |
-                 ((uint32_t)clamp255(yv + db[i]) << 16);
-        }
-      }
-      const int x = 4 * G - I.rx;
-      uint32_t *row = src + r * iw;
-      ESSL_CHECK(g_check_pix, (r + 1) * iw <= P.src_words, CK_SRC);
-#pragma unroll
-      for (int i = 0; i < 4; i++)
-        if ((unsigned)(x + i) < (unsigned)iw) row[x + i] = w[i];
-    }
-  } else {
-    // generic sampling factors: each thread keeps one column (its plane
-    // column offsets fixed) and walks rows, four in flight; no per-pixel
-    // division.
-    {
-      const int cpr = iw < kPixThreads ? iw : kPixThreads;   // columns per pass
-      const int rpp = iw < kPixThreads ? kPixThreads / iw : 1;  // rows per pass
-      const int r0 = threadIdx.x / cpr, x0 = threadIdx.x - r0 * cpr;
-      if (r0 < rpp) {
-        for (int x = x0; x < iw; x += cpr) {
-          int co[3];
-          S.col_off(I.rx + x, co);
-          for (int r = r0; r < nrows; r += 4 * rpp) {
-            int rr[4], gg[4], bb[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-              int ro[3];
-              S.row_off(I.ry + ys0 + min(r + u * rpp, nrows - 1), ro);
-              S.rgb_at(ro, co, rr[u], gg[u], bb[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-              if (r + u * rpp < nrows)
-                src[(r + u * rpp) * iw + x] = (uint32_t)rr[u] | ((uint32_t)gg[u] << 8) | ((uint32_t)bb[u] << 16);
-          }
-        }
-      }
-    }
-  }
+  // source rows -> RGBX words in shared memory (stage_rows)
+  stage_rows(I, S, ys0, nrows, src, P.src_words);
   // row taps of the band (imgops.py:37-41), shared by every column
   __shared__ int2 ry[kPairBandRows];
   __shared__ double rw[kPairBandRows];
