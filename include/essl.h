@@ -63,7 +63,7 @@ extern "C" {
 
 #define ESSL_OPT_DECODE_MODE 1
 #define ESSL_OPT_SEQ_BITS 2        /* minimum subsequence length per lane (bits, >= 32) */
-#define ESSL_OPT_CHECKPOINT_BITS 3 /* minimum checkpoint spacing (bits) */
+#define ESSL_OPT_CHECKPOINT_BITS 3 /* accepted and validated, no effect: every block start is a checkpoint */
 #define ESSL_OPT_PROFILE 4      /* 1: bracket every launch with CUDA events */
 #define ESSL_OPT_WARMUP_BITS 5  /* lanes start this far before their subsequence (0..4096) */
 #define ESSL_OPT_STAGE_BYTES 6  /* largest clean stream staged in shared memory (0: never) */

@@ -154,7 +154,7 @@ struct essl_ctx {
   uint64_t *d_offsets = nullptr;  // crop / dump output offsets
   int mode = kDefMode;
   int seq_bits = kDefSeqBits;
-  int ck_bits = kDefCkBits;
+  int ck_bits = kDefCkBits;  // (ESSL_OPT_CHECKPOINT_BITS: kept for the API, no effect)
   int warm_bits = kDefWarmBits;
   int stage_max = kDefStageBytes;
   int gather_ctas = kDefGatherCtas;  // k_host_gather grid (ESSL_OPT_GATHER_CTAS)
@@ -348,7 +348,6 @@ int launch_decode(essl_ctx *c, const uint8_t *blob, const essl_sample *d_desc, i
   p.s = c->s;
   p.mode = c->mode;
   p.seq_bits = c->seq_bits;
-  p.ck_bits = c->ck_bits;
   p.warm_bits = c->warm_bits;
   p.stage_bytes = c->stage_max;
   p.early_exit = c->early_exit;
@@ -422,15 +421,15 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
   CKC(cudaMalloc(&c->s.counters, 4 * sizeof(unsigned long long)));
   CKC(cudaMalloc(&c->s.info, sizeof(essl::ImgInfo) * max_batch));
   CKC(cudaMalloc(&c->s.hdr, essl::decode_hdr_bytes() * max_batch));
-  CKC(cudaMalloc(&c->s.ck, essl::ckpt_bytes() * essl::kEntropyLanes * essl::kCheckpoints * max_batch));
   CKC(cudaMalloc(&c->s.tabcache, essl::tabcache_bytes()));
   CKC(cudaMemset(c->s.tabcache, 0, essl::tabcache_bytes()));
-  // unit lists + block records per image: lanes x (cap + 8 + 2 (cap/2 + 10))
-  // u32, cap = (slen + warm + continuation)/4 + 68, lanes x slen <= 8 x payload
+  // unit lists + block records per image: lanes x (cap + 24 + 2 (cap/2 + 26)
+  // + 3) u32 (k_entropy's stride), cap = (slen + warm + continuation)/4 + 68,
+  // lanes x slen <= 8 x payload
   c->s.list_cap = (uint64_t)max_batch *
                   (4ull * max_payload + (uint64_t)essl::kEntropyLanes *
-                                            (2ull * ((essl::kMaxWarmBits + essl::kContinuationBits) / 4 + 68) + 32) + 8);
-  // (+ 4 words per entropy lane past the pool: overflow sinks)
+                                            (2ull * ((essl::kMaxWarmBits + essl::kContinuationBits) / 4 + 68) + 80) + 8);
+  // (+ 4 words per entropy lane past the pool: slack for the bounds checks)
   CKC(cudaMalloc(&c->s.list, (c->s.list_cap + 4 * essl::kEntropyLanes) * sizeof(uint32_t)));
   CKC(cudaMalloc(&c->d_offsets, sizeof(uint64_t) * max_batch));
   for (int r = 0; r < kDescRing; r++) {
@@ -478,7 +477,6 @@ int essl_ctx_destroy(essl_ctx *c) {
   cudaFree(c->s.counters);
   cudaFree(c->s.info);
   cudaFree(c->s.hdr);
-  cudaFree(c->s.ck);
   cudaFree(c->s.tabcache);
   cudaFree(c->s.list);
   cudaFree(c->d_offsets);

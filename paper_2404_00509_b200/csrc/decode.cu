@@ -67,7 +67,6 @@ constexpr int kCrcMaxChunks = 2048;      // payloads <= 256 KB use the table tre
 constexpr uint32_t kNoEnd = 0xFFFFFFF0u;
 constexpr int kNT = kDecodeThreads;
 constexpr int kLanes = kEntropyLanes;
-constexpr int kCk = kCheckpoints;  // checkpoints per lane
 constexpr uint32_t kContBits = kContinuationBits;
 
 // Huffman decode tables.  One 16-bit entry per kFastBits-bit lookahead:
@@ -137,10 +136,11 @@ struct __align__(16) DecodeHead {
   uint64_t coef_off[3], coef_base, clean_off;
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
   uint8_t zz[64];
-  int32_t q[3][64];  // dequantisation tables, natural order
 };
-// + the Huffman tables (k_prep builds them in global memory directly)
+// + the dequantisation and Huffman tables (k_prep writes them to global
+// memory directly; k_entropy's shared copy of the head leaves them out)
 struct __align__(16) DecodeHdr : DecodeHead {
+  int32_t q[3][64];  // dequantisation tables, natural order
   HuffTab tab[kMaxTables];
 };
 
@@ -524,10 +524,11 @@ constexpr int kGroup = 16;
 struct RingReader {
   const uint32_t *w;  // global words
   uint32_t cpad;      // first all-0xFF 16-byte chunk
-  uint32_t rs;        // this lane's ring (shared-window address)
+  uint32_t rs;        // this lane's ring (shared-window address, 128-byte aligned)
   uint32_t w0, w1, w2;
-  uint32_t o, q, p;   // bit offset in w0, word index of w0, bit position (32 q + o)
+  uint32_t o, qa, p;  // bit offset in w0, 4 x the word index of w2, bit position
   uint32_t lo, pend;  // ring window start (words, multiple of 8); quarters in flight
+  __device__ __forceinline__ uint32_t q() const { return (qa >> 2) - 2u; }  // word index of w0
   __device__ __forceinline__ uint32_t ld(uint32_t i) const { return lds_u32(rs + ((i & (kRingWords - 1)) << 2)); }
   // quarter j = words [8j, 8j + 8) = 16-byte chunks 2j, 2j + 1 (clamped to the
   // all-0xFF padding chunk past the data), one commit group
@@ -545,7 +546,8 @@ struct RingReader {
   }
   __device__ __forceinline__ void init(uint32_t pos) {
     asm volatile("cp.async.wait_group 0;" ::: "memory");  // this lane's copies in flight target the ring
-    q = pos >> 5;
+    const uint32_t q = pos >> 5;
+    qa = 4u * (q + 2u);
     o = pos & 31;
     p = pos;
     lo = q & ~7u;
@@ -560,6 +562,7 @@ struct RingReader {
   __device__ __forceinline__ void top_up() {
     // quarters below q + 3 are in registers or consumed: refetch them ahead
     // (a group advances q by at most kGroup words)
+    const uint32_t q = this->q();
     const bool f0 = lo + 8 <= q + 3;
     fetch(lo / 8 + kRingWords / 8, f0);
     lo += f0 ? 8u : 0u;
@@ -592,10 +595,10 @@ struct RingReader {
     p += bits;
     if (o >= 32) {
       o -= 32;
-      q++;
+      qa += 4;
       w0 = w1;
       w1 = w2;
-      w2 = ld(q + 2);
+      w2 = lds_u32((qa & 4u * (kRingWords - 1)) | rs);
     }
   }
 };
@@ -642,7 +645,7 @@ struct EntCtx {
   uint32_t zz_s;        // zig-zag -> natural table (shared-window address)
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
   int c1, c2, bpm, gx;
-  uint32_t cbits, limit, ck_bits;
+  uint32_t cbits, limit;
   uint32_t cend;  // end of the range phase 1 covers (N2 estimate; cbits without it)
   const uint32_t *list_lo, *list_hi;  // the unit-list pool incl. overflow sinks (ESSL_CHECK)
   const int16_t *coef_lo, *coef_hi;   // the coefficient scratch (ESSL_CHECK)
@@ -725,32 +728,29 @@ __device__ __forceinline__ int entry_value(uint32_t e) { return extend_raw(e & 0
 __device__ __forceinline__ int entry_zz(uint32_t e) { return (int)min(e >> 20, 64u) - 1; }
 constexpr uint32_t kEntrySentinel = 1u << 20;  // a DC entry: ends the last block
 
-// Checkpoint: the decoder state at a block start of a lane's path, with the
-// path's unit-list index and block count there.
-struct __align__(16) Ckpt {
-  uint32_t pb;   // bit position << 6 | block-in-MCU
-  uint32_t ord;  // index of the block's record in the lane's block list
-  uint32_t nblk;
-  uint32_t pad;
-};
+// Block record: {index of the block's DC entry in the lane's unit list,
+// pb = bit position of the block start << 6 | block-in-MCU}.  Every block
+// start of a lane's path gets one, so the records double as the path's
+// checkpoints: record m of a list is the decoder state after m complete
+// blocks (a list always begins at a block start).
 
 // Per-lane record (shared memory).
 struct LaneRec {
-  // phase 1 (decode from a guess): stop state, blocks, checkpoints, list
-  // length, lane-0 error
+  // phase 1 (decode from a guess): stop state, blocks, usable block records
+  // (checkpoints), list length, lane-0 error
   uint32_t xp, nblk, nck, errp, nlist, nbs;
-  int32_t xk, xb, err, ovf, xbe;
+  int8_t xk, xb, err, ovf, xbe;
   // phase 2 (continuation): 0 merged into checkpoint (cj, cm), 1 decode error
   // at cp, 2 end of data at cp (state ek, eb)
-  int32_t cst, cbe;
-  uint32_t cj, cm, cn, cp, ek, eb;
+  int8_t cst, cbe, ek, eb;
+  uint32_t cj, cm, cn, cp, cpb;  // (cpb: the merge record's pb)
   // resolution: the lane's segment of the exact path
   uint32_t w_ord, w_p, w_b, w_A, w_nb;
 };
 
 // Phase 1 (CONT=false): decode [p0, send) from the guess (k=0, b=0), storing
-// every unit in the lane's list and recording a checkpoint at the first block
-// start after every ck_bits.  Lane 0 starts at the exact state, so an error
+// every unit in the lane's list and a record (= checkpoint) at every block
+// start.  Lane 0 starts at the exact state, so an error
 // there is the reference's error; other lanes re-guess one bit later and drop
 // their list and checkpoints (the path before an error is not a decode path),
 // except at the end of the data (the fill bits after the final block), where
@@ -768,17 +768,16 @@ __device__ __forceinline__ void refill_of(RingReader &) {}
 
 template <bool CONT, bool SH>
 __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t sbeg, uint32_t send,
-                         uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, Ckpt *ck_all,
-                         LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
+                         uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, const uint2 *bsl0,
+                         uint32_t bstride, LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
   // SH: the ring reader (shared-memory window, grouped maintenance); !SH:
   // plain global reads (validation)
   using Rd = typename std::conditional<SH, RingReader, Reader<false>>::type;
   Rd r;
   int k, b;
-  uint32_t nblk, nl, nbs, nck = 0, ck_next = p0;
+  uint32_t nblk, nl, nbs;
   int be = 0;
-  Ckpt *ck = ck_all + lane * kCk;
-  // continuation cursor over later lanes' checkpoints
+  // continuation cursor over later lanes' block records
   int j = lane + 1;
   uint32_t m = 0, jn = 0, cand = 0xFFFFFFFFu;
   if (CONT) {
@@ -807,7 +806,9 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
         jn = Ls[j].nck;
         continue;
       }
-      cand = ck_all[j * kCk + m].pb;
+      ESSL_CHECK(g_check_dec, (const uint32_t *)(bsl0 + j * bstride + m) >= C.list_lo &&
+                                  (const uint32_t *)(bsl0 + j * bstride + m + 1) <= C.list_hi, CK_CKPT);
+      cand = bsl0[j * bstride + m].y;
       if ((cand >> 6) >= q) return;
       m++;
     }
@@ -820,7 +821,7 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     // is never part of the exact path through this lane's list: the
     // previous lane's continuation starts at sbeg, so it can only merge at
     // a checkpoint at or after sbeg.  Stop at the first block start at or
-    // after sbeg and record a checkpoint there, where the list begins.
+    // after sbeg, where the list (and its first record) begins.
     bool stop = false, done = false;
 #pragma unroll 1
     while (!done) {
@@ -857,21 +858,29 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
         if (bend && r.p >= sbeg) { done = true; break; }
       }
     }
-    if (stop) {
-      send = 0;  // the main loop does not run; the lane's path ends here
-    } else {
-      ck[0] = Ckpt{(r.p << 6) | (uint32_t)b, 0u, nblk, 0u};
-      nck = 1;
-      ck_next = r.p + C.ck_bits;
-    }
+    if (stop) send = 0;  // the main loop does not run; the lane's path ends here
+    nblk = 0;              // (blocks count from the list start)
   }
-  uint32_t *lp = list + min(nl, cap);
-  uint2 *bp = bsl + min(nbs, bcap);
+  // Capacity and the stop position are checked once per group of kGroup
+  // units: a group that might not fit stores into the kGroup-slot sinks past
+  // the list / record capacities (the lists are then incomplete: ovf), and a
+  // lane stops at the end of the group that reaches `send` (decoding a few
+  // units further is harmless: the path is the same).
+  uint32_t *lp = list + nl;
+  uint2 *bp = bsl + nbs;
+  bool sink = false;
+  uint32_t nrec_ok = 0xFFFFFFFFu;  // records stored before the sinks took over
   bool run = r.p < send;
 #pragma unroll 1
   while (run) {
     top_up_of(r);
-#pragma unroll 1
+    if (nl + kGroup > cap || nbs + kGroup > bcap) {
+      if (!sink) nrec_ok = nbs;
+      lp = list + cap;
+      bp = bsl + bcap;
+      sink = true;
+    }
+#pragma unroll 2
     for (int u = 0; u < kGroup; u++) {
       refill_of(r);
       const uint32_t hi = r.hi();
@@ -905,8 +914,8 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
           nbs = 0;
           lp = list;
           bp = bsl;
-          nck = 0;
-          ck_next = r.p;
+          sink = false;
+          nrec_ok = 0xFFFFFFFFu;
           run = r.p < send;
           break;  // (a fresh ring: maintenance restarts)
         }
@@ -914,13 +923,13 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
       const uint32_t raw = unit_raw(hi, tot, size);
       ESSL_CHECK(g_check_dec, lp >= C.list_lo && lp < C.list_hi, CK_LIST);
       *lp = unit_entry(raw, size, knew);
-      if (k == 0) {  // block record: where the block's units start, its DC difference (raw)
+      if (k == 0) {  // block record: where the block's units start, the block start state
         ESSL_CHECK(g_check_dec, (const uint32_t *)bp >= C.list_lo && (const uint32_t *)(bp + 1) <= C.list_hi, CK_LIST);
-        *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
-        bp += nbs < bcap;
+        *bp = make_uint2(nl, (r.p << 6) | (uint32_t)b);
+        bp++;
         nbs++;
       }
-      lp += nl < cap;  // past the capacity every store lands on the sink slot
+      lp++;
       nl++;
       r.skip(tot);
       be = knew >= 64;
@@ -928,31 +937,25 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
       k = be ? 0 : knew;
       b = be ? bn : b;
       nblk += be;
-      const uint32_t pb = (r.p << 6) | (uint32_t)b;
-      if (CONT) {
-        if (be) {
-          if ((cand >> 6) < r.p) seek(r.p);
-          if (cand == pb) { st = 0; run = false; break; }
-        }
-      } else if (be && r.p >= ck_next && nck < (uint32_t)kCk) {
-        ESSL_CHECK(g_check_dec, nck < (uint32_t)kCk, CK_CKPT);
-        ck[nck] = Ckpt{pb, nbs, nblk, 0u};
-        nck++;
-        ck_next = r.p + C.ck_bits;
+      if (CONT && be) {
+        if ((cand >> 6) < r.p) seek(r.p);
+        if (cand == ((r.p << 6) | (uint32_t)b)) { st = 0; run = false; break; }
       }
-      if (r.p >= send) { run = false; break; }
     }
+    if (r.p >= send) run = false;
   }
-  const bool ovf = nl >= cap || nbs > bcap;  // (slot cap is the sink; keep one for the sentinel)
+  const bool ovf = sink;
+  asm volatile("cp.async.wait_all;" ::: "memory");  // the ring is reused after phase 2 (DC sums)
   if (CONT) {
-    R.cst = st;
+    R.cst = (int8_t)st;
     R.cj = (uint32_t)j;
     R.cm = m;
+    R.cpb = cand;
     R.cn = nblk;
     R.cp = st == 1 ? R.errp : r.p;
-    R.ek = (uint32_t)k;
-    R.eb = (uint32_t)b;
-    R.cbe = be;
+    R.ek = (int8_t)k;
+    R.eb = (int8_t)b;
+    R.cbe = (int8_t)be;
     R.nlist = nl;
     R.nbs = nbs;
     if (ovf) R.ovf = 1;
@@ -962,11 +965,11 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
     atomicMax(dbg + 2, nl);
     R.err = st == 1;
     R.xp = r.p;
-    R.xk = k;
-    R.xb = b;
-    R.xbe = be;
+    R.xk = (int8_t)k;
+    R.xb = (int8_t)b;
+    R.xbe = (int8_t)be;
     R.nblk = nblk;
-    R.nck = nck;
+    R.nck = min(nbs, nrec_ok);  // records a continuation may merge into
     R.nlist = nl;
     R.nbs = nbs;
     R.ovf = ovf;
@@ -1015,7 +1018,7 @@ __device__ int extend_path(const EntCtx &C, uint32_t *list, uint32_t cap, uint2 
     *lp = unit_entry(raw, size, knew);
     if (isdc) {
       ESSL_CHECK(g_check_dec, (const uint32_t *)bp >= C.list_lo && (const uint32_t *)(bp + 1) <= C.list_hi, CK_LIST);
-      *bp = make_uint2(nl, raw | ((uint32_t)size << 16));
+      *bp = make_uint2(nl, (r.p << 6) | (uint32_t)b);
       bp += nbs < bcap;
       nbs++;
     }
@@ -1148,14 +1151,13 @@ __device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, u
 
 // DC pass A over a segment's block records (nb blocks from record `ord`,
 // block-in-MCU b0): the segment's DC-difference sums per scan slot.
-__device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int b0, uint32_t nb,
-                            int32_t sum[3]) {
+__device__ void seg_dc_sums(const EntCtx &C, const uint32_t *list, const uint2 *bsl, uint32_t ord, int b0,
+                            uint32_t nb, int32_t sum[3]) {
   int b = b0;
   int32_t s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll 4
   for (uint32_t i = 0; i < nb; i++) {
-    const uint32_t ry = bsl[ord + i].y;
-    const int32_t v = extend_raw(ry & 0x7FFFu, ry >> 16);
+    const int32_t v = entry_value(list[bsl[ord + i].x]);
     const int s = (b >= C.c1) + (b >= C.c2);
     s0 += s == 0 ? v : 0;
     s1 += s == 1 ? v : 0;
@@ -1172,8 +1174,8 @@ __device__ void seg_dc_sums(const EntCtx &C, const uint2 *bsl, uint32_t ord, int
 // gets its table entry {global unit-list index of its DC entry, DC value} in
 // the first 8 bytes of its coefficient slot (k_idct gathers the block from
 // the list).
-__device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, const uint2 *bsl,
-                          uint32_t ord, uint32_t lgbase, int b0, uint32_t A, uint32_t nb,
+__device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, const uint32_t *list,
+                          const uint2 *bsl, uint32_t ord, uint32_t lgbase, int b0, uint32_t A, uint32_t nb,
                           uint32_t nrec, uint32_t nlist, const int32_t base[3], int &range) {
   const uint32_t mcu = A / (uint32_t)C.bpm;
   int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
@@ -1183,7 +1185,7 @@ __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, c
   for (uint32_t i = 0; i < nb; i++) {
     const uint2 rec = bsl[ord + i];
     const int s = (b >= C.c1) + (b >= C.c2);
-    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + extend_raw(rec.y & 0x7FFFu, rec.y >> 16);
+    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + entry_value(list[rec.x]);
     p0 = s == 0 ? pv : p0;
     p1 = s == 1 ? pv : p1;
     p2 = s == 2 ? pv : p2;
@@ -1749,7 +1751,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       const int pos = tq <= 15 ? PS.quant_pos[tq] : -1;
       int v = 0;
       if (pos >= 0) v = PS.quant_pq[tq] == 1 ? ((raw[pos + 2 * k] << 8) | raw[pos + 2 * k + 1]) : raw[pos + k];
-      H.q[c][c_zz[k]] = v;
+      G->q[c][c_zz[k]] = v;
     }
   }
 
@@ -2068,7 +2070,8 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
 // ===========================================================================
 // k_entropy: entropy decode, one warp per image
 // ===========================================================================
-struct __align__(16) EntSmem {
+struct __align__(128) EntSmem {
+  uint32_t ring[kLanes][kRingWords];  // (128-byte aligned: RingReader::skip masks addresses)
   DecodeHead h;
   uint16_t tab[kSmemTabs][1 << kFastBits];  // first-level tables (<= kSmemTabs used)
   LaneRec lane[kLanes];
@@ -2077,10 +2080,8 @@ struct __align__(16) EntSmem {
   int coef_range, red;
   unsigned int dbg_units, dbg_guess, dbg_umax, dbg_ext;
   unsigned long long lbase;
-  int32_t dcsum[kLanes * 3];
   int fmt;
   int ms_nscan, ms_nlevel, ms_range;
-  __align__(16) uint32_t ring[kLanes][kRingWords];
   long long t_ph[8];
 };
 
@@ -2712,15 +2713,15 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
     nseq = max(1, min(nseq, kLanes));
     const uint32_t slen = (end_bits + nseq - 1) / nseq;
     const uint32_t warm = min((uint32_t)P.warm_bits, slen * 4);
-    C.ck_bits = max((uint32_t)P.ck_bits, (slen + kCk - 9) / (kCk - 8));  // checkpoints cover [sbeg, send)
-    Ckpt *ck_all = P.s.ck + (size_t)img * kLanes * kCk;
     // unit lists + block records: one region per lane, carved per image.
     // Lists hold every decoded unit; slot cap is a sink for overflow and the
     // slot after the last unit holds a sentinel.  (No room: one-entry sinks,
     // the image falls back to a serial re-decode.)
     const uint32_t cap = ((slen + warm + kContBits) / 4 + 64 + 3) & ~3u;
     const uint32_t bcap = cap / 2 + 8;  // a block has >= 2 units (DC + an AC unit)
-    const uint32_t stride = cap + 8 + ((2 * (bcap + 2) + 3) & ~3u);
+    // list: cap entries + a kGroup-slot sink (+ sentinel / pad); records: bcap +
+    // a kGroup-slot sink (the pool is sized for this stride: api.cu list_cap)
+    const uint32_t stride = cap + kGroup + 8 + ((2 * (bcap + kGroup + 2) + 3) & ~3u);
     if (lane == 0) {
       const unsigned long long need = (unsigned long long)nseq * stride;
       const unsigned long long b = atomicAdd(&P.s.counters[3], need + 4);
@@ -2729,22 +2730,38 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
       S.red = 0;
     }
     __syncthreads();
-    const bool lists_ok = S.lbase != ~0ull;
-    const unsigned long long lreg = lists_ok ? S.lbase + (unsigned long long)lane * stride : 0ull;
-    uint32_t *sink = P.s.list + P.s.list_cap + 4 * lane;  // 4 words per lane past the pool
-    uint32_t *list = lists_ok ? P.s.list + lreg : sink;
-    uint2 *bsl = reinterpret_cast<uint2 *>(lists_ok ? P.s.list + lreg + cap + 8 : sink + 2);
-    const uint32_t lcap = lists_ok ? cap : 0u, lbcap = lists_ok ? bcap : 0u;
+    if (S.lbase == ~0ull) {
+      // no room in the list pool: serial decode (the ESSL_DECODE_SERIAL path)
+      zero_window(H, coef, lane);
+      __syncthreads();
+      if (lane == 0) {
+        int32_t pred[3] = {0, 0, 0};
+        write_run<SH>(C, H, coef, 0, 0, 0, H.limit_blocks, pred, wo, &S.p_final);
+        if (wo.err) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, wo.errp));
+        else if (S.p_final > H.clean_bits) ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
+        if (wo.range) S.coef_range = 1;
+      }
+      return;
+    }
+    const unsigned long long lreg = S.lbase + (unsigned long long)lane * stride;
+    uint32_t *list = P.s.list + lreg;
+    uint2 *bsl = reinterpret_cast<uint2 *>(P.s.list + lreg + cap + kGroup + 8);
+    // every lane's block records (the continuations' merge targets): lane j's
+    // at bsl0 + j * bstride
+    const uint2 *bsl0 = reinterpret_cast<const uint2 *>(P.s.list + S.lbase + cap + kGroup + 8);
+    const uint32_t bstride = stride / 2;
     if (lane < nseq) {
       const uint32_t sbeg = lane * slen;
       const uint32_t send = lane == nseq - 1 ? end_bits : min(end_bits, (lane + 1) * slen);
       const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
-      run_path<false, SH>(C, lane, nseq, p0, sbeg, send, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
+      run_path<false, SH>(C, lane, nseq, p0, sbeg, send, list, cap, bsl, bcap, bsl0, bstride, S.lane, R,
+                          &S.dbg_units);
     }
     __syncthreads();
     PHASE(2);
     const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
-    if (cont) run_path<true, SH>(C, lane, nseq, 0, 0, 0, list, lcap, bsl, lbcap, ck_all, S.lane, R, &S.dbg_units);
+    if (cont)
+      run_path<true, SH>(C, lane, nseq, 0, 0, 0, list, cap, bsl, bcap, bsl0, bstride, S.lane, R, &S.dbg_units);
     dbg_nseq = (uint32_t)nseq;
     if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
     __syncthreads();
@@ -2782,14 +2799,12 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
         if (open_end && A + seg < limit && X.p < cbits) {
           // it stopped at the estimated end before the crop's last needed
           // block: extend the exact path, appending to this lane's lists
-          const unsigned long long lr = lists_ok ? S.lbase + (unsigned long long)o * stride : 0ull;
-          uint32_t *lo = lists_ok ? P.s.list + lr : P.s.list + P.s.list_cap + 4 * o;
-          uint2 *bo = reinterpret_cast<uint2 *>(lists_ok ? P.s.list + lr + cap + 8
-                                                         : P.s.list + P.s.list_cap + 4 * o + 2);
+          const unsigned long long lr = S.lbase + (unsigned long long)o * stride;
+          uint32_t *lo = P.s.list + lr;
+          uint2 *bo = reinterpret_cast<uint2 *>(P.s.list + lr + cap + kGroup + 8);
           uint32_t added = 0;
           int ovf = 0;
-          const int xs = extend_path<SH>(C, lo, lists_ok ? cap : 0u, bo, lists_ok ? bcap : 0u, L.nlist,
-                                         L.nbs, X, limit - (A + seg), added, ovf);
+          const int xs = extend_path<SH>(C, lo, cap, bo, bcap, L.nlist, L.nbs, X, limit - (A + seg), added, ovf);
           S.dbg_ext += 1;
           seg += added;
           if (ovf) {
@@ -2823,12 +2838,14 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
           break;
         }
         A += seg;
-        const Ckpt c = ck_all[L.cj * kCk + L.cm];
+        // merged into record cm of lane cj: the exact path continues there,
+        // after cm complete blocks of that lane's list
+        const uint32_t pb = L.cpb;  // == bsl0[L.cj * bstride + L.cm].y
         o = (int)L.cj;
-        sord = c.ord; sp = c.pb >> 6; sb = c.pb & 63; snb = c.nblk;
+        sord = L.cm; sp = pb >> 6; sb = pb & 63; snb = L.cm;
       }
-      if (!lists_ok) S.fmt = 0;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // (lane 0's serial readers: the rings are reused below)
     __syncthreads();
     PHASE(4);
     const bool own = S.status == 0 && R.w_nb > 0;
@@ -2837,16 +2854,16 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
       // block tables: each segment's DC continues from the earlier segments'
       // DC sums (segments are in lane order)
       int32_t sum[3] = {0, 0, 0};
-      if (own) seg_dc_sums(C, bsl, R.w_ord, (int)R.w_b, R.w_nb, sum);
-      int32_t *dcs = S.dcsum;
+      if (own) seg_dc_sums(C, list, bsl, R.w_ord, (int)R.w_b, R.w_nb, sum);
+      int32_t *dcs = reinterpret_cast<int32_t *>(&S.ring[0][0]);  // (the read rings are idle now: run_path drained its copies)
       for (int q = 0; q < 3; q++) dcs[lane * 3 + q] = sum[q];
       __syncthreads();
       if (own) {
         int32_t base[3] = {0, 0, 0};
         for (int t = 0; t < lane; t++)
           for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
-        seg_table(C, H, coef, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb,
-                  min(R.nbs, lbcap), R.nlist, base, range);
+        seg_table(C, H, coef, list, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb,
+                  min(R.nbs, bcap), R.nlist, base, range);
       }
     } else if (S.status == 0) {
       // fallback (an owner's unit list overflowed): serial re-decode into
@@ -2926,7 +2943,6 @@ __global__ void __launch_bounds__(kLanes, 12) k_entropy(DecodeParams P) {
   C.coef_hi = P.s.coef + P.s.coef_cap;
   C.words = reinterpret_cast<const uint32_t *>(P.s.clean + H.clean_off);
   C.wmax = H.wmax;
-  C.ck_bits = 0;
   uint32_t dbg_nseq = 0, dbg_cont = 0;
   // per-lane read rings (cp.async) unless the validation option asks for
   // plain global reads
@@ -3146,7 +3162,6 @@ void launch_dump_coefs(const Scratch &sc, int n, int16_t *out, const uint64_t *o
 constexpr int kMaxDynSmem = 160 * 1024;
 
 size_t decode_hdr_bytes() { return sizeof(DecodeHdr); }
-size_t ckpt_bytes() { return sizeof(Ckpt); }
 size_t tabcache_bytes() { return sizeof(TabCacheSlot) * kMaxTables; }
 
 void launch_prep(const DecodeParams &p0, cudaStream_t st, int max_len) {

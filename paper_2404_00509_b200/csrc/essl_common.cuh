@@ -20,7 +20,7 @@ enum CheckId : int {
   CK_CLEAN = 4,    // k_prep clean-stream bytes / restart table
   CK_SRC = 5,      // k_resize shared source-row staging
   CK_OUT = 6,      // k_resize output stores
-  CK_CKPT = 7,     // k_entropy checkpoints
+  CK_CKPT = 7,     // k_entropy checkpoint (block record) reads of later lanes
   CK_COUNT = 16,
 };
 #ifdef ESSL_CHECKED
@@ -36,10 +36,7 @@ enum CheckId : int {
 void check_read_decode(unsigned int *out, bool reset);
 void check_read_pixels(unsigned int *out, bool reset);
 
-struct Ckpt;
-
 constexpr int kDecodeThreads = 256;  // k_prep: one CTA per image
-constexpr int kCheckpoints = 64;     // k_entropy: checkpoints per lane
 constexpr int kEntropyLanes = 64;     // k_entropy: subsequences (threads) per image
 constexpr int kContinuationBits = 8192;  // k_entropy: list room per lane for its continuation
 constexpr int kMaxWarmBits = 4096;
@@ -93,7 +90,6 @@ struct Scratch {
   unsigned long long *counters;  // [0] clean bytes, [1] coef elems, [2] plane bytes, [3] list entries
   ImgInfo *info;
   uint8_t *hdr;  // per-image DecodeHdr handed from k_prep to k_entropy
-  struct Ckpt *ck;  // per-image checkpoints [32 lanes][kCheckpoints] (k_entropy)
   uint32_t *list;   // unit lists (k_entropy), carved per image with counters[3]
   uint64_t list_cap;  // entries
   uint8_t *tabcache;  // built Huffman tables reused across images (k_prep; tabcache_bytes())
@@ -141,7 +137,6 @@ struct DecodeParams {
   Scratch s;
   int mode;          // ESSL_DECODE_*
   int seq_bits;      // minimum subsequence length per lane (bits)
-  int ck_bits;       // minimum checkpoint spacing (bits)
   int warm_bits;     // each lane (but lane 0) starts this far before its subsequence
   int stage_bytes;   // k_entropy read rings (0: plain global reads)
   int early_exit;    // k_entropy: phase 1 stops near the crop's last needed block (N2)
@@ -218,7 +213,6 @@ void launch_prep(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_entropy(const DecodeParams &p, cudaStream_t st, int max_len);
 void launch_idct(const DecodeParams &p, cudaStream_t st);
 size_t decode_hdr_bytes();
-size_t ckpt_bytes();
 size_t tabcache_bytes();
 void launch_resize(const PixelParams &p, cudaStream_t st);
 void launch_aug(const AugOutParams &p, int max_radius, cudaStream_t st);

@@ -68,12 +68,13 @@ int essl_epoch_permutation(uint64_t seed, uint64_t epoch, int64_t n, int64_t *ou
   return ESSL_OK;
 }
 
-// pipeline.py:51-75
-int essl_sample_rrc(uint64_t *st, int64_t src_w, int64_t src_h, double scale_lo, double scale_hi,
-                    double ratio_lo, double ratio_hi, int max_attempts, int32_t *xywh) {
-  if (!st || !xywh || src_w < 1 || src_h < 1) return ESSL_E_ARG;
+namespace {
+// pipeline.py:51-75 with log(ratio) precomputed (the batch path computes the
+// two logs once per batch; same values)
+int sample_rrc_logs(uint64_t *st, int64_t src_w, int64_t src_h, double scale_lo, double scale_hi,
+                    double ratio_lo, double ratio_hi, double log_lo, double log_hi, int max_attempts,
+                    int32_t *xywh) {
   const double area = (double)(src_w * src_h);
-  const double log_lo = std::log(ratio_lo), log_hi = std::log(ratio_hi);
   for (int a = 0; a < max_attempts; a++) {
     const double target = area * (scale_lo + (scale_hi - scale_lo) * rnd(st));
     const double aspect = std::exp(log_lo + (log_hi - log_lo) * rnd(st));
@@ -102,19 +103,29 @@ int essl_sample_rrc(uint64_t *st, int64_t src_w, int64_t src_h, double scale_lo,
   xywh[2] = (int32_t)w; xywh[3] = (int32_t)h;
   return ESSL_OK;
 }
+}  // namespace
+
+// pipeline.py:51-75
+int essl_sample_rrc(uint64_t *st, int64_t src_w, int64_t src_h, double scale_lo, double scale_hi,
+                    double ratio_lo, double ratio_hi, int max_attempts, int32_t *xywh) {
+  if (!st || !xywh || src_w < 1 || src_h < 1) return ESSL_E_ARG;
+  return sample_rrc_logs(st, src_w, src_h, scale_lo, scale_hi, ratio_lo, ratio_hi, std::log(ratio_lo),
+                         std::log(ratio_hi), max_attempts, xywh);
+}
 
 // Loader._fill_sample draws (pipeline.py:221-222, 86-87) for a batch.
 int essl_rrc_batch(uint64_t seed, uint64_t epoch, const int64_t *indices, int n,
                    const uint16_t *widths, const uint16_t *heights, double scale_lo,
                    double scale_hi, double ratio_lo, double ratio_hi, essl_sample *samples) {
   if (n < 0 || (n > 0 && (!indices || !widths || !heights || !samples))) return ESSL_E_ARG;
+  const double log_lo = std::log(ratio_lo), log_hi = std::log(ratio_hi);
   for (int i = 0; i < n; i++) {
     const int64_t idx = indices[i];
     uint64_t st = essl_rng_init(seed, epoch, (uint64_t)idx, 0);
     int32_t r[4];
-    int rc = essl_sample_rrc(&st, widths[idx], heights[idx], scale_lo, scale_hi, ratio_lo,
-                             ratio_hi, 10, r);
-    if (rc) return rc;
+    if (widths[idx] < 1 || heights[idx] < 1) return ESSL_E_ARG;
+    sample_rrc_logs(&st, widths[idx], heights[idx], scale_lo, scale_hi, ratio_lo, ratio_hi, log_lo, log_hi,
+                    10, r);
     samples[i].x = r[0]; samples[i].y = r[1]; samples[i].w = r[2]; samples[i].h = r[3];
     samples[i].flip = rnd(&st) < 0.5 ? 1 : 0;
   }

@@ -32,6 +32,18 @@ def main():
     for p in pend:
         ld.finish(p)
     torch.cuda.synchronize()
+    # the native call alone, timed inside the Python enqueue
+    lib = N.lib()
+    native_fn = lib.essl_batch_enqueue
+    tn = []
+
+    class _Timed:
+        def __call__(self, *a):
+            t0 = time.perf_counter()
+            r = native_fn(*a)
+            tn.append(time.perf_counter() - t0)
+            return r
+    lib.essl_batch_enqueue = _Timed()
     # whole Python enqueue
     t = []
     pend = []
@@ -54,7 +66,9 @@ def main():
         N.lib().essl_rrc_batch(0, i, N.ptr(idx[i % 8]), 256, N.ptr(w), N.ptr(h), 0.08, 1.0, 0.75,
                                4 / 3, N.ptr(s))
         r.append(time.perf_counter() - t0)
+    lib.essl_batch_enqueue = native_fn
     out = {"enqueue_ms_median": 1e3 * float(np.median(t)), "enqueue_ms_p90": 1e3 * float(np.percentile(t, 90)),
+           "native_call_ms_median": 1e3 * float(np.median(tn)),
            "rrc_batch_ms_median": 1e3 * float(np.median(r))}
     print(json.dumps(out))
 
