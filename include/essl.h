@@ -357,11 +357,18 @@ typedef struct {
   void *tokens;                /* DEVICE bf16 visible tokens [n, N-k, patch^2*3], or NULL */
   essl_result *results;        /* DEVICE [n] */
   essl_result *results_host;   /* HOST pinned [n] copy of results, or NULL */
+  void *wait_stream;           /* cudaStream_t whose work so far precedes this batch's
+                                  work on `stream` (the consumer's stream), or NULL */
 } essl_batch_io;
 
 int essl_batch_enqueue(essl_ctx *ctx, const essl_dataset *ds, const essl_batch_cfg *cfg,
                        const int64_t *indices, int n, const essl_batch_io *io,
                        void *stream);
+
+/* ABI check for bindings: sizeof of the public structs, in the order
+ * essl_sample, essl_result, essl_aug, essl_batch_cfg, essl_batch_io.
+ * Writes min(n, 5) sizes; returns 5. */
+int essl_abi_sizes(int64_t *out, int n);
 
 /* ---- host-side sampling (C++, glibc libm: bit-exact with CPython) ---------
  * Replace rng.py:27-87 and pipeline.py:51-87. */

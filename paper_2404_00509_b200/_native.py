@@ -47,7 +47,7 @@ EXPORTS = (
     "essl_mask_count", "essl_encode_jpeg", "essl_synth_image", "essl_decode_rrc_aug",
     "essl_augment_u8", "essl_aug_draw", "essl_aug_batch", "essl_debug_lanes",
     "essl_trace_read", "essl_memcpy_async", "essl_option_default",
-    "essl_decode_rrc_visible", "essl_dataset_create", "essl_dataset_destroy", "essl_batch_enqueue",
+    "essl_decode_rrc_visible", "essl_dataset_create", "essl_dataset_destroy", "essl_batch_enqueue", "essl_abi_sizes",
     "essl_check_read",
 )
 
@@ -92,7 +92,7 @@ class EsslBatchIo(ctypes.Structure):
                 ("u8", ctypes.c_void_p), ("index_label", ctypes.c_void_p), ("mask", ctypes.c_void_p),
                 ("ids_keep", ctypes.c_void_p), ("ids_restore", ctypes.c_void_p),
                 ("tokens", ctypes.c_void_p), ("results", ctypes.c_void_p),
-                ("results_host", ctypes.c_void_p)]
+                ("results_host", ctypes.c_void_p), ("wait_stream", ctypes.c_void_p)]
 
 
 SAMPLE_NP_DTYPE = None  # filled lazily (numpy view of EsslSample arrays)
@@ -183,6 +183,7 @@ def lib():
         "essl_dataset_create": (i32, [i64, P, P, P, P, P, P, P]),
         "essl_dataset_destroy": (i32, [P]),
         "essl_batch_enqueue": (i32, [P, P, P, P, i32, P, P]),
+        "essl_abi_sizes": (i32, [P, i32]),
         "essl_check_read": (i32, [P, i32, i32]),
         "essl_decode_rrc_visible": (i32, [P, P, P, P, i32, i32, i32, P, i64, P, i32, P, i32, P,
                                           P, P]),

@@ -134,6 +134,7 @@ struct essl_ctx {
   essl_sample *h_desc[kDescRing] = {};
   essl_sample *d_desc[kDescRing] = {};
   cudaEvent_t ev_desc[kDescRing] = {};
+  cudaEvent_t ev_wait = nullptr;  // essl_batch_enqueue's wait on the consumer stream
   bool desc_used[kDescRing] = {};
   int desc_next = 0;
   int64_t *h_il[kDescRing] = {};    // essl_batch_enqueue: indices + labels, same ring slots
@@ -440,6 +441,7 @@ int essl_ctx_create(int device, int max_batch, int max_side, int max_payload, in
     CKC(cudaMallocHost(&c->h_il[r], 2 * sizeof(int64_t) * max_batch));
     CKC(cudaMalloc(&c->d_aug[r], sizeof(essl_aug) * max_batch));
   }
+  CKC(cudaEventCreateWithFlags(&c->ev_wait, cudaEventDisableTiming));
   c->stage_cap = (uint64_t)max_batch * (((uint64_t)max_payload + 63) / 64 * 64);
   for (int r = 0; r < 2; r++) {
     CKC(cudaMallocHost(&c->h_stage[r], c->stage_cap));
@@ -477,6 +479,7 @@ int essl_ctx_destroy(essl_ctx *c) {
   cudaFree(c->s.counters);
   cudaFree(c->s.info);
   cudaFree(c->s.hdr);
+  if (c->ev_wait) cudaEventDestroy(c->ev_wait);
   cudaFree(c->s.tabcache);
   cudaFree(c->s.list);
   cudaFree(c->d_offsets);
@@ -593,6 +596,13 @@ int essl_check_read(uint32_t *out, int n, int reset) {
 #else
   return 0;
 #endif
+}
+
+int essl_abi_sizes(int64_t *out, int n) {
+  const int64_t sz[5] = {(int64_t)sizeof(essl_sample), (int64_t)sizeof(essl_result), (int64_t)sizeof(essl_aug),
+                         (int64_t)sizeof(essl_batch_cfg), (int64_t)sizeof(essl_batch_io)};
+  for (int i = 0; i < n && i < 5; i++) out[i] = sz[i];
+  return 5;
 }
 
 int essl_option_default(int option, int64_t *value) {
@@ -1114,6 +1124,10 @@ int essl_batch_enqueue(essl_ctx *c, const essl_dataset *ds, const essl_batch_cfg
   if (n == 0) return ESSL_OK;
   NvtxRange nv_("essl_batch_enqueue");
   cudaStream_t st = (cudaStream_t)stream;
+  if (io->wait_stream && io->wait_stream != stream) {
+    CK(cudaEventRecord(c->ev_wait, (cudaStream_t)io->wait_stream));
+    CK(cudaStreamWaitEvent(st, c->ev_wait, 0));
+  }
   const int r = pick_slot(c);  // the batch that last used slot r has completed
   if (r < 0) return r;
   // descriptors: record fields + RRC rect and flip (host C++, pipeline.py:219-227)

@@ -37,6 +37,17 @@ def test_native_exports_every_declared_symbol(native):
     assert native.option_default(native.ESSL_OPT_DECODE_MODE) == native.ESSL_DECODE_SPECULATIVE
 
 
+def test_abi_struct_sizes_match_ctypes(native):
+    """The ctypes mirrors in _native.py have the C structs' sizes (a field
+    added on one side only would shift every later field)."""
+    import ctypes
+    out = (ctypes.c_int64 * 5)()
+    assert native.lib().essl_abi_sizes(ctypes.cast(out, ctypes.c_void_p), 5) == 5
+    mine = [ctypes.sizeof(t) for t in (native.EsslSample, native.EsslResult, native.EsslAug,
+                                       native.EsslBatchCfg, native.EsslBatchIo)]
+    assert list(out) == mine
+
+
 def test_rng_and_permutation(E, golden, arrays):
     assert [str(E.SampleRng(5, 7, 11, d).next_u64()) for d in (0, 1, 3)] == golden["rng_u64"]
     assert np.array_equal(E.epoch_permutation(3, 2, 1000), arrays["perm_3_2_1000"])
