@@ -1149,20 +1149,34 @@ __device__ void write_run(const EntCtx &C, const DecodeHead &H, int16_t *coef, u
   pred[2] = pr2;
 }
 
+constexpr int kSegChunk = 8;
+
 // DC pass A over a segment's block records (nb blocks from record `ord`,
 // block-in-MCU b0): the segment's DC-difference sums per scan slot.
 __device__ void seg_dc_sums(const EntCtx &C, const uint32_t *list, const uint2 *bsl, uint32_t ord, int b0,
                             uint32_t nb, int32_t sum[3]) {
   int b = b0;
   int32_t s0 = 0, s1 = 0, s2 = 0;
-#pragma unroll 4
-  for (uint32_t i = 0; i < nb; i++) {
-    const int32_t v = entry_value(list[bsl[ord + i].x]);
-    const int s = (b >= C.c1) + (b >= C.c2);
-    s0 += s == 0 ? v : 0;
-    s1 += s == 1 ? v : 0;
-    s2 += s == 2 ? v : 0;
-    b = b + 1 == C.bpm ? 0 : b + 1;
+  // chunks of kSegChunk blocks: the record loads, then the (dependent) DC
+  // entry loads, each batch in flight together
+#pragma unroll 1
+  for (uint32_t i0 = 0; i0 < nb; i0 += kSegChunk) {
+    uint32_t x[kSegChunk], e[kSegChunk];
+#pragma unroll
+    for (int u = 0; u < kSegChunk; u++) x[u] = i0 + u < nb ? bsl[ord + i0 + u].x : 0u;
+#pragma unroll
+    for (int u = 0; u < kSegChunk; u++) e[u] = i0 + u < nb ? list[x[u]] : 0u;
+#pragma unroll
+    for (int u = 0; u < kSegChunk; u++) {
+      if (i0 + u < nb) {
+        const int32_t v = entry_value(e[u]);
+        const int s = (b >= C.c1) + (b >= C.c2);
+        s0 += s == 0 ? v : 0;
+        s1 += s == 1 ? v : 0;
+        s2 += s == 2 ? v : 0;
+        b = b + 1 == C.bpm ? 0 : b + 1;
+      }
+    }
   }
   sum[0] = s0;
   sum[1] = s1;
@@ -1181,27 +1195,41 @@ __device__ void seg_table(const EntCtx &C, const DecodeHead &H, int16_t *coef, c
   int my = (int)(mcu / (uint32_t)C.gx), mx = (int)(mcu % (uint32_t)C.gx);
   int b = b0;
   int32_t p0 = base[0], p1 = base[1], p2 = base[2];
-#pragma unroll 4
-  for (uint32_t i = 0; i < nb; i++) {
-    const uint2 rec = bsl[ord + i];
-    const int s = (b >= C.c1) + (b >= C.c2);
-    const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + entry_value(list[rec.x]);
-    p0 = s == 0 ? pv : p0;
-    p1 = s == 1 ? pv : p1;
-    p2 = s == 2 ? pv : p2;
-    int16_t *cur = window_block(H, coef, mx, my, b);
-    if (cur) {
-      if (pv < -32768 || pv > 32767) range = 1;
-      // the block's AC entries run up to the next block's DC entry (or the
-      // list's sentinel): their count rides in the entry's high half
-      const uint32_t next = ord + i + 1 < nrec ? bsl[ord + i + 1].x : nlist;
-      const uint32_t cnt = min(next - rec.x - 1u, 63u);
-      ESSL_CHECK(g_check_dec, cur >= C.coef_lo && cur + 4 <= C.coef_hi, CK_COEF);
-      *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + rec.x, ((uint32_t)pv & 0xFFFFu) | (cnt << 16));
+#pragma unroll 1
+  for (uint32_t i0 = 0; i0 < nb; i0 += kSegChunk) {
+    // the chunk's records (+ the next record: where the last block's units
+    // end), then their DC entries
+    uint32_t x[kSegChunk + 1], e[kSegChunk];
+#pragma unroll
+    for (int u = 0; u <= kSegChunk; u++) {
+      const uint32_t i = i0 + u;
+      x[u] = (u < kSegChunk ? i < nb : true) && ord + i < nrec ? bsl[ord + i].x : nlist;
     }
-    if (++b == C.bpm) {
-      b = 0;
-      if (++mx == C.gx) { mx = 0; my++; }
+#pragma unroll
+    for (int u = 0; u < kSegChunk; u++) e[u] = i0 + u < nb ? list[x[u]] : 0u;
+#pragma unroll
+    for (int u = 0; u < kSegChunk; u++) {
+      if (i0 + u < nb) {
+        const int s = (b >= C.c1) + (b >= C.c2);
+        const int32_t pv = (s == 0 ? p0 : (s == 1 ? p1 : p2)) + entry_value(e[u]);
+        p0 = s == 0 ? pv : p0;
+        p1 = s == 1 ? pv : p1;
+        p2 = s == 2 ? pv : p2;
+        int16_t *cur = window_block(H, coef, mx, my, b);
+        if (cur) {
+          if (pv < -32768 || pv > 32767) range = 1;
+          // the block's AC entries run up to the next block's DC entry (or the
+          // list's sentinel): their count rides in the entry's high half
+          const uint32_t next = u + 1 < kSegChunk ? (i0 + u + 1 < nb ? x[u + 1] : (ord + i0 + u + 1 < nrec ? bsl[ord + i0 + u + 1].x : nlist)) : x[kSegChunk];
+          const uint32_t cnt = min(next - x[u] - 1u, 63u);
+          ESSL_CHECK(g_check_dec, cur >= C.coef_lo && cur + 4 <= C.coef_hi, CK_COEF);
+          *reinterpret_cast<uint2 *>(cur) = make_uint2(lgbase + x[u], ((uint32_t)pv & 0xFFFFu) | (cnt << 16));
+        }
+        if (++b == C.bpm) {
+          b = 0;
+          if (++mx == C.gx) { mx = 0; my++; }
+        }
+      }
     }
   }
 }
