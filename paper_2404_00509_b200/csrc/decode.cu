@@ -741,6 +741,12 @@ struct LaneRec {
   // (checkpoints), list length, lane-0 error
   uint32_t xp, nblk, nck, errp, nlist, nbs;
   int8_t xk, xb, err, ovf, xbe;
+};
+
+// Per-lane continuation result and exact-path segment, written after the
+// lane's staging row (EntSmem::stage) has served its last group: they live in
+// that row.
+struct LaneTail {
   // phase 2 (continuation): 0 merged into checkpoint (cj, cm), 1 decode error
   // at cp, 2 end of data at cp (state ek, eb)
   int8_t cst, cbe, ek, eb;
@@ -796,7 +802,7 @@ __device__ __forceinline__ void flush_stage(const EntCtx &C, uint32_t *lp, uint3
 template <bool CONT, bool SH>
 __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint32_t sbeg, uint32_t send,
                          uint32_t *list, uint32_t cap, uint2 *bsl, uint32_t bcap, const uint2 *bsl0,
-                         uint32_t bstride, LaneRec *Ls, LaneRec &R, unsigned int *dbg) {
+                         uint32_t bstride, LaneRec *Ls, LaneRec &R, LaneTail *T, unsigned int *dbg) {
   // SH: the ring reader (shared-memory window, grouped maintenance); !SH:
   // plain global reads (validation)
   using Rd = typename std::conditional<SH, RingReader, Reader<false>>::type;
@@ -977,15 +983,16 @@ __device__ void run_path(const EntCtx &C, int lane, int nseq, uint32_t p0, uint3
   const bool ovf = sink;
   asm volatile("cp.async.wait_all;" ::: "memory");  // the ring is reused after phase 2 (DC sums)
   if (CONT) {
-    R.cst = (int8_t)st;
-    R.cj = (uint32_t)j;
-    R.cm = m;
-    R.cpb = cand;
-    R.cn = nblk;
-    R.cp = st == 1 ? R.errp : r.p;
-    R.ek = (int8_t)k;
-    R.eb = (int8_t)b;
-    R.cbe = (int8_t)be;
+    // (the staging row is done: the tail lives there now)
+    T->cst = (int8_t)st;
+    T->cj = (uint32_t)j;
+    T->cm = m;
+    T->cpb = cand;
+    T->cn = nblk;
+    T->cp = st == 1 ? R.errp : r.p;
+    T->ek = (int8_t)k;
+    T->eb = (int8_t)b;
+    T->cbe = (int8_t)be;
     R.nlist = nl;
     R.nbs = nbs;
     if (ovf) R.ovf = 1;
@@ -2144,6 +2151,11 @@ struct __align__(128) EntSmem {
   long long t_ph[8];
 };
 
+static_assert(sizeof(LaneTail) <= sizeof(uint32_t) * (kGroup + 1), "LaneTail fits a staging row");
+__device__ __forceinline__ LaneTail &tail_of(EntSmem &S, int lane) {
+  return *reinterpret_cast<LaneTail *>(&S.stage[lane][0]);
+}
+
 __device__ __forceinline__ void ent_status(EntSmem &S, int st, int reason, int off) {
   if (S.status == 0) {
     S.status = st;
@@ -2699,6 +2711,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
   EntCtx C = C0;
   DecodeHead &H = S.h;
   LaneRec &R = S.lane[lane];
+  LaneTail &T = tail_of(S, lane);
   int16_t *coef = P.s.coef;
   const uint32_t *rst_tab = C.words + H.rst_off;
   WriteOut wo;
@@ -2814,22 +2827,24 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
       const uint32_t send = lane == nseq - 1 ? end_bits : min(end_bits, (lane + 1) * slen);
       const uint32_t p0 = lane == 0 ? 0u : (sbeg > warm ? sbeg - warm : 0u);
       run_path<false, SH>(C, lane, nseq, p0, sbeg, send, list, cap, bsl, bcap, bsl0, bstride, S.lane, R,
-                          &S.dbg_units);
+                          &T, &S.dbg_units);
     }
     __syncthreads();
     PHASE(2);
     const bool cont = lane < nseq - 1 && !(lane == 0 && R.err);
     if (cont)
-      run_path<true, SH>(C, lane, nseq, 0, 0, 0, list, cap, bsl, bcap, bsl0, bstride, S.lane, R, &S.dbg_units);
+      run_path<true, SH>(C, lane, nseq, 0, 0, 0, list, cap, bsl, bcap, bsl0, bstride, S.lane, R, &T,
+                         &S.dbg_units);
+    T.w_nb = 0;  // (every lane; the resolution sets the owners' segments)
     dbg_nseq = (uint32_t)nseq;
-    if (cont) atomicMax(&S.red, (int)(R.cp - R.xp));
+    if (cont) atomicMax(&S.red, (int)(T.cp - R.xp));
     __syncthreads();
     dbg_cont = (uint32_t)S.red;
     if (P.dbg_lanes) {
       int32_t *o = P.dbg_lanes + ((size_t)img * kLanes + lane) * 8;
       o[0] = nseq; o[1] = (int32_t)R.xp; o[2] = (int32_t)R.xb; o[3] = (int32_t)R.nck;
-      o[4] = R.err; o[5] = cont ? (int32_t)R.cp : -1; o[6] = cont ? R.cst : -1;
-      o[7] = cont ? (int32_t)R.cj : -1;
+      o[4] = R.err; o[5] = cont ? (int32_t)T.cp : -1; o[6] = cont ? T.cst : -1;
+      o[7] = cont ? (int32_t)T.cj : -1;
     }
     PHASE(3);
     // resolution: follow the exact path from lane 0 through the merges
@@ -2841,20 +2856,21 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
 #pragma unroll 1
       for (int hop = 0; hop < nseq; hop++) {
         LaneRec &L = S.lane[o];
+        LaneTail &TL = tail_of(S, o);
         const uint32_t own = L.nblk - snb;
-        L.w_ord = sord; L.w_p = sp; L.w_b = sb; L.w_A = A;
+        TL.w_ord = sord; TL.w_p = sp; TL.w_b = sb; TL.w_A = A;
         if (L.ovf) S.fmt = 0;  // an owner's list overflowed: serial re-decode
         if (L.err) {  // error on the exact path (phase 1 of lane 0)
-          L.w_nb = min(own, limit - A);
+          TL.w_nb = min(own, limit - A);
           if (A + own < limit) ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.errp));
           break;
         }
         const bool last = o == nseq - 1;
         // a path that ends without a merge: the last lane's, or a continuation
         // that ran to the end of the covered range
-        const bool open_end = last || L.cst == 2;
-        uint32_t seg = own + (last ? 0u : L.cn);
-        PathEnd X = last ? PathEnd{L.xp, L.xk, L.xb, L.xbe} : PathEnd{L.cp, (int)L.ek, (int)L.eb, L.cbe};
+        const bool open_end = last || TL.cst == 2;
+        uint32_t seg = own + (last ? 0u : TL.cn);
+        PathEnd X = last ? PathEnd{L.xp, L.xk, L.xb, L.xbe} : PathEnd{TL.cp, (int)TL.ek, (int)TL.eb, TL.cbe};
         if (open_end && A + seg < limit && X.p < cbits) {
           // it stopped at the estimated end before the crop's last needed
           // block: extend the exact path, appending to this lane's lists
@@ -2871,12 +2887,12 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
             S.fmt = 0;
           }
           if (xs == 1) {
-            L.w_nb = min(seg, limit - A);
+            TL.w_nb = min(seg, limit - A);
             ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, X.p));
             break;
           }
         }
-        L.w_nb = min(seg, limit - A);
+        TL.w_nb = min(seg, limit - A);
         const uint32_t end_p = X.p;
         const int end_be = X.be;
         if (A + seg >= limit) {
@@ -2892,28 +2908,28 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
           else ent_status(S, ESSL_ST_TRUNCATED, 0, H.scan_end);
           break;
         }
-        if (L.cst == 1) {
-          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, L.cp));
+        if (TL.cst == 1) {
+          ent_status(S, ESSL_ST_CORRUPT_HUFFMAN, 0, corrupt_offset(H, TL.cp));
           break;
         }
         A += seg;
         // merged into record cm of lane cj: the exact path continues there,
         // after cm complete blocks of that lane's list
-        const uint32_t pb = L.cpb;  // == bsl0[L.cj * bstride + L.cm].y
-        o = (int)L.cj;
-        sord = L.cm; sp = pb >> 6; sb = pb & 63; snb = L.cm;
+        const uint32_t pb = TL.cpb;  // == bsl0[TL.cj * bstride + TL.cm].y
+        o = (int)TL.cj;
+        sord = TL.cm; sp = pb >> 6; sb = pb & 63; snb = TL.cm;
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // (lane 0's serial readers: the rings are reused below)
     __syncthreads();
     PHASE(4);
-    const bool own = S.status == 0 && R.w_nb > 0;
+    const bool own = S.status == 0 && T.w_nb > 0;
     int range = 0;
     if (S.status == 0 && S.fmt == 1) {
       // block tables: each segment's DC continues from the earlier segments'
       // DC sums (segments are in lane order)
       int32_t sum[3] = {0, 0, 0};
-      if (own) seg_dc_sums(C, list, bsl, R.w_ord, (int)R.w_b, R.w_nb, sum);
+      if (own) seg_dc_sums(C, list, bsl, T.w_ord, (int)T.w_b, T.w_nb, sum);
       int32_t *dcs = reinterpret_cast<int32_t *>(&S.ring[0][0]);  // (the read rings are idle now: run_path drained its copies)
       for (int q = 0; q < 3; q++) dcs[lane * 3 + q] = sum[q];
       __syncthreads();
@@ -2921,7 +2937,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
         int32_t base[3] = {0, 0, 0};
         for (int t = 0; t < lane; t++)
           for (int q = 0; q < 3; q++) base[q] += dcs[t * 3 + q];
-        seg_table(C, H, coef, list, bsl, R.w_ord, (uint32_t)lreg, (int)R.w_b, R.w_A, R.w_nb,
+        seg_table(C, H, coef, list, bsl, T.w_ord, (uint32_t)lreg, (int)T.w_b, T.w_A, T.w_nb,
                   min(R.nbs, bcap), R.nlist, base, range);
       }
     } else if (S.status == 0) {
@@ -2940,7 +2956,7 @@ __device__ __forceinline__ void entropy_body(const DecodeParams &P, EntSmem &S, 
 #undef PHASE
 }
 
-__global__ void __launch_bounds__(kLanes, 8) k_entropy(DecodeParams P) {
+__global__ void __launch_bounds__(kLanes, 9) k_entropy(DecodeParams P) {
   TraceScope trace_(P.trace, ESSL_K_ENTROPY);
   __shared__ EntSmem S;
   const int img = blockIdx.x;
@@ -2974,7 +2990,6 @@ __global__ void __launch_bounds__(kLanes, 8) k_entropy(DecodeParams P) {
     S.dbg_units = 0; S.dbg_guess = 0; S.dbg_umax = 0; S.dbg_ext = 0;
   }
   LaneRec &R = S.lane[lane];
-  R.w_nb = 0;
   R.nck = 0;
   __syncthreads();
   PHASE(1);
