@@ -93,7 +93,8 @@ def config_dict(args, wl: dict, records: int, mean_payload: float) -> dict:
             "l2": f"inputs > L2: {args.pool}-image pool (~{args.pool * mean_payload / 1e6:.0f} MB of "
                   "JPEG bytes, 126 MB L2) visited in permutation order; outputs: a reused ring of "
                   "16 output buffers per loader (each written once per 16 steps)",
-            "parallelism": "ddp per GPU (rank shards perm[r::world], no collective on the path)"}
+            "parallelism": "ddp per GPU (rank shards perm[r::world], no collective on the path)",
+            "launch_group": getattr(args, "group", 1)}
 
 
 def dataset_dir(rank: int, ws: int) -> Path:
@@ -321,7 +322,7 @@ def run_gpu(args, wl):
                          mask_ratio=wl["mask"], aug=wl.get("aug", "simple"),
                          out_dtype="bfloat16", device=str(dev),
                          rank=rank, world_size=ws, resident=True, prefetch=args.streams,
-                         streams=args.streams, reuse_outputs=True)
+                         streams=args.streams, reuse_outputs=True, group=args.group)
     loader = E.Loader(cfg)
 
     def apply_options(ld):  # analysis knobs (library defaults unless given)
@@ -358,12 +359,30 @@ def run_gpu(args, wl):
     ring_depth = 2 * max(cfg.prefetch, cfg.streams) + 2  # pipeline.py _HostRing slots
     n_warm = max(args.warmup, args.streams * (ring_depth + 1))
     sched = wl.get("schedule")
-    for i in range(n_warm):
+    G = args.group
+
+    def issue(i, steps, stage_of, g):
+        """Batch i (+ up to g-1 following ones of the same epoch and stage) in
+        one launch set; returns (pendings, batches issued)."""
+        e, idx = batch_indices(i)
+        parts = [idx]
+        while len(parts) < g and i + len(parts) < steps:
+            e2, idx2 = batch_indices(i + len(parts))
+            if e2 != e or stage_of(i + len(parts)) != stage_of(i):
+                break
+            parts.append(idx2)
+        if len(parts) == 1:
+            return [loader.enqueue(e, idx)], 1
+        return loader.enqueue_group(e, parts), len(parts)
+
+    i = 0
+    while i < n_warm:
         if sched:  # every stage's output ring allocated before the timed region
             loader.retarget(res=sched[i * len(sched) // n_warm])
-        e, idx = batch_indices(i)
-        pend.append(loader.enqueue(e, idx))
-        if len(pend) > 2 * args.streams:
+        ps, k = issue(i, n_warm, lambda j: j * len(sched) // n_warm if sched else 0, G)
+        pend.extend(ps)
+        i += k
+        while len(pend) > 2 * args.streams * G:
             loader.finish(pend.pop(0))
     for p in pend:
         loader.finish(p)
@@ -396,17 +415,25 @@ def run_gpu(args, wl):
     torch.cuda.nvtx.range_push("bench.timed")
     t0.record(stream)
     n_img = 0
-    for i in range(args.steps):
+    def stage_of(i):  # progressive stages: equal shares of the timed steps
+        return min(len(sched) - 1, i * len(sched) // args.steps) if sched else 0
+
+    i = sets = 0
+    while i < args.steps:
         h0 = time.perf_counter()
-        if sched:  # progressive stages: equal shares of the timed steps
-            r_i = sched[min(len(sched) - 1, i * len(sched) // args.steps)]
+        if sched:
+            r_i = sched[stage_of(i)]
             if r_i != loader.config.res:
                 loader.retarget(res=r_i)
-        e, idx = batch_indices(args.warmup + i)
-        pend.append(loader.enqueue(e, idx))
-        n_img += len(idx)
+        # (as Loader.epochs: single batches until `streams` sets are in flight)
+        ps, k = issue(args.warmup + i, args.warmup + args.steps, lambda j: stage_of(j - args.warmup),
+                      G if sets >= args.streams else 1)
+        sets += 1
+        pend.extend(ps)
+        n_img += sum(len(p.indices) for p in ps)
+        i += k
         h1 = time.perf_counter()
-        if len(pend) > 2 * args.streams:  # bounded run-ahead; statuses checked as we go
+        while len(pend) > 2 * args.streams * G:  # bounded run-ahead; statuses checked as we go
             loader.finish(pend.pop(0))
         host_t.append((h1 - h0, time.perf_counter() - h1))
     for p in pend:  # join every in-flight batch before the end event
@@ -612,6 +639,8 @@ def main():
                     help="bracket every launch with CUDA events in the timed region (kernel_ms of all kernels)")
     ap.add_argument("--early-exit", type=int, default=-1,
                     help="ESSL_OPT_EARLY_EXIT (entropy decode stops near the crop's last row; -1: default)")
+    ap.add_argument("--group", type=int, default=2,
+                    help="consecutive batches decoded per launch set (LoaderConfig.group)")
     ap.add_argument("--streams", type=int, default=8,
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--gather-ctas", type=int, default=-1,

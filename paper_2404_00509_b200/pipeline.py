@@ -112,7 +112,7 @@ class ImageBatch:
 
 
 _GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch",
-             "streams", "staging", "shard_mode", "visible")
+             "streams", "staging", "shard_mode", "visible", "group")
 
 
 @dataclass
@@ -154,6 +154,10 @@ class LoaderConfig:
     # emit ImageBatch.visible: the MAE encoder's visible tokens, written by the
     # resize kernel itself (needs mask_ratio > 0)
     visible: bool = False
+    # the iterators (epoch / epochs) decode up to `group` consecutive batches
+    # of one epoch in one launch set (the same batches, fewer and larger
+    # launches); enqueue() is always one batch
+    group: int = 1
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
@@ -197,6 +201,8 @@ class LoaderConfig:
             raise ConfigError(f"staging must be gather or copy, got {self.staging!r}")
         if self.streams < 1 or self.prefetch < 1:
             raise ConfigError("streams and prefetch must be >= 1")
+        if self.group < 1:
+            raise ConfigError("group must be >= 1")
         if self.visible and self.mask_ratio <= 0.0:
             raise ConfigError("visible tokens need mask_ratio > 0")
         if self.shard_mode not in ("pad", "drop", "stride"):
@@ -248,6 +254,7 @@ class _Pending:
     epoch: int = 0
     keep: list = field(default_factory=list)
     results_np: object = None  # numpy view of results_host (fast path)
+    last: bool = True  # the last batch of its launch set (_enqueue_group)
 
 
 class Loader:
@@ -275,13 +282,13 @@ class Loader:
         # flight: consecutive batches overlap on the GPU
         self._engines = [engine] if engine is not None else []
         while len(self._engines) < config.streams:
-            self._engines.append(Engine(dev, max_batch=config.batch_size,
+            self._engines.append(Engine(dev, max_batch=config.batch_size * config.group,
                                         max_side=max(w, h, 16),
                                         max_payload=self.handle.max_payload()))
         self.engine = self._engines[0]
         self.device = self.engine.device
         self._streams = [torch.cuda.Stream(self.device) for _ in self._engines]
-        self._rings = [_HostRing(2 * max(config.prefetch, config.streams) + 2, config.batch_size,
+        self._rings = [_HostRing(2 * max(config.prefetch, config.streams) + 2, config.batch_size * config.group,
                                  ctypes.sizeof(N.EsslResult) // 4) for _ in self._engines]
         self._rr = 0
         self.workers = config.workers if config.workers > 0 else (os.cpu_count() or 1)
@@ -430,17 +437,22 @@ class Loader:
         dev = self.device
         res = cfg.res
 
+        bmax = cfg.batch_size * cfg.group
+
         def out(name, shape, dtype):
             if not cfg.reuse_outputs:
                 return torch.empty(shape, dtype=dtype, device=dev)
-            # keyed by shape too: progressive stages (retarget) keep their own
-            # rings instead of reallocating at every stage switch
-            key = (j, oslot, name, tuple(shape), dtype)
+            # one buffer per slot sized for the largest launch set, viewed
+            # [:n] (single batches, groups and partial batches share it: no
+            # allocation mid-run); keyed by the per-image shape too, so
+            # progressive stages (retarget) keep their own rings
+            full = (shape[0] // b * bmax,) + tuple(shape[1:])
+            key = (j, oslot, name, full, dtype)
             t = self._out_ring.get(key)
             if t is None:
-                t = torch.empty(shape, dtype=dtype, device=dev)
+                t = torch.empty(full, dtype=dtype, device=dev)
                 self._out_ring[key] = t
-            return t
+            return t[:shape[0]]
 
         o = {}
         if pixels is not None:
@@ -631,33 +643,83 @@ class Loader:
             yield epoch, perm[s:s + B]
 
     def _run(self, plan, into=None):
-        """Keep `depth` batches in flight over the (epoch, indices) plan."""
+        """Keep `depth` launch sets in flight over the (epoch, indices) plan
+        (one batch each, or up to `group` batches of one epoch each)."""
         q: deque = deque()
         depth = max(self.config.prefetch, len(self._engines))
         if into is not None and len(into) < depth + 1:
             raise ValueError(f"into: need at least {depth + 1} buffers for {depth} batches in flight")
+        G = self.config.group if into is None else 1
         it = iter(plan)
+        held = []  # a plan item read ahead that starts the next group
         nb = 0
 
-        def issue(e, idxs):
+        def take(g):
+            """The next launch set: [(epoch, indices), ...] (empty at the end)."""
+            items = [held.pop()] if held else []
+            while len(items) < g:
+                nxt = next(it, None)
+                if nxt is None:
+                    break
+                if items and nxt[0] != items[0][0]:  # groups stay within an epoch
+                    held.append(nxt)
+                    break
+                items.append(nxt)
+            return items
+
+        def issue(items):
             nonlocal nb
+            if len(items) > 1:
+                return self.enqueue_group(items[0][0], [i for _, i in items])
+            e, idxs = items[0]
             buf = None
             if into is not None:
                 buf = into[nb % len(into)]
                 buf = buf[:len(idxs)] if buf.shape[0] != len(idxs) else buf
             nb += 1
-            return self.enqueue(e, idxs, buf)
+            return [self.enqueue(e, idxs, buf)]
 
-        for e, idxs in it:
-            q.append(issue(e, idxs))
-            if len(q) >= depth:
+        # the pipeline fills with single batches (the first results come back
+        # soonest); groups take over once `depth` sets are in flight
+        sets = 0
+        while sets < depth:
+            items = take(1)
+            if not items:
                 break
+            q.extend(issue(items))
+            sets += 1
         while q:
             p = q.popleft()
-            nxt = next(it, None)
-            if nxt is not None:
-                q.append(issue(*nxt))
+            if p.last:  # its launch set is done with: issue the next one
+                items = take(G)
+                if items:
+                    q.extend(issue(items))
             yield self.finish(p)
+
+    def enqueue_group(self, epoch: int, parts: list) -> list:
+        """Consecutive batches of one epoch in ONE launch set (one native
+        call over their concatenated indices; at most `group` of them); each
+        batch's outputs are views of the set's ring buffers.  Returns one
+        pending batch per part, in order (finish / join each)."""
+        if sum(len(p) for p in parts) > self.config.batch_size * self.config.group:
+            raise ValueError("enqueue_group: more images than batch_size * group")
+        idxs = np.concatenate([np.asarray(p, np.int64) for p in parts])
+        p = self.enqueue(epoch, idxs)
+        g = p.batch
+        out, off = [], 0
+        for k, part in enumerate(parts):
+            b = len(part)
+            sl = slice(off, off + b)
+
+            def v(t):
+                return None if t is None else t[sl]
+            batch = ImageBatch(g.pixels[sl], g.labels[sl], g.indices[sl], epoch, v(g.mask), v(g.uint8),
+                               v(g.ids_keep), v(g.ids_restore), v(g.visible))
+            out.append(_Pending(batch, None, idxs[sl], p.results_host[sl], p.event, epoch,
+                                results_np=p.results_np[sl] if p.results_np is not None else None,
+                                last=k == len(parts) - 1))
+            off += b
+        return out
 
     def epoch(self, epoch: int, into=None):
         """Yield the batches of one epoch (this rank's shard) in permutation order.

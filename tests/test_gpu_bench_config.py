@@ -67,13 +67,13 @@ def _check_batch(oracle, h, b, epoch, res, scale, mask_ratio, patch=16):
 
 
 def _run(E, oracle, path, *, batch, res, scale, mask_ratio, epochs, resident=True,
-         visible=False, into=False, max_batches=None, streams=8):
+         visible=False, into=False, max_batches=None, streams=8, group=1):
     import torch
     with E.open_container(path) as h:
         cfg = E.LoaderConfig(data=str(path), batch_size=batch, res=res, scale=scale,
                              mask_ratio=mask_ratio, out_dtype="bfloat16", resident=resident,
                              streams=streams, prefetch=streams, reuse_outputs=True,
-                             visible=visible)
+                             visible=visible, group=group)
         loader = E.Loader(cfg, container=h)
         bufs = None
         if into:
@@ -103,11 +103,13 @@ def pool256(E, tmp_path_factory):
     return path
 
 
-def test_bench_config_resident(E, oracle, pool256):
+@pytest.mark.parametrize("group", [2, 1])
+def test_bench_config_resident(E, oracle, pool256, group):
     """The exact timed configuration: 8 streams, prefetch 8, output ring,
-    bf16 + mask 0.75, resident, batch 256; 2 epochs of 2048 images."""
+    bf16 + mask 0.75, resident, batch 256, two batches per launch set
+    (bench.py --group 2; and single batches); 2 epochs of 2048 images."""
     n, nb = _run(E, oracle, pool256, batch=256, res=224, scale=(0.08, 1.0), mask_ratio=0.75,
-                 epochs=(0, 1))
+                 epochs=(0, 1), group=group)
     assert n == 4096 and nb == 16
 
 
@@ -115,8 +117,17 @@ def test_bench_config_host_staged(E, oracle, pool256):
     """The e2e leg: the same loader with the page-locked host container
     gathered over the bus each batch."""
     n, _ = _run(E, oracle, pool256, batch=256, res=224, scale=(0.08, 1.0), mask_ratio=0.75,
-                epochs=(2,), resident=False)
+                epochs=(2,), resident=False, group=2)
     assert n == 2048
+
+
+def test_launch_groups_partial_and_epoch_boundaries(E, oracle, pool256):
+    """Groups of 3 batches over epochs of 10 2/3 batches of 192 (a partial
+    last batch, groups cut at every epoch boundary), 3 streams: the same
+    batches as single launches, each checked against the oracle."""
+    n, nb = _run(E, oracle, pool256, batch=192, res=160, scale=(0.08, 1.0), mask_ratio=0.75,
+                 epochs=(4, 5), streams=3, group=3)
+    assert n == 4096 and nb == 22
 
 
 def test_bench_config_visible_tokens_and_into(E, oracle, pool256):
