@@ -52,7 +52,7 @@ WORKLOADS = {
     "cfg1": dict(side=256, quality=95, scale=(0.08, 1.0), batch=256, res=224, mask=0.0,
                  desc="256 synthetic 256px q95 JPEGs per batch, crop-decode + RRC(0.08,1)->224 "
                       "+ flip + normalize (bf16 NCHW)"),
-    "cfg4": dict(side=512, quality=90, scale=(0.2, 1.0), batch=1024, res=224, mask=0.0,
+    "cfg4": dict(side=512, quality=90, scale=(0.2, 1.0), batch=1024, res=224, mask=0.0, group=1,
                  desc="1024 synthetic 512px q90 JPEGs per batch, RRC(0.2,1)->224 + flip + "
                       "normalize (bf16 NCHW)"),
     # progressive resolution (schedule.py custom scheme): the
@@ -639,8 +639,9 @@ def main():
                     help="bracket every launch with CUDA events in the timed region (kernel_ms of all kernels)")
     ap.add_argument("--early-exit", type=int, default=-1,
                     help="ESSL_OPT_EARLY_EXIT (entropy decode stops near the crop's last row; -1: default)")
-    ap.add_argument("--group", type=int, default=2,
-                    help="consecutive batches decoded per launch set (LoaderConfig.group)")
+    ap.add_argument("--group", type=int, default=0,
+                    help="consecutive batches decoded per launch set (LoaderConfig.group; "
+                         "0: the workload's, 2 unless it sets one)")
     ap.add_argument("--streams", type=int, default=8,
                     help="batches in flight (one libessl context + CUDA stream each)")
     ap.add_argument("--gather-ctas", type=int, default=-1,
@@ -660,6 +661,8 @@ def main():
     wl = dict(WORKLOADS[args.workload])
     if args.batch > 0:
         wl["batch"] = args.batch
+    if args.group <= 0:
+        args.group = wl.get("group", 2)
     if args.restart > 0:
         wl["restart"] = args.restart
         wl["desc"] += f"; restart interval {args.restart} MCUs (f3 variant)"
