@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-r2}
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench20.json 2> gpurun_out/${TAG}_bench20.err; echo "bench20 rc=$?"
 timeout 600 python bench.py --steps 300 --warmup 5 --no-cpu > gpurun_out/${TAG}_bench300.json 2> gpurun_out/${TAG}_bench300.err; echo "bench300 rc=$?"
-B="bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --streams 1"
+B="bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --streams 1 --group 1"
 timeout 300 python $B > gpurun_out/${TAG}_plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python $B > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
 for k in ${KERNELS:-k_entropy k_prep k_idct k_resize k_mask}; do
