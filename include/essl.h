@@ -346,7 +346,9 @@ typedef struct {
   const uint8_t *blob;         /* DEVICE resident container bytes, or NULL: */
   const uint8_t *pinned_base;  /* DEVICE address of the page-locked container */
   int32_t stage_slot;          /* staging slot (0/1) of the pinned gather */
-  int32_t pad;
+  int32_t stage_chain;         /* > 0: the gather runs after the device's previous chained
+                                  gather, on this many CTAs (a pipeline fill: the oldest
+                                  batch's payloads arrive first); 0: concurrent */
   const essl_aug *aug;         /* HOST n 3-Aug entries (essl_aug_batch), or NULL */
   void *pixels;                /* DEVICE [n,3,res,res] out_kind, caller-owned */
   int64_t pixel_stride;        /* elements between samples (0: dense) */

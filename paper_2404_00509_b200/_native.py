@@ -87,7 +87,7 @@ class EsslBatchCfg(ctypes.Structure):
 
 class EsslBatchIo(ctypes.Structure):
     _fields_ = [("blob", ctypes.c_void_p), ("pinned_base", ctypes.c_void_p),
-                ("stage_slot", ctypes.c_int32), ("pad", ctypes.c_int32), ("aug", ctypes.c_void_p),
+                ("stage_slot", ctypes.c_int32), ("stage_chain", ctypes.c_int32), ("aug", ctypes.c_void_p),
                 ("pixels", ctypes.c_void_p), ("pixel_stride", ctypes.c_int64),
                 ("u8", ctypes.c_void_p), ("index_label", ctypes.c_void_p), ("mask", ctypes.c_void_p),
                 ("ids_keep", ctypes.c_void_p), ("ids_restore", ctypes.c_void_p),

@@ -291,7 +291,7 @@ int rrc_impl(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int s
 // Pinned-container gather of a batch: samples[i].offset holds the payload's
 // container offset on entry and its offset inside the staging slot on return.
 int stage_pinned_impl(essl_ctx *c, int slot, const uint8_t *dev_base, essl_sample *samples, int n,
-                      cudaStream_t st, const uint8_t **dev_blob) {
+                      cudaStream_t st, const uint8_t **dev_blob, int chain_ctas) {
   if (c->stage_used[slot]) CK(cudaEventSynchronize(c->ev_stage[slot]));
   essl::GatherDesc *h = c->h_gather[slot];
   uint64_t pos = 0;
@@ -306,11 +306,24 @@ int stage_pinned_impl(essl_ctx *c, int slot, const uint8_t *dev_base, essl_sampl
   }
   if (n > 0) {
     CK(cudaMemcpyAsync(c->d_gather[slot], h, sizeof(essl::GatherDesc) * n, cudaMemcpyHostToDevice, st));
+    // chained gathers (a pipeline fill) run one after the other across every
+    // context of the device, each on more CTAs: the oldest batch's payloads
+    // arrive first instead of all batches' together
+    static std::mutex chain_m;
+    static std::vector<cudaEvent_t> chain_tail;
+    std::unique_lock<std::mutex> lk(chain_m, std::defer_lock);
+    if (chain_ctas > 0) {
+      lk.lock();
+      if ((int)chain_tail.size() <= c->device) chain_tail.resize(c->device + 1, nullptr);
+      if (!chain_tail[c->device]) CK(cudaEventCreateWithFlags(&chain_tail[c->device], cudaEventDisableTiming));
+      else CK(cudaStreamWaitEvent(st, chain_tail[c->device], 0));
+    }
     {
       Prof pr(c, ESSL_K_STAGE, st);
-      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot], c->gather_ctas,
-                               c->gather_tma, st);
+      essl::launch_host_gather(dev_base, c->d_gather[slot], n, c->d_stage[slot],
+                               chain_ctas > 0 ? chain_ctas : c->gather_ctas, c->gather_tma, st);
     }
+    if (chain_ctas > 0) CK(cudaEventRecord(chain_tail[c->device], st));
   }
   CK(cudaEventRecord(c->ev_stage[slot], st));
   c->stage_used[slot] = true;
@@ -778,7 +791,7 @@ int essl_stage_pinned(essl_ctx *c, int slot, const uint8_t *dev_base, const uint
     samples[i].offset = src_off[i];
     samples[i].length = len[i];
   }
-  return stage_pinned_impl(c, slot, dev_base, samples, n, (cudaStream_t)stream, dev_blob);
+  return stage_pinned_impl(c, slot, dev_base, samples, n, (cudaStream_t)stream, dev_blob, 0);
 }
 
 int essl_decode_rrc(essl_ctx *c, const uint8_t *blob, const essl_sample *samples, int n, int res,
@@ -1114,6 +1127,8 @@ int essl_batch_enqueue(essl_ctx *c, const essl_dataset *ds, const essl_batch_cfg
   if (!io->blob && !io->pinned_base) return fail(ESSL_E_ARG, "essl_batch_enqueue: no payload source");
   if (io->pinned_base && !io->blob && (io->stage_slot < 0 || io->stage_slot > 1))
     return fail(ESSL_E_ARG, "essl_batch_enqueue: bad staging slot");
+  if (io->stage_chain < 0 || io->stage_chain > 1024)
+    return fail(ESSL_E_ARG, "essl_batch_enqueue: bad stage_chain");
   if (cfg->tokens > 0 && (cfg->masked < 0 || cfg->masked > cfg->tokens || cfg->tokens > 4096))
     return fail(ESSL_E_ARG, "essl_batch_enqueue: bad mask geometry");
   if (io->tokens && cfg->tokens <= 0) return fail(ESSL_E_ARG, "visible tokens need the mask");
@@ -1150,7 +1165,7 @@ int essl_batch_enqueue(essl_ctx *c, const essl_dataset *ds, const essl_batch_cfg
   }
   const uint8_t *blob = io->blob;
   if (!blob) {
-    rc = stage_pinned_impl(c, io->stage_slot, io->pinned_base, smp, n, st, &blob);
+    rc = stage_pinned_impl(c, io->stage_slot, io->pinned_base, smp, n, st, &blob, io->stage_chain);
     if (rc) return rc;
   }
   // MAE mask first: the fused visible-token output reads ids_restore

@@ -112,7 +112,7 @@ class ImageBatch:
 
 
 _GPU_KEYS = ("reuse_outputs", "device", "out_dtype", "rank", "world_size", "resident", "prefetch",
-             "streams", "staging", "shard_mode", "visible", "group")
+             "streams", "staging", "shard_mode", "visible", "group", "fill_chain")
 
 
 @dataclass
@@ -158,6 +158,10 @@ class LoaderConfig:
     # of one epoch in one launch set (the same batches, fewer and larger
     # launches); enqueue() is always one batch
     group: int = 1
+    # host-staged containers: while the iterators fill the pipeline, each
+    # batch's bus gather waits for the previous one and runs on this many
+    # CTAs (the oldest batch's payloads arrive first); 0: all concurrent
+    fill_chain: int = 16
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS
@@ -203,6 +207,8 @@ class LoaderConfig:
             raise ConfigError("streams and prefetch must be >= 1")
         if self.group < 1:
             raise ConfigError("group must be >= 1")
+        if not 0 <= self.fill_chain <= 1024:
+            raise ConfigError("fill_chain must be in [0, 1024]")
         if self.visible and self.mask_ratio <= 0.0:
             raise ConfigError("visible tokens need mask_ratio > 0")
         if self.shard_mode not in ("pad", "drop", "stride"):
@@ -326,6 +332,7 @@ class Loader:
         n_st = len(self._engines)
         self._R = max(2, -(-(max(config.prefetch, n_st) + 2) // n_st))
         self._fast: dict = {}
+        self._chain = 0  # essl_batch_io.stage_chain of the next enqueues (the iterators' fill)
         self._refresh_cfg()
 
     @classmethod
@@ -503,6 +510,7 @@ class Loader:
         io = self._bio
         if self._blob is None:
             io.stage_slot = self._slots[j]
+            io.stage_chain = self._chain
             self._slots[j] ^= 1
         io.aug = None if aug is None else aug.ctypes.data
         (io.pixels, io.pixel_stride, io.u8, io.index_label, io.mask, io.ids_keep, io.ids_restore,
@@ -682,12 +690,17 @@ class Loader:
         # the pipeline fills with single batches (the first results come back
         # soonest); groups take over once `depth` sets are in flight
         sets = 0
-        while sets < depth:
-            items = take(1)
-            if not items:
-                break
-            q.extend(issue(items))
-            sets += 1
+        # host-staged payloads: the fill's bus gathers run oldest first
+        self._chain = self.config.fill_chain if self._blob is None else 0
+        try:
+            while sets < depth:
+                items = take(1)
+                if not items:
+                    break
+                q.extend(issue(items))
+                sets += 1
+        finally:
+            self._chain = 0
         while q:
             p = q.popleft()
             if p.last:  # its launch set is done with: issue the next one
