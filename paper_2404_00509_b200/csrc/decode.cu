@@ -134,6 +134,10 @@ struct __align__(16) DecodeHead {
   int32_t coef_pitch[3];  // blocks per coefficient-array row (window width; BW when multiscan)
   uint32_t rst_off;       // restart table, words from the clean region start
   uint64_t coef_off[3], coef_base, clean_off;
+  // device address of each used Huffman table: the context's table cache
+  // slot when the image's DHT matched it (no per-image copy), else the
+  // image's own DecodeHdr::tab entry
+  uint64_t tab_ptr[kMaxTables];
   uint8_t blk_slot[kMaxBpm], blk_dy[kMaxBpm], blk_dx[kMaxBpm];
   uint8_t zz[64];
 };
@@ -640,7 +644,7 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 constexpr uint32_t kTabStride = (1u << kFastBits) * 2u;
 constexpr int kSmemTabs = 4;
 struct EntCtx {
-  const HuffTab *gtab;  // the full tables (global memory)
+  const uint64_t *gtab;  // the full tables' device addresses (DecodeHead::tab_ptr, shared copy)
   uint32_t tabs_s;      // shared first-level tables, as a shared-window address
   uint32_t zz_s;        // zig-zag -> natural table (shared-window address)
   uint32_t d0, d1, d2, a0, a1, a2;  // byte offsets of the DC / AC table per scan slot
@@ -664,11 +668,11 @@ struct EntCtx {
   __device__ __forceinline__ uint32_t lookup_fast(int k, int b, uint32_t hi) const {
     const uint32_t off = tab_off(k, b);
     if (TS) return lds_u16(tabs_s + off + ((hi >> (32 - kFastBits)) << 1));
-    return __ldg(&gtab[off / kTabStride].fast[hi >> (32 - kFastBits)]);
+    return __ldg(&reinterpret_cast<const HuffTab *>(gtab[off / kTabStride])->fast[hi >> (32 - kFastBits)]);
   }
   __device__ __forceinline__ uint32_t zz(int i) const { return lds_u8(zz_s + (uint32_t)i); }
   __device__ __forceinline__ uint32_t lookup_long(int k, int b, uint32_t e, uint32_t hi) const {
-    const HuffTab &T = gtab[tab_off(k, b) / kTabStride];
+    const HuffTab &T = *reinterpret_cast<const HuffTab *>(gtab[tab_off(k, b) / kTabStride]);
     return essl::lookup_long(*reinterpret_cast<const HuffFast *>(&T), T, e, hi);
   }
   template <bool TS>
@@ -1991,14 +1995,11 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       bool eq = st == 2u && C.len == len && C.is_dc == s_tdc[t];
       for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == raw[pos + i];
       const int hit = __syncthreads_and(eq);
-      if (hit) {  // copy the built table (with this image's own dht_pos)
-        const int4 *src = reinterpret_cast<const int4 *>(&C.tab);
-        int4 *dst = reinterpret_cast<int4 *>(&G->tab[t]);
-        for (int i = tid; i < (int)(sizeof(HuffTab) / 16); i += kNT) dst[i] = src[i];
-        __syncthreads();
-        if (tid == 0) G->tab[t].dht_pos = pos;
+      // a hit is used in place (slots are written once, never replaced)
+      if (tid == 0) {
+        s_hit[t] = hit;
+        H.tab_ptr[t] = hit ? reinterpret_cast<uint64_t>(&C.tab) : reinterpret_cast<uint64_t>(&G->tab[t]);
       }
-      if (tid == 0) s_hit[t] = hit;
     }
   }
   __syncthreads();
@@ -2979,7 +2980,8 @@ __global__ void __launch_bounds__(kLanes, 9) k_entropy(DecodeParams P) {
     constexpr int per = (int)(kTabStride / 16);
     for (int i = lane; i < H.ntab * per; i += kLanes) {
       const int t = i / per, w = i % per;
-      reinterpret_cast<int4 *>(S.tab[t])[w] = reinterpret_cast<const int4 *>(G->tab[t].fast)[w];
+      reinterpret_cast<int4 *>(S.tab[t])[w] =
+          reinterpret_cast<const int4 *>(reinterpret_cast<const HuffTab *>(H.tab_ptr[t])->fast)[w];
     }
   }
   if (lane == 0) {
@@ -2995,7 +2997,7 @@ __global__ void __launch_bounds__(kLanes, 9) k_entropy(DecodeParams P) {
   PHASE(1);
 
   EntCtx C;
-  C.gtab = G->tab;
+  C.gtab = H.tab_ptr;
   C.tabs_s = (uint32_t)__cvta_generic_to_shared(S.tab);
   C.zz_s = (uint32_t)__cvta_generic_to_shared(H.zz);
   {

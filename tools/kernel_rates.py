@@ -67,6 +67,11 @@ def main():
     ph = np.stack([dbg[:, 3 + i] - dbg[:, 2 + i] for i in range(5)], 1)
     out["entropy_phase_kcycles"] = {names[i]: [round(float(np.percentile(ph[:, i], q)) / 1e3, 1)
                                                for q in (10, 50, 90, 100)] for i in range(5)}
+    pn = ["load", "crc", "parse", "destuff", "tables"]
+    pp = np.stack([dbg[:, 12] - dbg[:, 0], dbg[:, 13] - dbg[:, 12], dbg[:, 14] - dbg[:, 13],
+                   dbg[:, 15] - dbg[:, 14], dbg[:, 1] - dbg[:, 15]], 1)
+    out["prep_phase_kcycles"] = {pn[i]: [round(float(np.percentile(pp[:, i], q)) / 1e3, 1)
+                                         for q in (10, 50, 90)] for i in range(5)}
     out["entropy_cta_kcycles"] = [round(float(np.percentile(dbg[:, 7] - dbg[:, 2], q)) / 1e3, 1)
                                   for q in (10, 50, 90, 100)]
     print(json.dumps(out), flush=True)
