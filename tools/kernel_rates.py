@@ -72,6 +72,8 @@ def main():
                    dbg[:, 15] - dbg[:, 14], dbg[:, 1] - dbg[:, 15]], 1)
     out["prep_phase_kcycles"] = {pn[i]: [round(float(np.percentile(pp[:, i], q)) / 1e3, 1)
                                          for q in (10, 50, 90)] for i in range(5)}
+    out["extended_images_frac"] = round(float(((dbg[:, 10] >> 32) > 0).mean()), 4)
+    out["fallback_images"] = int((dbg[:, 9] >> 32).sum())
     out["entropy_cta_kcycles"] = [round(float(np.percentile(dbg[:, 7] - dbg[:, 2], q)) / 1e3, 1)
                                   for q in (10, 50, 90, 100)]
     print(json.dumps(out), flush=True)
