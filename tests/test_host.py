@@ -187,6 +187,14 @@ def test_loader_config_validation(E):
         E.LoaderConfig.from_document({"batch_size": 4})
     c = E.LoaderConfig.from_document('{"data": "x", "scale": [0.2, 1.0], "out_dtype": "bfloat16"}')
     assert c.scale == (0.2, 1.0) and c.out_dtype == "bfloat16"
+    # GPU keys of the launch-set grouping and the host-staged fill
+    c = E.LoaderConfig.from_document({"data": "x", "group": 2, "fill_chain": 0})
+    assert (c.group, c.fill_chain) == (2, 0)
+    assert (E.LoaderConfig(data="x").group, E.LoaderConfig(data="x").fill_chain) == (1, 16)
+    with pytest.raises(E.ConfigError, match="group"):
+        E.LoaderConfig(data="x", group=0).validate()
+    with pytest.raises(E.ConfigError, match="fill_chain"):
+        E.LoaderConfig(data="x", fill_chain=-1).validate()
 
 
 def test_shard_partition(E):
