@@ -33,7 +33,7 @@ def test_native_exports_every_declared_symbol(native):
     assert b"sm_100a" in L.essl_version()
     # option defaults are readable without a device (the GPU tests restore them)
     assert native.option_default(native.ESSL_OPT_SEQ_BITS) == 3072
-    assert native.option_default(native.ESSL_OPT_WARMUP_BITS) == 2048
+    assert native.option_default(native.ESSL_OPT_WARMUP_BITS) == 2560
     assert native.option_default(native.ESSL_OPT_DECODE_MODE) == native.ESSL_DECODE_SPECULATIVE
 
 
