@@ -183,7 +183,18 @@ struct __align__(16) PrepSmem {
   uint16_t sub_pf[kMaxTables][kSubTabs];
   int stop, carry, dstop;
   long long t0;
+  // the (< 16) bytes before the scan that the in-place destuff overwrites
+  // (its output starts 16-byte aligned): the tail of the segment before SOS
+  // can be the last DHT, whose bytes the table code reads afterwards
+  int save_lo, save_hi;
+  uint8_t save[16];
 };
+
+// A marker-segment byte of the payload after the in-place destuff: the bytes
+// it overwrote come from the save area.
+__device__ __forceinline__ uint8_t seg_byte(const PrepSmem &S, const uint8_t *raw, int i) {
+  return (i >= S.save_lo && i < S.save_hi) ? S.save[i - S.save_lo] : raw[i];
+}
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -1831,6 +1842,13 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
   //      global clean region ---------------------------------------------------
   uint8_t *gclean = P.s.clean + H.clean_off;
   uint8_t *clean = SMEM ? dyn + (PS.scan_start & ~15) : gclean;
+  if (tid == 0) {
+    S.save_lo = SMEM && H.status == 0 && !H.multiscan ? (PS.scan_start & ~15) : 0;
+    S.save_hi = SMEM && H.status == 0 && !H.multiscan ? PS.scan_start : 0;
+  }
+  if (SMEM && tid < 16 && H.status == 0 && !H.multiscan && (PS.scan_start & ~15) + tid < PS.scan_start)
+    S.save[tid] = raw[(PS.scan_start & ~15) + tid];
+  __syncthreads();
   if (H.status == 0 && !H.multiscan) {
     // Rounds of kNT x 16 bytes: thread t owns bytes [16t, 16t+16) of the
     // round (16-byte shared loads, conflict-free); a block scan per round
@@ -1993,7 +2011,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       unsigned int st;
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(st) : "l"(&C.state) : "memory");
       bool eq = st == 2u && C.len == len && C.is_dc == s_tdc[t];
-      for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == raw[pos + i];
+      for (int i = tid; eq && i < len; i += kNT) eq = C.key[i] == seg_byte(S, raw, pos + i);
       const int hit = __syncthreads_and(eq);
       // a hit is used in place (slots are written once, never replaced)
       if (tid == 0) {
@@ -2012,7 +2030,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       T.lim[0] = 0; T.first[0] = 0; T.vptr[0] = 0;
       int nsub = 0, last = -1;
       for (int L = 1; L <= 16; L++) {
-        const int cnt = raw[pos + L - 1];
+        const int cnt = seg_byte(S, raw, pos + L - 1);
         T.first[L] = code;
         T.vptr[L] = (int16_t)vi;
         if (cnt && code + cnt > (1 << L)) { hdr_status(H, ESSL_ST_HUFFTABLE, R_HUFF_OVERFLOW, -1); break; }
@@ -2044,7 +2062,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
       if (s_hit[e >> 8]) continue;
       HuffTab &T = G->tab[e >> 8];
       const int v = e & 255;
-      T.vals[v] = v < T.nvals ? (uint8_t)raw[T.dht_pos + 16 + v] : 0;
+      T.vals[v] = v < T.nvals ? seg_byte(S, raw, T.dht_pos + 16 + v) : (uint8_t)0;
     }
     __syncthreads();
     for (int t = 0; t < ntab; t++) {
@@ -2107,7 +2125,7 @@ __global__ void __launch_bounds__(kNT, 4) k_prep(DecodeParams P) {
         TabCacheSlot &C = cache[t];
         const HuffTab &T = G->tab[t];
         const int len = 16 + T.nvals;
-        for (int i = tid; i < len; i += kNT) C.key[i] = raw[T.dht_pos + i];
+        for (int i = tid; i < len; i += kNT) C.key[i] = seg_byte(S, raw, T.dht_pos + i);
         const int4 *src = reinterpret_cast<const int4 *>(&T);
         int4 *dst = reinterpret_cast<int4 *>(&C.tab);
         for (int i = tid; i < (int)(sizeof(HuffTab) / 16); i += kNT) dst[i] = src[i];

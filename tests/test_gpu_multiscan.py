@@ -90,3 +90,25 @@ def test_loader_over_progressive_container(E, key):
                             "pixels": sha(b.pixels[s]),
                             "mask": b.mask[s].cpu().tolist() if b.mask is not None else None})
     assert got == [s for s in spec["samples"] if s["cfg"] == key]
+
+
+GCL = json.loads((GOLDEN / "golden_clobber.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(GCL["streams"]))
+def test_tables_read_before_the_inplace_destuff_clobbers_them(E, name):
+    """Baseline streams whose last DHT ends right before SOS, scan start at
+    15 mod 16: k_prep's in-place destuff overwrites the 15 bytes below the
+    scan start (the SOS header and, for one component, the DHT's last 5
+    symbols -- here frequent 8-bit codes).  The Huffman tables must come from
+    the original bytes: decode_full and crops equal the reference's
+    (tests/golden/make_golden_clobber.py); also decoded twice in one batch
+    (the second copy hits the context's table cache)."""
+    ent = GCL["streams"][name]
+    data = (GOLDEN / "streams_clobber" / f"{name}.jpg").read_bytes()
+    full, st = E.decode_full(data)
+    assert sha(full) == ent["full"]["sha"]
+    items = [(data, E.CropRect(*c["rect"])) for c in ent["crops"]] * 2
+    for (crop, cs), c in zip(E.decode_crops(items), ent["crops"] * 2):
+        assert sha(crop) == c["sha"], c["rect"]
+        assert [cs.mcus_entropy_decoded, cs.mcus_reconstructed, cs.fallback_full] == c["stats"]

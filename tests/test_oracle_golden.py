@@ -181,3 +181,20 @@ def test_loader_batch_threads_match(oracle):
                                             mask_ratio=0.75)
         assert (st == 0).all() and (st2 == 0).all()
         assert np.array_equal(a, b) and np.array_equal(ma, mb)
+
+
+GCL = __import__("json").loads((GOLDEN / "golden_clobber.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(GCL["streams"]))
+def test_clobber_window_streams(oracle, name):
+    """Reference-decoded streams whose last DHT sits in the 16 bytes below a
+    scan start at 15 mod 16 (tests/golden/make_golden_clobber.py)."""
+    ent = GCL["streams"][name]
+    data = (GOLDEN / "streams_clobber" / f"{name}.jpg").read_bytes()
+    full, st = oracle.decode_full(data)
+    assert sha(full) == ent["full"]["sha"]
+    assert list(st) == ent["full"]["stats"][:2]
+    for c in ent["crops"]:
+        crop, cs = oracle.decode_crop(data, tuple(c["rect"]))
+        assert sha(crop) == c["sha"], c["rect"]
