@@ -463,7 +463,8 @@ def run_gpu(args, wl):
     e2e_v = None
     h2d = d2h = 0
     if not args.no_e2e:
-        cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False, "staging": args.staging})
+        cfg2 = E.LoaderConfig(**{**cfg.__dict__, "resident": False, "staging": args.staging,
+                                 **({"fill_chain": args.fill_chain} if args.fill_chain >= 0 else {})})
         l2 = E.Loader(cfg2, container=handle, engine=loader.engine)
         apply_options(l2)
         if args.gather_ctas >= 0:
@@ -639,6 +640,8 @@ def main():
                     help="bracket every launch with CUDA events in the timed region (kernel_ms of all kernels)")
     ap.add_argument("--early-exit", type=int, default=-1,
                     help="ESSL_OPT_EARLY_EXIT (entropy decode stops near the crop's last row; -1: default)")
+    ap.add_argument("--fill-chain", type=int, default=-1,
+                    help="e2e: LoaderConfig.fill_chain (-1: the loader default)")
     ap.add_argument("--group", type=int, default=0,
                     help="consecutive batches decoded per launch set (LoaderConfig.group; "
                          "0: the workload's, 2 unless it sets one)")

@@ -160,8 +160,9 @@ class LoaderConfig:
     group: int = 1
     # host-staged containers: while the iterators fill the pipeline, each
     # batch's bus gather waits for the previous one and runs on this many
-    # CTAs (the oldest batch's payloads arrive first); 0: all concurrent
-    fill_chain: int = 16
+    # CTAs (the oldest batch's payloads arrive first); 0 (default since the
+    # gather's 4 KB stages): all concurrent
+    fill_chain: int = 0
 
     _KEYS = ("data", "batch_size", "workers", "seed", "res", "scale", "ratio", "aug",
              "mask_ratio", "patch", "keep_uint8") + _GPU_KEYS

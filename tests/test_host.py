@@ -190,7 +190,7 @@ def test_loader_config_validation(E):
     # GPU keys of the launch-set grouping and the host-staged fill
     c = E.LoaderConfig.from_document({"data": "x", "group": 2, "fill_chain": 0})
     assert (c.group, c.fill_chain) == (2, 0)
-    assert (E.LoaderConfig(data="x").group, E.LoaderConfig(data="x").fill_chain) == (1, 16)
+    assert (E.LoaderConfig(data="x").group, E.LoaderConfig(data="x").fill_chain) == (1, 0)
     with pytest.raises(E.ConfigError, match="group"):
         E.LoaderConfig(data="x", group=0).validate()
     with pytest.raises(E.ConfigError, match="fill_chain"):
